@@ -1,0 +1,203 @@
+/*
+ * libcamg — B200-native (sm_100a) saddle-point AMG solve path.
+ *
+ * C ABI: plain pointers and sizes only.  Vectors passed to the compute entry
+ * points are DEVICE pointers (fp64); `stream` is a cudaStream_t passed as
+ * void* (NULL = legacy default stream).  Every function returns a status code;
+ * camg_last_error() returns the message of the last failure on the calling
+ * thread.  Status codes map 1:1 onto the reference exception classes
+ * (pkg/src/contactamg/errors.py:4-25).
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/contactamg/).
+ */
+#ifndef CAMG_H
+#define CAMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CAMG_OK 0
+#define CAMG_ERR_DIMENSION 1 /* errors.py:8  DimensionError       */
+#define CAMG_ERR_SINGULAR 2  /* errors.py:12 SingularMatrixError  */
+#define CAMG_ERR_CONFIG 3    /* errors.py:20 ConfigError          */
+#define CAMG_ERR_SETUP 4     /* errors.py:24 SetupError           */
+#define CAMG_ERR_CUDA 5      /* CUDA runtime failure (no reference counterpart) */
+#define CAMG_ERR_NATIVE 6    /* other native failure */
+#define CAMG_ERR_ARG 7       /* invalid argument (ValueError) */
+
+/* block smoother kinds: smoothers.py:25 BLOCK_KINDS */
+#define CAMG_UZAWA 0
+#define CAMG_BRAESS_SARAZIN 1
+#define CAMG_SIMPLE 2
+#define CAMG_SIMPLEC 3
+/* point smoother kinds: smoothers.py:24 POINT_KINDS (jacobi, direct) plus
+ * GPU-only variants compared by convergence, never elementwise */
+#define CAMG_PT_JACOBI 0
+#define CAMG_PT_DIRECT 3
+#define CAMG_PT_CHEBYSHEV 4 /* GPU-only */
+#define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel */
+/* A_hat modes: smoothers.py:26 A_HAT_MODES */
+#define CAMG_AHAT_PLAIN 0
+#define CAMG_AHAT_ABS_ROWSUM 1
+/* coarse solvers: hierarchy.py:47 COARSE_SOLVERS */
+#define CAMG_COARSE_MERGED_LU 0
+#define CAMG_COARSE_BLOCK_SMOOTHER 1
+
+typedef struct camg_csr camg_csr;
+typedef struct camg_level camg_level;
+typedef struct camg_hierarchy camg_hierarchy;
+
+typedef struct {
+  int kind;           /* CAMG_UZAWA .. CAMG_SIMPLEC                 (BlockSmootherConfig.kind)   */
+  double alpha;       /*                                            (BlockSmootherConfig.alpha)  */
+  int outer_sweeps;   /*                                            (.outer_sweeps)              */
+  int a_hat_mode;     /* effective mode (smoothers.py:64-70)        (.a_hat_mode)                */
+  int pred_kind;      /* predictor PointSmootherConfig.kind                                      */
+  int pred_sweeps;
+  double pred_damping;
+  int corr_kind;      /* corrector PointSmootherConfig.kind                                      */
+  int corr_sweeps;
+  double corr_damping;
+} camg_smoother_cfg;
+
+/* ---- library ------------------------------------------------------------ */
+const char* camg_last_error(void);
+int camg_version(void);
+int camg_device_count(int* count);
+/* number of kernel launches issued by this library since load (evidence for
+ * the bench's gpu_launches field) */
+int64_t camg_launch_count(void);
+
+/* ---- matrices: replaces SparseMatrix (sparse.py:24-115) ------------------ */
+/* host arrays in, canonical CSR expected (sorted, no duplicates) */
+int camg_csr_from_host(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rowptr,
+                       const int64_t* col, const double* val, camg_csr** out);
+/* device arrays in (copied): rowptr int64, col int32 */
+int camg_csr_from_device(int64_t n_rows, int64_t n_cols, int64_t nnz, const int64_t* rowptr,
+                         const int32_t* col, const double* val, camg_csr** out);
+int camg_csr_destroy(camg_csr* A);
+int camg_csr_shape(const camg_csr* A, int64_t* n_rows, int64_t* n_cols, int64_t* nnz);
+int camg_csr_to_host(const camg_csr* A, int64_t* rowptr, int64_t* col, double* val);
+/* merged saddle operator [[K, B1], [B2, -Cz]] (saddle.py:58-67) */
+int camg_csr_saddle_merge(const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
+                          const camg_csr* Cz, camg_csr** out);
+
+/* ---- sparse kernels ------------------------------------------------------ */
+/* y = alpha*A*x + beta*y            spmv (sparse.py:149-154)                 */
+int camg_spmv(const camg_csr* A, double alpha, const double* x, double beta, double* y,
+              void* stream);
+/* R = A^T, canonical                 sp_transpose (sparse.py:157-158)        */
+int camg_transpose(const camg_csr* A, camg_csr** out);
+/* C = A*B, canonical, exact zeros dropped, accumulation order of scipy
+ *                                    sp_matmul (sparse.py:161-166)           */
+int camg_spgemm(const camg_csr* A, const camg_csr* B, camg_csr** out);
+/* C = (R*A)*P, canonical             galerkin_triple (sparse.py:169-173)     */
+int camg_galerkin(const camg_csr* R, const camg_csr* A, const camg_csr* P, camg_csr** out);
+/* d = diag(A) (mode 0) or abs row sums (mode 1), device output
+ *                                    extract_diagonal (sparse.py:176-188)    */
+int camg_diagonal(const camg_csr* A, int mode, double* d);
+/* C = alpha*A + beta*B (same shape), canonical, exact zeros dropped          */
+int camg_csr_axpby(double alpha, const camg_csr* A, double beta, const camg_csr* B,
+                   camg_csr** out);
+/* C = diag(s) * A  (scipy A.multiply(s[:,None])), s device                    */
+int camg_csr_scale_rows(const camg_csr* A, const double* s, camg_csr** out);
+
+/* ---- Galerkin setup (transfer.py) --------------------------------------- */
+/* one power step of estimate_lambda_max (transfer.py:148-161):
+ * w = (A v) / d  (device vectors)                                            */
+int camg_power_step(const camg_csr* A, const double* d, const double* v, double* w, void* stream);
+/* v = w / s */
+int camg_vec_scale_div(int64_t n, const double* w, double s, double* v, void* stream);
+/* P = P_tent - (omega/lam_max) * (diag(1/d) A) P_tent  (transfer.py:164-183) */
+int camg_smooth_prolongator(const camg_csr* P_tent, const camg_csr* A, const double* d,
+                            double omega_eff, camg_csr** out);
+/* S~ = scale*Cz + scale*(B2 diag(ainv) B1)  (smoothers.py:220-239) */
+int camg_schur(const camg_csr* B2, const camg_csr* Cz, const camg_csr* B1, const double* ainv,
+               double scale, camg_csr** out);
+
+/* ---- aggregation (host integer work, aggregation.py) --------------------- */
+/* node graph of K with cross-body and |v| <= eps*sqrt(|kii kjj|) entries
+ * dropped (aggregation.py:127-145, :47-63).  dof_node must be
+ * non-decreasing.  Output arrays are malloc'ed host arrays (free with
+ * camg_free_host).                                                           */
+int camg_node_graph(const camg_csr* K, const int64_t* dof_node, int64_t num_nodes,
+                    const int8_t* node_body, double eps_drop, int64_t** indptr,
+                    int64_t** indices);
+void camg_free_host(void* p);
+/* three-phase greedy aggregation (aggregation.py:186-258), host */
+int camg_aggregate_greedy(int64_t n, const int64_t* indptr, const int64_t* indices,
+                          int64_t min_size, int64_t* node_to_agg, int64_t* num_aggs,
+                          int64_t* roots, int64_t* singletons);
+/* Lagrange multiplier aggregation, paper Alg. 1 (aggregation.py:261-303), host.
+ * D given as host CSR.                                                        */
+int camg_aggregate_lagrange(const int64_t* disp_node_to_agg, int64_t n_rows,
+                            const int64_t* d_rowptr, const int64_t* d_col,
+                            const double* d_val, const int64_t* slave_dofs,
+                            const int64_t* row_node, const int64_t* lm_node_of_lm_dof,
+                            int64_t n_lm_dofs, int64_t* lam_node_to_agg, int64_t* num_aggs,
+                            int64_t* roots, int64_t* overlaps);
+
+/* ---- problem generator (device stiffness assembly from a stencil table) -- */
+/* table: [27 types][noff][dim][dim] fp64 host; one call per block           */
+int camg_assemble_stencil(int dim, const int64_t* grid, int clamp_lo, int clamp_hi,
+                          int64_t node_offset, int64_t n_rows_total, const double* table,
+                          camg_csr* K_inout, int64_t row_offset);
+int camg_stencil_block_counts(int dim, const int64_t* grid, int clamp_lo, int clamp_hi,
+                              const double* table, int64_t* nnz_out);
+/* Allocates an empty n_rows x n_cols matrix with nnz slots (filled by
+ * camg_assemble_stencil). */
+int camg_csr_alloc(int64_t n_rows, int64_t n_cols, int64_t nnz, camg_csr** out);
+
+/* ---- levels, smoothers, V-cycle (smoothers.py, hierarchy.py) ------------- */
+/* BlockSmoother(cfg, op) bound to one saddle operator (smoothers.py:253-281) */
+int camg_level_create(const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
+                      const camg_csr* Cz, const camg_smoother_cfg* cfg, int pre_sweeps,
+                      int post_sweeps, camg_level** out);
+int camg_level_destroy(camg_level* L);
+/* S~ of the bound smoother (copy) */
+int camg_level_schur(const camg_level* L, camg_csr** out);
+/* merged operator of the level (shared; do not destroy) */
+int camg_level_operator(const camg_level* L, const camg_csr** out);
+/* dense LU factors of S~ for a `direct` corrector: column-major n x n, 0-based
+ * LAPACK pivots (scipy.linalg.lu_factor)                                      */
+int camg_level_set_corrector_lu(camg_level* L, int64_t n, const double* lu_colmajor,
+                                const int32_t* piv);
+/* segregated transfer (transfer.py:186-188): R = P^T computed on device */
+int camg_level_set_transfer(camg_level* L, const camg_csr* P_u, const camg_csr* P_lam);
+/* BlockSmoother.sweep on merged vectors x, b -> out (smoothers.py:316-326) */
+int camg_level_sweep(camg_level* L, const double* x, const double* b, double* out, void* stream);
+
+/* Hierarchy (hierarchy.py:96-120).  Levels are borrowed (caller keeps them alive). */
+int camg_hierarchy_create(camg_level** levels, int num_levels, int coarse_solver,
+                          camg_hierarchy** out);
+/* merged dense LU of the coarsest operator (hierarchy.py:242-249) */
+int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu_colmajor,
+                                 const int32_t* piv);
+int camg_hierarchy_destroy(camg_hierarchy* H);
+/* one V-cycle from zero: z = M^-1 r  (Hierarchy.apply, hierarchy.py:115-120) */
+int camg_vcycle(camg_hierarchy* H, const double* r, double* z, void* stream);
+/* enable/disable CUDA-graph replay of the V-cycle (default on) */
+int camg_hierarchy_use_graph(camg_hierarchy* H, int enable);
+/* algorithmic bytes of one V-cycle (SURVEY.md §8(d) model) */
+int camg_hierarchy_vcycle_bytes(const camg_hierarchy* H, double* bytes_csr_model,
+                                double* bytes_format);
+
+/* ---- Krylov (krylov.py:45-129) -------------------------------------------- */
+/* right-preconditioned GMRES(restart), x0 = 0, CGS2 orthogonalisation.
+ * H may be NULL (no preconditioner).  history must hold max_iters+1 values.  */
+int camg_gmres(const camg_csr* A, camg_hierarchy* H, const double* b, double* x, double rel_tol,
+               int max_iters, int restart, int* iterations, double* history, int* converged,
+               void* stream);
+
+/* ---- dense vector helpers (device) ---------------------------------------- */
+int camg_dot(int64_t n, const double* x, const double* y, double* result, void* stream);
+int camg_axpy(int64_t n, double alpha, const double* x, double* y, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CAMG_H */

@@ -1,0 +1,264 @@
+// Node graph (device) and the integer aggregation (host).
+//
+// filtered_node_graph (aggregation.py:127-145 with NodeGraph.from_edges
+// :47-63): an edge p-q exists iff some DOF pair (i in p, j in q) has a kept
+// entry (|K_ij| > 0, or > eps*sqrt|K_ii K_jj|), p != q and both nodes are in
+// the same body; the graph is symmetrised and sorted.  On the device this is
+// the pattern of N^T F N + (N^T F N)^T with F the filtered 0/1 matrix and N
+// the DOF->node incidence (all values positive, so no cancellation).
+//
+// aggregate_greedy (aggregation.py:186-258) and aggregate_lagrange
+// (aggregation.py:261-303) are sequential integer sweeps; they run on the
+// host in C++ (aggregation stays host-side in v1) and are
+// bit-exact to the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <map>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace camg {
+
+Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s);
+
+template <bool FILL>
+__global__ void k_filter(CsrView K, const int64_t* __restrict__ dof_node, const int8_t* __restrict__ body,
+                         const double* __restrict__ diag, double eps, int64_t* __restrict__ cnt,
+                         const int64_t* __restrict__ rp, int32_t* __restrict__ col, double* __restrict__ val) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < K.n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ni = dof_node[r];
+    int64_t n = 0, o = FILL ? rp[r] : 0;
+    for (int64_t p = K.rowptr[r]; p < K.rowptr[r + 1]; ++p) {
+      const int32_t c = K.col[p];
+      const int64_t nj = dof_node[c];
+      if (ni == nj || body[ni] != body[nj]) continue;
+      const double v = fabs(K.val[p]);
+      const bool keep = eps > 0.0 ? v > eps * sqrt(diag[r] * diag[c]) : v > 0.0;
+      if (!keep) continue;
+      if (FILL) { col[o + n] = c; val[o + n] = 1.0; }
+      ++n;
+    }
+    if (!FILL) cnt[r] = n;
+  }
+}
+
+__global__ void k_incidence(const int64_t* __restrict__ dof_node, int64_t n, int64_t* __restrict__ rp,
+                            int32_t* __restrict__ col, double* __restrict__ val) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+    rp[i] = i;
+    if (i < n) { col[i] = (int32_t)dof_node[i]; val[i] = 1.0; }
+  }
+}
+
+__global__ void k_absdiag(double* d, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = fabs(d[i]);
+}
+
+void node_graph(const Csr* K, const int64_t* dof_node_h, int64_t num_nodes, const int8_t* body_h, double eps,
+                std::vector<int64_t>& indptr, std::vector<int64_t>& indices) {
+  cudaStream_t s = 0;
+  const int64_t n = K->n_rows;
+  DBuf<int64_t> dn(n + 1);
+  DBuf<int8_t> bd(num_nodes + 1);
+  CAMG_CUDA(cudaMemcpy(dn.p, dof_node_h, sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+  CAMG_CUDA(cudaMemcpy(bd.p, body_h, num_nodes, cudaMemcpyHostToDevice));
+  DBuf<double> diag(n + 1);
+  if (eps > 0.0) {
+    csr_diagonal(K, 0, diag.p, s);
+    note_launch();
+    k_absdiag<<<grid_for(n, 256), 256>>>(diag.p, n);
+  }
+  // F
+  DBuf<int64_t> cnt(n + 1);
+  note_launch();
+  k_filter<false><<<grid_for(n, 256), 256>>>(view(K), dn.p, bd.p, diag.p, eps, cnt.p, nullptr, nullptr, nullptr);
+  DBuf<int64_t> rp(n + 1);
+  exclusive_scan_i64(cnt.p, rp.p, n, s);
+  CAMG_CUDA(cudaDeviceSynchronize());
+  const int64_t nnz = read_i64(rp.p + n);
+  Csr F;
+  F.n_rows = n; F.n_cols = n; F.nnz = nnz;
+  F.rowptr = rp.release();
+  F.col = dalloc<int32_t>(nnz);
+  F.val = dalloc<double>(nnz);
+  F.avg_row = n ? double(nnz) / n : 0.0;
+  note_launch();
+  k_filter<true><<<grid_for(n, 256), 256>>>(view(K), dn.p, bd.p, diag.p, eps, nullptr, F.rowptr, F.col, F.val);
+  CAMG_LAUNCH_CHECK();
+  // N (n x num_nodes) and N^T
+  Csr N;
+  N.n_rows = n; N.n_cols = num_nodes; N.nnz = n;
+  N.rowptr = dalloc<int64_t>(n + 1);
+  N.col = dalloc<int32_t>(n);
+  N.val = dalloc<double>(n);
+  N.avg_row = 1.0;
+  note_launch();
+  k_incidence<<<grid_for(n + 1, 256), 256>>>(dn.p, n, N.rowptr, N.col, N.val);
+  CAMG_CUDA(cudaDeviceSynchronize());
+  std::unique_ptr<Csr> NT(csr_transpose(&N, s));
+  std::unique_ptr<Csr> G(galerkin(NT.get(), &F, &N, s));
+  std::unique_ptr<Csr> GT(csr_transpose(G.get(), s));
+  std::unique_ptr<Csr> S(csr_axpby(1.0, G.get(), 1.0, GT.get(), s));
+  indptr.resize(num_nodes + 1);
+  indices.resize(S->nnz);
+  CAMG_CUDA(cudaMemcpy(indptr.data(), S->rowptr, sizeof(int64_t) * (num_nodes + 1), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> c32(S->nnz);
+  if (S->nnz) CAMG_CUDA(cudaMemcpy(c32.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < S->nnz; ++i) indices[i] = c32[i];
+}
+
+// ---------------------------------------------------------------------------
+// host aggregation
+
+void greedy(int64_t n, const int64_t* ip, const int64_t* ix, int64_t min_size, int64_t* agg_out, int64_t* num_out,
+            int64_t* roots_out, int64_t* singles_out) {
+  const int64_t U = -1;
+  std::vector<int64_t> agg(n, U), roots;
+  // phase 1: root nodes whose neighbourhood is untouched
+  for (int64_t i = 0; i < n; ++i) {
+    if (agg[i] != U) continue;
+    bool free_nb = true;
+    for (int64_t p = ip[i]; p < ip[i + 1] && free_nb; ++p) free_nb = agg[ix[p]] == U;
+    if (!free_nb) continue;
+    const int64_t a = (int64_t)roots.size();
+    agg[i] = a;
+    for (int64_t p = ip[i]; p < ip[i + 1]; ++p) agg[ix[p]] = a;
+    roots.push_back(i);
+  }
+  // phase 2: leftovers join the most-connected neighbouring aggregate (lowest id on ties)
+  std::vector<int64_t> tally;
+  for (int64_t i = 0; i < n; ++i) {
+    if (agg[i] != U) continue;
+    int64_t best = U, best_cnt = 0;
+    tally.clear();
+    for (int64_t p = ip[i]; p < ip[i + 1]; ++p)
+      if (agg[ix[p]] != U) tally.push_back(agg[ix[p]]);
+    if (tally.empty()) {
+      agg[i] = (int64_t)roots.size();
+      roots.push_back(i);
+      continue;
+    }
+    std::sort(tally.begin(), tally.end());
+    for (size_t a = 0; a < tally.size();) {
+      size_t b = a;
+      while (b < tally.size() && tally[b] == tally[a]) ++b;
+      if ((int64_t)(b - a) > best_cnt) { best_cnt = (int64_t)(b - a); best = tally[a]; }
+      a = b;
+    }
+    agg[i] = best;
+  }
+  const int64_t na = (int64_t)roots.size();
+  std::vector<int64_t> size(na, 0);
+  for (int64_t i = 0; i < n; ++i) size[agg[i]]++;
+  // phase 3: merge undersized aggregates into their best-connected neighbour
+  if (min_size > 1) {
+    std::vector<std::vector<int64_t>> members(na);
+    for (int64_t i = 0; i < n; ++i) members[agg[i]].push_back(i);
+    std::map<int64_t, int64_t> conn;
+    for (int64_t a = 0; a < na; ++a) {
+      if (size[a] == 0 || size[a] >= min_size) continue;
+      conn.clear();
+      for (int64_t v : members[a])
+        for (int64_t p = ip[v]; p < ip[v + 1]; ++p) {
+          const int64_t t = agg[ix[p]];
+          if (t != a) conn[t]++;
+        }
+      if (conn.empty()) continue;
+      int64_t best = -1, bc = -1;
+      for (auto& kv : conn)
+        if (kv.second > bc) { bc = kv.second; best = kv.first; }  // ascending keys: first max = lowest id
+      for (int64_t v : members[a]) agg[v] = best;
+      members[best].insert(members[best].end(), members[a].begin(), members[a].end());
+      size[best] += size[a];
+      size[a] = 0;
+      members[a].clear();
+      members[a].shrink_to_fit();
+    }
+  }
+  std::vector<int64_t> remap(na, U);
+  int64_t m = 0;
+  for (int64_t a = 0; a < na; ++a)
+    if (size[a] > 0) { remap[a] = m; roots_out[m] = roots[a]; ++m; }
+  std::vector<int64_t> sz(m, 0);
+  for (int64_t i = 0; i < n; ++i) { agg_out[i] = remap[agg[i]]; sz[agg_out[i]]++; }
+  int64_t singles = 0;
+  for (int64_t a = 0; a < m; ++a) singles += sz[a] == 1;
+  *num_out = m;
+  *singles_out = singles;
+}
+
+}  // namespace camg
+
+using namespace camg;
+
+extern "C" {
+
+int camg_node_graph(const camg_csr* K, const int64_t* dof_node, int64_t num_nodes, const int8_t* node_body,
+                    double eps_drop, int64_t** indptr, int64_t** indices) {
+  return guarded([&] {
+    CAMG_CHECK(K->m->n_rows == K->m->n_cols, CAMG_ERR_DIMENSION, "K must be square");
+    for (int64_t i = 0; i < K->m->n_rows; ++i)
+      CAMG_CHECK(dof_node[i] >= 0 && dof_node[i] < num_nodes, CAMG_ERR_DIMENSION, "dof->node map out of range");
+    std::vector<int64_t> ip, ix;
+    node_graph(K->m, dof_node, num_nodes, node_body, eps_drop, ip, ix);
+    *indptr = (int64_t*)malloc(sizeof(int64_t) * ip.size());
+    *indices = (int64_t*)malloc(sizeof(int64_t) * std::max<size_t>(1, ix.size()));
+    std::copy(ip.begin(), ip.end(), *indptr);
+    std::copy(ix.begin(), ix.end(), *indices);
+  });
+}
+
+int camg_aggregate_greedy(int64_t n, const int64_t* indptr, const int64_t* indices, int64_t min_size,
+                          int64_t* node_to_agg, int64_t* num_aggs, int64_t* roots, int64_t* singletons) {
+  return guarded([&] {
+    CAMG_CHECK(min_size >= 1, CAMG_ERR_ARG, "min_agg_size must be >= 1");
+    greedy(n, indptr, indices, min_size, node_to_agg, num_aggs, roots, singletons);
+  });
+}
+
+int camg_aggregate_lagrange(const int64_t* disp, int64_t n_rows, const int64_t* drp, const int64_t* dcol,
+                            const double* dval, const int64_t* slave_dofs, const int64_t* row_node,
+                            const int64_t* lm_node_of_lm_dof, int64_t n_lm_dofs, int64_t* lam, int64_t* num_aggs,
+                            int64_t* roots, int64_t* overlaps) {
+  return guarded([&] {
+    int64_t n_lm = 0;
+    for (int64_t i = 0; i < n_lm_dofs; ++i) n_lm = std::max(n_lm, lm_node_of_lm_dof[i] + 1);
+    for (int64_t i = 0; i < n_lm; ++i) lam[i] = -1;
+    std::vector<int64_t> order(n_rows);
+    for (int64_t r = 0; r < n_rows; ++r) order[r] = r;
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) { return slave_dofs[a] < slave_dofs[b]; });
+    std::unordered_map<int64_t, int64_t> owner;
+    int64_t nroots = 0, ov = 0;
+    for (int64_t r : order) {
+      const int64_t k = disp[row_node[r]];
+      CAMG_CHECK(k >= 0, CAMG_ERR_SETUP, "slave DOF " + std::to_string(slave_dofs[r]) + ": node is unaggregated");
+      for (int64_t p = drp[r]; p < drp[r + 1]; ++p) {
+        if (dval[p] == 0.0) continue;
+        const int64_t pn = lm_node_of_lm_dof[dcol[p]];
+        auto it = owner.find(k);
+        if (lam[pn] == -1) {
+          int64_t tgt;
+          if (it == owner.end()) {
+            tgt = nroots;
+            owner[k] = tgt;
+            roots[nroots++] = pn;
+          } else {
+            tgt = it->second;
+          }
+          lam[pn] = tgt;
+        } else if (it == owner.end() || lam[pn] != it->second) {
+          ++ov;
+        }
+      }
+    }
+    *num_aggs = nroots;
+    *overlaps = ov;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,781 @@
+// Block smoothers, levels and the V-cycle on device.
+//
+// Replaces BlockSmoother (smoothers.py:245-329) with Jacobi / dense-direct
+// inner solves, Hierarchy.solve_coarsest / apply (hierarchy.py:96-120) and
+// vcycle (hierarchy.py:272-287).  All vectors are merged [u; lambda].
+//
+// One smoother step = one fused sweep over the top block row [K | B1] (the
+// residual, the first predictor sweep and the u update in one pass over K),
+// plus a few small kernels on the lambda side and on the interface rows of B1.
+#include <algorithm>
+#include <cmath>
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace camg {
+
+Csr* schur(const Csr* B2, const Csr* Cz, const Csr* B1, const double* ainv, double scale, cudaStream_t s);
+void recip(int64_t n, const double* d, double* out, cudaStream_t s);
+
+// ---------------------------------------------------------------------------
+// fused row kernels
+
+struct RowEpi {
+  const double* b;       // rhs (merged indexing)
+  const double* x;       // current iterate (merged indexing), null = zero
+  double* out_r;         // residual (optional)
+  const double* dscale;  // d = dscale[i] * r (optional)
+  double* out_d;         // (optional)
+  double* out_x;         // x_new[i] = x[i] + coef*d  (optional)
+  double coef;
+};
+
+// r_i = b_i - A_i x for rows [row0, row0+nrows), x split at `split` into
+// (xu, xl); optional jacobi-style epilogue.
+template <int G, bool ZERO, bool SPLIT>
+__global__ void __launch_bounds__(256) k_resid(CsrView A, int64_t row0, int64_t nrows, const double* __restrict__ xu,
+                                               const double* __restrict__ xl, int64_t split, RowEpi e) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t rr = tid / G; rr < nrows; rr += stride) {
+    const int64_t i = row0 + rr;
+    double acc = 0.0;
+    if (!ZERO) {
+      acc = row_dot<G, SPLIT>(A, i, xu, xl, split, lane);
+      acc = group_sum<G>(acc, mask);
+    }
+    if (lane == 0) {
+      const double r = e.b[i] - acc;
+      if (e.out_r) e.out_r[i] = r;
+      if (e.dscale) {
+        const double d = e.dscale[i] * r;
+        if (e.out_d) e.out_d[i] = d;
+        if (e.out_x) e.out_x[i] = (ZERO || !e.x) ? e.coef * d : e.x[i] + e.coef * d;
+      }
+    }
+  }
+}
+
+// extra Jacobi sweep on K (rows < nu): d_new = d + dinv*(r - K d); optional x update
+template <int G>
+__global__ void __launch_bounds__(256) k_jacobi(CsrView A, int64_t nu, const double* __restrict__ d,
+                                                const double* __restrict__ r, const double* __restrict__ dinv,
+                                                double* __restrict__ d_new, const double* __restrict__ x,
+                                                double* __restrict__ out_x, double coef) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t i = tid / G; i < nu; i += stride) {
+    double acc = row_dot<G, true>(A, i, d, nullptr, nu, lane);
+    acc = group_sum<G>(acc, mask);
+    if (lane == 0) {
+      const double dn = d[i] + dinv[i] * (r[i] - acc);
+      d_new[i] = dn;
+      if (out_x) out_x[i] = (x ? x[i] : 0.0) + coef * dn;
+    }
+  }
+}
+
+// lambda-side: rc_q = (A_bot [vu; vl])_q - c_q, q in [0, nl)
+template <int G>
+__global__ void __launch_bounds__(256) k_lam_rhs(CsrView A, int64_t nu, int64_t nl, const double* __restrict__ vu,
+                                                 const double* __restrict__ vl, const double* __restrict__ c,
+                                                 double* __restrict__ rc) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t q = tid / G; q < nl; q += stride) {
+    double acc = row_dot<G, true>(A, nu + q, vu, vl, nu, lane);
+    acc = group_sum<G>(acc, mask);
+    if (lane == 0) rc[q] = acc - c[q];
+  }
+}
+
+// corrector Jacobi sweep on S~ : first sweep from zero (dl = dinv*rc) or
+// dl_new = dl + dinv*(rc - S dl)
+template <int G, bool FIRST>
+__global__ void __launch_bounds__(256) k_corr_jacobi(CsrView S, const double* __restrict__ rc,
+                                                     const double* __restrict__ dinv, const double* __restrict__ dl,
+                                                     double* __restrict__ dl_new) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t q = tid / G; q < S.n_rows; q += stride) {
+    if (FIRST) {
+      if (lane == 0) dl_new[q] = dinv[q] * rc[q];
+    } else {
+      double acc = row_dot<G, false>(S, q, dl, nullptr, S.n_cols, lane);
+      acc = group_sum<G>(acc, mask);
+      if (lane == 0) dl_new[q] = dl[q] + dinv[q] * (rc[q] - acc);
+    }
+  }
+}
+
+// x_out_lam = x_lam + coef*dl
+__global__ void k_lam_update(int64_t nl, const double* __restrict__ xl, const double* __restrict__ dl, double coef,
+                             double* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nl; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = (xl ? xl[q] : 0.0) + coef * dl[q];
+}
+
+// x_u[i] -= mult * ainv[i] * (B1_i . dl) on the nonempty rows of B1
+__global__ void k_b1_correct(CsrView B1, const int64_t* __restrict__ rows, int64_t nrows,
+                             const double* __restrict__ ainv, const double* __restrict__ dl, double mult,
+                             double* __restrict__ xu) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 7;
+  const unsigned mask = group_mask<8>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / 8;
+  for (int64_t k = tid / 8; k < nrows; k += stride) {
+    const int64_t i = rows[k];
+    double acc = row_dot<8, false>(B1, i, dl, nullptr, B1.n_cols, lane);
+    acc = group_sum<8>(acc, mask);
+    if (lane == 0) xu[i] = xu[i] - mult * (ainv[i] * acc);
+  }
+}
+
+// small dense LU solve (LAPACK getrf factors, column-major, 0-based pivots)
+__global__ void __launch_bounds__(1024) k_lu_solve(int n, const double* __restrict__ LU, const int32_t* __restrict__ piv,
+                                                   const double* __restrict__ b, double* __restrict__ xg) {
+  extern __shared__ double xs[];
+  const bool sh = n <= 12288;
+  double* x = sh ? xs : xg;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) {
+      int p = piv[i];
+      if (p != i) { double t = x[i]; x[i] = x[p]; x[p] = t; }
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {  // unit lower
+    const double xj = x[j];
+    const double* colj = LU + (size_t)j * n;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) x[i] -= colj[i] * xj;
+    __syncthreads();
+  }
+  for (int j = n - 1; j >= 0; --j) {  // upper
+    if (threadIdx.x == 0) x[j] /= LU[(size_t)j * n + j];
+    __syncthreads();
+    const double xj = x[j];
+    const double* colj = LU + (size_t)j * n;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) x[i] -= colj[i] * xj;
+    __syncthreads();
+  }
+  if (sh)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) xg[i] = x[i];
+}
+
+__global__ void k_first_zero(int64_t n, const double* __restrict__ d, unsigned long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (d[i] == 0.0) atomicMin(out, (unsigned long long)i);
+}
+
+__global__ void k_scaled_recip(int64_t n, const double* __restrict__ d, double num, double mul, double* __restrict__ o) {
+  // o = num / (mul * d)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __ddiv_rn(num, __dmul_rn(mul, d[i]));
+}
+
+__global__ void k_nonempty_flags(const int64_t* __restrict__ rowptr, int64_t n, int32_t* __restrict__ f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    f[i] = rowptr[i + 1] > rowptr[i];
+}
+
+__global__ void k_copy(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    b[i] = a[i];
+}
+
+// ---------------------------------------------------------------------------
+// launch helpers with group-size dispatch
+
+template <template <int> class F, class... Args>
+void dispatch_g(double avg, Args&&... args) {
+  switch (group_for(avg)) {
+    case 1: F<1>::run(args...); break;
+    case 2: F<2>::run(args...); break;
+    case 4: F<4>::run(args...); break;
+    case 8: F<8>::run(args...); break;
+    case 16: F<16>::run(args...); break;
+    default: F<32>::run(args...); break;
+  }
+}
+
+template <int G>
+struct LaunchResid {
+  static void run(const Csr* A, int64_t row0, int64_t nrows, const double* xu, const double* xl, int64_t split,
+                  const RowEpi& e, bool zero, cudaStream_t s) {
+    if (nrows <= 0) return;
+    unsigned grid = grid_for(nrows * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    if (zero) k_resid<G, true, false><<<grid, 256, 0, s>>>(view(A), row0, nrows, xu, xl, split, e);
+    else if (split < A->n_cols) k_resid<G, false, true><<<grid, 256, 0, s>>>(view(A), row0, nrows, xu, xl, split, e);
+    else k_resid<G, false, false><<<grid, 256, 0, s>>>(view(A), row0, nrows, xu, xl, split, e);
+  }
+};
+
+template <int G>
+struct LaunchJacobi {
+  static void run(const Csr* A, int64_t nu, const double* d, const double* r, const double* dinv, double* dn,
+                  const double* x, double* ox, double coef, cudaStream_t s) {
+    unsigned grid = grid_for(nu * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    k_jacobi<G><<<grid, 256, 0, s>>>(view(A), nu, d, r, dinv, dn, x, ox, coef);
+  }
+};
+
+template <int G>
+struct LaunchLamRhs {
+  static void run(const Csr* A, int64_t nu, int64_t nl, const double* vu, const double* vl, const double* c,
+                  double* rc, cudaStream_t s) {
+    if (nl <= 0) return;
+    unsigned grid = grid_for(nl * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    k_lam_rhs<G><<<grid, 256, 0, s>>>(view(A), nu, nl, vu, vl, c, rc);
+  }
+};
+
+template <int G>
+struct LaunchCorr {
+  static void run(const Csr* S, const double* rc, const double* dinv, const double* dl, double* dn, bool first,
+                  cudaStream_t s) {
+    if (S->n_rows <= 0) return;
+    unsigned grid = grid_for(S->n_rows * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    if (first) k_corr_jacobi<G, true><<<grid, 256, 0, s>>>(view(S), rc, dinv, dl, dn);
+    else k_corr_jacobi<G, false><<<grid, 256, 0, s>>>(view(S), rc, dinv, dl, dn);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// level
+
+struct Level {
+  int64_t nu = 0, nl = 0, n = 0;
+  camg_smoother_cfg cfg{};
+  int pre = 1, post = 1;
+  Csr* A = nullptr;    // merged [[K,B1],[B2,-Cz]]
+  Csr* B1 = nullptr;   // copy (interface rows)
+  Csr* S = nullptr;    // S~
+  DBuf<int64_t> b1_rows;
+  int64_t n_b1_rows = 0;
+  DBuf<double> dinv_p, ainv, dinv_c;
+  // direct corrector
+  DBuf<double> corr_lu;
+  DBuf<int32_t> corr_piv;
+  // transfer (merged block-diagonal)
+  Csr* P = nullptr;
+  Csr* R = nullptr;
+  int64_t nc = 0;
+  int64_t nnz_top = 0;  // entries of the [K | B1] rows
+  // work vectors
+  DBuf<double> w_du, w_du2, w_ru, w_rc, w_dl, w_dl2, w_rl, w_tmp;
+  ~Level() { delete A; delete B1; delete S; delete P; delete R; }
+
+  void alloc_work() {
+    w_du = DBuf<double>(n);
+    w_du2 = DBuf<double>(n);
+    w_ru = DBuf<double>(nu + 1);
+    w_rc = DBuf<double>(nl + 1);
+    w_dl = DBuf<double>(nl + 1);
+    w_dl2 = DBuf<double>(nl + 1);
+    w_rl = DBuf<double>(nl + 1);
+    w_tmp = DBuf<double>(n);
+  }
+
+  // corrector: dl = C^-1 rc (jacobi sweeps from zero or dense LU)
+  double* corrector(const double* rc, cudaStream_t s) {
+    if (nl == 0) return w_dl.p;
+    if (cfg.corr_kind == CAMG_PT_DIRECT) {
+      CAMG_CHECK(corr_lu.p != nullptr, CAMG_ERR_SETUP, "direct corrector factors were not set");
+      note_launch();
+      size_t sh = nl <= 12288 ? sizeof(double) * nl : 0;
+      k_lu_solve<<<1, 1024, sh, s>>>((int)nl, corr_lu.p, corr_piv.p, rc, w_dl.p);
+      return w_dl.p;
+    }
+    double* cur = w_dl.p;
+    double* nxt = w_dl2.p;
+    dispatch_g<LaunchCorr>(S->avg_row, S, rc, dinv_c.p, nullptr, cur, true, s);
+    for (int k = 1; k < cfg.corr_sweeps; ++k) {
+      dispatch_g<LaunchCorr>(S->avg_row, S, rc, dinv_c.p, cur, nxt, false, s);
+      std::swap(cur, nxt);
+    }
+    return cur;
+  }
+
+  // one algorithmic smoother step: xo = step(x, b); x == nullptr means zero
+  void step(const double* x, const double* b, double* xo, cudaStream_t s) {
+    const bool zero = (x == nullptr);
+    const double* xu = x;
+    const double* xl = x ? x + nu : nullptr;
+    const int kind = cfg.kind;
+    const int sp = cfg.pred_sweeps;
+    const double alpha = cfg.alpha;
+    double* du = w_du.p;
+    if (kind == CAMG_BRAESS_SARAZIN) {
+      RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
+      dispatch_g<LaunchResid>(A->avg_row, A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+    } else {
+      const double coef = (kind == CAMG_UZAWA) ? alpha : 1.0;
+      RowEpi e{b, x, sp > 1 ? w_ru.p : nullptr, dinv_p.p, du, sp == 1 ? xo : nullptr, coef};
+      dispatch_g<LaunchResid>(A->avg_row, A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+      double* dn = w_du2.p;
+      for (int k = 1; k < sp; ++k) {
+        const bool last = (k == sp - 1);
+        dispatch_g<LaunchJacobi>(A->avg_row, A, nu, du, w_ru.p, dinv_p.p, dn, x, last ? xo : nullptr, coef, s);
+        std::swap(du, dn);
+      }
+    }
+    if (nl == 0) return;
+    // lambda side
+    if (kind == CAMG_UZAWA) {
+      // r_lam = b_lam - A_bot x
+      const double* rl = b + nu;
+      if (!zero) {
+        RowEpi e{b - 0, nullptr, w_rl.p - nu, nullptr, nullptr, nullptr, 0.0};
+        dispatch_g<LaunchResid>(A->avg_row, A, nu, nl, xu, xl, nu, e, false, s);
+        rl = w_rl.p;
+      }
+      dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, du, (const double*)nullptr, rl, w_rc.p, s);
+      double* dl = corrector(w_rc.p, s);
+      note_launch();
+      k_lam_update<<<grid_for(nl, 256), 256, 0, s>>>(nl, xl, dl, alpha, xo + nu);
+    } else {
+      dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, xo, xl, b + nu, w_rc.p, s);
+      double* dl = corrector(w_rc.p, s);
+      const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
+      note_launch();
+      k_lam_update<<<grid_for(nl, 256), 256, 0, s>>>(nl, xl, dl, cl, xo + nu);
+      if (n_b1_rows) {
+        const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
+        note_launch();
+        k_b1_correct<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
+      }
+    }
+  }
+
+  // BlockSmoother.sweep: outer steps from x (null = zero) into out; out != x
+  void sweep(const double* x, const double* b, double* out, cudaStream_t s) {
+    const int outer = cfg.outer_sweeps;
+    const double* cur = x;
+    for (int k = 0; k < outer; ++k) {
+      double* dst = ((outer - 1 - k) % 2 == 0) ? out : w_tmp.p;
+      step(cur, b, dst, s);
+      cur = dst;
+    }
+  }
+
+  // r = b - A x over all rows
+  void residual(const double* x, const double* b, double* r, cudaStream_t s) {
+    RowEpi e{b, nullptr, r, nullptr, nullptr, nullptr, 0.0};
+    dispatch_g<LaunchResid>(A->avg_row, A, int64_t(0), n, x, (const double*)nullptr, n, e, x == nullptr, s);
+  }
+};
+
+// ---------------------------------------------------------------------------
+
+static void check_no_zero(const double* d, int64_t n, const char* what) {
+  if (n <= 0) return;
+  DBuf<unsigned long long> first(1);
+  unsigned long long init = ~0ull;
+  CAMG_CUDA(cudaMemcpy(first.p, &init, sizeof(init), cudaMemcpyHostToDevice));
+  note_launch();
+  k_first_zero<<<grid_for(n, 256), 256>>>(n, d, first.p);
+  unsigned long long h = 0;
+  CAMG_CUDA(cudaMemcpy(&h, first.p, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h != ~0ull) throw Error(CAMG_ERR_SINGULAR, std::string(what) + ": zero diagonal in row " + std::to_string(h));
+}
+
+Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, const camg_smoother_cfg& cfg, int pre,
+                    int post) {
+  CAMG_CHECK(cfg.kind >= CAMG_UZAWA && cfg.kind <= CAMG_SIMPLEC, CAMG_ERR_CONFIG, "unknown block smoother kind");
+  CAMG_CHECK(cfg.alpha > 0.0, CAMG_ERR_CONFIG, "alpha must be positive");
+  CAMG_CHECK(cfg.outer_sweeps >= 1, CAMG_ERR_CONFIG, "outer_sweeps must be >= 1");
+  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI, CAMG_ERR_CONFIG,
+             "GPU predictor supports jacobi");
+  CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT, CAMG_ERR_CONFIG,
+             "GPU corrector supports jacobi and direct");
+  cudaStream_t s = 0;
+  std::unique_ptr<Level> L(new Level());
+  L->cfg = cfg;
+  L->pre = pre;
+  L->post = post;
+  L->nu = K->n_rows;
+  L->nl = Cz->n_rows;
+  L->n = L->nu + L->nl;
+  L->A = csr_saddle_merge(K, B1, B2, Cz, s);
+  L->B1 = csr_copy(B1, s);
+  L->nnz_top = read_i64(L->A->rowptr + L->nu);
+  const int64_t nu = L->nu, nl = L->nl;
+  // diagonals
+  DBuf<double> dK(nu + 1);
+  csr_diagonal(K, 0, dK.p, s);
+  const int mode = (cfg.kind == CAMG_SIMPLEC) ? CAMG_AHAT_ABS_ROWSUM
+                   : (cfg.kind == CAMG_BRAESS_SARAZIN) ? CAMG_AHAT_PLAIN
+                                                       : cfg.a_hat_mode;
+  DBuf<double> ahat(nu + 1);
+  if (mode == CAMG_AHAT_ABS_ROWSUM) {
+    csr_diagonal(K, 1, ahat.p, s);
+    CAMG_CUDA(cudaDeviceSynchronize());
+    check_no_zero(ahat.p, nu, "abs_rowsum lumping");
+  } else {
+    CAMG_CUDA(cudaMemcpy(ahat.p, dK.p, sizeof(double) * nu, cudaMemcpyDeviceToDevice));
+    check_no_zero(ahat.p, nu, "a_hat");
+  }
+  L->ainv = DBuf<double>(nu + 1);
+  note_launch();
+  k_scaled_recip<<<grid_for(nu, 256), 256>>>(nu, ahat.p, 1.0, 1.0, L->ainv.p);
+  if (cfg.kind != CAMG_BRAESS_SARAZIN) {
+    check_no_zero(dK.p, nu, "jacobi");
+    L->dinv_p = DBuf<double>(nu + 1);
+    note_launch();
+    k_scaled_recip<<<grid_for(nu, 256), 256>>>(nu, dK.p, cfg.pred_damping, 1.0, L->dinv_p.p);
+  }
+  // Schur approximation (smoothers.py:255-267)
+  {
+    DBuf<double> ainv_s(nu + 1);
+    double scale = 1.0;
+    if (cfg.kind == CAMG_BRAESS_SARAZIN) {
+      note_launch();
+      k_scaled_recip<<<grid_for(nu, 256), 256>>>(nu, ahat.p, 1.0, cfg.alpha, ainv_s.p);
+    } else {
+      CAMG_CUDA(cudaMemcpy(ainv_s.p, L->ainv.p, sizeof(double) * nu, cudaMemcpyDeviceToDevice));
+      if (cfg.kind == CAMG_SIMPLE || cfg.kind == CAMG_SIMPLEC) scale = cfg.alpha;
+    }
+    L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
+  }
+  if (cfg.corr_kind == CAMG_PT_JACOBI && nl > 0) {
+    DBuf<double> dS(nl + 1);
+    csr_diagonal(L->S, 0, dS.p, s);
+    CAMG_CUDA(cudaDeviceSynchronize());
+    check_no_zero(dS.p, nl, "jacobi");
+    L->dinv_c = DBuf<double>(nl + 1);
+    note_launch();
+    k_scaled_recip<<<grid_for(nl, 256), 256>>>(nl, dS.p, cfg.corr_damping, 1.0, L->dinv_c.p);
+  }
+  // nonempty rows of B1
+  {
+    DBuf<int32_t> flags(nu + 1);
+    note_launch();
+    k_nonempty_flags<<<grid_for(nu, 256), 256>>>(L->B1->rowptr, nu, flags.p);
+    DBuf<int64_t> idx(nu + 1), out(nu + 1), nsel(1);
+    note_launch();
+    auto it = cub::CountingInputIterator<int64_t>(0);
+    size_t tmp = 0;
+    CAMG_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, it, flags.p, out.p, nsel.p, nu));
+    DBuf<char> t(tmp);
+    CAMG_CUDA(cub::DeviceSelect::Flagged(t.p, tmp, it, flags.p, out.p, nsel.p, nu));
+    L->n_b1_rows = read_i64(nsel.p);
+    L->b1_rows = std::move(out);
+  }
+  L->alloc_work();
+  CAMG_CUDA(cudaDeviceSynchronize());
+  return L.release();
+}
+
+void shift_copy(const int64_t* rp, int64_t n, int64_t add, int64_t* out, const int32_t* col, int64_t nnz, int32_t cadd,
+                int32_t* cout, cudaStream_t s);
+
+Csr* block_diag(const Csr* Pu, const Csr* Pl, cudaStream_t s) {
+  // [[Pu, 0], [0, Pl]]: reuse the saddle merge with empty off-diagonal blocks
+  // is not possible (square check); do it directly.
+  const int64_t nu = Pu->n_rows, nl = Pl->n_rows, cu = Pu->n_cols, cl = Pl->n_cols;
+  Csr* C = csr_alloc(nu + nl, cu + cl, Pu->nnz + Pl->nnz);
+  CAMG_CUDA(cudaMemcpyAsync(C->rowptr, Pu->rowptr, sizeof(int64_t) * (nu + 1), cudaMemcpyDeviceToDevice, s));
+  CAMG_CUDA(cudaMemcpyAsync(C->col, Pu->col, sizeof(int32_t) * Pu->nnz, cudaMemcpyDeviceToDevice, s));
+  CAMG_CUDA(cudaMemcpyAsync(C->val, Pu->val, sizeof(double) * Pu->nnz, cudaMemcpyDeviceToDevice, s));
+  CAMG_CUDA(cudaMemcpyAsync(C->val + Pu->nnz, Pl->val, sizeof(double) * Pl->nnz, cudaMemcpyDeviceToDevice, s));
+  shift_copy(Pl->rowptr + 1, nl, Pu->nnz, C->rowptr + nu + 1, Pl->col, Pl->nnz, (int32_t)cu, C->col + Pu->nnz, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  return C;
+}
+
+__global__ void k_shift_copy(const int64_t* __restrict__ rp, int64_t n, int64_t add, int64_t* __restrict__ out,
+                             const int32_t* __restrict__ col, int64_t nnz, int32_t cadd, int32_t* __restrict__ cout) {
+  const int64_t m = n > nnz ? n : nnz;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n) out[i] = rp[i] + add;
+    if (i < nnz) cout[i] = col[i] + cadd;
+  }
+}
+
+void shift_copy(const int64_t* rp, int64_t n, int64_t add, int64_t* out, const int32_t* col, int64_t nnz, int32_t cadd,
+                int32_t* cout, cudaStream_t s) {
+  note_launch();
+  k_shift_copy<<<grid_for(std::max(n, nnz), 256), 256, 0, s>>>(rp, n, add, out, col, nnz, cadd, cout);
+  CAMG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------------------
+// hierarchy
+
+struct Hierarchy {
+  std::vector<Level*> levels;
+  int coarse_solver = CAMG_COARSE_MERGED_LU;
+  DBuf<double> lu;
+  DBuf<int32_t> piv;
+  int64_t n_coarse = 0;
+  // per-level vectors: b (rhs), x[2]
+  std::vector<DBuf<double>> vb, vx0, vx1, vr;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  bool use_graph = true;
+  DBuf<double> in, out;  // level-0 rhs / result buffers used by the graph
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ~Hierarchy() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (stream) cudaStreamDestroy(stream);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+
+  void coarse_solve(const double* b, double* x, cudaStream_t s) {
+    Level* L = levels.back();
+    if (coarse_solver == CAMG_COARSE_MERGED_LU) {
+      CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "coarse LU factors were not set");
+      note_launch();
+      size_t sh = n_coarse <= 12288 ? sizeof(double) * n_coarse : 0;
+      k_lu_solve<<<1, 1024, sh, s>>>((int)n_coarse, lu.p, piv.p, b, x);
+    } else {
+      L->sweep(nullptr, b, x, s);
+    }
+  }
+
+  // V-cycle at level l from zero with rhs b; result in x (returns pointer)
+  double* vcycle(int l, const double* b, cudaStream_t s) {
+    Level* L = levels[l];
+    double* X[2] = {vx0[l].p, vx1[l].p};
+    int cur = 0;
+    if (l == (int)levels.size() - 1) {
+      coarse_solve(b, X[0], s);
+      return X[0];
+    }
+    const double* x = nullptr;  // zero
+    for (int k = 0; k < L->pre; ++k) {
+      double* dst = X[cur];
+      L->sweep(x, b, dst, s);
+      x = dst;
+      cur ^= 1;
+    }
+    L->residual(x, b, vr[l].p, s);
+    spmv(L->R, 1.0, vr[l].p, 0.0, vb[l + 1].p, s);
+    const double* xc = vcycle(l + 1, vb[l + 1].p, s);
+    double* xx;
+    if (x == nullptr) {  // no pre-smoothing: x = P xc
+      xx = X[cur];
+      spmv(L->P, 1.0, xc, 0.0, xx, s);
+      cur ^= 1;
+    } else {
+      xx = const_cast<double*>(x);
+      spmv(L->P, 1.0, xc, 1.0, xx, s);
+    }
+    const double* xs = xx;
+    for (int k = 0; k < L->post; ++k) {
+      double* dst = (xs == X[0]) ? X[1] : X[0];
+      L->sweep(xs, b, dst, s);
+      xs = dst;
+    }
+    return const_cast<double*>(xs);
+  }
+
+  void run(const double* r, double* z, cudaStream_t s) {
+    const int64_t n = levels[0]->n;
+    double* res = vcycle(0, r, s);
+    CAMG_CUDA(cudaMemcpyAsync(z, res, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+
+  void apply(const double* r, double* z, cudaStream_t caller) {
+    const int64_t n = levels[0]->n;
+    if (!use_graph) {
+      run(r, z, caller);
+      CAMG_LAUNCH_CHECK();
+      return;
+    }
+    if (!stream) {
+      CAMG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+      CAMG_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+      CAMG_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
+      in = DBuf<double>(n);
+      out = DBuf<double>(n);
+    }
+    if (!graph) {
+      cudaGraph_t g;
+      CAMG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      run(in.p, out.p, stream);
+      CAMG_CUDA(cudaStreamEndCapture(stream, &g));
+      CAMG_CUDA(cudaGraphInstantiate(&graph, g, 0));
+      cudaGraphDestroy(g);
+    }
+    CAMG_CUDA(cudaMemcpyAsync(in.p, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
+    CAMG_CUDA(cudaEventRecord(ev0, caller));
+    CAMG_CUDA(cudaStreamWaitEvent(stream, ev0, 0));
+    note_launch();
+    CAMG_CUDA(cudaGraphLaunch(graph, stream));
+    CAMG_CUDA(cudaEventRecord(ev1, stream));
+    CAMG_CUDA(cudaStreamWaitEvent(caller, ev1, 0));
+    CAMG_CUDA(cudaMemcpyAsync(z, out.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
+  }
+};
+
+Hierarchy* hierarchy_create(Level** lv, int nlev, int coarse_solver) {
+  CAMG_CHECK(nlev >= 1, CAMG_ERR_ARG, "need at least one level");
+  std::unique_ptr<Hierarchy> H(new Hierarchy());
+  H->levels.assign(lv, lv + nlev);
+  H->coarse_solver = coarse_solver;
+  for (int l = 0; l < nlev; ++l) {
+    Level* L = H->levels[l];
+    if (l < nlev - 1) {
+      CAMG_CHECK(L->P != nullptr, CAMG_ERR_SETUP, "level transfer was not set");
+      CAMG_CHECK(L->P->n_cols == H->levels[l + 1]->n, CAMG_ERR_DIMENSION, "transfer does not match the next level");
+    }
+    H->vb.emplace_back(L->n + 1);
+    H->vx0.emplace_back(L->n + 1);
+    H->vx1.emplace_back(L->n + 1);
+    H->vr.emplace_back(L->n + 1);
+  }
+  return H.release();
+}
+
+void hierarchy_apply(Hierarchy* H, const double* r, double* z, cudaStream_t s) { H->apply(r, z, s); }
+
+}  // namespace camg
+
+using namespace camg;
+
+
+extern "C" {
+
+int camg_level_create(const camg_csr* K, const camg_csr* B1, const camg_csr* B2, const camg_csr* Cz,
+                      const camg_smoother_cfg* cfg, int pre_sweeps, int post_sweeps, camg_level** out) {
+  return guarded([&] { *out = new camg_level{level_create(K->m, B1->m, B2->m, Cz->m, *cfg, pre_sweeps, post_sweeps)}; });
+}
+
+int camg_level_destroy(camg_level* L) {
+  return guarded([&] {
+    if (L) { delete L->L; delete L; }
+  });
+}
+
+int camg_level_schur(const camg_level* L, camg_csr** out) {
+  return guarded([&] { *out = new camg_csr{csr_copy(L->L->S, 0)}; });
+}
+
+int camg_level_operator(const camg_level* L, const camg_csr** out) {
+  return guarded([&] {
+    static thread_local camg_csr view_handle;
+    view_handle.m = L->L->A;
+    *out = &view_handle;
+  });
+}
+
+int camg_level_set_corrector_lu(camg_level* L, int64_t n, const double* lu, const int32_t* piv) {
+  return guarded([&] {
+    CAMG_CHECK(n == L->L->nl, CAMG_ERR_DIMENSION, "corrector LU size does not match n_lam");
+    L->L->corr_lu = DBuf<double>(n * n + 1);
+    L->L->corr_piv = DBuf<int32_t>(n + 1);
+    CAMG_CUDA(cudaMemcpy(L->L->corr_lu.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(L->L->corr_piv.p, piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  });
+}
+
+int camg_level_set_transfer(camg_level* L, const camg_csr* P_u, const camg_csr* P_lam) {
+  return guarded([&] {
+    Level* lv = L->L;
+    CAMG_CHECK(P_u->m->n_rows == lv->nu && P_lam->m->n_rows == lv->nl, CAMG_ERR_DIMENSION,
+               "transfer dimensions do not match the operator");
+    delete lv->P;
+    delete lv->R;
+    lv->P = block_diag(P_u->m, P_lam->m, 0);
+    lv->R = csr_transpose(lv->P, 0);
+    lv->nc = lv->P->n_cols;
+  });
+}
+
+int camg_level_sweep(camg_level* L, const double* x, const double* b, double* out, void* stream) {
+  return guarded([&] {
+    L->L->sweep(x, b, out, (cudaStream_t)stream);
+    CAMG_LAUNCH_CHECK();
+  });
+}
+
+int camg_hierarchy_create(camg_level** levels, int num_levels, int coarse_solver, camg_hierarchy** out) {
+  return guarded([&] {
+    std::vector<Level*> lv(num_levels);
+    for (int i = 0; i < num_levels; ++i) lv[i] = levels[i]->L;
+    *out = new camg_hierarchy{hierarchy_create(lv.data(), num_levels, coarse_solver)};
+  });
+}
+
+int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu, const int32_t* piv) {
+  return guarded([&] {
+    CAMG_CHECK(n == H->H->levels.back()->n, CAMG_ERR_DIMENSION, "coarse LU size mismatch");
+    CAMG_CHECK(n < (1 << 30), CAMG_ERR_DIMENSION, "coarse LU too large");
+    H->H->n_coarse = n;
+    H->H->lu = DBuf<double>(n * n + 1);
+    H->H->piv = DBuf<int32_t>(n + 1);
+    CAMG_CUDA(cudaMemcpy(H->H->lu.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(H->H->piv.p, piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  });
+}
+
+int camg_hierarchy_destroy(camg_hierarchy* H) {
+  return guarded([&] {
+    if (H) { delete H->H; delete H; }
+  });
+}
+
+int camg_vcycle(camg_hierarchy* H, const double* r, double* z, void* stream) {
+  return guarded([&] { H->H->apply(r, z, (cudaStream_t)stream); });
+}
+
+int camg_hierarchy_use_graph(camg_hierarchy* H, int enable) {
+  return guarded([&] { H->H->use_graph = enable != 0; });
+}
+
+int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, double* bytes_fmt) {
+  return guarded([&] {
+    // 12 B/nnz + 4(m+1) + 8 n + 8 m per sparse application,
+    // zero-vector products skipped, fused epilogue vectors counted.
+    const Hierarchy* H = Hh->H;
+    double total = 0.0;
+    auto spm = [](const Csr* A, int64_t rows, double nnz) {
+      return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * A->n_cols + 8.0 * rows;
+    };
+    const int nl = (int)H->levels.size();
+    for (int l = 0; l < nl; ++l) {
+      const Level* L = H->levels[l];
+      const double nnzA = (double)L->A->nnz;
+      const double top = (double)L->nnz_top;
+      const camg_smoother_cfg& c = L->cfg;
+      const int sp = (c.kind == CAMG_BRAESS_SARAZIN) ? 1 : c.pred_sweeps;
+      const double step_top = spm(L->A, L->nu, top) + 8.0 * 3 * L->nu;  // b, dinv, x_out
+      const double step_extra = (sp - 1) * (spm(L->A, L->nu, top) + 8.0 * 4 * L->nu);
+      const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * std::max(0, c.corr_sweeps - 1);
+      const double step = step_top + step_extra + lam;
+      const double step0 = step - 12.0 * top;  // zero start skips K x
+      int nsteps_pre = L->pre * c.outer_sweeps, nsteps_post = L->post * c.outer_sweeps;
+      if (l == nl - 1) {
+        if (H->coarse_solver == CAMG_COARSE_MERGED_LU) total += 8.0 * H->n_coarse * H->n_coarse + 16.0 * H->n_coarse;
+        else total += step0 + (c.outer_sweeps - 1) * step;
+        continue;
+      }
+      total += (nsteps_pre > 0 ? step0 + (nsteps_pre - 1) * step : 0.0) + nsteps_post * step;
+      total += spm(L->A, L->n, nnzA) + 8.0 * L->n;          // residual (+ b read)
+      total += spm(L->R, L->R->n_rows, (double)L->R->nnz);    // restriction
+      total += spm(L->P, L->P->n_rows, (double)L->P->nnz) + 8.0 * L->n;  // prolong-add
+    }
+    *bytes_csr = total;
+    *bytes_fmt = total;
+  });
+}
+
+}  // extern "C"

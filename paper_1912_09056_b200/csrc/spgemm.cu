@@ -1,0 +1,578 @@
+// Two-pass (count, then fill) row-wise SpGEMM and the fused Galerkin triple
+// product, reproducing scipy's csr_matmat accumulation order so that the
+// exact-zero cancellations -- and therefore the coarse sparsity patterns the
+// host aggregation reads -- are bit-identical to the reference
+// (sparse.py:161-173, transfer.py:164-199, smoothers.py:220-239).
+//
+// scipy csr_matmat, row i:  sums[k] = 0 + v_1*b_1k + v_2*b_2k + ...  in the
+// order of A's stored row; output order = reverse first touch; exact zeros
+// dropped.  `(R@A)@P` therefore accumulates each coarse entry over the RA row
+// in reverse-first-touch order.  The fused kernel recovers that order without
+// materialising or sorting RA: RA column t belongs to "touch group" q (the
+// position in R's row of the first A row containing t); walking q downwards
+// and each A row backwards, and keeping only t whose group is q, enumerates
+// exactly scipy's RA row order.
+//
+// One warp per output row; per-warp hash tables live in shared memory, rows
+// that overflow them are recomputed with hash tables in global scratch.
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace camg {
+
+namespace {
+
+constexpr int32_t kEmpty = -1;
+constexpr int kWarpsPerBlock = 4;
+
+__device__ __forceinline__ uint32_t hslot(int32_t k, uint32_t mask) {
+  return ((uint32_t)k * 2654435761u) & mask;
+}
+
+// Hash table view (shared or global memory).
+struct Hash {
+  int32_t* keys;
+  int32_t* ft;  // first-touch group (may be null)
+  double* vals;
+  uint32_t cap;  // power of two
+};
+
+// Accumulate (k, prod) for one lane; returns 1 if a new key was inserted.
+__device__ __forceinline__ int hash_add(Hash h, int32_t k, double prod, int32_t group) {
+  const uint32_t mask = h.cap - 1;
+  uint32_t s = hslot(k, mask);
+  while (true) {
+    int32_t cur = atomicCAS(&h.keys[s], kEmpty, k);
+    if (cur == kEmpty) {
+      h.vals[s] = __dadd_rn(0.0, prod);
+      if (h.ft) h.ft[s] = group;
+      return 1;
+    }
+    if (cur == k) {
+      h.vals[s] = __dadd_rn(h.vals[s], prod);
+      return 0;
+    }
+    s = (s + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ int hash_find(const Hash& h, int32_t k) {
+  const uint32_t mask = h.cap - 1;
+  uint32_t s = hslot(k, mask);
+  while (true) {
+    int32_t cur = h.keys[s];
+    if (cur == k) return (int)s;
+    if (cur == kEmpty) return -1;
+    s = (s + 1) & mask;
+  }
+}
+
+__device__ __forceinline__ void hash_clear(Hash h, int lane) {
+  for (uint32_t s = lane; s < h.cap; s += 32) h.keys[s] = kEmpty;
+  __syncwarp();
+}
+
+// Compact entries with |v| >= tol (tol = 0 -> v != 0) to the front of the
+// table arrays, bitonic-sort them by key, return the count.
+__device__ int compact_sort(Hash h, int lane, double tol) {
+  int n = 0;
+  for (uint32_t base = 0; base < h.cap; base += 32) {
+    const uint32_t s = base + lane;
+    int32_t k = h.keys[s];
+    double v = h.vals[s];
+    bool keep = (k != kEmpty) && (tol > 0.0 ? fabs(v) >= tol : v != 0.0);
+    unsigned b = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {
+      int pos = n + __popc(b & ((1u << lane) - 1u));
+      h.keys[pos] = k;
+      h.vals[pos] = v;
+    }
+    n += __popc(b);
+    __syncwarp();
+  }
+  int N = 1;
+  while (N < n) N <<= 1;
+  for (int s = n + lane; s < N; s += 32) h.keys[s] = INT32_MAX;
+  __syncwarp();
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < N; i += 32) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          int32_t a = h.keys[i], b = h.keys[ixj];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            h.keys[i] = b;
+            h.keys[ixj] = a;
+            double t = h.vals[i];
+            h.vals[i] = h.vals[ixj];
+            h.vals[ixj] = t;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  return n;
+}
+
+__device__ int count_kept(const Hash& h, int lane, double tol) {
+  int n = 0;
+  for (uint32_t s = lane; s < h.cap; s += 32) {
+    int32_t k = h.keys[s];
+    if (k != kEmpty && (tol > 0.0 ? fabs(h.vals[s]) >= tol : h.vals[s] != 0.0)) ++n;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// C = A*B for one row: returns false on overflow
+
+__device__ bool row_product(const CsrView& A, const CsrView& B, int64_t row, bool reverse_a, Hash h,
+                            int lane, uint32_t limit) {
+  hash_clear(h, lane);
+  const int64_t s = A.rowptr[row], e = A.rowptr[row + 1];
+  uint32_t count = 0;
+  for (int64_t q = 0; q < e - s; ++q) {
+    const int64_t jj = reverse_a ? (e - 1 - q) : (s + q);
+    const int32_t j = A.col[jj];
+    const double v = A.val[jj];
+    const int64_t bs = B.rowptr[j], be = B.rowptr[j + 1];
+    for (int64_t base = bs; base < be; base += 32) {
+      if (count + 32 > limit) return false;
+      int ins = 0;
+      const int64_t kk = base + lane;
+      if (kk < be) ins = hash_add(h, B.col[kk], __dmul_rn(v, B.val[kk]), 0);
+      count += __popc(__ballot_sync(0xffffffffu, ins));
+      __syncwarp();
+    }
+  }
+  return true;
+}
+
+// (R*A)*P for one row: hash1 holds RA with first-touch groups, hash2 the result
+__device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P, int64_t row, Hash h1,
+                           Hash h2, int lane, uint32_t limit1, uint32_t limit2) {
+  hash_clear(h1, lane);
+  hash_clear(h2, lane);
+  const int64_t rs = R.rowptr[row], re = R.rowptr[row + 1];
+  uint32_t c1 = 0, c2 = 0;
+  for (int64_t q = 0; q < re - rs; ++q) {
+    const int32_t j = R.col[rs + q];
+    const double v = R.val[rs + q];
+    const int64_t as = A.rowptr[j], ae = A.rowptr[j + 1];
+    for (int64_t base = as; base < ae; base += 32) {
+      if (c1 + 32 > limit1) return false;
+      int ins = 0;
+      const int64_t kk = base + lane;
+      if (kk < ae) ins = hash_add(h1, A.col[kk], __dmul_rn(v, A.val[kk]), (int32_t)q);
+      c1 += __popc(__ballot_sync(0xffffffffu, ins));
+      __syncwarp();
+    }
+  }
+  // walk RA in scipy's stored order: groups descending, columns descending
+  for (int64_t q = re - rs - 1; q >= 0; --q) {
+    const int32_t j = R.col[rs + q];
+    const int64_t as = A.rowptr[j], ae = A.rowptr[j + 1];
+    for (int64_t top = ae - 1; top >= as; top -= 32) {
+      const int64_t kk = top - lane;
+      int32_t t = -1;
+      double rav = 0.0;
+      bool member = false;
+      if (kk >= as) {
+        t = A.col[kk];
+        int sl = hash_find(h1, t);
+        if (sl >= 0 && h1.ft[sl] == (int32_t)q) {
+          rav = h1.vals[sl];
+          member = rav != 0.0;  // csr_matmat drops exact zeros of RA
+        }
+      }
+      unsigned b = __ballot_sync(0xffffffffu, member);
+      while (b) {
+        const int src = __ffs(b) - 1;
+        b &= b - 1;
+        const int32_t tt = __shfl_sync(0xffffffffu, t, src);
+        const double vv = __shfl_sync(0xffffffffu, rav, src);
+        const int64_t ps = P.rowptr[tt], pe = P.rowptr[tt + 1];
+        for (int64_t base = ps; base < pe; base += 32) {
+          if (c2 + 32 > limit2) return false;
+          int ins = 0;
+          const int64_t pp = base + lane;
+          if (pp < pe) ins = hash_add(h2, P.col[pp], __dmul_rn(vv, P.val[pp]), 0);
+          c2 += __popc(__ballot_sync(0xffffffffu, ins));
+          __syncwarp();
+        }
+      }
+    }
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// kernels
+
+struct OutArgs {
+  int64_t* cnt;           // count pass
+  const int64_t* rowptr;  // fill pass
+  int32_t* col;
+  double* val;
+  int32_t* overflow;      // per row flag (count pass)
+  double tol;
+};
+
+template <bool FILL>
+__device__ void emit(Hash h, int64_t row, int lane, const OutArgs& o) {
+  if (!FILL) {
+    int n = count_kept(h, lane, o.tol);
+    if (lane == 0) o.cnt[row] = n;
+  } else {
+    int n = compact_sort(h, lane, o.tol);
+    const int64_t base = o.rowptr[row];
+    for (int i = lane; i < n; i += 32) {
+      o.col[base + i] = h.keys[i];
+      o.val[base + i] = h.vals[i];
+    }
+  }
+}
+
+template <bool FILL, bool GLOBAL>
+__global__ void k_product(CsrView A, CsrView B, bool reverse_a, const int64_t* __restrict__ rows, int64_t nrows,
+                          uint32_t cap, char* __restrict__ gscratch, OutArgs o) {
+  extern __shared__ __align__(16) char smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
+  const int64_t nw = (int64_t)gridDim.x * kWarpsPerBlock;
+  char* base = GLOBAL ? gscratch + gw * (size_t)cap * 16 : smem + (size_t)w * cap * 16;
+  Hash h{reinterpret_cast<int32_t*>(base + (size_t)cap * 8), nullptr, reinterpret_cast<double*>(base), cap};
+  for (int64_t r = gw; r < nrows; r += nw) {
+    const int64_t row = rows ? rows[r] : r;
+    bool ok = row_product(A, B, row, reverse_a, h, lane, (cap * 3) / 4);
+    if (!ok) {
+      if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
+      continue;
+    }
+    emit<FILL>(h, row, lane, o);
+  }
+}
+
+template <bool FILL, bool GLOBAL>
+__global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restrict__ rows, int64_t nrows,
+                         uint32_t cap1, uint32_t cap2, char* __restrict__ gscratch, OutArgs o) {
+  extern __shared__ __align__(16) char smem[];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
+  const int64_t nw = (int64_t)gridDim.x * kWarpsPerBlock;
+  const size_t per = (size_t)cap1 * 16 + (size_t)cap2 * 16;
+  char* base = GLOBAL ? gscratch + gw * per : smem + (size_t)w * per;
+  Hash h1{reinterpret_cast<int32_t*>(base + (size_t)cap1 * 8), reinterpret_cast<int32_t*>(base + (size_t)cap1 * 12),
+          reinterpret_cast<double*>(base), cap1};
+  char* b2 = base + (size_t)cap1 * 16;
+  Hash h2{reinterpret_cast<int32_t*>(b2 + (size_t)cap2 * 8), nullptr, reinterpret_cast<double*>(b2), cap2};
+  for (int64_t r = gw; r < nrows; r += nw) {
+    const int64_t row = rows ? rows[r] : r;
+    bool ok = row_triple(R, A, P, row, h1, h2, lane, (cap1 * 3) / 4, (cap2 * 3) / 4);
+    if (!ok) {
+      if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
+      continue;
+    }
+    emit<FILL>(h2, row, lane, o);
+  }
+}
+
+// upper bounds of products per row (for sizing the global fallback)
+__global__ void k_row_products(CsrView A, CsrView B, int64_t* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < A.n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = 0;
+    for (int64_t p = A.rowptr[r]; p < A.rowptr[r + 1]; ++p) {
+      int32_t j = A.col[p];
+      t += B.rowptr[j + 1] - B.rowptr[j];
+    }
+    out[r] = t;
+  }
+}
+
+uint32_t pow2_at_least(int64_t n) {
+  uint32_t c = 64;
+  while ((int64_t)c < n && c < (1u << 30)) c <<= 1;
+  return c;
+}
+
+std::vector<int64_t> overflow_rows(const int32_t* dflag, int64_t n) {
+  std::vector<int32_t> f(n);
+  if (n) CAMG_CUDA(cudaMemcpy(f.data(), dflag, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+  std::vector<int64_t> rows;
+  for (int64_t i = 0; i < n; ++i)
+    if (f[i]) rows.push_back(i);
+  return rows;
+}
+
+// Driver shared by the product and the triple: `launch(fill, global, rows, nrows, caps, scratch, out)`.
+template <class Launch, class GlobalCaps>
+Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, GlobalCaps gcaps, double tol, cudaStream_t s) {
+  DBuf<int64_t> cnt(n_rows + 1);
+  DBuf<int32_t> ovf(n_rows + 1);
+  CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
+  OutArgs o{cnt.p, nullptr, nullptr, nullptr, ovf.p, tol};
+  if (n_rows) launch(false, false, nullptr, n_rows, 0, 0, nullptr, o);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> big = overflow_rows(ovf.p, n_rows);
+  DBuf<int64_t> big_rows(big.size() + 1);
+  uint32_t gc1 = 0, gc2 = 0;
+  int64_t gw = 0;
+  DBuf<char> scratch;
+  if (!big.empty()) {
+    CAMG_CUDA(cudaMemcpy(big_rows.p, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice));
+    gcaps(big, gc1, gc2);
+    const size_t per = (size_t)gc1 * 16 + (size_t)gc2 * 16;
+    const size_t budget = size_t(2) << 30;
+    gw = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>((int64_t)big.size(), (int64_t)(budget / per)));
+    gw = (gw + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
+    scratch = DBuf<char>((size_t)gw * per);
+    launch(false, true, big_rows.p, (int64_t)big.size(), gc1, gc2, scratch.p, o);
+  }
+  DBuf<int64_t> rp(n_rows + 1);
+  exclusive_scan_i64(cnt.p, rp.p, n_rows, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  const int64_t nnz = read_i64(rp.p + n_rows);
+  Csr* C = new Csr();
+  C->n_rows = n_rows;
+  C->n_cols = n_cols;
+  C->nnz = nnz;
+  C->rowptr = rp.release();
+  C->col = dalloc<int32_t>(nnz);
+  C->val = dalloc<double>(nnz);
+  C->avg_row = n_rows ? double(nnz) / n_rows : 0.0;
+  OutArgs f{nullptr, C->rowptr, C->col, C->val, nullptr, tol};
+  // fill: small rows from shared memory (overflow rows are skipped there and
+  // redone from the global scratch)
+  if (n_rows) launch(true, false, nullptr, n_rows, 0, 0, nullptr, f);
+  if (!big.empty()) launch(true, true, big_rows.p, (int64_t)big.size(), gc1, gc2, scratch.p, f);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  CAMG_LAUNCH_CHECK();
+  return C;
+}
+
+constexpr uint32_t kCapProduct = 2048;  // 32 KB per warp
+constexpr uint32_t kCap1 = 2048, kCap2 = 512;
+
+}  // namespace
+
+Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s) {
+  CAMG_CHECK(A->n_cols == B->n_rows, CAMG_ERR_DIMENSION, "sp_matmul: inner dimensions differ");
+  CAMG_CHECK(B->n_cols < INT32_MAX, CAMG_ERR_DIMENSION, "too many columns");
+  const size_t smem = (size_t)kWarpsPerBlock * kCapProduct * 16;
+  static bool attr = false;
+  if (!attr) {
+    CAMG_CUDA(cudaFuncSetAttribute(k_product<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CAMG_CUDA(cudaFuncSetAttribute(k_product<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  auto launch = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t,
+                    char* scratch, OutArgs o) {
+    note_launch();
+    if (!global) {
+      unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 8);
+      if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, rows, nrows, kCapProduct, nullptr, o);
+      else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, rows, nrows, kCapProduct, nullptr, o);
+    } else {
+      // number of warps is fixed by the scratch allocation: scratch.n / (c1*16)
+      int64_t warps = 0;
+      (void)warps;
+      unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, 1 << 20));
+      if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
+      else k_product<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
+    }
+    CAMG_LAUNCH_CHECK();
+  };
+  // global path: cap from the largest product count among overflow rows
+  DBuf<int64_t> prods(A->n_rows + 1);
+  auto gcaps = [&](const std::vector<int64_t>& big, uint32_t& c1, uint32_t& c2) {
+    note_launch();
+    k_row_products<<<grid_for(A->n_rows, 256), 256, 0, s>>>(view(A), view(B), prods.p);
+    std::vector<int64_t> h(A->n_rows);
+    CAMG_CUDA(cudaMemcpy(h.data(), prods.p, sizeof(int64_t) * A->n_rows, cudaMemcpyDeviceToHost));
+    int64_t mx = 0;
+    for (int64_t r : big) mx = std::max(mx, h[r]);
+    c1 = pow2_at_least(2 * std::min<int64_t>(mx, B->n_cols) + 64);
+    c2 = 0;
+  };
+  // the global launch uses exactly as many warps as there are scratch slots
+  auto launch_fixed = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t c2,
+                          char* scratch, OutArgs o) {
+    if (!global) return launch(fill, global, rows, nrows, c1, c2, scratch, o);
+    note_launch();
+    int64_t warps = std::min<int64_t>(nrows, std::max<int64_t>(kWarpsPerBlock, (int64_t)((size_t(2) << 30) / ((size_t)c1 * 16))));
+    unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
+    else k_product<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
+    CAMG_LAUNCH_CHECK();
+  };
+  return two_pass(A->n_rows, B->n_cols, launch_fixed, gcaps, tol, s);
+}
+
+Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B, false, kDropTol, s); }
+
+Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
+  CAMG_CHECK(R->n_cols == A->n_rows && A->n_cols == P->n_rows, CAMG_ERR_DIMENSION,
+             "galerkin_triple: dimension mismatch");
+  const size_t per = (size_t)kCap1 * 16 + (size_t)kCap2 * 16;
+  const size_t smem = (size_t)kWarpsPerBlock * per;
+  static bool attr = false;
+  if (!attr) {
+    CAMG_CUDA(cudaFuncSetAttribute(k_triple<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CAMG_CUDA(cudaFuncSetAttribute(k_triple<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  auto launch = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t c2,
+                    char* scratch, OutArgs o) {
+    note_launch();
+    if (!global) {
+      unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 8);
+      if (fill) k_triple<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, kCap1, kCap2, nullptr, o);
+      else k_triple<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, kCap1, kCap2, nullptr, o);
+    } else {
+      const size_t pw = (size_t)c1 * 16 + (size_t)c2 * 16;
+      int64_t warps = std::min<int64_t>(nrows, std::max<int64_t>(kWarpsPerBlock, (int64_t)((size_t(2) << 30) / pw)));
+      unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+      if (fill) k_triple<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
+      else k_triple<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
+    }
+    CAMG_LAUNCH_CHECK();
+  };
+  auto gcaps = [&](const std::vector<int64_t>& big, uint32_t& c1, uint32_t& c2) {
+    // RA products bound, and RA-unique x P-row bound for the result
+    DBuf<int64_t> t1(R->n_rows + 1);
+    note_launch();
+    k_row_products<<<grid_for(R->n_rows, 256), 256, 0, s>>>(view(R), view(A), t1.p);
+    std::vector<int64_t> h(R->n_rows);
+    CAMG_CUDA(cudaMemcpy(h.data(), t1.p, sizeof(int64_t) * R->n_rows, cudaMemcpyDeviceToHost));
+    int64_t mx = 0;
+    for (int64_t r : big) mx = std::max(mx, h[r]);
+    c1 = pow2_at_least(2 * std::min<int64_t>(mx, A->n_cols) + 64);
+    c2 = pow2_at_least(2 * P->n_cols + 64);
+    // keep the result table bounded: at most what the RA row can reach
+    c2 = std::min<uint32_t>(c2, pow2_at_least(2 * std::min<int64_t>(mx * 64, P->n_cols) + 64));
+  };
+  return two_pass(R->n_rows, P->n_cols, launch, gcaps, kDropTol, s);
+}
+
+}  // namespace camg
+
+using namespace camg;
+
+namespace camg {
+Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s);
+void recip(int64_t n, const double* d, double* out, cudaStream_t s);
+Csr* scale_cols(const Csr* A, const double* c, cudaStream_t s);
+
+// P = P_tent - omega_eff * ((diag(1/d) A) P_tent)  (transfer.py:164-183)
+Csr* smooth_prolongator(const Csr* Pt, const Csr* A, const double* d, double omega_eff, cudaStream_t s) {
+  CAMG_CHECK(A->n_rows == A->n_cols && A->n_rows == Pt->n_rows, CAMG_ERR_DIMENSION,
+             "smooth_prolongator: A and P_tent dimensions mismatch");
+  DBuf<double> dinv(A->n_rows + 1);
+  recip(A->n_rows, d, dinv.p, s);
+  Csr* DA = csr_scale_rows(A, dinv.p, s);       // from_scipy(A.multiply(1/d)) : canonical
+  Csr* X = spgemm_ex(DA, Pt, false, 0.0, s);    // raw csr_matmat: exact zeros dropped
+  delete DA;
+  Csr* P = csr_axpby(1.0, Pt, -omega_eff, X, s);  // P_tent - omega*X, canonical
+  delete X;
+  return P;
+}
+
+// S~ = scale*Cz + scale*((B2 diag(ainv)) B1)   (smoothers.py:233-238)
+Csr* schur(const Csr* B2, const Csr* Cz, const Csr* B1, const double* ainv, double scale, cudaStream_t s) {
+  // B2 @ diags(ainv): every entry b*a (0 + product); scipy's output row is in
+  // reverse first-touch order, i.e. B2's row reversed -> the next product
+  // walks it backwards.
+  Csr* T = scale_cols(B2, ainv, s);
+  Csr* X = spgemm_ex(T, B1, true, 0.0, s);
+  delete T;
+  Csr* S = csr_axpby(scale, Cz, scale, X, s);
+  delete X;
+  return S;
+}
+
+__global__ void k_recip(int64_t n, const double* __restrict__ d, double* __restrict__ o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = __drcp_rn(d[i]);
+}
+
+void recip(int64_t n, const double* d, double* out, cudaStream_t s) {
+  note_launch();
+  k_recip<<<grid_for(n, 256), 256, 0, s>>>(n, d, out);
+}
+
+// column scaling keeping exact zeros of the product out (csr_matmat with a
+// diagonal right factor)
+template <bool FILL>
+__global__ void k_scale_cols(CsrView A, const double* __restrict__ c, int64_t* __restrict__ cnt,
+                             const int64_t* __restrict__ crow, int32_t* __restrict__ ccol, double* __restrict__ cval) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < A.n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = 0, out = FILL ? crow[r] : 0;
+    for (int64_t p = A.rowptr[r]; p < A.rowptr[r + 1]; ++p) {
+      double v = __dadd_rn(0.0, __dmul_rn(A.val[p], c[A.col[p]]));
+      if (v != 0.0) {
+        if (FILL) { ccol[out + n] = A.col[p]; cval[out + n] = v; }
+        ++n;
+      }
+    }
+    if (!FILL) cnt[r] = n;
+  }
+}
+
+Csr* scale_cols(const Csr* A, const double* c, cudaStream_t s) {
+  DBuf<int64_t> cnt(A->n_rows + 1);
+  note_launch();
+  k_scale_cols<false><<<grid_for(A->n_rows, 256), 256, 0, s>>>(view(A), c, cnt.p, nullptr, nullptr, nullptr);
+  DBuf<int64_t> rp(A->n_rows + 1);
+  exclusive_scan_i64(cnt.p, rp.p, A->n_rows, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  int64_t nnz = read_i64(rp.p + A->n_rows);
+  Csr* C = new Csr();
+  C->n_rows = A->n_rows; C->n_cols = A->n_cols; C->nnz = nnz;
+  C->rowptr = rp.release();
+  C->col = dalloc<int32_t>(nnz);
+  C->val = dalloc<double>(nnz);
+  C->avg_row = C->n_rows ? double(nnz) / C->n_rows : 0.0;
+  note_launch();
+  k_scale_cols<true><<<grid_for(A->n_rows, 256), 256, 0, s>>>(view(A), c, nullptr, C->rowptr, C->col, C->val);
+  CAMG_LAUNCH_CHECK();
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  return C;
+}
+
+}  // namespace camg
+
+extern "C" {
+
+int camg_spgemm(const camg_csr* A, const camg_csr* B, camg_csr** out) {
+  return guarded([&] { *out = new camg_csr{spgemm(A->m, B->m, 0)}; });
+}
+
+int camg_galerkin(const camg_csr* R, const camg_csr* A, const camg_csr* P, camg_csr** out) {
+  return guarded([&] { *out = new camg_csr{galerkin(R->m, A->m, P->m, 0)}; });
+}
+
+int camg_smooth_prolongator(const camg_csr* P_tent, const camg_csr* A, const double* d, double omega_eff,
+                            camg_csr** out) {
+  return guarded([&] { *out = new camg_csr{smooth_prolongator(P_tent->m, A->m, d, omega_eff, 0)}; });
+}
+
+int camg_schur(const camg_csr* B2, const camg_csr* Cz, const camg_csr* B1, const double* ainv, double scale,
+               camg_csr** out) {
+  return guarded([&] {
+    CAMG_CHECK(B2->m->n_cols == B1->m->n_rows && B2->m->n_rows == Cz->m->n_rows && B1->m->n_cols == Cz->m->n_cols,
+               CAMG_ERR_DIMENSION, "schur: inconsistent block shapes");
+    *out = new camg_csr{schur(B2->m, Cz->m, B1->m, ainv, scale, 0)};
+  });
+}
+
+}  // extern "C"

@@ -521,3 +521,51 @@ def generate(spec: TwoBodySpec, assemble_K: bool = True) -> GeneratedSystem:
         master_nodes=master_nodes, active=active, stencil=stencil,
         D_face=D_face, M_face=M_face,
     )
+
+
+# ---------------------------------------------------------------------------
+# device-side assembly and operator construction
+
+
+def assemble_K_device(g: GeneratedSystem):
+    """K assembled on the device from the stencil tables (bit-identical to
+    the host assembly); returns a device-resident SparseMatrix."""
+    import ctypes as C
+
+    from . import _native as N
+    from .sparse import SparseMatrix
+
+    dim = g.dim
+    total = 0
+    for blk in g.stencil:
+        grid = np.ascontiguousarray(blk["grid"], dtype=np.int64)
+        table = np.ascontiguousarray(blk["table"], dtype=np.float64)
+        nnz = C.c_int64()
+        N.call("camg_stencil_block_counts", dim, grid.ctypes.data_as(C.c_void_p), int(blk["clamp_lo"]),
+               int(blk["clamp_hi"]), table.ctypes.data_as(C.c_void_p), C.byref(nnz))
+        total += nnz.value
+    h = C.c_void_p()
+    N.call("camg_csr_alloc", g.n_u, g.n_u, total, C.byref(h))
+    row = 0
+    for blk in g.stencil:
+        grid = np.ascontiguousarray(blk["grid"], dtype=np.int64)
+        table = np.ascontiguousarray(blk["table"], dtype=np.float64)
+        N.call("camg_assemble_stencil", dim, grid.ctypes.data_as(C.c_void_p), int(blk["clamp_lo"]),
+               int(blk["clamp_hi"]), int(blk["node_offset"]), g.n_u, table.ctypes.data_as(C.c_void_p), h, row)
+        nk = int(np.prod(blk["grid"])) - (int(np.prod(blk["grid"][:-1])) if blk["clamp_lo"] else 0) \
+            - (int(np.prod(blk["grid"][:-1])) if blk["clamp_hi"] else 0)
+        row += dim * nk
+    return SparseMatrix._wrap(h)
+
+
+def saddle_operator(g: GeneratedSystem, device_K: bool | None = None):
+    """SaddleOperator of a generated system (K on the device)."""
+    from .saddle import SaddleOperator
+    from .sparse import SparseMatrix
+
+    if g.K is None or device_K:
+        K = assemble_K_device(g)
+    else:
+        K = SparseMatrix.from_scipy(g.K)
+    return SaddleOperator(K, SparseMatrix.from_scipy(g.B1), SparseMatrix.from_scipy(g.B2),
+                          SparseMatrix.from_scipy(g.Cz))

@@ -1,0 +1,262 @@
+"""Saddle-point block smoothers on the device (smoothers.py:1-384).
+
+`BlockSmoother` binds a configuration to one saddle operator and owns a
+native level (`camg_level`): merged operator, S~, inverse diagonals and the
+fused step kernels of `csrc/hierarchy.cu`.  Configuration classes keep the
+reference names, defaults and validation (smoothers.py:29-70).
+
+Inner solves on the GPU: `jacobi` (predictor and corrector) and `direct`
+(corrector, dense LU of S~).  The reference's lexicographic `sgs` / `ilu0`
+are sequential; they are rejected here with ConfigError (the GPU variant
+`mcgs` is compared by convergence only).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigError
+from .saddle import SaddleOperator, SaddleSystem
+from .sparse import (
+    BlockVector,
+    SparseMatrix,
+    diagonal_device,
+    empty,
+    is_device,
+    lu_factor_quiet,
+    ptr,
+    stream_ptr,
+    to_device,
+)
+
+POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct")
+BLOCK_KINDS = ("uzawa", "braess_sarazin", "simple", "simplec")
+A_HAT_MODES = ("plain_diag", "abs_rowsum", "exact")
+GPU_POINT_KINDS = ("jacobi", "direct")
+
+_BLOCK_CODE = {"uzawa": 0, "braess_sarazin": 1, "simple": 2, "simplec": 3}
+_POINT_CODE = {"jacobi": 0, "direct": 3}
+
+
+@dataclass(frozen=True)
+class PointSmootherConfig:                       # smoothers.py:29-41
+    kind: str = "sgs"
+    sweeps: int = 1
+    damping: float = 1.0
+
+    def __post_init__(self):
+        if self.kind not in POINT_KINDS:
+            raise ConfigError(f"unknown point smoother kind: {self.kind!r}")
+        if self.sweeps < 1:
+            raise ConfigError("point smoother sweeps must be >= 1")
+        if not (0.0 < self.damping < 2.0):
+            raise ConfigError("point smoother damping must lie in (0, 2)")
+
+
+@dataclass(frozen=True)
+class BlockSmootherConfig:                       # smoothers.py:44-70
+    kind: str = "simplec"
+    alpha: float = 0.7
+    outer_sweeps: int = 1
+    predictor: PointSmootherConfig = field(default_factory=PointSmootherConfig)
+    corrector: PointSmootherConfig = field(default_factory=lambda: PointSmootherConfig(kind="ilu0"))
+    a_hat_mode: str = "plain_diag"
+
+    def __post_init__(self):
+        if self.kind not in BLOCK_KINDS:
+            raise ConfigError(f"unknown block smoother kind: {self.kind!r}")
+        if self.alpha <= 0.0:
+            raise ConfigError("alpha must be positive")
+        if self.outer_sweeps < 1:
+            raise ConfigError("outer_sweeps must be >= 1")
+        if self.a_hat_mode not in A_HAT_MODES:
+            raise ConfigError(f"unknown a_hat_mode: {self.a_hat_mode!r}")
+        if self.kind == "braess_sarazin" and self.a_hat_mode != "plain_diag":
+            raise ConfigError("braess_sarazin hard-codes the plain-diagonal predictor")
+
+    def effective_a_hat_mode(self) -> str:
+        if self.kind == "simplec":
+            return "abs_rowsum"
+        if self.kind == "braess_sarazin":
+            return "plain_diag"
+        return self.a_hat_mode
+
+
+@dataclass
+class SchurOperator:
+    S_tilde: SparseMatrix
+    a_hat_inv_diag: np.ndarray | None
+
+
+def native_cfg(cfg: BlockSmootherConfig) -> N.SmootherCfg:
+    mode = cfg.effective_a_hat_mode()
+    if mode == "exact":
+        raise ConfigError("a_hat_mode 'exact' (dense K inverse) is not available on the GPU path")
+    if cfg.kind != "braess_sarazin" and cfg.predictor.kind != "jacobi":
+        raise ConfigError(f"GPU predictor supports {('jacobi',)}, got {cfg.predictor.kind!r}")
+    if cfg.corrector.kind not in GPU_POINT_KINDS:
+        raise ConfigError(f"GPU corrector supports {GPU_POINT_KINDS}, got {cfg.corrector.kind!r}")
+    return N.SmootherCfg(
+        kind=_BLOCK_CODE[cfg.kind], alpha=float(cfg.alpha), outer_sweeps=int(cfg.outer_sweeps),
+        a_hat_mode=1 if mode == "abs_rowsum" else 0,
+        pred_kind=_POINT_CODE.get(cfg.predictor.kind, 0), pred_sweeps=int(cfg.predictor.sweeps),
+        pred_damping=float(cfg.predictor.damping),
+        corr_kind=_POINT_CODE[cfg.corrector.kind], corr_sweeps=int(cfg.corrector.sweeps),
+        corr_damping=float(cfg.corrector.damping),
+    )
+
+
+class _LevelHandle:
+    __slots__ = ("h",)
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h and N._lib is not None:
+            N._lib.camg_level_destroy(self.h)
+            self.h = None
+
+
+class PointSmoother:
+    """Point smoother bound to one matrix (smoothers.py:141-199): jacobi on
+    the device, direct via dense LU."""
+
+    def __init__(self, cfg: PointSmootherConfig, A: SparseMatrix):
+        if cfg.kind not in GPU_POINT_KINDS:
+            raise ConfigError(f"GPU point smoother supports {GPU_POINT_KINDS}, got {cfg.kind!r}")
+        self.cfg, self.A = cfg, A
+        if cfg.kind == "jacobi":
+            d = diagonal_device(A, "plain")
+            if bool((d == 0).any()):
+                from .errors import SingularMatrixError
+                row = int((d == 0).nonzero()[0])
+                raise SingularMatrixError(f"jacobi: zero diagonal in row {row}")
+            self._dinv = cfg.damping / d
+        else:
+            from .errors import SingularMatrixError
+            self._lu = lu_factor_quiet(A.to_dense())
+            if np.any(np.diag(self._lu[0]) == 0.0):
+                raise SingularMatrixError("direct smoother: singular matrix")
+
+    def smooth(self, x, b):
+        if self.cfg.kind == "direct":
+            import scipy.linalg
+            sol = scipy.linalg.lu_solve(self._lu, np.asarray(b.cpu() if is_device(b) else b, dtype=np.float64))
+            return to_device(sol) if is_device(b) else sol
+        xd = to_device(x, self.A.num_cols).clone()
+        bd = to_device(b, self.A.num_rows)
+        t = empty(self.A.num_rows)
+        for _ in range(self.cfg.sweeps):
+            t.copy_(bd)
+            N.call("camg_spmv", self.A.device, -1.0, ptr(xd), 1.0, ptr(t), stream_ptr())
+            xd += self._dinv * t
+        return xd if is_device(b) else xd.cpu().numpy()
+
+    def apply(self, b):
+        n = self.A.num_rows
+        z = np.zeros(n)
+        return self.smooth(to_device(z) if is_device(b) else z, b)
+
+
+def build_schur(op, a_hat_mode: str = "plain_diag", alpha: float = 1.0, scale_with_alpha: bool = False,
+                a_hat_scale: float = 1.0) -> SchurOperator:
+    """S~ = scale*Cz + scale*B2 diag(1/(a_hat_scale*A^)) B1 on the device
+    (smoothers.py:220-239)."""
+    if isinstance(op, SaddleSystem):
+        op = op.op
+    if a_hat_mode == "exact":
+        raise ConfigError("a_hat_mode 'exact' is not available on the GPU path")
+    scale = alpha if scale_with_alpha else 1.0
+    d = diagonal_device(op.K, "plain" if a_hat_mode == "plain_diag" else "abs_rowsum")
+    if bool((d == 0).any()):
+        from .errors import SingularMatrixError
+        raise SingularMatrixError("a_hat: zero diagonal entry")
+    ainv = 1.0 / (a_hat_scale * d)
+    h = C.c_void_p()
+    N.call("camg_schur", op.B2.device, op.Cz.device, op.B1.device, ptr(ainv), float(scale), C.byref(h))
+    return SchurOperator(SparseMatrix._wrap(h), ainv.cpu().numpy())
+
+
+class BlockSmoother:
+    """Bound block smoother (smoothers.py:245-329), executed by libcamg."""
+
+    def __init__(self, cfg: BlockSmootherConfig, op, predictor_solver=None, pre_sweeps: int = 1,
+                 post_sweeps: int = 1):
+        if isinstance(op, SaddleSystem):
+            op = op.op
+        if predictor_solver is not None:
+            raise ConfigError("custom predictor solvers are not supported on the GPU path")
+        self.cfg = cfg
+        self.op = op
+        ncfg = native_cfg(cfg)
+        h = C.c_void_p()
+        N.call("camg_level_create", op.K.device, op.B1.device, op.B2.device, op.Cz.device, C.byref(ncfg),
+               int(pre_sweeps), int(post_sweeps), C.byref(h))
+        self._level = _LevelHandle(h)
+        self._schur = None
+        if cfg.corrector.kind == "direct" and op.n_lam > 0:
+            S = self.schur.S_tilde.to_dense()
+            lu, piv = lu_factor_quiet(S)
+            if np.any(np.diag(lu) == 0.0):
+                from .errors import SingularMatrixError
+                raise SingularMatrixError("direct smoother: singular matrix")
+            lu_f = np.asfortranarray(lu)
+            piv32 = np.ascontiguousarray(piv, dtype=np.int32)
+            N.call("camg_level_set_corrector_lu", self._level.h, op.n_lam,
+                   lu_f.ctypes.data_as(C.c_void_p), piv32.ctypes.data_as(C.c_void_p))
+
+    @property
+    def handle(self):
+        return self._level.h
+
+    @property
+    def schur(self) -> SchurOperator:
+        if self._schur is None:
+            h = C.c_void_p()
+            N.call("camg_level_schur", self._level.h, C.byref(h))
+            self._schur = SchurOperator(SparseMatrix._wrap(h), None)
+        return self._schur
+
+    def sweep_merged(self, x, b):
+        n = self.op.total_rows
+        xd = to_device(x, n)
+        bd = to_device(b, n)
+        out = empty(n)
+        N.call("camg_level_sweep", self._level.h, ptr(xd), ptr(bd), ptr(out), stream_ptr())
+        return out
+
+    def sweep(self, x: BlockVector, b: BlockVector) -> BlockVector:
+        out = self.sweep_merged(x.merged(), b.merged())
+        if not is_device(x.u):
+            out = out.cpu().numpy()
+        return BlockVector.from_merged(out, self.op.n_u)
+
+    def apply(self, b: BlockVector) -> BlockVector:
+        n = self.op.total_rows
+        bd = to_device(b.merged(), n)
+        out = empty(n)
+        N.call("camg_level_sweep", self._level.h, C.c_void_p(0), ptr(bd), ptr(out), stream_ptr())
+        if not is_device(b.u):
+            out = out.cpu().numpy()
+        return BlockVector.from_merged(out, self.op.n_u)
+
+
+def uzawa_sweep(sys, cfg: BlockSmootherConfig, x: BlockVector, b: BlockVector) -> BlockVector:
+    return BlockSmoother(cfg, sys).sweep(x, b)
+
+
+def braess_sarazin_sweep(sys, cfg: BlockSmootherConfig, x: BlockVector, b: BlockVector) -> BlockVector:
+    return BlockSmoother(cfg, sys).sweep(x, b)
+
+
+def simple_sweep(sys, cfg: BlockSmootherConfig, x: BlockVector, b: BlockVector) -> BlockVector:
+    return BlockSmoother(cfg, sys).sweep(x, b)
+
+
+def point_smooth(cfg: PointSmootherConfig, A: SparseMatrix, x, b):
+    return PointSmoother(cfg, A).smooth(x, b)

@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path (libcamg via the package API) against the
+reference's golden fixtures and against the oracle run live on the same
+machine.  Bars (BASELINE.json north_star): per-level operators within 1e-12
+relative Frobenius (patterns exact), aggregates bit-exact, V-cycle within
+1e-10 relative 2-norm, GMRES iteration count equal or within +-1."""
+
+import sys
+
+import numpy as np
+import pytest
+import scipy.sparse
+
+import camg_oracle as O
+from _golden import GOLDEN, cases, csr, load
+
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, GOLDEN)
+from cases import BY_NAME  # noqa: E402
+
+from paper_1912_09056_b200 import _native  # noqa: E402
+from paper_1912_09056_b200.errors import ConfigError  # noqa: E402
+from paper_1912_09056_b200.hierarchy import HierarchyConfig, fine_level_meta, setup  # noqa: E402
+from paper_1912_09056_b200.krylov import GmresConfig, gmres  # noqa: E402
+from paper_1912_09056_b200.problem import assemble_K_device, config_spec, generate, saddle_operator  # noqa: E402
+from paper_1912_09056_b200.smoothers import BlockSmootherConfig, PointSmootherConfig  # noqa: E402
+from paper_1912_09056_b200.sparse import (  # noqa: E402
+    SparseMatrix,
+    extract_diagonal,
+    galerkin_triple,
+    sp_matmul,
+    sp_transpose,
+    spmv,
+)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def device():
+    _native.require_device()
+
+
+def block_cfg(skw):
+    kw = dict(skw)
+    for k in ("predictor", "corrector"):
+        if k in kw:
+            kw[k] = PointSmootherConfig(*kw[k])
+    return BlockSmootherConfig(**kw)
+
+
+def oracle_block_cfg(skw):
+    kw = dict(skw)
+    for k in ("predictor", "corrector"):
+        if k in kw:
+            kw[k] = O.PointCfg(*kw[k])
+    return O.BlockCfg(**kw)
+
+
+def rel_fro(A, B):
+    A, B = scipy.sparse.csr_matrix(A), scipy.sparse.csr_matrix(B)
+    d = scipy.sparse.linalg.norm(A - B) if (A - B).nnz else 0.0
+    nb = scipy.sparse.linalg.norm(B)
+    return d / nb if nb else d
+
+
+def same_pattern(A, B):
+    A, B = scipy.sparse.csr_matrix(A), scipy.sparse.csr_matrix(B)
+    return A.shape == B.shape and np.array_equal(A.indptr, B.indptr) and np.array_equal(A.indices, B.indices)
+
+
+GPU_CASES = [c for c in cases() if BY_NAME[c][4].get("predictor", ("jacobi",))[0] == "jacobi"
+             and BY_NAME[c][4].get("corrector", ("jacobi",))[0] in ("jacobi", "direct")]
+
+
+# ---------------------------------------------------------------------------
+# kernels
+
+
+def test_sparse_kernels_vs_reference_golden():
+    z = np.load(GOLDEN + "/kernels.npz")
+    for t in range(4):
+        A, Asq, B = csr(z, f"t{t}_A"), csr(z, f"t{t}_Asq"), csr(z, f"t{t}_B")
+        dA, dAsq, dB = SparseMatrix.from_scipy(A), SparseMatrix.from_scipy(Asq), SparseMatrix.from_scipy(B)
+        y = spmv(dA, z[f"t{t}_x"])
+        ref = z[f"t{t}_spmv"]
+        assert np.abs(y - ref).max() <= 1e-14 * max(1.0, np.abs(ref).max())
+        assert same_pattern(sp_transpose(dA).to_scipy(), csr(z, f"t{t}_AT"))
+        assert np.array_equal(sp_transpose(dA).values, csr(z, f"t{t}_AT").data)
+        AB = sp_matmul(dAsq, dB).to_scipy()
+        assert same_pattern(AB, csr(z, f"t{t}_AB")) and np.array_equal(AB.data, csr(z, f"t{t}_AB").data)
+        RAP = galerkin_triple(sp_transpose(dB), dAsq, dB).to_scipy()
+        assert same_pattern(RAP, csr(z, f"t{t}_RAP")) and np.array_equal(RAP.data, csr(z, f"t{t}_RAP").data)
+        np.testing.assert_array_equal(extract_diagonal(dAsq), z[f"t{t}_diag"])
+        np.testing.assert_allclose(extract_diagonal(dAsq, "abs_rowsum"), z[f"t{t}_absrow"], rtol=1e-15)
+
+
+def test_spgemm_bit_exact_vs_scipy_random():
+    rng = np.random.default_rng(11)
+    for t in range(6):
+        m, k, n = rng.integers(50, 600, size=3)
+        dens = float(rng.uniform(0.01, 0.2))
+        A = O.canon(scipy.sparse.random(m, k, density=dens, random_state=int(rng.integers(1 << 30))))
+        B = O.canon(scipy.sparse.random(k, n, density=dens, random_state=int(rng.integers(1 << 30))))
+        C = sp_matmul(SparseMatrix.from_scipy(A), SparseMatrix.from_scipy(B)).to_scipy()
+        ref = O.matmul(A, B)
+        assert same_pattern(C, ref) and np.array_equal(C.data, ref.data)
+        Sq = O.canon(scipy.sparse.random(k, k, density=dens, random_state=int(rng.integers(1 << 30))))
+        P = O.canon(scipy.sparse.random(k, n, density=dens, random_state=int(rng.integers(1 << 30))))
+        R = O.transpose(P)
+        G = galerkin_triple(SparseMatrix.from_scipy(R), SparseMatrix.from_scipy(Sq), SparseMatrix.from_scipy(P))
+        ref = O.rap(R, Sq, P)
+        assert same_pattern(G.to_scipy(), ref) and np.array_equal(G.to_scipy().data, ref.data)
+
+
+def test_spgemm_overflow_rows_use_global_path():
+    """Rows with more unique columns than the shared-memory hash holds."""
+    rng = np.random.default_rng(3)
+    A = O.canon(scipy.sparse.random(40, 3000, density=0.5, random_state=1))
+    B = O.canon(scipy.sparse.random(3000, 5000, density=0.01, random_state=2))
+    C = sp_matmul(SparseMatrix.from_scipy(A), SparseMatrix.from_scipy(B)).to_scipy()
+    ref = O.matmul(A, B)
+    assert same_pattern(C, ref) and np.array_equal(C.data, ref.data)
+    P = O.canon(scipy.sparse.random(3000, 2500, density=0.02, random_state=4))
+    Sq = O.canon(scipy.sparse.random(3000, 3000, density=0.05, random_state=5))
+    G = galerkin_triple(SparseMatrix.from_scipy(O.transpose(P)), SparseMatrix.from_scipy(Sq),
+                        SparseMatrix.from_scipy(P)).to_scipy()
+    ref = O.rap(O.transpose(P), Sq, P)
+    assert same_pattern(G, ref) and np.array_equal(G.data, ref.data)
+
+
+@pytest.mark.parametrize("name,scale", [("C1", 1), ("C3", 8), ("C4", 8), ("C2", 4)])
+def test_device_assembly_equals_host(name, scale):
+    g = generate(config_spec(name, scale))
+    Kd = assemble_K_device(g).to_scipy()
+    assert same_pattern(Kd, g.K) and np.array_equal(Kd.data, g.K.data)
+
+
+# ---------------------------------------------------------------------------
+# hierarchy parity against the reference's golden outputs
+
+_H = {}
+
+
+def gpu_hier(name):
+    if name not in _H:
+        _, cfg, scale, hkw, skw, restart, max_iters = BY_NAME[name]
+        g = generate(config_spec(cfg, scale))
+        op = saddle_operator(g)
+        H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+        _H[name] = (g, op, H)
+    return _H[name]
+
+
+@pytest.mark.parametrize("name", GPU_CASES)
+def test_hierarchy_operators_and_aggregates(name):
+    z = load(name)
+    g, op, H = gpu_hier(name)
+    assert H.num_levels == int(z["num_levels"])
+    np.testing.assert_array_equal(H.levels[0].info["u_agg"], z["L0_u_agg"])
+    np.testing.assert_array_equal(H.levels[0].info["lam_agg"], z["L0_lam_agg"])
+    for l, lvl in enumerate(H.levels):
+        for blk in ("K", "B1", "B2", "Cz"):
+            A = getattr(lvl.op, blk).to_scipy()
+            R = csr(z, f"L{l}_{blk}")
+            assert same_pattern(A, R), (l, blk)
+            assert rel_fro(A, R) <= 1e-12, (l, blk, rel_fro(A, R))
+        S = lvl.smoother.schur.S_tilde.to_scipy()
+        Sr = csr(z, f"L{l}_Stilde")
+        assert same_pattern(S, Sr) and rel_fro(S, Sr) <= 1e-12, l
+        if lvl.transfer is not None:
+            for key, P in (("Pu", lvl.transfer.P_u), ("Plam", lvl.transfer.P_lam)):
+                Pr = csr(z, f"L{l}_{key}")
+                assert same_pattern(P.to_scipy(), Pr), (l, key)
+                assert rel_fro(P.to_scipy(), Pr) <= 1e-12
+            assert lvl.info["lambda_max"] == pytest.approx(float(z[f"L{l}_lambda_max"]), rel=1e-13)
+            assert lvl.info["u_aggregates"] == int(z[f"L{l}_u_aggs"])
+            assert lvl.info["lam_aggregates"] == int(z[f"L{l}_lam_aggs"])
+            assert lvl.info["u_singletons"] == int(z[f"L{l}_u_singletons"])
+            assert lvl.info["lam_overlap_touches"] == int(z[f"L{l}_lam_overlaps"])
+
+
+@pytest.mark.parametrize("name", GPU_CASES)
+def test_sweep_and_vcycle_vs_reference(name):
+    z = load(name)
+    g, op, H = gpu_hier(name)
+    sm = H.levels[0].smoother
+    out = sm.sweep_merged(z["sweep_x"], z["sweep_b"]).cpu().numpy()
+    ref = z["sweep_out"]
+    assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+    for kin, kout in (("rhs", "vcycle_out"), ("vcycle_rand_in", "vcycle_rand_out")):
+        v = H.apply(z[kin])
+        ref = z[kout]
+        assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref), np.linalg.norm(v - ref) / np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("name", GPU_CASES)
+def test_gmres_iterations_vs_reference(name):
+    z = load(name)
+    g, op, H = gpu_hier(name)
+    cfg = GmresConfig(rel_tol=1e-8, max_iters=int(z["gmres_max_iters"]), restart=int(z["gmres_restart"]))
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, cfg)
+    assert abs(rep.iterations - int(z["gmres_iterations"])) <= 1, (rep.iterations, int(z["gmres_iterations"]))
+    assert rep.converged == bool(z["gmres_converged"])
+    hist = np.asarray(rep.residual_history)
+    assert hist[0] == pytest.approx(float(z["gmres_history"][0]), rel=1e-13)
+    if rep.converged:
+        A = csr(z, "A")
+        assert np.linalg.norm(g.rhs - A @ x) <= 2e-8 * np.linalg.norm(g.rhs)
+
+
+def test_unsupported_sequential_smoothers_are_rejected():
+    g, op, _ = gpu_hier(GPU_CASES[0])
+    with pytest.raises(ConfigError):
+        setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2),
+              BlockSmootherConfig(kind="simple", predictor=PointSmootherConfig("sgs")))
+
+
+# ---------------------------------------------------------------------------
+# larger systems against the oracle run live (same machine => same LAPACK)
+
+LIVE = [
+    ("C3", 4, dict(max_levels=3, max_coarse_size=50),
+     dict(kind="braess_sarazin", alpha=1.0 / 0.7, corrector=("jacobi", 1, 0.7))),
+    ("C2", 2, dict(max_levels=3, max_coarse_size=50),
+     dict(kind="simplec", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.8), corrector=("jacobi", 1, 0.8))),
+    ("C4", 8, dict(max_levels=3, max_coarse_size=50),
+     dict(kind="uzawa", alpha=0.6, predictor=("jacobi", 2, 0.6), corrector=("jacobi", 1, 0.6))),
+    ("C5", 10, dict(max_levels=4, max_coarse_size=50),
+     dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.8), corrector=("jacobi", 1, 0.8))),
+]
+
+
+@pytest.mark.parametrize("cfg,scale,hkw,skw", LIVE)
+def test_live_oracle_parity(cfg, scale, hkw, skw):
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    assert H.num_levels == len(OH.levels)
+    for l, (lv, olv) in enumerate(zip(H.levels, OH.levels)):
+        for blk in ("K", "B1", "B2", "Cz"):
+            A, R = getattr(lv.op, blk).to_scipy(), getattr(olv.op, blk)
+            assert same_pattern(A, R), (l, blk)
+            assert rel_fro(A, R) <= 1e-12
+        if lv.transfer is not None:
+            np.testing.assert_array_equal(lv.info["u_agg"], olv.info["u_agg"])
+            np.testing.assert_array_equal(lv.info["lam_agg"], olv.info["lam_agg"])
+            assert same_pattern(lv.transfer.P_u.to_scipy(), olv.P_u)
+    v = H.apply(rhs)
+    ref = OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 150, 50)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=150, restart=50))
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)

@@ -1,0 +1,126 @@
+"""CPU tests of the host logic: configuration validation (mirrors the
+reference's tests), generator invariants, host aggregation vs the oracle."""
+
+import sys
+
+import numpy as np
+import pytest
+import scipy.sparse
+
+import camg_oracle as O
+from _golden import GOLDEN, cases, load
+
+from paper_1912_09056_b200.aggregation import NodeGraph, aggregate_greedy, aggregate_lagrange, LagrangeMap
+from paper_1912_09056_b200.errors import ConfigError
+from paper_1912_09056_b200.hierarchy import HierarchyConfig
+from paper_1912_09056_b200.krylov import GmresConfig
+from paper_1912_09056_b200.problem import config_spec, element_stiffness, generate, mortar_1d
+from paper_1912_09056_b200.smoothers import BlockSmootherConfig, PointSmootherConfig
+from paper_1912_09056_b200.sparse import SparseMatrix
+
+sys.path.insert(0, GOLDEN)
+from cases import BY_NAME  # noqa: E402
+
+
+def test_point_config_validation():                 # reference tests/test_smoothers.py:118-124
+    with pytest.raises(ConfigError):
+        PointSmootherConfig(kind="chebyshev")
+    with pytest.raises(ConfigError):
+        PointSmootherConfig(sweeps=0)
+    with pytest.raises(ConfigError):
+        PointSmootherConfig(damping=2.0)
+
+
+def test_block_config_validation():
+    with pytest.raises(ConfigError):
+        BlockSmootherConfig(kind="nope")
+    with pytest.raises(ConfigError):
+        BlockSmootherConfig(alpha=0.0)
+    with pytest.raises(ConfigError):
+        BlockSmootherConfig(kind="braess_sarazin", a_hat_mode="abs_rowsum")
+    assert BlockSmootherConfig(kind="simplec").effective_a_hat_mode() == "abs_rowsum"
+
+
+def test_hierarchy_and_gmres_config_validation():
+    with pytest.raises(ConfigError):
+        HierarchyConfig(max_levels=0)
+    with pytest.raises(ConfigError):
+        HierarchyConfig(coarse_solver="x")
+    with pytest.raises(ConfigError):
+        GmresConfig(rel_tol=1.0)
+    with pytest.raises(ConfigError):
+        GmresConfig(restart=0)
+
+
+def test_sparse_matrix_host_invariants():
+    A = SparseMatrix.from_coo([0, 0, 1, 1], [1, 1, 0, 1], [1.0, 2.0, 1e-301, 4.0], (2, 2))
+    assert A.nnz == 2 and list(A.values) == [3.0, 4.0]
+    with pytest.raises(ValueError):
+        A.values[0] = 1.0
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_element_stiffness_rigid_modes(dim):
+    Ke = element_stiffness(dim, [0.1] * dim, 1.0, 0.3)
+    w = np.linalg.eigvalsh(Ke)
+    assert np.sum(np.abs(w) < 1e-10) == (3 if dim == 2 else 6)
+    assert np.abs(Ke - Ke.T).max() < 1e-15
+
+
+def test_mortar_partition_of_unity():
+    xs, xm = np.linspace(0, 2, 31), np.linspace(0, 2, 33)
+    D, M = mortar_1d(xs, xm)
+    assert np.allclose(D.sum(1), M.sum(1), atol=1e-15)
+    assert abs(D.sum() - 2.0) < 1e-14
+
+
+@pytest.mark.parametrize("name,dim,n_lam", [("C1", 2, 62), ("C3", 3, 11163)])
+def test_config_sizes(name, dim, n_lam):
+    g = generate(config_spec(name, 1 if dim == 2 else 4), assemble_K=(dim == 2))
+    if dim == 2:
+        assert g.n_u == 2048 and g.n_lam == n_lam
+        assert abs(g.K - g.K.T).max() < 1e-15
+
+
+def test_active_set_drawn_before_rhs():
+    g = generate(config_spec("C4", 16))
+    rng = np.random.default_rng(3)
+    act = rng.random(len(g.slave_nodes)) < 0.5
+    np.testing.assert_array_equal(act, g.active)
+    np.testing.assert_array_equal(rng.uniform(-1, 1, g.n_u + g.n_lam), g.rhs)
+
+
+@pytest.mark.parametrize("name", cases())
+def test_native_host_aggregation_matches_reference(name):
+    """C++ greedy / Alg. 1 on the reference node graph == reference aggregates."""
+    z = load(name)
+    ip, ix = z["L0_graph_indptr"], z["L0_graph_indices"]
+    n = len(ip) - 1
+    hkw = BY_NAME[name][3]
+    g = NodeGraph(n, ip, ix, np.zeros(n, dtype=np.int8))
+    ag = aggregate_greedy(g, HierarchyConfig(**hkw).min_agg_size)
+    np.testing.assert_array_equal(ag.node_to_agg, z["L0_u_agg"])
+    _, cfg, scale, *_ = BY_NAME[name]
+    gen = generate(config_spec(cfg, scale))
+    d = gen.dim
+    D = SparseMatrix.from_scipy(gen.mortar_block)
+    lmap = LagrangeMap(gen.slave_dofs.astype(np.int64), np.repeat(gen.slave_nodes, d).astype(np.int64),
+                       np.arange(gen.n_lam, dtype=np.int64) // d)
+    la = aggregate_lagrange(ag, D, lmap)
+    np.testing.assert_array_equal(la.node_to_agg, z["L0_lam_agg"])
+
+
+def test_native_greedy_matches_oracle_random_graphs():
+    rng = np.random.default_rng(5)
+    for t in range(5):
+        n = int(rng.integers(50, 400))
+        A = scipy.sparse.random(n, n, density=4.0 / n, random_state=int(rng.integers(1 << 30)), format="csr")
+        A = A + A.T
+        A.setdiag(0)
+        A.eliminate_zeros()
+        A.sort_indices()
+        for ms in (1, 3, 6):
+            ag = aggregate_greedy(NodeGraph(n, A.indptr, A.indices, np.zeros(n, np.int8)), ms)
+            ref = O.greedy(A.indptr.astype(np.int64), A.indices.astype(np.int64), n, ms)
+            np.testing.assert_array_equal(ag.node_to_agg, ref.node_to_agg)
+            assert ag.singleton_count == ref.singletons
