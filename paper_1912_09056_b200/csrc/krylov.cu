@@ -40,10 +40,10 @@ __global__ void __launch_bounds__(kBlk) k_ortho(const double* __restrict__ V, in
                                                 const double* __restrict__ h, double* __restrict__ w,
                                                 double* __restrict__ part) {
   extern __shared__ double sh[];
-  double* sacc = sh;                 // kWarps x k
-  double* sh_h = sh + kWarps * k;    // k
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nacc = (MODE == 2) ? 1 : k;
+  double* sacc = sh;                 // kWarps x nacc
+  double* sh_h = sh + kWarps * nacc; // k
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kWarps * nacc; i += kBlk) sacc[i] = 0.0;
   if (MODE != 0)
     for (int i = threadIdx.x; i < k; i += kBlk) sh_h[i] = h[i];
