@@ -1,0 +1,444 @@
+"""Benchmark: AMG preconditioner V-cycles/s (+ SpMV GB/s, GMRES time to
+solution) on BASELINE config C5 (3-D frictionless contact, ~23.8M unknowns),
+one B200 per rank.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--scale 1]
+    python bench.py --impl reference ...     # CPU reference arm (oracle port)
+
+One step = one preconditioner application (one V-cycle from zero,
+`Hierarchy.apply`) on the fine-level residual.  Multi-GPU = independent
+replicas (the path does not shard in v1); value = all
+ranks' V-cycles / max-over-ranks time.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+# BASELINE config -> reference-API mapping
+def solver_for(config):
+    from paper_1912_09056_b200.hierarchy import HierarchyConfig
+    from paper_1912_09056_b200.smoothers import BlockSmootherConfig, PointSmootherConfig as P
+
+    table = {
+        "C1": (dict(max_levels=2, max_coarse_size=1),
+               BlockSmootherConfig(kind="uzawa", alpha=1.0, predictor=P("jacobi", 2, 0.6),
+                                   corrector=P("jacobi", 1, 0.6)), 30),
+        "C2": (dict(max_levels=3, max_coarse_size=500),
+               BlockSmootherConfig(kind="simplec", alpha=0.8, outer_sweeps=3, predictor=P("jacobi", 1, 0.8),
+                                   corrector=P("jacobi", 1, 0.8)), 50),
+        "C3": (dict(max_levels=4, max_coarse_size=500),
+               BlockSmootherConfig(kind="braess_sarazin", alpha=1.0 / 0.7, corrector=P("jacobi", 1, 0.7)), 50),
+        "C4": (dict(max_levels=5, max_coarse_size=500),
+               BlockSmootherConfig(kind="uzawa", alpha=0.6, predictor=P("jacobi", 2, 0.6),
+                                   corrector=P("jacobi", 1, 0.6)), 100),
+        "C5": (dict(max_levels=6, max_coarse_size=500),
+               BlockSmootherConfig(kind="uzawa", alpha=1.0, predictor=P("jacobi", 2, 0.6),
+                                   corrector=P("jacobi", 1, 0.6)), 100),
+    }
+    h, s, r = table[config]
+    return HierarchyConfig(**h), s, r
+
+
+def smoother_desc(s):
+    return (f"{s.kind}(alpha={s.alpha:.4g}, outer={s.outer_sweeps}, pred={s.predictor.kind}"
+            f"({s.predictor.sweeps},{s.predictor.damping}), corr={s.corrector.kind}"
+            f"({s.corrector.sweeps},{s.corrector.damping}))")
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+_REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [s[0] for s in self.samples]
+        mx = max(s[1] for s in self.samples)
+        mask = 0
+        for s in self.samples:
+            mask |= s[2]
+        reasons = [name for bit, name in _REASONS.items() if mask & bit and name != "gpu_idle"]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons, "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm / cpu_baseline (oracle port, bounded sample)
+
+
+def vcycle_cost_units(levels):
+    """Work units of one V-cycle: sum over levels of the sparse entries the
+    cycle streams (same structure on CPU and GPU, so the ratio scales a CPU
+    sample to the GPU workload)."""
+    return float(sum(lv["nnz_A"] * lv["streams"] + lv["nnz_P"] + lv["nnz_R"] for lv in levels))
+
+
+def cpu_reference_sample(config, sample_scale, steps, warmup):
+    """Time the oracle V-cycle (scipy, single-threaded sparse kernels) on a
+    coarsened copy of the config.  Returns (seconds per V-cycle, cost units,
+    description)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import camg_oracle as O
+
+    from paper_1912_09056_b200.problem import config_spec, generate
+
+    hcfg, scfg, _ = solver_for(config)
+    g = generate(config_spec(config, sample_scale))
+    op, meta, rhs = O.system_from_generated(g)
+    bc = O.BlockCfg(kind=scfg.kind, alpha=scfg.alpha, outer_sweeps=scfg.outer_sweeps,
+                    predictor=O.PointCfg(scfg.predictor.kind, scfg.predictor.sweeps, scfg.predictor.damping),
+                    corrector=O.PointCfg(scfg.corrector.kind, scfg.corrector.sweeps, scfg.corrector.damping),
+                    a_hat_mode=scfg.a_hat_mode)
+    t0 = time.perf_counter()
+    H = O.setup(op, meta, O.HierCfg(**{k: getattr(hcfg, k) for k in
+                                       ("max_levels", "max_coarse_size", "coarse_solver", "min_agg_size")}), bc)
+    setup_s = time.perf_counter() - t0
+    for _ in range(warmup):
+        H.apply(rhs)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        H.apply(rhs)
+        times.append(time.perf_counter() - t0)
+    lv = []
+    streams = steps_per_level(scfg)
+    for i, l in enumerate(H.levels):
+        A_nnz = l.op.nnz
+        lv.append(dict(nnz_A=A_nnz, streams=streams if i < len(H.levels) - 1 else 0,
+                       nnz_P=(l.P_u.nnz + l.P_lam.nnz) if l.P_u is not None else 0,
+                       nnz_R=(l.R_u.nnz + l.R_lam.nnz) if l.R_u is not None else 0))
+    desc = (f"oracle (numpy/scipy port of the reference) V-cycle on {config}/{sample_scale} "
+            f"(n={op.n}, nnz(K)={op.K.nnz}, {len(H.levels)} levels, setup {setup_s:.1f}s), "
+            f"{steps} timed cycles; scaled to the full config by V-cycle sparse-entry ratio")
+    return float(np.median(times)), vcycle_cost_units(lv), desc
+
+
+def steps_per_level(scfg):
+    """Operator streams per non-coarsest level in one V(1,1) cycle."""
+    sp = 1 if scfg.kind == "braess_sarazin" else scfg.predictor.sweeps
+    per_step = sp  # first predictor sweep fused with the step residual
+    s = scfg.outer_sweeps
+    return max(0, s * per_step - 1) + 1 + s * per_step
+
+
+def gpu_cost_units(H, scfg):
+    lv = []
+    streams = steps_per_level(scfg)
+    for i, l in enumerate(H.levels):
+        last = i == len(H.levels) - 1
+        lv.append(dict(nnz_A=l.op.nnz, streams=0 if last else streams,
+                       nnz_P=0 if last else l.transfer.P_u.nnz + l.transfer.P_lam.nnz,
+                       nnz_R=0 if last else l.transfer.R_u.nnz + l.transfer.R_lam.nnz))
+    return vcycle_cost_units(lv)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps = max(1, args.steps)
+    sample_scale = args.cpu_sample_scale
+    per_cycle, units, desc = cpu_reference_sample(args.config, sample_scale, steps, min(args.warmup, 1))
+    # scale to the full workload by the same cost model the GPU arm reports
+    full_units = estimate_full_units(args.config, args.scale, sample_scale, units)
+    sec_full = per_cycle * full_units / units
+    value = 1.0 / sec_full
+    line = {
+        "impl": "reference",
+        "metric": metric_name(args.config), "value": value, "unit": "V-cycles/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": sec_full * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": "V-cycles/s", "cores": 1, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def estimate_full_units(config, scale, sample_scale, sample_units):
+    """Cost units of the full config from the sample by the nnz(K) ratio of
+    the two meshes (computed from the mesh formulas, no assembly)."""
+    from paper_1912_09056_b200.problem import config_spec
+    def knnz(spec):
+        tot = 0
+        for b in (spec.lower, spec.upper):
+            tot += np.prod([e + 1 for e in b.elems]) * 27 * 9 if spec.dim == 3 else np.prod([e + 1 for e in b.elems]) * 9 * 4
+        return float(tot)
+    return sample_units * knnz(config_spec(config, scale)) / knnz(config_spec(config, sample_scale))
+
+
+def metric_name(config):
+    return f"AMG V-cycles/s (GMRES preconditioner apply), BASELINE {config}, fp64, 1 B200 per rank"
+
+
+def workload_config(args):
+    from paper_1912_09056_b200.problem import config_spec
+    spec = config_spec(args.config, args.scale)
+    hcfg, scfg, restart = solver_for(args.config)
+    return {
+        "workload": f"{args.config}{'' if args.scale == 1 else '/' + str(args.scale)}: 3-D two-block mortar "
+                    f"{spec.coupling}, lower {spec.lower.elems} E={spec.lower.youngs}, upper {spec.upper.elems} "
+                    f"E={spec.upper.youngs}, nu={spec.nu}" if spec.dim == 3 else f"{args.config} 2-D",
+        "hierarchy": {"max_levels": hcfg.max_levels, "max_coarse_size": hcfg.max_coarse_size,
+                      "coarse_solver": hcfg.coarse_solver, "min_agg_size": hcfg.min_agg_size},
+        "smoother": smoother_desc(scfg), "gmres_restart": restart,
+        "l2": "inputs exceed L2 (fine-level operator >> 126 MB); no flush needed",
+        "parallelism": f"replicas x{args.gpus}",
+    }
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1912_09056_b200 import _native as N
+    from paper_1912_09056_b200.hierarchy import fine_level_meta, setup
+    from paper_1912_09056_b200.krylov import GmresConfig, gmres_device
+    from paper_1912_09056_b200.problem import config_spec, generate, saddle_operator
+    from paper_1912_09056_b200.sparse import empty, ptr, stream_ptr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N.require_device()
+
+    t0 = time.perf_counter()
+    g = generate(config_spec(args.config, args.scale), assemble_K=False)
+    op = saddle_operator(g, device_K=True)
+    t_gen = time.perf_counter() - t0
+    meta = fine_level_meta(g)
+    hcfg, scfg, restart = solver_for(args.config)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    H = setup(op, meta, hcfg, scfg)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t0
+    n = H.n
+    rhs = torch.from_numpy(g.rhs).cuda()
+    z = empty(n)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- dominant kernel: fine-level operator stream (merged [K B1; B2 -Cz] SpMV)
+    A0 = H.levels[0].smoother  # noqa: F841
+    Am = op.merged()
+    y = empty(n)
+    for _ in range(3):
+        N.call("camg_spmv", Am.device, 1.0, ptr(rhs), 0.0, ptr(y), stream_ptr())
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(reps):
+        N.call("camg_spmv", Am.device, 1.0, ptr(rhs), 0.0, ptr(y), stream_ptr())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    spmv_ms = e0.elapsed_time(e1) / reps
+    nnzA, nA = Am.nnz, Am.num_rows
+    spmv_bytes = 12.0 * nnzA + 4.0 * (nA + 1) + 8.0 * nA + 8.0 * nA
+    spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
+
+    # ---- V-cycle, device-resident input (the metric)
+    for _ in range(max(3, args.warmup)):
+        H.apply_device(rhs, z)
+    launches_before = N.launch_count()
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            H.apply_device(rhs, z)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = N.launch_count() - launches_before
+    vc_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    total_cycles = args.steps * world
+    value = total_cycles / (vc_ms * 1e-3 * args.steps)
+    kernels_per_cycle = N.kernels_per_apply(H.handle) if hasattr(N, "kernels_per_apply") else None
+    bytes_csr, bytes_fmt = H.vcycle_bytes()
+    vc_gbs = bytes_csr / (vc_ms * 1e-3) / 1e9
+
+    # ---- e2e through the public API with pinned host buffers
+    r_host = torch.from_numpy(g.rhs.copy()).pin_memory()
+    z_host = torch.empty(n, dtype=torch.float64).pin_memory()
+    r_dev = empty(n)
+    for _ in range(2):
+        r_dev.copy_(r_host, non_blocking=True)
+        H.apply_device(r_dev, z)
+        z_host.copy_(z, non_blocking=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        r_dev.copy_(r_host, non_blocking=True)
+        H.apply_device(r_dev, z)
+        z_host.copy_(z, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    e2e_value = total_cycles / (e2e_ms * 1e-3 * args.steps)
+
+    # ---- time to solution (GMRES, rtol 1e-8), outside the timed region
+    solve = None
+    if not args.no_solve:
+        barrier()
+        t0 = time.perf_counter()
+        x, its, conv, hist = gmres_device(Am, H, rhs, GmresConfig(rel_tol=1e-8, max_iters=args.max_iters,
+                                                                  restart=restart))
+        torch.cuda.synchronize()
+        t_solve = time.perf_counter() - t0
+        r = rhs.clone()
+        N.call("camg_spmv", Am.device, -1.0, ptr(x), 1.0, ptr(r), stream_ptr())
+        relres = float(torch.linalg.vector_norm(r) / torch.linalg.vector_norm(rhs))
+        solve = {"gmres_iterations": its, "converged": conv, "true_relres": relres,
+                 "time_to_solution_s": t_solve, "setup_s": t_setup, "generate_s": t_gen,
+                 "setup_breakdown_s": {k: round(v, 3) for k, v in H.timings.items()}}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = peaks()
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        per_cycle, units, desc = cpu_reference_sample(args.config, args.cpu_sample_scale, 2, 1)
+        full_units = gpu_cost_units(H, scfg)
+        cpu_value = 1.0 / (per_cycle * full_units / units)
+        cpu = {"value": cpu_value, "unit": "V-cycles/s", "cores": 1, "kind": "port", "sample": desc}
+
+    levels = [{"n_u": l.op.n_u, "n_lam": l.op.n_lam, "nnz_K": l.op.K.nnz, "nnz_total": l.op.nnz}
+              for l in H.levels]
+    line = {
+        "metric": metric_name(args.config),
+        "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": vc_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config geometry/materials)",
+        "config": dict(workload_config(args), levels=levels, operator_complexity=H.complexity),
+        "roofline": {"bound": "hbm", "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": spmv_gbs / peak, "traffic": None,
+                     "kernel": "fine-level merged-operator SpMV (k_spmv, CSR fp64/int32)",
+                     "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_ms,
+                     "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"},
+        "vcycle_roofline": {"achieved": vc_gbs, "unit": "GB/s", "bytes_per_cycle": bytes_csr,
+                            "frac_of_measured_peak": vc_gbs / peak, "frac_of_8TBs": vc_gbs / 8000.0,
+                            "model": "SURVEY.md §8(d): 12 B/nnz + index/vector terms, zero products skipped"},
+        "spmv": {"GB/s": spmv_gbs, "ms": spmv_ms, "nnz": nnzA},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "path": "Hierarchy.apply_device with pinned-host copies"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "solve": solve,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--cpu-sample-scale", type=int, default=5)
+    ap.add_argument("--max-iters", type=int, default=300)
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -528,6 +528,7 @@ struct Hierarchy {
   std::vector<DBuf<double>> vb, vx0, vx1, vr;
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph = nullptr;
+  int64_t kernels_in_graph = 0;
   bool use_graph = true;
   DBuf<double> in, out;  // level-0 rhs / result buffers used by the graph
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -610,7 +611,10 @@ struct Hierarchy {
     if (!graph) {
       cudaGraph_t g;
       CAMG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t before = g_launches.load();
       run(in.p, out.p, stream);
+      kernels_in_graph = g_launches.load() - before;
+      g_launches.fetch_sub(kernels_in_graph);
       CAMG_CUDA(cudaStreamEndCapture(stream, &g));
       CAMG_CUDA(cudaGraphInstantiate(&graph, g, 0));
       cudaGraphDestroy(g);
@@ -618,7 +622,7 @@ struct Hierarchy {
     CAMG_CUDA(cudaMemcpyAsync(in.p, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
     CAMG_CUDA(cudaEventRecord(ev0, caller));
     CAMG_CUDA(cudaStreamWaitEvent(stream, ev0, 0));
-    note_launch();
+    note_launch((int)kernels_in_graph);
     CAMG_CUDA(cudaGraphLaunch(graph, stream));
     CAMG_CUDA(cudaEventRecord(ev1, stream));
     CAMG_CUDA(cudaStreamWaitEvent(caller, ev1, 0));

@@ -314,29 +314,54 @@ std::vector<int64_t> overflow_rows(const int32_t* dflag, int64_t n) {
   return rows;
 }
 
-// Driver shared by the product and the triple: `launch(fill, global, rows, nrows, caps, scratch, out)`.
-template <class Launch, class GlobalCaps>
-Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, GlobalCaps gcaps, double tol, cudaStream_t s) {
+// Driver shared by the product and the triple:
+// `launch(fill, global, rows, nrows, cap1, cap2, scratch, out)`.
+// Rows whose hash tables overflow shared memory are retried from global
+// scratch with doubling table sizes until every row fits; each row is
+// filled with the table size its count pass succeeded with.
+template <class Launch>
+Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint32_t c2_0, double tol,
+              cudaStream_t s) {
   DBuf<int64_t> cnt(n_rows + 1);
   DBuf<int32_t> ovf(n_rows + 1);
   CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
   OutArgs o{cnt.p, nullptr, nullptr, nullptr, ovf.p, tol};
   if (n_rows) launch(false, false, nullptr, n_rows, 0, 0, nullptr, o);
   CAMG_CUDA(cudaStreamSynchronize(s));
+  CAMG_LAUNCH_CHECK();
   std::vector<int64_t> big = overflow_rows(ovf.p, n_rows);
-  DBuf<int64_t> big_rows(big.size() + 1);
-  uint32_t gc1 = 0, gc2 = 0;
-  int64_t gw = 0;
-  DBuf<char> scratch;
-  if (!big.empty()) {
-    CAMG_CUDA(cudaMemcpy(big_rows.p, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice));
-    gcaps(big, gc1, gc2);
-    const size_t per = (size_t)gc1 * 16 + (size_t)gc2 * 16;
-    const size_t budget = size_t(2) << 30;
-    gw = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>((int64_t)big.size(), (int64_t)(budget / per)));
-    gw = (gw + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
-    scratch = DBuf<char>((size_t)gw * per);
-    launch(false, true, big_rows.p, (int64_t)big.size(), gc1, gc2, scratch.p, o);
+  struct Batch { DBuf<int64_t> rows; int64_t n; uint32_t c1, c2; };
+  std::vector<Batch> batches;
+  uint32_t c1 = c1_0, c2 = c2_0;
+  const size_t budget = size_t(2) << 30;
+  while (!big.empty()) {
+    CAMG_CHECK(c1 <= (1u << 28) && c2 <= (1u << 28), CAMG_ERR_NATIVE, "spgemm: row too large for the hash tables");
+    DBuf<int64_t> rows(big.size() + 1);
+    CAMG_CUDA(cudaMemcpy(rows.p, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice));
+    const size_t per = (size_t)c1 * 16 + (size_t)c2 * 16;
+    int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>((int64_t)big.size(), (int64_t)(budget / per)));
+    warps = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
+    DBuf<char> scratch((size_t)warps * per);
+    CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
+    launch(false, true, rows.p, (int64_t)big.size(), c1, c2, scratch.p, o);
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    CAMG_LAUNCH_CHECK();
+    std::vector<int64_t> still = overflow_rows(ovf.p, n_rows);
+    std::vector<int64_t> done;
+    size_t k = 0;
+    for (int64_t r : big) {
+      while (k < still.size() && still[k] < r) ++k;
+      if (k < still.size() && still[k] == r) continue;
+      done.push_back(r);
+    }
+    if (!done.empty()) {
+      Batch b{DBuf<int64_t>(done.size() + 1), (int64_t)done.size(), c1, c2};
+      CAMG_CUDA(cudaMemcpy(b.rows.p, done.data(), sizeof(int64_t) * done.size(), cudaMemcpyHostToDevice));
+      batches.push_back(std::move(b));
+    }
+    big.swap(still);
+    c1 *= 2;
+    if (c2) c2 *= 2;
   }
   DBuf<int64_t> rp(n_rows + 1);
   exclusive_scan_i64(cnt.p, rp.p, n_rows, s);
@@ -351,10 +376,16 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, GlobalCaps gcaps, d
   C->val = dalloc<double>(nnz);
   C->avg_row = n_rows ? double(nnz) / n_rows : 0.0;
   OutArgs f{nullptr, C->rowptr, C->col, C->val, nullptr, tol};
-  // fill: small rows from shared memory (overflow rows are skipped there and
-  // redone from the global scratch)
+  // fill: small rows from shared memory (overflow rows are skipped there)
   if (n_rows) launch(true, false, nullptr, n_rows, 0, 0, nullptr, f);
-  if (!big.empty()) launch(true, true, big_rows.p, (int64_t)big.size(), gc1, gc2, scratch.p, f);
+  for (auto& b : batches) {
+    const size_t per = (size_t)b.c1 * 16 + (size_t)b.c2 * 16;
+    int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(b.n, (int64_t)(budget / per)));
+    warps = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
+    DBuf<char> scratch((size_t)warps * per);
+    launch(true, true, b.rows.p, b.n, b.c1, b.c2, scratch.p, f);
+    CAMG_CUDA(cudaStreamSynchronize(s));
+  }
   CAMG_CUDA(cudaStreamSynchronize(s));
   CAMG_LAUNCH_CHECK();
   return C;
@@ -375,7 +406,7 @@ Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStrea
     CAMG_CUDA(cudaFuncSetAttribute(k_product<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  auto launch = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t,
+  auto launch = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t c2,
                     char* scratch, OutArgs o) {
     note_launch();
     if (!global) {
@@ -383,39 +414,15 @@ Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStrea
       if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, rows, nrows, kCapProduct, nullptr, o);
       else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, rows, nrows, kCapProduct, nullptr, o);
     } else {
-      // number of warps is fixed by the scratch allocation: scratch.n / (c1*16)
-      int64_t warps = 0;
-      (void)warps;
-      unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, 1 << 20));
+      const size_t per = (size_t)c1 * 16 + (size_t)c2 * 16;
+      int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(nrows, (int64_t)((size_t(2) << 30) / per)));
+      unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
       if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
       else k_product<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
     }
     CAMG_LAUNCH_CHECK();
   };
-  // global path: cap from the largest product count among overflow rows
-  DBuf<int64_t> prods(A->n_rows + 1);
-  auto gcaps = [&](const std::vector<int64_t>& big, uint32_t& c1, uint32_t& c2) {
-    note_launch();
-    k_row_products<<<grid_for(A->n_rows, 256), 256, 0, s>>>(view(A), view(B), prods.p);
-    std::vector<int64_t> h(A->n_rows);
-    CAMG_CUDA(cudaMemcpy(h.data(), prods.p, sizeof(int64_t) * A->n_rows, cudaMemcpyDeviceToHost));
-    int64_t mx = 0;
-    for (int64_t r : big) mx = std::max(mx, h[r]);
-    c1 = pow2_at_least(2 * std::min<int64_t>(mx, B->n_cols) + 64);
-    c2 = 0;
-  };
-  // the global launch uses exactly as many warps as there are scratch slots
-  auto launch_fixed = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t c2,
-                          char* scratch, OutArgs o) {
-    if (!global) return launch(fill, global, rows, nrows, c1, c2, scratch, o);
-    note_launch();
-    int64_t warps = std::min<int64_t>(nrows, std::max<int64_t>(kWarpsPerBlock, (int64_t)((size_t(2) << 30) / ((size_t)c1 * 16))));
-    unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
-    else k_product<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
-    CAMG_LAUNCH_CHECK();
-  };
-  return two_pass(A->n_rows, B->n_cols, launch_fixed, gcaps, tol, s);
+  return two_pass(A->n_rows, B->n_cols, launch, 2 * kCapProduct, 0, tol, s);
 }
 
 Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B, false, kDropTol, s); }
@@ -447,21 +454,7 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
     }
     CAMG_LAUNCH_CHECK();
   };
-  auto gcaps = [&](const std::vector<int64_t>& big, uint32_t& c1, uint32_t& c2) {
-    // RA products bound, and RA-unique x P-row bound for the result
-    DBuf<int64_t> t1(R->n_rows + 1);
-    note_launch();
-    k_row_products<<<grid_for(R->n_rows, 256), 256, 0, s>>>(view(R), view(A), t1.p);
-    std::vector<int64_t> h(R->n_rows);
-    CAMG_CUDA(cudaMemcpy(h.data(), t1.p, sizeof(int64_t) * R->n_rows, cudaMemcpyDeviceToHost));
-    int64_t mx = 0;
-    for (int64_t r : big) mx = std::max(mx, h[r]);
-    c1 = pow2_at_least(2 * std::min<int64_t>(mx, A->n_cols) + 64);
-    c2 = pow2_at_least(2 * P->n_cols + 64);
-    // keep the result table bounded: at most what the RA row can reach
-    c2 = std::min<uint32_t>(c2, pow2_at_least(2 * std::min<int64_t>(mx * 64, P->n_cols) + 64));
-  };
-  return two_pass(R->n_rows, P->n_cols, launch, gcaps, kDropTol, s);
+  return two_pass(R->n_rows, P->n_cols, launch, 2 * kCap1, 2 * kCap2, kDropTol, s);
 }
 
 }  // namespace camg
