@@ -82,6 +82,9 @@ int camg_csr_from_device(int64_t n_rows, int64_t n_cols, int64_t nnz, const int6
 int camg_csr_destroy(camg_csr* A);
 int camg_csr_shape(const camg_csr* A, int64_t* n_rows, int64_t* n_cols, int64_t* nnz);
 int camg_csr_to_host(const camg_csr* A, int64_t* rowptr, int64_t* col, double* val);
+/* attach a block SELL-32 mirror (node blocks of size bs in {2,3,6}) of the
+ * first nrows rows; SpMV / smoother kernels then stream those rows from it */
+int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows);
 /* merged saddle operator [[K, B1], [B2, -Cz]] (saddle.py:58-67) */
 int camg_csr_saddle_merge(const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
                           const camg_csr* Cz, camg_csr** out);
@@ -157,6 +160,11 @@ int camg_csr_alloc(int64_t n_rows, int64_t n_cols, int64_t nnz, camg_csr** out);
 int camg_level_create(const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
                       const camg_csr* Cz, const camg_smoother_cfg* cfg, int pre_sweeps,
                       int post_sweeps, camg_level** out);
+/* same, borrowing an existing merged operator A = [[K,B1],[B2,-Cz]] (the
+ * caller keeps A alive; one copy serves GMRES and the smoother) */
+int camg_level_create_shared(camg_csr* A, const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
+                             const camg_csr* Cz, const camg_smoother_cfg* cfg, int pre_sweeps,
+                             int post_sweeps, camg_level** out);
 int camg_level_destroy(camg_level* L);
 /* S~ of the bound smoother (copy) */
 int camg_level_schur(const camg_level* L, camg_csr** out);

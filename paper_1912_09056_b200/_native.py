@@ -66,7 +66,10 @@ _SIGS = {
     "camg_assemble_stencil": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, i64, i64, vp, vp, i64]),
     "camg_stencil_block_counts": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, vp, P64]),
     "camg_level_create": (C.c_int, [vp, vp, vp, vp, C.POINTER(SmootherCfg), C.c_int, C.c_int, C.POINTER(vp)]),
+    "camg_level_create_shared": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(SmootherCfg), C.c_int, C.c_int,
+                                           C.POINTER(vp)]),
     "camg_level_destroy": (C.c_int, [vp]),
+    "camg_csr_attach_blocks": (C.c_int, [vp, C.c_int, i64]),
     "camg_level_schur": (C.c_int, [vp, C.POINTER(vp)]),
     "camg_level_operator": (C.c_int, [vp, C.POINTER(vp)]),
     "camg_level_set_corrector_lu": (C.c_int, [vp, i64, vp, vp]),

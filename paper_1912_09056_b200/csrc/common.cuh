@@ -13,6 +13,8 @@
 
 namespace camg {
 
+struct Sell;
+
 // ---------------------------------------------------------------------------
 // error handling: every C entry point catches camg::Error and returns its code
 
@@ -107,6 +109,7 @@ struct Csr {
   int32_t* bcol = nullptr;
   double* bval = nullptr;
   double avg_row = 0.0;
+  Sell* sell = nullptr;  // optional block SELL-32 mirror of the leading rows
   ~Csr();
 };
 

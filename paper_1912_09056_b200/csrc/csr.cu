@@ -11,6 +11,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "sell.cuh"
 
 namespace camg {
 
@@ -26,6 +27,7 @@ Csr::~Csr() {
   dfree(browptr);
   dfree(bcol);
   dfree(bval);
+  delete sell;
 }
 
 Csr* csr_alloc(int64_t n_rows, int64_t n_cols, int64_t nnz) {
@@ -119,7 +121,16 @@ void spmv(const Csr* A, double alpha, const double* x, double beta, double* y, c
     vec_scale(A->n_rows, beta, y, s);
     return;
   }
-  spmv_rows(A, 0, A->n_rows, alpha, x, nullptr, A->n_cols, beta, y, s);
+  int64_t row0 = 0;
+  if (A->sell) {
+    SellEpi e;
+    e.y = y;
+    e.alpha = alpha;
+    e.beta = beta;
+    sell_launch(A->sell, 0, false, x, nullptr, -1, e, s);
+    row0 = A->sell->rows();
+  }
+  spmv_rows(A, row0, A->n_rows - row0, alpha, x, nullptr, A->n_cols, beta, y, s);
 }
 
 // ---------------------------------------------------------------------------

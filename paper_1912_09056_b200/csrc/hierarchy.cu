@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "sell.cuh"
 
 namespace camg {
 
@@ -256,6 +257,35 @@ struct LaunchCorr {
   }
 };
 
+
+// residual over rows [row0, row0+nrows): SELL mirror for the rows it covers,
+// CSR for the rest
+static void resid_rows(const Csr* A, int64_t row0, int64_t nrows, const double* xu, const double* xl,
+                       int64_t split, const RowEpi& e, bool zero, cudaStream_t s) {
+  if (A->sell && row0 == 0 && nrows >= A->sell->rows()) {
+    SellEpi se;
+    se.b = e.b; se.x = e.x; se.out_r = e.out_r; se.dscale = e.dscale; se.out_d = e.out_d;
+    se.out_x = e.out_x; se.coef = e.coef;
+    sell_launch(A->sell, 1, zero, xu, xl, split < A->n_cols ? split : -1, se, s);
+    const int64_t done = A->sell->rows();
+    row0 += done;
+    nrows -= done;
+    if (nrows <= 0) return;
+  }
+  dispatch_g<LaunchResid>(A->avg_row, A, row0, nrows, xu, xl, split, e, zero, s);
+}
+
+static void jacobi_rows(const Csr* A, int64_t nu, const double* d, const double* r, const double* dinv, double* dn,
+                        const double* x, double* ox, double coef, cudaStream_t s) {
+  if (A->sell && A->sell->rows() == nu) {
+    SellEpi se;
+    se.d = d; se.r = r; se.dscale = dinv; se.out_d = dn; se.x = x; se.out_x = ox; se.coef = coef;
+    sell_launch(A->sell, 2, false, d, nullptr, nu, se, s);
+    return;
+  }
+  dispatch_g<LaunchJacobi>(A->avg_row, A, nu, d, r, dinv, dn, x, ox, coef, s);
+}
+
 // ---------------------------------------------------------------------------
 // level
 
@@ -264,6 +294,7 @@ struct Level {
   camg_smoother_cfg cfg{};
   int pre = 1, post = 1;
   Csr* A = nullptr;    // merged [[K,B1],[B2,-Cz]]
+  bool owns_A = true;
   Csr* B1 = nullptr;   // copy (interface rows)
   Csr* S = nullptr;    // S~
   DBuf<int64_t> b1_rows;
@@ -279,7 +310,7 @@ struct Level {
   int64_t nnz_top = 0;  // entries of the [K | B1] rows
   // work vectors
   DBuf<double> w_du, w_du2, w_ru, w_rc, w_dl, w_dl2, w_rl, w_tmp;
-  ~Level() { delete A; delete B1; delete S; delete P; delete R; }
+  ~Level() { if (owns_A) delete A; delete B1; delete S; delete P; delete R; }
 
   void alloc_work() {
     w_du = DBuf<double>(n);
@@ -323,15 +354,15 @@ struct Level {
     double* du = w_du.p;
     if (kind == CAMG_BRAESS_SARAZIN) {
       RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
-      dispatch_g<LaunchResid>(A->avg_row, A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+      resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
     } else {
       const double coef = (kind == CAMG_UZAWA) ? alpha : 1.0;
       RowEpi e{b, x, sp > 1 ? w_ru.p : nullptr, dinv_p.p, du, sp == 1 ? xo : nullptr, coef};
-      dispatch_g<LaunchResid>(A->avg_row, A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+      resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
       double* dn = w_du2.p;
       for (int k = 1; k < sp; ++k) {
         const bool last = (k == sp - 1);
-        dispatch_g<LaunchJacobi>(A->avg_row, A, nu, du, w_ru.p, dinv_p.p, dn, x, last ? xo : nullptr, coef, s);
+        jacobi_rows(A, nu, du, w_ru.p, dinv_p.p, dn, x, last ? xo : nullptr, coef, s);
         std::swap(du, dn);
       }
     }
@@ -377,7 +408,7 @@ struct Level {
   // r = b - A x over all rows
   void residual(const double* x, const double* b, double* r, cudaStream_t s) {
     RowEpi e{b, nullptr, r, nullptr, nullptr, nullptr, 0.0};
-    dispatch_g<LaunchResid>(A->avg_row, A, int64_t(0), n, x, (const double*)nullptr, n, e, x == nullptr, s);
+    resid_rows(A, int64_t(0), n, x, (const double*)nullptr, n, e, x == nullptr, s);
   }
 };
 
@@ -396,7 +427,7 @@ static void check_no_zero(const double* d, int64_t n, const char* what) {
 }
 
 Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, const camg_smoother_cfg& cfg, int pre,
-                    int post) {
+                    int post, Csr* A_shared) {
   CAMG_CHECK(cfg.kind >= CAMG_UZAWA && cfg.kind <= CAMG_SIMPLEC, CAMG_ERR_CONFIG, "unknown block smoother kind");
   CAMG_CHECK(cfg.alpha > 0.0, CAMG_ERR_CONFIG, "alpha must be positive");
   CAMG_CHECK(cfg.outer_sweeps >= 1, CAMG_ERR_CONFIG, "outer_sweeps must be >= 1");
@@ -412,7 +443,14 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
   L->nu = K->n_rows;
   L->nl = Cz->n_rows;
   L->n = L->nu + L->nl;
-  L->A = csr_saddle_merge(K, B1, B2, Cz, s);
+  if (A_shared) {
+    CAMG_CHECK(A_shared->n_rows == K->n_rows + Cz->n_rows && A_shared->n_cols == A_shared->n_rows,
+               CAMG_ERR_DIMENSION, "merged operator does not match the blocks");
+    L->A = A_shared;
+    L->owns_A = false;
+  } else {
+    L->A = csr_saddle_merge(K, B1, B2, Cz, s);
+  }
   L->B1 = csr_copy(B1, s);
   L->nnz_top = read_i64(L->A->rowptr + L->nu);
   const int64_t nu = L->nu, nl = L->nl;
@@ -660,7 +698,15 @@ extern "C" {
 
 int camg_level_create(const camg_csr* K, const camg_csr* B1, const camg_csr* B2, const camg_csr* Cz,
                       const camg_smoother_cfg* cfg, int pre_sweeps, int post_sweeps, camg_level** out) {
-  return guarded([&] { *out = new camg_level{level_create(K->m, B1->m, B2->m, Cz->m, *cfg, pre_sweeps, post_sweeps)}; });
+  return guarded([&] { *out = new camg_level{level_create(K->m, B1->m, B2->m, Cz->m, *cfg, pre_sweeps, post_sweeps, nullptr)}; });
+}
+
+int camg_level_create_shared(camg_csr* A, const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
+                             const camg_csr* Cz, const camg_smoother_cfg* cfg, int pre_sweeps, int post_sweeps,
+                             camg_level** out) {
+  return guarded([&] {
+    *out = new camg_level{level_create(K->m, B1->m, B2->m, Cz->m, *cfg, pre_sweeps, post_sweeps, A->m)};
+  });
 }
 
 int camg_level_destroy(camg_level* L) {

@@ -1,0 +1,272 @@
+// Block SELL-32 mirror of the leading rows of a CSR matrix (node blocks of
+// size BS = DOFs per node), used for the fine-level [K | B1] stream.
+//
+// Slice = 32 consecutive block rows, one lane per block row.  Slot k of a
+// slice holds block k of each of its 32 rows: the column index as one int32
+// per lane and the BS*BS values interleaved as [k][e][lane], so every load of
+// the warp is a contiguous 128 B (cols) / 256 B (values) transaction.  Each
+// lane keeps BS independent FMA chains in registers; no shuffles.  Rows
+// shorter than the slice width skip their padding (per-row length byte).
+//
+// Compared with int32 CSR (12 B per non-zero, 193 non-zeros per 3-D node
+// row), a 3x3 block costs 76 B for 9 entries including the exact zeros the
+// CSR drops: 2052 B vs 2316 B per node row (-11%), fully coalesced.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "sell.cuh"
+
+namespace camg {
+
+Sell::~Sell() {
+  dfree(slice_ptr);
+  dfree(len);
+  dfree(bcol);
+  dfree(bval);
+}
+
+namespace {
+
+// number of distinct block columns of block row p (union of its BS rows)
+template <int BS>
+__device__ int merge_blocks(const CsrView& A, int64_t p, int32_t* out, bool write) {
+  int64_t pos[BS], end[BS];
+#pragma unroll
+  for (int r = 0; r < BS; ++r) {
+    pos[r] = A.rowptr[p * BS + r];
+    end[r] = A.rowptr[p * BS + r + 1];
+  }
+  int n = 0;
+  while (true) {
+    int32_t best = INT32_MAX;
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+      if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BS);
+    if (best == INT32_MAX) break;
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+      while (pos[r] < end[r] && A.col[pos[r]] / BS == best) ++pos[r];
+    if (write) out[n] = best;
+    ++n;
+  }
+  return n;
+}
+
+template <int BS>
+__global__ void k_sell_count(CsrView A, int64_t nbr, uint8_t* __restrict__ len, int32_t* __restrict__ overflow) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    int n = merge_blocks<BS>(A, p, nullptr, false);
+    if (n > 255) { atomicExch(overflow, 1); n = 255; }
+    len[p] = (uint8_t)n;
+  }
+}
+
+__global__ void k_slice_width(const uint8_t* __restrict__ len, int64_t nbr, int64_t nslices, int64_t* __restrict__ w) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices; s += (int64_t)gridDim.x * blockDim.x) {
+    int m = 0;
+    for (int l = 0; l < 32; ++l) {
+      int64_t p = s * 32 + l;
+      if (p < nbr) m = max(m, (int)len[p]);
+    }
+    w[s] = m;
+  }
+}
+
+template <int BS>
+__global__ void k_sell_fill(CsrView A, int64_t nbr, const int64_t* __restrict__ slice_ptr,
+                            int32_t* __restrict__ bcol, double* __restrict__ bval) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = p >> 5;
+    const int lane = (int)(p & 31);
+    const int64_t base = slice_ptr[s];       // slot index of slot 0 of this slice
+    const int64_t width = slice_ptr[s + 1] - base;
+    int64_t pos[BS], end[BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) {
+      pos[r] = A.rowptr[p * BS + r];
+      end[r] = A.rowptr[p * BS + r + 1];
+    }
+    int k = 0;
+    while (true) {
+      int32_t best = INT32_MAX;
+#pragma unroll
+      for (int r = 0; r < BS; ++r)
+        if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BS);
+      if (best == INT32_MAX) break;
+      const int64_t slot = base + k;
+      bcol[slot * 32 + lane] = best;
+#pragma unroll
+      for (int r = 0; r < BS; ++r) {
+#pragma unroll
+        for (int c = 0; c < BS; ++c) bval[(slot * (BS * BS) + r * BS + c) * 32 + lane] = 0.0;
+        while (pos[r] < end[r] && A.col[pos[r]] / BS == best) {
+          const int c = A.col[pos[r]] - best * BS;
+          bval[(slot * (BS * BS) + r * BS + c) * 32 + lane] = A.val[pos[r]];
+          ++pos[r];
+        }
+      }
+      ++k;
+    }
+    // padding slots: valid column, zero values (never read: per-row length)
+    for (; k < width; ++k) {
+      const int64_t slot = base + k;
+      bcol[slot * 32 + lane] = 0;
+#pragma unroll
+      for (int e = 0; e < BS * BS; ++e) bval[(slot * (BS * BS) + e) * 32 + lane] = 0.0;
+    }
+  }
+}
+
+template <int BS>
+Sell* build(const Csr* A, int64_t nrows, cudaStream_t s) {
+  const int64_t nbr = nrows / BS;
+  const int64_t nslices = (nbr + 31) / 32;
+  std::unique_ptr<Sell> S(new Sell());
+  S->bs = BS;
+  S->nbr = nbr;
+  S->nslices = nslices;
+  S->split_blocks = 0;
+  S->len = dalloc<uint8_t>(nbr + 1);
+  DBuf<int32_t> ovf(1);
+  CAMG_CUDA(cudaMemset(ovf.p, 0, sizeof(int32_t)));
+  note_launch();
+  k_sell_count<BS><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->len, ovf.p);
+  int32_t h_ovf = 0;
+  CAMG_CUDA(cudaMemcpy(&h_ovf, ovf.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CAMG_CHECK(!h_ovf, CAMG_ERR_ARG, "block row with more than 255 blocks");
+  DBuf<int64_t> w(nslices + 1);
+  note_launch();
+  k_slice_width<<<grid_for(nslices, 256), 256, 0, s>>>(S->len, nbr, nslices, w.p);
+  S->slice_ptr = dalloc<int64_t>(nslices + 1);
+  exclusive_scan_i64(w.p, S->slice_ptr, nslices, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  const int64_t slots = read_i64(S->slice_ptr + nslices);
+  S->slots = slots;
+  S->bcol = dalloc<int32_t>((size_t)slots * 32);
+  S->bval = dalloc<double>((size_t)slots * 32 * BS * BS);
+  note_launch();
+  k_sell_fill<BS><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->bcol, S->bval);
+  CAMG_LAUNCH_CHECK();
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  return S.release();
+}
+
+}  // namespace
+
+Sell* sell_build(const Csr* A, int bs, int64_t nrows, cudaStream_t s) {
+  CAMG_CHECK(nrows % bs == 0 && nrows <= A->n_rows, CAMG_ERR_DIMENSION, "block rows must divide the row range");
+  CAMG_CHECK(A->n_cols % bs == 0, CAMG_ERR_DIMENSION, "block size must divide the column count");
+  switch (bs) {
+    case 2: return build<2>(A, nrows, s);
+    case 3: return build<3>(A, nrows, s);
+    case 6: return build<6>(A, nrows, s);
+    default: throw Error(CAMG_ERR_ARG, "unsupported block size (2, 3, 6)");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SELL row kernels
+
+template <int BS, bool ZERO, bool SPLIT, int MODE>
+__global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __restrict__ xu,
+                                                  const double* __restrict__ xl, int64_t split_blocks,
+                                                  SellEpi e) {
+  // MODE 0: spmv y = alpha*acc + beta*y
+  // MODE 1: residual / fused Jacobi epilogue (RowEpi semantics)
+  // MODE 2: extra Jacobi sweep: d_new = d + dinv*(r - acc), optional x update
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < S.nslices; s += nwarps) {
+    const int64_t p = s * 32 + lane;
+    if (p >= S.nbr) continue;
+    double acc[BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+    if (!ZERO) {
+      const int n = S.len[p];
+      const int64_t base = S.slice_ptr[s];
+      for (int k = 0; k < n; ++k) {
+        const int64_t slot = base + k;
+        const int32_t bc = __ldcs(S.bcol + slot * 32 + lane);
+        const double* xs;
+        if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BS;
+        else xs = xl ? xl + ((int64_t)bc - split_blocks) * BS : nullptr;
+        double xv[BS];
+#pragma unroll
+        for (int c = 0; c < BS; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
+        const double* v = S.bval + slot * (BS * BS) * 32 + lane;
+#pragma unroll
+        for (int r = 0; r < BS; ++r)
+#pragma unroll
+          for (int c = 0; c < BS; ++c) acc[r] = fma(__ldcs(v + (r * BS + c) * 32), xv[c], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < BS; ++r) {
+      const int64_t i = p * BS + r;
+      if (MODE == 0) {
+        e.y[i] = e.beta != 0.0 ? e.alpha * acc[r] + e.beta * e.y[i] : e.alpha * acc[r];
+      } else if (MODE == 1) {
+        const double res = e.b[i] - acc[r];
+        if (e.out_r) e.out_r[i] = res;
+        if (e.dscale) {
+          const double d = e.dscale[i] * res;
+          if (e.out_d) e.out_d[i] = d;
+          if (e.out_x) e.out_x[i] = (ZERO || !e.x) ? e.coef * d : e.x[i] + e.coef * d;
+        }
+      } else {
+        const double dn = e.d[i] + e.dscale[i] * (e.r[i] - acc[r]);
+        e.out_d[i] = dn;
+        if (e.out_x) e.out_x[i] = (e.x ? e.x[i] : 0.0) + e.coef * dn;
+      }
+    }
+  }
+}
+
+template <int BS>
+static void launch_bs(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
+                      const SellEpi& e, cudaStream_t st) {
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->nbr, S->nslices};
+  const unsigned grid = grid_for(S->nslices * 32, 256, int64_t(kNumSMs) * 16);
+  const bool sp = split >= 0;
+  const int64_t sb = sp ? split / BS : 0;
+  note_launch();
+#define CAMG_SELL_LAUNCH(Z, SP, M) k_sell_row<BS, Z, SP, M><<<grid, 256, 0, st>>>(v, xu, xl, sb, e)
+  if (mode == 0) {
+    if (sp) CAMG_SELL_LAUNCH(false, true, 0); else CAMG_SELL_LAUNCH(false, false, 0);
+  } else if (mode == 1) {
+    if (zero) CAMG_SELL_LAUNCH(true, false, 1);
+    else if (sp) CAMG_SELL_LAUNCH(false, true, 1);
+    else CAMG_SELL_LAUNCH(false, false, 1);
+  } else {
+    if (sp) CAMG_SELL_LAUNCH(false, true, 2); else CAMG_SELL_LAUNCH(false, false, 2);
+  }
+#undef CAMG_SELL_LAUNCH
+  CAMG_LAUNCH_CHECK();
+}
+
+void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
+                 const SellEpi& e, cudaStream_t st) {
+  switch (S->bs) {
+    case 2: launch_bs<2>(S, mode, zero, xu, xl, split, e, st); break;
+    case 3: launch_bs<3>(S, mode, zero, xu, xl, split, e, st); break;
+    case 6: launch_bs<6>(S, mode, zero, xu, xl, split, e, st); break;
+    default: throw Error(CAMG_ERR_NATIVE, "bad SELL block size");
+  }
+}
+
+}  // namespace camg
+
+using namespace camg;
+
+extern "C" int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows) {
+  return guarded([&] {
+    Csr* M = A->m;
+    delete M->sell;
+    M->sell = nullptr;
+    if (bs <= 1 || nrows <= 0) return;
+    M->sell = sell_build(M, bs, nrows, 0);
+  });
+}

@@ -1,0 +1,47 @@
+// Block SELL-32 acceleration mirror (see sell.cu).
+#pragma once
+#include "common.cuh"
+
+namespace camg {
+
+struct Sell {
+  int bs = 0;
+  int64_t nbr = 0, nslices = 0, slots = 0, split_blocks = 0;
+  int64_t* slice_ptr = nullptr;  // slot offset of each slice (nslices+1)
+  uint8_t* len = nullptr;        // blocks per block row
+  int32_t* bcol = nullptr;       // [slot][lane]
+  double* bval = nullptr;        // [slot][e][lane]
+  ~Sell();
+  int64_t rows() const { return nbr * bs; }
+};
+
+struct SellView {
+  const int64_t* __restrict__ slice_ptr;
+  const uint8_t* __restrict__ len;
+  const int32_t* __restrict__ bcol;
+  const double* __restrict__ bval;
+  int64_t nbr, nslices;
+};
+
+// epilogue arguments of the three SELL row kernels (modes 0/1/2)
+struct SellEpi {
+  double* y = nullptr;
+  double alpha = 1.0, beta = 0.0;
+  const double* b = nullptr;
+  const double* x = nullptr;
+  double* out_r = nullptr;
+  const double* dscale = nullptr;
+  double* out_d = nullptr;
+  double* out_x = nullptr;
+  double coef = 0.0;
+  const double* d = nullptr;
+  const double* r = nullptr;
+};
+
+Sell* sell_build(const Csr* A, int bs, int64_t nrows, cudaStream_t s);
+// mode 0: spmv, 1: residual (+ fused Jacobi epilogue), 2: extra Jacobi sweep.
+// split < 0: x is one vector (xu); else columns >= split read xl (null = 0).
+void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
+                 const SellEpi& e, cudaStream_t st);
+
+}  // namespace camg

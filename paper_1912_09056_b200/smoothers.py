@@ -195,8 +195,10 @@ class BlockSmoother:
         self.op = op
         ncfg = native_cfg(cfg)
         h = C.c_void_p()
-        N.call("camg_level_create", op.K.device, op.B1.device, op.B2.device, op.Cz.device, C.byref(ncfg),
-               int(pre_sweeps), int(post_sweeps), C.byref(h))
+        # the level borrows the operator's merged matrix (one device copy shared
+        # with GMRES); self.op keeps it alive
+        N.call("camg_level_create_shared", op.merged().device, op.K.device, op.B1.device, op.B2.device,
+               op.Cz.device, C.byref(ncfg), int(pre_sweeps), int(post_sweeps), C.byref(h))
         self._level = _LevelHandle(h)
         self._schur = None
         if cfg.corrector.kind == "direct" and op.n_lam > 0:

@@ -253,3 +253,25 @@ def test_live_oracle_parity(cfg, scale, hkw, skw):
     _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 150, 50)
     x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=150, restart=50))
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+
+
+@pytest.mark.parametrize("cfg,scale,hkw,skw", [LIVE[2], LIVE[3], LIVE[1]])
+def test_sell_block_path_parity(cfg, scale, hkw, skw, monkeypatch):
+    """Force the block SELL-32 mirror on every level that has uniform node
+    blocks and check the V-cycle / GMRES against the oracle."""
+    import paper_1912_09056_b200.hierarchy as hmod
+    monkeypatch.setattr(hmod, "SELL_MIN_ROWS", 0)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    v = H.apply(rhs)
+    ref = OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    y = op.apply_merged(rhs)
+    assert np.linalg.norm(y - A @ rhs) <= 1e-13 * np.linalg.norm(A @ rhs)
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 150, 50)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=150, restart=50))
+    assert abs(rep.iterations - orep.iterations) <= 1
