@@ -47,8 +47,8 @@ def solver_for(config):
                BlockSmootherConfig(kind="uzawa", alpha=0.6, predictor=P("jacobi", 2, 0.6),
                                    corrector=P("jacobi", 1, 0.6)), 100),
         "C5": (dict(max_levels=6, max_coarse_size=500),
-               BlockSmootherConfig(kind="uzawa", alpha=1.0, predictor=P("jacobi", 2, 0.6),
-                                   corrector=P("jacobi", 1, 0.6)), 100),
+               BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=3, predictor=P("jacobi", 2, 0.6),
+                                   corrector=P("mcgs", 1, 1.0)), 100),
     }
     h, s, r = table[config]
     return HierarchyConfig(**h), s, r

@@ -192,12 +192,37 @@ def ilu0_values(A):
     return v
 
 
+def greedy_colors(A):
+    """Greedy colouring of the symmetrised pattern in natural order -- the
+    colouring libcamg uses for its multicolour SGS (GPU-only variant, not in
+    the reference; emulated here to check the GPU elementwise)."""
+    A = scipy.sparse.csr_matrix(A)
+    G = (abs(A) + abs(A.T)).tocsr()
+    G.sort_indices()
+    n = A.shape[0]
+    col = -np.ones(n, dtype=np.int64)
+    for i in range(n):
+        nb = G.indices[G.indptr[i]:G.indptr[i + 1]]
+        used = set(col[nb][col[nb] >= 0].tolist())
+        c = 0
+        while c in used:
+            c += 1
+        col[i] = c
+    return col
+
+
 class Point:
     """Point smoother bound to one matrix (smoothers.py:141-199)."""
 
     def __init__(self, cfg: PointCfg, A):
         self.cfg, self.A = cfg, A
         n = A.shape[0]
+        if cfg.kind == "mcgs":
+            # reference SSOR ("sgs") on the colour-permuted matrix
+            perm = np.argsort(greedy_colors(A), kind="stable")
+            self.perm = perm
+            self.inner = Point(PointCfg("sgs", cfg.sweeps, cfg.damping), canon(A[perm][:, perm]))
+            return
         if cfg.kind in ("jacobi", "sgs"):
             d = A.diagonal()
             if np.any(d == 0.0):
@@ -226,6 +251,11 @@ class Point:
     def smooth(self, x, b):
         x = np.array(x, dtype=np.float64)
         k = self.cfg.kind
+        if k == "mcgs":
+            xp = self.inner.smooth(x[self.perm], np.asarray(b)[self.perm])
+            out = np.empty_like(xp)
+            out[self.perm] = xp
+            return out
         if k == "direct":
             return scipy.linalg.lu_solve(self.lu, b)
         for _ in range(self.cfg.sweeps):

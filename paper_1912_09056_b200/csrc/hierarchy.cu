@@ -119,6 +119,42 @@ __global__ void __launch_bounds__(256) k_corr_jacobi(CsrView S, const double* __
   }
 }
 
+// one colour of a multicolour Gauss-Seidel sweep on S: rows of one colour
+// are mutually uncoupled, so they update in place:
+//   x_i += dinv_i * (b_i - S_i . x)          (dinv = omega / S_ii)
+// Sweeping colours forward then backward is the reference's residual-form
+// SSOR (smoothers.py:155-164, 189-191) applied to the colour-permuted S.
+template <int G, bool ZEROX>
+__global__ void __launch_bounds__(256) k_mcgs_color(CsrView S, const int32_t* __restrict__ rows, int64_t nrows,
+                                                    const double* __restrict__ b, const double* __restrict__ dinv,
+                                                    double* __restrict__ x) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t k = tid / G; k < nrows; k += stride) {
+    const int64_t i = rows[k];
+    double acc = 0.0;
+    if (!ZEROX) {
+      acc = row_dot<G, false>(S, i, x, nullptr, S.n_cols, lane);
+      acc = group_sum<G>(acc, mask);
+    }
+    if (lane == 0) x[i] = (ZEROX ? 0.0 : x[i]) + dinv[i] * (b[i] - acc);
+  }
+}
+
+template <int G>
+struct LaunchMcgs {
+  static void run(const Csr* S, const int32_t* rows, int64_t nrows, const double* b, const double* dinv, double* x,
+                  bool zerox, cudaStream_t s) {
+    if (nrows <= 0) return;
+    unsigned grid = grid_for(nrows * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    if (zerox) k_mcgs_color<G, true><<<grid, 256, 0, s>>>(view(S), rows, nrows, b, dinv, x);
+    else k_mcgs_color<G, false><<<grid, 256, 0, s>>>(view(S), rows, nrows, b, dinv, x);
+  }
+};
+
 // x_out_lam = x_lam + coef*dl
 __global__ void k_lam_update(int64_t nl, const double* __restrict__ xl, const double* __restrict__ dl, double coef,
                              double* __restrict__ out) {
@@ -300,6 +336,9 @@ struct Level {
   DBuf<int64_t> b1_rows;
   int64_t n_b1_rows = 0;
   DBuf<double> dinv_p, ainv, dinv_c;
+  // multicolour Gauss-Seidel corrector: rows grouped by colour
+  std::vector<int64_t> color_ptr;
+  DBuf<int32_t> color_rows;
   // direct corrector
   DBuf<double> corr_lu;
   DBuf<int32_t> corr_piv;
@@ -332,6 +371,21 @@ struct Level {
       size_t sh = nl <= 12288 ? sizeof(double) * nl : 0;
       k_lu_solve<<<1, 1024, sh, s>>>((int)nl, corr_lu.p, corr_piv.p, rc, w_dl.p);
       return w_dl.p;
+    }
+    if (cfg.corr_kind == CAMG_PT_MCGS) {
+      const int nc_ = (int)color_ptr.size() - 1;
+      double* x = w_dl.p;
+      // x = 0, then colour 0 of the first sweep needs no product
+      CAMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nl, s));
+      for (int sw = 0; sw < cfg.corr_sweeps; ++sw) {
+        for (int c = 0; c < nc_; ++c)
+          dispatch_g<LaunchMcgs>(S->avg_row, S, color_rows.p + color_ptr[c], color_ptr[c + 1] - color_ptr[c], rc,
+                                 dinv_c.p, x, sw == 0 && c == 0, s);
+        for (int c = nc_ - 1; c >= 0; --c)
+          dispatch_g<LaunchMcgs>(S->avg_row, S, color_rows.p + color_ptr[c], color_ptr[c + 1] - color_ptr[c], rc,
+                                 dinv_c.p, x, false, s);
+      }
+      return x;
     }
     double* cur = w_dl.p;
     double* nxt = w_dl2.p;
@@ -426,6 +480,45 @@ static void check_no_zero(const double* d, int64_t n, const char* what) {
   if (h != ~0ull) throw Error(CAMG_ERR_SINGULAR, std::string(what) + ": zero diagonal in row " + std::to_string(h));
 }
 
+// greedy colouring of the symmetrised pattern of S in natural row order
+// (host; S~ has n_lam rows), rows grouped by colour in ascending order
+static void greedy_coloring(const Csr* S, std::vector<int64_t>& color_ptr, DBuf<int32_t>& rows_out) {
+  const int64_t n = S->n_rows;
+  std::vector<int64_t> rp(n + 1);
+  std::vector<int32_t> ci(S->nnz);
+  CAMG_CUDA(cudaMemcpy(rp.data(), S->rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+  if (S->nnz) CAMG_CUDA(cudaMemcpy(ci.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
+  // transpose pattern
+  std::vector<int64_t> tp(n + 1, 0);
+  for (int64_t k = 0; k < S->nnz; ++k) tp[ci[k] + 1]++;
+  for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+  std::vector<int32_t> ti(S->nnz);
+  std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) ti[fill[ci[k]]++] = (int32_t)i;
+  std::vector<int32_t> color(n, -1);
+  std::vector<int64_t> mark;
+  int ncol = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    mark.clear();
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) if (color[ci[k]] >= 0) mark.push_back(color[ci[k]]);
+    for (int64_t k = tp[i]; k < tp[i + 1]; ++k) if (color[ti[k]] >= 0) mark.push_back(color[ti[k]]);
+    std::sort(mark.begin(), mark.end());
+    int c = 0;
+    for (int64_t m : mark) { if (m == c) ++c; else if (m > c) break; }
+    color[i] = c;
+    ncol = std::max(ncol, c + 1);
+  }
+  color_ptr.assign(ncol + 1, 0);
+  for (int64_t i = 0; i < n; ++i) color_ptr[color[i] + 1]++;
+  for (int c = 0; c < ncol; ++c) color_ptr[c + 1] += color_ptr[c];
+  std::vector<int32_t> rows(n);
+  std::vector<int64_t> pos(color_ptr.begin(), color_ptr.end() - 1);
+  for (int64_t i = 0; i < n; ++i) rows[pos[color[i]]++] = (int32_t)i;
+  rows_out = DBuf<int32_t>(n + 1);
+  CAMG_CUDA(cudaMemcpy(rows_out.p, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+}
+
 Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, const camg_smoother_cfg& cfg, int pre,
                     int post, Csr* A_shared) {
   CAMG_CHECK(cfg.kind >= CAMG_UZAWA && cfg.kind <= CAMG_SIMPLEC, CAMG_ERR_CONFIG, "unknown block smoother kind");
@@ -433,8 +526,8 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
   CAMG_CHECK(cfg.outer_sweeps >= 1, CAMG_ERR_CONFIG, "outer_sweeps must be >= 1");
   CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI, CAMG_ERR_CONFIG,
              "GPU predictor supports jacobi");
-  CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT, CAMG_ERR_CONFIG,
-             "GPU corrector supports jacobi and direct");
+  CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT || cfg.corr_kind == CAMG_PT_MCGS,
+             CAMG_ERR_CONFIG, "GPU corrector supports jacobi, mcgs and direct");
   cudaStream_t s = 0;
   std::unique_ptr<Level> L(new Level());
   L->cfg = cfg;
@@ -491,7 +584,8 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     }
     L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
   }
-  if (cfg.corr_kind == CAMG_PT_JACOBI && nl > 0) {
+  if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) greedy_coloring(L->S, L->color_ptr, L->color_rows);
+  if ((cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_MCGS) && nl > 0) {
     DBuf<double> dS(nl + 1);
     csr_diagonal(L->S, 0, dS.p, s);
     CAMG_CUDA(cudaDeviceSynchronize());

@@ -7,8 +7,11 @@ reference names, defaults and validation (smoothers.py:29-70).
 
 Inner solves on the GPU: `jacobi` (predictor and corrector) and `direct`
 (corrector, dense LU of S~).  The reference's lexicographic `sgs` / `ilu0`
-are sequential; they are rejected here with ConfigError (the GPU variant
-`mcgs` is compared by convergence only).
+are sequential; they are rejected here with ConfigError.  The GPU variant
+`mcgs` (corrector on S~) is the reference's residual-form SSOR applied to
+S~ with rows renumbered by a greedy colouring: multicolour symmetric
+Gauss-Seidel, compared with the reference SGS by convergence, and
+elementwise with the oracle's emulation of the same colouring.
 """
 
 from __future__ import annotations
@@ -33,13 +36,14 @@ from .sparse import (
     to_device,
 )
 
-POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct")
+POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct", "mcgs")
 BLOCK_KINDS = ("uzawa", "braess_sarazin", "simple", "simplec")
 A_HAT_MODES = ("plain_diag", "abs_rowsum", "exact")
 GPU_POINT_KINDS = ("jacobi", "direct")
+GPU_CORRECTOR_KINDS = ("jacobi", "direct", "mcgs")
 
 _BLOCK_CODE = {"uzawa": 0, "braess_sarazin": 1, "simple": 2, "simplec": 3}
-_POINT_CODE = {"jacobi": 0, "direct": 3}
+_POINT_CODE = {"jacobi": 0, "direct": 3, "mcgs": 5}
 
 
 @dataclass(frozen=True)
@@ -98,8 +102,8 @@ def native_cfg(cfg: BlockSmootherConfig) -> N.SmootherCfg:
         raise ConfigError("a_hat_mode 'exact' (dense K inverse) is not available on the GPU path")
     if cfg.kind != "braess_sarazin" and cfg.predictor.kind != "jacobi":
         raise ConfigError(f"GPU predictor supports {('jacobi',)}, got {cfg.predictor.kind!r}")
-    if cfg.corrector.kind not in GPU_POINT_KINDS:
-        raise ConfigError(f"GPU corrector supports {GPU_POINT_KINDS}, got {cfg.corrector.kind!r}")
+    if cfg.corrector.kind not in GPU_CORRECTOR_KINDS:
+        raise ConfigError(f"GPU corrector supports {GPU_CORRECTOR_KINDS}, got {cfg.corrector.kind!r}")
     return N.SmootherCfg(
         kind=_BLOCK_CODE[cfg.kind], alpha=float(cfg.alpha), outer_sweeps=int(cfg.outer_sweeps),
         a_hat_mode=1 if mode == "abs_rowsum" else 0,

@@ -275,3 +275,28 @@ def test_sell_block_path_parity(cfg, scale, hkw, skw, monkeypatch):
     _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 150, 50)
     x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=150, restart=50))
     assert abs(rep.iterations - orep.iterations) <= 1
+
+
+@pytest.mark.parametrize("cfg,scale,levels", [("C5", 10, 3), ("C4", 8, 3), ("C2", 4, 3)])
+def test_mcgs_corrector_vs_oracle_emulation(cfg, scale, levels):
+    """GPU multicolour SGS corrector == reference SSOR on the colour-permuted
+    S~ (oracle emulation), V-cycle within 1e-10, GMRES its within +-1."""
+    skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 2, 0.6), corrector=("mcgs", 1, 1.0))
+    hkw = dict(max_levels=levels, max_coarse_size=50)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    x0 = np.random.default_rng(0).standard_normal(op.total_rows)
+    out = H.levels[0].smoother.sweep_merged(x0, rhs).cpu().numpy()
+    u, lam = OH.levels[0].smoother.sweep(x0[:op.n_u], x0[op.n_u:], rhs[:op.n_u], rhs[op.n_u:])
+    ref = np.concatenate([u, lam])
+    assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+    v, ref = H.apply(rhs), OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 200, 100)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
+    assert orep.converged and rep.converged
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
