@@ -21,12 +21,17 @@ import sys
 import threading
 import time
 
+import ctypes as C
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# ncu dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per
+# launch, from profiles/ (one `ncu --set full` capture; None until measured)
+TRAFFIC = {}
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 # BASELINE config -> reference-API mapping
@@ -320,6 +325,24 @@ def run_gpu(args):
     nnzA, nA = Am.nnz, Am.num_rows
     spmv_bytes = 12.0 * nnzA + 4.0 * (nA + 1) + 8.0 * nA + 8.0 * nA
     spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
+    fmt = C.c_double()
+    N.call("camg_csr_stream_bytes", Am.device, C.byref(fmt))
+    spmv_fmt_gbs = fmt.value / (spmv_ms * 1e-3) / 1e9
+
+    # ---- dominant kernel of the V-cycle: the fine-level extra Jacobi sweep
+    # (SELL mode 2; 6 of the ~12 fine-level operator passes per cycle)
+    xk = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).cuda()
+    for _ in range(3):
+        H.fine_pass(2, xk, rhs)
+    barrier()
+    e0.record(stream)
+    for _ in range(reps):
+        dom_model, dom_fmt = H.fine_pass(2, xk, rhs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dom_ms = e0.elapsed_time(e1) / reps
+    dom_gbs = dom_model / (dom_ms * 1e-3) / 1e9
+    dom_fmt_gbs = dom_fmt / (dom_ms * 1e-3) / 1e9
 
     # ---- V-cycle, device-resident input (the metric)
     for _ in range(max(3, args.warmup)):
@@ -397,15 +420,21 @@ def run_gpu(args):
         "ms_per_step": vc_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config geometry/materials)",
         "config": dict(workload_config(args), levels=levels, operator_complexity=H.complexity),
-        "roofline": {"bound": "hbm", "achieved": spmv_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": spmv_gbs / peak, "traffic": None,
-                     "kernel": "fine-level merged-operator SpMV (k_spmv, CSR fp64/int32)",
-                     "algorithmic_bytes_per_launch": spmv_bytes, "avg_launch_ms": spmv_ms,
+        "roofline": {"bound": "hbm", "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": dom_gbs / peak, "traffic": TRAFFIC.get(args.config),
+                     "kernel": "k_sell_row<3,3,mode 2>: fine-level extra Jacobi sweep d += D^-1 (r - K d), x update "
+                               "(block SELL-32 [K | B1] stream)",
+                     "algorithmic_bytes_per_launch": dom_model,
+                     "bytes_model": "SURVEY §8(d): 12 B/nnz (int32 CSR) + offsets + 6 vector streams",
+                     "avg_launch_ms": dom_ms,
+                     "achieved_format_bytes": dom_fmt_gbs, "frac_format_bytes": dom_fmt_gbs / peak,
+                     "format_bytes_per_launch": dom_fmt,
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"},
         "vcycle_roofline": {"achieved": vc_gbs, "unit": "GB/s", "bytes_per_cycle": bytes_csr,
                             "frac_of_measured_peak": vc_gbs / peak, "frac_of_8TBs": vc_gbs / 8000.0,
                             "model": "SURVEY.md §8(d): 12 B/nnz + index/vector terms, zero products skipped"},
-        "spmv": {"GB/s": spmv_gbs, "ms": spmv_ms, "nnz": nnzA},
+        "spmv": {"GB/s": spmv_gbs, "GB/s_format_bytes": spmv_fmt_gbs, "ms": spmv_ms, "nnz": nnzA,
+                 "kernel": "merged operator y = A x (SELL-32 [K|B1] rows + CSR [B2 -Cz] rows)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "V-cycles/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "path": "Hierarchy.apply_device with pinned-host copies"},

@@ -85,6 +85,10 @@ int camg_csr_to_host(const camg_csr* A, int64_t* rowptr, int64_t* col, double* v
 /* attach a block SELL-32 mirror (node blocks of size bs in {2,3,6}) of the
  * first nrows rows; SpMV / smoother kernels then stream those rows from it */
 int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows);
+/* same with br x bc blocks over the first ncols_blocked columns */
+int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked);
+/* compulsory bytes of one SpMV pass in the matrix's current format */
+int camg_csr_stream_bytes(const camg_csr* A, double* bytes);
 /* merged saddle operator [[K, B1], [B2, -Cz]] (saddle.py:58-67) */
 int camg_csr_saddle_merge(const camg_csr* K, const camg_csr* B1, const camg_csr* B2,
                           const camg_csr* Cz, camg_csr** out);
@@ -176,6 +180,15 @@ int camg_level_set_corrector_lu(camg_level* L, int64_t n, const double* lu_colma
                                 const int32_t* piv);
 /* segregated transfer (transfer.py:186-188): R = P^T computed on device */
 int camg_level_set_transfer(camg_level* L, const camg_csr* P_u, const camg_csr* P_lam);
+/* block SELL-32 mirrors for the transfers of a level with uniform node
+ * blocks: P rows [0,nu) in bs_fine x bs_coarse blocks over the first
+ * ncoarse_u columns, R = P^T rows [0,ncoarse_u) in bs_coarse x bs_fine blocks */
+int camg_level_block_transfer(camg_level* L, int bs_fine, int bs_coarse, int64_t ncoarse_u);
+/* one fine-level pass of the dominant smoother kernel (mode 1: fused
+ * residual + first Jacobi sweep; mode 2: extra Jacobi sweep) on x, b;
+ * returns its algorithmic bytes (SURVEY §8(d) CSR model, and the format's) */
+int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double* b, void* stream,
+                         double* bytes_csr_model, double* bytes_format);
 /* BlockSmoother.sweep on merged vectors x, b -> out (smoothers.py:316-326) */
 int camg_level_sweep(camg_level* L, const double* x, const double* b, double* out, void* stream);
 

@@ -70,6 +70,10 @@ _SIGS = {
                                            C.POINTER(vp)]),
     "camg_level_destroy": (C.c_int, [vp]),
     "camg_csr_attach_blocks": (C.c_int, [vp, C.c_int, i64]),
+    "camg_csr_attach_rect_blocks": (C.c_int, [vp, C.c_int, C.c_int, i64, i64]),
+    "camg_csr_stream_bytes": (C.c_int, [vp, C.POINTER(f64)]),
+    "camg_level_block_transfer": (C.c_int, [vp, C.c_int, C.c_int, i64]),
+    "camg_level_fine_pass": (C.c_int, [vp, C.c_int, vp, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "camg_level_schur": (C.c_int, [vp, C.POINTER(vp)]),
     "camg_level_operator": (C.c_int, [vp, C.POINTER(vp)]),
     "camg_level_set_corrector_lu": (C.c_int, [vp, i64, vp, vp]),

@@ -844,6 +844,47 @@ int camg_level_set_transfer(camg_level* L, const camg_csr* P_u, const camg_csr* 
   });
 }
 
+int camg_level_block_transfer(camg_level* L, int bs_fine, int bs_coarse, int64_t ncoarse_u) {
+  return guarded([&] {
+    Level* lv = L->L;
+    CAMG_CHECK(lv->P != nullptr, CAMG_ERR_SETUP, "transfer not set");
+    delete lv->P->sell;
+    lv->P->sell = sell_build(lv->P, bs_fine, bs_coarse, lv->nu, ncoarse_u, 0);
+    delete lv->R->sell;
+    lv->R->sell = sell_build(lv->R, bs_coarse, bs_fine, ncoarse_u, lv->nu, 0);
+  });
+}
+
+// one fine-level pass of the dominant smoother kernel (timing / profiling):
+// mode 1 = fused residual + first Jacobi sweep, mode 2 = extra Jacobi sweep
+int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double* b, void* stream,
+                         double* bytes_csr_model, double* bytes_format) {
+  return guarded([&] {
+    Level* lv = L->L;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nu = lv->nu;
+    CAMG_CHECK(lv->dinv_p.p != nullptr, CAMG_ERR_CONFIG, "level has no Jacobi predictor");
+    if (mode == 1) {
+      RowEpi e{b, x, nullptr, lv->dinv_p.p, lv->w_du.p, lv->w_tmp.p, 1.0};
+      resid_rows(lv->A, int64_t(0), nu, x, x + nu, nu, e, false, s);
+    } else {
+      jacobi_rows(lv->A, nu, x, b, lv->dinv_p.p, lv->w_du2.p, x, lv->w_tmp.p, 1.0, s);
+    }
+    CAMG_LAUNCH_CHECK();
+    // §8(d): 12 B per non-zero of the [K | B1] rows + int32 offsets + x read
+    // + 5 (mode 1: b, dinv, x_i, d out, x out) or 6 (mode 2) vector streams
+    const double nv = mode == 1 ? 5.0 : 6.0;
+    const double vec = 8.0 * (double)lv->n + nv * 8.0 * (double)nu;
+    if (bytes_csr_model) *bytes_csr_model = 12.0 * (double)lv->nnz_top + 4.0 * (nu + 1) + vec;
+    if (bytes_format) {
+      if (lv->A->sell && lv->A->sell->rows() == nu)
+        *bytes_format = sell_pass_bytes(lv->A->sell) + vec;
+      else
+        *bytes_format = 12.0 * (double)lv->nnz_top + 8.0 * (nu + 1) + vec;
+    }
+  });
+}
+
 int camg_level_sweep(camg_level* L, const double* x, const double* b, double* out, void* stream) {
   return guarded([&] {
     L->L->sweep(x, b, out, (cudaStream_t)stream);

@@ -1,11 +1,13 @@
-// Block SELL-32 mirror of the leading rows of a CSR matrix (node blocks of
-// size BS = DOFs per node), used for the fine-level [K | B1] stream.
+// Block SELL-32 mirror of the leading rows of a CSR matrix, with BR x BC
+// node blocks (BR = DOFs per row node, BC = DOFs per column node), used for
+// the fine-level [K | B1] stream (3x3 in 3-D) and the transfers (P: 3x6,
+// R: 6x3 with rigid-body coarse spaces).
 //
 // Slice = 32 consecutive block rows, one lane per block row.  Slot k of a
 // slice holds block k of each of its 32 rows: the column index as one int32
-// per lane and the BS*BS values interleaved as [k][e][lane], so every load of
+// per lane and the BR*BC values interleaved as [k][e][lane], so every load of
 // the warp is a contiguous 128 B (cols) / 256 B (values) transaction.  Each
-// lane keeps BS independent FMA chains in registers; no shuffles.  Rows
+// lane keeps BR independent FMA chains in registers; no shuffles.  Rows
 // shorter than the slice width skip their padding (per-row length byte).
 //
 // Compared with int32 CSR (12 B per non-zero, 193 non-zeros per 3-D node
@@ -28,36 +30,38 @@ Sell::~Sell() {
 
 namespace {
 
-// number of distinct block columns of block row p (union of its BS rows)
-template <int BS>
-__device__ int merge_blocks(const CsrView& A, int64_t p, int32_t* out, bool write) {
-  int64_t pos[BS], end[BS];
+// number of distinct block columns of block row p (union of its BR rows);
+// flags entries at or beyond the blocked column range
+template <int BR, int BC>
+__device__ int count_blocks(const CsrView& A, int64_t p, int64_t ncols_blocked, int32_t* overflow) {
+  int64_t pos[BR], end[BR];
 #pragma unroll
-  for (int r = 0; r < BS; ++r) {
-    pos[r] = A.rowptr[p * BS + r];
-    end[r] = A.rowptr[p * BS + r + 1];
+  for (int r = 0; r < BR; ++r) {
+    pos[r] = A.rowptr[p * BR + r];
+    end[r] = A.rowptr[p * BR + r + 1];
+    if (end[r] > pos[r] && A.col[end[r] - 1] >= ncols_blocked) atomicExch(overflow, 1);
   }
   int n = 0;
   while (true) {
     int32_t best = INT32_MAX;
 #pragma unroll
-    for (int r = 0; r < BS; ++r)
-      if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BS);
+    for (int r = 0; r < BR; ++r)
+      if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BC);
     if (best == INT32_MAX) break;
 #pragma unroll
-    for (int r = 0; r < BS; ++r)
-      while (pos[r] < end[r] && A.col[pos[r]] / BS == best) ++pos[r];
-    if (write) out[n] = best;
+    for (int r = 0; r < BR; ++r)
+      while (pos[r] < end[r] && A.col[pos[r]] / BC == best) ++pos[r];
     ++n;
   }
   return n;
 }
 
-template <int BS>
-__global__ void k_sell_count(CsrView A, int64_t nbr, uint8_t* __restrict__ len, int32_t* __restrict__ overflow) {
+template <int BR, int BC>
+__global__ void k_sell_count(CsrView A, int64_t nbr, int64_t ncols_blocked, uint8_t* __restrict__ len,
+                             int32_t* __restrict__ overflow) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
-    int n = merge_blocks<BS>(A, p, nullptr, false);
-    if (n > 255) { atomicExch(overflow, 1); n = 255; }
+    int n = count_blocks<BR, BC>(A, p, ncols_blocked, overflow);
+    if (n > 255) { atomicExch(overflow, 2); n = 255; }
     len[p] = (uint8_t)n;
   }
 }
@@ -73,36 +77,37 @@ __global__ void k_slice_width(const uint8_t* __restrict__ len, int64_t nbr, int6
   }
 }
 
-template <int BS>
+template <int BR, int BC>
 __global__ void k_sell_fill(CsrView A, int64_t nbr, const int64_t* __restrict__ slice_ptr,
                             int32_t* __restrict__ bcol, double* __restrict__ bval) {
+  constexpr int BE = BR * BC;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = p >> 5;
     const int lane = (int)(p & 31);
-    const int64_t base = slice_ptr[s];       // slot index of slot 0 of this slice
+    const int64_t base = slice_ptr[s];
     const int64_t width = slice_ptr[s + 1] - base;
-    int64_t pos[BS], end[BS];
+    int64_t pos[BR], end[BR];
 #pragma unroll
-    for (int r = 0; r < BS; ++r) {
-      pos[r] = A.rowptr[p * BS + r];
-      end[r] = A.rowptr[p * BS + r + 1];
+    for (int r = 0; r < BR; ++r) {
+      pos[r] = A.rowptr[p * BR + r];
+      end[r] = A.rowptr[p * BR + r + 1];
     }
     int k = 0;
     while (true) {
       int32_t best = INT32_MAX;
 #pragma unroll
-      for (int r = 0; r < BS; ++r)
-        if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BS);
+      for (int r = 0; r < BR; ++r)
+        if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BC);
       if (best == INT32_MAX) break;
       const int64_t slot = base + k;
       bcol[slot * 32 + lane] = best;
 #pragma unroll
-      for (int r = 0; r < BS; ++r) {
+      for (int r = 0; r < BR; ++r) {
 #pragma unroll
-        for (int c = 0; c < BS; ++c) bval[(slot * (BS * BS) + r * BS + c) * 32 + lane] = 0.0;
-        while (pos[r] < end[r] && A.col[pos[r]] / BS == best) {
-          const int c = A.col[pos[r]] - best * BS;
-          bval[(slot * (BS * BS) + r * BS + c) * 32 + lane] = A.val[pos[r]];
+        for (int c = 0; c < BC; ++c) bval[(slot * BE + r * BC + c) * 32 + lane] = 0.0;
+        while (pos[r] < end[r] && A.col[pos[r]] / BC == best) {
+          const int c = A.col[pos[r]] - best * BC;
+          bval[(slot * BE + r * BC + c) * 32 + lane] = A.val[pos[r]];
           ++pos[r];
         }
       }
@@ -113,28 +118,29 @@ __global__ void k_sell_fill(CsrView A, int64_t nbr, const int64_t* __restrict__ 
       const int64_t slot = base + k;
       bcol[slot * 32 + lane] = 0;
 #pragma unroll
-      for (int e = 0; e < BS * BS; ++e) bval[(slot * (BS * BS) + e) * 32 + lane] = 0.0;
+      for (int e = 0; e < BE; ++e) bval[(slot * BE + e) * 32 + lane] = 0.0;
     }
   }
 }
 
-template <int BS>
-Sell* build(const Csr* A, int64_t nrows, cudaStream_t s) {
-  const int64_t nbr = nrows / BS;
+template <int BR, int BC>
+Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, cudaStream_t s) {
+  const int64_t nbr = nrows / BR;
   const int64_t nslices = (nbr + 31) / 32;
   std::unique_ptr<Sell> S(new Sell());
-  S->bs = BS;
+  S->br = BR;
+  S->bc = BC;
   S->nbr = nbr;
   S->nslices = nslices;
-  S->split_blocks = 0;
   S->len = dalloc<uint8_t>(nbr + 1);
   DBuf<int32_t> ovf(1);
   CAMG_CUDA(cudaMemset(ovf.p, 0, sizeof(int32_t)));
   note_launch();
-  k_sell_count<BS><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->len, ovf.p);
+  k_sell_count<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, ncols_blocked, S->len, ovf.p);
   int32_t h_ovf = 0;
   CAMG_CUDA(cudaMemcpy(&h_ovf, ovf.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
-  CAMG_CHECK(!h_ovf, CAMG_ERR_ARG, "block row with more than 255 blocks");
+  CAMG_CHECK(h_ovf != 2, CAMG_ERR_ARG, "block row with more than 255 blocks");
+  CAMG_CHECK(h_ovf != 1, CAMG_ERR_ARG, "entries outside the blocked column range");
   DBuf<int64_t> w(nslices + 1);
   note_launch();
   k_slice_width<<<grid_for(nslices, 256), 256, 0, s>>>(S->len, nbr, nslices, w.p);
@@ -144,46 +150,54 @@ Sell* build(const Csr* A, int64_t nrows, cudaStream_t s) {
   const int64_t slots = read_i64(S->slice_ptr + nslices);
   S->slots = slots;
   S->bcol = dalloc<int32_t>((size_t)slots * 32);
-  S->bval = dalloc<double>((size_t)slots * 32 * BS * BS);
+  S->bval = dalloc<double>((size_t)slots * 32 * BR * BC);
   note_launch();
-  k_sell_fill<BS><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->bcol, S->bval);
+  k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->bcol, S->bval);
   CAMG_LAUNCH_CHECK();
   CAMG_CUDA(cudaStreamSynchronize(s));
+  // bytes one pass streams: per row length, slice offsets, and the slots in use
+  std::vector<uint8_t> hl(nbr);
+  CAMG_CUDA(cudaMemcpy(hl.data(), S->len, nbr, cudaMemcpyDeviceToHost));
+  int64_t used = 0;
+  for (uint8_t v : hl) used += v;
+  S->used_blocks = used;
   return S.release();
 }
 
 }  // namespace
 
-Sell* sell_build(const Csr* A, int bs, int64_t nrows, cudaStream_t s) {
-  CAMG_CHECK(nrows % bs == 0 && nrows <= A->n_rows, CAMG_ERR_DIMENSION, "block rows must divide the row range");
-  CAMG_CHECK(A->n_cols % bs == 0, CAMG_ERR_DIMENSION, "block size must divide the column count");
-  switch (bs) {
-    case 2: return build<2>(A, nrows, s);
-    case 3: return build<3>(A, nrows, s);
-    case 6: return build<6>(A, nrows, s);
-    default: throw Error(CAMG_ERR_ARG, "unsupported block size (2, 3, 6)");
-  }
+Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s) {
+  CAMG_CHECK(nrows % br == 0 && nrows <= A->n_rows, CAMG_ERR_DIMENSION, "block rows must divide the row range");
+  CAMG_CHECK(ncols_blocked % bc == 0 && ncols_blocked <= A->n_cols, CAMG_ERR_DIMENSION,
+             "block columns must divide the column range");
+#define CAMG_SELL_CASE(R_, C_) \
+  if (br == R_ && bc == C_) return build<R_, C_>(A, nrows, ncols_blocked, s);
+  CAMG_SELL_CASE(2, 2) CAMG_SELL_CASE(3, 3) CAMG_SELL_CASE(6, 6)
+  CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
+#undef CAMG_SELL_CASE
+  throw Error(CAMG_ERR_ARG, "unsupported block shape");
 }
 
 // ---------------------------------------------------------------------------
 // SELL row kernels
 
-template <int BS, bool ZERO, bool SPLIT, int MODE>
+template <int BR, int BC, bool ZERO, bool SPLIT, int MODE>
 __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
   // MODE 0: spmv y = alpha*acc + beta*y
   // MODE 1: residual / fused Jacobi epilogue (RowEpi semantics)
   // MODE 2: extra Jacobi sweep: d_new = d + dinv*(r - acc), optional x update
+  constexpr int BE = BR * BC;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp; s < S.nslices; s += nwarps) {
     const int64_t p = s * 32 + lane;
     if (p >= S.nbr) continue;
-    double acc[BS];
+    double acc[BR];
 #pragma unroll
-    for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+    for (int r = 0; r < BR; ++r) acc[r] = 0.0;
     if (!ZERO) {
       const int n = S.len[p];
       const int64_t base = S.slice_ptr[s];
@@ -191,24 +205,24 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
         const int64_t slot = base + k;
         const int32_t bc = __ldcs(S.bcol + slot * 32 + lane);
         const double* xs;
-        if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BS;
-        else xs = xl ? xl + ((int64_t)bc - split_blocks) * BS : nullptr;
-        double xv[BS];
+        if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
+        else xs = xl ? xl + ((int64_t)bc - split_blocks) * BC : nullptr;
+        double xv[BC];
 #pragma unroll
-        for (int c = 0; c < BS; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
-        const double* v = S.bval + slot * (BS * BS) * 32 + lane;
+        for (int c = 0; c < BC; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
+        const double* v = S.bval + slot * BE * 32 + lane;
 #pragma unroll
-        for (int r = 0; r < BS; ++r)
+        for (int r = 0; r < BR; ++r)
 #pragma unroll
-          for (int c = 0; c < BS; ++c) acc[r] = fma(__ldcs(v + (r * BS + c) * 32), xv[c], acc[r]);
+          for (int c = 0; c < BC; ++c) acc[r] = fma(__ldcs(v + (r * BC + c) * 32), xv[c], acc[r]);
       }
     }
 #pragma unroll
-    for (int r = 0; r < BS; ++r) {
-      const int64_t i = p * BS + r;
-      if (MODE == 0) {
+    for (int r = 0; r < BR; ++r) {
+      const int64_t i = p * BR + r;
+      if constexpr (MODE == 0) {
         e.y[i] = e.beta != 0.0 ? e.alpha * acc[r] + e.beta * e.y[i] : e.alpha * acc[r];
-      } else if (MODE == 1) {
+      } else if constexpr (MODE == 1) {
         const double res = e.b[i] - acc[r];
         if (e.out_r) e.out_r[i] = res;
         if (e.dscale) {
@@ -225,23 +239,29 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
   }
 }
 
-template <int BS>
-static void launch_bs(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                      const SellEpi& e, cudaStream_t st) {
+template <int BR, int BC>
+static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
+                       const SellEpi& e, cudaStream_t st) {
   SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->nbr, S->nslices};
   const unsigned grid = grid_for(S->nslices * 32, 256, int64_t(kNumSMs) * 16);
   const bool sp = split >= 0;
-  const int64_t sb = sp ? split / BS : 0;
+  const int64_t sb = sp ? split / BC : 0;
   note_launch();
-#define CAMG_SELL_LAUNCH(Z, SP, M) k_sell_row<BS, Z, SP, M><<<grid, 256, 0, st>>>(v, xu, xl, sb, e)
+#define CAMG_SELL_LAUNCH(Z, SP, M) k_sell_row<BR, BC, Z, SP, M><<<grid, 256, 0, st>>>(v, xu, xl, sb, e)
   if (mode == 0) {
     if (sp) CAMG_SELL_LAUNCH(false, true, 0); else CAMG_SELL_LAUNCH(false, false, 0);
-  } else if (mode == 1) {
-    if (zero) CAMG_SELL_LAUNCH(true, false, 1);
-    else if (sp) CAMG_SELL_LAUNCH(false, true, 1);
-    else CAMG_SELL_LAUNCH(false, false, 1);
   } else {
-    if (sp) CAMG_SELL_LAUNCH(false, true, 2); else CAMG_SELL_LAUNCH(false, false, 2);
+    if constexpr (BR == BC) {
+      if (mode == 1) {
+        if (zero) CAMG_SELL_LAUNCH(true, false, 1);
+        else if (sp) CAMG_SELL_LAUNCH(false, true, 1);
+        else CAMG_SELL_LAUNCH(false, false, 1);
+      } else {
+        if (sp) CAMG_SELL_LAUNCH(false, true, 2); else CAMG_SELL_LAUNCH(false, false, 2);
+      }
+    } else {
+      throw Error(CAMG_ERR_NATIVE, "smoother modes need square blocks");
+    }
   }
 #undef CAMG_SELL_LAUNCH
   CAMG_LAUNCH_CHECK();
@@ -249,12 +269,19 @@ static void launch_bs(const Sell* S, int mode, bool zero, const double* xu, cons
 
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                  const SellEpi& e, cudaStream_t st) {
-  switch (S->bs) {
-    case 2: launch_bs<2>(S, mode, zero, xu, xl, split, e, st); break;
-    case 3: launch_bs<3>(S, mode, zero, xu, xl, split, e, st); break;
-    case 6: launch_bs<6>(S, mode, zero, xu, xl, split, e, st); break;
-    default: throw Error(CAMG_ERR_NATIVE, "bad SELL block size");
-  }
+#define CAMG_SELL_CASE(R_, C_) \
+  if (S->br == R_ && S->bc == C_) return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st);
+  CAMG_SELL_CASE(2, 2) CAMG_SELL_CASE(3, 3) CAMG_SELL_CASE(6, 6)
+  CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
+#undef CAMG_SELL_CASE
+  throw Error(CAMG_ERR_NATIVE, "bad SELL block shape");
+}
+
+double sell_pass_bytes(const Sell* S) {
+  // compulsory bytes of one pass: blocks in use (values + column), row
+  // lengths, slice offsets, x read once, y written once
+  const double blk = 8.0 * S->br * S->bc + 4.0;
+  return blk * (double)S->used_blocks + (double)S->nbr + 8.0 * (S->nslices + 1);
 }
 
 }  // namespace camg
@@ -267,6 +294,32 @@ extern "C" int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows) {
     delete M->sell;
     M->sell = nullptr;
     if (bs <= 1 || nrows <= 0) return;
-    M->sell = sell_build(M, bs, nrows, 0);
+    M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0);
+  });
+}
+
+extern "C" int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked) {
+  return guarded([&] {
+    Csr* M = A->m;
+    delete M->sell;
+    M->sell = nullptr;
+    if (br <= 0 || bc <= 0 || nrows <= 0) return;
+    M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0);
+  });
+}
+
+extern "C" int camg_csr_stream_bytes(const camg_csr* A, double* bytes) {
+  return guarded([&] {
+    const Csr* M = A->m;
+    double b = 0.0;
+    int64_t row0 = 0;
+    if (M->sell) {
+      b += sell_pass_bytes(M->sell);
+      row0 = M->sell->rows();
+    }
+    const int64_t tail_nnz = M->nnz - (row0 ? read_i64(M->rowptr + row0) : 0);
+    b += 12.0 * (double)tail_nnz + 8.0 * (double)(M->n_rows - row0 + 1);
+    b += 8.0 * (double)M->n_cols + 8.0 * (double)M->n_rows;  // x read, y written
+    *bytes = b;
   });
 }

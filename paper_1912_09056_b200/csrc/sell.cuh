@@ -5,14 +5,14 @@
 namespace camg {
 
 struct Sell {
-  int bs = 0;
-  int64_t nbr = 0, nslices = 0, slots = 0, split_blocks = 0;
+  int br = 0, bc = 0;             // block rows x block columns
+  int64_t nbr = 0, nslices = 0, slots = 0, used_blocks = 0;
   int64_t* slice_ptr = nullptr;  // slot offset of each slice (nslices+1)
   uint8_t* len = nullptr;        // blocks per block row
   int32_t* bcol = nullptr;       // [slot][lane]
   double* bval = nullptr;        // [slot][e][lane]
   ~Sell();
-  int64_t rows() const { return nbr * bs; }
+  int64_t rows() const { return nbr * br; }
 };
 
 struct SellView {
@@ -38,10 +38,12 @@ struct SellEpi {
   const double* r = nullptr;
 };
 
-Sell* sell_build(const Csr* A, int bs, int64_t nrows, cudaStream_t s);
-// mode 0: spmv, 1: residual (+ fused Jacobi epilogue), 2: extra Jacobi sweep.
-// split < 0: x is one vector (xu); else columns >= split read xl (null = 0).
+Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s);
+// mode 0: spmv, 1: residual (+ fused Jacobi epilogue), 2: extra Jacobi sweep
+// (modes 1/2 need square blocks).  split < 0: x is one vector (xu); else
+// columns >= split read xl (null = 0).
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                  const SellEpi& e, cudaStream_t st);
+double sell_pass_bytes(const Sell* S);
 
 }  // namespace camg
