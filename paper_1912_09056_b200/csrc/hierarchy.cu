@@ -29,8 +29,11 @@ struct RowEpi {
   double* out_r;         // residual (optional)
   const double* dscale;  // d = dscale[i] * r (optional)
   double* out_d;         // (optional)
-  double* out_x;         // x_new[i] = x[i] + coef*d  (optional)
+  double* out_x;         // xmode 0: x[i] + coef*d ; xmode 1: x0 + coef*((x + d) - x0)
   double coef;
+  const double* x0 = nullptr;  // relaxation origin for xmode 1 (null = 0)
+  int xmode = 0;
+  double* out_y = nullptr;     // Jacobi iterate y = x + d (optional)
 };
 
 // r_i = b_i - A_i x for rows [row0, row0+nrows), x split at `split` into
@@ -55,7 +58,17 @@ __global__ void __launch_bounds__(256) k_resid(CsrView A, int64_t row0, int64_t 
       if (e.dscale) {
         const double d = e.dscale[i] * r;
         if (e.out_d) e.out_d[i] = d;
-        if (e.out_x) e.out_x[i] = (ZERO || !e.x) ? e.coef * d : e.x[i] + e.coef * d;
+        const double xi = (ZERO || !e.x) ? 0.0 : e.x[i];
+        const double y = xi + d;
+        if (e.out_y) e.out_y[i] = y;
+        if (e.out_x) {
+          if (e.xmode) {
+            const double o = e.x0 ? e.x0[i] : 0.0;
+            e.out_x[i] = o + e.coef * (y - o);
+          } else {
+            e.out_x[i] = xi + e.coef * d;
+          }
+        }
       }
     }
   }
@@ -301,7 +314,7 @@ static void resid_rows(const Csr* A, int64_t row0, int64_t nrows, const double* 
   if (A->sell && row0 == 0 && nrows >= A->sell->rows()) {
     SellEpi se;
     se.b = e.b; se.x = e.x; se.out_r = e.out_r; se.dscale = e.dscale; se.out_d = e.out_d;
-    se.out_x = e.out_x; se.coef = e.coef;
+    se.out_x = e.out_x; se.coef = e.coef; se.x0 = e.x0; se.xmode = e.xmode; se.out_y = e.out_y;
     sell_launch(A->sell, 1, zero, xu, xl, split < A->n_cols ? split : -1, se, s);
     const int64_t done = A->sell->rows();
     row0 += done;
@@ -405,46 +418,52 @@ struct Level {
     const int kind = cfg.kind;
     const int sp = cfg.pred_sweeps;
     const double alpha = cfg.alpha;
-    double* du = w_du.p;
+    // u-half: the predicted displacement the lambda side is coupled to
+    const double* uh = xo;
     if (kind == CAMG_BRAESS_SARAZIN) {
+      // u_half = u + (A^-1 r_u) / alpha   (smoothers.py:296)
       RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
       resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
     } else {
-      const double coef = (kind == CAMG_UZAWA) ? alpha : 1.0;
-      RowEpi e{b, x, sp > 1 ? w_ru.p : nullptr, dinv_p.p, du, sp == 1 ? xo : nullptr, coef};
-      resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
-      double* dn = w_du2.p;
-      for (int k = 1; k < sp; ++k) {
+      // Jacobi predictor in iterate form: y_0 = u, y_k = y_{k-1} + w D^-1
+      // (b_u - K y_{k-1} - B1 lam) -- the reference's zero-start correction
+      // sweeps on r_u (smoothers.py:186-199, 285-314) with u added back, so
+      // no residual / increment vectors are stored.  Uzawa keeps y_sp for the
+      // lambda side and relaxes u_new = u + alpha (y_sp - u).
+      const double* y = x;
+      double* bufs[2] = {w_du.p, w_du2.p};
+      for (int k = 0; k < sp; ++k) {
         const bool last = (k == sp - 1);
-        jacobi_rows(A, nu, du, w_ru.p, dinv_p.p, dn, x, last ? xo : nullptr, coef, s);
-        std::swap(du, dn);
+        double* dst = bufs[k & 1];
+        RowEpi e{b, y, nullptr, dinv_p.p, nullptr, nullptr, 1.0};
+        if (!last) {
+          e.out_x = dst;
+        } else if (kind == CAMG_UZAWA) {
+          e.out_y = dst;
+          e.out_x = xo;
+          e.x0 = x;
+          e.xmode = 1;
+          e.coef = alpha;
+          uh = dst;
+        } else {
+          e.out_x = xo;
+        }
+        resid_rows(A, int64_t(0), nu, y, xl, nu, e, y == nullptr, s);
+        y = dst;
       }
     }
     if (nl == 0) return;
-    // lambda side
-    if (kind == CAMG_UZAWA) {
-      // r_lam = b_lam - A_bot x
-      const double* rl = b + nu;
-      if (!zero) {
-        RowEpi e{b - 0, nullptr, w_rl.p - nu, nullptr, nullptr, nullptr, 0.0};
-        dispatch_g<LaunchResid>(A->avg_row, A, nu, nl, xu, xl, nu, e, false, s);
-        rl = w_rl.p;
-      }
-      dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, du, (const double*)nullptr, rl, w_rc.p, s);
-      double* dl = corrector(w_rc.p, s);
+    // lambda side: rc = B2 u_half - Cz lam - b_lam = -(b_lam + Cz lam - B2 u_half)
+    dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, s);
+    double* dl = corrector(w_rc.p, s);
+    const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
+    note_launch();
+    k_lam_update<<<grid_for(nl, 256), 256, 0, s>>>(nl, xl, dl, cl, xo + nu);
+    if (kind != CAMG_UZAWA && n_b1_rows) {
+      // u_new = u_half - c A^-1 B1 dlam on the interface rows
+      const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
       note_launch();
-      k_lam_update<<<grid_for(nl, 256), 256, 0, s>>>(nl, xl, dl, alpha, xo + nu);
-    } else {
-      dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, xo, xl, b + nu, w_rc.p, s);
-      double* dl = corrector(w_rc.p, s);
-      const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
-      note_launch();
-      k_lam_update<<<grid_for(nl, 256), 256, 0, s>>>(nl, xl, dl, cl, xo + nu);
-      if (n_b1_rows) {
-        const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
-        note_launch();
-        k_b1_correct<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
-      }
+      k_b1_correct<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
     }
   }
 
@@ -865,15 +884,16 @@ int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double*
     const int64_t nu = lv->nu;
     CAMG_CHECK(lv->dinv_p.p != nullptr, CAMG_ERR_CONFIG, "level has no Jacobi predictor");
     if (mode == 1) {
-      RowEpi e{b, x, nullptr, lv->dinv_p.p, lv->w_du.p, lv->w_tmp.p, 1.0};
+      // the smoother's predictor sweep: y_new = y + w D^-1 (b - [K B1][y; lam])
+      RowEpi e{b, x, nullptr, lv->dinv_p.p, nullptr, lv->w_tmp.p, 1.0};
       resid_rows(lv->A, int64_t(0), nu, x, x + nu, nu, e, false, s);
     } else {
       jacobi_rows(lv->A, nu, x, b, lv->dinv_p.p, lv->w_du2.p, x, lv->w_tmp.p, 1.0, s);
     }
     CAMG_LAUNCH_CHECK();
     // §8(d): 12 B per non-zero of the [K | B1] rows + int32 offsets + x read
-    // + 5 (mode 1: b, dinv, x_i, d out, x out) or 6 (mode 2) vector streams
-    const double nv = mode == 1 ? 5.0 : 6.0;
+    // + 3 (mode 1: b, dinv, y out) or 6 (mode 2) vector streams
+    const double nv = mode == 1 ? 3.0 : 6.0;
     const double vec = 8.0 * (double)lv->n + nv * 8.0 * (double)nu;
     if (bytes_csr_model) *bytes_csr_model = 12.0 * (double)lv->nnz_top + 4.0 * (nu + 1) + vec;
     if (bytes_format) {
@@ -942,11 +962,15 @@ int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, dou
       const double top = (double)L->nnz_top;
       const camg_smoother_cfg& c = L->cfg;
       const int sp = (c.kind == CAMG_BRAESS_SARAZIN) ? 1 : c.pred_sweeps;
-      const double step_top = spm(L->A, L->nu, top) + 8.0 * 3 * L->nu;  // b, dinv, x_out
-      const double step_extra = (sp - 1) * (spm(L->A, L->nu, top) + 8.0 * 4 * L->nu);
-      const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * std::max(0, c.corr_sweeps - 1);
-      const double step = step_top + step_extra + lam;
-      const double step0 = step - 12.0 * top;  // zero start skips K x
+      // one predictor sweep over [K | B1]: matrix + x read + (b, D^-1, y out)
+      const double sweep = spm(L->A, L->nu, top) + 8.0 * 2 * L->nu;
+      // lambda side: B2/Cz rows, corrector sweeps over S~ (MCGS: forward +
+      // backward), interface-row B1 correction, a few lambda vectors
+      const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps : std::max(0, c.corr_sweeps - 1);
+      const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
+                         (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
+      const double step = sp * sweep + lam;
+      const double step0 = step - 12.0 * top - 8.0 * L->n;  // zero start: first sweep reads no matrix / x
       int nsteps_pre = L->pre * c.outer_sweeps, nsteps_post = L->post * c.outer_sweeps;
       if (l == nl - 1) {
         if (H->coarse_solver == CAMG_COARSE_MERGED_LU) total += 8.0 * H->n_coarse * H->n_coarse + 16.0 * H->n_coarse;

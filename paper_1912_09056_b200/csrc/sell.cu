@@ -4,15 +4,20 @@
 // R: 6x3 with rigid-body coarse spaces).
 //
 // Slice = 32 consecutive block rows, one lane per block row.  Slot k of a
-// slice holds block k of each of its 32 rows: the column index as one int32
-// per lane and the BR*BC values interleaved as [k][e][lane], so every load of
-// the warp is a contiguous 128 B (cols) / 256 B (values) transaction.  Each
-// lane keeps BR independent FMA chains in registers; no shuffles.  Rows
-// shorter than the slice width skip their padding (per-row length byte).
+// slice holds block k of each of its 32 rows: one int32 column per lane, and
+// the block values interleaved as [value][lane] so every load of the warp is
+// one contiguous 128 B (columns) / 256 B (values) transaction.  Each lane
+// keeps BR independent FMA chains in registers; no shuffles.  Rows shorter
+// than the slice width skip their padding (per-row length byte).
 //
-// Compared with int32 CSR (12 B per non-zero, 193 non-zeros per 3-D node
-// row), a 3x3 block costs 76 B for 9 entries including the exact zeros the
-// CSR drops: 2052 B vs 2316 B per node row (-11%), fully coalesced.
+// Masked slots: a slot stores only the block positions that are non-zero in
+// at least one lane of its slice (a per-slot bit mask, warp-uniform).
+// Structured-mesh stencils repeat along a slice, so the union equals the
+// exact pattern of interior nodes: a hex8 interior node row has 183 non-zeros
+// in its 27 3x3 blocks, so the slice streams 183*8 + 27*4 = 1572 B per node
+// row instead of 2052 B (full blocks) or 2316 B (int32 CSR of the same
+// matrix).  Unstructured patterns fall back to the union (never worse than
+// full blocks).
 #include <algorithm>
 
 #include "common.cuh"
@@ -26,41 +31,54 @@ Sell::~Sell() {
   dfree(len);
   dfree(bcol);
   dfree(bval);
+  dfree(mask);
+  dfree(voff);
 }
 
 namespace {
 
-// number of distinct block columns of block row p (union of its BR rows);
-// flags entries at or beyond the blocked column range
-template <int BR, int BC>
-__device__ int count_blocks(const CsrView& A, int64_t p, int64_t ncols_blocked, int32_t* overflow) {
+// Walk the distinct block columns of block row p (union over its BR rows);
+// f(k, block_col, pos[]) is called per block with the row cursors positioned
+// at that block's entries.
+template <int BR, int BC, class F>
+__device__ int for_blocks(const CsrView& A, int64_t p, F f) {
   int64_t pos[BR], end[BR];
 #pragma unroll
   for (int r = 0; r < BR; ++r) {
     pos[r] = A.rowptr[p * BR + r];
     end[r] = A.rowptr[p * BR + r + 1];
-    if (end[r] > pos[r] && A.col[end[r] - 1] >= ncols_blocked) atomicExch(overflow, 1);
   }
-  int n = 0;
+  int k = 0;
   while (true) {
     int32_t best = INT32_MAX;
 #pragma unroll
     for (int r = 0; r < BR; ++r)
       if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BC);
     if (best == INT32_MAX) break;
+    uint64_t m = 0;
 #pragma unroll
     for (int r = 0; r < BR; ++r)
-      while (pos[r] < end[r] && A.col[pos[r]] / BC == best) ++pos[r];
-    ++n;
+      while (pos[r] < end[r] && A.col[pos[r]] / BC == best) {
+        const int c = A.col[pos[r]] - best * BC;
+        f(k, best, r, c, A.val[pos[r]]);
+        m |= 1ull << (r * BC + c);
+        ++pos[r];
+      }
+    f(k, best, -1, -1, (double)m);  // end of block k: m = its entry mask
+    ++k;
   }
-  return n;
+  return k;
 }
 
 template <int BR, int BC>
 __global__ void k_sell_count(CsrView A, int64_t nbr, int64_t ncols_blocked, uint8_t* __restrict__ len,
                              int32_t* __restrict__ overflow) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
-    int n = count_blocks<BR, BC>(A, p, ncols_blocked, overflow);
+    for (int r = 0; r < BR; ++r) {
+      const int64_t e = A.rowptr[p * BR + r + 1];
+      if (e > A.rowptr[p * BR + r] && A.col[e - 1] >= ncols_blocked) atomicExch(overflow, 1);
+    }
+    int n = for_blocks<BR, BC>(A, p, [](int, int32_t, int, int, double) {});
     if (n > 255) { atomicExch(overflow, 2); n = 255; }
     len[p] = (uint8_t)n;
   }
@@ -77,54 +95,49 @@ __global__ void k_slice_width(const uint8_t* __restrict__ len, int64_t nbr, int6
   }
 }
 
+// union mask of every slot (masked mode) or all-ones (full blocks)
+template <int BR, int BC>
+__global__ void k_sell_masks(CsrView A, int64_t nbr, const int64_t* __restrict__ slice_ptr,
+                             unsigned long long* __restrict__ mask) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t base = slice_ptr[p >> 5];
+    for_blocks<BR, BC>(A, p, [&](int k, int32_t, int r, int, double m) {
+      if (r < 0) atomicOr(mask + base + k, (unsigned long long)m);
+    });
+  }
+}
+
+__global__ void k_slot_popc(const unsigned long long* __restrict__ mask, int64_t slots, int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < slots; i += (int64_t)gridDim.x * blockDim.x)
+    cnt[i] = __popcll(mask[i]);
+}
+
 template <int BR, int BC>
 __global__ void k_sell_fill(CsrView A, int64_t nbr, const int64_t* __restrict__ slice_ptr,
+                            const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
                             int32_t* __restrict__ bcol, double* __restrict__ bval) {
-  constexpr int BE = BR * BC;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = p >> 5;
     const int lane = (int)(p & 31);
-    const int64_t base = slice_ptr[s];
-    const int64_t width = slice_ptr[s + 1] - base;
-    int64_t pos[BR], end[BR];
-#pragma unroll
-    for (int r = 0; r < BR; ++r) {
-      pos[r] = A.rowptr[p * BR + r];
-      end[r] = A.rowptr[p * BR + r + 1];
-    }
-    int k = 0;
-    while (true) {
-      int32_t best = INT32_MAX;
-#pragma unroll
-      for (int r = 0; r < BR; ++r)
-        if (pos[r] < end[r]) best = min(best, A.col[pos[r]] / BC);
-      if (best == INT32_MAX) break;
+    const int64_t base = slice_ptr[p >> 5];
+    const int64_t width = slice_ptr[(p >> 5) + 1] - base;
+    int n = for_blocks<BR, BC>(A, p, [&](int k, int32_t bc, int r, int c, double v) {
       const int64_t slot = base + k;
-      bcol[slot * 32 + lane] = best;
-#pragma unroll
-      for (int r = 0; r < BR; ++r) {
-#pragma unroll
-        for (int c = 0; c < BC; ++c) bval[(slot * BE + r * BC + c) * 32 + lane] = 0.0;
-        while (pos[r] < end[r] && A.col[pos[r]] / BC == best) {
-          const int c = A.col[pos[r]] - best * BC;
-          bval[(slot * BE + r * BC + c) * 32 + lane] = A.val[pos[r]];
-          ++pos[r];
-        }
+      if (r < 0) {
+        bcol[slot * 32 + lane] = bc;
+        return;
       }
-      ++k;
-    }
-    // padding slots: valid column, zero values (never read: per-row length)
-    for (; k < width; ++k) {
-      const int64_t slot = base + k;
-      bcol[slot * 32 + lane] = 0;
-#pragma unroll
-      for (int e = 0; e < BE; ++e) bval[(slot * BE + e) * 32 + lane] = 0.0;
-    }
+      const int e = r * BC + c;
+      const uint64_t m = mask[slot];
+      const int64_t idx = voff[slot] + __popcll(m & ((1ull << e) - 1ull));
+      bval[idx * 32 + lane] = v;
+    });
+    for (int k = n; k < width; ++k) bcol[(base + k) * 32 + lane] = 0;  // padding (never read)
   }
 }
 
 template <int BR, int BC>
-Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, cudaStream_t s) {
+Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cudaStream_t s) {
+  constexpr int BE = BR * BC;
   const int64_t nbr = nrows / BR;
   const int64_t nslices = (nbr + 31) / 32;
   std::unique_ptr<Sell> S(new Sell());
@@ -149,29 +162,59 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, cudaStream_t s) 
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t slots = read_i64(S->slice_ptr + nslices);
   S->slots = slots;
-  S->bcol = dalloc<int32_t>((size_t)slots * 32);
-  S->bval = dalloc<double>((size_t)slots * 32 * BR * BC);
+  // slot masks and value offsets
+  S->mask = dalloc<unsigned long long>(slots + 1);
+  if (masked) {
+    CAMG_CUDA(cudaMemsetAsync(S->mask, 0, sizeof(unsigned long long) * (slots + 1), s));
+    note_launch();
+    k_sell_masks<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->mask);
+  } else {
+    std::vector<unsigned long long> full(slots + 1, (BE == 64) ? ~0ull : ((1ull << BE) - 1ull));
+    CAMG_CUDA(cudaMemcpy(S->mask, full.data(), sizeof(unsigned long long) * (slots + 1), cudaMemcpyHostToDevice));
+  }
+  DBuf<int64_t> cnt(slots + 1);
   note_launch();
-  k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->bcol, S->bval);
+  k_slot_popc<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, slots, cnt.p);
+  S->voff = dalloc<int64_t>(slots + 1);
+  exclusive_scan_i64(cnt.p, S->voff, slots, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  const int64_t groups = read_i64(S->voff + slots);
+  S->bcol = dalloc<int32_t>((size_t)slots * 32);
+  S->bval = dalloc<double>((size_t)groups * 32);
+  CAMG_CUDA(cudaMemsetAsync(S->bval, 0, sizeof(double) * (size_t)groups * 32, s));
+  note_launch();
+  k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->mask, S->voff, S->bcol,
+                                                         S->bval);
   CAMG_LAUNCH_CHECK();
   CAMG_CUDA(cudaStreamSynchronize(s));
-  // bytes one pass streams: per row length, slice offsets, and the slots in use
-  std::vector<uint8_t> hl(nbr);
+  // compulsory bytes of one pass: for every row, its blocks' stored values and
+  // column (the padding of shorter rows is skipped)
+  std::vector<uint8_t> hl(nbr + 1);
+  std::vector<int64_t> hs(nslices + 1);
+  std::vector<unsigned long long> hm(slots + 1);
   CAMG_CUDA(cudaMemcpy(hl.data(), S->len, nbr, cudaMemcpyDeviceToHost));
+  CAMG_CUDA(cudaMemcpy(hs.data(), S->slice_ptr, sizeof(int64_t) * (nslices + 1), cudaMemcpyDeviceToHost));
+  CAMG_CUDA(cudaMemcpy(hm.data(), S->mask, sizeof(unsigned long long) * (slots + 1), cudaMemcpyDeviceToHost));
+  double bytes = 0.0;
   int64_t used = 0;
-  for (uint8_t v : hl) used += v;
+  for (int64_t p = 0; p < nbr; ++p) {
+    const int64_t base = hs[p >> 5];
+    for (int k = 0; k < hl[p]; ++k) bytes += 8.0 * __builtin_popcountll(hm[base + k]) + 4.0;
+    used += hl[p];
+  }
   S->used_blocks = used;
+  S->pass_bytes = bytes + (double)nbr + 16.0 * (double)(nslices + 1) + 16.0 * (double)slots / 32.0;
   return S.release();
 }
 
 }  // namespace
 
-Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s) {
+Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s, bool masked) {
   CAMG_CHECK(nrows % br == 0 && nrows <= A->n_rows, CAMG_ERR_DIMENSION, "block rows must divide the row range");
   CAMG_CHECK(ncols_blocked % bc == 0 && ncols_blocked <= A->n_cols, CAMG_ERR_DIMENSION,
              "block columns must divide the column range");
 #define CAMG_SELL_CASE(R_, C_) \
-  if (br == R_ && bc == C_) return build<R_, C_>(A, nrows, ncols_blocked, s);
+  if (br == R_ && bc == C_) return build<R_, C_>(A, nrows, ncols_blocked, masked, s);
   CAMG_SELL_CASE(2, 2) CAMG_SELL_CASE(3, 3) CAMG_SELL_CASE(6, 6)
   CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
 #undef CAMG_SELL_CASE
@@ -203,6 +246,8 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
       const int64_t base = S.slice_ptr[s];
       for (int k = 0; k < n; ++k) {
         const int64_t slot = base + k;
+        const uint64_t m = __ldg(S.mask + slot);
+        const double* v = S.bval + __ldg(S.voff + slot) * 32 + lane;
         const int32_t bc = __ldcs(S.bcol + slot * 32 + lane);
         const double* xs;
         if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
@@ -210,11 +255,13 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
         double xv[BC];
 #pragma unroll
         for (int c = 0; c < BC; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
-        const double* v = S.bval + slot * BE * 32 + lane;
 #pragma unroll
-        for (int r = 0; r < BR; ++r)
-#pragma unroll
-          for (int c = 0; c < BC; ++c) acc[r] = fma(__ldcs(v + (r * BC + c) * 32), xv[c], acc[r]);
+        for (int q = 0; q < BE; ++q) {
+          if (m & (1ull << q)) {
+            const int idx = __popcll(m & ((1ull << q) - 1ull));
+            acc[q / BC] = fma(__ldcs(v + idx * 32), xv[q % BC], acc[q / BC]);
+          }
+        }
       }
     }
 #pragma unroll
@@ -228,7 +275,17 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
         if (e.dscale) {
           const double d = e.dscale[i] * res;
           if (e.out_d) e.out_d[i] = d;
-          if (e.out_x) e.out_x[i] = (ZERO || !e.x) ? e.coef * d : e.x[i] + e.coef * d;
+          const double xi = (ZERO || !e.x) ? 0.0 : e.x[i];
+          const double y = xi + d;
+          if (e.out_y) e.out_y[i] = y;
+          if (e.out_x) {
+            if (e.xmode) {
+              const double o = e.x0 ? e.x0[i] : 0.0;
+              e.out_x[i] = o + e.coef * (y - o);
+            } else {
+              e.out_x[i] = xi + e.coef * d;
+            }
+          }
         }
       } else {
         const double dn = e.d[i] + e.dscale[i] * (e.r[i] - acc[r]);
@@ -242,7 +299,7 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st) {
-  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->nbr, S->nslices};
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->nbr, S->nslices};
   const unsigned grid = grid_for(S->nslices * 32, 256, int64_t(kNumSMs) * 16);
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
@@ -277,12 +334,7 @@ void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const dou
   throw Error(CAMG_ERR_NATIVE, "bad SELL block shape");
 }
 
-double sell_pass_bytes(const Sell* S) {
-  // compulsory bytes of one pass: blocks in use (values + column), row
-  // lengths, slice offsets, x read once, y written once
-  const double blk = 8.0 * S->br * S->bc + 4.0;
-  return blk * (double)S->used_blocks + (double)S->nbr + 8.0 * (S->nslices + 1);
-}
+double sell_pass_bytes(const Sell* S) { return S->pass_bytes; }
 
 }  // namespace camg
 
@@ -294,7 +346,7 @@ extern "C" int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows) {
     delete M->sell;
     M->sell = nullptr;
     if (bs <= 1 || nrows <= 0) return;
-    M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0);
+    M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0, true);
   });
 }
 
@@ -304,7 +356,7 @@ extern "C" int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t 
     delete M->sell;
     M->sell = nullptr;
     if (br <= 0 || bc <= 0 || nrows <= 0) return;
-    M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0);
+    M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0, true);
   });
 }
 

@@ -5,12 +5,15 @@
 namespace camg {
 
 struct Sell {
-  int br = 0, bc = 0;             // block rows x block columns
+  int br = 0, bc = 0;                 // block rows x block columns
   int64_t nbr = 0, nslices = 0, slots = 0, used_blocks = 0;
-  int64_t* slice_ptr = nullptr;  // slot offset of each slice (nslices+1)
-  uint8_t* len = nullptr;        // blocks per block row
-  int32_t* bcol = nullptr;       // [slot][lane]
-  double* bval = nullptr;        // [slot][e][lane]
+  double pass_bytes = 0.0;            // compulsory bytes of one pass over the blocks
+  int64_t* slice_ptr = nullptr;       // slot offset of each slice (nslices+1)
+  uint8_t* len = nullptr;             // blocks per block row
+  int32_t* bcol = nullptr;            // [slot][lane]
+  double* bval = nullptr;             // [voff[slot] + rank in mask][lane]
+  unsigned long long* mask = nullptr; // per slot: union of the block patterns of its lanes
+  int64_t* voff = nullptr;            // per slot: offset of its value groups (32 doubles each)
   ~Sell();
   int64_t rows() const { return nbr * br; }
 };
@@ -20,6 +23,8 @@ struct SellView {
   const uint8_t* __restrict__ len;
   const int32_t* __restrict__ bcol;
   const double* __restrict__ bval;
+  const unsigned long long* __restrict__ mask;
+  const int64_t* __restrict__ voff;
   int64_t nbr, nslices;
 };
 
@@ -36,9 +41,13 @@ struct SellEpi {
   double coef = 0.0;
   const double* d = nullptr;
   const double* r = nullptr;
+  const double* x0 = nullptr;  // mode 1, xmode 1: out_x = x0 + coef*((x + d) - x0)
+  int xmode = 0;
+  double* out_y = nullptr;     // mode 1: Jacobi iterate y = x + d
 };
 
-Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s);
+Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s,
+                 bool masked = true);
 // mode 0: spmv, 1: residual (+ fused Jacobi epilogue), 2: extra Jacobi sweep
 // (modes 1/2 need square blocks).  split < 0: x is one vector (xu); else
 // columns >= split read xl (null = 0).
