@@ -156,6 +156,40 @@ __global__ void __launch_bounds__(256) k_mcgs_color(CsrView S, const int32_t* __
   }
 }
 
+// Whole multicolour SSOR sweeps of a small S in one CTA (all colours forward
+// then backward, __syncthreads between colours): replaces 2 x ncolours tiny
+// launches per sweep on the coarse levels.  x lives in shared memory.
+__global__ void __launch_bounds__(1024) k_mcgs_cta(CsrView S, const int32_t* __restrict__ rows,
+                                                   const int64_t* __restrict__ cptr, int ncol, int sweeps,
+                                                   const double* __restrict__ b, const double* __restrict__ dinv,
+                                                   double* __restrict__ xg) {
+  extern __shared__ double xs[];
+  const int64_t n = S.n_rows;
+  constexpr int G = 8;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int grp = threadIdx.x / G, ngrp = blockDim.x / G;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = 0.0;
+  __syncthreads();
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int dir = 0; dir < 2; ++dir) {
+      for (int cc = 0; cc < ncol; ++cc) {
+        const int c = dir == 0 ? cc : ncol - 1 - cc;
+        const int64_t lo = cptr[c], hi = cptr[c + 1];
+        for (int64_t k = lo + grp; k < hi; k += ngrp) {
+          const int64_t i = rows[k];
+          double acc = 0.0;
+          for (int64_t p = S.rowptr[i] + lane; p < S.rowptr[i + 1]; p += G) acc = fma(S.val[p], xs[S.col[p]], acc);
+          acc = group_sum<G>(acc, mask);
+          if (lane == 0) xs[i] = xs[i] + dinv[i] * (b[i] - acc);
+        }
+        __syncthreads();
+      }
+    }
+  }
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xg[i] = xs[i];
+}
+
 template <int G>
 struct LaunchMcgs {
   static void run(const Csr* S, const int32_t* rows, int64_t nrows, const double* b, const double* dinv, double* x,
@@ -351,6 +385,7 @@ struct Level {
   DBuf<double> dinv_p, ainv, dinv_c;
   // multicolour Gauss-Seidel corrector: rows grouped by colour
   std::vector<int64_t> color_ptr;
+  DBuf<int64_t> color_ptr_dev;
   DBuf<int32_t> color_rows;
   // direct corrector
   DBuf<double> corr_lu;
@@ -388,6 +423,18 @@ struct Level {
     if (cfg.corr_kind == CAMG_PT_MCGS) {
       const int nc_ = (int)color_ptr.size() - 1;
       double* x = w_dl.p;
+      if (nl <= kMcgsCtaRows) {
+        static bool attr = false;
+        if (!attr) {
+          CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(double) * kMcgsCtaRows)));
+          attr = true;
+        }
+        note_launch();
+        k_mcgs_cta<<<1, 1024, sizeof(double) * nl, s>>>(view(S), color_rows.p, color_ptr_dev.p, nc_, cfg.corr_sweeps,
+                                                        rc, dinv_c.p, x);
+        return x;
+      }
       // x = 0, then colour 0 of the first sweep needs no product
       CAMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nl, s));
       for (int sw = 0; sw < cfg.corr_sweeps; ++sw) {
@@ -603,7 +650,12 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     }
     L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
   }
-  if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) greedy_coloring(L->S, L->color_ptr, L->color_rows);
+  if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) {
+    greedy_coloring(L->S, L->color_ptr, L->color_rows);
+    L->color_ptr_dev = DBuf<int64_t>(L->color_ptr.size());
+    CAMG_CUDA(cudaMemcpy(L->color_ptr_dev.p, L->color_ptr.data(), sizeof(int64_t) * L->color_ptr.size(),
+                         cudaMemcpyHostToDevice));
+  }
   if ((cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_MCGS) && nl > 0) {
     DBuf<double> dS(nl + 1);
     csr_diagonal(L->S, 0, dS.p, s);
@@ -870,7 +922,11 @@ int camg_level_block_transfer(camg_level* L, int bs_fine, int bs_coarse, int64_t
     delete lv->P->sell;
     lv->P->sell = sell_build(lv->P, bs_fine, bs_coarse, lv->nu, ncoarse_u, 0);
     delete lv->R->sell;
-    lv->R->sell = sell_build(lv->R, bs_coarse, bs_fine, ncoarse_u, lv->nu, 0);
+    lv->R->sell = nullptr;
+    // R has few, long rows: one lane per block row only pays when there are
+    // enough block rows to fill the GPU; otherwise the warp-per-row CSR wins
+    if (ncoarse_u / bs_coarse >= kSellMinBlockRows)
+      lv->R->sell = sell_build(lv->R, bs_coarse, bs_fine, ncoarse_u, lv->nu, 0);
   });
 }
 
