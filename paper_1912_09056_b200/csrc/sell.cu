@@ -19,6 +19,7 @@
 // matrix).  Unstructured patterns fall back to the union (never worse than
 // full blocks).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -232,6 +233,7 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
   // MODE 1: residual / fused Jacobi epilogue (RowEpi semantics)
   // MODE 2: extra Jacobi sweep: d_new = d + dinv*(r - acc), optional x update
   constexpr int BE = BR * BC;
+  constexpr uint64_t kFull = (BE == 64) ? ~0ull : ((1ull << BE) - 1ull);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -255,11 +257,16 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
         double xv[BC];
 #pragma unroll
         for (int c = 0; c < BC; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
+        if (m == kFull) {  // dense slot: fixed offsets, all loads independent
 #pragma unroll
-        for (int q = 0; q < BE; ++q) {
-          if (m & (1ull << q)) {
-            const int idx = __popcll(m & ((1ull << q) - 1ull));
-            acc[q / BC] = fma(__ldcs(v + idx * 32), xv[q % BC], acc[q / BC]);
+          for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
+        } else {           // masked slot: warp-uniform branches, running pointer
+#pragma unroll
+          for (int q = 0; q < BE; ++q) {
+            if (m & (1ull << q)) {
+              acc[q / BC] = fma(__ldcs(v), xv[q % BC], acc[q / BC]);
+              v += 32;
+            }
           }
         }
       }
@@ -346,7 +353,9 @@ extern "C" int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows) {
     delete M->sell;
     M->sell = nullptr;
     if (bs <= 1 || nrows <= 0) return;
-    M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0, true);
+    const char* env = getenv("CAMG_SELL_MASKED");
+    const bool masked = !(env && env[0] == '0');
+    M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0, masked);
   });
 }
 
