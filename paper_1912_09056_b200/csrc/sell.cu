@@ -163,6 +163,7 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t slots = read_i64(S->slice_ptr + nslices);
   S->slots = slots;
+  S->masked = masked;
   // slot masks and value offsets
   S->mask = dalloc<unsigned long long>(slots + 1);
   if (masked) {
@@ -225,7 +226,7 @@ Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_bloc
 // ---------------------------------------------------------------------------
 // SELL row kernels
 
-template <int BR, int BC, bool ZERO, bool SPLIT, int MODE>
+template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED>
 __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
@@ -239,38 +240,60 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp; s < S.nslices; s += nwarps) {
     const int64_t p = s * 32 + lane;
-    if (p >= S.nbr) continue;
+    const bool active = p < S.nbr;
     double acc[BR];
 #pragma unroll
     for (int r = 0; r < BR; ++r) acc[r] = 0.0;
     if (!ZERO) {
-      const int n = S.len[p];
+      const int n = active ? S.len[p] : 0;
       const int64_t base = S.slice_ptr[s];
-      for (int k = 0; k < n; ++k) {
-        const int64_t slot = base + k;
-        const uint64_t m = __ldg(S.mask + slot);
-        const double* v = S.bval + __ldg(S.voff + slot) * 32 + lane;
+      auto load_x = [&](int64_t slot, double* xv) {
         const int32_t bc = __ldcs(S.bcol + slot * 32 + lane);
         const double* xs;
         if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
         else xs = xl ? xl + ((int64_t)bc - split_blocks) * BC : nullptr;
-        double xv[BC];
 #pragma unroll
         for (int c = 0; c < BC; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
-        if (m == kFull) {  // dense slot: fixed offsets, all loads independent
+      };
+      if constexpr (!MASKED) {
+        // full blocks: addresses follow from the slot index alone
+        for (int k = 0; k < n; ++k) {
+          const int64_t slot = base + k;
+          double xv[BC];
+          load_x(slot, xv);
+          const double* v = S.bval + slot * (BE * 32) + lane;
 #pragma unroll
           for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
-        } else {           // masked slot: warp-uniform branches, running pointer
+        }
+      } else {
+        // masked slots: the slice's masks arrive in one coalesced load and
+        // are broadcast by shuffles; the value offset is a running sum
+        const int width = (int)(S.slice_ptr[s + 1] - base);
+        const uint64_t m0 = lane < width ? __ldg(S.mask + base + lane) : 0ull;
+        const uint64_t m1 = lane + 32 < width ? __ldg(S.mask + base + 32 + lane) : 0ull;
+        int64_t voff = __ldg(S.voff + base);
+        for (int k = 0; k < width; ++k) {
+          const uint64_t m = k < 32 ? __shfl_sync(0xffffffffu, m0, k)
+                                    : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.mask + base + k));
+          if (k < n) {
+            double xv[BC];
+            load_x(base + k, xv);
+            const double* v = S.bval + voff * 32 + lane;
+            if (m == kFull) {
 #pragma unroll
-          for (int q = 0; q < BE; ++q) {
-            if (m & (1ull << q)) {
-              acc[q / BC] = fma(__ldcs(v), xv[q % BC], acc[q / BC]);
-              v += 32;
+              for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
+            } else {
+#pragma unroll
+              for (int q = 0; q < BE; ++q)
+                if (m & (1ull << q))
+                  acc[q / BC] = fma(__ldcs(v + __popcll(m & ((1ull << q) - 1ull)) * 32), xv[q % BC], acc[q / BC]);
             }
           }
+          voff += __popcll(m);
         }
       }
     }
+    if (!active) continue;
 #pragma unroll
     for (int r = 0; r < BR; ++r) {
       const int64_t i = p * BR + r;
@@ -311,7 +334,11 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
   note_launch();
-#define CAMG_SELL_LAUNCH(Z, SP, M) k_sell_row<BR, BC, Z, SP, M><<<grid, 256, 0, st>>>(v, xu, xl, sb, e)
+#define CAMG_SELL_LAUNCH(Z, SP, M)                                                   \
+  do {                                                                               \
+    if (S->masked) k_sell_row<BR, BC, Z, SP, M, true><<<grid, 256, 0, st>>>(v, xu, xl, sb, e); \
+    else k_sell_row<BR, BC, Z, SP, M, false><<<grid, 256, 0, st>>>(v, xu, xl, sb, e);          \
+  } while (0)
   if (mode == 0) {
     if (sp) CAMG_SELL_LAUNCH(false, true, 0); else CAMG_SELL_LAUNCH(false, false, 0);
   } else {

@@ -6,6 +6,7 @@ namespace camg {
 
 struct Sell {
   int br = 0, bc = 0;                 // block rows x block columns
+  bool masked = false;                // per-slot union masks (else full blocks)
   int64_t nbr = 0, nslices = 0, slots = 0, used_blocks = 0;
   double pass_bytes = 0.0;            // compulsory bytes of one pass over the blocks
   int64_t* slice_ptr = nullptr;       // slot offset of each slice (nslices+1)
