@@ -381,7 +381,9 @@ extern "C" int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows) {
     M->sell = nullptr;
     if (bs <= 1 || nrows <= 0) return;
     const char* env = getenv("CAMG_SELL_MASKED");
-    const bool masked = !(env && env[0] == '0');
+    // masked slots move 16% fewer bytes on hex8 stencils but measured slower
+    // (issue-bound, scripts/sell_ab.py); full blocks unless asked for
+    const bool masked = env && env[0] == '1';
     M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0, masked);
   });
 }
@@ -392,7 +394,7 @@ extern "C" int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t 
     delete M->sell;
     M->sell = nullptr;
     if (br <= 0 || bc <= 0 || nrows <= 0) return;
-    M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0, true);
+    M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0, false);
   });
 }
 

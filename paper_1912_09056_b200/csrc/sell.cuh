@@ -48,7 +48,7 @@ struct SellEpi {
 };
 
 Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s,
-                 bool masked = true);
+                 bool masked = false);
 // mode 0: spmv, 1: residual (+ fused Jacobi epilogue), 2: extra Jacobi sweep
 // (modes 1/2 need square blocks).  split < 0: x is one vector (xu); else
 // columns >= split read xl (null = 0).
