@@ -59,10 +59,99 @@ __global__ void k_absdiag(double* d, int64_t n) {
     d[i] = fabs(d[i]);
 }
 
+// Uniform node blocks (dof_node = i / bs): node p's neighbours are the
+// distinct col/bs of its bs DOF rows, filtered -- one merge per node, no
+// filtered copy of K and no Galerkin product.
+template <bool FILL>
+__global__ void k_block_graph(CsrView K, int bs, int64_t nn, const int8_t* __restrict__ body,
+                              const double* __restrict__ diag, double eps, int64_t* __restrict__ cnt,
+                              const int64_t* __restrict__ rp, int32_t* __restrict__ out) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nn; p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pos[6], end[6];
+    for (int r = 0; r < bs; ++r) {
+      pos[r] = K.rowptr[p * bs + r];
+      end[r] = K.rowptr[p * bs + r + 1];
+    }
+    int64_t n = 0, o = FILL ? rp[p] : 0;
+    while (true) {
+      int32_t best = INT32_MAX;
+      for (int r = 0; r < bs; ++r)
+        if (pos[r] < end[r]) best = min(best, K.col[pos[r]] / bs);
+      if (best == INT32_MAX) break;
+      bool keep = false;
+      for (int r = 0; r < bs; ++r)
+        while (pos[r] < end[r] && K.col[pos[r]] / bs == best) {
+          const double v = fabs(K.val[pos[r]]);
+          const int64_t i = p * bs + r, j = K.col[pos[r]];
+          keep |= eps > 0.0 ? v > eps * sqrt(diag[i] * diag[j]) : v > 0.0;
+          ++pos[r];
+        }
+      if (keep && best != p && body[best] == body[p]) {
+        if (FILL) out[o + n] = best;
+        ++n;
+      }
+    }
+    if (!FILL) cnt[p] = n;
+  }
+}
+
+static Csr* block_graph(const Csr* K, int bs, int64_t nn, const int8_t* body, const double* diag, double eps) {
+  cudaStream_t s = 0;
+  DBuf<int64_t> cnt(nn + 1);
+  note_launch();
+  k_block_graph<false><<<grid_for(nn, 256), 256>>>(view(K), bs, nn, body, diag, eps, cnt.p, nullptr, nullptr);
+  DBuf<int64_t> rp(nn + 1);
+  exclusive_scan_i64(cnt.p, rp.p, nn, s);
+  CAMG_CUDA(cudaDeviceSynchronize());
+  const int64_t nnz = read_i64(rp.p + nn);
+  Csr* G = new Csr();
+  G->n_rows = nn; G->n_cols = nn; G->nnz = nnz;
+  G->rowptr = rp.release();
+  G->col = dalloc<int32_t>(nnz);
+  G->val = dalloc<double>(nnz);
+  G->avg_row = nn ? double(nnz) / nn : 0.0;
+  CAMG_CUDA(cudaMemset(G->val, 0, sizeof(double) * nnz));
+  note_launch();
+  k_block_graph<true><<<grid_for(nn, 256), 256>>>(view(K), bs, nn, body, diag, eps, nullptr, G->rowptr, G->col);
+  CAMG_LAUNCH_CHECK();
+  CAMG_CUDA(cudaDeviceSynchronize());
+  return G;
+}
+
+__global__ void k_fill_ones(double* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = 1.0;
+}
+
 void node_graph(const Csr* K, const int64_t* dof_node_h, int64_t num_nodes, const int8_t* body_h, double eps,
                 std::vector<int64_t>& indptr, std::vector<int64_t>& indices) {
   cudaStream_t s = 0;
   const int64_t n = K->n_rows;
+  int bs = (num_nodes > 0 && n % num_nodes == 0) ? (int)(n / num_nodes) : 0;
+  if (bs < 1 || bs > 6) bs = 0;
+  for (int64_t i = 0; bs && i < n; ++i)
+    if (dof_node_h[i] != i / bs) bs = 0;
+  if (bs) {
+    DBuf<int8_t> bd(num_nodes + 1);
+    CAMG_CUDA(cudaMemcpy(bd.p, body_h, num_nodes, cudaMemcpyHostToDevice));
+    DBuf<double> diag(n + 1);
+    if (eps > 0.0) {
+      csr_diagonal(K, 0, diag.p, s);
+      note_launch();
+      k_absdiag<<<grid_for(n, 256), 256>>>(diag.p, n);
+    }
+    std::unique_ptr<Csr> G(block_graph(K, bs, num_nodes, bd.p, diag.p, eps));
+    note_launch();
+    k_fill_ones<<<grid_for(G->nnz, 256), 256>>>(G->val, G->nnz);
+    std::unique_ptr<Csr> GT(csr_transpose(G.get(), s));
+    std::unique_ptr<Csr> S(csr_axpby(1.0, G.get(), 1.0, GT.get(), s));
+    indptr.resize(num_nodes + 1);
+    indices.resize(S->nnz);
+    CAMG_CUDA(cudaMemcpy(indptr.data(), S->rowptr, sizeof(int64_t) * (num_nodes + 1), cudaMemcpyDeviceToHost));
+    std::vector<int32_t> c32(S->nnz);
+    if (S->nnz) CAMG_CUDA(cudaMemcpy(c32.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < S->nnz; ++i) indices[i] = c32[i];
+    return;
+  }
   DBuf<int64_t> dn(n + 1);
   DBuf<int8_t> bd(num_nodes + 1);
   CAMG_CUDA(cudaMemcpy(dn.p, dof_node_h, sizeof(int64_t) * n, cudaMemcpyHostToDevice));

@@ -8,6 +8,7 @@
 // per iteration:  h1 = V^T w ;  w -= V h1 fused with h2 = V^T w ;
 // w -= V h2 fused with ||w||^2.  One host synchronisation per iteration.
 #include <cmath>
+#include <memory>
 #include <vector>
 
 #include "common.cuh"
@@ -188,7 +189,14 @@ void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rt
   CAMG_CHECK(restart >= 1 && max_iters >= 1, CAMG_ERR_CONFIG, "restart and max_iters must be >= 1");
   const int64_t n = A->n_rows;
   const int mmax = std::min(restart, max_iters);
-  Gmres G(n, mmax);
+  // the Krylov basis (n x (m+1), 19 GB at C5) is allocated once and reused
+  // by later solves of the same size on this thread
+  static thread_local std::unique_ptr<Gmres> cache;
+  if (!cache || cache->n != n || cache->m != mmax) {
+    cache.reset();
+    cache.reset(new Gmres(n, mmax));
+  }
+  Gmres& G = *cache;
   CAMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
   const double norm_b = G.norm(b, s);
   hist[0] = norm_b;

@@ -134,7 +134,8 @@ __device__ int count_kept(const Hash& h, int lane, double tol) {
 // ---------------------------------------------------------------------------
 // C = A*B for one row: returns false on overflow
 
-__device__ bool row_product(const CsrView& A, const CsrView& B, int64_t row, bool reverse_a, Hash h,
+__device__ bool row_product(const CsrView& A, const CsrView& B, int64_t row, bool reverse_a,
+                            const double* __restrict__ scale_a, Hash h,
                             int lane, uint32_t limit) {
   hash_clear(h, lane);
   const int64_t s = A.rowptr[row], e = A.rowptr[row + 1];
@@ -142,7 +143,11 @@ __device__ bool row_product(const CsrView& A, const CsrView& B, int64_t row, boo
   for (int64_t q = 0; q < e - s; ++q) {
     const int64_t jj = reverse_a ? (e - 1 - q) : (s + q);
     const int32_t j = A.col[jj];
-    const double v = A.val[jj];
+    double v = A.val[jj];
+    if (scale_a) {  // (diag(s) A)_ij exactly as scipy's A.multiply(s[:,None]); canon drops |v| < 1e-300
+      v = __dmul_rn(v, scale_a[row]);
+      if (fabs(v) < kDropTol) continue;
+    }
     const int64_t bs = B.rowptr[j], be = B.rowptr[j + 1];
     for (int64_t base = bs; base < be; base += 32) {
       if (count + 32 > limit) return false;
@@ -242,7 +247,8 @@ __device__ void emit(Hash h, int64_t row, int lane, const OutArgs& o) {
 }
 
 template <bool FILL, bool GLOBAL>
-__global__ void k_product(CsrView A, CsrView B, bool reverse_a, const int64_t* __restrict__ rows, int64_t nrows,
+__global__ void k_product(CsrView A, CsrView B, bool reverse_a, const double* __restrict__ scale_a,
+                          const int64_t* __restrict__ rows, int64_t nrows,
                           uint32_t cap, char* __restrict__ gscratch, OutArgs o) {
   extern __shared__ __align__(16) char smem[];
   const int lane = threadIdx.x & 31;
@@ -253,7 +259,7 @@ __global__ void k_product(CsrView A, CsrView B, bool reverse_a, const int64_t* _
   Hash h{reinterpret_cast<int32_t*>(base + (size_t)cap * 8), nullptr, reinterpret_cast<double*>(base), cap};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
-    bool ok = row_product(A, B, row, reverse_a, h, lane, (cap * 3) / 4);
+    bool ok = row_product(A, B, row, reverse_a, scale_a, h, lane, (cap * 3) / 4);
     if (!ok) {
       if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
       continue;
@@ -396,7 +402,7 @@ constexpr uint32_t kCap1 = 2048, kCap2 = 512;
 
 }  // namespace
 
-Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s) {
+Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s, const double* scale_a) {
   CAMG_CHECK(A->n_cols == B->n_rows, CAMG_ERR_DIMENSION, "sp_matmul: inner dimensions differ");
   CAMG_CHECK(B->n_cols < INT32_MAX, CAMG_ERR_DIMENSION, "too many columns");
   const size_t smem = (size_t)kWarpsPerBlock * kCapProduct * 16;
@@ -411,21 +417,21 @@ Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStrea
     note_launch();
     if (!global) {
       unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 8);
-      if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, rows, nrows, kCapProduct, nullptr, o);
-      else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, rows, nrows, kCapProduct, nullptr, o);
+      if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, kCapProduct, nullptr, o);
+      else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, kCapProduct, nullptr, o);
     } else {
       const size_t per = (size_t)c1 * 16 + (size_t)c2 * 16;
       int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(nrows, (int64_t)((size_t(2) << 30) / per)));
       unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
-      if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
-      else k_product<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, rows, nrows, c1, scratch, o);
+      if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, c1, scratch, o);
+      else k_product<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, c1, scratch, o);
     }
     CAMG_LAUNCH_CHECK();
   };
   return two_pass(A->n_rows, B->n_cols, launch, 2 * kCapProduct, 0, tol, s);
 }
 
-Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B, false, kDropTol, s); }
+Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B, false, kDropTol, s, nullptr); }
 
 Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
   CAMG_CHECK(R->n_cols == A->n_rows && A->n_cols == P->n_rows, CAMG_ERR_DIMENSION,
@@ -462,7 +468,7 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
 using namespace camg;
 
 namespace camg {
-Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s);
+Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s, const double* scale_a);
 void recip(int64_t n, const double* d, double* out, cudaStream_t s);
 Csr* scale_cols(const Csr* A, const double* c, cudaStream_t s);
 
@@ -472,9 +478,9 @@ Csr* smooth_prolongator(const Csr* Pt, const Csr* A, const double* d, double ome
              "smooth_prolongator: A and P_tent dimensions mismatch");
   DBuf<double> dinv(A->n_rows + 1);
   recip(A->n_rows, d, dinv.p, s);
-  Csr* DA = csr_scale_rows(A, dinv.p, s);       // from_scipy(A.multiply(1/d)) : canonical
-  Csr* X = spgemm_ex(DA, Pt, false, 0.0, s);    // raw csr_matmat: exact zeros dropped
-  delete DA;
+  // X = (D^-1 A) P_tent as raw csr_matmat (exact zeros dropped); the row
+  // scaling happens on the fly, bit-identical to materialising D^-1 A
+  Csr* X = spgemm_ex(A, Pt, false, 0.0, s, dinv.p);
   Csr* P = csr_axpby(1.0, Pt, -omega_eff, X, s);  // P_tent - omega*X, canonical
   delete X;
   return P;
@@ -486,7 +492,7 @@ Csr* schur(const Csr* B2, const Csr* Cz, const Csr* B1, const double* ainv, doub
   // reverse first-touch order, i.e. B2's row reversed -> the next product
   // walks it backwards.
   Csr* T = scale_cols(B2, ainv, s);
-  Csr* X = spgemm_ex(T, B1, true, 0.0, s);
+  Csr* X = spgemm_ex(T, B1, true, 0.0, s, nullptr);
   delete T;
   Csr* S = csr_axpby(scale, Cz, scale, X, s);
   delete X;
