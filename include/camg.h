@@ -128,12 +128,12 @@ int camg_schur(const camg_csr* B2, const camg_csr* Cz, const camg_csr* B1, const
 
 /* ---- aggregation (host integer work, aggregation.py) --------------------- */
 /* node graph of K with cross-body and |v| <= eps*sqrt(|kii kjj|) entries
- * dropped (aggregation.py:127-145, :47-63).  dof_node must be
- * non-decreasing.  Output arrays are malloc'ed host arrays (free with
- * camg_free_host).                                                           */
+ * dropped, symmetrised (aggregation.py:127-145, :47-63), returned as a device
+ * pattern matrix (fetch with camg_pattern_to_host).                          */
 int camg_node_graph(const camg_csr* K, const int64_t* dof_node, int64_t num_nodes,
-                    const int8_t* node_body, double eps_drop, int64_t** indptr,
-                    int64_t** indices);
+                    const int8_t* node_body, double eps_drop, camg_csr** graph, int64_t* nnz);
+/* sparsity pattern of a device matrix into host int64 arrays (n_rows+1, nnz) */
+int camg_pattern_to_host(const camg_csr* A, int64_t* indptr, int64_t* indices);
 void camg_free_host(void* p);
 /* three-phase greedy aggregation (aggregation.py:186-258), host */
 int camg_aggregate_greedy(int64_t n, const int64_t* indptr, const int64_t* indices,
@@ -147,6 +147,14 @@ int camg_aggregate_lagrange(const int64_t* disp_node_to_agg, int64_t n_rows,
                             const int64_t* row_node, const int64_t* lm_node_of_lm_dof,
                             int64_t n_lm_dofs, int64_t* lam_node_to_agg, int64_t* num_aggs,
                             int64_t* roots, int64_t* overlaps);
+
+/* tentative prolongator CSR from host QR factors (transfer.py:86-145):
+ * groups of aggregates with equal DOF count M; meta[6*g] = {G, M, kk, dof_off,
+ * q_off, agg_off}; dofs[dof_off + a*M + i] = DOF i of aggregate a of the
+ * group, Q[q_off + (a*M + i)*kk + c], rank/col0 per aggregate (group order).  */
+int camg_tentative_csr(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta,
+                       const int64_t* dofs, int64_t ndofs_total, const double* Q, int64_t nq,
+                       const int64_t* rank, const int64_t* col0, int64_t naggs, camg_csr** out);
 
 /* ---- problem generator (device stiffness assembly from a stencil table) -- */
 /* table: [27 types][noff][dim][dim] fp64 host; one call per block           */

@@ -59,10 +59,12 @@ _SIGS = {
     "camg_vec_scale_div": (C.c_int, [i64, vp, f64, vp, vp]),
     "camg_smooth_prolongator": (C.c_int, [vp, vp, vp, f64, C.POINTER(vp)]),
     "camg_schur": (C.c_int, [vp, vp, vp, vp, f64, C.POINTER(vp)]),
-    "camg_node_graph": (C.c_int, [vp, vp, i64, vp, f64, C.POINTER(P64), C.POINTER(P64)]),
+    "camg_node_graph": (C.c_int, [vp, vp, i64, vp, f64, C.POINTER(vp), P64]),
+    "camg_pattern_to_host": (C.c_int, [vp, vp, vp]),
     "camg_free_host": (None, [vp]),
     "camg_aggregate_greedy": (C.c_int, [i64, vp, vp, i64, vp, P64, vp, P64]),
     "camg_aggregate_lagrange": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp, i64, vp, P64, vp, P64]),
+    "camg_tentative_csr": (C.c_int, [i64, i64, i64, vp, vp, i64, vp, i64, vp, vp, i64, C.POINTER(vp)]),
     "camg_assemble_stencil": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, i64, i64, vp, vp, i64]),
     "camg_stencil_block_counts": (C.c_int, [C.c_int, vp, C.c_int, C.c_int, vp, P64]),
     "camg_level_create": (C.c_int, [vp, vp, vp, vp, C.POINTER(SmootherCfg), C.c_int, C.c_int, C.POINTER(vp)]),

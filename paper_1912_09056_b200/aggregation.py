@@ -102,18 +102,16 @@ def filtered_node_graph(K: SparseMatrix, dof_node, num_nodes, node_body, interfa
     if len(dof_node) != K.num_rows:
         raise DimensionError("dof->node map length does not match K")
     body = np.ascontiguousarray(node_body, dtype=np.int8)
-    ip = C.POINTER(C.c_int64)()
-    ix = C.POINTER(C.c_int64)()
+    h, nnz = C.c_void_p(), C.c_int64()
     N.call("camg_node_graph", K.device, _p(dof_node), int(num_nodes), _p(body), float(eps_drop),
-           C.byref(ip), C.byref(ix))
+           C.byref(h), C.byref(nnz))
     try:
-        indptr = np.ctypeslib.as_array(ip, shape=(int(num_nodes) + 1,)).copy()
-        nnz = int(indptr[-1])
-        indices = np.ctypeslib.as_array(ix, shape=(max(nnz, 1),))[:nnz].copy()
+        indptr = np.empty(int(num_nodes) + 1, dtype=np.int64)
+        indices = np.empty(max(int(nnz.value), 1), dtype=np.int64)
+        N.call("camg_pattern_to_host", h, _p(indptr), _p(indices))
     finally:
-        N.lib().camg_free_host(C.cast(ip, C.c_void_p))
-        N.lib().camg_free_host(C.cast(ix, C.c_void_p))
-    return NodeGraph(num_nodes, indptr, indices, body, interface_tag)
+        N.lib().camg_csr_destroy(h)
+    return NodeGraph(num_nodes, indptr, indices[:int(nnz.value)], body, interface_tag)
 
 
 def build_filtered_graph(K: SparseMatrix, dofs_per_node: int, dof_class=None, node_body=None,

@@ -122,8 +122,8 @@ __global__ void k_fill_ones(double* v, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = 1.0;
 }
 
-void node_graph(const Csr* K, const int64_t* dof_node_h, int64_t num_nodes, const int8_t* body_h, double eps,
-                std::vector<int64_t>& indptr, std::vector<int64_t>& indices) {
+// symmetrised node graph on the device (caller owns the result)
+Csr* node_graph_dev(const Csr* K, const int64_t* dof_node_h, int64_t num_nodes, const int8_t* body_h, double eps) {
   cudaStream_t s = 0;
   const int64_t n = K->n_rows;
   int bs = (num_nodes > 0 && n % num_nodes == 0) ? (int)(n / num_nodes) : 0;
@@ -143,14 +143,7 @@ void node_graph(const Csr* K, const int64_t* dof_node_h, int64_t num_nodes, cons
     note_launch();
     k_fill_ones<<<grid_for(G->nnz, 256), 256>>>(G->val, G->nnz);
     std::unique_ptr<Csr> GT(csr_transpose(G.get(), s));
-    std::unique_ptr<Csr> S(csr_axpby(1.0, G.get(), 1.0, GT.get(), s));
-    indptr.resize(num_nodes + 1);
-    indices.resize(S->nnz);
-    CAMG_CUDA(cudaMemcpy(indptr.data(), S->rowptr, sizeof(int64_t) * (num_nodes + 1), cudaMemcpyDeviceToHost));
-    std::vector<int32_t> c32(S->nnz);
-    if (S->nnz) CAMG_CUDA(cudaMemcpy(c32.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < S->nnz; ++i) indices[i] = c32[i];
-    return;
+    return csr_axpby(1.0, G.get(), 1.0, GT.get(), s);
   }
   DBuf<int64_t> dn(n + 1);
   DBuf<int8_t> bd(num_nodes + 1);
@@ -192,13 +185,7 @@ void node_graph(const Csr* K, const int64_t* dof_node_h, int64_t num_nodes, cons
   std::unique_ptr<Csr> NT(csr_transpose(&N, s));
   std::unique_ptr<Csr> G(galerkin(NT.get(), &F, &N, s));
   std::unique_ptr<Csr> GT(csr_transpose(G.get(), s));
-  std::unique_ptr<Csr> S(csr_axpby(1.0, G.get(), 1.0, GT.get(), s));
-  indptr.resize(num_nodes + 1);
-  indices.resize(S->nnz);
-  CAMG_CUDA(cudaMemcpy(indptr.data(), S->rowptr, sizeof(int64_t) * (num_nodes + 1), cudaMemcpyDeviceToHost));
-  std::vector<int32_t> c32(S->nnz);
-  if (S->nnz) CAMG_CUDA(cudaMemcpy(c32.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
-  for (int64_t i = 0; i < S->nnz; ++i) indices[i] = c32[i];
+  return csr_axpby(1.0, G.get(), 1.0, GT.get(), s);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,17 +275,30 @@ using namespace camg;
 extern "C" {
 
 int camg_node_graph(const camg_csr* K, const int64_t* dof_node, int64_t num_nodes, const int8_t* node_body,
-                    double eps_drop, int64_t** indptr, int64_t** indices) {
+                    double eps_drop, camg_csr** graph, int64_t* nnz) {
   return guarded([&] {
     CAMG_CHECK(K->m->n_rows == K->m->n_cols, CAMG_ERR_DIMENSION, "K must be square");
     for (int64_t i = 0; i < K->m->n_rows; ++i)
       CAMG_CHECK(dof_node[i] >= 0 && dof_node[i] < num_nodes, CAMG_ERR_DIMENSION, "dof->node map out of range");
-    std::vector<int64_t> ip, ix;
-    node_graph(K->m, dof_node, num_nodes, node_body, eps_drop, ip, ix);
-    *indptr = (int64_t*)malloc(sizeof(int64_t) * ip.size());
-    *indices = (int64_t*)malloc(sizeof(int64_t) * std::max<size_t>(1, ix.size()));
-    std::copy(ip.begin(), ip.end(), *indptr);
-    std::copy(ix.begin(), ix.end(), *indices);
+    Csr* G = node_graph_dev(K->m, dof_node, num_nodes, node_body, eps_drop);
+    *nnz = G->nnz;
+    *graph = new camg_csr{G};
+  });
+}
+
+int camg_pattern_to_host(const camg_csr* A, int64_t* indptr, int64_t* indices) {
+  return guarded([&] {
+    const Csr* M = A->m;
+    CAMG_CUDA(cudaMemcpy(indptr, M->rowptr, sizeof(int64_t) * (M->n_rows + 1), cudaMemcpyDeviceToHost));
+    if (!M->nnz) return;
+    // int32 columns widened in chunks straight into the caller's buffer
+    const int64_t chunk = int64_t(1) << 24;
+    std::vector<int32_t> c32(std::min(M->nnz, chunk));
+    for (int64_t o = 0; o < M->nnz; o += chunk) {
+      const int64_t m = std::min(chunk, M->nnz - o);
+      CAMG_CUDA(cudaMemcpy(c32.data(), M->col + o, sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+      for (int64_t i = 0; i < m; ++i) indices[o + i] = c32[i];
+    }
   });
 }
 
@@ -351,3 +351,83 @@ int camg_aggregate_lagrange(const int64_t* disp, int64_t n_rows, const int64_t* 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// tentative prolongator assembly (transfer.py:86-145): the per-aggregate Q
+// factors come from host LAPACK (batched, grouped by aggregate size); the
+// device scatters them into canonical CSR (row = DOF, columns col0(agg)+c,
+// c < rank, |q| >= 1e-300 kept as from_scipy does).
+
+namespace camg {
+
+struct PtGroup {
+  int64_t G, M, kk, dof_off, q_off, agg_off;
+};
+
+template <bool FILL>
+__global__ void k_ptent(PtGroup gp, const int64_t* __restrict__ dofs, const double* __restrict__ Q,
+                        const int64_t* __restrict__ rank, const int64_t* __restrict__ col0, int64_t* __restrict__ cnt,
+                        const int64_t* __restrict__ rp, int32_t* __restrict__ col, double* __restrict__ val) {
+  const int64_t rows = gp.G * gp.M;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = t / gp.M;
+    const int64_t dof = dofs[gp.dof_off + t];
+    const int64_t r = rank[gp.agg_off + g];
+    const double* q = Q + gp.q_off + t * gp.kk;
+    int64_t n = 0, o = FILL ? rp[dof] : 0;
+    for (int64_t c = 0; c < r; ++c) {
+      const double v = q[c];
+      if (fabs(v) >= kDropTol) {
+        if (FILL) { col[o + n] = (int32_t)(col0[gp.agg_off + g] + c); val[o + n] = v; }
+        ++n;
+      }
+    }
+    if (!FILL) cnt[dof] = n;
+  }
+}
+
+}  // namespace camg
+
+extern "C" int camg_tentative_csr(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta,
+                                  const int64_t* dofs, int64_t ndofs_total, const double* Q, int64_t nq,
+                                  const int64_t* rank, const int64_t* col0, int64_t naggs, camg_csr** out) {
+  return guarded([&] {
+    cudaStream_t s = 0;
+    CAMG_CHECK(ndofs_total == n_dofs, CAMG_ERR_DIMENSION, "every DOF must belong to one aggregate");
+    DBuf<int64_t> d_dofs(ndofs_total + 1), d_rank(naggs + 1), d_col0(naggs + 1);
+    DBuf<double> d_q(nq + 1);
+    CAMG_CUDA(cudaMemcpy(d_dofs.p, dofs, sizeof(int64_t) * ndofs_total, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(d_q.p, Q, sizeof(double) * nq, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(d_rank.p, rank, sizeof(int64_t) * naggs, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(d_col0.p, col0, sizeof(int64_t) * naggs, cudaMemcpyHostToDevice));
+    DBuf<int64_t> cnt(n_dofs + 1);
+    CAMG_CUDA(cudaMemset(cnt.p, 0, sizeof(int64_t) * (n_dofs + 1)));
+    for (int64_t gi = 0; gi < ngroups; ++gi) {
+      const int64_t* m = meta + 6 * gi;
+      PtGroup gp{m[0], m[1], m[2], m[3], m[4], m[5]};
+      note_launch();
+      k_ptent<false><<<grid_for(gp.G * gp.M, 256), 256, 0, s>>>(gp, d_dofs.p, d_q.p, d_rank.p, d_col0.p, cnt.p,
+                                                                 nullptr, nullptr, nullptr);
+    }
+    DBuf<int64_t> rp(n_dofs + 1);
+    exclusive_scan_i64(cnt.p, rp.p, n_dofs, s);
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    const int64_t nnz = read_i64(rp.p + n_dofs);
+    Csr* P = new Csr();
+    P->n_rows = n_dofs; P->n_cols = ncoarse; P->nnz = nnz;
+    P->rowptr = rp.release();
+    P->col = dalloc<int32_t>(nnz);
+    P->val = dalloc<double>(nnz);
+    P->avg_row = n_dofs ? double(nnz) / n_dofs : 0.0;
+    for (int64_t gi = 0; gi < ngroups; ++gi) {
+      const int64_t* m = meta + 6 * gi;
+      PtGroup gp{m[0], m[1], m[2], m[3], m[4], m[5]};
+      note_launch();
+      k_ptent<true><<<grid_for(gp.G * gp.M, 256), 256, 0, s>>>(gp, d_dofs.p, d_q.p, d_rank.p, d_col0.p, nullptr,
+                                                                P->rowptr, P->col, P->val);
+    }
+    CAMG_LAUNCH_CHECK();
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    *out = new camg_csr{P};
+  });
+}

@@ -300,3 +300,37 @@ def test_mcgs_corrector_vs_oracle_emulation(cfg, scale, levels):
     x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
     assert orep.converged and rep.converged
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+
+
+@pytest.mark.parametrize("cfg,scale", [("C5", 4), ("C2", 2), ("C3", 8)])
+def test_tentative_prolongator_bit_identical(cfg, scale):
+    """Batched host LAPACK + device CSR assembly == the reference's
+    per-aggregate pivoted QR (oracle), bit for bit, for u and lambda."""
+    from paper_1912_09056_b200.aggregation import NodeGraph, aggregate_greedy, aggregate_lagrange
+    from paper_1912_09056_b200.transfer import NullSpace, tentative_prolongator
+    from paper_1912_09056_b200.aggregation import filtered_node_graph
+    g = generate(config_spec(cfg, scale))
+    oop, ometa, _ = O.system_from_generated(g)
+    meta = fine_level_meta(g)
+    op = saddle_operator(g)
+    gr = filtered_node_graph(op.K, meta.u_dof_node, meta.num_u_nodes, meta.node_body)
+    ip, ix = O.node_graph(oop.K, ometa.u_dof_node, ometa.num_u_nodes, ometa.node_body)
+    np.testing.assert_array_equal(gr.indptr, ip)
+    np.testing.assert_array_equal(gr.indices, ix)
+    ag = aggregate_greedy(gr, 6)
+    oag = O.greedy(ip, ix, ometa.num_u_nodes, 6)
+    np.testing.assert_array_equal(ag.node_to_agg, oag.node_to_agg)
+    res = tentative_prolongator(ag, meta.ns_u, dof_node=meta.u_dof_node)
+    Po, nso, cao, dro = O.tentative(oag, ometa.ns_u, ometa.u_dof_node)
+    P = res.P.to_scipy()
+    assert same_pattern(P, Po) and np.array_equal(P.data, Po.data)
+    np.testing.assert_array_equal(res.coarse_ns.vectors, nso)
+    np.testing.assert_array_equal(res.coarse_dof_agg, cao)
+    assert res.dropped_columns == dro
+    la = aggregate_lagrange(ag, meta.mortar_block, meta.lmap)
+    ola = O.lagrange(oag, ometa.mortar, ometa.slave_dofs, ometa.row_node, ometa.lm_node_of_lm_dof)
+    np.testing.assert_array_equal(la.node_to_agg, ola.node_to_agg)
+    rl = tentative_prolongator(la, meta.ns_lam, dof_node=meta.lam_dof_node)
+    Pl, nsl, _, _ = O.tentative(ola, ometa.ns_lam, ometa.lam_dof_node)
+    assert same_pattern(rl.P.to_scipy(), Pl) and np.array_equal(rl.P.to_scipy().data, Pl.data)
+    np.testing.assert_array_equal(rl.coarse_ns.vectors, nsl)
