@@ -161,6 +161,98 @@ __device__ bool row_product(const CsrView& A, const CsrView& B, int64_t row, boo
   return true;
 }
 
+// Same product with the row's products flattened into 32-wide chunks (for
+// short B rows, where one A entry per warp step would idle most lanes).
+// Order is kept exactly: lanes holding the same key in a chunk form a
+// __match_any group whose lowest lane adds the members' products in lane
+// order (= A-row order), i.e. sums[k] = ((sums[k] + p1) + p2) + ... as in
+// csr_matmat.  `sp` is 32 doubles of per-warp scratch.
+__device__ bool row_product_flat(const CsrView& A, const CsrView& B, int64_t row, bool reverse_a,
+                                 const double* __restrict__ scale_a, Hash h, int lane, uint32_t limit,
+                                 double* sp) {
+  hash_clear(h, lane);
+  const int64_t s = A.rowptr[row], e = A.rowptr[row + 1];
+  const int64_t L = e - s;
+  uint32_t count = 0;
+  for (int64_t w0 = 0; w0 < L; w0 += 32) {
+    // window of up to 32 A entries: lane t owns A entry w0 + t
+    const int64_t q = w0 + lane;
+    int32_t j = 0;
+    double v = 0.0;
+    int64_t blen = 0, bstart = 0;
+    if (q < L) {
+      const int64_t jj = reverse_a ? (e - 1 - q) : (s + q);
+      j = A.col[jj];
+      v = A.val[jj];
+      if (scale_a) {
+        v = __dmul_rn(v, scale_a[row]);
+        if (fabs(v) < kDropTol) v = 0.0, j = -1;  // dropped entry of diag(s)A
+      }
+      if (j >= 0) {
+        bstart = B.rowptr[j];
+        blen = B.rowptr[j + 1] - bstart;
+      }
+    }
+    // inclusive scan of the window's product counts
+    int64_t incl = blen;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int64_t total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int64_t f0 = 0; f0 < total; f0 += 32) {
+      if (count + 32 > limit) return false;
+      const int64_t f = f0 + lane;
+      const bool act = f < total;
+      // owner lane of product f: first t with incl[t] > f (binary search over shuffles)
+      int lo = 0;
+#pragma unroll
+      for (int stepw = 16; stepw > 0; stepw >>= 1) {
+        const int64_t c = __shfl_sync(0xffffffffu, incl, lo + stepw - 1);
+        if (act && c <= f) lo += stepw;
+      }
+      const int owner = act ? lo : 0;
+      const int64_t before = __shfl_sync(0xffffffffu, incl - blen, owner);
+      const int64_t ob = __shfl_sync(0xffffffffu, bstart, owner);
+      const double ov = __shfl_sync(0xffffffffu, v, owner);
+      int32_t key = -1;
+      double prod = 0.0;
+      if (act) {
+        const int64_t kk = ob + (f - before);
+        key = B.col[kk];
+        prod = __dmul_rn(ov, B.val[kk]);
+      }
+      sp[lane] = prod;
+      const unsigned am = __ballot_sync(0xffffffffu, act);
+      const unsigned grp = __match_any_sync(0xffffffffu, act ? key : -1 - lane);
+      __syncwarp();
+      int ins = 0;
+      if (act && (__ffs(grp) - 1) == lane) {  // group leader
+        const uint32_t mask = h.cap - 1;
+        uint32_t slot = hslot(key, mask);
+        double acc;
+        while (true) {
+          const int32_t cur = atomicCAS(&h.keys[slot], kEmpty, key);
+          if (cur == kEmpty) { acc = 0.0; ins = 1; break; }
+          if (cur == key) { acc = h.vals[slot]; break; }
+          slot = (slot + 1) & mask;
+        }
+        unsigned m = grp & am;
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1;
+          acc = __dadd_rn(acc, sp[src]);
+        }
+        h.vals[slot] = acc;
+      }
+      count += __popc(__ballot_sync(0xffffffffu, ins));
+      __syncwarp();
+    }
+  }
+  return true;
+}
+
 // (R*A)*P for one row: hash1 holds RA with first-touch groups, hash2 the result
 __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P, int64_t row, Hash h1,
                            Hash h2, int lane, uint32_t limit1, uint32_t limit2) {
@@ -251,6 +343,7 @@ __global__ void k_product(CsrView A, CsrView B, bool reverse_a, const double* __
                           const int64_t* __restrict__ rows, int64_t nrows,
                           uint32_t cap, char* __restrict__ gscratch, OutArgs o) {
   extern __shared__ __align__(16) char smem[];
+  __shared__ double sp_all[kWarpsPerBlock][32];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
@@ -259,7 +352,7 @@ __global__ void k_product(CsrView A, CsrView B, bool reverse_a, const double* __
   Hash h{reinterpret_cast<int32_t*>(base + (size_t)cap * 8), nullptr, reinterpret_cast<double*>(base), cap};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
-    bool ok = row_product(A, B, row, reverse_a, scale_a, h, lane, (cap * 3) / 4);
+    bool ok = row_product_flat(A, B, row, reverse_a, scale_a, h, lane, (cap * 3) / 4, sp_all[w]);
     if (!ok) {
       if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
       continue;
