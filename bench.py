@@ -258,6 +258,28 @@ def workload_config(args):
 
 
 # ---------------------------------------------------------------------------
+# multi-rank aggregation (replicas: no data-path collective, timing only)
+
+
+def replica_max(x, world, device):
+    """Max of a per-rank scalar over all ranks (the slowest replica sets the
+    job time).  Works with the nccl (cuda) and gloo (cpu) backends."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(units_per_rank, seconds_per_rank, world, device):
+    """Whole-job throughput: all ranks' units / max-over-ranks time."""
+    return units_per_rank * world / replica_max(seconds_per_rank, world, device)
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 
 
@@ -301,11 +323,7 @@ def run_gpu(args):
             dist.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return replica_max(x, world, "cuda")
 
     # ---- dominant kernel: fine-level operator stream (merged [K B1; B2 -Cz] SpMV)
     A0 = H.levels[0].smoother  # noqa: F841

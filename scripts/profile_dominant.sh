@@ -1,12 +1,14 @@
 #!/bin/bash
-# (1) per-kernel launch list of the C5 V-cycle (solve-phase kernels only)
-# (2) full ncu capture of the dominant kernel: the first fine-level extra
-#     Jacobi sweep timed by bench.py (23 k_sell_row SpMV launches precede it)
+# Round-1 ncu evidence on C5 (run under gpurun from the repo root):
+# (1) per-kernel launch list of the solve-phase kernels (timed V-cycles)
+# (2) one `ncu --set full` capture of the dominant kernel: the fine-level
+#     Jacobi predictor sweep timed by bench.py (the 23 SELL SpMV launches of
+#     the SpMV measurement precede it)
 CMD="python bench.py --steps 1 --warmup 3 --no-solve --no-cpu-baseline"
 $CMD > gpurun_out/plain_dom.log 2>&1 || { echo plain failed; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:'k_sell_row|k_resid|k_jacobi|k_spmv|k_lam|k_corr|k_lu_solve|k_b1_correct|k_mcgs' -c 4000 --csv \
-    --log-file gpurun_out/launches_vc_c5_r01.csv $CMD > gpurun_out/ncu_vc.log 2>&1
+    -k regex:'k_sell_row|k_resid|k_jacobi|k_spmv|k_lam|k_corr|k_lu_solve|k_b1_correct|k_mcgs' -c 3000 --csv \
+    --log-file gpurun_out/launches_vc_c5_r01b.csv $CMD > gpurun_out/ncu_vc.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_sell_row -s 23 -c 1 \
-    -o gpurun_out/prof_dom_c5 $CMD > gpurun_out/ncu_dom.log 2>&1
+    -o gpurun_out/prof_dom_c5b $CMD > gpurun_out/ncu_dom.log 2>&1
 echo rc=$?

@@ -334,3 +334,92 @@ def test_tentative_prolongator_bit_identical(cfg, scale):
     Pl, nsl, _, _ = O.tentative(ola, ometa.ns_lam, ometa.lam_dof_node)
     assert same_pattern(rl.P.to_scipy(), Pl) and np.array_equal(rl.P.to_scipy().data, Pl.data)
     np.testing.assert_array_equal(rl.coarse_ns.vectors, nsl)
+
+
+# ---------------------------------------------------------------------------
+# edge cases (reference behaviour: krylov.py:56-61, hierarchy.py:194,
+# smoothers.py:151-153, saddle.py:22-27)
+
+
+def _small():
+    g = generate(config_spec("C1"))
+    return g, saddle_operator(g)
+
+
+def test_gmres_zero_rhs_returns_zero():
+    g, op = _small()
+    H = setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2, max_coarse_size=1),
+              block_cfg(BY_NAME["c1_uzawa_jac2"][4]))
+    x, rep = gmres(op.apply_merged, H.apply, np.zeros(op.total_rows), GmresConfig())
+    assert rep.converged and rep.iterations == 0 and not np.any(x)
+    assert rep.residual_history == [0.0]
+
+
+def test_single_level_hierarchy_is_a_direct_solve():
+    """max_levels=1: the fine level is the coarsest (merged dense LU); one
+    GMRES iteration, like the reference's perfect-preconditioner case."""
+    g, op = _small()
+    H = setup(op, fine_level_meta(g), HierarchyConfig(max_levels=1), block_cfg(BY_NAME["c1_uzawa_jac2"][4]))
+    assert H.num_levels == 1
+    A = op.merged().to_scipy()
+    z = H.apply(g.rhs)
+    assert np.linalg.norm(A @ z - g.rhs) <= 1e-9 * np.linalg.norm(g.rhs)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=10))
+    assert rep.converged and rep.iterations == 1
+
+
+def test_gmres_without_preconditioner_matches_oracle():
+    g = generate(config_spec("C1"))
+    op = saddle_operator(g)
+    oop, _, rhs = O.system_from_generated(g)
+    A = oop.merged()
+    _, orep = O.gmres(lambda v: A @ v, lambda v: v, rhs, 1e-6, 60, 30)
+    x, rep = gmres(op.apply_merged, None, g.rhs, GmresConfig(rel_tol=1e-6, max_iters=60, restart=30))
+    assert abs(rep.iterations - orep.iterations) <= 1
+    assert np.allclose(rep.residual_history[:10], orep.residual_history[:10], rtol=1e-6)
+
+
+def test_singular_diagonal_raises():
+    from paper_1912_09056_b200.errors import SingularMatrixError
+    from paper_1912_09056_b200.saddle import SaddleOperator
+    from paper_1912_09056_b200.smoothers import BlockSmoother
+    K = scipy.sparse.csr_matrix(np.array([[2.0, 1.0, 0.0], [1.0, 0.0, 1.0], [0.0, 1.0, 2.0]]))
+    B1 = scipy.sparse.csr_matrix(np.array([[1.0], [0.0], [1.0]]))
+    op = SaddleOperator(*(SparseMatrix.from_scipy(m) for m in (K, B1, B1.T, scipy.sparse.csr_matrix((1, 1)))))
+    with pytest.raises(SingularMatrixError):
+        BlockSmoother(block_cfg(dict(kind="uzawa", alpha=1.0, predictor=("jacobi", 1, 0.8),
+                                     corrector=("jacobi", 1, 0.8))), op)
+
+
+def test_dimension_errors():
+    from paper_1912_09056_b200.errors import DimensionError
+    from paper_1912_09056_b200.saddle import SaddleOperator
+    A = SparseMatrix.from_dense(np.eye(3))
+    with pytest.raises(DimensionError):
+        spmv(A, np.ones(4))
+    with pytest.raises(DimensionError):
+        sp_matmul(A, SparseMatrix.from_dense(np.ones((2, 2))))
+    with pytest.raises(DimensionError):
+        SaddleOperator(A, SparseMatrix.from_dense(np.ones((2, 1))), SparseMatrix.from_dense(np.ones((1, 3))),
+                       SparseMatrix.from_dense(np.ones((1, 1))))
+
+
+def test_public_vcycle_function_matches_native():
+    """hierarchy.vcycle (Python orchestration over the device level kernels,
+    arbitrary start) from zero == the native graph-captured Hierarchy.apply."""
+    from paper_1912_09056_b200.hierarchy import vcycle
+    from paper_1912_09056_b200.sparse import BlockVector
+    g, op, H = gpu_hier("c4s_uzawa")
+    b = BlockVector.from_merged(g.rhs, op.n_u)
+    x = vcycle(H, 0, BlockVector.zeros(op.n_u, op.n_lam), b).merged()
+    z = H.apply(g.rhs)
+    assert np.linalg.norm(x - z) <= 1e-12 * np.linalg.norm(z)
+
+
+def test_graph_disabled_equals_graph():
+    g, op, H = gpu_hier("c5s_simple")
+    z1 = H.apply(g.rhs)
+    H.use_graph(False)
+    z2 = H.apply(g.rhs)
+    H.use_graph(True)
+    np.testing.assert_array_equal(z1, z2)
