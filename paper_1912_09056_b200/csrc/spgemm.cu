@@ -254,57 +254,154 @@ __device__ bool row_product_flat(const CsrView& A, const CsrView& B, int64_t row
 }
 
 // (R*A)*P for one row: hash1 holds RA with first-touch groups, hash2 the result
+// ordered accumulation of one 32-wide chunk of (key, product) pairs into h:
+// lanes with equal keys form a __match_any group, the lowest lane adds the
+// members' products in lane order.  `ft` is recorded for new keys.
+__device__ __forceinline__ int chunk_accumulate(Hash h, bool act, int32_t key, double prod, int32_t ft, int lane,
+                                                double* sp) {
+  sp[lane] = prod;
+  const unsigned am = __ballot_sync(0xffffffffu, act);
+  const unsigned grp = __match_any_sync(0xffffffffu, act ? key : -1 - lane);
+  __syncwarp();
+  int ins = 0;
+  if (act && (__ffs(grp) - 1) == lane) {
+    const uint32_t mask = h.cap - 1;
+    uint32_t slot = hslot(key, mask);
+    double acc;
+    while (true) {
+      const int32_t cur = atomicCAS(&h.keys[slot], kEmpty, key);
+      if (cur == kEmpty) {
+        acc = 0.0;
+        ins = 1;
+        if (h.ft) h.ft[slot] = ft;
+        break;
+      }
+      if (cur == key) { acc = h.vals[slot]; break; }
+      slot = (slot + 1) & mask;
+    }
+    unsigned m = grp & am;
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      acc = __dadd_rn(acc, sp[src]);
+    }
+    h.vals[slot] = acc;
+  }
+  const int n = __popc(__ballot_sync(0xffffffffu, ins));
+  __syncwarp();
+  return n;
+}
+
+// lane index owning flattened position f (first t with incl[t] > f)
+__device__ __forceinline__ int owner_of(int64_t incl, int64_t f, bool act) {
+  int lo = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int64_t c = __shfl_sync(0xffffffffu, incl, lo + w - 1);
+    if (act && c <= f) lo += w;
+  }
+  return act ? lo : 0;
+}
+
+// (R*A)*P for one row: hash1 holds RA with first-touch groups, hash2 the result
 __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P, int64_t row, Hash h1,
-                           Hash h2, int lane, uint32_t limit1, uint32_t limit2) {
+                           Hash h2, int lane, uint32_t limit1, uint32_t limit2, double* sp) {
   hash_clear(h1, lane);
   hash_clear(h2, lane);
   const int64_t rs = R.rowptr[row], re = R.rowptr[row + 1];
+  const int64_t nR = re - rs;
   uint32_t c1 = 0, c2 = 0;
-  for (int64_t q = 0; q < re - rs; ++q) {
-    const int32_t j = R.col[rs + q];
-    const double v = R.val[rs + q];
-    const int64_t as = A.rowptr[j], ae = A.rowptr[j + 1];
-    for (int64_t base = as; base < ae; base += 32) {
+  // ---- stage 1: RA row in R's order, one A-row chunk per step, next chunk prefetched
+  for (int64_t w0 = 0; w0 < nR; w0 += 32) {
+    const int64_t qq = w0 + lane;
+    double vq = 0.0;
+    int64_t aq = 0, lq = 0;
+    if (qq < nR) {
+      const int32_t j = R.col[rs + qq];
+      vq = R.val[rs + qq];
+      aq = A.rowptr[j];
+      lq = A.rowptr[j + 1] - aq;
+    }
+    const int64_t nch = (lq + 31) >> 5;
+    int64_t incl = nch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
+    auto fetch = [&](int64_t st, int32_t& col, double& val, double& vv, int& ql, bool& ok) {
+      const bool act = st < T;
+      const int o = owner_of(incl, st, act);
+      const int64_t c = st - (__shfl_sync(0xffffffffu, incl - nch, o));
+      const int64_t a = __shfl_sync(0xffffffffu, aq, o);
+      const int64_t l = __shfl_sync(0xffffffffu, lq, o);
+      vv = __shfl_sync(0xffffffffu, vq, o);
+      ql = o;
+      const int64_t off = 32 * c + lane;
+      ok = act && off < l;
+      col = ok ? A.col[a + off] : -1;
+      val = ok ? A.val[a + off] : 0.0;
+    };
+    int32_t col, ncol;
+    double val, vv, nval, nvv;
+    int ql, nql;
+    bool ok, nok;
+    if (T > 0) fetch(0, col, val, vv, ql, ok);
+    for (int64_t st = 0; st < T; ++st) {
+      if (st + 1 < T) fetch(st + 1, ncol, nval, nvv, nql, nok);
       if (c1 + 32 > limit1) return false;
       int ins = 0;
-      const int64_t kk = base + lane;
-      if (kk < ae) ins = hash_add(h1, A.col[kk], __dmul_rn(v, A.val[kk]), (int32_t)q);
+      if (ok) ins = hash_add(h1, col, __dmul_rn(vv, val), (int32_t)(w0 + ql));
       c1 += __popc(__ballot_sync(0xffffffffu, ins));
       __syncwarp();
+      col = ncol; val = nval; vv = nvv; ql = nql; ok = nok;
     }
   }
-  // walk RA in scipy's stored order: groups descending, columns descending
-  for (int64_t q = re - rs - 1; q >= 0; --q) {
+  // ---- stage 2: walk RA in scipy's stored order (groups descending, columns
+  // descending); the members of each A-row chunk times their P rows are
+  // flattened into ordered 32-wide chunks
+  for (int64_t q = nR - 1; q >= 0; --q) {
     const int32_t j = R.col[rs + q];
     const int64_t as = A.rowptr[j], ae = A.rowptr[j + 1];
     for (int64_t top = ae - 1; top >= as; top -= 32) {
       const int64_t kk = top - lane;
-      int32_t t = -1;
       double rav = 0.0;
-      bool member = false;
+      int64_t pb = 0, pl = 0;
       if (kk >= as) {
-        t = A.col[kk];
-        int sl = hash_find(h1, t);
+        const int32_t t = A.col[kk];
+        const int sl = hash_find(h1, t);
         if (sl >= 0 && h1.ft[sl] == (int32_t)q) {
           rav = h1.vals[sl];
-          member = rav != 0.0;  // csr_matmat drops exact zeros of RA
+          if (rav != 0.0) {  // csr_matmat drops exact zeros of RA
+            pb = P.rowptr[t];
+            pl = P.rowptr[t + 1] - pb;
+          }
         }
       }
-      unsigned b = __ballot_sync(0xffffffffu, member);
-      while (b) {
-        const int src = __ffs(b) - 1;
-        b &= b - 1;
-        const int32_t tt = __shfl_sync(0xffffffffu, t, src);
-        const double vv = __shfl_sync(0xffffffffu, rav, src);
-        const int64_t ps = P.rowptr[tt], pe = P.rowptr[tt + 1];
-        for (int64_t base = ps; base < pe; base += 32) {
-          if (c2 + 32 > limit2) return false;
-          int ins = 0;
-          const int64_t pp = base + lane;
-          if (pp < pe) ins = hash_add(h2, P.col[pp], __dmul_rn(vv, P.val[pp]), 0);
-          c2 += __popc(__ballot_sync(0xffffffffu, ins));
-          __syncwarp();
+      int64_t incl = pl;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
+      for (int64_t f0 = 0; f0 < T; f0 += 32) {
+        if (c2 + 32 > limit2) return false;
+        const int64_t f = f0 + lane;
+        const bool act = f < T;
+        const int o = owner_of(incl, f, act);
+        const int64_t before = __shfl_sync(0xffffffffu, incl - pl, o);
+        const int64_t ob = __shfl_sync(0xffffffffu, pb, o);
+        const double ov = __shfl_sync(0xffffffffu, rav, o);
+        int32_t key = -1;
+        double prod = 0.0;
+        if (act) {
+          const int64_t pp = ob + (f - before);
+          key = P.col[pp];
+          prod = __dmul_rn(ov, P.val[pp]);
         }
+        c2 += chunk_accumulate(h2, act, key, prod, 0, lane, sp);
       }
     }
   }
@@ -365,6 +462,7 @@ template <bool FILL, bool GLOBAL>
 __global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restrict__ rows, int64_t nrows,
                          uint32_t cap1, uint32_t cap2, char* __restrict__ gscratch, OutArgs o) {
   extern __shared__ __align__(16) char smem[];
+  __shared__ double sp_all[kWarpsPerBlock][32];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
@@ -377,7 +475,7 @@ __global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restr
   Hash h2{reinterpret_cast<int32_t*>(b2 + (size_t)cap2 * 8), nullptr, reinterpret_cast<double*>(b2), cap2};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
-    bool ok = row_triple(R, A, P, row, h1, h2, lane, (cap1 * 3) / 4, (cap2 * 3) / 4);
+    bool ok = row_triple(R, A, P, row, h1, h2, lane, (cap1 * 3) / 4, (cap2 * 3) / 4, sp_all[w]);
     if (!ok) {
       if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
       continue;
