@@ -12,7 +12,8 @@ inline void note_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_r
 constexpr double kDropTol = 1e-300;  // sparse.py:21 DROP_TOL
 constexpr int kDotBlocks = 592;      // 4 x 148 SMs
 constexpr int64_t kSellMinBlockRows = 50000;  // fewer block rows: lanes cannot fill 148 SMs
-constexpr int64_t kMcgsCtaRows = 12288;  // S~ up to this size: single-CTA MC-SGS (x in 96 KB smem)
+constexpr int64_t kSellPairSlices = 40000;  // below: two lanes per block row (wave balance)
+constexpr int64_t kMcgsCtaRows = 24576;  // S~ up to this size: single-CTA MC-SGS (x in 192 KB smem)
 
 // lanes per row for vector-CSR kernels, from the mean row length
 inline int group_for(double avg) {

@@ -326,6 +326,80 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
   }
 }
 
+// Small matrices (few slices) lose a quarter of the time to wave
+// quantisation with one warp per slice; this variant gives each block row to
+// a lane pair (even lane: first half of its slots, odd lane: second half,
+// deterministic pair reduction), i.e. two work units per slice.
+template <int BR, int BC, bool ZERO, bool SPLIT, int MODE>
+__global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __restrict__ xu,
+                                                   const double* __restrict__ xl, int64_t split_blocks,
+                                                   SellEpi e) {
+  constexpr int BE = BR * BC;
+  const int lane = threadIdx.x & 31;
+  const int half = lane & 1;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t hs = warp; hs < 2 * S.nslices; hs += nwarps) {
+    const int64_t s = hs >> 1;
+    const int pl = (int)(hs & 1) * 16 + (lane >> 1);
+    const int64_t p = s * 32 + pl;
+    const bool active = p < S.nbr;
+    double acc[BR];
+#pragma unroll
+    for (int r = 0; r < BR; ++r) acc[r] = 0.0;
+    if (!ZERO) {
+      const int n = active ? S.len[p] : 0;
+      const int k0 = half ? (n + 1) / 2 : 0, k1 = half ? n : (n + 1) / 2;
+      const int64_t base = S.slice_ptr[s];
+      for (int k = k0; k < k1; ++k) {
+        const int64_t slot = base + k;
+        const int32_t bc = __ldcs(S.bcol + slot * 32 + pl);
+        const double* xs;
+        if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
+        else xs = xl ? xl + ((int64_t)bc - split_blocks) * BC : nullptr;
+        double xv[BC];
+#pragma unroll
+        for (int c = 0; c < BC; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
+        const double* v = S.bval + slot * (BE * 32) + pl;
+#pragma unroll
+        for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < BR; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 1);
+    if (!active || half) continue;
+#pragma unroll
+    for (int r = 0; r < BR; ++r) {
+      const int64_t i = p * BR + r;
+      if constexpr (MODE == 0) {
+        e.y[i] = e.beta != 0.0 ? e.alpha * acc[r] + e.beta * e.y[i] : e.alpha * acc[r];
+      } else if constexpr (MODE == 1) {
+        const double res = e.b[i] - acc[r];
+        if (e.out_r) e.out_r[i] = res;
+        if (e.dscale) {
+          const double d = e.dscale[i] * res;
+          if (e.out_d) e.out_d[i] = d;
+          const double xi = (ZERO || !e.x) ? 0.0 : e.x[i];
+          const double y = xi + d;
+          if (e.out_y) e.out_y[i] = y;
+          if (e.out_x) {
+            if (e.xmode) {
+              const double o = e.x0 ? e.x0[i] : 0.0;
+              e.out_x[i] = o + e.coef * (y - o);
+            } else {
+              e.out_x[i] = xi + e.coef * d;
+            }
+          }
+        }
+      } else {
+        const double dn = e.d[i] + e.dscale[i] * (e.r[i] - acc[r]);
+        e.out_d[i] = dn;
+        if (e.out_x) e.out_x[i] = (e.x ? e.x[i] : 0.0) + e.coef * dn;
+      }
+    }
+  }
+}
+
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st) {
@@ -334,10 +408,13 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
   note_launch();
-#define CAMG_SELL_LAUNCH(Z, SP, M)                                                   \
-  do {                                                                               \
-    if (S->masked) k_sell_row<BR, BC, Z, SP, M, true><<<grid, 256, 0, st>>>(v, xu, xl, sb, e); \
-    else k_sell_row<BR, BC, Z, SP, M, false><<<grid, 256, 0, st>>>(v, xu, xl, sb, e);          \
+#define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
+  do {                                                                                       \
+    if (S->masked) k_sell_row<BR, BC, Z, SP, M, true><<<grid, 256, 0, st>>>(v, xu, xl, sb, e);         \
+    else if (S->nslices < kSellPairSlices)                                                   \
+      k_sell_row2<BR, BC, Z, SP, M><<<grid_for(S->nslices * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st>>>( \
+          v, xu, xl, sb, e);                                                                 \
+    else k_sell_row<BR, BC, Z, SP, M, false><<<grid, 256, 0, st>>>(v, xu, xl, sb, e);                  \
   } while (0)
   if (mode == 0) {
     if (sp) CAMG_SELL_LAUNCH(false, true, 0); else CAMG_SELL_LAUNCH(false, false, 0);

@@ -16,6 +16,8 @@
 // One warp per output row; per-warp hash tables live in shared memory, rows
 // that overflow them are recomputed with hash tables in global scratch.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -527,6 +529,8 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   CAMG_CUDA(cudaStreamSynchronize(s));
   CAMG_LAUNCH_CHECK();
   std::vector<int64_t> big = overflow_rows(ovf.p, n_rows);
+  if (getenv("CAMG_DEBUG"))
+    fprintf(stderr, "[camg] spgemm rows=%lld smem-overflow rows=%zu\n", (long long)n_rows, big.size());
   struct Batch { DBuf<int64_t> rows; int64_t n; uint32_t c1, c2; };
   std::vector<Batch> batches;
   uint32_t c1 = c1_0, c2 = c2_0;
