@@ -423,7 +423,7 @@ struct Level {
     if (cfg.corr_kind == CAMG_PT_MCGS) {
       const int nc_ = (int)color_ptr.size() - 1;
       double* x = w_dl.p;
-      if (nl <= kMcgsCtaRows) {
+      if (nl <= kMcgsCtaRows && S->nnz <= kMcgsCtaNnz) {
         static bool attr = false;
         if (!attr) {
           CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
