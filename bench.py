@@ -31,7 +31,11 @@ sys.path.insert(0, ROOT)
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # ncu dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per
 # launch, from profiles/ (one `ncu --set full` capture; None until measured)
-TRAFFIC = {}
+TRAFFIC = {
+    # profiles/r01_dominant_kernel_ncu_full.txt: k_sell_row<3,3,0,1,1,0>, C5,
+    # dram__bytes_read.sum 16.658436 GB + dram__bytes_write.sum 0.176741 GB
+    "C5": 16.835177e9,
+}
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 # BASELINE config -> reference-API mapping
