@@ -101,13 +101,6 @@ struct Csr {
   int64_t* rowptr = nullptr;
   int32_t* col = nullptr;
   double* val = nullptr;
-  // Optional 3x3 / 2x2 block (BSR) mirror of the same matrix, built on demand
-  // for the fine-level hot kernels (see spmv.cu).
-  int bs = 0;
-  int64_t nnzb = 0;
-  int64_t* browptr = nullptr;
-  int32_t* bcol = nullptr;
-  double* bval = nullptr;
   double avg_row = 0.0;
   Sell* sell = nullptr;  // optional block SELL-32 mirror of the leading rows
   ~Csr();

@@ -24,9 +24,6 @@ Csr::~Csr() {
   dfree(rowptr);
   dfree(col);
   dfree(val);
-  dfree(browptr);
-  dfree(bcol);
-  dfree(bval);
   delete sell;
 }
 

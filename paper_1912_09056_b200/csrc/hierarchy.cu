@@ -378,6 +378,7 @@ struct Level {
   int pre = 1, post = 1;
   Csr* A = nullptr;    // merged [[K,B1],[B2,-Cz]]
   bool owns_A = true;
+  camg_csr op_handle{nullptr};  // borrowed view handed out by camg_level_operator
   Csr* B1 = nullptr;   // copy (interface rows)
   Csr* S = nullptr;    // S~
   DBuf<int64_t> b1_rows;
@@ -886,9 +887,8 @@ int camg_level_schur(const camg_level* L, camg_csr** out) {
 
 int camg_level_operator(const camg_level* L, const camg_csr** out) {
   return guarded([&] {
-    static thread_local camg_csr view_handle;
-    view_handle.m = L->L->A;
-    *out = &view_handle;
+    L->L->op_handle.m = L->L->A;
+    *out = &L->L->op_handle;
   });
 }
 
