@@ -360,51 +360,83 @@ __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P,
       col = ncol; val = nval; vv = nvv; ql = nql; ok = nok;
     }
   }
-  // ---- stage 2: walk RA in scipy's stored order (groups descending, columns
-  // descending); the members of each A-row chunk times their P rows are
-  // flattened into ordered 32-wide chunks
-  for (int64_t q = nR - 1; q >= 0; --q) {
-    const int32_t j = R.col[rs + q];
-    const int64_t as = A.rowptr[j], ae = A.rowptr[j + 1];
-    for (int64_t top = ae - 1; top >= as; top -= 32) {
-      const int64_t kk = top - lane;
-      double rav = 0.0;
-      int64_t pb = 0, pl = 0;
-      if (kk >= as) {
-        const int32_t t = A.col[kk];
-        const int sl = hash_find(h1, t);
-        if (sl >= 0 && h1.ft[sl] == (int32_t)q) {
-          rav = h1.vals[sl];
-          if (rav != 0.0) {  // csr_matmat drops exact zeros of RA
-            pb = P.rowptr[t];
-            pl = P.rowptr[t + 1] - pb;
+  // ---- stage 2: RA in scipy's stored order = descending (first-touch group,
+  // column) -- csr_matmat's reverse first-touch linked list, exact zeros
+  // dropped.  Compact the table, bitonic-sort it by that key, then stream
+  // the entries times their P rows as ordered 32-wide chunks.
+  int n1 = 0;
+  for (uint32_t base = 0; base < h1.cap; base += 32) {
+    const uint32_t sl = base + lane;
+    const int32_t k = h1.keys[sl];
+    const double v = h1.vals[sl];
+    const int32_t g = h1.ft[sl];
+    const bool keep = (k != kEmpty) && v != 0.0;
+    const unsigned bb = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) {
+      const int pos = n1 + __popc(bb & ((1u << lane) - 1u));
+      h1.keys[pos] = k;
+      h1.vals[pos] = v;
+      h1.ft[pos] = g;
+    }
+    n1 += __popc(bb);
+    __syncwarp();
+  }
+  int N = 1;
+  while (N < n1) N <<= 1;
+  for (int i = n1 + lane; i < N; i += 32) { h1.keys[i] = INT32_MIN; h1.ft[i] = -1; }
+  __syncwarp();
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int jb = k >> 1; jb > 0; jb >>= 1) {
+      for (int i = lane; i < N; i += 32) {
+        const int ixj = i ^ jb;
+        if (ixj > i) {
+          const int64_t ka = ((int64_t)h1.ft[i] << 32) | (uint32_t)(h1.keys[i] - INT32_MIN);
+          const int64_t kb = ((int64_t)h1.ft[ixj] << 32) | (uint32_t)(h1.keys[ixj] - INT32_MIN);
+          const bool desc = (i & k) == 0;
+          if ((ka < kb) == desc) {
+            int32_t tk = h1.keys[i]; h1.keys[i] = h1.keys[ixj]; h1.keys[ixj] = tk;
+            int32_t tg = h1.ft[i]; h1.ft[i] = h1.ft[ixj]; h1.ft[ixj] = tg;
+            double tv = h1.vals[i]; h1.vals[i] = h1.vals[ixj]; h1.vals[ixj] = tv;
           }
         }
       }
-      int64_t incl = pl;
+      __syncwarp();
+    }
+  }
+  for (int e0 = 0; e0 < n1; e0 += 32) {
+    const int e = e0 + lane;
+    double rav = 0.0;
+    int64_t pb = 0, pl = 0;
+    if (e < n1) {
+      const int32_t t = h1.keys[e];
+      rav = h1.vals[e];
+      pb = P.rowptr[t];
+      pl = P.rowptr[t + 1] - pb;
+    }
+    int64_t incl = pl;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
+    for (int64_t f0 = 0; f0 < T; f0 += 32) {
+      if (c2 + 32 > limit2) return false;
+      const int64_t f = f0 + lane;
+      const bool act = f < T;
+      const int o = owner_of(incl, f, act);
+      const int64_t before = __shfl_sync(0xffffffffu, incl - pl, o);
+      const int64_t ob = __shfl_sync(0xffffffffu, pb, o);
+      const double ov = __shfl_sync(0xffffffffu, rav, o);
+      int32_t key = -1;
+      double prod = 0.0;
+      if (act) {
+        const int64_t pp = ob + (f - before);
+        key = P.col[pp];
+        prod = __dmul_rn(ov, P.val[pp]);
       }
-      const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
-      for (int64_t f0 = 0; f0 < T; f0 += 32) {
-        if (c2 + 32 > limit2) return false;
-        const int64_t f = f0 + lane;
-        const bool act = f < T;
-        const int o = owner_of(incl, f, act);
-        const int64_t before = __shfl_sync(0xffffffffu, incl - pl, o);
-        const int64_t ob = __shfl_sync(0xffffffffu, pb, o);
-        const double ov = __shfl_sync(0xffffffffu, rav, o);
-        int32_t key = -1;
-        double prod = 0.0;
-        if (act) {
-          const int64_t pp = ob + (f - before);
-          key = P.col[pp];
-          prod = __dmul_rn(ov, P.val[pp]);
-        }
-        c2 += chunk_accumulate(h2, act, key, prod, 0, lane, sp);
-      }
+      c2 += chunk_accumulate(h2, act, key, prod, 0, lane, sp);
     }
   }
   return true;
