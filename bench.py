@@ -60,6 +60,11 @@ def solver_for(config):
                                    corrector=P("mcgs", 1, 1.0)), 100),
     }
     h, s, r = table[config]
+    override = os.environ.get("CAMG_BENCH_SMOOTHER")
+    if override:  # "kind,alpha,outer,pred_kind,pred_sweeps,pred_damping,corr_kind,corr_sweeps,corr_damping"
+        f = override.split(",")
+        s = BlockSmootherConfig(kind=f[0], alpha=float(f[1]), outer_sweeps=int(f[2]),
+                                predictor=P(f[3], int(f[4]), float(f[5])), corrector=P(f[6], int(f[7]), float(f[8])))
     return HierarchyConfig(**h), s, r
 
 
