@@ -55,8 +55,10 @@ def solver_for(config):
         "C4": (dict(max_levels=5, max_coarse_size=500),
                BlockSmootherConfig(kind="uzawa", alpha=0.6, predictor=P("jacobi", 2, 0.6),
                                    corrector=P("jacobi", 1, 0.6)), 100),
+        # chosen on C5 time to solution: Jacobi(1,0.6) predictor
+        # 0.96 s / 30 its; Jacobi(2,0.6) 1.39 s / 26 its; outer x2 1.30 s / 34 its
         "C5": (dict(max_levels=6, max_coarse_size=500),
-               BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=3, predictor=P("jacobi", 2, 0.6),
+               BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=3, predictor=P("jacobi", 1, 0.6),
                                    corrector=P("mcgs", 1, 1.0)), 100),
     }
     h, s, r = table[config]
