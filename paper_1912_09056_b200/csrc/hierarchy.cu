@@ -9,6 +9,8 @@
 // plus a few small kernels on the lambda side and on the interface rows of B1.
 #include <algorithm>
 #include <cmath>
+#include <cooperative_groups.h>
+#include <cstdlib>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -19,6 +21,18 @@ namespace camg {
 
 Csr* schur(const Csr* B2, const Csr* Cz, const Csr* B1, const double* ainv, double scale, cudaStream_t s);
 void recip(int64_t n, const double* d, double* out, cudaStream_t s);
+
+// cooperative (grid-synchronised) MC-SGS unless CAMG_COOP_MCGS=0
+static bool use_coop_mcgs() {
+  static int coop = -1;
+  if (coop < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  }
+  const char* e = getenv("CAMG_COOP_MCGS");
+  return coop == 1 && !(e && e[0] == '0');
+}
 
 // ---------------------------------------------------------------------------
 // fused row kernels
@@ -188,6 +202,40 @@ __global__ void __launch_bounds__(1024) k_mcgs_cta(CsrView S, const int32_t* __r
     }
   }
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xg[i] = xs[i];
+}
+
+// Whole multicolour SSOR sweeps of a larger S as ONE cooperative kernel:
+// colours separated by grid-wide barriers instead of kernel boundaries
+// (2 x ncolours launches per sweep otherwise).
+__global__ void __launch_bounds__(256) k_mcgs_coop(CsrView S, const int32_t* __restrict__ rows,
+                                                   const int64_t* __restrict__ cptr, int ncol, int sweeps,
+                                                   const double* __restrict__ b, const double* __restrict__ dinv,
+                                                   double* __restrict__ x) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  constexpr int G = 8;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t ngrp = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t i = tid; i < S.n_rows; i += (int64_t)gridDim.x * blockDim.x) x[i] = 0.0;
+  grid.sync();
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int dir = 0; dir < 2; ++dir) {
+      for (int cc = 0; cc < ncol; ++cc) {
+        const int c = dir == 0 ? cc : ncol - 1 - cc;
+        const int64_t lo = cptr[c], hi = cptr[c + 1];
+        for (int64_t k = lo + tid / G; k < hi; k += ngrp) {
+          const int64_t i = rows[k];
+          double acc = 0.0;
+          for (int64_t p = S.rowptr[i] + lane; p < S.rowptr[i + 1]; p += G) acc = fma(S.val[p], x[S.col[p]], acc);
+          acc = group_sum<G>(acc, mask);
+          if (lane == 0) x[i] = x[i] + dinv[i] * (b[i] - acc);
+        }
+        grid.sync();
+      }
+    }
+  }
 }
 
 template <int G>
@@ -424,7 +472,8 @@ struct Level {
     if (cfg.corr_kind == CAMG_PT_MCGS) {
       const int nc_ = (int)color_ptr.size() - 1;
       double* x = w_dl.p;
-      if (nl <= kMcgsCtaRows && S->nnz <= kMcgsCtaNnz) {
+      const char* cta_env = getenv("CAMG_MCGS_CTA");
+      if (nl <= kMcgsCtaRows && S->nnz <= kMcgsCtaNnz && !(cta_env && cta_env[0] == '0')) {
         static bool attr = false;
         if (!attr) {
           CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -434,6 +483,20 @@ struct Level {
         note_launch();
         k_mcgs_cta<<<1, 1024, sizeof(double) * nl, s>>>(view(S), color_rows.p, color_ptr_dev.p, nc_, cfg.corr_sweeps,
                                                         rc, dinv_c.p, x);
+        return x;
+      }
+      if (use_coop_mcgs()) {
+        static int blocks_per_sm = -1;
+        if (blocks_per_sm < 0)
+          CAMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_mcgs_coop, 256, 0));
+        const int nb = std::max(1, std::min(blocks_per_sm, 4)) * kNumSMs;
+        CsrView sv = view(S);
+        const int32_t* rp = color_rows.p;
+        const int64_t* cp = color_ptr_dev.p;
+        int ncol = nc_, sweeps = cfg.corr_sweeps;
+        void* args[] = {&sv, &rp, &cp, &ncol, &sweeps, (void*)&rc, (void*)&dinv_c.p, &x};
+        note_launch();
+        CAMG_CUDA(cudaLaunchCooperativeKernel((void*)k_mcgs_coop, dim3(nb), dim3(256), args, 0, s));
         return x;
       }
       // x = 0, then colour 0 of the first sweep needs no product

@@ -423,3 +423,20 @@ def test_graph_disabled_equals_graph():
     z2 = H.apply(g.rhs)
     H.use_graph(True)
     np.testing.assert_array_equal(z1, z2)
+
+
+@pytest.mark.parametrize("path", ["coop", "per-colour"])
+def test_mcgs_large_s_paths(path, monkeypatch):
+    """The MC-SGS corrector paths used for large S~ (cooperative grid-synced
+    sweep, or one launch per colour) against the oracle emulation."""
+    monkeypatch.setenv("CAMG_MCGS_CTA", "0")
+    monkeypatch.setenv("CAMG_COOP_MCGS", "1" if path == "coop" else "0")
+    skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcgs", 1, 1.0))
+    hkw = dict(max_levels=3, max_coarse_size=50)
+    g = generate(config_spec("C5", 10))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    v, ref = H.apply(rhs), OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
