@@ -411,7 +411,7 @@ def run_gpu(args):
     solve = None
     if not args.no_solve:
         # one-time allocation of the cached Krylov basis (n x (restart+1)) outside the timing
-        gmres_device(Am, H, rhs, GmresConfig(rel_tol=0.5, max_iters=1, restart=min(restart, args.max_iters)))
+        gmres_device(Am, H, rhs, GmresConfig(rel_tol=0.5, max_iters=args.max_iters, restart=restart))
         barrier()
         t0 = time.perf_counter()
         x, its, conv, hist = gmres_device(Am, H, rhs, GmresConfig(rel_tol=1e-8, max_iters=args.max_iters,
