@@ -283,28 +283,10 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
 #pragma unroll
               for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
             } else {
-              // all stored values of the slot are loaded first (independent,
-              // predicated on the warp-uniform count), then routed to their
-              // (row, col) by selects -- no per-position branches
-              const int cnt = __popcll(m);
-              double vals[BE];
 #pragma unroll
-              for (int q = 0; q < BE; ++q) vals[q] = (q < cnt) ? __ldcs(v + q * 32) : 0.0;
-              uint64_t mm = m;
-#pragma unroll
-              for (int q = 0; q < BE; ++q) {
-                if (q < cnt) {
-                  const int pos = __ffsll((long long)mm) - 1;
-                  mm &= mm - 1;
-                  const int r = pos / BC, c = pos - (pos / BC) * BC;
-                  double xc = xv[0];
-#pragma unroll
-                  for (int cc = 1; cc < BC; ++cc) xc = (c == cc) ? xv[cc] : xc;
-                  const double pr = vals[q] * xc;
-#pragma unroll
-                  for (int rr = 0; rr < BR; ++rr) acc[rr] += (r == rr) ? pr : 0.0;
-                }
-              }
+              for (int q = 0; q < BE; ++q)
+                if (m & (1ull << q))
+                  acc[q / BC] = fma(__ldcs(v + __popcll(m & ((1ull << q) - 1ull)) * 32), xv[q % BC], acc[q / BC]);
             }
           }
           voff += __popcll(m);
