@@ -1003,10 +1003,13 @@ int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double*
     Level* lv = L->L;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nu = lv->nu;
-    CAMG_CHECK(lv->dinv_p.p != nullptr, CAMG_ERR_CONFIG, "level has no Jacobi predictor");
+    // the smoother's predictor sweep: y_new = y + w D^-1 (b - [K B1][y; lam]),
+    // or Braess-Sarazin's u_half = u + A^-1 r / alpha (no Jacobi predictor)
+    const bool bs = lv->dinv_p.p == nullptr;
+    CAMG_CHECK(mode == 1 || !bs, CAMG_ERR_CONFIG, "level has no Jacobi predictor");
     if (mode == 1) {
-      // the smoother's predictor sweep: y_new = y + w D^-1 (b - [K B1][y; lam])
-      RowEpi e{b, x, nullptr, lv->dinv_p.p, nullptr, lv->w_tmp.p, 1.0};
+      RowEpi e{b, x, nullptr, bs ? lv->ainv.p : lv->dinv_p.p, nullptr, lv->w_tmp.p,
+               bs ? 1.0 / lv->cfg.alpha : 1.0};
       resid_rows(lv->A, int64_t(0), nu, x, x + nu, nu, e, false, s);
     } else {
       jacobi_rows(lv->A, nu, x, b, lv->dinv_p.p, lv->w_du2.p, x, lv->w_tmp.p, 1.0, s);
