@@ -28,7 +28,7 @@ namespace camg {
 namespace {
 
 constexpr int32_t kEmpty = -1;
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 2;  // smem hash per warp: 2-warp blocks pack 3+ blocks per SM
 
 __device__ __forceinline__ uint32_t hslot(int32_t k, uint32_t mask) {
   return ((uint32_t)k * 2654435761u) & mask;
@@ -37,7 +37,7 @@ __device__ __forceinline__ uint32_t hslot(int32_t k, uint32_t mask) {
 // Hash table view (shared or global memory).
 struct Hash {
   int32_t* keys;
-  int32_t* ft;  // first-touch group (may be null)
+  int16_t* ft;  // first-touch group (may be null); R rows are < 32768 long (checked)
   double* vals;
   uint32_t cap;  // power of two
 };
@@ -50,7 +50,7 @@ __device__ __forceinline__ int hash_add(Hash h, int32_t k, double prod, int32_t 
     int32_t cur = atomicCAS(&h.keys[s], kEmpty, k);
     if (cur == kEmpty) {
       h.vals[s] = __dadd_rn(0.0, prod);
-      if (h.ft) h.ft[s] = group;
+      if (h.ft) h.ft[s] = (int16_t)group;
       return 1;
     }
     if (cur == k) {
@@ -275,7 +275,7 @@ __device__ __forceinline__ int chunk_accumulate(Hash h, bool act, int32_t key, d
       if (cur == kEmpty) {
         acc = 0.0;
         ins = 1;
-        if (h.ft) h.ft[slot] = ft;
+        if (h.ft) h.ft[slot] = (int16_t)ft;
         break;
       }
       if (cur == key) { acc = h.vals[slot]; break; }
@@ -312,6 +312,7 @@ __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P,
   hash_clear(h2, lane);
   const int64_t rs = R.rowptr[row], re = R.rowptr[row + 1];
   const int64_t nR = re - rs;
+  if (nR > 32767) return false;  // first-touch groups are 16-bit (never retried to success)
   uint32_t c1 = 0, c2 = 0;
   // ---- stage 1: RA row in R's order, one A-row chunk per step, next chunk prefetched
   for (int64_t w0 = 0; w0 < nR; w0 += 32) {
@@ -369,7 +370,7 @@ __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P,
     const uint32_t sl = base + lane;
     const int32_t k = h1.keys[sl];
     const double v = h1.vals[sl];
-    const int32_t g = h1.ft[sl];
+    const int16_t g = h1.ft[sl];
     const bool keep = (k != kEmpty) && v != 0.0;
     const unsigned bb = __ballot_sync(0xffffffffu, keep);
     __syncwarp();
@@ -396,7 +397,7 @@ __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P,
           const bool desc = (i & k) == 0;
           if ((ka < kb) == desc) {
             int32_t tk = h1.keys[i]; h1.keys[i] = h1.keys[ixj]; h1.keys[ixj] = tk;
-            int32_t tg = h1.ft[i]; h1.ft[i] = h1.ft[ixj]; h1.ft[ixj] = tg;
+            int16_t tg = h1.ft[i]; h1.ft[i] = h1.ft[ixj]; h1.ft[ixj] = tg;
             double tv = h1.vals[i]; h1.vals[i] = h1.vals[ixj]; h1.vals[ixj] = tv;
           }
         }
@@ -479,7 +480,7 @@ __global__ void k_product(CsrView A, CsrView B, bool reverse_a, const double* __
   const int w = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
   const int64_t nw = (int64_t)gridDim.x * kWarpsPerBlock;
-  char* base = GLOBAL ? gscratch + gw * (size_t)cap * 16 : smem + (size_t)w * cap * 16;
+  char* base = GLOBAL ? gscratch + gw * (size_t)cap * 12 : smem + (size_t)w * cap * 12;
   Hash h{reinterpret_cast<int32_t*>(base + (size_t)cap * 8), nullptr, reinterpret_cast<double*>(base), cap};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
@@ -501,11 +502,12 @@ __global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restr
   const int w = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
   const int64_t nw = (int64_t)gridDim.x * kWarpsPerBlock;
-  const size_t per = (size_t)cap1 * 16 + (size_t)cap2 * 16;
+  // per warp: vals f64 | keys i32 | ft i16 (14 B/slot) then vals f64 | keys i32 (12 B/slot)
+  const size_t per = (size_t)cap1 * 14 + (size_t)cap2 * 12;
   char* base = GLOBAL ? gscratch + gw * per : smem + (size_t)w * per;
-  Hash h1{reinterpret_cast<int32_t*>(base + (size_t)cap1 * 8), reinterpret_cast<int32_t*>(base + (size_t)cap1 * 12),
+  Hash h1{reinterpret_cast<int32_t*>(base + (size_t)cap1 * 8), reinterpret_cast<int16_t*>(base + (size_t)cap1 * 12),
           reinterpret_cast<double*>(base), cap1};
-  char* b2 = base + (size_t)cap1 * 16;
+  char* b2 = base + (size_t)cap1 * 14;
   Hash h2{reinterpret_cast<int32_t*>(b2 + (size_t)cap2 * 8), nullptr, reinterpret_cast<double*>(b2), cap2};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
@@ -571,7 +573,7 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
     CAMG_CHECK(c1 <= (1u << 28) && c2 <= (1u << 28), CAMG_ERR_NATIVE, "spgemm: row too large for the hash tables");
     DBuf<int64_t> rows(big.size() + 1);
     CAMG_CUDA(cudaMemcpy(rows.p, big.data(), sizeof(int64_t) * big.size(), cudaMemcpyHostToDevice));
-    const size_t per = (size_t)c1 * 16 + (size_t)c2 * 16;
+    const size_t per = (size_t)c1 * 14 + (size_t)c2 * 12;
     int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>((int64_t)big.size(), (int64_t)(budget / per)));
     warps = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
     DBuf<char> scratch((size_t)warps * per);
@@ -612,7 +614,7 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   // fill: small rows from shared memory (overflow rows are skipped there)
   if (n_rows) launch(true, false, nullptr, n_rows, 0, 0, nullptr, f);
   for (auto& b : batches) {
-    const size_t per = (size_t)b.c1 * 16 + (size_t)b.c2 * 16;
+    const size_t per = (size_t)b.c1 * 14 + (size_t)b.c2 * 12;
     int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(b.n, (int64_t)(budget / per)));
     warps = (warps + kWarpsPerBlock - 1) / kWarpsPerBlock * kWarpsPerBlock;
     DBuf<char> scratch((size_t)warps * per);
@@ -632,7 +634,7 @@ constexpr uint32_t kCap1 = 2048, kCap2 = 512;
 Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s, const double* scale_a) {
   CAMG_CHECK(A->n_cols == B->n_rows, CAMG_ERR_DIMENSION, "sp_matmul: inner dimensions differ");
   CAMG_CHECK(B->n_cols < INT32_MAX, CAMG_ERR_DIMENSION, "too many columns");
-  const size_t smem = (size_t)kWarpsPerBlock * kCapProduct * 16;
+  const size_t smem = (size_t)kWarpsPerBlock * kCapProduct * 12;
   static bool attr = false;
   if (!attr) {
     CAMG_CUDA(cudaFuncSetAttribute(k_product<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -647,7 +649,7 @@ Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStrea
       if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, kCapProduct, nullptr, o);
       else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, kCapProduct, nullptr, o);
     } else {
-      const size_t per = (size_t)c1 * 16 + (size_t)c2 * 16;
+      const size_t per = (size_t)c1 * 14 + (size_t)c2 * 12;
       int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(nrows, (int64_t)((size_t(2) << 30) / per)));
       unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
       if (fill) k_product<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, c1, scratch, o);
@@ -663,7 +665,7 @@ Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B,
 Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
   CAMG_CHECK(R->n_cols == A->n_rows && A->n_cols == P->n_rows, CAMG_ERR_DIMENSION,
              "galerkin_triple: dimension mismatch");
-  const size_t per = (size_t)kCap1 * 16 + (size_t)kCap2 * 16;
+  const size_t per = (size_t)kCap1 * 14 + (size_t)kCap2 * 12;
   const size_t smem = (size_t)kWarpsPerBlock * per;
   static bool attr = false;
   if (!attr) {
@@ -679,7 +681,7 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
       if (fill) k_triple<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, kCap1, kCap2, nullptr, o);
       else k_triple<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, kCap1, kCap2, nullptr, o);
     } else {
-      const size_t pw = (size_t)c1 * 16 + (size_t)c2 * 16;
+      const size_t pw = (size_t)c1 * 14 + (size_t)c2 * 12;
       int64_t warps = std::min<int64_t>(nrows, std::max<int64_t>(kWarpsPerBlock, (int64_t)((size_t(2) << 30) / pw)));
       unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
       if (fill) k_triple<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
