@@ -39,7 +39,8 @@ extern "C" {
 #define CAMG_PT_JACOBI 0
 #define CAMG_PT_DIRECT 3
 #define CAMG_PT_CHEBYSHEV 4 /* GPU-only */
-#define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel */
+#define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel: corrector on S~ (point
+                               colouring), predictor on K (node-block colouring, node_block)    */
 /* A_hat modes: smoothers.py:26 A_HAT_MODES */
 #define CAMG_AHAT_PLAIN 0
 #define CAMG_AHAT_ABS_ROWSUM 1
@@ -62,6 +63,8 @@ typedef struct {
   int corr_kind;      /* corrector PointSmootherConfig.kind                                      */
   int corr_sweeps;
   double corr_damping;
+  int node_block;     /* DOFs per node of the level (uniform contiguous blocks; 1 = none): the
+                         node colouring of a CAMG_PT_MCGS predictor on K                         */
 } camg_smoother_cfg;
 
 /* ---- library ------------------------------------------------------------ */
@@ -193,8 +196,10 @@ int camg_level_set_transfer(camg_level* L, const camg_csr* P_u, const camg_csr* 
  * ncoarse_u columns, R = P^T rows [0,ncoarse_u) in bs_coarse x bs_fine blocks */
 int camg_level_block_transfer(camg_level* L, int bs_fine, int bs_coarse, int64_t ncoarse_u);
 /* one fine-level pass of the dominant smoother kernel (mode 1: fused
- * residual + first Jacobi sweep; mode 2: extra Jacobi sweep) on x, b;
- * returns its algorithmic bytes (SURVEY §8(d) CSR model, and the format's) */
+ * residual + first Jacobi sweep; mode 2: extra Jacobi sweep; mode 3: one
+ * multicolour SGS predictor sweep, forward + backward over all colours) on
+ * x, b; returns its algorithmic bytes (SURVEY §8(d) CSR model, and the
+ * format's) */
 int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double* b, void* stream,
                          double* bytes_csr_model, double* bytes_format);
 /* BlockSmoother.sweep on merged vectors x, b -> out (smoothers.py:316-326) */

@@ -19,7 +19,7 @@ from __future__ import annotations
 
 import time
 import warnings
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 import scipy.linalg
@@ -143,6 +143,7 @@ class PointCfg:
     kind: str = "sgs"
     sweeps: int = 1
     damping: float = 1.0
+    block: int = 1          # mcgs only: DOFs per node of the colouring
 
 
 @dataclass(frozen=True)
@@ -192,11 +193,21 @@ def ilu0_values(A):
     return v
 
 
-def greedy_colors(A):
+def greedy_colors(A, block=1):
     """Greedy colouring of the symmetrised pattern in natural order -- the
     colouring libcamg uses for its multicolour SGS (GPU-only variant, not in
-    the reference; emulated here to check the GPU elementwise)."""
+    the reference; emulated here to check the GPU elementwise).  With
+    block > 1 the nodes of `block` consecutive rows are coloured (node graph:
+    p != q coupled by a non-zero entry) and every row takes its node's
+    colour."""
     A = scipy.sparse.csr_matrix(A)
+    if block > 1:
+        nn = A.shape[0] // block
+        rows = np.repeat(np.arange(A.shape[0]), np.diff(A.indptr)) // block
+        cols = A.indices // block
+        keep = (rows != cols) & (A.data != 0.0)
+        A = scipy.sparse.csr_matrix((np.ones(int(keep.sum())), (rows[keep], cols[keep])), shape=(nn, nn))
+        return np.repeat(greedy_colors(A), block)
     G = (abs(A) + abs(A.T)).tocsr()
     G.sort_indices()
     n = A.shape[0]
@@ -219,7 +230,7 @@ class Point:
         n = A.shape[0]
         if cfg.kind == "mcgs":
             # reference SSOR ("sgs") on the colour-permuted matrix
-            perm = np.argsort(greedy_colors(A), kind="stable")
+            perm = np.argsort(greedy_colors(A, cfg.block), kind="stable")
             self.perm = perm
             self.inner = Point(PointCfg("sgs", cfg.sweeps, cfg.damping), canon(A[perm][:, perm]))
             return
@@ -299,7 +310,7 @@ def schur(op: Saddle, mode, scale=1.0, a_scale=1.0):
 class Block:
     """Bound block smoother (smoothers.py:245-329)."""
 
-    def __init__(self, cfg: BlockCfg, op: Saddle):
+    def __init__(self, cfg: BlockCfg, op: Saddle, node_block: int = 1):
         self.cfg, self.op = cfg, op
         mode = cfg.effective_a_hat_mode()
         if cfg.kind == "uzawa":
@@ -314,7 +325,10 @@ class Block:
         else:
             inv = 1.0 / a_hat(op.K, mode)
             self.ahat_solve = lambda r, inv=inv: inv * r
-        self.pred = None if cfg.kind == "braess_sarazin" else Point(cfg.predictor, op.K)
+        pcfg = cfg.predictor
+        if pcfg.kind == "mcgs" and op.K.shape[0] % max(1, node_block) == 0:
+            pcfg = replace(pcfg, block=max(1, node_block))
+        self.pred = None if cfg.kind == "braess_sarazin" else Point(pcfg, op.K)
         self.corr = Point(cfg.corrector, self.S)
 
     def _uzawa(self, u, lam, bu, bl):                # smoothers.py:285-291
@@ -639,19 +653,31 @@ def coarse_meta(opc: Saddle, cns_u, cagg_u, cns_l, cagg_l, disp: Aggregates, lam
     )
 
 
+def node_block(meta: Meta) -> int:
+    """DOFs per node when every node owns the same consecutive DOF count
+    (2, 3 or 6), else 1 -- the node size of the mcgs predictor colouring."""
+    n = len(meta.u_dof_node)
+    if meta.num_u_nodes == 0 or n % meta.num_u_nodes:
+        return 1
+    bs = n // meta.num_u_nodes
+    if bs not in (2, 3, 6) or not np.array_equal(meta.u_dof_node, np.arange(n) // bs):
+        return 1
+    return bs
+
+
 def setup(op: Saddle, meta: Meta, cfg: HierCfg, scfg: BlockCfg, pre=1, post=1) -> Hier:
     """Level loop (hierarchy.py:180-269)."""
     levels = []
     while True:
         if len(levels) + 1 >= cfg.max_levels or op.n < cfg.max_coarse_size:
-            levels.append(Level(op, Block(scfg, op)))
+            levels.append(Level(op, Block(scfg, op, node_block(meta))))
             break
         ip, ix = node_graph(op.K, meta.u_dof_node, meta.num_u_nodes, meta.node_body, cfg.eps_drop)
         disp = greedy(ip, ix, meta.num_u_nodes, cfg.min_agg_size)
         if disp.num_aggs == 0:
             raise OracleError("no aggregates")
         if disp.num_aggs >= meta.num_u_nodes:
-            levels.append(Level(op, Block(scfg, op)))
+            levels.append(Level(op, Block(scfg, op, node_block(meta))))
             break
         lam = lagrange(disp, meta.mortar, meta.slave_dofs, meta.row_node, meta.lm_node_of_lm_dof)
         if np.any(lam.node_to_agg == UNASSIGNED):
@@ -667,7 +693,7 @@ def setup(op: Saddle, meta: Meta, cfg: HierCfg, scfg: BlockCfg, pre=1, post=1) -
                     u_singletons=disp.singletons, lam_overlap_touches=lam.overlaps,
                     lambda_max=lmax, dropped_ns_columns=dropped,
                     u_agg=disp.node_to_agg, lam_agg=lam.node_to_agg)
-        levels.append(Level(op, Block(scfg, op), Pu, Pl, Ru, Rl, info))
+        levels.append(Level(op, Block(scfg, op, node_block(meta)), Pu, Pl, Ru, Rl, info))
         meta = coarse_meta(opc, cns_u, cagg_u, cns_l, cagg_l, disp, lam, meta)
         op = opc
     lu = lu_factor(levels[-1].op.merged_dense()) if cfg.coarse_solver == "merged_lu" else None

@@ -33,6 +33,7 @@ class SmootherCfg(C.Structure):
         ("kind", C.c_int), ("alpha", f64), ("outer_sweeps", C.c_int), ("a_hat_mode", C.c_int),
         ("pred_kind", C.c_int), ("pred_sweeps", C.c_int), ("pred_damping", f64),
         ("corr_kind", C.c_int), ("corr_sweeps", C.c_int), ("corr_damping", f64),
+        ("node_block", C.c_int),
     ]
 
 

@@ -86,7 +86,8 @@ __global__ void k_block_graph(CsrView K, int bs, int64_t nn, const int8_t* __res
           keep |= eps > 0.0 ? v > eps * sqrt(diag[i] * diag[j]) : v > 0.0;
           ++pos[r];
         }
-      if (keep && best != p && body[best] == body[p]) {
+      // columns past the node range (e.g. B1 in a merged operator) are not nodes
+      if (keep && best != p && best < nn && (!body || body[best] == body[p])) {
         if (FILL) out[o + n] = best;
         ++n;
       }
@@ -95,7 +96,7 @@ __global__ void k_block_graph(CsrView K, int bs, int64_t nn, const int8_t* __res
   }
 }
 
-static Csr* block_graph(const Csr* K, int bs, int64_t nn, const int8_t* body, const double* diag, double eps) {
+Csr* block_graph(const Csr* K, int bs, int64_t nn, const int8_t* body, const double* diag, double eps) {
   cudaStream_t s = 0;
   DBuf<int64_t> cnt(nn + 1);
   note_launch();
@@ -120,6 +121,17 @@ static Csr* block_graph(const Csr* K, int bs, int64_t nn, const int8_t* body, co
 
 __global__ void k_fill_ones(double* v, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = 1.0;
+}
+
+// symmetrised node graph of uniform node blocks: no filter, no bodies, columns
+// past the node range ignored (the multicolour predictor's colouring graph)
+Csr* block_graph_sym(const Csr* K, int bs, int64_t nn) {
+  cudaStream_t s = 0;
+  std::unique_ptr<Csr> G(block_graph(K, bs, nn, nullptr, nullptr, 0.0));
+  note_launch();
+  k_fill_ones<<<grid_for(G->nnz, 256), 256>>>(G->val, G->nnz);
+  std::unique_ptr<Csr> GT(csr_transpose(G.get(), s));
+  return csr_axpby(1.0, G.get(), 1.0, GT.get(), s);
 }
 
 // symmetrised node graph on the device (caller owns the result)

@@ -252,6 +252,83 @@ struct LaunchMcgs {
   }
 };
 
+// Multicolour Gauss-Seidel on the [K | B1] rows of a merged operator (CSR
+// path of the MC-SGS predictor, levels without a colour-ordered SELL): one
+// colour's nodes, the bs DOFs of a node visited in order (backward: reverse)
+// by one lane group, each DOF row reading the values updated before it:
+//   y_i += dinv_i * (b_i - [K B1]_i [y; lam])
+// y is written and re-read inside the kernel: plain (coherent) loads.
+template <int G, bool FWD>
+__global__ void __launch_bounds__(256) k_mcgs_block(CsrView A, const int32_t* __restrict__ nodes, int64_t nn, int bs,
+                                                    const double* __restrict__ xl, int64_t split,
+                                                    const double* __restrict__ b, const double* __restrict__ dinv,
+                                                    double* y) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  for (int64_t k = tid / G; k < nn; k += stride) {
+    const int64_t node = nodes[k];
+    for (int dd = 0; dd < bs; ++dd) {
+      const int64_t i = node * bs + (FWD ? dd : bs - 1 - dd);
+      double acc = 0.0;
+      for (int64_t p = A.rowptr[i] + lane; p < A.rowptr[i + 1]; p += G) {
+        const int32_t c = __ldcs(A.col + p);
+        const double xv = c < split ? y[c] : (xl ? xl[c - split] : 0.0);
+        acc = fma(__ldcs(A.val + p), xv, acc);
+      }
+      acc = group_sum<G>(acc, mask);
+      if (lane == 0) y[i] = y[i] + dinv[i] * (b[i] - acc);
+      __syncwarp(mask);
+    }
+  }
+}
+
+template <int G>
+struct LaunchMcgsBlock {
+  static void run(const Csr* A, const int32_t* nodes, int64_t nn, int bs, const double* xl, int64_t split,
+                  const double* b, const double* dinv, double* y, bool fwd, cudaStream_t s) {
+    if (nn <= 0) return;
+    unsigned grid = grid_for(nn * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    if (fwd) k_mcgs_block<G, true><<<grid, 256, 0, s>>>(view(A), nodes, nn, bs, xl, split, b, dinv, y);
+    else k_mcgs_block<G, false><<<grid, 256, 0, s>>>(view(A), nodes, nn, bs, xl, split, b, dinv, y);
+  }
+};
+
+// y = x_u (zero if x is null), g = b_u
+__global__ void k_gs_init(int64_t nu, const double* __restrict__ x, const double* __restrict__ b,
+                          double* __restrict__ y, double* __restrict__ g) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nu; i += (int64_t)gridDim.x * blockDim.x) {
+    y[i] = x ? x[i] : 0.0;
+    g[i] = b[i];
+  }
+}
+
+// g_i -= B1_i . lam on the nonempty rows of B1 (g = b_u - B1 lam)
+__global__ void k_b1_sub(CsrView B1, const int64_t* __restrict__ rows, int64_t nrows, const double* __restrict__ lam,
+                         double* __restrict__ g) {
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 7;
+  const unsigned mask = group_mask<8>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / 8;
+  for (int64_t k = tid / 8; k < nrows; k += stride) {
+    const int64_t i = rows[k];
+    double acc = row_dot<8, false>(B1, i, lam, nullptr, B1.n_cols, lane);
+    acc = group_sum<8>(acc, mask);
+    if (lane == 0) g[i] = g[i] - acc;
+  }
+}
+
+// Uzawa relaxation: out = x0 + alpha (y - x0)   (x0 null = 0)
+__global__ void k_relax(int64_t n, const double* __restrict__ x0, const double* __restrict__ y, double alpha,
+                        double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double o = x0 ? x0[i] : 0.0;
+    out[i] = o + alpha * (y[i] - o);
+  }
+}
+
 // x_out_lam = x_lam + coef*dl
 __global__ void k_lam_update(int64_t nl, const double* __restrict__ xl, const double* __restrict__ dl, double coef,
                              double* __restrict__ out) {
@@ -438,6 +515,13 @@ struct Level {
   std::vector<int64_t> color_ptr;
   DBuf<int64_t> color_ptr_dev;
   DBuf<int32_t> color_rows;
+  // multicolour Gauss-Seidel predictor on K: nodes of pbs DOFs grouped by
+  // colour (CSR path), or a colour-ordered block SELL of K (slices per colour)
+  int pbs = 1;
+  std::vector<int64_t> pcol_ptr, pcol_slice;
+  DBuf<int32_t> pnodes;
+  Sell* gs_sell = nullptr;
+  DBuf<double> w_g;
   // direct corrector
   DBuf<double> corr_lu;
   DBuf<int32_t> corr_piv;
@@ -448,7 +532,7 @@ struct Level {
   int64_t nnz_top = 0;  // entries of the [K | B1] rows
   // work vectors
   DBuf<double> w_du, w_du2, w_ru, w_rc, w_dl, w_dl2, w_rl, w_tmp;
-  ~Level() { if (owns_A) delete A; delete B1; delete S; delete P; delete R; }
+  ~Level() { if (owns_A) delete A; delete B1; delete S; delete P; delete R; delete gs_sell; }
 
   void alloc_work() {
     w_du = DBuf<double>(n);
@@ -523,6 +607,46 @@ struct Level {
     return cur;
   }
 
+  int pred_colors() const { return (int)pcol_ptr.size() - 1; }
+
+  // one colour pass of the MC-SGS predictor (b: rhs of the CSR path, which
+  // reads lambda through the merged rows; the SELL path reads g = b_u - B1 lam)
+  void gs_pass(int c, bool fwd, bool zero, const double* xl, const double* b, double* y, cudaStream_t s) {
+    if (gs_sell) {
+      sell_gs_launch(gs_sell, pcol_slice[c], pcol_slice[c + 1], fwd, zero, nullptr, nu, w_g.p, dinv_p.p, y, s);
+    } else {
+      dispatch_g<LaunchMcgsBlock>(A->avg_row, A, pnodes.p + pcol_ptr[c], pcol_ptr[c + 1] - pcol_ptr[c], pbs, xl, nu,
+                                  b, dinv_p.p, y, fwd, s);
+    }
+  }
+
+  // MC-SGS predictor in iterate form: y_0 = u, then pred_sweeps forward +
+  // backward colour sweeps of Gauss-Seidel on K y = b_u - B1 lam -- the
+  // reference's zero-start SSOR correction on r_u (smoothers.py:186-199) with
+  // u added back, on the colour-permuted K
+  void gs_predict(const double* x, const double* b, double* y, int sweeps, cudaStream_t s) {
+    const bool zero = (x == nullptr);
+    const double* xl = x ? x + nu : nullptr;
+    const int nc = pred_colors();
+    if (gs_sell) {
+      note_launch();
+      k_gs_init<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, b, y, w_g.p);
+      if (xl && n_b1_rows) {
+        note_launch();
+        k_b1_sub<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, xl, w_g.p);
+      }
+    } else if (zero) {
+      CAMG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * nu, s));
+    } else {
+      note_launch();
+      k_copy<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, y);
+    }
+    for (int k = 0; k < sweeps; ++k) {
+      for (int c = 0; c < nc; ++c) gs_pass(c, true, zero && k == 0 && c == 0, xl, b, y, s);
+      for (int c = nc - 1; c >= 0; --c) gs_pass(c, false, false, xl, b, y, s);
+    }
+  }
+
   // one algorithmic smoother step: xo = step(x, b); x == nullptr means zero
   void step(const double* x, const double* b, double* xo, cudaStream_t s) {
     const bool zero = (x == nullptr);
@@ -537,6 +661,15 @@ struct Level {
       // u_half = u + (A^-1 r_u) / alpha   (smoothers.py:296)
       RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
       resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+    } else if (cfg.pred_kind == CAMG_PT_MCGS) {
+      // Uzawa keeps y for the lambda side and relaxes u_new = u + alpha (y - u)
+      double* y = (kind == CAMG_UZAWA) ? w_du.p : xo;
+      gs_predict(x, b, y, sp, s);
+      if (kind == CAMG_UZAWA) {
+        note_launch();
+        k_relax<<<grid_for(nu, 256), 256, 0, s>>>(nu, xu, y, alpha, xo);
+        uh = y;
+      }
     } else {
       // Jacobi predictor in iterate form: y_0 = u, y_k = y_{k-1} + w D^-1
       // (b_u - K y_{k-1} - B1 lam) -- the reference's zero-start correction
@@ -651,13 +784,84 @@ static void greedy_coloring(const Csr* S, std::vector<int64_t>& color_ptr, DBuf<
   CAMG_CUDA(cudaMemcpy(rows_out.p, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
 }
 
+Csr* block_graph_sym(const Csr* K, int bs, int64_t nn);
+
+// Greedy colouring of the nodes (bs consecutive DOFs) of K in natural node
+// order over the symmetrised node graph (nodes p != q coupled by a non-zero
+// K entry); the multicolour predictor's colouring, emulated by the oracle.
+static std::vector<int32_t> node_colors(const Csr* K, int64_t nu, int bs) {
+  const int64_t nn = nu / bs;
+  std::unique_ptr<Csr> Gs(block_graph_sym(K, bs, nn));
+  std::vector<int64_t> rp(nn + 1);
+  std::vector<int32_t> ci(Gs->nnz);
+  CAMG_CUDA(cudaMemcpy(rp.data(), Gs->rowptr, sizeof(int64_t) * (nn + 1), cudaMemcpyDeviceToHost));
+  if (Gs->nnz) CAMG_CUDA(cudaMemcpy(ci.data(), Gs->col, sizeof(int32_t) * Gs->nnz, cudaMemcpyDeviceToHost));
+  if (getenv("CAMG_DEBUG"))
+    fprintf(stderr, "[camg] node graph: %lld nodes, %lld edges\n", (long long)nn, (long long)Gs->nnz);
+  std::vector<int32_t> color(nn, -1);
+  std::vector<int64_t> seen(64, -1);  // seen[c] == i: colour c is taken by a neighbour of i
+  for (int64_t i = 0; i < nn; ++i) {
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int32_t c = color[ci[k]];
+      if (c >= 0) {
+        if (c >= (int32_t)seen.size()) seen.resize(2 * c + 2, -1);
+        seen[c] = i;
+      }
+    }
+    int32_t c = 0;
+    while (c < (int32_t)seen.size() && seen[c] == i) ++c;
+    color[i] = c;
+  }
+  return color;
+}
+
+static void setup_gs_predictor(Level* L, const Csr* K, int node_block, cudaStream_t s) {
+  const int64_t nu = L->nu;
+  int bs = node_block > 1 ? node_block : 1;
+  if (nu % bs) bs = 1;
+  L->pbs = bs;
+  const int64_t nn = nu / bs;
+  std::vector<int32_t> color = node_colors(K, nu, bs);
+  int ncol = 0;
+  for (int32_t c : color) ncol = std::max(ncol, c + 1);
+  if (getenv("CAMG_DEBUG"))
+    fprintf(stderr, "[camg] mcgs predictor: %lld nodes of %d DOFs, %d colours\n", (long long)nn, bs, ncol);
+  L->pcol_ptr.assign(ncol + 1, 0);
+  for (int32_t c : color) L->pcol_ptr[c + 1]++;
+  for (int c = 0; c < ncol; ++c) L->pcol_ptr[c + 1] += L->pcol_ptr[c];
+  std::vector<int32_t> nodes(nn);
+  {
+    std::vector<int64_t> pos(L->pcol_ptr.begin(), L->pcol_ptr.end() - 1);
+    for (int64_t i = 0; i < nn; ++i) nodes[pos[color[i]]++] = (int32_t)i;
+  }
+  L->pnodes = DBuf<int32_t>(nn + 1);
+  CAMG_CUDA(cudaMemcpy(L->pnodes.p, nodes.data(), sizeof(int32_t) * nn, cudaMemcpyHostToDevice));
+  // colour-ordered SELL from kGsSellMinRows rows (CAMG_GS_SELL=1 forces it,
+  // =0 keeps the CSR path)
+  const char* env = getenv("CAMG_GS_SELL");
+  const bool want = env ? env[0] == '1' : nu >= kGsSellMinRows;
+  if (want && (bs == 1 || bs == 2 || bs == 3 || bs == 6)) {
+    // positions: each colour's nodes in ascending order, padded to whole slices
+    std::vector<int32_t> order;
+    L->pcol_slice.assign(ncol + 1, 0);
+    for (int c = 0; c < ncol; ++c) {
+      for (int64_t k = L->pcol_ptr[c]; k < L->pcol_ptr[c + 1]; ++k) order.push_back(nodes[k]);
+      while (order.size() % 32) order.push_back(-1);
+      L->pcol_slice[c + 1] = (int64_t)order.size() / 32;
+    }
+    L->gs_sell = sell_build_ordered(K, bs, nu, nu, order, s);
+    L->w_g = DBuf<double>(nu + 1);
+  }
+}
+
 Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, const camg_smoother_cfg& cfg, int pre,
                     int post, Csr* A_shared) {
   CAMG_CHECK(cfg.kind >= CAMG_UZAWA && cfg.kind <= CAMG_SIMPLEC, CAMG_ERR_CONFIG, "unknown block smoother kind");
   CAMG_CHECK(cfg.alpha > 0.0, CAMG_ERR_CONFIG, "alpha must be positive");
   CAMG_CHECK(cfg.outer_sweeps >= 1, CAMG_ERR_CONFIG, "outer_sweeps must be >= 1");
-  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI, CAMG_ERR_CONFIG,
-             "GPU predictor supports jacobi");
+  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI || cfg.pred_kind == CAMG_PT_MCGS,
+             CAMG_ERR_CONFIG, "GPU predictor supports jacobi and mcgs");
+  CAMG_CHECK(cfg.pred_sweeps >= 1, CAMG_ERR_CONFIG, "predictor sweeps must be >= 1");
   CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT || cfg.corr_kind == CAMG_PT_MCGS,
              CAMG_ERR_CONFIG, "GPU corrector supports jacobi, mcgs and direct");
   cudaStream_t s = 0;
@@ -716,6 +920,7 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     }
     L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
   }
+  if (cfg.kind != CAMG_BRAESS_SARAZIN && cfg.pred_kind == CAMG_PT_MCGS) setup_gs_predictor(L.get(), K, cfg.node_block, s);
   if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) {
     greedy_coloring(L->S, L->color_ptr, L->color_rows);
     L->color_ptr_dev = DBuf<int64_t>(L->color_ptr.size());
@@ -1007,6 +1212,27 @@ int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double*
     // or Braess-Sarazin's u_half = u + A^-1 r / alpha (no Jacobi predictor)
     const bool bs = lv->dinv_p.p == nullptr;
     CAMG_CHECK(mode == 1 || !bs, CAMG_ERR_CONFIG, "level has no Jacobi predictor");
+    CAMG_CHECK(mode != 3 || lv->pred_colors() > 0, CAMG_ERR_CONFIG, "level has no multicolour predictor");
+    if (mode == 3) {
+      lv->gs_predict(x, b, lv->w_tmp.p, 1, s);
+      CAMG_LAUNCH_CHECK();
+      // two passes over K: matrix + x read + y written + b, D^-1 read; the
+      // init pass reads x_u, b_u and writes y, g; lambda via B1 is < 0.1%
+      const double nnzK = (double)(lv->nnz_top - lv->B1->nnz);
+      const double vec = 4.0 * 8.0 * nu;
+      const double pass = 12.0 * nnzK + 4.0 * (nu + 1) + vec;
+      if (bytes_csr_model) *bytes_csr_model = 2.0 * pass + 32.0 * nu;
+      if (bytes_format) {
+        if (lv->gs_sell) {
+          const int br = lv->gs_sell->br;
+          *bytes_format = 2.0 * (sell_pass_bytes(lv->gs_sell) + vec + 4.0 * lv->gs_sell->nbr +
+                                 8.0 * (br * (br - 1) / 2) * (double)(nu / br)) + 32.0 * nu;
+        } else {
+          *bytes_format = 2.0 * (12.0 * (double)lv->nnz_top + 8.0 * (nu + 1) + vec) + 16.0 * nu;
+        }
+      }
+      return;
+    }
     if (mode == 1) {
       RowEpi e{b, x, nullptr, bs ? lv->ainv.p : lv->dinv_p.p, nullptr, lv->w_tmp.p,
                bs ? 1.0 / lv->cfg.alpha : 1.0};
@@ -1086,15 +1312,22 @@ int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, dou
       const double top = (double)L->nnz_top;
       const camg_smoother_cfg& c = L->cfg;
       const int sp = (c.kind == CAMG_BRAESS_SARAZIN) ? 1 : c.pred_sweeps;
-      // one predictor sweep over [K | B1]: matrix + x read + (b, D^-1, y out)
-      const double sweep = spm(L->A, L->nu, top) + 8.0 * 2 * L->nu;
+      // one predictor sweep over [K | B1]: matrix + x read + (b, D^-1, y out);
+      // a multicolour SGS sweep is two such passes (forward, backward) plus
+      // the per-step init of y (and g) from x, b
+      const bool gs = c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_MCGS;
+      const double sweep = gs ? 2.0 * (spm(L->A, L->nu, top) + 8.0 * 2 * L->nu)
+                              : spm(L->A, L->nu, top) + 8.0 * 2 * L->nu;
       // lambda side: B2/Cz rows, corrector sweeps over S~ (MCGS: forward +
       // backward), interface-row B1 correction, a few lambda vectors
       const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps : std::max(0, c.corr_sweeps - 1);
       const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
                          (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
-      const double step = sp * sweep + lam;
-      const double step0 = step - 12.0 * top - 8.0 * L->n;  // zero start: first sweep reads no matrix / x
+      const double step = sp * sweep + lam + (gs ? 32.0 * L->nu + (c.kind == CAMG_UZAWA ? 24.0 * L->nu : 0.0) : 0.0);
+      // zero start: the first sweep reads no matrix / x (MC-SGS: only its
+      // first colour is skipped)
+      const double step0 = gs ? step - (12.0 * top + 8.0 * L->n) / std::max(1, L->pred_colors())
+                              : step - 12.0 * top - 8.0 * L->n;
       int nsteps_pre = L->pre * c.outer_sweeps, nsteps_post = L->post * c.outer_sweeps;
       if (l == nl - 1) {
         if (H->coarse_solver == CAMG_COARSE_MERGED_LU) total += 8.0 * H->n_coarse * H->n_coarse + 16.0 * H->n_coarse;

@@ -34,6 +34,8 @@ Sell::~Sell() {
   dfree(bval);
   dfree(mask);
   dfree(voff);
+  dfree(perm);
+  dfree(dblk);
 }
 
 namespace {
@@ -72,16 +74,18 @@ __device__ int for_blocks(const CsrView& A, int64_t p, F f) {
 }
 
 template <int BR, int BC>
-__global__ void k_sell_count(CsrView A, int64_t nbr, int64_t ncols_blocked, uint8_t* __restrict__ len,
-                             int32_t* __restrict__ overflow) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+__global__ void k_sell_count(CsrView A, int64_t nbr, int64_t ncols_blocked, const int32_t* __restrict__ perm,
+                             uint8_t* __restrict__ len, int32_t* __restrict__ overflow) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nbr; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = perm ? perm[t] : t;  // position t holds block row p (-1: padding)
+    if (p < 0) { len[t] = 0; continue; }
     for (int r = 0; r < BR; ++r) {
       const int64_t e = A.rowptr[p * BR + r + 1];
       if (e > A.rowptr[p * BR + r] && A.col[e - 1] >= ncols_blocked) atomicExch(overflow, 1);
     }
     int n = for_blocks<BR, BC>(A, p, [](int, int32_t, int, int, double) {});
     if (n > 255) { atomicExch(overflow, 2); n = 255; }
-    len[p] = (uint8_t)n;
+    len[t] = (uint8_t)n;
   }
 }
 
@@ -114,20 +118,25 @@ __global__ void k_slot_popc(const unsigned long long* __restrict__ mask, int64_t
 }
 
 template <int BR, int BC>
-__global__ void k_sell_fill(CsrView A, int64_t nbr, const int64_t* __restrict__ slice_ptr,
-                            const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
-                            int32_t* __restrict__ bcol, double* __restrict__ bval) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
-    const int lane = (int)(p & 31);
-    const int64_t base = slice_ptr[p >> 5];
-    const int64_t width = slice_ptr[(p >> 5) + 1] - base;
-    int n = for_blocks<BR, BC>(A, p, [&](int k, int32_t bc, int r, int c, double v) {
+__global__ void k_sell_fill(CsrView A, int64_t nbr, const int32_t* __restrict__ perm,
+                            const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ mask,
+                            const int64_t* __restrict__ voff, int32_t* __restrict__ bcol, double* __restrict__ bval,
+                            double* __restrict__ dblk) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nbr; t += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = (int)(t & 31);
+    const int64_t base = slice_ptr[t >> 5];
+    const int64_t width = slice_ptr[(t >> 5) + 1] - base;
+    const int64_t p = perm ? perm[t] : t;
+    int n = 0;
+    if (p >= 0) n = for_blocks<BR, BC>(A, p, [&](int k, int32_t bc, int r, int c, double v) {
       const int64_t slot = base + k;
       if (r < 0) {
         bcol[slot * 32 + lane] = bc;
         return;
       }
       const int e = r * BC + c;
+      // diagonal node block, [slice][entry][lane] (Gauss-Seidel within the node)
+      if (dblk && bc == p) dblk[((t >> 5) * (BR * BC) + e) * 32 + lane] = v;
       const uint64_t m = mask[slot];
       const int64_t idx = voff[slot] + __popcll(m & ((1ull << e) - 1ull));
       bval[idx * 32 + lane] = v;
@@ -137,9 +146,12 @@ __global__ void k_sell_fill(CsrView A, int64_t nbr, const int64_t* __restrict__ 
 }
 
 template <int BR, int BC>
-Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cudaStream_t s) {
+Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cudaStream_t s,
+            const std::vector<int32_t>* order = nullptr) {
   constexpr int BE = BR * BC;
-  const int64_t nbr = nrows / BR;
+  // natural order: position = block row; with `order`: position t holds
+  // block row order[t] (-1 = padding lane) and the diagonal blocks are kept
+  const int64_t nbr = order ? (int64_t)order->size() : nrows / BR;
   const int64_t nslices = (nbr + 31) / 32;
   std::unique_ptr<Sell> S(new Sell());
   S->br = BR;
@@ -147,10 +159,16 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   S->nbr = nbr;
   S->nslices = nslices;
   S->len = dalloc<uint8_t>(nbr + 1);
+  if (order) {
+    S->perm = dalloc<int32_t>(nbr + 1);
+    CAMG_CUDA(cudaMemcpy(S->perm, order->data(), sizeof(int32_t) * nbr, cudaMemcpyHostToDevice));
+    S->dblk = dalloc<double>((size_t)nslices * BE * 32 + 1);
+    CAMG_CUDA(cudaMemsetAsync(S->dblk, 0, sizeof(double) * ((size_t)nslices * BE * 32 + 1), s));
+  }
   DBuf<int32_t> ovf(1);
   CAMG_CUDA(cudaMemset(ovf.p, 0, sizeof(int32_t)));
   note_launch();
-  k_sell_count<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, ncols_blocked, S->len, ovf.p);
+  k_sell_count<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, ncols_blocked, S->perm, S->len, ovf.p);
   int32_t h_ovf = 0;
   CAMG_CUDA(cudaMemcpy(&h_ovf, ovf.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
   CAMG_CHECK(h_ovf != 2, CAMG_ERR_ARG, "block row with more than 255 blocks");
@@ -185,8 +203,8 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   S->bval = dalloc<double>((size_t)groups * 32);
   CAMG_CUDA(cudaMemsetAsync(S->bval, 0, sizeof(double) * (size_t)groups * 32, s));
   note_launch();
-  k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->mask, S->voff, S->bcol,
-                                                         S->bval);
+  k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->perm, S->slice_ptr, S->mask, S->voff,
+                                                         S->bcol, S->bval, S->dblk);
   CAMG_LAUNCH_CHECK();
   CAMG_CUDA(cudaStreamSynchronize(s));
   // compulsory bytes of one pass: for every row, its blocks' stored values and
@@ -221,6 +239,18 @@ Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_bloc
   CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
 #undef CAMG_SELL_CASE
   throw Error(CAMG_ERR_ARG, "unsupported block shape");
+}
+
+Sell* sell_build_ordered(const Csr* A, int bs, int64_t nrows, int64_t ncols_blocked, const std::vector<int32_t>& order,
+                         cudaStream_t s) {
+  CAMG_CHECK(order.size() % 32 == 0, CAMG_ERR_ARG, "ordered SELL positions must fill whole slices");
+  CAMG_CHECK(nrows % bs == 0 && nrows <= A->n_rows && ncols_blocked % bs == 0, CAMG_ERR_DIMENSION,
+             "block rows must divide the row range");
+  if (bs == 1) return build<1, 1>(A, nrows, ncols_blocked, false, s, &order);
+  if (bs == 2) return build<2, 2>(A, nrows, ncols_blocked, false, s, &order);
+  if (bs == 3) return build<3, 3>(A, nrows, ncols_blocked, false, s, &order);
+  if (bs == 6) return build<6, 6>(A, nrows, ncols_blocked, false, s, &order);
+  throw Error(CAMG_ERR_ARG, "unsupported node block size");
 }
 
 // ---------------------------------------------------------------------------
@@ -446,6 +476,105 @@ void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const dou
 }
 
 double sell_pass_bytes(const Sell* S) { return S->pass_bytes; }
+
+// ---------------------------------------------------------------------------
+// Multicolour Gauss-Seidel on a colour-ordered SELL (slices [s0, s1) hold the
+// block rows of one colour; rows of one colour share no entries, so each lane
+// updates its node in place).  Within a node the BR DOFs are visited in order
+// (backward: reverse order): every off-node product and the node's own block
+// use the values from before this pass (acc), and the DOFs already updated
+// in this pass enter through the stored diagonal block:
+//   dv_d = dinv_d * (b_d - acc_d - sum_{e before d} K_de dv_e),  y_d += dv_d
+// which is the sequential Gauss-Seidel update of SSOR (smoothers.py:155-164)
+// on the colour-permuted matrix.  Columns >= split read xl (lambda; null = 0).
+template <int BR, bool FWD, bool ZERO>
+__global__ void __launch_bounds__(256) k_sell_gs(SellView S, const int32_t* __restrict__ perm,
+                                                 const double* __restrict__ dblk, int64_t s0, int64_t s1,
+                                                 const double* __restrict__ xl, int64_t split_blocks,
+                                                 const double* __restrict__ b, const double* __restrict__ dinv,
+                                                 double* y) {
+  constexpr int BE = BR * BR;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // no address this kernel writes is read by another lane (same-colour rows
+  // are uncoupled), so the read-only path is safe for y
+  const double* __restrict__ yr = y;
+  for (int64_t s = s0 + warp; s < s1; s += nwarps) {
+    const int64_t t = s * 32 + lane;
+    const int32_t p = perm[t];
+    double acc[BR];
+#pragma unroll
+    for (int r = 0; r < BR; ++r) acc[r] = 0.0;
+    if (!ZERO) {
+      const int n = S.len[t];
+      const int64_t base = S.slice_ptr[s];
+      for (int k = 0; k < n; ++k) {
+        const int64_t slot = base + k;
+        const int32_t bc = __ldcs(S.bcol + slot * 32 + lane);
+        const double* xs;
+        if (bc < split_blocks) xs = yr + (int64_t)bc * BR;
+        else xs = xl ? xl + ((int64_t)bc - split_blocks) * BR : nullptr;
+        double xv[BR];
+#pragma unroll
+        for (int c = 0; c < BR; ++c) xv[c] = xs ? __ldg(xs + c) : 0.0;
+        const double* v = S.bval + slot * (BE * 32) + lane;
+#pragma unroll
+        for (int q = 0; q < BE; ++q) acc[q / BR] = fma(__ldcs(v + q * 32), xv[q % BR], acc[q / BR]);
+      }
+    }
+    if (p < 0) continue;
+    const double* db = dblk + s * (BE * 32) + lane;
+    double dv[BR];
+#pragma unroll
+    for (int dd = 0; dd < BR; ++dd) {
+      const int d = FWD ? dd : BR - 1 - dd;
+      double corr = 0.0;
+#pragma unroll
+      for (int ee = 0; ee < dd; ++ee) {
+        const int e = FWD ? ee : BR - 1 - ee;
+        corr = fma(__ldg(db + (d * BR + e) * 32), dv[e], corr);
+      }
+      const int64_t i = (int64_t)p * BR + d;
+      dv[d] = __ldg(dinv + i) * ((__ldg(b + i) - acc[d]) - corr);
+    }
+#pragma unroll
+    for (int d = 0; d < BR; ++d) {
+      const int64_t i = (int64_t)p * BR + d;
+      y[i] = (ZERO ? 0.0 : y[i]) + dv[d];
+    }
+  }
+}
+
+template <int BR>
+static void launch_gs(const Sell* S, int64_t s0, int64_t s1, bool fwd, bool zero, const double* xl, int64_t split,
+                      const double* b, const double* dinv, double* y, cudaStream_t st) {
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->nbr, S->nslices};
+  const unsigned grid = grid_for((s1 - s0) * 32, 256, int64_t(kNumSMs) * 16);
+  const int64_t sb = split / BR;
+  note_launch();
+  if (zero) {
+    if (fwd) k_sell_gs<BR, true, true><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+    else k_sell_gs<BR, false, true><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+  } else {
+    if (fwd) k_sell_gs<BR, true, false><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+    else k_sell_gs<BR, false, false><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+  }
+  CAMG_LAUNCH_CHECK();
+}
+
+void sell_gs_launch(const Sell* S, int64_t s0, int64_t s1, bool fwd, bool zero, const double* xl, int64_t split,
+                    const double* b, const double* dinv, double* y, cudaStream_t st) {
+  if (s1 <= s0) return;
+  CAMG_CHECK(S->perm && S->dblk && S->br == S->bc, CAMG_ERR_NATIVE, "not a colour-ordered SELL");
+  switch (S->br) {
+    case 1: return launch_gs<1>(S, s0, s1, fwd, zero, xl, split, b, dinv, y, st);
+    case 2: return launch_gs<2>(S, s0, s1, fwd, zero, xl, split, b, dinv, y, st);
+    case 3: return launch_gs<3>(S, s0, s1, fwd, zero, xl, split, b, dinv, y, st);
+    case 6: return launch_gs<6>(S, s0, s1, fwd, zero, xl, split, b, dinv, y, st);
+    default: throw Error(CAMG_ERR_NATIVE, "bad SELL block size");
+  }
+}
 
 }  // namespace camg
 

@@ -1,5 +1,7 @@
 // Block SELL-32 acceleration mirror (see sell.cu).
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace camg {
@@ -15,6 +17,8 @@ struct Sell {
   double* bval = nullptr;             // [voff[slot] + rank in mask][lane]
   unsigned long long* mask = nullptr; // per slot: union of the block patterns of its lanes
   int64_t* voff = nullptr;            // per slot: offset of its value groups (32 doubles each)
+  int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
+  double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]
   ~Sell();
   int64_t rows() const { return nbr * br; }
 };
@@ -55,5 +59,12 @@ Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_bloc
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                  const SellEpi& e, cudaStream_t st);
 double sell_pass_bytes(const Sell* S);
+// colour-ordered SELL (square bs x bs blocks, full): position t of the
+// mirror holds block row order[t] (-1 = padding), order.size() % 32 == 0
+Sell* sell_build_ordered(const Csr* A, int bs, int64_t nrows, int64_t ncols_blocked, const std::vector<int32_t>& order,
+                         cudaStream_t s);
+// one colour pass of multicolour Gauss-Seidel over slices [s0, s1)
+void sell_gs_launch(const Sell* S, int64_t s0, int64_t s1, bool fwd, bool zero, const double* xl, int64_t split,
+                    const double* b, const double* dinv, double* y, cudaStream_t st);
 
 }  // namespace camg

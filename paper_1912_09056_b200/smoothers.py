@@ -8,10 +8,13 @@ reference names, defaults and validation (smoothers.py:29-70).
 Inner solves on the GPU: `jacobi` (predictor and corrector) and `direct`
 (corrector, dense LU of S~).  The reference's lexicographic `sgs` / `ilu0`
 are sequential; they are rejected here with ConfigError.  The GPU variant
-`mcgs` (corrector on S~) is the reference's residual-form SSOR applied to
-S~ with rows renumbered by a greedy colouring: multicolour symmetric
-Gauss-Seidel, compared with the reference SGS by convergence, and
-elementwise with the oracle's emulation of the same colouring.
+`mcgs` is the reference's residual-form SSOR applied with rows renumbered by
+a greedy colouring: multicolour symmetric Gauss-Seidel, compared with the
+reference SGS by convergence, and elementwise with the oracle's emulation of
+the same colouring.  As corrector it colours the rows of S~; as predictor it
+colours the nodes of K (`node_block` consecutive DOFs per node, visited in
+order within a node), which is the block Gauss-Seidel the paper's Uzawa / BGS
+configurations use on the GPU.
 """
 
 from __future__ import annotations
@@ -40,6 +43,7 @@ POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct", "mcgs")
 BLOCK_KINDS = ("uzawa", "braess_sarazin", "simple", "simplec")
 A_HAT_MODES = ("plain_diag", "abs_rowsum", "exact")
 GPU_POINT_KINDS = ("jacobi", "direct")
+GPU_PREDICTOR_KINDS = ("jacobi", "mcgs")
 GPU_CORRECTOR_KINDS = ("jacobi", "direct", "mcgs")
 
 _BLOCK_CODE = {"uzawa": 0, "braess_sarazin": 1, "simple": 2, "simplec": 3}
@@ -96,12 +100,12 @@ class SchurOperator:
     a_hat_inv_diag: np.ndarray | None
 
 
-def native_cfg(cfg: BlockSmootherConfig) -> N.SmootherCfg:
+def native_cfg(cfg: BlockSmootherConfig, node_block: int = 1) -> N.SmootherCfg:
     mode = cfg.effective_a_hat_mode()
     if mode == "exact":
         raise ConfigError("a_hat_mode 'exact' (dense K inverse) is not available on the GPU path")
-    if cfg.kind != "braess_sarazin" and cfg.predictor.kind != "jacobi":
-        raise ConfigError(f"GPU predictor supports {('jacobi',)}, got {cfg.predictor.kind!r}")
+    if cfg.kind != "braess_sarazin" and cfg.predictor.kind not in GPU_PREDICTOR_KINDS:
+        raise ConfigError(f"GPU predictor supports {GPU_PREDICTOR_KINDS}, got {cfg.predictor.kind!r}")
     if cfg.corrector.kind not in GPU_CORRECTOR_KINDS:
         raise ConfigError(f"GPU corrector supports {GPU_CORRECTOR_KINDS}, got {cfg.corrector.kind!r}")
     return N.SmootherCfg(
@@ -110,7 +114,7 @@ def native_cfg(cfg: BlockSmootherConfig) -> N.SmootherCfg:
         pred_kind=_POINT_CODE.get(cfg.predictor.kind, 0), pred_sweeps=int(cfg.predictor.sweeps),
         pred_damping=float(cfg.predictor.damping),
         corr_kind=_POINT_CODE[cfg.corrector.kind], corr_sweeps=int(cfg.corrector.sweeps),
-        corr_damping=float(cfg.corrector.damping),
+        corr_damping=float(cfg.corrector.damping), node_block=max(1, int(node_block)),
     )
 
 
@@ -187,17 +191,21 @@ def build_schur(op, a_hat_mode: str = "plain_diag", alpha: float = 1.0, scale_wi
 
 
 class BlockSmoother:
-    """Bound block smoother (smoothers.py:245-329), executed by libcamg."""
+    """Bound block smoother (smoothers.py:245-329), executed by libcamg.
+
+    `node_block` (extension): DOFs per node of the level when every node owns
+    that many consecutive DOFs; it sets the node colouring of an `mcgs`
+    predictor (1 = colour single DOFs)."""
 
     def __init__(self, cfg: BlockSmootherConfig, op, predictor_solver=None, pre_sweeps: int = 1,
-                 post_sweeps: int = 1):
+                 post_sweeps: int = 1, node_block: int = 1):
         if isinstance(op, SaddleSystem):
             op = op.op
         if predictor_solver is not None:
             raise ConfigError("custom predictor solvers are not supported on the GPU path")
         self.cfg = cfg
         self.op = op
-        ncfg = native_cfg(cfg)
+        ncfg = native_cfg(cfg, node_block)
         h = C.c_void_p()
         # the level borrows the operator's merged matrix (one device copy shared
         # with GMRES); self.op keeps it alive

@@ -440,3 +440,58 @@ def test_mcgs_large_s_paths(path, monkeypatch):
     OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
     v, ref = H.apply(rhs), OH.apply(rhs)
     assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("cfg,scale,kind,path", [
+    ("C5", 10, "simple", "sell"), ("C5", 10, "simple", "csr"), ("C4", 8, "uzawa", "sell"),
+    ("C4", 8, "uzawa", "csr"), ("C2", 4, "simple", "sell"), ("C3", 8, "uzawa", "csr")])
+def test_mcgs_predictor_vs_oracle_emulation(cfg, scale, kind, path, monkeypatch):
+    """GPU multicolour (node-block) SGS predictor on K == reference SSOR on
+    the node-colour-permuted K (oracle emulation): one smoother sweep within
+    1e-12, V-cycle within 1e-10, GMRES its within +-1; both the colour-ordered
+    SELL kernel and the CSR kernel."""
+    monkeypatch.setenv("CAMG_GS_SELL", "1" if path == "sell" else "0")
+    if kind == "simple":
+        skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("mcgs", 1, 1.0), corrector=("mcgs", 1, 1.0))
+    else:  # block Gauss-Seidel = Uzawa(alpha=1) with the GPU Gauss-Seidel on K
+        skw = dict(kind="uzawa", alpha=1.0, outer_sweeps=1, predictor=("mcgs", 1, 1.0), corrector=("jacobi", 1, 0.8))
+    hkw = dict(max_levels=3, max_coarse_size=50)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    x0 = np.random.default_rng(1).standard_normal(op.total_rows)
+    for lvl, olvl in zip(H.levels, OH.levels):
+        n_u = lvl.op.n_u
+        xl = x0[:lvl.op.total_rows]
+        bl = rhs[:lvl.op.total_rows] if lvl is H.levels[0] else np.random.default_rng(2).standard_normal(len(xl))
+        out = lvl.smoother.sweep_merged(xl, bl).cpu().numpy()
+        u, lam = olvl.smoother.sweep(xl[:n_u], xl[n_u:], bl[:n_u], bl[n_u:])
+        ref = np.concatenate([u, lam])
+        assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+    v, ref = H.apply(rhs), OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 200, 100)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
+    assert rep.converged == orep.converged
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+
+
+def test_mcgs_predictor_fine_pass_and_zero_start():
+    """fine_pass mode 3 (one MC-SGS predictor sweep) runs and reports bytes;
+    a sweep from zero equals a sweep from an explicit zero vector."""
+    skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("mcgs", 1, 1.0), corrector=("mcgs", 1, 1.0))
+    g = generate(config_spec("C5", 10))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2, max_coarse_size=50), block_cfg(skw))
+    from paper_1912_09056_b200.sparse import BlockVector, to_device
+    sm = H.levels[0].smoother
+    rhs = g.rhs
+    a = sm.apply(BlockVector.from_merged(rhs, op.n_u)).merged()
+    b = sm.sweep_merged(np.zeros(op.total_rows), rhs).cpu().numpy()
+    assert np.linalg.norm(a - b) <= 1e-13 * np.linalg.norm(b)
+    x = to_device(np.random.default_rng(0).standard_normal(op.total_rows))
+    csr_b, fmt_b = H.fine_pass(3, x, to_device(rhs))
+    assert csr_b > 0 and fmt_b > 0

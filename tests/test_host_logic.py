@@ -124,3 +124,37 @@ def test_native_greedy_matches_oracle_random_graphs():
             ref = O.greedy(A.indptr.astype(np.int64), A.indices.astype(np.int64), n, ms)
             np.testing.assert_array_equal(ag.node_to_agg, ref.node_to_agg)
             assert ag.singleton_count == ref.singletons
+
+
+@pytest.mark.parametrize("name,scale,bs", [("C4", 16, 3), ("C2", 8, 2)])
+def test_oracle_node_colouring_is_valid(name, scale, bs):
+    """The MC-SGS predictor's node colouring: no two coupled nodes share a
+    colour, every DOF takes its node's colour, and the structured hex8 / Q1
+    stencils need 8 / 4 colours under natural-order greedy."""
+    g = generate(config_spec(name, scale))
+    oop, ometa, _ = O.system_from_generated(g)
+    assert O.node_block(ometa) == bs
+    K = oop.K
+    col = O.greedy_colors(K, bs)
+    assert np.array_equal(col, np.repeat(col[::bs], bs))
+    rows = np.repeat(np.arange(K.shape[0]), np.diff(K.indptr))
+    off = (rows // bs) != (K.indices // bs)
+    assert not np.any(col[rows[off]] == col[K.indices[off]])
+    assert col.max() + 1 == (8 if bs == 3 else 4)
+
+
+def test_oracle_mcgs_block_equals_permuted_ssor():
+    """mcgs(block) is the reference SSOR on K renumbered colour-major, node
+    by node, DOFs in order (the GPU kernels' visiting order)."""
+    g = generate(config_spec("C4", 16))
+    oop, ometa, _ = O.system_from_generated(g)
+    K = oop.K
+    b = np.random.default_rng(0).standard_normal(K.shape[0])
+    x = np.random.default_rng(1).standard_normal(K.shape[0])
+    P = O.Point(O.PointCfg("mcgs", 2, 0.9, block=3), K)
+    col = O.greedy_colors(K, 3)
+    perm = np.lexsort((np.arange(K.shape[0]), col))
+    S = O.Point(O.PointCfg("sgs", 2, 0.9), O.canon(K[perm][:, perm]))
+    ref = np.empty_like(x)
+    ref[perm] = S.smooth(x[perm], b[perm])
+    np.testing.assert_array_equal(P.smooth(x, b), ref)
