@@ -358,15 +358,18 @@ def run_gpu(args):
     N.call("camg_csr_stream_bytes", Am.device, C.byref(fmt))
     spmv_fmt_gbs = fmt.value / (spmv_ms * 1e-3) / 1e9
 
-    # ---- dominant kernel of the V-cycle: the fine-level extra Jacobi sweep
-    # (SELL mode 2; 6 of the ~12 fine-level operator passes per cycle)
+    # ---- dominant kernel of the V-cycle: the fine-level predictor pass over
+    # [K | B1] (Jacobi: one fused SELL pass per step; multicolour SGS: one
+    # forward + backward sweep of colour passes)
+    gs = scfg.kind != "braess_sarazin" and scfg.predictor.kind == "mcgs"
+    dom_mode = 3 if gs else 1
     xk = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).cuda()
     for _ in range(3):
-        H.fine_pass(1, xk, rhs)
+        H.fine_pass(dom_mode, xk, rhs)
     barrier()
     e0.record(stream)
     for _ in range(reps):
-        dom_model, dom_fmt = H.fine_pass(1, xk, rhs)
+        dom_model, dom_fmt = H.fine_pass(dom_mode, xk, rhs)
     e1.record(stream)
     torch.cuda.synchronize()
     dom_ms = e0.elapsed_time(e1) / reps
@@ -448,11 +451,14 @@ def run_gpu(args):
         "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config geometry/materials)",
         "config": dict(workload_config(args), levels=levels, operator_complexity=H.complexity),
         "roofline": {"bound": "hbm", "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": dom_gbs / peak, "traffic": TRAFFIC.get(args.config),
-                     "kernel": "k_sell_row<3,3,mode 1>: fine-level Jacobi predictor sweep y += w D^-1 (b - [K B1][y; lam]) "
-                               "(block SELL-32 [K | B1] stream)",
+                     "frac": dom_gbs / peak, "traffic": None if gs else TRAFFIC.get(args.config),
+                     "kernel": ("k_sell_gs<3>: one fine-level multicolour block-SGS predictor sweep (forward + backward "
+                                "colour passes over a colour-ordered block SELL of K)") if gs else
+                               ("k_sell_row<3,3,mode 1>: fine-level Jacobi predictor sweep y += w D^-1 (b - [K B1][y; lam]) "
+                                "(block SELL-32 [K | B1] stream)"),
                      "algorithmic_bytes_per_launch": dom_model,
-                     "bytes_model": "SURVEY §8(d): 12 B/nnz (int32 CSR) + offsets + x read + 3 vector streams (b, D^-1, y out)",
+                     "bytes_model": ("SURVEY §8(d): 2 x (12 B/nnz(K) + offsets + 4 vector streams) + y/g init" if gs else
+                                     "SURVEY §8(d): 12 B/nnz (int32 CSR) + offsets + x read + 3 vector streams (b, D^-1, y out)"),
                      "avg_launch_ms": dom_ms,
                      "achieved_format_bytes": dom_fmt_gbs, "frac_format_bytes": dom_fmt_gbs / peak,
                      "format_bytes_per_launch": dom_fmt,

@@ -234,6 +234,17 @@ class Point:
             self.perm = perm
             self.inner = Point(PointCfg("sgs", cfg.sweeps, cfg.damping), canon(A[perm][:, perm]))
             return
+        if cfg.kind == "gpu_chebyshev":
+            # GPU-only predictor (not in the reference): Chebyshev polynomial
+            # of D^-1 A, degree = sweeps, on [lmax/30, 1.1 lmax]
+            d = A.diagonal()
+            if np.any(d == 0.0):
+                raise OracleError("chebyshev: zero diagonal")
+            self.dinv = 1.0 / d
+            beta = 1.1 * lambda_max(A, d)
+            alpha = beta / 30.0
+            self.theta, self.delta = 0.5 * (beta + alpha), 0.5 * (beta - alpha)
+            return
         if cfg.kind in ("jacobi", "sgs"):
             d = A.diagonal()
             if np.any(d == 0.0):
@@ -269,6 +280,17 @@ class Point:
             return out
         if k == "direct":
             return scipy.linalg.lu_solve(self.lu, b)
+        if k == "gpu_chebyshev":
+            sigma = self.theta / self.delta
+            rho = 1.0 / sigma
+            d = self.dinv * (b - self.A @ x) / self.theta
+            x += d
+            for _ in range(1, self.cfg.sweeps):
+                rn = 1.0 / (2.0 * sigma - rho)
+                d = rn * rho * d + (2.0 * rn / self.delta) * (self.dinv * (b - self.A @ x))
+                rho = rn
+                x += d
+            return x
         for _ in range(self.cfg.sweeps):
             if k == "jacobi":
                 x += self.dinv * (b - self.A @ x)

@@ -445,6 +445,32 @@ __global__ void k_div(int64_t n, const double* __restrict__ w, double s, double*
     v[i] = __ddiv_rn(w[i], s);
 }
 
+// lambda_max(D^-1 A) by power iteration from ones/sqrt(n) (the algorithm of
+// transfer.py:148-161, device norms): bounds of the Chebyshev predictor
+double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s) {
+  const int64_t n = A->n_rows;
+  if (n == 0) return 1.0;
+  DBuf<double> v(n + 1), w(n + 1), part(kDotBlocks + 1);
+  std::vector<double> ones(n, 1.0 / std::sqrt((double)n));
+  CAMG_CUDA(cudaMemcpy(v.p, ones.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  double lam = 1.0;
+  for (int k = 0; k < iters; ++k) {
+    note_launch();
+    k_power_step<<<grid_for(n, 256), 256, 0, s>>>(view(A), d, v.p, w.p);
+    dot_device(n, w.p, w.p, part.p + kDotBlocks, part.p, s);
+    double nn = 0.0;
+    CAMG_CUDA(cudaMemcpyAsync(&nn, part.p + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    const double nrm = std::sqrt(nn);
+    if (nrm == 0.0) return 1.0;
+    lam = nrm;
+    note_launch();
+    k_div<<<grid_for(n, 256), 256, 0, s>>>(n, w.p, nrm, v.p);
+  }
+  CAMG_LAUNCH_CHECK();
+  return lam;
+}
+
 }  // namespace camg
 
 using namespace camg;

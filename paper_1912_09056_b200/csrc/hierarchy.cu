@@ -50,6 +50,8 @@ struct RowEpi {
   const double* x0 = nullptr;  // relaxation origin for xmode 1 (null = 0)
   int xmode = 0;
   double* out_y = nullptr;     // Jacobi iterate y = x + d (optional)
+  const double* dprev = nullptr;  // Chebyshev: d = c1*dprev + c2*dscale*r
+  double c1 = 0.0, c2 = 1.0;
 };
 
 // r_i = b_i - A_i x for rows [row0, row0+nrows), x split at `split` into
@@ -72,7 +74,9 @@ __global__ void __launch_bounds__(256) k_resid(CsrView A, int64_t row0, int64_t 
       const double r = e.b[i] - acc;
       if (e.out_r) e.out_r[i] = r;
       if (e.dscale) {
-        const double d = e.dscale[i] * r;
+        double d = e.dscale[i] * r;
+        if (e.dprev) d = e.c1 * e.dprev[i] + e.c2 * d;
+        else if (e.c2 != 1.0) d = e.c2 * d;
         if (e.out_d) e.out_d[i] = d;
         const double xi = (ZERO || !e.x) ? 0.0 : e.x[i];
         const double y = xi + d;
@@ -476,6 +480,7 @@ static void resid_rows(const Csr* A, int64_t row0, int64_t nrows, const double* 
     SellEpi se;
     se.b = e.b; se.x = e.x; se.out_r = e.out_r; se.dscale = e.dscale; se.out_d = e.out_d;
     se.out_x = e.out_x; se.coef = e.coef; se.x0 = e.x0; se.xmode = e.xmode; se.out_y = e.out_y;
+    se.dprev = e.dprev; se.c1 = e.c1; se.c2 = e.c2;
     sell_launch(A->sell, 1, zero, xu, xl, split < A->n_cols ? split : -1, se, s);
     const int64_t done = A->sell->rows();
     row0 += done;
@@ -522,6 +527,10 @@ struct Level {
   DBuf<int32_t> pnodes;
   Sell* gs_sell = nullptr;
   DBuf<double> w_g;
+  // Chebyshev predictor: d_k = c1[k] d_{k-1} + c2[k] D^-1 r_k, y_{k+1} = y_k + d_k
+  double cheb_lmax = 0.0;
+  std::vector<double> cheb_c1, cheb_c2;
+  DBuf<double> w_cd[2];
   // direct corrector
   DBuf<double> corr_lu;
   DBuf<int32_t> corr_piv;
@@ -676,12 +685,21 @@ struct Level {
       // sweeps on r_u (smoothers.py:186-199, 285-314) with u added back, so
       // no residual / increment vectors are stored.  Uzawa keeps y_sp for the
       // lambda side and relaxes u_new = u + alpha (y_sp - u).
+      // Chebyshev: the same pass with d_k = c1 d_{k-1} + c2 D^-1 r_k kept
+      // between steps (w_cd ping-pong)
+      const bool cheb = cfg.pred_kind == CAMG_PT_CHEBYSHEV;
       const double* y = x;
       double* bufs[2] = {w_du.p, w_du2.p};
       for (int k = 0; k < sp; ++k) {
         const bool last = (k == sp - 1);
         double* dst = bufs[k & 1];
         RowEpi e{b, y, nullptr, dinv_p.p, nullptr, nullptr, 1.0};
+        if (cheb) {
+          e.c1 = cheb_c1[k];
+          e.c2 = cheb_c2[k];
+          e.dprev = k ? w_cd[(k - 1) & 1].p : nullptr;
+          if (!last) e.out_d = w_cd[k & 1].p;
+        }
         if (!last) {
           e.out_x = dst;
         } else if (kind == CAMG_UZAWA) {
@@ -815,6 +833,34 @@ static std::vector<int32_t> node_colors(const Csr* K, int64_t nu, int bs) {
   return color;
 }
 
+double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s);
+
+// Chebyshev polynomial of D^-1 K (degree = predictor sweeps) on
+// [lmax/kChebRatio, kChebBoost*lmax], lmax by 10 power steps (the
+// smoothed-aggregation estimate, transfer.py:148-161):
+//   theta = (b+a)/2, delta = (b-a)/2, sigma = theta/delta, rho_0 = 1/sigma
+//   d_0 = D^-1 r_0 / theta; d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k/delta) D^-1 r_k,
+//   rho_k = 1/(2 sigma - rho_{k-1})
+static void setup_chebyshev(Level* L, const Csr* K, const double* dK, int degree, cudaStream_t s) {
+  L->cheb_lmax = lambda_max_dinv(K, dK, 10, s);
+  const double beta = kChebBoost * L->cheb_lmax, alpha = beta / kChebRatio;
+  const double theta = 0.5 * (beta + alpha), delta = 0.5 * (beta - alpha), sigma = theta / delta;
+  L->cheb_c1.assign(degree, 0.0);
+  L->cheb_c2.assign(degree, 0.0);
+  double rho = 1.0 / sigma;
+  L->cheb_c2[0] = 1.0 / theta;
+  for (int k = 1; k < degree; ++k) {
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    L->cheb_c1[k] = rn * rho;
+    L->cheb_c2[k] = 2.0 * rn / delta;
+    rho = rn;
+  }
+  if (degree > 1) {
+    L->w_cd[0] = DBuf<double>(L->nu + 1);
+    L->w_cd[1] = DBuf<double>(L->nu + 1);
+  }
+}
+
 static void setup_gs_predictor(Level* L, const Csr* K, int node_block, cudaStream_t s) {
   const int64_t nu = L->nu;
   int bs = node_block > 1 ? node_block : 1;
@@ -859,8 +905,9 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
   CAMG_CHECK(cfg.kind >= CAMG_UZAWA && cfg.kind <= CAMG_SIMPLEC, CAMG_ERR_CONFIG, "unknown block smoother kind");
   CAMG_CHECK(cfg.alpha > 0.0, CAMG_ERR_CONFIG, "alpha must be positive");
   CAMG_CHECK(cfg.outer_sweeps >= 1, CAMG_ERR_CONFIG, "outer_sweeps must be >= 1");
-  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI || cfg.pred_kind == CAMG_PT_MCGS,
-             CAMG_ERR_CONFIG, "GPU predictor supports jacobi and mcgs");
+  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI || cfg.pred_kind == CAMG_PT_MCGS ||
+                 cfg.pred_kind == CAMG_PT_CHEBYSHEV,
+             CAMG_ERR_CONFIG, "GPU predictor supports jacobi, chebyshev and mcgs");
   CAMG_CHECK(cfg.pred_sweeps >= 1, CAMG_ERR_CONFIG, "predictor sweeps must be >= 1");
   CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT || cfg.corr_kind == CAMG_PT_MCGS,
              CAMG_ERR_CONFIG, "GPU corrector supports jacobi, mcgs and direct");
@@ -904,8 +951,10 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
   if (cfg.kind != CAMG_BRAESS_SARAZIN) {
     check_no_zero(dK.p, nu, "jacobi");
     L->dinv_p = DBuf<double>(nu + 1);
+    const bool cheb = cfg.pred_kind == CAMG_PT_CHEBYSHEV;
     note_launch();
-    k_scaled_recip<<<grid_for(nu, 256), 256>>>(nu, dK.p, cfg.pred_damping, 1.0, L->dinv_p.p);
+    k_scaled_recip<<<grid_for(nu, 256), 256>>>(nu, dK.p, cheb ? 1.0 : cfg.pred_damping, 1.0, L->dinv_p.p);
+    if (cheb) setup_chebyshev(L.get(), K, dK.p, cfg.pred_sweeps, s);
   }
   // Schur approximation (smoothers.py:255-267)
   {
@@ -1323,7 +1372,11 @@ int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, dou
       const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps : std::max(0, c.corr_sweeps - 1);
       const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
                          (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
-      const double step = sp * sweep + lam + (gs ? 32.0 * L->nu + (c.kind == CAMG_UZAWA ? 24.0 * L->nu : 0.0) : 0.0);
+      // Chebyshev keeps d_k between its steps: + write / read of one vector
+      const double cheb = (!gs && c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_CHEBYSHEV)
+                              ? 16.0 * L->nu * std::max(0, sp - 1) : 0.0;
+      const double step = sp * sweep + lam + cheb +
+                          (gs ? 32.0 * L->nu + (c.kind == CAMG_UZAWA ? 24.0 * L->nu : 0.0) : 0.0);
       // zero start: the first sweep reads no matrix / x (MC-SGS: only its
       // first colour is skipped)
       const double step0 = gs ? step - (12.0 * top + 8.0 * L->n) / std::max(1, L->pred_colors())

@@ -333,7 +333,9 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
         const double res = e.b[i] - acc[r];
         if (e.out_r) e.out_r[i] = res;
         if (e.dscale) {
-          const double d = e.dscale[i] * res;
+          double d = e.dscale[i] * res;
+          if (e.dprev) d = e.c1 * e.dprev[i] + e.c2 * d;
+          else if (e.c2 != 1.0) d = e.c2 * d;
           if (e.out_d) e.out_d[i] = d;
           const double xi = (ZERO || !e.x) ? 0.0 : e.x[i];
           const double y = xi + d;
@@ -407,7 +409,9 @@ __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __r
         const double res = e.b[i] - acc[r];
         if (e.out_r) e.out_r[i] = res;
         if (e.dscale) {
-          const double d = e.dscale[i] * res;
+          double d = e.dscale[i] * res;
+          if (e.dprev) d = e.c1 * e.dprev[i] + e.c2 * d;
+          else if (e.c2 != 1.0) d = e.c2 * d;
           if (e.out_d) e.out_d[i] = d;
           const double xi = (ZERO || !e.x) ? 0.0 : e.x[i];
           const double y = xi + d;

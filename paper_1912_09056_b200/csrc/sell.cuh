@@ -49,6 +49,8 @@ struct SellEpi {
   const double* x0 = nullptr;  // mode 1, xmode 1: out_x = x0 + coef*((x + d) - x0)
   int xmode = 0;
   double* out_y = nullptr;     // mode 1: Jacobi iterate y = x + d
+  const double* dprev = nullptr;  // mode 1 (Chebyshev): d = c1*dprev + c2*dscale*res
+  double c1 = 0.0, c2 = 1.0;
 };
 
 Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s,

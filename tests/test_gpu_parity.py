@@ -495,3 +495,34 @@ def test_mcgs_predictor_fine_pass_and_zero_start():
     x = to_device(np.random.default_rng(0).standard_normal(op.total_rows))
     csr_b, fmt_b = H.fine_pass(3, x, to_device(rhs))
     assert csr_b > 0 and fmt_b > 0
+
+
+@pytest.mark.parametrize("cfg,scale,kind,degree", [("C5", 10, "simple", 2), ("C4", 8, "uzawa", 3), ("C2", 4, "simplec", 1)])
+def test_chebyshev_predictor_vs_oracle(cfg, scale, kind, degree):
+    """GPU Chebyshev predictor (fused into the [K | B1] pass, d_k carried
+    between steps) == the oracle's Chebyshev iteration on the same bounds:
+    one sweep per level within 1e-12, V-cycle within 1e-10, GMRES its +-1."""
+    alpha = 0.8 if kind != "uzawa" else 0.6
+    skw = dict(kind=kind, alpha=alpha, outer_sweeps=2, predictor=("gpu_chebyshev", degree, 1.0),
+               corrector=("jacobi", 1, 0.8))
+    hkw = dict(max_levels=3, max_coarse_size=50)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    rng = np.random.default_rng(3)
+    for lvl, olvl in zip(H.levels, OH.levels):
+        n_u, n = lvl.op.n_u, lvl.op.total_rows
+        xl, bl = rng.standard_normal(n), rng.standard_normal(n)
+        out = lvl.smoother.sweep_merged(xl, bl).cpu().numpy()
+        u, lam = olvl.smoother.sweep(xl[:n_u], xl[n_u:], bl[:n_u], bl[n_u:])
+        ref = np.concatenate([u, lam])
+        assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+    v, ref = H.apply(rhs), OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 200, 100)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
+    assert rep.converged == orep.converged
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
