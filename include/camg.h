@@ -51,6 +51,7 @@ extern "C" {
 typedef struct camg_csr camg_csr;
 typedef struct camg_level camg_level;
 typedef struct camg_hierarchy camg_hierarchy;
+typedef struct camg_scalar_hierarchy camg_scalar_hierarchy;
 
 typedef struct {
   int kind;           /* CAMG_UZAWA .. CAMG_SIMPLEC                 (BlockSmootherConfig.kind)   */
@@ -219,6 +220,26 @@ int camg_hierarchy_use_graph(camg_hierarchy* H, int enable);
 /* algorithmic bytes of one V-cycle (SURVEY.md §8(d) model) */
 int camg_hierarchy_vcycle_bytes(const camg_hierarchy* H, double* bytes_csr_model,
                                 double* bytes_format);
+
+/* ---- nested preconditioner (hierarchy.py:289-385) -------------------------- */
+/* ScalarHierarchy (hierarchy.py:300-320) from the Python-built levels
+ * (build_scalar_hierarchy, :323-363): operators A[0..n-1] (borrowed), transfers
+ * P[0..n-2] (copied; R = P^T on device), one point smoother for every
+ * non-coarsest level: kind CAMG_PT_JACOBI / CAMG_PT_MCGS (node colouring with
+ * node_block[l] DOFs per node) / CAMG_PT_CHEBYSHEV                            */
+int camg_scalar_hierarchy_create(int num_levels, const camg_csr* const* A, const camg_csr* const* P,
+                                 const int* node_block, int kind, int sweeps, double damping,
+                                 camg_scalar_hierarchy** out);
+/* dense LU of the coarsest scalar operator (hierarchy.py:356-360) */
+int camg_scalar_hierarchy_set_coarse_lu(camg_scalar_hierarchy* H, int64_t n, const double* lu_colmajor,
+                                        const int32_t* piv);
+/* x = one scalar V-cycle from zero on b (ScalarHierarchy.apply, :317-318) */
+int camg_scalar_hierarchy_apply(camg_scalar_hierarchy* H, const double* b, double* x, void* stream);
+int camg_scalar_hierarchy_destroy(camg_scalar_hierarchy* H);
+/* BlockSmoother(cfg, op, predictor_solver=inner) (smoothers.py:251-278): the
+ * level's predictor becomes du = inner(r_u) (NULL restores the configured
+ * predictor); inner is borrowed                                              */
+int camg_level_set_predictor_solver(camg_level* L, camg_scalar_hierarchy* inner);
 
 /* ---- Krylov (krylov.py:45-129) -------------------------------------------- */
 /* right-preconditioned GMRES(restart), x0 = 0, CGS2 orthogonalisation.

@@ -332,7 +332,7 @@ def schur(op: Saddle, mode, scale=1.0, a_scale=1.0):
 class Block:
     """Bound block smoother (smoothers.py:245-329)."""
 
-    def __init__(self, cfg: BlockCfg, op: Saddle, node_block: int = 1):
+    def __init__(self, cfg: BlockCfg, op: Saddle, node_block: int = 1, predictor_solver=None):
         self.cfg, self.op = cfg, op
         mode = cfg.effective_a_hat_mode()
         if cfg.kind == "uzawa":
@@ -350,7 +350,12 @@ class Block:
         pcfg = cfg.predictor
         if pcfg.kind == "mcgs" and op.K.shape[0] % max(1, node_block) == 0:
             pcfg = replace(pcfg, block=max(1, node_block))
-        self.pred = None if cfg.kind == "braess_sarazin" else Point(pcfg, op.K)
+        if cfg.kind == "braess_sarazin":
+            self.pred = None
+        elif predictor_solver is not None:            # smoothers.py:277-278
+            self.pred = predictor_solver
+        else:
+            self.pred = Point(pcfg, op.K)
         self.corr = Point(cfg.corrector, self.S)
 
     def _uzawa(self, u, lam, bu, bl):                # smoothers.py:285-291
@@ -720,6 +725,73 @@ def setup(op: Saddle, meta: Meta, cfg: HierCfg, scfg: BlockCfg, pre=1, post=1) -
         op = opc
     lu = lu_factor(levels[-1].op.merged_dense()) if cfg.coarse_solver == "merged_lu" else None
     return Hier(levels, cfg, lu, pre, post)
+
+
+# ---------------------------------------------------------------------------
+# nested preconditioner (hierarchy.py:289-385)
+
+
+def node_block_of(dof_node, num_nodes) -> int:
+    n = len(dof_node)
+    if num_nodes == 0 or n % num_nodes:
+        return 1
+    bs = n // num_nodes
+    if bs not in (2, 3, 6) or not np.array_equal(dof_node, np.arange(n) // bs):
+        return 1
+    return bs
+
+
+class ScalarHier:
+    """Scalar smoothed-aggregation AMG on K (hierarchy.py:300-363)."""
+
+    def __init__(self, K, meta: Meta, cfg: HierCfg, pcfg: PointCfg):
+        self.levels = []                             # (A, P, R, smoother)
+        A, dof_node, nn, body, ns = K, meta.u_dof_node, meta.num_u_nodes, meta.node_body, meta.ns_u
+        while len(self.levels) + 1 < cfg.max_levels and A.shape[0] >= cfg.max_coarse_size:
+            ip, ix = node_graph(A, dof_node, nn, body, cfg.eps_drop)
+            aggs = greedy(ip, ix, nn, cfg.min_agg_size)
+            if aggs.num_aggs >= nn:
+                break
+            P, cns, cagg, _ = tentative(aggs, ns, dof_node)
+            if cfg.smooth_displacement_transfers:
+                P, _ = smooth_prolongator(P, A, cfg.omega)
+            R = transpose(P)
+            c = pcfg
+            if c.kind == "mcgs":
+                c = replace(c, block=node_block_of(dof_node, nn))
+            self.levels.append((A, P, R, Point(c, A)))
+            nbody = np.full(aggs.num_aggs, -1, dtype=np.int8)
+            nbody[aggs.node_to_agg] = body
+            A, dof_node, nn, body, ns = rap(R, A, P), cagg, aggs.num_aggs, nbody, cns
+        self.levels.append((A, None, None, None))
+        self.lu = lu_factor(A.toarray())
+
+    def vcycle(self, l, x, b):                       # hierarchy.py:305-315
+        A, P, R, sm = self.levels[l]
+        if l == len(self.levels) - 1:
+            return scipy.linalg.lu_solve(self.lu, b)
+        x = sm.smooth(x, b)
+        r = b - A @ x
+        c = self.vcycle(l + 1, np.zeros(P.shape[1]), R @ r)
+        x = x + P @ c
+        return sm.smooth(x, b)
+
+    def apply(self, b):
+        return self.vcycle(0, np.zeros(len(b)), np.asarray(b, dtype=np.float64))
+
+
+class Nested:
+    """NestedPreconditioner (hierarchy.py:366-376)."""
+
+    def __init__(self, op: Saddle, meta: Meta, scfg: BlockCfg, icfg: HierCfg, ipcfg: PointCfg):
+        self.op = op
+        self.inner = ScalarHier(op.K, meta, icfg, ipcfg)
+        self.outer = Block(scfg, op, node_block(meta), predictor_solver=self.inner)
+
+    def apply(self, r):
+        r = np.asarray(r, dtype=np.float64)
+        u, lam = self.outer.apply(r[:self.op.n_u], r[self.op.n_u:])
+        return np.concatenate([u, lam])
 
 
 # ---------------------------------------------------------------------------

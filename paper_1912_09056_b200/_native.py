@@ -87,6 +87,11 @@ _SIGS = {
     "camg_hierarchy_destroy": (C.c_int, [vp]),
     "camg_vcycle": (C.c_int, [vp, vp, vp, vp]),
     "camg_hierarchy_use_graph": (C.c_int, [vp, C.c_int]),
+    "camg_scalar_hierarchy_create": (C.c_int, [C.c_int, vp, vp, vp, C.c_int, C.c_int, f64, C.POINTER(vp)]),
+    "camg_scalar_hierarchy_set_coarse_lu": (C.c_int, [vp, i64, vp, vp]),
+    "camg_scalar_hierarchy_apply": (C.c_int, [vp, vp, vp, vp]),
+    "camg_scalar_hierarchy_destroy": (C.c_int, [vp]),
+    "camg_level_set_predictor_solver": (C.c_int, [vp, vp]),
     "camg_hierarchy_vcycle_bytes": (C.c_int, [vp, C.POINTER(f64), C.POINTER(f64)]),
     "camg_gmres": (C.c_int, [vp, vp, vp, vp, f64, C.c_int, C.c_int, C.POINTER(C.c_int), vp,
                              C.POINTER(C.c_int), vp]),

@@ -141,7 +141,8 @@ constexpr int kNumSMs = 148;
 }  // namespace camg
 
 // opaque handle types exposed through the C ABI
-namespace camg { struct Level; struct Hierarchy; }
+namespace camg { struct Level; struct Hierarchy; struct ScalarHier; }
 struct camg_csr { camg::Csr* m; };
 struct camg_level { camg::Level* L; };
 struct camg_hierarchy { camg::Hierarchy* H; };
+struct camg_scalar_hierarchy { camg::ScalarHier* H; };

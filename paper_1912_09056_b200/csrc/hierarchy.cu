@@ -501,6 +501,138 @@ static void jacobi_rows(const Csr* A, int64_t nu, const double* d, const double*
   dispatch_g<LaunchJacobi>(A->avg_row, A, nu, d, r, dinv, dn, x, ox, coef, s);
 }
 
+Csr* block_graph_sym(const Csr* K, int bs, int64_t nn);
+
+// Greedy colouring of the nodes (bs consecutive DOFs) of K in natural node
+// order over the symmetrised node graph (nodes p != q coupled by a non-zero
+// K entry); the multicolour predictor's colouring, emulated by the oracle.
+static std::vector<int32_t> node_colors(const Csr* K, int64_t nu, int bs) {
+  const int64_t nn = nu / bs;
+  std::unique_ptr<Csr> Gs(block_graph_sym(K, bs, nn));
+  std::vector<int64_t> rp(nn + 1);
+  std::vector<int32_t> ci(Gs->nnz);
+  CAMG_CUDA(cudaMemcpy(rp.data(), Gs->rowptr, sizeof(int64_t) * (nn + 1), cudaMemcpyDeviceToHost));
+  if (Gs->nnz) CAMG_CUDA(cudaMemcpy(ci.data(), Gs->col, sizeof(int32_t) * Gs->nnz, cudaMemcpyDeviceToHost));
+  if (getenv("CAMG_DEBUG"))
+    fprintf(stderr, "[camg] node graph: %lld nodes, %lld edges\n", (long long)nn, (long long)Gs->nnz);
+  std::vector<int32_t> color(nn, -1);
+  std::vector<int64_t> seen(64, -1);  // seen[c] == i: colour c is taken by a neighbour of i
+  for (int64_t i = 0; i < nn; ++i) {
+    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int32_t c = color[ci[k]];
+      if (c >= 0) {
+        if (c >= (int32_t)seen.size()) seen.resize(2 * c + 2, -1);
+        seen[c] = i;
+      }
+    }
+    int32_t c = 0;
+    while (c < (int32_t)seen.size() && seen[c] == i) ++c;
+    color[i] = c;
+  }
+  return color;
+}
+
+// Multicolour (node-block) Gauss-Seidel on the rows [0, nu) of an operator
+// whose leading nu x nu block is K: greedy node colouring, and for large K a
+// colour-ordered block SELL of K (rhs g) instead of the CSR kernel (rhs b and
+// the lambda columns of the merged rows).
+struct McgsK {
+  int64_t nu = 0;
+  int bs = 1;
+  std::vector<int64_t> col_ptr, col_slice;
+  DBuf<int32_t> nodes;
+  Sell* sell = nullptr;
+  DBuf<double> g;
+  ~McgsK() { delete sell; }
+  int colors() const { return (int)col_ptr.size() - 1; }
+
+  void setup(const Csr* K, int node_block, cudaStream_t s) {
+    nu = K->n_rows;
+    bs = node_block > 1 ? node_block : 1;
+    if (nu % bs) bs = 1;
+    const int64_t nn = nu / bs;
+    std::vector<int32_t> color = node_colors(K, nu, bs);
+    int ncol = 0;
+    for (int32_t c : color) ncol = std::max(ncol, c + 1);
+    if (getenv("CAMG_DEBUG"))
+      fprintf(stderr, "[camg] mcgs: %lld nodes of %d DOFs, %d colours\n", (long long)nn, bs, ncol);
+    col_ptr.assign(ncol + 1, 0);
+    for (int32_t c : color) col_ptr[c + 1]++;
+    for (int c = 0; c < ncol; ++c) col_ptr[c + 1] += col_ptr[c];
+    std::vector<int32_t> nd(nn);
+    {
+      std::vector<int64_t> pos(col_ptr.begin(), col_ptr.end() - 1);
+      for (int64_t i = 0; i < nn; ++i) nd[pos[color[i]]++] = (int32_t)i;
+    }
+    nodes = DBuf<int32_t>(nn + 1);
+    CAMG_CUDA(cudaMemcpy(nodes.p, nd.data(), sizeof(int32_t) * nn, cudaMemcpyHostToDevice));
+    // colour-ordered SELL from kGsSellMinRows rows (CAMG_GS_SELL=1 forces it,
+    // =0 keeps the CSR path)
+    const char* env = getenv("CAMG_GS_SELL");
+    const bool want = env ? env[0] == '1' : nu >= kGsSellMinRows;
+    if (want && (bs == 1 || bs == 2 || bs == 3 || bs == 6)) {
+      // positions: each colour's nodes in ascending order, padded to whole slices
+      std::vector<int32_t> order;
+      col_slice.assign(ncol + 1, 0);
+      for (int c = 0; c < ncol; ++c) {
+        for (int64_t k = col_ptr[c]; k < col_ptr[c + 1]; ++k) order.push_back(nd[k]);
+        while (order.size() % 32) order.push_back(-1);
+        col_slice[c + 1] = (int64_t)order.size() / 32;
+      }
+      sell = sell_build_ordered(K, bs, nu, nu, order, s);
+      g = DBuf<double>(nu + 1);
+    }
+  }
+
+  // y = x_u (zero for x == null); the SELL path also sets g = b_u (callers
+  // subtract B1 lam from g when the operator has lambda columns)
+  void init(const double* x, const double* b, double* y, cudaStream_t s) {
+    if (sell) {
+      note_launch();
+      k_gs_init<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, b, y, g.p);
+    } else if (!x) {
+      CAMG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * nu, s));
+    } else {
+      note_launch();
+      k_copy<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, y);
+    }
+  }
+
+  void pass(int c, bool fwd, bool zero, const Csr* Arows, const double* xl, const double* b, const double* dinv,
+            double* y, cudaStream_t s) {
+    if (sell) {
+      sell_gs_launch(sell, col_slice[c], col_slice[c + 1], fwd, zero, nullptr, nu, g.p, dinv, y, s);
+    } else {
+      dispatch_g<LaunchMcgsBlock>(Arows->avg_row, Arows, nodes.p + col_ptr[c], col_ptr[c + 1] - col_ptr[c], bs, xl,
+                                  nu, b, dinv, y, fwd, s);
+    }
+  }
+
+  // `sweeps` forward + backward colour sweeps of y_i += dinv_i (b_i - A_i [y; xl])
+  // (zero: y == 0 and xl == null on entry, the first colour reads no matrix)
+  void run(bool zero, const Csr* Arows, const double* xl, const double* b, const double* dinv, double* y, int sweeps,
+           cudaStream_t s) {
+    const int nc = colors();
+    for (int k = 0; k < sweeps; ++k) {
+      for (int c = 0; c < nc; ++c) pass(c, true, zero && k == 0 && c == 0, Arows, xl, b, dinv, y, s);
+      for (int c = nc - 1; c >= 0; --c) pass(c, false, false, Arows, xl, b, dinv, y, s);
+    }
+  }
+};
+
+// pred_update: out = x + alpha du (and, when uh != null, uh = x + du)
+__global__ void k_pred_update(int64_t n, const double* __restrict__ x, const double* __restrict__ du, double alpha,
+                              double* __restrict__ uh, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double xi = x ? x[i] : 0.0;
+    if (uh) uh[i] = xi + du[i];
+    out[i] = uh ? xi + alpha * du[i] : xi + du[i];
+  }
+}
+
+struct ScalarHier;
+const double* scalar_run(ScalarHier* H, const double* b, cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // level
 
@@ -520,13 +652,11 @@ struct Level {
   std::vector<int64_t> color_ptr;
   DBuf<int64_t> color_ptr_dev;
   DBuf<int32_t> color_rows;
-  // multicolour Gauss-Seidel predictor on K: nodes of pbs DOFs grouped by
-  // colour (CSR path), or a colour-ordered block SELL of K (slices per colour)
-  int pbs = 1;
-  std::vector<int64_t> pcol_ptr, pcol_slice;
-  DBuf<int32_t> pnodes;
-  Sell* gs_sell = nullptr;
-  DBuf<double> w_g;
+  // multicolour Gauss-Seidel predictor on K
+  McgsK gs;
+  // external predictor solver (nested preconditioner: scalar AMG V-cycle on
+  // K, hierarchy.py:364-371 via smoothers.py:277-278); borrowed
+  ScalarHier* inner = nullptr;
   // Chebyshev predictor: d_k = c1[k] d_{k-1} + c2[k] D^-1 r_k, y_{k+1} = y_k + d_k
   double cheb_lmax = 0.0;
   std::vector<double> cheb_c1, cheb_c2;
@@ -541,7 +671,7 @@ struct Level {
   int64_t nnz_top = 0;  // entries of the [K | B1] rows
   // work vectors
   DBuf<double> w_du, w_du2, w_ru, w_rc, w_dl, w_dl2, w_rl, w_tmp;
-  ~Level() { if (owns_A) delete A; delete B1; delete S; delete P; delete R; delete gs_sell; }
+  ~Level() { if (owns_A) delete A; delete B1; delete S; delete P; delete R; }
 
   void alloc_work() {
     w_du = DBuf<double>(n);
@@ -616,44 +746,20 @@ struct Level {
     return cur;
   }
 
-  int pred_colors() const { return (int)pcol_ptr.size() - 1; }
-
-  // one colour pass of the MC-SGS predictor (b: rhs of the CSR path, which
-  // reads lambda through the merged rows; the SELL path reads g = b_u - B1 lam)
-  void gs_pass(int c, bool fwd, bool zero, const double* xl, const double* b, double* y, cudaStream_t s) {
-    if (gs_sell) {
-      sell_gs_launch(gs_sell, pcol_slice[c], pcol_slice[c + 1], fwd, zero, nullptr, nu, w_g.p, dinv_p.p, y, s);
-    } else {
-      dispatch_g<LaunchMcgsBlock>(A->avg_row, A, pnodes.p + pcol_ptr[c], pcol_ptr[c + 1] - pcol_ptr[c], pbs, xl, nu,
-                                  b, dinv_p.p, y, fwd, s);
-    }
-  }
+  int pred_colors() const { return gs.colors(); }
 
   // MC-SGS predictor in iterate form: y_0 = u, then pred_sweeps forward +
   // backward colour sweeps of Gauss-Seidel on K y = b_u - B1 lam -- the
   // reference's zero-start SSOR correction on r_u (smoothers.py:186-199) with
   // u added back, on the colour-permuted K
   void gs_predict(const double* x, const double* b, double* y, int sweeps, cudaStream_t s) {
-    const bool zero = (x == nullptr);
     const double* xl = x ? x + nu : nullptr;
-    const int nc = pred_colors();
-    if (gs_sell) {
+    gs.init(x, b, y, s);
+    if (gs.sell && xl && n_b1_rows) {
       note_launch();
-      k_gs_init<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, b, y, w_g.p);
-      if (xl && n_b1_rows) {
-        note_launch();
-        k_b1_sub<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, xl, w_g.p);
-      }
-    } else if (zero) {
-      CAMG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * nu, s));
-    } else {
-      note_launch();
-      k_copy<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, y);
+      k_b1_sub<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, xl, gs.g.p);
     }
-    for (int k = 0; k < sweeps; ++k) {
-      for (int c = 0; c < nc; ++c) gs_pass(c, true, zero && k == 0 && c == 0, xl, b, y, s);
-      for (int c = nc - 1; c >= 0; --c) gs_pass(c, false, false, xl, b, y, s);
-    }
+    gs.run(x == nullptr, A, xl, b, dinv_p.p, y, sweeps, s);
   }
 
   // one algorithmic smoother step: xo = step(x, b); x == nullptr means zero
@@ -670,6 +776,19 @@ struct Level {
       // u_half = u + (A^-1 r_u) / alpha   (smoothers.py:296)
       RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
       resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+    } else if (inner) {
+      // du = inner.apply(r_u), r_u = b_u - K u - B1 lam (smoothers.py:285-314
+      // with predictor_solver); SIMPLE: u_half = u + du; Uzawa: u + alpha du
+      RowEpi e{b, x, w_ru.p, nullptr, nullptr, nullptr, 0.0};
+      resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+      const double* du = scalar_run(inner, w_ru.p, s);
+      note_launch();
+      if (kind == CAMG_UZAWA) {
+        k_pred_update<<<grid_for(nu, 256), 256, 0, s>>>(nu, xu, du, alpha, w_du2.p, xo);
+        uh = w_du2.p;
+      } else {
+        k_pred_update<<<grid_for(nu, 256), 256, 0, s>>>(nu, xu, du, 1.0, nullptr, xo);
+      }
     } else if (cfg.pred_kind == CAMG_PT_MCGS) {
       // Uzawa keeps y for the lambda side and relaxes u_new = u + alpha (y - u)
       double* y = (kind == CAMG_UZAWA) ? w_du.p : xo;
@@ -802,36 +921,6 @@ static void greedy_coloring(const Csr* S, std::vector<int64_t>& color_ptr, DBuf<
   CAMG_CUDA(cudaMemcpy(rows_out.p, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
 }
 
-Csr* block_graph_sym(const Csr* K, int bs, int64_t nn);
-
-// Greedy colouring of the nodes (bs consecutive DOFs) of K in natural node
-// order over the symmetrised node graph (nodes p != q coupled by a non-zero
-// K entry); the multicolour predictor's colouring, emulated by the oracle.
-static std::vector<int32_t> node_colors(const Csr* K, int64_t nu, int bs) {
-  const int64_t nn = nu / bs;
-  std::unique_ptr<Csr> Gs(block_graph_sym(K, bs, nn));
-  std::vector<int64_t> rp(nn + 1);
-  std::vector<int32_t> ci(Gs->nnz);
-  CAMG_CUDA(cudaMemcpy(rp.data(), Gs->rowptr, sizeof(int64_t) * (nn + 1), cudaMemcpyDeviceToHost));
-  if (Gs->nnz) CAMG_CUDA(cudaMemcpy(ci.data(), Gs->col, sizeof(int32_t) * Gs->nnz, cudaMemcpyDeviceToHost));
-  if (getenv("CAMG_DEBUG"))
-    fprintf(stderr, "[camg] node graph: %lld nodes, %lld edges\n", (long long)nn, (long long)Gs->nnz);
-  std::vector<int32_t> color(nn, -1);
-  std::vector<int64_t> seen(64, -1);  // seen[c] == i: colour c is taken by a neighbour of i
-  for (int64_t i = 0; i < nn; ++i) {
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
-      const int32_t c = color[ci[k]];
-      if (c >= 0) {
-        if (c >= (int32_t)seen.size()) seen.resize(2 * c + 2, -1);
-        seen[c] = i;
-      }
-    }
-    int32_t c = 0;
-    while (c < (int32_t)seen.size() && seen[c] == i) ++c;
-    color[i] = c;
-  }
-  return color;
-}
 
 double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s);
 
@@ -841,62 +930,27 @@ double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s)
 //   theta = (b+a)/2, delta = (b-a)/2, sigma = theta/delta, rho_0 = 1/sigma
 //   d_0 = D^-1 r_0 / theta; d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k/delta) D^-1 r_k,
 //   rho_k = 1/(2 sigma - rho_{k-1})
-static void setup_chebyshev(Level* L, const Csr* K, const double* dK, int degree, cudaStream_t s) {
-  L->cheb_lmax = lambda_max_dinv(K, dK, 10, s);
-  const double beta = kChebBoost * L->cheb_lmax, alpha = beta / kChebRatio;
+static void cheb_coefficients(double lmax, int degree, std::vector<double>& c1, std::vector<double>& c2) {
+  const double beta = kChebBoost * lmax, alpha = beta / kChebRatio;
   const double theta = 0.5 * (beta + alpha), delta = 0.5 * (beta - alpha), sigma = theta / delta;
-  L->cheb_c1.assign(degree, 0.0);
-  L->cheb_c2.assign(degree, 0.0);
+  c1.assign(degree, 0.0);
+  c2.assign(degree, 0.0);
   double rho = 1.0 / sigma;
-  L->cheb_c2[0] = 1.0 / theta;
+  c2[0] = 1.0 / theta;
   for (int k = 1; k < degree; ++k) {
     const double rn = 1.0 / (2.0 * sigma - rho);
-    L->cheb_c1[k] = rn * rho;
-    L->cheb_c2[k] = 2.0 * rn / delta;
+    c1[k] = rn * rho;
+    c2[k] = 2.0 * rn / delta;
     rho = rn;
-  }
-  if (degree > 1) {
-    L->w_cd[0] = DBuf<double>(L->nu + 1);
-    L->w_cd[1] = DBuf<double>(L->nu + 1);
   }
 }
 
-static void setup_gs_predictor(Level* L, const Csr* K, int node_block, cudaStream_t s) {
-  const int64_t nu = L->nu;
-  int bs = node_block > 1 ? node_block : 1;
-  if (nu % bs) bs = 1;
-  L->pbs = bs;
-  const int64_t nn = nu / bs;
-  std::vector<int32_t> color = node_colors(K, nu, bs);
-  int ncol = 0;
-  for (int32_t c : color) ncol = std::max(ncol, c + 1);
-  if (getenv("CAMG_DEBUG"))
-    fprintf(stderr, "[camg] mcgs predictor: %lld nodes of %d DOFs, %d colours\n", (long long)nn, bs, ncol);
-  L->pcol_ptr.assign(ncol + 1, 0);
-  for (int32_t c : color) L->pcol_ptr[c + 1]++;
-  for (int c = 0; c < ncol; ++c) L->pcol_ptr[c + 1] += L->pcol_ptr[c];
-  std::vector<int32_t> nodes(nn);
-  {
-    std::vector<int64_t> pos(L->pcol_ptr.begin(), L->pcol_ptr.end() - 1);
-    for (int64_t i = 0; i < nn; ++i) nodes[pos[color[i]]++] = (int32_t)i;
-  }
-  L->pnodes = DBuf<int32_t>(nn + 1);
-  CAMG_CUDA(cudaMemcpy(L->pnodes.p, nodes.data(), sizeof(int32_t) * nn, cudaMemcpyHostToDevice));
-  // colour-ordered SELL from kGsSellMinRows rows (CAMG_GS_SELL=1 forces it,
-  // =0 keeps the CSR path)
-  const char* env = getenv("CAMG_GS_SELL");
-  const bool want = env ? env[0] == '1' : nu >= kGsSellMinRows;
-  if (want && (bs == 1 || bs == 2 || bs == 3 || bs == 6)) {
-    // positions: each colour's nodes in ascending order, padded to whole slices
-    std::vector<int32_t> order;
-    L->pcol_slice.assign(ncol + 1, 0);
-    for (int c = 0; c < ncol; ++c) {
-      for (int64_t k = L->pcol_ptr[c]; k < L->pcol_ptr[c + 1]; ++k) order.push_back(nodes[k]);
-      while (order.size() % 32) order.push_back(-1);
-      L->pcol_slice[c + 1] = (int64_t)order.size() / 32;
-    }
-    L->gs_sell = sell_build_ordered(K, bs, nu, nu, order, s);
-    L->w_g = DBuf<double>(nu + 1);
+static void setup_chebyshev(Level* L, const Csr* K, const double* dK, int degree, cudaStream_t s) {
+  L->cheb_lmax = lambda_max_dinv(K, dK, 10, s);
+  cheb_coefficients(L->cheb_lmax, degree, L->cheb_c1, L->cheb_c2);
+  if (degree > 1) {
+    L->w_cd[0] = DBuf<double>(L->nu + 1);
+    L->w_cd[1] = DBuf<double>(L->nu + 1);
   }
 }
 
@@ -969,7 +1023,7 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     }
     L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
   }
-  if (cfg.kind != CAMG_BRAESS_SARAZIN && cfg.pred_kind == CAMG_PT_MCGS) setup_gs_predictor(L.get(), K, cfg.node_block, s);
+  if (cfg.kind != CAMG_BRAESS_SARAZIN && cfg.pred_kind == CAMG_PT_MCGS) L->gs.setup(K, cfg.node_block, s);
   if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) {
     greedy_coloring(L->S, L->color_ptr, L->color_rows);
     L->color_ptr_dev = DBuf<int64_t>(L->color_ptr.size());
@@ -1174,6 +1228,128 @@ Hierarchy* hierarchy_create(Level** lv, int nlev, int coarse_solver) {
 
 void hierarchy_apply(Hierarchy* H, const double* r, double* z, cudaStream_t s) { H->apply(r, z, s); }
 
+// ---------------------------------------------------------------------------
+// scalar smoothed-aggregation hierarchy on K (ScalarHierarchy,
+// hierarchy.py:293-320): V(1,1) with one point-smoother call before and after
+// the coarse correction, dense LU on the coarsest level
+
+struct ScalarLevel {
+  const Csr* A = nullptr;  // borrowed
+  Csr* P = nullptr;        // owned copy
+  Csr* R = nullptr;        // P^T (owned)
+  int64_t n = 0;
+  int kind = CAMG_PT_JACOBI, sweeps = 1;
+  DBuf<double> dinv;
+  McgsK gs;
+  std::vector<double> c1, c2;  // Chebyshev coefficients
+  DBuf<double> cd[2];
+  DBuf<double> b, x0, x1, r, t;
+  ~ScalarLevel() { delete P; delete R; }
+};
+
+struct ScalarHier {
+  std::vector<std::unique_ptr<ScalarLevel>> levels;
+  DBuf<double> lu;
+  DBuf<int32_t> piv;
+  int64_t n_coarse = 0;
+
+  // PointSmoother.smooth (smoothers.py:186-199): `sweeps` sweeps from x
+  // (null = zero) into out
+  void smooth(ScalarLevel& L, const double* x, const double* b, double* out, cudaStream_t s) {
+    if (L.kind == CAMG_PT_MCGS) {
+      L.gs.init(x, b, out, s);
+      L.gs.run(x == nullptr, L.A, nullptr, b, L.dinv.p, out, L.sweeps, s);
+      return;
+    }
+    const bool cheb = L.kind == CAMG_PT_CHEBYSHEV;
+    const double* cur = x;
+    for (int k = 0; k < L.sweeps; ++k) {
+      const bool last = k == L.sweeps - 1;
+      double* dst = ((L.sweeps - 1 - k) % 2 == 0) ? out : L.t.p;
+      RowEpi e{b, cur, nullptr, L.dinv.p, nullptr, dst, 1.0};
+      if (cheb) {
+        e.c1 = L.c1[k];
+        e.c2 = L.c2[k];
+        e.dprev = k ? L.cd[(k - 1) & 1].p : nullptr;
+        if (!last) e.out_d = L.cd[k & 1].p;
+      }
+      resid_rows(L.A, int64_t(0), L.n, cur, (const double*)nullptr, L.n, e, cur == nullptr, s);
+      cur = dst;
+    }
+  }
+
+  // ScalarHierarchy.vcycle from zero (hierarchy.py:305-315)
+  const double* vcycle(int l, const double* b, cudaStream_t s) {
+    ScalarLevel& L = *levels[l];
+    if (l == (int)levels.size() - 1) {
+      CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "scalar coarse LU factors were not set");
+      note_launch();
+      size_t sh = n_coarse <= 12288 ? sizeof(double) * n_coarse : 0;
+      k_lu_solve<<<1, 1024, sh, s>>>((int)n_coarse, lu.p, piv.p, b, L.x0.p);
+      return L.x0.p;
+    }
+    smooth(L, nullptr, b, L.x0.p, s);
+    RowEpi e{b, nullptr, L.r.p, nullptr, nullptr, nullptr, 0.0};
+    resid_rows(L.A, int64_t(0), L.n, L.x0.p, (const double*)nullptr, L.n, e, false, s);
+    ScalarLevel& C = *levels[l + 1];
+    spmv(L.R, 1.0, L.r.p, 0.0, C.b.p, s);
+    const double* xc = vcycle(l + 1, C.b.p, s);
+    spmv(L.P, 1.0, xc, 1.0, L.x0.p, s);
+    smooth(L, L.x0.p, b, L.x1.p, s);
+    return L.x1.p;
+  }
+};
+
+const double* scalar_run(ScalarHier* H, const double* b, cudaStream_t s) { return H->vcycle(0, b, s); }
+
+static ScalarHier* scalar_hierarchy_create(int nlev, const Csr* const* A, const Csr* const* P, const int* node_block,
+                                           int kind, int sweeps, double damping) {
+  CAMG_CHECK(nlev >= 1, CAMG_ERR_ARG, "need at least one level");
+  CAMG_CHECK(kind == CAMG_PT_JACOBI || kind == CAMG_PT_MCGS || kind == CAMG_PT_CHEBYSHEV, CAMG_ERR_CONFIG,
+             "GPU scalar smoother supports jacobi, mcgs and chebyshev");
+  CAMG_CHECK(sweeps >= 1, CAMG_ERR_CONFIG, "point smoother sweeps must be >= 1");
+  cudaStream_t s = 0;
+  std::unique_ptr<ScalarHier> H(new ScalarHier());
+  for (int l = 0; l < nlev; ++l) {
+    std::unique_ptr<ScalarLevel> L(new ScalarLevel());
+    L->A = A[l];
+    L->n = A[l]->n_rows;
+    CAMG_CHECK(A[l]->n_cols == L->n, CAMG_ERR_DIMENSION, "scalar level operator must be square");
+    L->kind = kind;
+    L->sweeps = sweeps;
+    const int64_t n = L->n;
+    L->b = DBuf<double>(n + 1);
+    L->x0 = DBuf<double>(n + 1);
+    if (l < nlev - 1) {
+      CAMG_CHECK(P[l]->n_rows == n && P[l]->n_cols == A[l + 1]->n_rows, CAMG_ERR_DIMENSION,
+                 "scalar transfer does not match the levels");
+      L->P = csr_copy(P[l], s);
+      L->R = csr_transpose(L->P, s);
+      L->x1 = DBuf<double>(n + 1);
+      L->r = DBuf<double>(n + 1);
+      L->t = DBuf<double>(n + 1);
+      DBuf<double> d(n + 1);
+      csr_diagonal(L->A, 0, d.p, s);
+      CAMG_CUDA(cudaDeviceSynchronize());
+      check_no_zero(d.p, n, kind == CAMG_PT_MCGS ? "sgs" : "jacobi");
+      L->dinv = DBuf<double>(n + 1);
+      note_launch();
+      k_scaled_recip<<<grid_for(n, 256), 256>>>(n, d.p, kind == CAMG_PT_CHEBYSHEV ? 1.0 : damping, 1.0, L->dinv.p);
+      if (kind == CAMG_PT_MCGS) L->gs.setup(L->A, node_block ? node_block[l] : 1, s);
+      if (kind == CAMG_PT_CHEBYSHEV) {
+        cheb_coefficients(lambda_max_dinv(L->A, d.p, 10, s), sweeps, L->c1, L->c2);
+        if (sweeps > 1) {
+          L->cd[0] = DBuf<double>(n + 1);
+          L->cd[1] = DBuf<double>(n + 1);
+        }
+      }
+    }
+    H->levels.push_back(std::move(L));
+  }
+  CAMG_CUDA(cudaDeviceSynchronize());
+  return H.release();
+}
+
 }  // namespace camg
 
 using namespace camg;
@@ -1272,9 +1448,9 @@ int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double*
       const double pass = 12.0 * nnzK + 4.0 * (nu + 1) + vec;
       if (bytes_csr_model) *bytes_csr_model = 2.0 * pass + 32.0 * nu;
       if (bytes_format) {
-        if (lv->gs_sell) {
-          const int br = lv->gs_sell->br;
-          *bytes_format = 2.0 * (sell_pass_bytes(lv->gs_sell) + vec + 4.0 * lv->gs_sell->nbr +
+        if (lv->gs.sell) {
+          const int br = lv->gs.sell->br;
+          *bytes_format = 2.0 * (sell_pass_bytes(lv->gs.sell) + vec + 4.0 * lv->gs.sell->nbr +
                                  8.0 * (br * (br - 1) / 2) * (double)(nu / br)) + 32.0 * nu;
         } else {
           *bytes_format = 2.0 * (12.0 * (double)lv->nnz_top + 8.0 * (nu + 1) + vec) + 16.0 * nu;
@@ -1339,6 +1515,58 @@ int camg_hierarchy_destroy(camg_hierarchy* H) {
 
 int camg_vcycle(camg_hierarchy* H, const double* r, double* z, void* stream) {
   return guarded([&] { H->H->apply(r, z, (cudaStream_t)stream); });
+}
+
+int camg_scalar_hierarchy_create(int num_levels, const camg_csr* const* A, const camg_csr* const* P,
+                                 const int* node_block, int kind, int sweeps, double damping,
+                                 camg_scalar_hierarchy** out) {
+  return guarded([&] {
+    std::vector<const Csr*> a(num_levels), p(num_levels);
+    for (int i = 0; i < num_levels; ++i) {
+      a[i] = A[i]->m;
+      p[i] = (i < num_levels - 1) ? P[i]->m : nullptr;
+    }
+    *out = new camg_scalar_hierarchy{scalar_hierarchy_create(num_levels, a.data(), p.data(), node_block, kind, sweeps,
+                                                             damping)};
+  });
+}
+
+int camg_scalar_hierarchy_set_coarse_lu(camg_scalar_hierarchy* H, int64_t n, const double* lu, const int32_t* piv) {
+  return guarded([&] {
+    CAMG_CHECK(n == H->H->levels.back()->n, CAMG_ERR_DIMENSION, "coarse LU size mismatch");
+    CAMG_CHECK(n < (1 << 30), CAMG_ERR_DIMENSION, "coarse LU too large");
+    H->H->n_coarse = n;
+    H->H->lu = DBuf<double>(n * n + 1);
+    H->H->piv = DBuf<int32_t>(n + 1);
+    CAMG_CUDA(cudaMemcpy(H->H->lu.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(H->H->piv.p, piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  });
+}
+
+int camg_scalar_hierarchy_apply(camg_scalar_hierarchy* H, const double* b, double* x, void* stream) {
+  return guarded([&] {
+    cudaStream_t s = (cudaStream_t)stream;
+    const double* res = H->H->vcycle(0, b, s);
+    CAMG_CUDA(cudaMemcpyAsync(x, res, sizeof(double) * H->H->levels[0]->n, cudaMemcpyDeviceToDevice, s));
+    CAMG_LAUNCH_CHECK();
+  });
+}
+
+int camg_scalar_hierarchy_destroy(camg_scalar_hierarchy* H) {
+  return guarded([&] {
+    if (H) { delete H->H; delete H; }
+  });
+}
+
+int camg_level_set_predictor_solver(camg_level* L, camg_scalar_hierarchy* inner) {
+  return guarded([&] {
+    Level* lv = L->L;
+    if (inner) {
+      CAMG_CHECK(inner->H->levels[0]->n == lv->nu, CAMG_ERR_DIMENSION, "predictor solver size does not match n_u");
+      CAMG_CHECK(lv->cfg.kind != CAMG_BRAESS_SARAZIN, CAMG_ERR_CONFIG, "braess_sarazin has no predictor");
+    }
+    lv->inner = inner ? inner->H : nullptr;
+  });
 }
 
 int camg_hierarchy_use_graph(camg_hierarchy* H, int enable) {

@@ -205,11 +205,25 @@ class BlockSmoother:
                  post_sweeps: int = 1, node_block: int = 1):
         if isinstance(op, SaddleSystem):
             op = op.op
+        inner = None
         if predictor_solver is not None:
-            raise ConfigError("custom predictor solvers are not supported on the GPU path")
+            # smoothers.py:277-278: any object with apply(rhs); on the GPU path it
+            # must be a native solver (the nested preconditioner's ScalarHierarchy)
+            if not hasattr(predictor_solver, "handle") or not hasattr(predictor_solver, "smoother_cfg"):
+                raise ConfigError("GPU predictor_solver must be a ScalarHierarchy (build_scalar_hierarchy)")
+            inner = predictor_solver
+            if cfg.kind != "braess_sarazin":
+                # the configured predictor is unused (reference: overridden)
+                cfg_native = BlockSmootherConfig(kind=cfg.kind, alpha=cfg.alpha, outer_sweeps=cfg.outer_sweeps,
+                                                 predictor=PointSmootherConfig("jacobi", 1, 1.0),
+                                                 corrector=cfg.corrector, a_hat_mode=cfg.a_hat_mode)
+            else:
+                cfg_native = cfg
+        else:
+            cfg_native = cfg
         self.cfg = cfg
         self.op = op
-        ncfg = native_cfg(cfg, node_block)
+        ncfg = native_cfg(cfg_native, node_block)
         h = C.c_void_p()
         # the level borrows the operator's merged matrix (one device copy shared
         # with GMRES); self.op keeps it alive
@@ -217,6 +231,9 @@ class BlockSmoother:
                op.Cz.device, C.byref(ncfg), int(pre_sweeps), int(post_sweeps), C.byref(h))
         self._level = _LevelHandle(h)
         self._schur = None
+        self.predictor_solver = inner
+        if inner is not None and cfg.kind != "braess_sarazin":
+            N.call("camg_level_set_predictor_solver", h, inner.handle)
         if cfg.corrector.kind == "direct" and op.n_lam > 0:
             S = self.schur.S_tilde.to_dense()
             lu, piv = lu_factor_quiet(S)
@@ -241,11 +258,13 @@ class BlockSmoother:
         return self._schur
 
     def sweep_merged(self, x, b):
+        """sweep on merged device vectors (x None = zero start)."""
         n = self.op.total_rows
-        xd = to_device(x, n)
+        xd = None if x is None else to_device(x, n)
         bd = to_device(b, n)
         out = empty(n)
-        N.call("camg_level_sweep", self._level.h, ptr(xd), ptr(bd), ptr(out), stream_ptr())
+        N.call("camg_level_sweep", self._level.h, None if xd is None else ptr(xd), ptr(bd), ptr(out),
+               stream_ptr())
         return out
 
     def sweep(self, x: BlockVector, b: BlockVector) -> BlockVector:

@@ -9,8 +9,14 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def cases():
+    """Hierarchy cases (the nested-preconditioner fixtures are listed by
+    nested_cases())."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not p.endswith("kernels.npz"))
+                  if not p.endswith("kernels.npz") and not os.path.basename(p).startswith("nested_"))
+
+
+def nested_cases():
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "nested_*.npz")))
 
 
 def load(name):

@@ -27,3 +27,16 @@ CASES = [
 ]
 
 BY_NAME = {c[0]: c for c in CASES}
+
+# nested preconditioner (hierarchy.py:289-385): (name, config, scale, inner
+# HierarchyConfig kwargs, outer SIMPLE-type BlockSmootherConfig kwargs, inner
+# point smoother (kind, sweeps, damping), GMRES restart, GMRES max_iters)
+NESTED = [
+    ("nested_c5s", "C5", 25, dict(max_levels=3, max_coarse_size=50),
+     dict(kind="simple", alpha=0.8, outer_sweeps=1, predictor=("jacobi", 1, 0.8), corrector=("jacobi", 1, 0.8)),
+     ("jacobi", 2, 0.6), 100, 200),
+    ("nested_c2s", "C2", 8, dict(max_levels=3, max_coarse_size=50),
+     dict(kind="simplec", alpha=0.8, outer_sweeps=2, predictor=("jacobi", 1, 0.8), corrector=("jacobi", 1, 0.8)),
+     ("jacobi", 1, 0.8), 50, 200),
+]
+NESTED_BY_NAME = {c[0]: c for c in NESTED}

@@ -76,7 +76,7 @@ def ref_system(g):
     return op, meta
 
 
-from cases import CASES  # noqa: E402
+from cases import CASES, NESTED  # noqa: E402
 
 
 def _point(t):
@@ -153,6 +153,38 @@ def run_case(name, cfg_name, scale, hkw, skw, restart, max_iters):
           f"relres={out['gmres_true_relres']:.3e}\n{H.report}")
 
 
+def run_nested(name, cfg_name, scale, ikw, skw, ipt, restart, max_iters):
+    """Reference NestedPreconditioner (hierarchy.py:366-385) outputs."""
+    g = generate(config_spec(cfg_name, scale))
+    op, meta = ref_system(g)
+    NP = R_h.nested_preconditioner(op, meta, _block(skw), R_h.HierarchyConfig(**ikw), _point(ipt))
+    out = {"rhs": g.rhs, "n_u": np.int64(g.n_u), "n_lam": np.int64(g.n_lam)}
+    out["inner_rows"] = np.array([lvl.A.num_rows for lvl in NP.inner.levels], dtype=np.int64)
+    out["inner_nnz"] = np.array([lvl.A.nnz for lvl in NP.inner.levels], dtype=np.int64)
+    for l, lvl in enumerate(NP.inner.levels):
+        put(out, f"S{l}_A", lvl.A)
+        if lvl.P is not None:
+            put(out, f"S{l}_P", lvl.P)
+    rng = np.random.default_rng(321)
+    b0 = rng.standard_normal(g.n_u + g.n_lam)
+    out["apply_rhs"] = NP.apply(g.rhs)
+    out["rand_in"] = b0
+    out["apply_rand"] = NP.apply(b0)
+    out["inner_rand_in"] = b0[:g.n_u]
+    out["inner_apply_rand"] = NP.inner.apply(b0[:g.n_u])
+    Asp = op.merged().to_scipy()
+    x, rep = R_k.gmres(lambda v: Asp @ v, NP.apply, g.rhs,
+                       R_k.GmresConfig(rel_tol=1e-8, max_iters=max_iters, restart=restart))
+    out["gmres_restart"] = np.int64(restart)
+    out["gmres_max_iters"] = np.int64(max_iters)
+    out["gmres_iterations"] = np.int64(rep.iterations)
+    out["gmres_converged"] = np.bool_(rep.converged)
+    out["gmres_history"] = np.asarray(rep.residual_history)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: inner levels={len(NP.inner.levels)} rows={out['inner_rows'].tolist()} "
+          f"its={rep.iterations} conv={rep.converged}")
+
+
 def kernels():
     """Small-matrix cases pinning the sparse core (spmv, transpose, SpGEMM,
     Galerkin, diagonals, smoother sweeps on random saddle systems)."""
@@ -186,3 +218,7 @@ if __name__ == "__main__":
         if only and case[0] not in only:
             continue
         run_case(*case)
+    for case in NESTED:
+        if only and case[0] not in only:
+            continue
+        run_nested(*case)

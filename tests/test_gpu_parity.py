@@ -526,3 +526,76 @@ def test_chebyshev_predictor_vs_oracle(cfg, scale, kind, degree):
     x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
     assert rep.converged == orep.converged
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+
+
+# ---------------------------------------------------------------------------
+# nested preconditioner (hierarchy.py:289-385)
+
+from _golden import nested_cases  # noqa: E402
+from cases import NESTED_BY_NAME  # noqa: E402
+
+
+@pytest.mark.parametrize("name", nested_cases())
+def test_nested_vs_reference_golden(name):
+    """GPU NestedPreconditioner (device scalar AMG inner solve as the SIMPLE
+    predictor) against the unmodified reference: scalar levels (patterns
+    exact, values 1e-12), inner V-cycle and apply within 1e-10, GMRES its +-1."""
+    from paper_1912_09056_b200.hierarchy import nested_preconditioner
+    z = load(name)
+    _, cfg, scale, ikw, skw, ipt, restart, max_iters = NESTED_BY_NAME[name]
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    NP = nested_preconditioner(op, fine_level_meta(g), block_cfg(skw), HierarchyConfig(**ikw),
+                               PointSmootherConfig(*ipt))
+    assert [lvl.A.num_rows for lvl in NP.inner.levels] == z["inner_rows"].tolist()
+    for l, lvl in enumerate(NP.inner.levels):
+        A, ref = lvl.A.to_scipy(), csr(z, f"S{l}_A")
+        assert same_pattern(A, ref) and rel_fro(A, ref) <= 1e-12
+    v = NP.inner.apply(z["inner_rand_in"])
+    assert np.linalg.norm(v - z["inner_apply_rand"]) <= 1e-10 * np.linalg.norm(z["inner_apply_rand"])
+    for key_in, key_out in (("rhs", "apply_rhs"), ("rand_in", "apply_rand")):
+        v = NP.apply(z[key_in])
+        assert np.linalg.norm(v - z[key_out]) <= 1e-10 * np.linalg.norm(z[key_out])
+    x, rep = gmres(op.apply_merged, NP.apply, g.rhs,
+                   GmresConfig(rel_tol=1e-8, max_iters=int(max_iters), restart=int(restart)))
+    assert rep.converged == bool(z["gmres_converged"])
+    assert abs(rep.iterations - int(z["gmres_iterations"])) <= 1
+
+
+@pytest.mark.parametrize("inner", [("mcgs", 1, 0.8), ("gpu_chebyshev", 2, 1.0)])
+def test_nested_gpu_inner_smoothers_vs_oracle(inner):
+    """GPU-only inner smoothers of the nested preconditioner (multicolour SGS
+    -- the GPU variant of the reference's default SGS -- and Chebyshev)
+    against the oracle emulation."""
+    from paper_1912_09056_b200.hierarchy import nested_preconditioner
+    ikw = dict(max_levels=3, max_coarse_size=50)
+    skw = dict(kind="simple", alpha=0.8, outer_sweeps=1, predictor=("jacobi", 1, 0.8), corrector=("mcgs", 1, 1.0))
+    g = generate(config_spec("C5", 20))
+    op = saddle_operator(g)
+    NP = nested_preconditioner(op, fine_level_meta(g), block_cfg(skw), HierarchyConfig(**ikw),
+                               PointSmootherConfig(*inner))
+    oop, ometa, rhs = O.system_from_generated(g)
+    ONP = O.Nested(oop, ometa, oracle_block_cfg(skw), O.HierCfg(**ikw), O.PointCfg(*inner))
+    b = np.random.default_rng(5).standard_normal(op.n_u)
+    v, ref = NP.inner.apply(b), ONP.inner.apply(b)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    v, ref = NP.apply(rhs), ONP.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, ONP.apply, rhs, 1e-8, 200, 100)
+    x, rep = gmres(op.apply_merged, NP.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
+    assert rep.converged == orep.converged
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+
+
+def test_nested_config_errors():
+    from paper_1912_09056_b200.hierarchy import nested_preconditioner
+    g = generate(config_spec("C1", 1))
+    op = saddle_operator(g)
+    with pytest.raises(ConfigError):
+        nested_preconditioner(op, fine_level_meta(g), block_cfg(dict(kind="uzawa", alpha=1.0)),
+                              HierarchyConfig(max_levels=2, max_coarse_size=50))
+    with pytest.raises(ConfigError):
+        nested_preconditioner(op, fine_level_meta(g), block_cfg(dict(kind="simple", alpha=0.8,
+                                                                     corrector=("jacobi", 1, 0.8))),
+                              HierarchyConfig(max_levels=2, max_coarse_size=50), PointSmootherConfig("ilu0", 1, 1.0))

@@ -128,3 +128,34 @@ def test_oracle_sparse_kernels():
         same_csr(O.rap(O.transpose(B), Asq, B), csr(z, f"t{t}_RAP"))
         np.testing.assert_array_equal(O.diagonal(Asq), z[f"t{t}_diag"])
         np.testing.assert_array_equal(O.diagonal(Asq, "abs_rowsum"), z[f"t{t}_absrow"])
+
+
+# ---------------------------------------------------------------------------
+# nested preconditioner (hierarchy.py:289-385)
+
+from _golden import nested_cases  # noqa: E402
+from cases import NESTED_BY_NAME  # noqa: E402
+
+
+@pytest.mark.parametrize("name", nested_cases())
+def test_oracle_nested_matches_reference(name):
+    """Scalar AMG levels exactly, inner V-cycle and NestedPreconditioner.apply
+    to rounding, GMRES iteration count equal."""
+    z = load(name)
+    _, cfg, scale, ikw, skw, ipt, restart, max_iters = NESTED_BY_NAME[name]
+    g = generate(config_spec(cfg, scale))
+    op, meta, rhs = O.system_from_generated(g)
+    NP = O.Nested(op, meta, block_cfg(skw), O.HierCfg(**ikw), O.PointCfg(*ipt))
+    assert [l[0].shape[0] for l in NP.inner.levels] == z["inner_rows"].tolist()
+    for l, (A, P, _, _) in enumerate(NP.inner.levels):
+        same_csr(A, csr(z, f"S{l}_A"))
+        if P is not None:
+            same_csr(P, csr(z, f"S{l}_P"))
+    v = NP.inner.apply(z["inner_rand_in"])
+    assert np.linalg.norm(v - z["inner_apply_rand"]) <= 1e-12 * np.linalg.norm(z["inner_apply_rand"])
+    for key_in, key_out in (("rhs", "apply_rhs"), ("rand_in", "apply_rand")):
+        v = NP.apply(z[key_in])
+        assert np.linalg.norm(v - z[key_out]) <= 1e-12 * np.linalg.norm(z[key_out])
+    A = op.merged()
+    _, rep = O.gmres(lambda t: A @ t, NP.apply, rhs, 1e-8, int(max_iters), int(restart))
+    assert rep.iterations == int(z["gmres_iterations"]) and rep.converged == bool(z["gmres_converged"])
