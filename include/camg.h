@@ -39,8 +39,8 @@ extern "C" {
 #define CAMG_PT_JACOBI 0
 #define CAMG_PT_DIRECT 3
 #define CAMG_PT_CHEBYSHEV 4 /* GPU-only */
-#define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel: corrector on S~ (point
-                               colouring), predictor on K (node-block colouring, node_block)    */
+#define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel: predictor on K (node-block
+                               colouring, node_block), corrector on S~ (point colouring)      */
 /* A_hat modes: smoothers.py:26 A_HAT_MODES */
 #define CAMG_AHAT_PLAIN 0
 #define CAMG_AHAT_ABS_ROWSUM 1
@@ -64,8 +64,8 @@ typedef struct {
   int corr_kind;      /* corrector PointSmootherConfig.kind                                      */
   int corr_sweeps;
   double corr_damping;
-  int node_block;     /* DOFs per node of the level (uniform contiguous blocks; 1 = none): the
-                         node colouring of a CAMG_PT_MCGS predictor on K                         */
+  int node_block;     /* DOFs per displacement node of the level (uniform contiguous blocks;
+                         1 = none): the node colouring of a CAMG_PT_MCGS predictor on K          */
 } camg_smoother_cfg;
 
 /* ---- library ------------------------------------------------------------ */

@@ -9,7 +9,6 @@
 // plus a few small kernels on the lambda side and on the interface rows of B1.
 #include <algorithm>
 #include <cmath>
-#include <cooperative_groups.h>
 #include <cstdlib>
 #include <cub/cub.cuh>
 
@@ -21,20 +20,6 @@ namespace camg {
 
 Csr* schur(const Csr* B2, const Csr* Cz, const Csr* B1, const double* ainv, double scale, cudaStream_t s);
 void recip(int64_t n, const double* d, double* out, cudaStream_t s);
-
-// cooperative (grid-synchronised) MC-SGS when CAMG_COOP_MCGS=1
-static bool use_coop_mcgs() {
-  static int coop = -1;
-  if (coop < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-  }
-  // measured slower than per-colour launches inside the V-cycle graph on
-  // B200 (C5: 28.1 vs 25.7 ms per cycle): opt-in only
-  const char* e = getenv("CAMG_COOP_MCGS");
-  return coop == 1 && e && e[0] == '1';
-}
 
 // ---------------------------------------------------------------------------
 // fused row kernels
@@ -152,151 +137,200 @@ __global__ void __launch_bounds__(256) k_corr_jacobi(CsrView S, const double* __
   }
 }
 
-// one colour of a multicolour Gauss-Seidel sweep on S: rows of one colour
-// are mutually uncoupled, so they update in place:
-//   x_i += dinv_i * (b_i - S_i . x)          (dinv = omega / S_ii)
-// Sweeping colours forward then backward is the reference's residual-form
-// SSOR (smoothers.py:155-164, 189-191) applied to the colour-permuted S.
-template <int G, bool ZEROX>
-__global__ void __launch_bounds__(256) k_mcgs_color(CsrView S, const int32_t* __restrict__ rows, int64_t nrows,
-                                                    const double* __restrict__ b, const double* __restrict__ dinv,
-                                                    double* __restrict__ x) {
+// Multicolour (node-block) Gauss-Seidel kernels for the CSR path (levels
+// without a colour-ordered SELL) and for one-CTA sweeps of small operators.
+// One lane group per node of one colour: the BS rows of the node are
+// accumulated together with the values from before this pass (independent
+// loads, one reduction per row), then the node's DOFs are updated in order
+// (backward: reverse) through its stored diagonal block,
+//   dv_d = dinv_d * (b_d - acc_d - sum_{e before d} K_de dv_e),  y_d += dv_d,
+// which is the sequential Gauss-Seidel update (smoothers.py:155-164) on the
+// colour-permuted operator.  Columns >= split read xl (lambda; null = 0).
+// Rows of one colour share no entries, so no address a group writes is read
+// by another group of the same launch.
+template <int BS, bool FWD>
+__device__ __forceinline__ void node_delta(const double* acc, const double* __restrict__ db,
+                                           const double* __restrict__ b, const double* __restrict__ dinv,
+                                           int64_t base, double* dv) {
+#pragma unroll
+  for (int dd = 0; dd < BS; ++dd) {
+    const int d = FWD ? dd : BS - 1 - dd;
+    double corr = 0.0;
+#pragma unroll
+    for (int ee = 0; ee < dd; ++ee) {
+      const int e = FWD ? ee : BS - 1 - ee;
+      corr = fma(db[d * BS + e], dv[e], corr);
+    }
+    dv[d] = dinv[base + d] * ((b[base + d] - acc[d]) - corr);
+  }
+}
+
+template <int G, int BS, bool FWD>
+__global__ void __launch_bounds__(256) k_mcgs_node(CsrView A, const int32_t* __restrict__ nodes, int64_t nn,
+                                                   const double* __restrict__ dblk, const double* __restrict__ xl,
+                                                   int64_t split, const double* __restrict__ b,
+                                                   const double* __restrict__ dinv, double* y) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
-  for (int64_t k = tid / G; k < nrows; k += stride) {
-    const int64_t i = rows[k];
-    double acc = 0.0;
-    if (!ZEROX) {
-      acc = row_dot<G, false>(S, i, x, nullptr, S.n_cols, lane);
-      acc = group_sum<G>(acc, mask);
+  const double* __restrict__ yr = y;
+  for (int64_t k = tid / G; k < nn; k += stride) {
+    const int64_t node = nodes[k];
+    const int64_t base = node * BS;
+    int64_t p0[BS];
+    int len[BS];
+    int maxlen = 0;
+#pragma unroll
+    for (int r = 0; r < BS; ++r) {
+      p0[r] = A.rowptr[base + r];
+      len[r] = (int)(A.rowptr[base + r + 1] - p0[r]);
+      maxlen = max(maxlen, len[r]);
     }
-    if (lane == 0) x[i] = (ZEROX ? 0.0 : x[i]) + dinv[i] * (b[i] - acc);
+    double acc[BS];
+#pragma unroll
+    for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+    for (int t = lane; t < maxlen; t += G) {
+#pragma unroll
+      for (int r = 0; r < BS; ++r) {
+        if (t < len[r]) {
+          const int32_t c = __ldcs(A.col + p0[r] + t);
+          const double xv = c < split ? __ldg(yr + c) : (xl ? __ldg(xl + (c - split)) : 0.0);
+          acc[r] = fma(__ldcs(A.val + p0[r] + t), xv, acc[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < BS; ++r) acc[r] = group_sum<G>(acc[r], mask);
+    if (lane == 0) {
+      double dv[BS];
+      node_delta<BS, FWD>(acc, dblk + node * (BS * BS), b, dinv, base, dv);
+#pragma unroll
+      for (int d = 0; d < BS; ++d) y[base + d] = yr[base + d] + dv[d];
+    }
   }
 }
 
-// Whole multicolour SSOR sweeps of a small S in one CTA (all colours forward
-// then backward, __syncthreads between colours): replaces 2 x ncolours tiny
-// launches per sweep on the coarse levels.  x lives in shared memory.
-__global__ void __launch_bounds__(1024) k_mcgs_cta(CsrView S, const int32_t* __restrict__ rows,
-                                                   const int64_t* __restrict__ cptr, int ncol, int sweeps,
-                                                   const double* __restrict__ b, const double* __restrict__ dinv,
-                                                   double* __restrict__ xg) {
+// Whole sweeps (all colours forward then backward, __syncthreads between
+// colours) of a small square operator in one CTA, the iterate in shared
+// memory: replaces 2 x ncolours tiny launches per sweep on coarse levels.
+template <int G, int BS>
+__global__ void __launch_bounds__(1024) k_mcgs_node_cta(CsrView A, const int32_t* __restrict__ nodes,
+                                                        const int64_t* __restrict__ cptr, int ncol, int sweeps,
+                                                        bool zero, const double* __restrict__ dblk,
+                                                        const double* __restrict__ b,
+                                                        const double* __restrict__ dinv, double* __restrict__ yg) {
   extern __shared__ double xs[];
-  const int64_t n = S.n_rows;
-  constexpr int G = 8;
+  const int64_t n = A.n_rows;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
   const int grp = threadIdx.x / G, ngrp = blockDim.x / G;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = zero ? 0.0 : yg[i];
   __syncthreads();
   for (int sw = 0; sw < sweeps; ++sw) {
     for (int dir = 0; dir < 2; ++dir) {
       for (int cc = 0; cc < ncol; ++cc) {
         const int c = dir == 0 ? cc : ncol - 1 - cc;
-        const int64_t lo = cptr[c], hi = cptr[c + 1];
-        for (int64_t k = lo + grp; k < hi; k += ngrp) {
-          const int64_t i = rows[k];
-          double acc = 0.0;
-          for (int64_t p = S.rowptr[i] + lane; p < S.rowptr[i + 1]; p += G) acc = fma(S.val[p], xs[S.col[p]], acc);
-          acc = group_sum<G>(acc, mask);
-          if (lane == 0) xs[i] = xs[i] + dinv[i] * (b[i] - acc);
+        for (int64_t k = cptr[c] + grp; k < cptr[c + 1]; k += ngrp) {
+          const int64_t node = nodes[k];
+          const int64_t base = node * BS;
+          int64_t p0[BS];
+          int len[BS];
+          int maxlen = 0;
+#pragma unroll
+          for (int r = 0; r < BS; ++r) {
+            p0[r] = A.rowptr[base + r];
+            len[r] = (int)(A.rowptr[base + r + 1] - p0[r]);
+            maxlen = max(maxlen, len[r]);
+          }
+          double acc[BS];
+#pragma unroll
+          for (int r = 0; r < BS; ++r) acc[r] = 0.0;
+          for (int t = lane; t < maxlen; t += G) {
+#pragma unroll
+            for (int r = 0; r < BS; ++r)
+              if (t < len[r]) acc[r] = fma(A.val[p0[r] + t], xs[A.col[p0[r] + t]], acc[r]);
+          }
+#pragma unroll
+          for (int r = 0; r < BS; ++r) acc[r] = group_sum<G>(acc[r], mask);
+          if (lane == 0) {
+            double dv[BS];
+            if (dir == 0) node_delta<BS, true>(acc, dblk + node * (BS * BS), b, dinv, base, dv);
+            else node_delta<BS, false>(acc, dblk + node * (BS * BS), b, dinv, base, dv);
+#pragma unroll
+            for (int d = 0; d < BS; ++d) xs[base + d] = xs[base + d] + dv[d];
+          }
         }
         __syncthreads();
       }
     }
   }
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xg[i] = xs[i];
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) yg[i] = xs[i];
 }
 
-// Whole multicolour SSOR sweeps of a larger S as ONE cooperative kernel:
-// colours separated by grid-wide barriers instead of kernel boundaries
-// (2 x ncolours launches per sweep otherwise).
-__global__ void __launch_bounds__(256) k_mcgs_coop(CsrView S, const int32_t* __restrict__ rows,
-                                                   const int64_t* __restrict__ cptr, int ncol, int sweeps,
-                                                   const double* __restrict__ b, const double* __restrict__ dinv,
-                                                   double* __restrict__ x) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
-  constexpr int G = 8;
-  const int lane = threadIdx.x & (G - 1);
-  const unsigned mask = group_mask<G>();
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t ngrp = (int64_t)gridDim.x * blockDim.x / G;
-  for (int64_t i = tid; i < S.n_rows; i += (int64_t)gridDim.x * blockDim.x) x[i] = 0.0;
-  grid.sync();
-  for (int sw = 0; sw < sweeps; ++sw) {
-    for (int dir = 0; dir < 2; ++dir) {
-      for (int cc = 0; cc < ncol; ++cc) {
-        const int c = dir == 0 ? cc : ncol - 1 - cc;
-        const int64_t lo = cptr[c], hi = cptr[c + 1];
-        for (int64_t k = lo + tid / G; k < hi; k += ngrp) {
-          const int64_t i = rows[k];
-          double acc = 0.0;
-          for (int64_t p = S.rowptr[i] + lane; p < S.rowptr[i + 1]; p += G) acc = fma(S.val[p], x[S.col[p]], acc);
-          acc = group_sum<G>(acc, mask);
-          if (lane == 0) x[i] = x[i] + dinv[i] * (b[i] - acc);
-        }
-        grid.sync();
-      }
+// diagonal node blocks of rows [0, nn*bs): dblk[node][r][c] (zeros where absent)
+__global__ void k_extract_dblk(CsrView A, int64_t nn, int bs, double* __restrict__ dblk) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nn * bs; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t node = q / bs;
+    const int r = (int)(q % bs);
+    for (int64_t p = A.rowptr[q]; p < A.rowptr[q + 1]; ++p) {
+      const int64_t c = A.col[p] - node * bs;
+      if (c >= 0 && c < bs) dblk[(node * bs + r) * bs + c] = A.val[p];
     }
   }
 }
 
+template <int G, int BS>
+static void launch_mcgs_node(const Csr* A, const int32_t* nodes, int64_t nn, const double* dblk, const double* xl,
+                             int64_t split, const double* b, const double* dinv, double* y, bool fwd, cudaStream_t s) {
+  unsigned grid = grid_for(nn * G, 256, int64_t(kNumSMs) * 16);
+  note_launch();
+  if (fwd) k_mcgs_node<G, BS, true><<<grid, 256, 0, s>>>(view(A), nodes, nn, dblk, xl, split, b, dinv, y);
+  else k_mcgs_node<G, BS, false><<<grid, 256, 0, s>>>(view(A), nodes, nn, dblk, xl, split, b, dinv, y);
+}
+
 template <int G>
-struct LaunchMcgs {
-  static void run(const Csr* S, const int32_t* rows, int64_t nrows, const double* b, const double* dinv, double* x,
-                  bool zerox, cudaStream_t s) {
-    if (nrows <= 0) return;
-    unsigned grid = grid_for(nrows * G, 256, int64_t(kNumSMs) * 16);
-    note_launch();
-    if (zerox) k_mcgs_color<G, true><<<grid, 256, 0, s>>>(view(S), rows, nrows, b, dinv, x);
-    else k_mcgs_color<G, false><<<grid, 256, 0, s>>>(view(S), rows, nrows, b, dinv, x);
+struct LaunchMcgsNode {
+  static void run(const Csr* A, const int32_t* nodes, int64_t nn, int bs, const double* dblk, const double* xl,
+                  int64_t split, const double* b, const double* dinv, double* y, bool fwd, cudaStream_t s) {
+    if (nn <= 0) return;
+    constexpr int GG = G < 4 ? 4 : G;
+    switch (bs) {
+      case 1: return launch_mcgs_node<GG, 1>(A, nodes, nn, dblk, xl, split, b, dinv, y, fwd, s);
+      case 2: return launch_mcgs_node<GG, 2>(A, nodes, nn, dblk, xl, split, b, dinv, y, fwd, s);
+      case 3: return launch_mcgs_node<GG, 3>(A, nodes, nn, dblk, xl, split, b, dinv, y, fwd, s);
+      case 6: return launch_mcgs_node<GG, 6>(A, nodes, nn, dblk, xl, split, b, dinv, y, fwd, s);
+      default: throw Error(CAMG_ERR_NATIVE, "unsupported node block size");
+    }
   }
 };
 
-// Multicolour Gauss-Seidel on the [K | B1] rows of a merged operator (CSR
-// path of the MC-SGS predictor, levels without a colour-ordered SELL): one
-// colour's nodes, the bs DOFs of a node visited in order (backward: reverse)
-// by one lane group, each DOF row reading the values updated before it:
-//   y_i += dinv_i * (b_i - [K B1]_i [y; lam])
-// y is written and re-read inside the kernel: plain (coherent) loads.
-template <int G, bool FWD>
-__global__ void __launch_bounds__(256) k_mcgs_block(CsrView A, const int32_t* __restrict__ nodes, int64_t nn, int bs,
-                                                    const double* __restrict__ xl, int64_t split,
-                                                    const double* __restrict__ b, const double* __restrict__ dinv,
-                                                    double* y) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & (G - 1);
-  const unsigned mask = group_mask<G>();
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
-  for (int64_t k = tid / G; k < nn; k += stride) {
-    const int64_t node = nodes[k];
-    for (int dd = 0; dd < bs; ++dd) {
-      const int64_t i = node * bs + (FWD ? dd : bs - 1 - dd);
-      double acc = 0.0;
-      for (int64_t p = A.rowptr[i] + lane; p < A.rowptr[i + 1]; p += G) {
-        const int32_t c = __ldcs(A.col + p);
-        const double xv = c < split ? y[c] : (xl ? xl[c - split] : 0.0);
-        acc = fma(__ldcs(A.val + p), xv, acc);
-      }
-      acc = group_sum<G>(acc, mask);
-      if (lane == 0) y[i] = y[i] + dinv[i] * (b[i] - acc);
-      __syncwarp(mask);
-    }
+template <int G, int BS>
+static void launch_mcgs_cta(const Csr* A, const int32_t* nodes, const int64_t* cptr, int ncol, int sweeps, bool zero,
+                            const double* dblk, const double* b, const double* dinv, double* y, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_node_cta<G, BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * kMcgsCtaRows)));
+    attr = true;
   }
+  note_launch();
+  k_mcgs_node_cta<G, BS><<<1, 1024, sizeof(double) * A->n_rows, s>>>(view(A), nodes, cptr, ncol, sweeps, zero, dblk, b,
+                                                                     dinv, y);
 }
 
 template <int G>
-struct LaunchMcgsBlock {
-  static void run(const Csr* A, const int32_t* nodes, int64_t nn, int bs, const double* xl, int64_t split,
-                  const double* b, const double* dinv, double* y, bool fwd, cudaStream_t s) {
-    if (nn <= 0) return;
-    unsigned grid = grid_for(nn * G, 256, int64_t(kNumSMs) * 16);
-    note_launch();
-    if (fwd) k_mcgs_block<G, true><<<grid, 256, 0, s>>>(view(A), nodes, nn, bs, xl, split, b, dinv, y);
-    else k_mcgs_block<G, false><<<grid, 256, 0, s>>>(view(A), nodes, nn, bs, xl, split, b, dinv, y);
+struct LaunchMcgsCta {
+  static void run(const Csr* A, const int32_t* nodes, const int64_t* cptr, int ncol, int bs, int sweeps, bool zero,
+                  const double* dblk, const double* b, const double* dinv, double* y, cudaStream_t s) {
+    constexpr int GG = G < 4 ? 4 : G;
+    switch (bs) {
+      case 1: return launch_mcgs_cta<GG, 1>(A, nodes, cptr, ncol, sweeps, zero, dblk, b, dinv, y, s);
+      case 2: return launch_mcgs_cta<GG, 2>(A, nodes, cptr, ncol, sweeps, zero, dblk, b, dinv, y, s);
+      case 3: return launch_mcgs_cta<GG, 3>(A, nodes, cptr, ncol, sweeps, zero, dblk, b, dinv, y, s);
+      case 6: return launch_mcgs_cta<GG, 6>(A, nodes, cptr, ncol, sweeps, zero, dblk, b, dinv, y, s);
+      default: throw Error(CAMG_ERR_NATIVE, "unsupported node block size");
+    }
   }
 };
 
@@ -540,9 +574,12 @@ struct McgsK {
   int64_t nu = 0;
   int bs = 1;
   std::vector<int64_t> col_ptr, col_slice;
+  DBuf<int64_t> col_ptr_dev;
   DBuf<int32_t> nodes;
+  DBuf<double> dblk;  // diagonal node blocks (CSR / CTA paths)
   Sell* sell = nullptr;
   DBuf<double> g;
+  bool cta = false;  // small square operator: whole sweeps in one CTA
   ~McgsK() { delete sell; }
   int colors() const { return (int)col_ptr.size() - 1; }
 
@@ -566,11 +603,24 @@ struct McgsK {
     }
     nodes = DBuf<int32_t>(nn + 1);
     CAMG_CUDA(cudaMemcpy(nodes.p, nd.data(), sizeof(int32_t) * nn, cudaMemcpyHostToDevice));
+    dblk = DBuf<double>(nn * bs * bs + 1);
+    CAMG_CUDA(cudaMemsetAsync(dblk.p, 0, sizeof(double) * (nn * bs * bs + 1), s));
+    note_launch();
+    k_extract_dblk<<<grid_for(nu, 256), 256, 0, s>>>(view(K), nn, bs, dblk.p);
+    col_ptr_dev = DBuf<int64_t>(ncol + 1);
+    CAMG_CUDA(cudaMemcpy(col_ptr_dev.p, col_ptr.data(), sizeof(int64_t) * (ncol + 1), cudaMemcpyHostToDevice));
+    // one-CTA sweeps for small square operators (CAMG_MCGS_CTA=0 disables,
+    // =1 lifts the non-zero limit)
+    // (CAMG_MCGS_CTA=0 disables; measured against per-colour launches)
+    const char* cta_env = getenv("CAMG_MCGS_CTA");
+    cta = !(cta_env && cta_env[0] == '0') && K->n_cols == nu && nu <= kMcgsCtaRows && K->nnz <= kMcgsCtaNnz;
     // colour-ordered SELL from kGsSellMinRows rows (CAMG_GS_SELL=1 forces it,
     // =0 keeps the CSR path)
     const char* env = getenv("CAMG_GS_SELL");
-    const bool want = env ? env[0] == '1' : nu >= kGsSellMinRows;
-    if (want && (bs == 1 || bs == 2 || bs == 3 || bs == 6)) {
+    // (lane-per-node SELL needs enough nodes per colour to fill the GPU;
+    // below that the group-per-row CSR kernel has more parallelism)
+    const bool want = env ? env[0] == '1' : (nu >= kGsSellMinRows && nn >= (int64_t)ncol * kGsSellMinNodesPerColour);
+    if (!cta && want && (bs == 1 || bs == 2 || bs == 3 || bs == 6)) {
       // positions: each colour's nodes in ascending order, padded to whole slices
       std::vector<int32_t> order;
       col_slice.assign(ncol + 1, 0);
@@ -603,8 +653,8 @@ struct McgsK {
     if (sell) {
       sell_gs_launch(sell, col_slice[c], col_slice[c + 1], fwd, zero, nullptr, nu, g.p, dinv, y, s);
     } else {
-      dispatch_g<LaunchMcgsBlock>(Arows->avg_row, Arows, nodes.p + col_ptr[c], col_ptr[c + 1] - col_ptr[c], bs, xl,
-                                  nu, b, dinv, y, fwd, s);
+      dispatch_g<LaunchMcgsNode>(Arows->avg_row, Arows, nodes.p + col_ptr[c], col_ptr[c + 1] - col_ptr[c], bs,
+                                 dblk.p, xl, nu, b, dinv, y, fwd, s);
     }
   }
 
@@ -613,6 +663,11 @@ struct McgsK {
   void run(bool zero, const Csr* Arows, const double* xl, const double* b, const double* dinv, double* y, int sweeps,
            cudaStream_t s) {
     const int nc = colors();
+    if (cta && Arows->n_cols == nu) {
+      dispatch_g<LaunchMcgsCta>(Arows->avg_row, Arows, nodes.p, col_ptr_dev.p, nc, bs, sweeps, zero, dblk.p, b, dinv, y,
+                                s);
+      return;
+    }
     for (int k = 0; k < sweeps; ++k) {
       for (int c = 0; c < nc; ++c) pass(c, true, zero && k == 0 && c == 0, Arows, xl, b, dinv, y, s);
       for (int c = nc - 1; c >= 0; --c) pass(c, false, false, Arows, xl, b, dinv, y, s);
@@ -648,10 +703,8 @@ struct Level {
   DBuf<int64_t> b1_rows;
   int64_t n_b1_rows = 0;
   DBuf<double> dinv_p, ainv, dinv_c;
-  // multicolour Gauss-Seidel corrector: rows grouped by colour
-  std::vector<int64_t> color_ptr;
-  DBuf<int64_t> color_ptr_dev;
-  DBuf<int32_t> color_rows;
+  // multicolour Gauss-Seidel corrector on S~ (point colouring)
+  McgsK cgs;
   // multicolour Gauss-Seidel predictor on K
   McgsK gs;
   // external predictor solver (nested preconditioner: scalar AMG V-cycle on
@@ -695,46 +748,11 @@ struct Level {
       return w_dl.p;
     }
     if (cfg.corr_kind == CAMG_PT_MCGS) {
-      const int nc_ = (int)color_ptr.size() - 1;
-      double* x = w_dl.p;
-      const char* cta_env = getenv("CAMG_MCGS_CTA");
-      if (nl <= kMcgsCtaRows && S->nnz <= kMcgsCtaNnz && !(cta_env && cta_env[0] == '0')) {
-        static bool attr = false;
-        if (!attr) {
-          CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(sizeof(double) * kMcgsCtaRows)));
-          attr = true;
-        }
-        note_launch();
-        k_mcgs_cta<<<1, 1024, sizeof(double) * nl, s>>>(view(S), color_rows.p, color_ptr_dev.p, nc_, cfg.corr_sweeps,
-                                                        rc, dinv_c.p, x);
-        return x;
-      }
-      if (use_coop_mcgs()) {
-        static int blocks_per_sm = -1;
-        if (blocks_per_sm < 0)
-          CAMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_mcgs_coop, 256, 0));
-        const int nb = std::max(1, std::min(blocks_per_sm, 4)) * kNumSMs;
-        CsrView sv = view(S);
-        const int32_t* rp = color_rows.p;
-        const int64_t* cp = color_ptr_dev.p;
-        int ncol = nc_, sweeps = cfg.corr_sweeps;
-        void* args[] = {&sv, &rp, &cp, &ncol, &sweeps, (void*)&rc, (void*)&dinv_c.p, &x};
-        note_launch();
-        CAMG_CUDA(cudaLaunchCooperativeKernel((void*)k_mcgs_coop, dim3(nb), dim3(256), args, 0, s));
-        return x;
-      }
-      // x = 0, then colour 0 of the first sweep needs no product
-      CAMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nl, s));
-      for (int sw = 0; sw < cfg.corr_sweeps; ++sw) {
-        for (int c = 0; c < nc_; ++c)
-          dispatch_g<LaunchMcgs>(S->avg_row, S, color_rows.p + color_ptr[c], color_ptr[c + 1] - color_ptr[c], rc,
-                                 dinv_c.p, x, sw == 0 && c == 0, s);
-        for (int c = nc_ - 1; c >= 0; --c)
-          dispatch_g<LaunchMcgs>(S->avg_row, S, color_rows.p + color_ptr[c], color_ptr[c + 1] - color_ptr[c], rc,
-                                 dinv_c.p, x, false, s);
-      }
-      return x;
+      // reference SSOR (smoothers.py:155-164, 189-191) on the node-colour
+      // permuted S~, from zero
+      cgs.init(nullptr, rc, w_dl.p, s);
+      cgs.run(true, S, nullptr, rc, dinv_c.p, w_dl.p, cfg.corr_sweeps, s);
+      return w_dl.p;
     }
     double* cur = w_dl.p;
     double* nxt = w_dl2.p;
@@ -882,44 +900,6 @@ static void check_no_zero(const double* d, int64_t n, const char* what) {
   if (h != ~0ull) throw Error(CAMG_ERR_SINGULAR, std::string(what) + ": zero diagonal in row " + std::to_string(h));
 }
 
-// greedy colouring of the symmetrised pattern of S in natural row order
-// (host; S~ has n_lam rows), rows grouped by colour in ascending order
-static void greedy_coloring(const Csr* S, std::vector<int64_t>& color_ptr, DBuf<int32_t>& rows_out) {
-  const int64_t n = S->n_rows;
-  std::vector<int64_t> rp(n + 1);
-  std::vector<int32_t> ci(S->nnz);
-  CAMG_CUDA(cudaMemcpy(rp.data(), S->rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
-  if (S->nnz) CAMG_CUDA(cudaMemcpy(ci.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
-  // transpose pattern
-  std::vector<int64_t> tp(n + 1, 0);
-  for (int64_t k = 0; k < S->nnz; ++k) tp[ci[k] + 1]++;
-  for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
-  std::vector<int32_t> ti(S->nnz);
-  std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) ti[fill[ci[k]]++] = (int32_t)i;
-  std::vector<int32_t> color(n, -1);
-  std::vector<int64_t> mark;
-  int ncol = 0;
-  for (int64_t i = 0; i < n; ++i) {
-    mark.clear();
-    for (int64_t k = rp[i]; k < rp[i + 1]; ++k) if (color[ci[k]] >= 0) mark.push_back(color[ci[k]]);
-    for (int64_t k = tp[i]; k < tp[i + 1]; ++k) if (color[ti[k]] >= 0) mark.push_back(color[ti[k]]);
-    std::sort(mark.begin(), mark.end());
-    int c = 0;
-    for (int64_t m : mark) { if (m == c) ++c; else if (m > c) break; }
-    color[i] = c;
-    ncol = std::max(ncol, c + 1);
-  }
-  color_ptr.assign(ncol + 1, 0);
-  for (int64_t i = 0; i < n; ++i) color_ptr[color[i] + 1]++;
-  for (int c = 0; c < ncol; ++c) color_ptr[c + 1] += color_ptr[c];
-  std::vector<int32_t> rows(n);
-  std::vector<int64_t> pos(color_ptr.begin(), color_ptr.end() - 1);
-  for (int64_t i = 0; i < n; ++i) rows[pos[color[i]]++] = (int32_t)i;
-  rows_out = DBuf<int32_t>(n + 1);
-  CAMG_CUDA(cudaMemcpy(rows_out.p, rows.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
-}
 
 
 double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s);
@@ -1024,12 +1004,9 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
   }
   if (cfg.kind != CAMG_BRAESS_SARAZIN && cfg.pred_kind == CAMG_PT_MCGS) L->gs.setup(K, cfg.node_block, s);
-  if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) {
-    greedy_coloring(L->S, L->color_ptr, L->color_rows);
-    L->color_ptr_dev = DBuf<int64_t>(L->color_ptr.size());
-    CAMG_CUDA(cudaMemcpy(L->color_ptr_dev.p, L->color_ptr.data(), sizeof(int64_t) * L->color_ptr.size(),
-                         cudaMemcpyHostToDevice));
-  }
+  // point colouring of S~: the multiplier-node graph needs as many colours
+  // (16 on C5) and the per-node kernels measured slower
+  if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) L->cgs.setup(L->S, 1, s);
   if ((cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_MCGS) && nl > 0) {
     DBuf<double> dS(nl + 1);
     csr_diagonal(L->S, 0, dS.p, s);

@@ -16,6 +16,7 @@ constexpr int64_t kSellPairSlices = 40000;  // below: two lanes per block row (w
 constexpr int64_t kMcgsCtaRows = 24576;  // S~ up to this size: single-CTA MC-SGS (x in 192 KB smem)
 constexpr int64_t kMcgsCtaNnz = 131072;
 constexpr int64_t kGsSellMinRows = 30000;
+constexpr int64_t kGsSellMinNodesPerColour = 16384;  // ... and this many nodes per colour
 constexpr double kChebRatio = 30.0;  // Chebyshev predictor: lower bound lmax / 30 (Ifpack2 / MueLu default)
 constexpr double kChebBoost = 1.1;   // ... upper bound 1.1 lmax  // MC-SGS predictor: colour-ordered SELL from this many K rows  // ... and this many non-zeros (one SM streams it per colour pass)
 

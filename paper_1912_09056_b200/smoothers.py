@@ -197,9 +197,10 @@ def build_schur(op, a_hat_mode: str = "plain_diag", alpha: float = 1.0, scale_wi
 class BlockSmoother:
     """Bound block smoother (smoothers.py:245-329), executed by libcamg.
 
-    `node_block` (extension): DOFs per node of the level when every node owns
-    that many consecutive DOFs; it sets the node colouring of an `mcgs`
-    predictor (1 = colour single DOFs)."""
+    `node_block` (extension): DOFs per displacement node of the level when
+    every node owns that many consecutive DOFs; it sets the node colouring of
+    an `mcgs` predictor (1 = colour single DOFs).  An `mcgs` corrector colours
+    the rows of S~."""
 
     def __init__(self, cfg: BlockSmootherConfig, op, predictor_solver=None, pre_sweeps: int = 1,
                  post_sweeps: int = 1, node_block: int = 1):

@@ -425,12 +425,14 @@ def test_graph_disabled_equals_graph():
     np.testing.assert_array_equal(z1, z2)
 
 
-@pytest.mark.parametrize("path", ["coop", "per-colour"])
+@pytest.mark.parametrize("path", ["csr", "sell", "default"])
 def test_mcgs_large_s_paths(path, monkeypatch):
-    """The MC-SGS corrector paths used for large S~ (cooperative grid-synced
-    sweep, or one launch per colour) against the oracle emulation."""
-    monkeypatch.setenv("CAMG_MCGS_CTA", "0")
-    monkeypatch.setenv("CAMG_COOP_MCGS", "1" if path == "coop" else "0")
+    """Every MC-SGS execution path (one CSR launch per colour, the
+    colour-ordered SELL kernel, the default choice incl. one-CTA sweeps on
+    small levels) against the oracle emulation."""
+    if path != "default":
+        monkeypatch.setenv("CAMG_MCGS_CTA", "0")
+        monkeypatch.setenv("CAMG_GS_SELL", "1" if path == "sell" else "0")
     skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcgs", 1, 1.0))
     hkw = dict(max_levels=3, max_coarse_size=50)
     g = generate(config_spec("C5", 10))
