@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) k_spmv(CsrView A, int64_t row0, int64_t n
                                               const double* __restrict__ xu,
                                               const double* __restrict__ xl, int64_t split,
                                               double beta, double* __restrict__ y) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
@@ -91,11 +92,11 @@ static void spmv_launch(const Csr* A, int64_t row0, int64_t nrows, double alpha,
   note_launch();
   bool sp = split < A->n_cols;
   if (beta != 0.0) {
-    if (sp) k_spmv<G, true, true><<<grid, block, 0, s>>>(view(A), row0, nrows, alpha, xu, xl, split, beta, y);
-    else k_spmv<G, true, false><<<grid, block, 0, s>>>(view(A), row0, nrows, alpha, xu, xl, split, beta, y);
+    if (sp) launch_k(k_spmv<G, true, true>, grid, block, 0, s, view(A), row0, nrows, alpha, xu, xl, split, beta, y);
+    else launch_k(k_spmv<G, true, false>, grid, block, 0, s, view(A), row0, nrows, alpha, xu, xl, split, beta, y);
   } else {
-    if (sp) k_spmv<G, false, true><<<grid, block, 0, s>>>(view(A), row0, nrows, alpha, xu, xl, split, beta, y);
-    else k_spmv<G, false, false><<<grid, block, 0, s>>>(view(A), row0, nrows, alpha, xu, xl, split, beta, y);
+    if (sp) launch_k(k_spmv<G, false, true>, grid, block, 0, s, view(A), row0, nrows, alpha, xu, xl, split, beta, y);
+    else launch_k(k_spmv<G, false, false>, grid, block, 0, s, view(A), row0, nrows, alpha, xu, xl, split, beta, y);
   }
   CAMG_LAUNCH_CHECK();
 }
@@ -443,6 +444,15 @@ __global__ void k_power_step(CsrView A, const double* __restrict__ d, const doub
 __global__ void k_div(int64_t n, const double* __restrict__ w, double s, double* __restrict__ v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[i] = __ddiv_rn(w[i], s);
+}
+
+bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAMG_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 // lambda_max(D^-1 A) by power iteration from ones/sqrt(n) (the algorithm of

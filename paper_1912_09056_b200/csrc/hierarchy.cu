@@ -44,6 +44,7 @@ struct RowEpi {
 template <int G, bool ZERO, bool SPLIT>
 __global__ void __launch_bounds__(256) k_resid(CsrView A, int64_t row0, int64_t nrows, const double* __restrict__ xu,
                                                const double* __restrict__ xl, int64_t split, RowEpi e) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(256) k_jacobi(CsrView A, int64_t nu, const dou
                                                 const double* __restrict__ r, const double* __restrict__ dinv,
                                                 double* __restrict__ d_new, const double* __restrict__ x,
                                                 double* __restrict__ out_x, double coef) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
@@ -105,6 +107,7 @@ template <int G>
 __global__ void __launch_bounds__(256) k_lam_rhs(CsrView A, int64_t nu, int64_t nl, const double* __restrict__ vu,
                                                  const double* __restrict__ vl, const double* __restrict__ c,
                                                  double* __restrict__ rc) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
@@ -122,6 +125,7 @@ template <int G, bool FIRST>
 __global__ void __launch_bounds__(256) k_corr_jacobi(CsrView S, const double* __restrict__ rc,
                                                      const double* __restrict__ dinv, const double* __restrict__ dl,
                                                      double* __restrict__ dl_new) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
@@ -165,16 +169,23 @@ __device__ __forceinline__ void node_delta(const double* acc, const double* __re
   }
 }
 
+// The colour passes form a chain of small kernels: each lets its successor
+// launch at once and the successor loads its constant operands (node list,
+// row structure, the first matrix entries) before waiting (PDL, kernels.cuh),
+// so the launch gap and the matrix-load latency leave the critical path.
 template <int G, int BS, bool FWD>
 __global__ void __launch_bounds__(256) k_mcgs_node(CsrView A, const int32_t* __restrict__ nodes, int64_t nn,
                                                    const double* __restrict__ dblk, const double* __restrict__ xl,
                                                    int64_t split, const double* __restrict__ b,
                                                    const double* __restrict__ dinv, double* y) {
+  pdl_launch_dependents();
+  constexpr int PRE = BS == 1 ? 4 : (BS <= 3 ? 2 : 1);  // entries per row and lane loaded before the wait
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
   const double* __restrict__ yr = y;
+  bool waited = false;
   for (int64_t k = tid / G; k < nn; k += stride) {
     const int64_t node = nodes[k];
     const int64_t base = node * BS;
@@ -187,10 +198,34 @@ __global__ void __launch_bounds__(256) k_mcgs_node(CsrView A, const int32_t* __r
       len[r] = (int)(A.rowptr[base + r + 1] - p0[r]);
       maxlen = max(maxlen, len[r]);
     }
+    int32_t pc[BS][PRE];
+    double pv[BS][PRE];
+#pragma unroll
+    for (int r = 0; r < BS; ++r)
+#pragma unroll
+      for (int j = 0; j < PRE; ++j) {
+        const int t = lane + j * G;
+        pc[r][j] = t < len[r] ? __ldcs(A.col + p0[r] + t) : -1;
+        pv[r][j] = t < len[r] ? __ldcs(A.val + p0[r] + t) : 0.0;
+      }
+    if (!waited) {
+      pdl_wait();  // y, b and lambda come from the preceding kernels
+      waited = true;
+    }
     double acc[BS];
 #pragma unroll
-    for (int r = 0; r < BS; ++r) acc[r] = 0.0;
-    for (int t = lane; t < maxlen; t += G) {
+    for (int r = 0; r < BS; ++r) {
+      acc[r] = 0.0;
+#pragma unroll
+      for (int j = 0; j < PRE; ++j) {
+        const int32_t c = pc[r][j];
+        if (c >= 0) {
+          const double xv = c < split ? __ldg(yr + c) : (xl ? __ldg(xl + (c - split)) : 0.0);
+          acc[r] = fma(pv[r][j], xv, acc[r]);
+        }
+      }
+    }
+    for (int t = lane + PRE * G; t < maxlen; t += G) {
 #pragma unroll
       for (int r = 0; r < BS; ++r) {
         if (t < len[r]) {
@@ -220,6 +255,7 @@ __global__ void __launch_bounds__(1024) k_mcgs_node_cta(CsrView A, const int32_t
                                                         bool zero, const double* __restrict__ dblk,
                                                         const double* __restrict__ b,
                                                         const double* __restrict__ dinv, double* __restrict__ yg) {
+  CAMG_PDL_ENTRY();
   extern __shared__ double xs[];
   const int64_t n = A.n_rows;
   const int lane = threadIdx.x & (G - 1);
@@ -285,8 +321,8 @@ static void launch_mcgs_node(const Csr* A, const int32_t* nodes, int64_t nn, con
                              int64_t split, const double* b, const double* dinv, double* y, bool fwd, cudaStream_t s) {
   unsigned grid = grid_for(nn * G, 256, int64_t(kNumSMs) * 16);
   note_launch();
-  if (fwd) k_mcgs_node<G, BS, true><<<grid, 256, 0, s>>>(view(A), nodes, nn, dblk, xl, split, b, dinv, y);
-  else k_mcgs_node<G, BS, false><<<grid, 256, 0, s>>>(view(A), nodes, nn, dblk, xl, split, b, dinv, y);
+  if (fwd) launch_k(k_mcgs_node<G, BS, true>, grid, 256, 0, s, view(A), nodes, nn, dblk, xl, split, b, dinv, y);
+  else launch_k(k_mcgs_node<G, BS, false>, grid, 256, 0, s, view(A), nodes, nn, dblk, xl, split, b, dinv, y);
 }
 
 template <int G>
@@ -337,6 +373,7 @@ struct LaunchMcgsCta {
 // y = x_u (zero if x is null), g = b_u
 __global__ void k_gs_init(int64_t nu, const double* __restrict__ x, const double* __restrict__ b,
                           double* __restrict__ y, double* __restrict__ g) {
+  CAMG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nu; i += (int64_t)gridDim.x * blockDim.x) {
     y[i] = x ? x[i] : 0.0;
     g[i] = b[i];
@@ -346,6 +383,7 @@ __global__ void k_gs_init(int64_t nu, const double* __restrict__ x, const double
 // g_i -= B1_i . lam on the nonempty rows of B1 (g = b_u - B1 lam)
 __global__ void k_b1_sub(CsrView B1, const int64_t* __restrict__ rows, int64_t nrows, const double* __restrict__ lam,
                          double* __restrict__ g) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 7;
   const unsigned mask = group_mask<8>();
@@ -361,6 +399,7 @@ __global__ void k_b1_sub(CsrView B1, const int64_t* __restrict__ rows, int64_t n
 // Uzawa relaxation: out = x0 + alpha (y - x0)   (x0 null = 0)
 __global__ void k_relax(int64_t n, const double* __restrict__ x0, const double* __restrict__ y, double alpha,
                         double* __restrict__ out) {
+  CAMG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double o = x0 ? x0[i] : 0.0;
     out[i] = o + alpha * (y[i] - o);
@@ -370,6 +409,7 @@ __global__ void k_relax(int64_t n, const double* __restrict__ x0, const double* 
 // x_out_lam = x_lam + coef*dl
 __global__ void k_lam_update(int64_t nl, const double* __restrict__ xl, const double* __restrict__ dl, double coef,
                              double* __restrict__ out) {
+  CAMG_PDL_ENTRY();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nl; q += (int64_t)gridDim.x * blockDim.x)
     out[q] = (xl ? xl[q] : 0.0) + coef * dl[q];
 }
@@ -378,6 +418,7 @@ __global__ void k_lam_update(int64_t nl, const double* __restrict__ xl, const do
 __global__ void k_b1_correct(CsrView B1, const int64_t* __restrict__ rows, int64_t nrows,
                              const double* __restrict__ ainv, const double* __restrict__ dl, double mult,
                              double* __restrict__ xu) {
+  CAMG_PDL_ENTRY();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 7;
   const unsigned mask = group_mask<8>();
@@ -393,6 +434,7 @@ __global__ void k_b1_correct(CsrView B1, const int64_t* __restrict__ rows, int64
 // small dense LU solve (LAPACK getrf factors, column-major, 0-based pivots)
 __global__ void __launch_bounds__(1024) k_lu_solve(int n, const double* __restrict__ LU, const int32_t* __restrict__ piv,
                                                    const double* __restrict__ b, double* __restrict__ xg) {
+  CAMG_PDL_ENTRY();
   extern __shared__ double xs[];
   const bool sh = n <= 12288;
   double* x = sh ? xs : xg;
@@ -440,6 +482,7 @@ __global__ void k_nonempty_flags(const int64_t* __restrict__ rowptr, int64_t n, 
 }
 
 __global__ void k_copy(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  CAMG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     b[i] = a[i];
 }
@@ -466,9 +509,9 @@ struct LaunchResid {
     if (nrows <= 0) return;
     unsigned grid = grid_for(nrows * G, 256, int64_t(kNumSMs) * 16);
     note_launch();
-    if (zero) k_resid<G, true, false><<<grid, 256, 0, s>>>(view(A), row0, nrows, xu, xl, split, e);
-    else if (split < A->n_cols) k_resid<G, false, true><<<grid, 256, 0, s>>>(view(A), row0, nrows, xu, xl, split, e);
-    else k_resid<G, false, false><<<grid, 256, 0, s>>>(view(A), row0, nrows, xu, xl, split, e);
+    if (zero) launch_k(k_resid<G, true, false>, grid, 256, 0, s, view(A), row0, nrows, xu, xl, split, e);
+    else if (split < A->n_cols) launch_k(k_resid<G, false, true>, grid, 256, 0, s, view(A), row0, nrows, xu, xl, split, e);
+    else launch_k(k_resid<G, false, false>, grid, 256, 0, s, view(A), row0, nrows, xu, xl, split, e);
   }
 };
 
@@ -478,7 +521,7 @@ struct LaunchJacobi {
                   const double* x, double* ox, double coef, cudaStream_t s) {
     unsigned grid = grid_for(nu * G, 256, int64_t(kNumSMs) * 16);
     note_launch();
-    k_jacobi<G><<<grid, 256, 0, s>>>(view(A), nu, d, r, dinv, dn, x, ox, coef);
+    launch_k(k_jacobi<G>, grid, 256, 0, s, view(A), nu, d, r, dinv, dn, x, ox, coef);
   }
 };
 
@@ -489,7 +532,7 @@ struct LaunchLamRhs {
     if (nl <= 0) return;
     unsigned grid = grid_for(nl * G, 256, int64_t(kNumSMs) * 16);
     note_launch();
-    k_lam_rhs<G><<<grid, 256, 0, s>>>(view(A), nu, nl, vu, vl, c, rc);
+    launch_k(k_lam_rhs<G>, grid, 256, 0, s, view(A), nu, nl, vu, vl, c, rc);
   }
 };
 
@@ -500,8 +543,8 @@ struct LaunchCorr {
     if (S->n_rows <= 0) return;
     unsigned grid = grid_for(S->n_rows * G, 256, int64_t(kNumSMs) * 16);
     note_launch();
-    if (first) k_corr_jacobi<G, true><<<grid, 256, 0, s>>>(view(S), rc, dinv, dl, dn);
-    else k_corr_jacobi<G, false><<<grid, 256, 0, s>>>(view(S), rc, dinv, dl, dn);
+    if (first) launch_k(k_corr_jacobi<G, true>, grid, 256, 0, s, view(S), rc, dinv, dl, dn);
+    else launch_k(k_corr_jacobi<G, false>, grid, 256, 0, s, view(S), rc, dinv, dl, dn);
   }
 };
 
@@ -639,12 +682,12 @@ struct McgsK {
   void init(const double* x, const double* b, double* y, cudaStream_t s) {
     if (sell) {
       note_launch();
-      k_gs_init<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, b, y, g.p);
+      launch_k(k_gs_init, grid_for(nu, 256), 256, 0, s, nu, x, b, y, g.p);
     } else if (!x) {
       CAMG_CUDA(cudaMemsetAsync(y, 0, sizeof(double) * nu, s));
     } else {
       note_launch();
-      k_copy<<<grid_for(nu, 256), 256, 0, s>>>(nu, x, y);
+      launch_k(k_copy, grid_for(nu, 256), 256, 0, s, nu, x, y);
     }
   }
 
@@ -678,6 +721,7 @@ struct McgsK {
 // pred_update: out = x + alpha du (and, when uh != null, uh = x + du)
 __global__ void k_pred_update(int64_t n, const double* __restrict__ x, const double* __restrict__ du, double alpha,
                               double* __restrict__ uh, double* __restrict__ out) {
+  CAMG_PDL_ENTRY();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double xi = x ? x[i] : 0.0;
     if (uh) uh[i] = xi + du[i];
@@ -744,7 +788,7 @@ struct Level {
       CAMG_CHECK(corr_lu.p != nullptr, CAMG_ERR_SETUP, "direct corrector factors were not set");
       note_launch();
       size_t sh = nl <= 12288 ? sizeof(double) * nl : 0;
-      k_lu_solve<<<1, 1024, sh, s>>>((int)nl, corr_lu.p, corr_piv.p, rc, w_dl.p);
+      launch_k(k_lu_solve, 1, 1024, sh, s, (int)nl, corr_lu.p, corr_piv.p, rc, w_dl.p);
       return w_dl.p;
     }
     if (cfg.corr_kind == CAMG_PT_MCGS) {
@@ -775,7 +819,7 @@ struct Level {
     gs.init(x, b, y, s);
     if (gs.sell && xl && n_b1_rows) {
       note_launch();
-      k_b1_sub<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, xl, gs.g.p);
+      launch_k(k_b1_sub, grid_for(n_b1_rows * 8, 256), 256, 0, s, view(B1), b1_rows.p, n_b1_rows, xl, gs.g.p);
     }
     gs.run(x == nullptr, A, xl, b, dinv_p.p, y, sweeps, s);
   }
@@ -802,10 +846,10 @@ struct Level {
       const double* du = scalar_run(inner, w_ru.p, s);
       note_launch();
       if (kind == CAMG_UZAWA) {
-        k_pred_update<<<grid_for(nu, 256), 256, 0, s>>>(nu, xu, du, alpha, w_du2.p, xo);
+        launch_k(k_pred_update, grid_for(nu, 256), 256, 0, s, nu, xu, du, alpha, w_du2.p, xo);
         uh = w_du2.p;
       } else {
-        k_pred_update<<<grid_for(nu, 256), 256, 0, s>>>(nu, xu, du, 1.0, nullptr, xo);
+        launch_k(k_pred_update, grid_for(nu, 256), 256, 0, s, nu, xu, du, 1.0, nullptr, xo);
       }
     } else if (cfg.pred_kind == CAMG_PT_MCGS) {
       // Uzawa keeps y for the lambda side and relaxes u_new = u + alpha (y - u)
@@ -813,7 +857,7 @@ struct Level {
       gs_predict(x, b, y, sp, s);
       if (kind == CAMG_UZAWA) {
         note_launch();
-        k_relax<<<grid_for(nu, 256), 256, 0, s>>>(nu, xu, y, alpha, xo);
+        launch_k(k_relax, grid_for(nu, 256), 256, 0, s, nu, xu, y, alpha, xo);
         uh = y;
       }
     } else {
@@ -859,12 +903,12 @@ struct Level {
     double* dl = corrector(w_rc.p, s);
     const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
     note_launch();
-    k_lam_update<<<grid_for(nl, 256), 256, 0, s>>>(nl, xl, dl, cl, xo + nu);
+    launch_k(k_lam_update, grid_for(nl, 256), 256, 0, s, nl, xl, dl, cl, xo + nu);
     if (kind != CAMG_UZAWA && n_b1_rows) {
       // u_new = u_half - c A^-1 B1 dlam on the interface rows
       const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
       note_launch();
-      k_b1_correct<<<grid_for(n_b1_rows * 8, 256), 256, 0, s>>>(view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
+      launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, s, view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
     }
   }
 
@@ -1099,7 +1143,7 @@ struct Hierarchy {
       CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "coarse LU factors were not set");
       note_launch();
       size_t sh = n_coarse <= 12288 ? sizeof(double) * n_coarse : 0;
-      k_lu_solve<<<1, 1024, sh, s>>>((int)n_coarse, lu.p, piv.p, b, x);
+      launch_k(k_lu_solve, 1, 1024, sh, s, (int)n_coarse, lu.p, piv.p, b, x);
     } else {
       L->sweep(nullptr, b, x, s);
     }
@@ -1262,7 +1306,7 @@ struct ScalarHier {
       CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "scalar coarse LU factors were not set");
       note_launch();
       size_t sh = n_coarse <= 12288 ? sizeof(double) * n_coarse : 0;
-      k_lu_solve<<<1, 1024, sh, s>>>((int)n_coarse, lu.p, piv.p, b, L.x0.p);
+      launch_k(k_lu_solve, 1, 1024, sh, s, (int)n_coarse, lu.p, piv.p, b, L.x0.p);
       return L.x0.p;
     }
     smooth(L, nullptr, b, L.x0.p, s);

@@ -20,6 +20,40 @@ constexpr int64_t kGsSellMinNodesPerColour = 16384;  // ... and this many nodes 
 constexpr double kChebRatio = 30.0;  // Chebyshev predictor: lower bound lmax / 30 (Ifpack2 / MueLu default)
 constexpr double kChebBoost = 1.1;   // ... upper bound 1.1 lmax  // MC-SGS predictor: colour-ordered SELL from this many K rows  // ... and this many non-zeros (one SM streams it per colour pass)
 
+// Programmatic dependent launch (PDL): V-cycle kernels let their successor
+// launch as soon as every CTA of theirs runs (launch_dependents) and wait for
+// the predecessor's completion before touching produced data (wait), so the
+// launch latency of the ~500 kernels of a cycle overlaps the previous tail.
+// Without the PDL launch attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define CAMG_PDL_ENTRY() \
+  do {                    \
+    pdl_launch_dependents(); \
+    pdl_wait();           \
+  } while (0)
+
+bool use_pdl();  // CAMG_PDL=0 disables
+
+template <class K, class... Args>
+inline void launch_k(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  if (!use_pdl()) {
+    kernel<<<grid, block, smem, s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CAMG_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+}
+
 // lanes per row for vector-CSR kernels, from the mean row length
 inline int group_for(double avg) {
   if (avg <= 1.5) return 1;

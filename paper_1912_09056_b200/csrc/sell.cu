@@ -260,6 +260,7 @@ template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED>
 __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
+  CAMG_PDL_ENTRY();
   // MODE 0: spmv y = alpha*acc + beta*y
   // MODE 1: residual / fused Jacobi epilogue (RowEpi semantics)
   // MODE 2: extra Jacobi sweep: d_new = d + dinv*(r - acc), optional x update
@@ -366,6 +367,7 @@ template <int BR, int BC, bool ZERO, bool SPLIT, int MODE>
 __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __restrict__ xu,
                                                    const double* __restrict__ xl, int64_t split_blocks,
                                                    SellEpi e) {
+  CAMG_PDL_ENTRY();
   constexpr int BE = BR * BC;
   const int lane = threadIdx.x & 31;
   const int half = lane & 1;
@@ -444,11 +446,11 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   note_launch();
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
-    if (S->masked) k_sell_row<BR, BC, Z, SP, M, true><<<grid, 256, 0, st>>>(v, xu, xl, sb, e);         \
+    if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \
     else if (S->nslices < kSellPairSlices)                                                   \
-      k_sell_row2<BR, BC, Z, SP, M><<<grid_for(S->nslices * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st>>>( \
-          v, xu, xl, sb, e);                                                                 \
-    else k_sell_row<BR, BC, Z, SP, M, false><<<grid, 256, 0, st>>>(v, xu, xl, sb, e);                  \
+      launch_k(k_sell_row2<BR, BC, Z, SP, M>, grid_for(S->nslices * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
+               v, xu, xl, sb, e);                                                            \
+    else launch_k(k_sell_row<BR, BC, Z, SP, M, false>, grid, 256, 0, st, v, xu, xl, sb, e);                  \
   } while (0)
   if (mode == 0) {
     if (sp) CAMG_SELL_LAUNCH(false, true, 0); else CAMG_SELL_LAUNCH(false, false, 0);
@@ -497,6 +499,7 @@ __global__ void __launch_bounds__(256) k_sell_gs(SellView S, const int32_t* __re
                                                  const double* __restrict__ xl, int64_t split_blocks,
                                                  const double* __restrict__ b, const double* __restrict__ dinv,
                                                  double* y) {
+  CAMG_PDL_ENTRY();
   constexpr int BE = BR * BR;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -558,11 +561,11 @@ static void launch_gs(const Sell* S, int64_t s0, int64_t s1, bool fwd, bool zero
   const int64_t sb = split / BR;
   note_launch();
   if (zero) {
-    if (fwd) k_sell_gs<BR, true, true><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
-    else k_sell_gs<BR, false, true><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+    if (fwd) launch_k(k_sell_gs<BR, true, true>, grid, 256, 0, st, v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+    else launch_k(k_sell_gs<BR, false, true>, grid, 256, 0, st, v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
   } else {
-    if (fwd) k_sell_gs<BR, true, false><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
-    else k_sell_gs<BR, false, false><<<grid, 256, 0, st>>>(v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+    if (fwd) launch_k(k_sell_gs<BR, true, false>, grid, 256, 0, st, v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
+    else launch_k(k_sell_gs<BR, false, false>, grid, 256, 0, st, v, S->perm, S->dblk, s0, s1, xl, sb, b, dinv, y);
   }
   CAMG_LAUNCH_CHECK();
 }

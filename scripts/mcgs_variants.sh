@@ -2,5 +2,5 @@
 run() { python bench.py --steps 10 --no-solve --no-cpu-baseline 2>&1 | tail -1 | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); print('$1', round(d['ms_per_step'],3))"; }
 run default
+CAMG_PDL=0 run no-pdl
 CAMG_MCGS_CTA=0 run no-cta
-CAMG_BENCH_SMOOTHER="simple,0.8,3,jacobi,1,0.6,jacobi,1,1.0" run jacobi-corrector
