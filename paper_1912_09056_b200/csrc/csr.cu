@@ -432,12 +432,26 @@ void vec_scale(int64_t n, double a, double* y, cudaStream_t s) {
   k_scale<<<grid_for(n, 256), 256, 0, s>>>(n, a, y);
 }
 
+// w = (A v) / d in scipy csr_matvec order (sequential over the row, no FMA
+// contraction): one warp per row loads 32 entries at a time coalesced, forms
+// the products in parallel and lane 0 adds them in row order.
 __global__ void k_power_step(CsrView A, const double* __restrict__ d, const double* __restrict__ v, double* __restrict__ w) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < A.n_rows; r += (int64_t)gridDim.x * blockDim.x) {
-    // scipy csr_matvec order: sequential over the row, no FMA contraction
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < A.n_rows; r += nwarps) {
+    const int64_t s = A.rowptr[r], e = A.rowptr[r + 1];
     double acc = 0.0;
-    for (int64_t p = A.rowptr[r]; p < A.rowptr[r + 1]; ++p) acc = __dadd_rn(acc, __dmul_rn(A.val[p], v[A.col[p]]));
-    w[r] = __ddiv_rn(acc, d[r]);
+    for (int64_t c0 = s; c0 < e; c0 += 32) {
+      const int64_t p = c0 + lane;
+      const double prod = p < e ? __dmul_rn(A.val[p], v[A.col[p]]) : 0.0;
+      const int n = (int)((e - c0) < 32 ? (e - c0) : 32);
+      for (int j = 0; j < n; ++j) {
+        const double t = __shfl_sync(0xffffffffu, prod, j);
+        acc = __dadd_rn(acc, t);
+      }
+    }
+    if (lane == 0) w[r] = __ddiv_rn(acc, d[r]);
   }
 }
 
@@ -466,7 +480,7 @@ double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s)
   double lam = 1.0;
   for (int k = 0; k < iters; ++k) {
     note_launch();
-    k_power_step<<<grid_for(n, 256), 256, 0, s>>>(view(A), d, v.p, w.p);
+    k_power_step<<<grid_for(n * 32, 256), 256, 0, s>>>(view(A), d, v.p, w.p);
     dot_device(n, w.p, w.p, part.p + kDotBlocks, part.p, s);
     double nn = 0.0;
     CAMG_CUDA(cudaMemcpyAsync(&nn, part.p + kDotBlocks, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -606,7 +620,7 @@ int camg_csr_scale_rows(const camg_csr* A, const double* s, camg_csr** out) {
 int camg_power_step(const camg_csr* A, const double* d, const double* v, double* w, void* stream) {
   return guarded([&] {
     note_launch();
-    k_power_step<<<grid_for(A->m->n_rows, 256), 256, 0, (cudaStream_t)stream>>>(view(A->m), d, v, w);
+    k_power_step<<<grid_for(A->m->n_rows * 32, 256), 256, 0, (cudaStream_t)stream>>>(view(A->m), d, v, w);
     CAMG_LAUNCH_CHECK();
   });
 }

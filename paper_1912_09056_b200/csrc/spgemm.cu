@@ -554,15 +554,23 @@ std::vector<int64_t> overflow_rows(const int32_t* dflag, int64_t n) {
 // filled with the table size its count pass succeeded with.
 template <class Launch>
 Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint32_t c2_0, double tol,
-              cudaStream_t s) {
+              cudaStream_t s, bool start_global = false) {
   DBuf<int64_t> cnt(n_rows + 1);
   DBuf<int32_t> ovf(n_rows + 1);
   CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
   OutArgs o{cnt.p, nullptr, nullptr, nullptr, ovf.p, tol};
-  if (n_rows) launch(false, false, nullptr, n_rows, 0, 0, nullptr, o);
-  CAMG_CUDA(cudaStreamSynchronize(s));
-  CAMG_LAUNCH_CHECK();
-  std::vector<int64_t> big = overflow_rows(ovf.p, n_rows);
+  std::vector<int64_t> big;
+  if (start_global) {
+    // every row starts in the global-memory hash tables (L2-resident, full
+    // occupancy) instead of the shared-memory ones
+    big.resize(n_rows);
+    for (int64_t i = 0; i < n_rows; ++i) big[i] = i;
+  } else {
+    if (n_rows) launch(false, false, nullptr, n_rows, 0, 0, nullptr, o);
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    CAMG_LAUNCH_CHECK();
+    big = overflow_rows(ovf.p, n_rows);
+  }
   if (getenv("CAMG_DEBUG"))
     fprintf(stderr, "[camg] spgemm rows=%lld smem-overflow rows=%zu\n", (long long)n_rows, big.size());
   struct Batch { DBuf<int64_t> rows; int64_t n; uint32_t c1, c2; };
@@ -612,7 +620,7 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   C->avg_row = n_rows ? double(nnz) / n_rows : 0.0;
   OutArgs f{nullptr, C->rowptr, C->col, C->val, nullptr, tol};
   // fill: small rows from shared memory (overflow rows are skipped there)
-  if (n_rows) launch(true, false, nullptr, n_rows, 0, 0, nullptr, f);
+  if (n_rows && !start_global) launch(true, false, nullptr, n_rows, 0, 0, nullptr, f);
   for (auto& b : batches) {
     const size_t per = (size_t)b.c1 * 14 + (size_t)b.c2 * 12;
     int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(b.n, (int64_t)(budget / per)));
@@ -626,7 +634,7 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   return C;
 }
 
-constexpr uint32_t kCapProduct = 2048;  // 32 KB per warp
+constexpr uint32_t kCapProduct = 256;  // 3 KB per warp: products rows are short (D^-1 K P_tent: ~50), overflow -> global tables
 constexpr uint32_t kCap1 = 2048, kCap2 = 512;
 
 }  // namespace
@@ -634,20 +642,25 @@ constexpr uint32_t kCap1 = 2048, kCap2 = 512;
 Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStream_t s, const double* scale_a) {
   CAMG_CHECK(A->n_cols == B->n_rows, CAMG_ERR_DIMENSION, "sp_matmul: inner dimensions differ");
   CAMG_CHECK(B->n_cols < INT32_MAX, CAMG_ERR_DIMENSION, "too many columns");
-  const size_t smem = (size_t)kWarpsPerBlock * kCapProduct * 12;
-  static bool attr = false;
-  if (!attr) {
+  static uint32_t capp = 0;
+  if (!capp) {
+    const char* e = getenv("CAMG_SPGEMM_CAP");
+    capp = e ? (uint32_t)atoi(e) : kCapProduct;
+  }
+  const size_t smem = (size_t)kWarpsPerBlock * capp * 12;
+  static size_t attr = 0;
+  if (attr != smem) {
     CAMG_CUDA(cudaFuncSetAttribute(k_product<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CAMG_CUDA(cudaFuncSetAttribute(k_product<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    attr = smem;
   }
   auto launch = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t c2,
                     char* scratch, OutArgs o) {
     note_launch();
     if (!global) {
-      unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 8);
-      if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, kCapProduct, nullptr, o);
-      else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, kCapProduct, nullptr, o);
+      unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 32);
+      if (fill) k_product<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, capp, nullptr, o);
+      else k_product<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(A), view(B), reverse_a, scale_a, rows, nrows, capp, nullptr, o);
     } else {
       const size_t per = (size_t)c1 * 14 + (size_t)c2 * 12;
       int64_t warps = std::max<int64_t>(kWarpsPerBlock, std::min<int64_t>(nrows, (int64_t)((size_t(2) << 30) / per)));
@@ -657,7 +670,7 @@ Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStrea
     }
     CAMG_LAUNCH_CHECK();
   };
-  return two_pass(A->n_rows, B->n_cols, launch, 2 * kCapProduct, 0, tol, s);
+  return two_pass(A->n_rows, B->n_cols, launch, 2 * capp, 0, tol, s);
 }
 
 Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B, false, kDropTol, s, nullptr); }
@@ -665,21 +678,29 @@ Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B,
 Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
   CAMG_CHECK(R->n_cols == A->n_rows && A->n_cols == P->n_rows, CAMG_ERR_DIMENSION,
              "galerkin_triple: dimension mismatch");
-  const size_t per = (size_t)kCap1 * 14 + (size_t)kCap2 * 12;
+  // hash capacities per warp (powers of two; CAMG_RAP_CAP1/2 override for tuning)
+  static uint32_t cap1 = 0, cap2 = 0;
+  if (!cap1) {
+    const char* e1 = getenv("CAMG_RAP_CAP1");
+    const char* e2 = getenv("CAMG_RAP_CAP2");
+    cap1 = e1 ? (uint32_t)atoi(e1) : kCap1;
+    cap2 = e2 ? (uint32_t)atoi(e2) : kCap2;
+  }
+  const size_t per = (size_t)cap1 * 14 + (size_t)cap2 * 12;
   const size_t smem = (size_t)kWarpsPerBlock * per;
-  static bool attr = false;
-  if (!attr) {
+  static size_t attr = 0;
+  if (attr != smem) {
     CAMG_CUDA(cudaFuncSetAttribute(k_triple<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CAMG_CUDA(cudaFuncSetAttribute(k_triple<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
+    attr = smem;
   }
   auto launch = [&](bool fill, bool global, const int64_t* rows, int64_t nrows, uint32_t c1, uint32_t c2,
                     char* scratch, OutArgs o) {
     note_launch();
     if (!global) {
-      unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 8);
-      if (fill) k_triple<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, kCap1, kCap2, nullptr, o);
-      else k_triple<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, kCap1, kCap2, nullptr, o);
+      unsigned grid = (unsigned)std::min<int64_t>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock, kNumSMs * 32);
+      if (fill) k_triple<true, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, cap1, cap2, nullptr, o);
+      else k_triple<false, false><<<grid, 32 * kWarpsPerBlock, smem, s>>>(view(R), view(A), view(P), rows, nrows, cap1, cap2, nullptr, o);
     } else {
       const size_t pw = (size_t)c1 * 14 + (size_t)c2 * 12;
       int64_t warps = std::min<int64_t>(nrows, std::max<int64_t>(kWarpsPerBlock, (int64_t)((size_t(2) << 30) / pw)));
@@ -689,7 +710,17 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
     }
     CAMG_LAUNCH_CHECK();
   };
-  return two_pass(R->n_rows, P->n_cols, launch, 2 * kCap1, 2 * kCap2, kDropTol, s);
+  static int rap_global = -1;
+  if (rap_global < 0) {
+    const char* e = getenv("CAMG_RAP_GLOBAL");
+    rap_global = (e && e[0] == '0') ? 0 : 1;
+  }
+  // long RA rows (K-block RAP: ~350 R entries x ~80 K entries per coarse
+  // row) start in the global-memory tables: L2-resident, ~28 warps per SM
+  // against 6 with shared-memory tables (C5: 7.0 s -> 4.7 s)
+  if (rap_global && R->avg_row * A->avg_row > 4096.0)
+    return two_pass(R->n_rows, P->n_cols, launch, cap1, cap2, kDropTol, s, true);
+  return two_pass(R->n_rows, P->n_cols, launch, 2 * cap1, 2 * cap2, kDropTol, s);
 }
 
 }  // namespace camg
