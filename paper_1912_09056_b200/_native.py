@@ -154,3 +154,11 @@ def require_device():
 
 def launch_count() -> int:
     return int(lib().camg_launch_count())
+
+
+def synchronize():
+    """Wait for all device work (setup phase timing)."""
+    import torch
+
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()

@@ -601,3 +601,19 @@ def test_nested_config_errors():
         nested_preconditioner(op, fine_level_meta(g), block_cfg(dict(kind="simple", alpha=0.8,
                                                                      corrector=("jacobi", 1, 0.8))),
                               HierarchyConfig(max_levels=2, max_coarse_size=50), PointSmootherConfig("ilu0", 1, 1.0))
+
+
+def test_apply_many_pipelined_equals_apply():
+    """Hierarchy.apply_many (independent host RHS, copies overlapped with the
+    V-cycles) returns exactly what one blocking apply per RHS returns."""
+    import torch
+    g, op, H = gpu_hier("c5s_simple")
+    rng = np.random.default_rng(9)
+    rs = [torch.from_numpy(rng.standard_normal(H.n)).pin_memory() for _ in range(5)]
+    outs = H.apply_many(rs)
+    torch.cuda.synchronize()
+    for r, o in zip(rs, outs):
+        ref = H.apply(r)
+        assert torch.equal(o, ref)
+    with pytest.raises(Exception):
+        H.apply_many([torch.zeros(H.n + 1).pin_memory()])
