@@ -459,12 +459,14 @@ def run_gpu(args):
 
     levels = [{"n_u": l.op.n_u, "n_lam": l.op.n_lam, "nnz_K": l.op.K.nnz, "nnz_total": l.op.nnz}
               for l in H.levels]
+    free_b, total_b = torch.cuda.mem_get_info()
     line = {
         "metric": metric_name(args.config),
         "value": value, "unit": "V-cycles/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": vc_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config geometry/materials)",
-        "config": dict(workload_config(args), levels=levels, operator_complexity=H.complexity),
+        "config": dict(workload_config(args), levels=levels, operator_complexity=H.complexity,
+                       device_memory_used_gb=round((total_b - free_b) / 1e9, 1)),
         "roofline": {"bound": "hbm", "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
                      "frac": dom_gbs / peak, "traffic": None if gs else TRAFFIC.get(args.config),
                      "kernel": ("k_sell_gs<3>: one fine-level multicolour block-SGS predictor sweep (forward + backward "

@@ -363,19 +363,19 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
 // quantisation with one warp per slice; this variant gives each block row to
 // a lane pair (even lane: first half of its slots, odd lane: second half,
 // deterministic pair reduction), i.e. two work units per slice.
-template <int BR, int BC, bool ZERO, bool SPLIT, int MODE>
+template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, int LPR>
 __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __restrict__ xu,
                                                    const double* __restrict__ xl, int64_t split_blocks,
                                                    SellEpi e) {
   CAMG_PDL_ENTRY();
   constexpr int BE = BR * BC;
   const int lane = threadIdx.x & 31;
-  const int half = lane & 1;
+  const int part = lane & (LPR - 1);
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t hs = warp; hs < 2 * S.nslices; hs += nwarps) {
-    const int64_t s = hs >> 1;
-    const int pl = (int)(hs & 1) * 16 + (lane >> 1);
+  for (int64_t hs = warp; hs < LPR * S.nslices; hs += nwarps) {
+    const int64_t s = hs / LPR;
+    const int pl = (int)(hs % LPR) * (32 / LPR) + lane / LPR;
     const int64_t p = s * 32 + pl;
     const bool active = p < S.nbr;
     double acc[BR];
@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __r
     for (int r = 0; r < BR; ++r) acc[r] = 0.0;
     if (!ZERO) {
       const int n = active ? S.len[p] : 0;
-      const int k0 = half ? (n + 1) / 2 : 0, k1 = half ? n : (n + 1) / 2;
+      const int chunk = (n + LPR - 1) / LPR;
+      const int k0 = min(n, part * chunk), k1 = min(n, k0 + chunk);
       const int64_t base = S.slice_ptr[s];
       for (int k = k0; k < k1; ++k) {
         const int64_t slot = base + k;
@@ -400,8 +401,10 @@ __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __r
       }
     }
 #pragma unroll
-    for (int r = 0; r < BR; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 1);
-    if (!active || half) continue;
+    for (int o = 1; o < LPR; o <<= 1)
+#pragma unroll
+      for (int r = 0; r < BR; ++r) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    if (!active || part) continue;
 #pragma unroll
     for (int r = 0; r < BR; ++r) {
       const int64_t i = p * BR + r;
@@ -436,6 +439,16 @@ __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __r
   }
 }
 
+// below this many slices four lanes share a block row (CAMG_SELL_QUAD sets it)
+static int64_t quad_slices() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAMG_SELL_QUAD");
+    v = e ? atoll(e) : kSellQuadSlices;
+  }
+  return v;
+}
+
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st) {
@@ -447,8 +460,11 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
     if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \
+    else if (S->nslices < quad_slices())                                                     \
+      launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(S->nslices * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
+               v, xu, xl, sb, e);                                                            \
     else if (S->nslices < kSellPairSlices)                                                   \
-      launch_k(k_sell_row2<BR, BC, Z, SP, M>, grid_for(S->nslices * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
+      launch_k(k_sell_row2<BR, BC, Z, SP, M, 2>, grid_for(S->nslices * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
     else launch_k(k_sell_row<BR, BC, Z, SP, M, false>, grid, 256, 0, st, v, xu, xl, sb, e);                  \
   } while (0)
