@@ -158,3 +158,25 @@ def test_oracle_mcgs_block_equals_permuted_ssor():
     ref = np.empty_like(x)
     ref[perm] = S.smooth(x[perm], b[perm])
     np.testing.assert_array_equal(P.smooth(x, b), ref)
+
+
+def test_parallel_pivoted_qr_bit_identical():
+    """The process-parallel batched QR of the tentative prolongator equals
+    scipy's batched (= per-aggregate) pivoted QR bit for bit."""
+    from multiprocessing import shared_memory
+    import scipy.linalg
+    from paper_1912_09056_b200 import transfer as T
+    rng = np.random.default_rng(4)
+    vecs = rng.standard_normal((30000, 6))
+    dofs = rng.integers(0, 30000, size=(25000, 12))
+    G, M = dofs.shape
+    Qr, Rr, Pr = scipy.linalg.qr(vecs[dofs], mode="economic", pivoting=True)
+    shm = shared_memory.SharedMemory(create=True, size=8 * (G * M * 6 + 16))
+    try:
+        q = np.ndarray((G, M, 6), dtype=np.float64, buffer=shm.buf, offset=8 * 16)
+        R, P = T._pivoted_qr_into(vecs, dofs, q, shm, 8 * 16, 4)
+        assert np.array_equal(q, Qr) and np.array_equal(R, Rr) and np.array_equal(P, Pr)
+        del q
+    finally:
+        shm.close()
+        shm.unlink()
