@@ -1,4 +1,4 @@
 # C5 setup phases (setup_breakdown)
-run() { CAMG_DEBUG=1 python scripts/setup_breakdown.py 1 > gpurun_out/setup_$1.log 2>&1
-  echo "$1 $(grep -o "{'generate.*" gpurun_out/setup_$1.log)"; }
-run default
+run() { python scripts/setup_breakdown.py 1 > gpurun_out/setup_$1.log 2>&1
+  echo "$1 $(grep -o "'rap_K': [0-9.]*" gpurun_out/setup_$1.log)"; }
+run lb64_16

@@ -168,7 +168,7 @@ def test_parallel_pivoted_qr_bit_identical():
     from paper_1912_09056_b200 import transfer as T
     rng = np.random.default_rng(4)
     vecs = rng.standard_normal((30000, 6))
-    dofs = rng.integers(0, 30000, size=(25000, 12))
+    dofs = rng.integers(0, 30000, size=(25000, 16))
     G, M = dofs.shape
     Qr, Rr, Pr = scipy.linalg.qr(vecs[dofs], mode="economic", pivoting=True)
     shm = shared_memory.SharedMemory(create=True, size=8 * (G * M * 6 + 16))
