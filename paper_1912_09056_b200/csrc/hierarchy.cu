@@ -549,15 +549,20 @@ struct LaunchCorr {
 };
 
 
+static SellEpi sell_epi(const RowEpi& e) {
+  SellEpi se;
+  se.b = e.b; se.x = e.x; se.out_r = e.out_r; se.dscale = e.dscale; se.out_d = e.out_d;
+  se.out_x = e.out_x; se.coef = e.coef; se.x0 = e.x0; se.xmode = e.xmode; se.out_y = e.out_y;
+  se.dprev = e.dprev; se.c1 = e.c1; se.c2 = e.c2;
+  return se;
+}
+
 // residual over rows [row0, row0+nrows): SELL mirror for the rows it covers,
 // CSR for the rest
 static void resid_rows(const Csr* A, int64_t row0, int64_t nrows, const double* xu, const double* xl,
                        int64_t split, const RowEpi& e, bool zero, cudaStream_t s) {
   if (A->sell && row0 == 0 && nrows >= A->sell->rows()) {
-    SellEpi se;
-    se.b = e.b; se.x = e.x; se.out_r = e.out_r; se.dscale = e.dscale; se.out_d = e.out_d;
-    se.out_x = e.out_x; se.coef = e.coef; se.x0 = e.x0; se.xmode = e.xmode; se.out_y = e.out_y;
-    se.dprev = e.dprev; se.c1 = e.c1; se.c2 = e.c2;
+    const SellEpi se = sell_epi(e);
     sell_launch(A->sell, 1, zero, xu, xl, split < A->n_cols ? split : -1, se, s);
     const int64_t done = A->sell->rows();
     row0 += done;
@@ -754,6 +759,18 @@ struct Level {
   // external predictor solver (nested preconditioner: scalar AMG V-cycle on
   // K, hierarchy.py:364-371 via smoothers.py:277-278); borrowed
   ScalarHier* inner = nullptr;
+  // Overlap of a step's lambda side (latency-bound: B2/Cz rows, the S~
+  // corrector, lambda update, interface-row B1 correction) with the next
+  // bandwidth-bound [K | B1] pass: that chain runs on `side`, and the next
+  // pass first streams the SELL slices whose rows read no interface row and
+  // no multiplier (sl_indep), then waits for the chain and streams the rest
+  // (sl_dep).  Same arithmetic per row, so results are bit-identical.
+  bool overlap = false;
+  bool pending = false;  // a lambda-side chain runs on `side`
+  DBuf<int32_t> sl_indep, sl_dep;
+  int64_t n_indep = 0, n_dep = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // Chebyshev predictor: d_k = c1[k] d_{k-1} + c2[k] D^-1 r_k, y_{k+1} = y_k + d_k
   double cheb_lmax = 0.0;
   std::vector<double> cheb_c1, cheb_c2;
@@ -768,7 +785,34 @@ struct Level {
   int64_t nnz_top = 0;  // entries of the [K | B1] rows
   // work vectors
   DBuf<double> w_du, w_du2, w_ru, w_rc, w_dl, w_dl2, w_rl, w_tmp;
-  ~Level() { if (owns_A) delete A; delete B1; delete S; delete P; delete R; }
+  ~Level() {
+    if (owns_A) delete A;
+    delete B1; delete S; delete P; delete R;
+    if (side) cudaStreamDestroy(side);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+  }
+
+  // order stream s after the pending lambda-side chain
+  void join(cudaStream_t s) {
+    if (!pending) return;
+    CAMG_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+    pending = false;
+  }
+
+  // fused pass over the [K | B1] rows reading x = [xu; xl]: with a pending
+  // lambda-side chain, the independent slices go first
+  void top_pass(const RowEpi& e, const double* xu, const double* xl, bool zero, cudaStream_t s) {
+    if (!pending || !overlap) {
+      join(s);
+      resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+      return;
+    }
+    const SellEpi se = sell_epi(e);
+    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, sl_indep.p, n_indep);
+    join(s);
+    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, sl_dep.p, n_dep);
+  }
 
   void alloc_work() {
     w_du = DBuf<double>(n);
@@ -837,8 +881,9 @@ struct Level {
     if (kind == CAMG_BRAESS_SARAZIN) {
       // u_half = u + (A^-1 r_u) / alpha   (smoothers.py:296)
       RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
-      resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
+      top_pass(e, xu, xl, zero, s);
     } else if (inner) {
+      join(s);
       // du = inner.apply(r_u), r_u = b_u - K u - B1 lam (smoothers.py:285-314
       // with predictor_solver); SIMPLE: u_half = u + du; Uzawa: u + alpha du
       RowEpi e{b, x, w_ru.p, nullptr, nullptr, nullptr, 0.0};
@@ -853,6 +898,7 @@ struct Level {
       }
     } else if (cfg.pred_kind == CAMG_PT_MCGS) {
       // Uzawa keeps y for the lambda side and relaxes u_new = u + alpha (y - u)
+      join(s);
       double* y = (kind == CAMG_UZAWA) ? w_du.p : xo;
       gs_predict(x, b, y, sp, s);
       if (kind == CAMG_UZAWA) {
@@ -893,22 +939,34 @@ struct Level {
         } else {
           e.out_x = xo;
         }
-        resid_rows(A, int64_t(0), nu, y, xl, nu, e, y == nullptr, s);
+        if (k == 0) top_pass(e, y, xl, y == nullptr, s);
+        else resid_rows(A, int64_t(0), nu, y, xl, nu, e, false, s);
         y = dst;
       }
     }
     if (nl == 0) return;
+    join(s);
+    cudaStream_t ls = s;
+    if (overlap) {  // fork the lambda side onto `side`
+      CAMG_CUDA(cudaEventRecord(ev_fork, s));
+      CAMG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
+      ls = side;
+    }
     // lambda side: rc = B2 u_half - Cz lam - b_lam = -(b_lam + Cz lam - B2 u_half)
-    dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, s);
-    double* dl = corrector(w_rc.p, s);
+    dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, ls);
+    double* dl = corrector(w_rc.p, ls);
     const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
     note_launch();
-    launch_k(k_lam_update, grid_for(nl, 256), 256, 0, s, nl, xl, dl, cl, xo + nu);
+    launch_k(k_lam_update, grid_for(nl, 256), 256, 0, ls, nl, xl, dl, cl, xo + nu);
     if (kind != CAMG_UZAWA && n_b1_rows) {
       // u_new = u_half - c A^-1 B1 dlam on the interface rows
       const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
       note_launch();
-      launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, s, view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
+      launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, ls, view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
+    }
+    if (overlap) {
+      CAMG_CUDA(cudaEventRecord(ev_join, side));
+      pending = true;
     }
   }
 
@@ -923,9 +981,20 @@ struct Level {
     }
   }
 
-  // r = b - A x over all rows
+  // r = b - A x over all rows (independent slices first while a lambda-side
+  // chain is pending)
   void residual(const double* x, const double* b, double* r, cudaStream_t s) {
     RowEpi e{b, nullptr, r, nullptr, nullptr, nullptr, 0.0};
+    if (pending && overlap && x) {
+      const SellEpi se = sell_epi(e);
+      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, sl_indep.p, n_indep);
+      join(s);
+      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, sl_dep.p, n_dep);
+      const int64_t done = A->sell->rows();
+      if (n > done) dispatch_g<LaunchResid>(A->avg_row, A, done, n - done, x, (const double*)nullptr, n, e, false, s);
+      return;
+    }
+    join(s);
     resid_rows(A, int64_t(0), n, x, (const double*)nullptr, n, e, x == nullptr, s);
   }
 };
@@ -976,6 +1045,66 @@ static void setup_chebyshev(Level* L, const Csr* K, const double* dK, int degree
     L->w_cd[0] = DBuf<double>(L->nu + 1);
     L->w_cd[1] = DBuf<double>(L->nu + 1);
   }
+}
+
+// rows r < nu with a multiplier column (B1 part of the merged rows)
+__global__ void k_iface_rows(CsrView A, int64_t nu, int8_t* __restrict__ iface) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nu; r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = A.rowptr[r], e = A.rowptr[r + 1];
+    iface[r] = (e > b && A.col[e - 1] >= nu) ? 1 : 0;
+  }
+}
+
+// rows that read an interface row or a multiplier
+__global__ void k_dep_rows(CsrView A, int64_t nu, const int8_t* __restrict__ iface, int8_t* __restrict__ dep) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nu; r += (int64_t)gridDim.x * blockDim.x) {
+    int8_t d = iface[r];
+    for (int64_t p = A.rowptr[r]; p < A.rowptr[r + 1] && !d; ++p) {
+      const int32_t c = A.col[p];
+      if (c < nu && iface[c]) d = 1;
+    }
+    dep[r] = d;
+  }
+}
+
+__global__ void k_dep_slices(const int8_t* __restrict__ dep, int64_t nu, int64_t rows_per_slice, int64_t nslices,
+                             int8_t* __restrict__ ds) {
+  for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nslices; sl += (int64_t)gridDim.x * blockDim.x) {
+    int8_t d = 0;
+    const int64_t r1 = min(nu, (sl + 1) * rows_per_slice);
+    for (int64_t r = sl * rows_per_slice; r < r1 && !d; ++r) d = dep[r];
+    ds[sl] = d;
+  }
+}
+
+static void setup_overlap(Level* L) {
+  const Sell* S = L->A->sell;
+  const char* env = getenv("CAMG_OVERLAP");
+  if ((env && env[0] == '0') || !S || L->nl == 0 || S->rows() != L->nu || L->cfg.kind == CAMG_UZAWA) return;
+  const int64_t nu = L->nu;
+  DBuf<int8_t> iface(nu + 1), dep(nu + 1), ds(S->nslices + 1);
+  note_launch(3);
+  k_iface_rows<<<grid_for(nu, 256), 256>>>(view(L->A), nu, iface.p);
+  k_dep_rows<<<grid_for(nu, 256), 256>>>(view(L->A), nu, iface.p, dep.p);
+  k_dep_slices<<<grid_for(S->nslices, 256), 256>>>(dep.p, nu, 32 * (int64_t)S->br, S->nslices, ds.p);
+  CAMG_LAUNCH_CHECK();
+  std::vector<int8_t> h(S->nslices);
+  CAMG_CUDA(cudaMemcpy(h.data(), ds.p, S->nslices, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> ind, dp;
+  for (int64_t i = 0; i < S->nslices; ++i) (h[i] ? dp : ind).push_back((int32_t)i);
+  L->n_indep = (int64_t)ind.size();
+  L->n_dep = (int64_t)dp.size();
+  L->sl_indep = DBuf<int32_t>(ind.size() + 1);
+  L->sl_dep = DBuf<int32_t>(dp.size() + 1);
+  if (!ind.empty()) CAMG_CUDA(cudaMemcpy(L->sl_indep.p, ind.data(), sizeof(int32_t) * ind.size(), cudaMemcpyHostToDevice));
+  if (!dp.empty()) CAMG_CUDA(cudaMemcpy(L->sl_dep.p, dp.data(), sizeof(int32_t) * dp.size(), cudaMemcpyHostToDevice));
+  CAMG_CUDA(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
+  CAMG_CUDA(cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming));
+  CAMG_CUDA(cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming));
+  L->overlap = true;
+  if (getenv("CAMG_DEBUG"))
+    fprintf(stderr, "[camg] overlap: %lld independent / %lld dependent slices\n", (long long)L->n_indep,
+            (long long)L->n_dep);
 }
 
 Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, const camg_smoother_cfg& cfg, int pre,
@@ -1075,6 +1204,7 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     L->n_b1_rows = read_i64(nsel.p);
     L->b1_rows = std::move(out);
   }
+  setup_overlap(L.get());
   L->alloc_work();
   CAMG_CUDA(cudaDeviceSynchronize());
   return L.release();
@@ -1146,6 +1276,7 @@ struct Hierarchy {
       launch_k(k_lu_solve, 1, 1024, sh, s, (int)n_coarse, lu.p, piv.p, b, x);
     } else {
       L->sweep(nullptr, b, x, s);
+      L->join(s);
     }
   }
 
@@ -1183,6 +1314,7 @@ struct Hierarchy {
       L->sweep(xs, b, dst, s);
       xs = dst;
     }
+    L->join(s);
     return const_cast<double*>(xs);
   }
 
@@ -1504,6 +1636,7 @@ int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double*
 int camg_level_sweep(camg_level* L, const double* x, const double* b, double* out, void* stream) {
   return guarded([&] {
     L->L->sweep(x, b, out, (cudaStream_t)stream);
+    L->L->join((cudaStream_t)stream);
     CAMG_LAUNCH_CHECK();
   });
 }

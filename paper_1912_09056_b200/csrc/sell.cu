@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s = warp; s < S.nslices; s += nwarps) {
+  for (int64_t w = warp; w < S.nwork; w += nwarps) {
+    const int64_t s = S.slist ? (int64_t)S.slist[w] : w;
     const int64_t p = s * 32 + lane;
     const bool active = p < S.nbr;
     double acc[BR];
@@ -373,8 +374,8 @@ __global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __r
   const int part = lane & (LPR - 1);
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t hs = warp; hs < LPR * S.nslices; hs += nwarps) {
-    const int64_t s = hs / LPR;
+  for (int64_t hs = warp; hs < LPR * S.nwork; hs += nwarps) {
+    const int64_t s = S.slist ? (int64_t)S.slist[hs / LPR] : hs / LPR;
     const int pl = (int)(hs % LPR) * (32 / LPR) + lane / LPR;
     const int64_t p = s * 32 + pl;
     const bool active = p < S.nbr;
@@ -451,20 +452,24 @@ static int64_t quad_slices() {
 
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                       const SellEpi& e, cudaStream_t st) {
+                       const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
   SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->nbr, S->nslices};
-  const unsigned grid = grid_for(S->nslices * 32, 256, int64_t(kNumSMs) * 16);
+  v.slist = slist;
+  v.nwork = slist ? nlist : S->nslices;
+  if (v.nwork <= 0) return;
+  const int64_t nw = v.nwork;
+  const unsigned grid = grid_for(nw * 32, 256, int64_t(kNumSMs) * 16);
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
   note_launch();
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
     if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \
-    else if (S->nslices < quad_slices())                                                     \
-      launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(S->nslices * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
+    else if (nw < quad_slices())                                                             \
+      launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(nw * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
-    else if (S->nslices < kSellPairSlices)                                                   \
-      launch_k(k_sell_row2<BR, BC, Z, SP, M, 2>, grid_for(S->nslices * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
+    else if (nw < kSellPairSlices)                                                           \
+      launch_k(k_sell_row2<BR, BC, Z, SP, M, 2>, grid_for(nw * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
     else launch_k(k_sell_row<BR, BC, Z, SP, M, false>, grid, 256, 0, st, v, xu, xl, sb, e);                  \
   } while (0)
@@ -488,9 +493,9 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
 }
 
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                 const SellEpi& e, cudaStream_t st) {
+                 const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
 #define CAMG_SELL_CASE(R_, C_) \
-  if (S->br == R_ && S->bc == C_) return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st);
+  if (S->br == R_ && S->bc == C_) return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st, slist, nlist);
   CAMG_SELL_CASE(2, 2) CAMG_SELL_CASE(3, 3) CAMG_SELL_CASE(6, 6)
   CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
 #undef CAMG_SELL_CASE

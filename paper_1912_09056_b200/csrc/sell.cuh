@@ -31,6 +31,8 @@ struct SellView {
   const unsigned long long* __restrict__ mask;
   const int64_t* __restrict__ voff;
   int64_t nbr, nslices;
+  const int32_t* __restrict__ slist = nullptr;  // optional subset of slices to process
+  int64_t nwork = 0;                            // slices to process (slist length, or nslices)
 };
 
 // epilogue arguments of the three SELL row kernels (modes 0/1/2)
@@ -59,7 +61,7 @@ Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_bloc
 // (modes 1/2 need square blocks).  split < 0: x is one vector (xu); else
 // columns >= split read xl (null = 0).
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                 const SellEpi& e, cudaStream_t st);
+                 const SellEpi& e, cudaStream_t st, const int32_t* slist = nullptr, int64_t nlist = -1);
 double sell_pass_bytes(const Sell* S);
 // colour-ordered SELL (square bs x bs blocks, full): position t of the
 // mirror holds block row order[t] (-1 = padding), order.size() % 32 == 0
