@@ -712,7 +712,12 @@ struct McgsK {
            cudaStream_t s) {
     const int nc = colors();
     if (cta && Arows->n_cols == nu) {
-      dispatch_g<LaunchMcgsCta>(Arows->avg_row, Arows, nodes.p, col_ptr_dev.p, nc, bs, sweeps, zero, dblk.p, b, dinv, y,
+      static double cta_avg = -1.0;  // CAMG_MCGS_CTA_G forces the lanes per row (tuning)
+      if (cta_avg < 0.0) {
+        const char* e = getenv("CAMG_MCGS_CTA_G");
+        cta_avg = e ? atof(e) : 0.0;
+      }
+      dispatch_g<LaunchMcgsCta>(cta_avg > 0.0 ? cta_avg : Arows->avg_row, Arows, nodes.p, col_ptr_dev.p, nc, bs, sweeps, zero, dblk.p, b, dinv, y,
                                 s);
       return;
     }
