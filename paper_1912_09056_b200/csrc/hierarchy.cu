@@ -465,6 +465,60 @@ __global__ void __launch_bounds__(1024) k_lu_solve(int n, const double* __restri
     for (int i = threadIdx.x; i < n; i += blockDim.x) xg[i] = x[i];
 }
 
+// Same solve with the factors staged in shared memory (n^2 + 2n doubles fit):
+// every substitution step reads shared memory instead of L2, one barrier per
+// step.  Identical operations to k_lu_solve.
+__global__ void __launch_bounds__(1024) k_lu_solve_smem(int n, const double* __restrict__ LU,
+                                                        const int32_t* __restrict__ piv, const double* __restrict__ b,
+                                                        double* __restrict__ xg) {
+  CAMG_PDL_ENTRY();
+  extern __shared__ double sm[];
+  double* lu = sm;
+  double* x = sm + (size_t)n * n;
+  double* y = x + n;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) lu[i] = LU[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < n; ++i) {
+      int p = piv[i];
+      if (p != i) { double t = x[i]; x[i] = x[p]; x[p] = t; }
+    }
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {  // unit lower
+    const double xj = x[j];
+    const double* colj = lu + (size_t)j * n;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) x[i] -= colj[i] * xj;
+    __syncthreads();
+  }
+  for (int j = n - 1; j >= 0; --j) {  // upper: y_j = x_j / u_jj, then eliminate it
+    const double yj = x[j] / lu[(size_t)j * n + j];
+    const double* colj = lu + (size_t)j * n;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) x[i] -= colj[i] * yj;
+    if (threadIdx.x == 0) y[j] = yj;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) xg[i] = y[i];
+}
+
+// dense LU solve on one CTA: factors in shared memory when they fit
+static void lu_solve(int n, const double* LU, const int32_t* piv, const double* b, double* x, cudaStream_t s) {
+  const size_t need = sizeof(double) * ((size_t)n * n + 2 * (size_t)n);
+  note_launch();
+  if (need <= size_t(220) * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      CAMG_CUDA(cudaFuncSetAttribute(k_lu_solve_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr = true;
+    }
+    launch_k(k_lu_solve_smem, 1, 1024, need, s, n, LU, piv, b, x);
+    return;
+  }
+  const size_t sh = n <= 12288 ? sizeof(double) * n : 0;
+  launch_k(k_lu_solve, 1, 1024, sh, s, n, LU, piv, b, x);
+}
+
 __global__ void k_first_zero(int64_t n, const double* __restrict__ d, unsigned long long* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (d[i] == 0.0) atomicMin(out, (unsigned long long)i);
@@ -835,9 +889,7 @@ struct Level {
     if (nl == 0) return w_dl.p;
     if (cfg.corr_kind == CAMG_PT_DIRECT) {
       CAMG_CHECK(corr_lu.p != nullptr, CAMG_ERR_SETUP, "direct corrector factors were not set");
-      note_launch();
-      size_t sh = nl <= 12288 ? sizeof(double) * nl : 0;
-      launch_k(k_lu_solve, 1, 1024, sh, s, (int)nl, corr_lu.p, corr_piv.p, rc, w_dl.p);
+      lu_solve((int)nl, corr_lu.p, corr_piv.p, rc, w_dl.p, s);
       return w_dl.p;
     }
     if (cfg.corr_kind == CAMG_PT_MCGS) {
@@ -1276,9 +1328,7 @@ struct Hierarchy {
     Level* L = levels.back();
     if (coarse_solver == CAMG_COARSE_MERGED_LU) {
       CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "coarse LU factors were not set");
-      note_launch();
-      size_t sh = n_coarse <= 12288 ? sizeof(double) * n_coarse : 0;
-      launch_k(k_lu_solve, 1, 1024, sh, s, (int)n_coarse, lu.p, piv.p, b, x);
+      lu_solve((int)n_coarse, lu.p, piv.p, b, x, s);
     } else {
       L->sweep(nullptr, b, x, s);
       L->join(s);
@@ -1441,9 +1491,7 @@ struct ScalarHier {
     ScalarLevel& L = *levels[l];
     if (l == (int)levels.size() - 1) {
       CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "scalar coarse LU factors were not set");
-      note_launch();
-      size_t sh = n_coarse <= 12288 ? sizeof(double) * n_coarse : 0;
-      launch_k(k_lu_solve, 1, 1024, sh, s, (int)n_coarse, lu.p, piv.p, b, L.x0.p);
+      lu_solve((int)n_coarse, lu.p, piv.p, b, L.x0.p, s);
       return L.x0.p;
     }
     smooth(L, nullptr, b, L.x0.p, s);
