@@ -450,6 +450,15 @@ static int64_t quad_slices() {
   return v;
 }
 
+static int64_t quad_min_blocks() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAMG_SELL_QUAD_BLOCKS");
+    v = e ? atoll(e) : kSellQuadBlocks;
+  }
+  return v;
+}
+
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
@@ -458,6 +467,9 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   v.nwork = slist ? nlist : S->nslices;
   if (v.nwork <= 0) return;
   const int64_t nw = v.nwork;
+  // rows with many blocks (R = P^T: ~117 6x3 blocks per coarse node) split
+  // over four lanes, short ones over two
+  const bool long_rows = S->nbr > 0 && S->used_blocks >= quad_min_blocks() * S->nbr;
   const unsigned grid = grid_for(nw * 32, 256, int64_t(kNumSMs) * 16);
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
@@ -465,7 +477,7 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
     if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \
-    else if (nw < quad_slices())                                                             \
+    else if (nw < quad_slices() || (nw < kSellPairSlices && long_rows))                     \
       launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(nw * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
     else if (nw < kSellPairSlices)                                                           \
