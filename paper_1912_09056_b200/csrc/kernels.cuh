@@ -12,7 +12,7 @@ inline void note_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_r
 constexpr double kDropTol = 1e-300;  // sparse.py:21 DROP_TOL
 constexpr int kDotBlocks = 592;      // 4 x 148 SMs
 constexpr int64_t kSellMinBlockRows = 50000;  // fewer block rows: lanes cannot fill 148 SMs
-constexpr int64_t kSellPairSlices = 40000;  // below: two lanes per block row (wave balance)
+constexpr int64_t kSellPairSlices = 5000;  // below: two lanes per block row (C5: level-1 passes faster one lane per row)
 constexpr int64_t kSellQuadBlocks = int64_t(1) << 40;  // ... or rows averaging this many blocks (R at 117: measured slower, opt-in)
 constexpr int64_t kSellQuadSlices = 0;  // below: four lanes per block row (measured slower on C5 level 1: opt-in)
 constexpr int64_t kMcgsCtaRows = 24576;  // S~ up to this size: single-CTA MC-SGS (x in 192 KB smem)

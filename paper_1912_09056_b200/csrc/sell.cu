@@ -450,6 +450,15 @@ static int64_t quad_slices() {
   return v;
 }
 
+static int64_t pair_slices() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAMG_SELL_PAIR");
+    v = e ? atoll(e) : kSellPairSlices;
+  }
+  return v;
+}
+
 static int64_t quad_min_blocks() {
   static int64_t v = -1;
   if (v < 0) {
@@ -477,10 +486,10 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
     if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \
-    else if (nw < quad_slices() || (nw < kSellPairSlices && long_rows))                     \
+    else if (nw < quad_slices() || (nw < pair_slices() && long_rows))                       \
       launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(nw * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
-    else if (nw < kSellPairSlices)                                                           \
+    else if (nw < pair_slices())                                                             \
       launch_k(k_sell_row2<BR, BC, Z, SP, M, 2>, grid_for(nw * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
     else launch_k(k_sell_row<BR, BC, Z, SP, M, false>, grid, 256, 0, st, v, xu, xl, sb, e);                  \
