@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -370,6 +371,100 @@ struct LaunchMcgsCta {
   }
 };
 
+// Multicolour Gauss-Seidel sweeps of a small square operator (point colouring)
+// on one 16-CTA thread-block cluster: every CTA keeps the rows it owns (the
+// p-th node of each colour goes to CTA p mod 16) and a replica of the iterate
+// in shared memory; a row update is stored into all 16 replicas through
+// distributed shared memory and the colours are separated by cluster
+// barriers.  The matrix is read from L2/HBM once per launch instead of once
+// per colour pass, and a pass costs ~1 us instead of a kernel launch.  Same
+// visiting order and update as k_mcgs_node<G, 1>.
+constexpr int kMcgsCluster = 16;
+
+template <int G>
+__global__ void __launch_bounds__(1024, 1) k_mcgs_cl(int n, int ncol, int sweeps, const int32_t* __restrict__ nd_all,
+                                                     const int32_t* __restrict__ rp_all,
+                                                     const uint16_t* __restrict__ col_all,
+                                                     const double* __restrict__ val_all,
+                                                     const int64_t* __restrict__ off_nd,
+                                                     const int64_t* __restrict__ off_nz,
+                                                     const int32_t* __restrict__ cp_all, const double* __restrict__ b,
+                                                     const double* __restrict__ dinv, double* __restrict__ y) {
+  CAMG_PDL_ENTRY();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int64_t nloc = off_nd[r + 1] - off_nd[r];
+  const int64_t nz = off_nz[r + 1] - off_nz[r];
+  double* x = reinterpret_cast<double*>(smraw);
+  double* val = x + n;
+  int32_t* rp = reinterpret_cast<int32_t*>(val + nz);
+  int32_t* nd = rp + nloc + 1;
+  int32_t* cp = nd + nloc;
+  uint16_t* col = reinterpret_cast<uint16_t*>(cp + ncol + 1);
+  for (int64_t i = threadIdx.x; i < nz; i += blockDim.x) {
+    val[i] = val_all[off_nz[r] + i];
+    col[i] = col_all[off_nz[r] + i];
+  }
+  for (int64_t i = threadIdx.x; i <= nloc; i += blockDim.x) rp[i] = rp_all[off_nd[r] + r + i];
+  for (int64_t i = threadIdx.x; i < nloc; i += blockDim.x) nd[i] = nd_all[off_nd[r] + i];
+  for (int i = threadIdx.x; i <= ncol; i += blockDim.x) cp[i] = cp_all[(int64_t)r * (ncol + 1) + i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = 0.0;
+  cl.sync();
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int grp = threadIdx.x / G, ngrp = blockDim.x / G;
+  for (int sw = 0; sw < sweeps; ++sw) {
+    for (int dir = 0; dir < 2; ++dir) {
+      for (int cc = 0; cc < ncol; ++cc) {
+        const int c = dir == 0 ? cc : ncol - 1 - cc;
+        for (int k = cp[c] + grp; k < cp[c + 1]; k += ngrp) {
+          const int i = nd[k];
+          double acc = 0.0;
+          for (int p = rp[k] + lane; p < rp[k + 1]; p += G) acc = fma(val[p], x[col[p]], acc);
+          acc = group_sum<G>(acc, mask);
+          const double xn = x[i] + dinv[i] * (b[i] - acc);
+          for (int t = lane; t < kMcgsCluster; t += G) *cl.map_shared_rank(x + i, t) = xn;
+        }
+        cl.sync();
+      }
+    }
+  }
+  if (r == 0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = x[i];
+}
+
+template <int G>
+struct LaunchMcgsCl {
+  static void run(int n, int ncol, int sweeps, const int32_t* nd, const int32_t* rp, const uint16_t* col,
+                  const double* val, const int64_t* off_nd, const int64_t* off_nz, const int32_t* cp, size_t smem,
+                  const double* b, const double* dinv, double* y, cudaStream_t s) {
+    constexpr int GG = G < 4 ? 4 : G;
+    static bool attr = false;
+    if (!attr) {
+      CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_cl<GG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      CAMG_CUDA(cudaFuncSetAttribute(k_mcgs_cl<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kMcgsCluster);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kMcgsCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    note_launch();
+    CAMG_CUDA(cudaLaunchKernelEx(&cfg, k_mcgs_cl<GG>, n, ncol, sweeps, nd, rp, col, val, off_nd, off_nz, cp, b, dinv,
+                                 y));
+  }
+};
+
 // y = x_u (zero if x is null), g = b_u
 __global__ void k_gs_init(int64_t nu, const double* __restrict__ x, const double* __restrict__ b,
                           double* __restrict__ y, double* __restrict__ g) {
@@ -682,6 +777,15 @@ struct McgsK {
   Sell* sell = nullptr;
   DBuf<double> g;
   bool cta = false;  // small square operator: whole sweeps in one CTA
+  // small square operators with point colouring: whole sweeps on one
+  // 16-CTA cluster with the rows in distributed shared memory
+  bool cl = false;
+  size_t cl_smem = 0;
+  DBuf<int32_t> cl_nd, cl_rp, cl_cp;
+  DBuf<uint16_t> cl_col;
+  DBuf<double> cl_val;
+  DBuf<int64_t> cl_offnd, cl_offnz;
+  double cl_avg = 0.0;
   ~McgsK() { delete sell; }
   int colors() const { return (int)col_ptr.size() - 1; }
 
@@ -716,6 +820,10 @@ struct McgsK {
     // (CAMG_MCGS_CTA=0 disables; measured against per-colour launches)
     const char* cta_env = getenv("CAMG_MCGS_CTA");
     cta = !(cta_env && cta_env[0] == '0') && K->n_cols == nu && nu <= kMcgsCtaRows && K->nnz <= kMcgsCtaNnz;
+    const char* cl_env = getenv("CAMG_MCGS_CLUSTER");
+    if (bs == 1 && K->n_cols == nu && nu <= 65535 && K->nnz <= (int64_t)kMcgsCluster * 24576 &&
+        !(cl_env && cl_env[0] == '0'))
+      setup_cluster(K, nd, ncol);
     // colour-ordered SELL from kGsSellMinRows rows (CAMG_GS_SELL=1 forces it,
     // =0 keeps the CSR path)
     const char* env = getenv("CAMG_GS_SELL");
@@ -734,6 +842,74 @@ struct McgsK {
       sell = sell_build_ordered(K, bs, nu, nu, order, s);
       g = DBuf<double>(nu + 1);
     }
+  }
+
+  // rows of the p-th node of every colour on CTA p mod 16, compact CSR per
+  // CTA (16-bit columns) and its colour ranges; enabled if the largest
+  // CTA's rows plus the iterate fit in shared memory
+  void setup_cluster(const Csr* K, const std::vector<int32_t>& nd, int ncol) {
+    const int64_t n = nu, CS = kMcgsCluster;
+    std::vector<int64_t> rp(n + 1);
+    std::vector<int32_t> ci(K->nnz);
+    std::vector<double> va(K->nnz);
+    CAMG_CUDA(cudaMemcpy(rp.data(), K->rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    if (K->nnz) {
+      CAMG_CUDA(cudaMemcpy(ci.data(), K->col, sizeof(int32_t) * K->nnz, cudaMemcpyDeviceToHost));
+      CAMG_CUDA(cudaMemcpy(va.data(), K->val, sizeof(double) * K->nnz, cudaMemcpyDeviceToHost));
+    }
+    std::vector<std::vector<int32_t>> lnd(CS), lrp(CS), lcp(CS);
+    std::vector<std::vector<uint16_t>> lcol(CS);
+    std::vector<std::vector<double>> lval(CS);
+    for (int64_t r = 0; r < CS; ++r) lrp[r].push_back(0);
+    for (int c = 0; c < ncol; ++c) {
+      for (int64_t r = 0; r < CS; ++r) lcp[r].push_back((int32_t)lnd[r].size());
+      for (int64_t k = col_ptr[c]; k < col_ptr[c + 1]; ++k) {
+        const int64_t r = (k - col_ptr[c]) % CS;
+        const int32_t i = nd[k];
+        lnd[r].push_back(i);
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+          lcol[r].push_back((uint16_t)ci[p]);
+          lval[r].push_back(va[p]);
+        }
+        lrp[r].push_back((int32_t)lcol[r].size());
+      }
+    }
+    for (int64_t r = 0; r < CS; ++r) lcp[r].push_back((int32_t)lnd[r].size());
+    size_t need = 0;
+    for (int64_t r = 0; r < CS; ++r) {
+      const size_t b = 8 * (size_t)n + 10 * lval[r].size() + 4 * (2 * lnd[r].size() + 1) + 4 * (size_t)(ncol + 1) + 16;
+      need = std::max(need, b);
+    }
+    if (need > size_t(200) * 1024) return;
+    std::vector<int32_t> fnd, frp, fcp;
+    std::vector<uint16_t> fcol;
+    std::vector<double> fval;
+    std::vector<int64_t> ond(CS + 1, 0), onz(CS + 1, 0);
+    for (int64_t r = 0; r < CS; ++r) {
+      ond[r + 1] = ond[r] + (int64_t)lnd[r].size();
+      onz[r + 1] = onz[r] + (int64_t)lval[r].size();
+      fnd.insert(fnd.end(), lnd[r].begin(), lnd[r].end());
+      frp.insert(frp.end(), lrp[r].begin(), lrp[r].end());  // nloc+1 entries per CTA: offset ond[r] + r
+      fcp.insert(fcp.end(), lcp[r].begin(), lcp[r].end());
+      fcol.insert(fcol.end(), lcol[r].begin(), lcol[r].end());
+      fval.insert(fval.end(), lval[r].begin(), lval[r].end());
+    }
+    auto up = [](auto& dst, const auto& src) {
+      using T = typename std::decay_t<decltype(src)>::value_type;
+      dst = std::decay_t<decltype(dst)>(src.size() + 1);
+      if (!src.empty()) CAMG_CUDA(cudaMemcpy(dst.p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+    };
+    up(cl_nd, fnd);
+    up(cl_rp, frp);
+    up(cl_cp, fcp);
+    up(cl_col, fcol);
+    up(cl_val, fval);
+    up(cl_offnd, ond);
+    up(cl_offnz, onz);
+    cl_smem = need;
+    cl_avg = n ? double(K->nnz) / n : 0.0;
+    cl = true;
+    cta = false;
   }
 
   // y = x_u (zero for x == null); the SELL path also sets g = b_u (callers
@@ -765,6 +941,11 @@ struct McgsK {
   void run(bool zero, const Csr* Arows, const double* xl, const double* b, const double* dinv, double* y, int sweeps,
            cudaStream_t s) {
     const int nc = colors();
+    if (cl && zero && xl == nullptr && Arows->n_cols == nu) {
+      dispatch_g<LaunchMcgsCl>(cl_avg, (int)nu, nc, sweeps, cl_nd.p, cl_rp.p, cl_col.p, cl_val.p, cl_offnd.p, cl_offnz.p,
+                               cl_cp.p, cl_smem, b, dinv, y, s);
+      return;
+    }
     if (cta && Arows->n_cols == nu) {
       static double cta_avg = -1.0;  // CAMG_MCGS_CTA_G forces the lanes per row (tuning)
       if (cta_avg < 0.0) {

@@ -425,12 +425,14 @@ def test_graph_disabled_equals_graph():
     np.testing.assert_array_equal(z1, z2)
 
 
-@pytest.mark.parametrize("path", ["csr", "sell", "default"])
+@pytest.mark.parametrize("path", ["csr", "sell", "cta", "default"])
 def test_mcgs_large_s_paths(path, monkeypatch):
     """Every MC-SGS execution path (one CSR launch per colour, the
-    colour-ordered SELL kernel, the default choice incl. one-CTA sweeps on
-    small levels) against the oracle emulation."""
+    colour-ordered SELL kernel, one-CTA sweeps, the default choice incl. the
+    16-CTA cluster sweeps on small levels) against the oracle emulation."""
     if path != "default":
+        monkeypatch.setenv("CAMG_MCGS_CLUSTER", "0")
+    if path in ("csr", "sell"):
         monkeypatch.setenv("CAMG_MCGS_CTA", "0")
         monkeypatch.setenv("CAMG_GS_SELL", "1" if path == "sell" else "0")
     skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcgs", 1, 1.0))
