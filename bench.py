@@ -32,9 +32,9 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # ncu dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per
 # launch, from profiles/ (one `ncu --set full` capture; None until measured)
 TRAFFIC = {
-    # profiles/r01_dominant_kernel_ncu_full.txt: k_sell_row<3,3,0,1,1,0>, C5,
-    # dram__bytes_read.sum 16.658436 GB + dram__bytes_write.sum 0.176741 GB
-    "C5": 16.835177e9,
+    # profiles/r01_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1> (masked
+    # slots), C5, dram__bytes_read.sum 14.204624 GB + dram__bytes_write.sum 0.183540 GB
+    "C5": 14.388164e9,
 }
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
@@ -471,7 +471,7 @@ def run_gpu(args):
                      "frac": dom_gbs / peak, "traffic": None if gs else TRAFFIC.get(args.config),
                      "kernel": ("k_sell_gs<3>: one fine-level multicolour block-SGS predictor sweep (forward + backward "
                                 "colour passes over a colour-ordered block SELL of K)") if gs else
-                               ("k_sell_row<3,3,mode 1>: fine-level Jacobi predictor sweep y += w D^-1 (b - [K B1][y; lam]) "
+                               ("k_sell_row<3,3,mode 1,masked>: fine-level Jacobi predictor sweep y += w D^-1 (b - [K B1][y; lam]) "
                                 "(block SELL-32 [K | B1] stream)"),
                      "algorithmic_bytes_per_launch": dom_model,
                      "bytes_model": ("SURVEY §8(d): 2 x (12 B/nnz(K) + offsets + 4 vector streams) + y/g init" if gs else

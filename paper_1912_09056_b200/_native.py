@@ -19,7 +19,8 @@ from .errors import (
 )
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcamg.so")
+# CAMG_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("CAMG_LIB") or os.path.join(_HERE, "libcamg.so")
 
 i64 = C.c_int64
 i32 = C.c_int32

@@ -25,7 +25,16 @@
 #include "kernels.cuh"
 #include "sell.cuh"
 
+#ifndef CAMG_MASKED_MINB
+#define CAMG_MASKED_MINB 6
+#endif
+#ifndef CAMG_MASKED_UNROLL
+#define CAMG_MASKED_UNROLL 1
+#endif
+
 namespace camg {
+
+constexpr int kMaskedUnroll = CAMG_MASKED_UNROLL;
 
 Sell::~Sell() {
   dfree(slice_ptr);
@@ -34,6 +43,7 @@ Sell::~Sell() {
   dfree(bval);
   dfree(mask);
   dfree(voff);
+  dfree(desc);
   dfree(perm);
   dfree(dblk);
 }
@@ -117,6 +127,22 @@ __global__ void k_slot_popc(const unsigned long long* __restrict__ mask, int64_t
     cnt[i] = __popcll(mask[i]);
 }
 
+// slot descriptors of masked SELL with at most 15 positions per block: the
+// kernel reads position q's value from group (nibble q) - 1 of the slot, or
+// uses 0 when the nibble is 0, so every load address is a shift-and-mask of
+// one warp-uniform word (no per-position branches, all loads independent)
+__global__ void k_slot_desc(const unsigned long long* __restrict__ mask, int64_t slots, int be,
+                            unsigned long long* __restrict__ desc) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < slots; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long m = mask[i];
+    unsigned long long d = 0;
+    int rank = 0;
+    for (int q = 0; q < be; ++q)
+      if (m & (1ull << q)) d |= (unsigned long long)(++rank) << (4 * q);
+    desc[i] = d | ((unsigned long long)rank << 60);
+  }
+}
+
 template <int BR, int BC>
 __global__ void k_sell_fill(CsrView A, int64_t nbr, const int32_t* __restrict__ perm,
                             const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ mask,
@@ -181,6 +207,7 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t slots = read_i64(S->slice_ptr + nslices);
   S->slots = slots;
+  masked = masked && BE <= 15;  // slot descriptors hold at most 15 positions
   S->masked = masked;
   // slot masks and value offsets
   S->mask = dalloc<unsigned long long>(slots + 1);
@@ -195,6 +222,11 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   DBuf<int64_t> cnt(slots + 1);
   note_launch();
   k_slot_popc<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, slots, cnt.p);
+  if (masked) {
+    S->desc = dalloc<unsigned long long>(slots + 1);
+    note_launch();
+    k_slot_desc<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, slots, BE, S->desc);
+  }
   S->voff = dalloc<int64_t>(slots + 1);
   exclusive_scan_i64(cnt.p, S->voff, slots, s);
   CAMG_CUDA(cudaStreamSynchronize(s));
@@ -257,7 +289,7 @@ Sell* sell_build_ordered(const Csr* A, int bs, int64_t nrows, int64_t ncols_bloc
 // SELL row kernels
 
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED>
-__global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __restrict__ xu,
+__global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
   CAMG_PDL_ENTRY();
@@ -265,7 +297,6 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
   // MODE 1: residual / fused Jacobi epilogue (RowEpi semantics)
   // MODE 2: extra Jacobi sweep: d_new = d + dinv*(r - acc), optional x update
   constexpr int BE = BR * BC;
-  constexpr uint64_t kFull = (BE == 64) ? ~0ull : ((1ull << BE) - 1ull);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -297,31 +328,37 @@ __global__ void __launch_bounds__(256) k_sell_row(SellView S, const double* __re
 #pragma unroll
           for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
         }
-      } else {
-        // masked slots: the slice's masks arrive in one coalesced load and
-        // are broadcast by shuffles; the value offset is a running sum
+      } else if constexpr (BE <= 15) {
+        // masked slots: the slice's slot descriptors arrive in one coalesced
+        // load and are broadcast by shuffles; the value offset is a running sum
         const int width = (int)(S.slice_ptr[s + 1] - base);
-        const uint64_t m0 = lane < width ? __ldg(S.mask + base + lane) : 0ull;
-        const uint64_t m1 = lane + 32 < width ? __ldg(S.mask + base + 32 + lane) : 0ull;
+        const uint64_t m0 = lane < width ? __ldg(S.desc + base + lane) : 0ull;
+        const uint64_t m1 = lane + 32 < width ? __ldg(S.desc + base + 32 + lane) : 0ull;
         int64_t voff = __ldg(S.voff + base);
+#pragma unroll kMaskedUnroll
         for (int k = 0; k < width; ++k) {
           const uint64_t m = k < 32 ? __shfl_sync(0xffffffffu, m0, k)
-                                    : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.mask + base + k));
+                                    : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
           if (k < n) {
             double xv[BC];
             load_x(base + k, xv);
             const double* v = S.bval + voff * 32 + lane;
-            if (m == kFull) {
+            // absent positions enter as fma(0, x, acc): the same operations
+            // (and results) as the full-block kernel on its stored zeros
+            double val[BE];
 #pragma unroll
-              for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
-            } else {
-#pragma unroll
-              for (int q = 0; q < BE; ++q)
-                if (m & (1ull << q))
-                  acc[q / BC] = fma(__ldcs(v + __popcll(m & ((1ull << q) - 1ull)) * 32), xv[q % BC], acc[q / BC]);
+            for (int q = 0; q < BE; ++q) {
+              // absent positions load group 0 (a sector the slot streams
+              // anyway) and are zeroed after the load, so all BE loads are
+              // unconditional and independent
+              const int g = (int)((m >> (4 * q)) & 15u);
+              const double t = __ldcs(v + max(g - 1, 0) * 32);
+              val[q] = g ? t : 0.0;
             }
+#pragma unroll
+            for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
           }
-          voff += __popcll(m);
+          voff += (int64_t)(m >> 60);
         }
       }
     }
@@ -450,13 +487,10 @@ static int64_t quad_slices() {
   return v;
 }
 
+// read per call (build and capture time only): tests switch it per case
 static int64_t pair_slices() {
-  static int64_t v = -1;
-  if (v < 0) {
-    const char* e = getenv("CAMG_SELL_PAIR");
-    v = e ? atoll(e) : kSellPairSlices;
-  }
-  return v;
+  const char* e = getenv("CAMG_SELL_PAIR");
+  return e ? atoll(e) : kSellPairSlices;
 }
 
 static int64_t quad_min_blocks() {
@@ -471,7 +505,7 @@ static int64_t quad_min_blocks() {
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
-  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->nbr, S->nslices};
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->nbr, S->nslices};
   v.slist = slist;
   v.nwork = slist ? nlist : S->nslices;
   if (v.nwork <= 0) return;
@@ -598,7 +632,7 @@ __global__ void __launch_bounds__(256) k_sell_gs(SellView S, const int32_t* __re
 template <int BR>
 static void launch_gs(const Sell* S, int64_t s0, int64_t s1, bool fwd, bool zero, const double* xl, int64_t split,
                       const double* b, const double* dinv, double* y, cudaStream_t st) {
-  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->nbr, S->nslices};
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->nbr, S->nslices};
   const unsigned grid = grid_for((s1 - s0) * 32, 256, int64_t(kNumSMs) * 16);
   const int64_t sb = split / BR;
   note_launch();
@@ -636,9 +670,12 @@ extern "C" int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows) {
     M->sell = nullptr;
     if (bs <= 1 || nrows <= 0) return;
     const char* env = getenv("CAMG_SELL_MASKED");
-    // masked slots move 16% fewer bytes on hex8 stencils but measured slower
-    // (issue-bound, scripts/sell_ab.py); full blocks unless asked for
-    const bool masked = env && env[0] == '1';
+    // masked slots (3x3 / 2x2 blocks) stream 16% fewer bytes on hex8
+    // stencils: C5 merged SpMV 2.58 -> 2.23 ms, V-cycle 23.3 -> 22.1 ms
+    // (scripts/sell_ab.py); CAMG_SELL_MASKED=0 keeps full blocks
+    // (only where the one-lane-per-row kernel runs: smaller mirrors split
+    // rows over lane pairs, which need the full-block layout)
+    const bool masked = !(env && env[0] == '0') && (nrows / bs + 31) / 32 >= pair_slices();
     M->sell = sell_build(M, bs, bs, nrows, M->n_cols - M->n_cols % bs, 0, masked);
   });
 }

@@ -17,6 +17,7 @@ struct Sell {
   double* bval = nullptr;             // [voff[slot] + rank in mask][lane]
   unsigned long long* mask = nullptr; // per slot: union of the block patterns of its lanes
   int64_t* voff = nullptr;            // per slot: offset of its value groups (32 doubles each)
+  unsigned long long* desc = nullptr; // per slot (BR*BC <= 15): nibble q = 1 + rank of position q (0: absent), bits 60-63 = count
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
   double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]
   ~Sell();
@@ -30,6 +31,7 @@ struct SellView {
   const double* __restrict__ bval;
   const unsigned long long* __restrict__ mask;
   const int64_t* __restrict__ voff;
+  const unsigned long long* __restrict__ desc;
   int64_t nbr, nslices;
   const int32_t* __restrict__ slist = nullptr;  // optional subset of slices to process
   int64_t nwork = 0;                            // slices to process (slist length, or nslices)

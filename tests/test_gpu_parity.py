@@ -255,12 +255,17 @@ def test_live_oracle_parity(cfg, scale, hkw, skw):
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
 
 
+@pytest.mark.parametrize("masked", ["1", "0"])
 @pytest.mark.parametrize("cfg,scale,hkw,skw", [LIVE[2], LIVE[3], LIVE[1]])
-def test_sell_block_path_parity(cfg, scale, hkw, skw, monkeypatch):
+def test_sell_block_path_parity(cfg, scale, hkw, skw, masked, monkeypatch):
     """Force the block SELL-32 mirror on every level that has uniform node
-    blocks and check the V-cycle / GMRES against the oracle."""
+    blocks (masked slots, the default, and full blocks) and check the
+    V-cycle / GMRES against the oracle."""
     import paper_1912_09056_b200.hierarchy as hmod
     monkeypatch.setattr(hmod, "SELL_MIN_ROWS", 0)
+    monkeypatch.setenv("CAMG_SELL_MASKED", masked)
+    if masked == "1":  # one lane per row everywhere, so small levels get masked slots too
+        monkeypatch.setenv("CAMG_SELL_PAIR", "0")
     g = generate(config_spec(cfg, scale))
     op = saddle_operator(g)
     H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
@@ -275,6 +280,32 @@ def test_sell_block_path_parity(cfg, scale, hkw, skw, monkeypatch):
     _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 150, 50)
     x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=150, restart=50))
     assert abs(rep.iterations - orep.iterations) <= 1
+
+
+@pytest.mark.parametrize("cfg,scale,bs", [("C3", 1, 3), ("C5", 3, 3)])
+def test_masked_sell_bit_identical_to_full_blocks(cfg, scale, bs, monkeypatch):
+    """Masked slots (only the union pattern of each slot stored) perform the
+    same FMA sequence as full blocks on their stored zeros: the merged SpMV is
+    bit-identical, and matches scipy.  (Sizes with enough slices for the
+    one-lane-per-row kernel, where masked slots are used.)"""
+    import torch
+    from paper_1912_09056_b200.sparse import empty, ptr, stream_ptr
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    A = op.merged()
+    n = A.num_rows
+    x = torch.from_numpy(np.random.default_rng(7).standard_normal(n)).cuda()
+    out = {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("CAMG_SELL_MASKED", m)
+        _native.call("camg_csr_attach_blocks", A.device, bs, op.n_u)
+        y = empty(n)
+        _native.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
+        torch.cuda.synchronize()
+        out[m] = y.cpu().numpy()
+    np.testing.assert_array_equal(out["0"], out["1"])
+    ref = A.to_scipy() @ x.cpu().numpy()
+    assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
 
 
 @pytest.mark.parametrize("cfg,scale,levels", [("C5", 10, 3), ("C4", 8, 3), ("C2", 4, 3)])
