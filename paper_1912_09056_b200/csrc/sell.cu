@@ -25,8 +25,14 @@
 #include "kernels.cuh"
 #include "sell.cuh"
 
+// 4 CTAs of 256 threads per SM (62 registers): every slot's value loads go
+// out in one batch (at 6 CTAs / 40 registers ptxas splits them into two or
+// more dependent rounds: C5 V-cycle 21.7 vs 22.5+ ms)
 #ifndef CAMG_MASKED_MINB
-#define CAMG_MASKED_MINB 6
+#define CAMG_MASKED_MINB 4
+#endif
+#ifndef CAMG_MASKED_PIPE
+#define CAMG_MASKED_PIPE 0
 #endif
 #ifndef CAMG_MASKED_UNROLL
 #define CAMG_MASKED_UNROLL 1
@@ -127,7 +133,30 @@ __global__ void k_slot_popc(const unsigned long long* __restrict__ mask, int64_t
     cnt[i] = __popcll(mask[i]);
 }
 
-// slot descriptors of masked SELL with at most 15 positions per block: the
+// linear slots of masked SELL: every lane of a full slice has a block in the
+// slot and lane l's block column is c0 + l (interior nodes of a structured
+// mesh: one stencil offset per slot).  The descriptor then carries c0 + 1 in
+// bits 36-59 and the kernel derives the columns instead of loading them.
+__global__ void k_slot_linear(const int64_t* __restrict__ slice_ptr, const uint8_t* __restrict__ len,
+                              const int32_t* __restrict__ bcol, int64_t nbr, int64_t nslices,
+                              unsigned long long* __restrict__ desc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = warp; sl < nslices; sl += nwarps) {
+    const int64_t base = slice_ptr[sl], width = slice_ptr[sl + 1] - base;
+    const int64_t p = sl * 32 + lane;
+    const int n = p < nbr ? len[p] : -1;
+    for (int64_t k = 0; k < width; ++k) {
+      const int32_t c = n > k ? bcol[(base + k) * 32 + lane] : -1;
+      const int32_t c0 = __shfl_sync(0xffffffffu, c, 0);
+      const bool lin = __all_sync(0xffffffffu, n > k && c == c0 + lane) && c0 >= 0 && c0 + 1 < (1 << 24);
+      if (lin && lane == 0) desc[base + k] |= (unsigned long long)(c0 + 1) << 36;
+    }
+  }
+}
+
+// slot descriptors of masked SELL with at most 9 positions per block: the
 // kernel reads position q's value from group (nibble q) - 1 of the slot, or
 // uses 0 when the nibble is 0, so every load address is a shift-and-mask of
 // one warp-uniform word (no per-position branches, all loads independent)
@@ -207,7 +236,7 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t slots = read_i64(S->slice_ptr + nslices);
   S->slots = slots;
-  masked = masked && BE <= 15;  // slot descriptors hold at most 15 positions
+  masked = masked && BE <= 9;  // slot descriptors hold at most 9 positions (bits 0-35)
   S->masked = masked;
   // slot masks and value offsets
   S->mask = dalloc<unsigned long long>(slots + 1);
@@ -238,9 +267,17 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->perm, S->slice_ptr, S->mask, S->voff,
                                                          S->bcol, S->bval, S->dblk);
   CAMG_LAUNCH_CHECK();
+  std::vector<unsigned long long> hd;
+  if (masked) {
+    note_launch();
+    k_slot_linear<<<grid_for(nslices * 32, 256), 256, 0, s>>>(S->slice_ptr, S->len, S->bcol, nbr, nslices, S->desc);
+    CAMG_LAUNCH_CHECK();
+    hd.resize(slots + 1);
+    CAMG_CUDA(cudaMemcpyAsync(hd.data(), S->desc, sizeof(unsigned long long) * (slots + 1), cudaMemcpyDeviceToHost, s));
+  }
   CAMG_CUDA(cudaStreamSynchronize(s));
   // compulsory bytes of one pass: for every row, its blocks' stored values and
-  // column (the padding of shorter rows is skipped)
+  // column (the padding of shorter rows is skipped; linear slots load no column)
   std::vector<uint8_t> hl(nbr + 1);
   std::vector<int64_t> hs(nslices + 1);
   std::vector<unsigned long long> hm(slots + 1);
@@ -251,7 +288,8 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   int64_t used = 0;
   for (int64_t p = 0; p < nbr; ++p) {
     const int64_t base = hs[p >> 5];
-    for (int k = 0; k < hl[p]; ++k) bytes += 8.0 * __builtin_popcountll(hm[base + k]) + 4.0;
+    for (int k = 0; k < hl[p]; ++k)
+      bytes += 8.0 * __builtin_popcountll(hm[base + k]) + ((masked && (hd[base + k] >> 36) & 0xFFFFFFull) ? 0.0 : 4.0);
     used += hl[p];
   }
   S->used_blocks = used;
@@ -310,8 +348,8 @@ __global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row
     if (!ZERO) {
       const int n = active ? S.len[p] : 0;
       const int64_t base = S.slice_ptr[s];
-      auto load_x = [&](int64_t slot, double* xv) {
-        const int32_t bc = __ldcs(S.bcol + slot * 32 + lane);
+      auto load_x = [&](int64_t slot, double* xv, uint32_t lin = 0) {
+        const int32_t bc = lin ? (int32_t)(lin - 1) + lane : __ldcs(S.bcol + slot * 32 + lane);
         const double* xs;
         if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
         else xs = xl ? xl + ((int64_t)bc - split_blocks) * BC : nullptr;
@@ -328,21 +366,59 @@ __global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row
 #pragma unroll
           for (int q = 0; q < BE; ++q) acc[q / BC] = fma(__ldcs(v + q * 32), xv[q % BC], acc[q / BC]);
         }
-      } else if constexpr (BE <= 15) {
+      } else if constexpr (BE <= 9) {
         // masked slots: the slice's slot descriptors arrive in one coalesced
         // load and are broadcast by shuffles; the value offset is a running sum
         const int width = (int)(S.slice_ptr[s + 1] - base);
         const uint64_t m0 = lane < width ? __ldg(S.desc + base + lane) : 0ull;
         const uint64_t m1 = lane + 32 < width ? __ldg(S.desc + base + 32 + lane) : 0ull;
-        int64_t voff = __ldg(S.voff + base);
+        // the slice's values start at group voff[base]; slots follow in order
+        const double* v = S.bval + __ldg(S.voff + base) * 32 + lane;
+#if CAMG_MASKED_PIPE
+        // software pipeline: slot k+1's value and x loads are issued before
+        // slot k's FMAs, so two slots' bytes are in flight per warp
+        auto desc_at = [&](int k) -> uint64_t {
+          return k < 32 ? __shfl_sync(0xffffffffu, m0, k)
+                        : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
+        };
+        auto fetch = [&](int k, uint64_t m, const double* vp, double* val, double* xv) {
+          if (k < n) {
+            load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
+#pragma unroll
+            for (int q = 0; q < BE; ++q) {
+              const int g = (int)((m >> (4 * q)) & 15u);
+              const double t = __ldcs(vp + max(g - 1, 0) * 32);
+              val[q] = g ? t : 0.0;
+            }
+          }
+        };
+        double vc[BE], xc[BC];
+        uint64_t mc = width > 0 ? desc_at(0) : 0ull;
+        fetch(0, mc, v, vc, xc);
+        for (int k = 0; k < width; ++k) {
+          const double* vn = v + (int)(mc >> 60) * 32;
+          const uint64_t mn = k + 1 < width ? desc_at(k + 1) : 0ull;
+          double vv[BE], xx[BC];
+          fetch(k + 1, mn, vn, vv, xx);
+          if (k < n) {
+#pragma unroll
+            for (int q = 0; q < BE; ++q) acc[q / BC] = fma(vc[q], xc[q % BC], acc[q / BC]);
+          }
+#pragma unroll
+          for (int q = 0; q < BE; ++q) vc[q] = vv[q];
+#pragma unroll
+          for (int c = 0; c < BC; ++c) xc[c] = xx[c];
+          mc = mn;
+          v = vn;
+        }
+#else
 #pragma unroll kMaskedUnroll
         for (int k = 0; k < width; ++k) {
           const uint64_t m = k < 32 ? __shfl_sync(0xffffffffu, m0, k)
                                     : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
           if (k < n) {
             double xv[BC];
-            load_x(base + k, xv);
-            const double* v = S.bval + voff * 32 + lane;
+            load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
             // absent positions enter as fma(0, x, acc): the same operations
             // (and results) as the full-block kernel on its stored zeros
             double val[BE];
@@ -358,8 +434,9 @@ __global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row
 #pragma unroll
             for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
           }
-          voff += (int64_t)(m >> 60);
+          v += (int)(m >> 60) * 32;
         }
+#endif
       }
     }
     if (!active) continue;

@@ -17,7 +17,8 @@ struct Sell {
   double* bval = nullptr;             // [voff[slot] + rank in mask][lane]
   unsigned long long* mask = nullptr; // per slot: union of the block patterns of its lanes
   int64_t* voff = nullptr;            // per slot: offset of its value groups (32 doubles each)
-  unsigned long long* desc = nullptr; // per slot (BR*BC <= 15): nibble q = 1 + rank of position q (0: absent), bits 60-63 = count
+  unsigned long long* desc = nullptr; // per slot (BR*BC <= 15): nibble q = 1 + rank of position q (0: absent),
+                                      // bits 36-59 = 1 + first column of a linear slot (0: load bcol), bits 60-63 = count
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
   double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]
   ~Sell();
