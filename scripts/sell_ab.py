@@ -1,5 +1,7 @@
 """A/B micro-benchmark of the fine-level merged-operator SpMV formats on C5:
-CSR, block SELL-32 with full 3x3 slots, masked slots (CAMG_SELL_MASKED)."""
+CSR, block SELL-32 with full 3x3 slots, masked slots (CAMG_SELL_MASKED), and
+masked slots through the per-warp TMA ring (CAMG_SELL_TMA=depth); `ident`
+= results bit-identical to the full-block kernel."""
 import ctypes as C, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -12,9 +14,9 @@ op = saddle_operator(g, device_K=True)
 A = op.merged()
 n = A.num_rows
 x = torch.from_numpy(np.random.default_rng(0).standard_normal(n)).cuda()
-y = empty(n); ref = None
+y = empty(n); ref = None; full = None
 def bench(label):
-    global ref
+    global ref, full
     for _ in range(3): N.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); 
@@ -25,9 +27,15 @@ def bench(label):
     csr_model = 12.0 * A.nnz + 4.0 * (n + 1) + 16.0 * n
     if ref is None: ref = y.clone()
     err = float((y - ref).abs().max() / ref.abs().max())
-    print(f"{label:14s} {ms:7.3f} ms  format {b.value/1e9:6.2f} GB {b.value/ms/1e6:7.0f} GB/s  csr-model {csr_model/ms/1e6:7.0f} GB/s  maxrel {err:.1e}", flush=True)
+    if label == "sell-full": full = y.clone()
+    ident = "" if full is None else f"  ident {bool(torch.equal(y, full))}"
+    print(f"{label:14s} {ms:7.3f} ms  format {b.value/1e9:6.2f} GB {b.value/ms/1e6:7.0f} GB/s  csr-model {csr_model/ms/1e6:7.0f} GB/s  maxrel {err:.1e}{ident}", flush=True)
 bench("csr")
 for mode in ("0", "1"):
     os.environ["CAMG_SELL_MASKED"] = mode
     N.call("camg_csr_attach_blocks", A.device, 3, op.n_u)
     bench("sell-full" if mode == "0" else "sell-masked")
+for d in (sys.argv[2].split(",") if len(sys.argv) > 2 else []):
+    os.environ["CAMG_SELL_TMA"] = d
+    bench(f"sell-tma-{d}")
+os.environ["CAMG_SELL_TMA"] = "0"
