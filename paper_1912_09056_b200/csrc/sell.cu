@@ -480,223 +480,6 @@ __global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row
   }
 }
 
-// ---------------------------------------------------------------------------
-// Masked 3x3 block SELL through a per-warp TMA ring.  The register-fed kernel
-// above can only keep as many value bytes in flight as it has registers to
-// receive them (one slot per warp, 32 warps per SM).  Here every warp streams
-// its slots' value groups (and the column indices of non-linear slots) into a
-// shared-memory ring of D stages with one-instruction bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx), D-1 slots ahead of the slot it
-// multiplies, so D-1 slots per warp are in flight without holding registers.
-// The x gathers of slot k+1 are issued before slot k's FMAs.  Same operations
-// in the same order as k_sell_row<..., MASKED> (bit-identical results).
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          (unsigned)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-      : "memory");
-}
-
-constexpr int kTmaWarps = 4;                 // warps per CTA
-constexpr int kTmaVals = 0;                  // stage layout: <= 9 value groups,
-constexpr int kTmaX = 9 * 256;               // the slot's x gathers (3 x 256 B),
-constexpr int kTmaCol = kTmaX + 3 * 256;     // one column row (128 B)
-constexpr int kTmaStageBytes = kTmaCol + 128;
-
-template <int D>
-constexpr size_t sell_tma_smem() {
-  return (size_t)kTmaWarps * D * (kTmaStageBytes + 16);
-}
-
-// cursor over the (slice, slot) sequence of one warp
-struct SlotCursor {
-  int64_t w;      // index into the warp's work list
-  int64_t s;      // slice
-  int64_t base;   // first slot of the slice
-  int width;      // slots in the slice
-  int k;          // slot within the slice
-  int64_t g;      // value group of slot k
-};
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"((unsigned)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-
-// Stage j of a warp's ring receives slot j's value groups and column row by
-// bulk copies (barrier bv), and later -- H slots ahead of its use, once the
-// columns have landed -- the slot's x gathers by per-lane cp.async (barrier
-// bx).  The FMAs read everything from shared memory.
-template <int MODE, bool SPLIT, int D>
-__global__ void __launch_bounds__(kTmaWarps * 32) k_sell_tma(SellView S, const double* __restrict__ xu,
-                                                           const double* __restrict__ xl, int64_t split_blocks,
-                                                           SellEpi e) {
-  constexpr int BR = 3, BC = 3, BE = 9;
-  constexpr int H = D / 2;  // x lead in slots (values lead by D)
-  extern __shared__ __align__(128) unsigned char sm_raw[];
-  const int lane = threadIdx.x & 31;
-  const int wl = threadIdx.x >> 5;
-  unsigned char* ring = sm_raw + (size_t)wl * D * kTmaStageBytes;
-  uint64_t* bv = reinterpret_cast<uint64_t*>(sm_raw + (size_t)kTmaWarps * D * kTmaStageBytes) + wl * 2 * D;
-  uint64_t* bx = bv + D;
-  if (lane == 0)
-    for (int i = 0; i < D; ++i) {
-      mbar_init(bv + i, 1);
-      mbar_init(bx + i, 32);
-    }
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-  CAMG_PDL_ENTRY();
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-
-  auto open = [&](SlotCursor& c) {  // position c at slot 0 of the first non-empty slice from c.w on
-    for (; c.w < S.nwork; c.w += nw) {
-      c.s = S.slist ? (int64_t)S.slist[c.w] : c.w;
-      c.base = S.slice_ptr[c.s];
-      c.width = (int)(S.slice_ptr[c.s + 1] - c.base);
-      c.k = 0;
-      if (c.width > 0) {
-        c.g = S.voff[c.base];
-        return;
-      }
-    }
-  };
-  auto advance = [&](SlotCursor& c, uint64_t m) {
-    c.g += (int64_t)(m >> 60);
-    if (++c.k == c.width) {
-      c.w += nw;
-      open(c);
-    }
-  };
-  // value producer: slot vseq -> stage vseq % D
-  SlotCursor vc{gw, 0, 0, 0, 0, 0};
-  open(vc);
-  int64_t vseq = 0;
-  auto issue_vals = [&]() {
-    if (vc.w >= S.nwork) return;
-    const uint64_t m = __ldg(S.desc + vc.base + vc.k);
-    const int cnt = (int)(m >> 60);
-    const bool lin = ((m >> 36) & 0xFFFFFFull) != 0;
-    const int st = (int)(vseq % D);
-    if (lane == 0) {
-      unsigned char* dst = ring + (size_t)st * kTmaStageBytes;
-      mbar_expect_tx(bv + st, (unsigned)(cnt * 256 + (lin ? 0 : 128)));
-      if (cnt) bulk_g2s(dst + kTmaVals, S.bval + vc.g * 32, (unsigned)(cnt * 256), bv + st);
-      if (!lin) bulk_g2s(dst + kTmaCol, S.bcol + (vc.base + vc.k) * 32, 128u, bv + st);
-    }
-    ++vseq;
-    advance(vc, m);
-  };
-  // x producer: slot xseq (its values and columns have landed) -> x area
-  SlotCursor xc{gw, 0, 0, 0, 0, 0};
-  open(xc);
-  int64_t xseq = 0;
-  auto issue_x = [&]() {
-    if (xc.w >= S.nwork) return;
-    const int st = (int)(xseq % D);
-    const uint64_t m = __ldg(S.desc + xc.base + xc.k);
-    const int64_t p = xc.s * 32 + lane;
-    const int n = p < S.nbr ? S.len[p] : 0;
-    if (xc.k < n) {
-      const uint32_t lin = (uint32_t)(m >> 36) & 0xFFFFFFu;
-      unsigned char* stg = ring + (size_t)st * kTmaStageBytes;
-      int32_t bc;
-      if (lin) {
-        bc = (int32_t)(lin - 1) + lane;
-      } else {
-        mbar_wait(bv + st, (unsigned)((xseq / D) & 1));
-        bc = reinterpret_cast<const int32_t*>(stg + kTmaCol)[lane];
-      }
-      const double* xs;
-      if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
-      else xs = xl ? xl + ((int64_t)bc - split_blocks) * BC : nullptr;
-      double* xd = reinterpret_cast<double*>(stg + kTmaX) + lane;
-      if (xs) {
-#pragma unroll
-        for (int q = 0; q < BC; ++q) cp_async8(xd + q * 32, xs + q);
-      } else {
-#pragma unroll
-        for (int q = 0; q < BC; ++q) xd[q * 32] = 0.0;
-      }
-    }
-    cp_async_arrive(bx + st);
-    ++xseq;
-    advance(xc, m);
-  };
-  for (int i = 0; i < D; ++i) issue_vals();
-  for (int i = 0; i < H; ++i) issue_x();
-
-  SlotCursor cc{gw, 0, 0, 0, 0, 0};
-  open(cc);
-  int64_t cseq = 0;
-  while (cc.w < S.nwork) {
-    const int64_t p = cc.s * 32 + lane;
-    const bool active = p < S.nbr;
-    const int n = active ? S.len[p] : 0;
-    double acc[BR] = {0.0, 0.0, 0.0};
-    for (int k = 0; k < cc.width; ++k) {
-      issue_x();  // slot cseq + H
-      const int st = (int)(cseq % D);
-      const unsigned par = (unsigned)((cseq / D) & 1);
-      mbar_wait(bv + st, par);
-      mbar_wait(bx + st, par);
-      if (k < n) {
-        const uint64_t m = __ldg(S.desc + cc.base + k);
-        const unsigned char* stg = ring + (size_t)st * kTmaStageBytes;
-        const double* sv = reinterpret_cast<const double*>(stg + kTmaVals) + lane;
-        const double* sx = reinterpret_cast<const double*>(stg + kTmaX) + lane;
-        double xv[BC], val[BE];
-#pragma unroll
-        for (int q = 0; q < BC; ++q) xv[q] = sx[q * 32];
-#pragma unroll
-        for (int q = 0; q < BE; ++q) {
-          const int g = (int)((m >> (4 * q)) & 15u);
-          const double t = sv[max(g - 1, 0) * 32];
-          val[q] = g ? t : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
-      }
-      __syncwarp();
-      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      issue_vals();  // refill this stage with slot cseq + D
-      ++cseq;
-    }
-    if (active) sell_epilogue<BR, false, MODE>(e, p, acc);
-    cc.w += nw;
-    open(cc);
-  }
-}
-
 // Small matrices (few slices) lose a quarter of the time to wave
 // quantisation with one warp per slice; this variant gives each block row to
 // a lane pair (even lane: first half of its slots, odd lane: second half,
@@ -772,40 +555,6 @@ static int64_t quad_min_blocks() {
   return v;
 }
 
-// TMA ring depth of the masked 3x3 kernel (CAMG_SELL_TMA; 0 = register-fed)
-static int sell_tma_depth() {
-  const char* e = getenv("CAMG_SELL_TMA");
-  return e ? atoi(e) : 0;
-}
-
-template <int MODE, bool SP, int D>
-static void launch_tma_d(const SellView& v, const double* xu, const double* xl, int64_t sb, const SellEpi& e,
-                         cudaStream_t st) {
-  auto kern = k_sell_tma<MODE, SP, D>;
-  constexpr size_t smem = sell_tma_smem<D>();
-  static int ctas = 0;  // resident CTAs per SM
-  if (!ctas) {
-    CAMG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CAMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, kTmaWarps * 32, smem));
-    if (ctas < 1) ctas = 1;
-  }
-  const int64_t want = (v.nwork + kTmaWarps - 1) / kTmaWarps;
-  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)kNumSMs * ctas);
-  launch_k(kern, grid, kTmaWarps * 32, smem, st, v, xu, xl, sb, e);
-}
-
-template <int MODE, bool SP>
-static void launch_tma(int depth, const SellView& v, const double* xu, const double* xl, int64_t sb,
-                       const SellEpi& e, cudaStream_t st) {
-  switch (depth) {
-    case 2: return launch_tma_d<MODE, SP, 2>(v, xu, xl, sb, e, st);
-    case 3: return launch_tma_d<MODE, SP, 3>(v, xu, xl, sb, e, st);
-    case 4: return launch_tma_d<MODE, SP, 4>(v, xu, xl, sb, e, st);
-    case 6: return launch_tma_d<MODE, SP, 6>(v, xu, xl, sb, e, st);
-    default: return launch_tma_d<MODE, SP, 8>(v, xu, xl, sb, e, st);
-  }
-}
-
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
@@ -821,16 +570,6 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
   note_launch();
-  if constexpr (BR == 3 && BC == 3) {
-    const int depth = sell_tma_depth();
-    if (S->masked && !zero && depth > 0) {
-      if (mode == 0) { if (sp) launch_tma<0, true>(depth, v, xu, xl, sb, e, st); else launch_tma<0, false>(depth, v, xu, xl, sb, e, st); }
-      else if (mode == 1) { if (sp) launch_tma<1, true>(depth, v, xu, xl, sb, e, st); else launch_tma<1, false>(depth, v, xu, xl, sb, e, st); }
-      else { if (sp) launch_tma<2, true>(depth, v, xu, xl, sb, e, st); else launch_tma<2, false>(depth, v, xu, xl, sb, e, st); }
-      CAMG_LAUNCH_CHECK();
-      return;
-    }
-  }
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
     if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \

@@ -1,7 +1,6 @@
 """A/B micro-benchmark of the fine-level merged-operator SpMV formats on C5:
-CSR, block SELL-32 with full 3x3 slots, masked slots (CAMG_SELL_MASKED), and
-masked slots through the per-warp TMA ring (CAMG_SELL_TMA=depth); `ident`
-= results bit-identical to the full-block kernel."""
+CSR, block SELL-32 with full 3x3 slots, masked slots (CAMG_SELL_MASKED); `ident` =
+results bit-identical to the full-block kernel."""
 import ctypes as C, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -35,7 +34,4 @@ for mode in ("0", "1"):
     os.environ["CAMG_SELL_MASKED"] = mode
     N.call("camg_csr_attach_blocks", A.device, 3, op.n_u)
     bench("sell-full" if mode == "0" else "sell-masked")
-for d in (sys.argv[2].split(",") if len(sys.argv) > 2 else []):
-    os.environ["CAMG_SELL_TMA"] = d
-    bench(f"sell-tma-{d}")
-os.environ["CAMG_SELL_TMA"] = "0"
+
