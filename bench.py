@@ -33,8 +33,8 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # launch, from profiles/ (one `ncu --set full` capture; None until measured)
 TRAFFIC = {
     # profiles/r01_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1> (masked
-    # slots), C5, dram__bytes_read.sum 14.204624 GB + dram__bytes_write.sum 0.183540 GB
-    "C5": 14.388164e9,
+    # slots), C5, dram__bytes_read.sum 13.510467 GB + dram__bytes_write.sum 0.176302 GB
+    "C5": 13.686769e9,
 }
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 

@@ -25,22 +25,22 @@
 #include "kernels.cuh"
 #include "sell.cuh"
 
-// 4 CTAs of 256 threads per SM (62 registers): every slot's value loads go
-// out in one batch (at 6 CTAs / 40 registers ptxas splits them into two or
-// more dependent rounds: C5 V-cycle 21.7 vs 22.5+ ms)
+// 4 CTAs of 256 threads per SM (64 registers): every slot's value loads go
+// out in one batch (at 5-6 CTAs / 40-48 registers ptxas interleaves them with
+// their FMAs: C5 V-cycle 20.0 ms vs 24.2 / 27.3 ms)
 #ifndef CAMG_MASKED_MINB
 #define CAMG_MASKED_MINB 4
 #endif
-#ifndef CAMG_MASKED_PIPE
-#define CAMG_MASKED_PIPE 0
-#endif
-#ifndef CAMG_MASKED_UNROLL
-#define CAMG_MASKED_UNROLL 1
+// blocks of >= 18 entries (6x6 level-1 operators, 3x6 / 6x3 transfers): at
+// the default 40 registers ptxas interleaves each load with its FMA (a few
+// loads in flight per warp); 4 CTAs/SM (62 registers) batches them (C5
+// V-cycle 21.72 -> 21.35 ms; 2 CTAs / 122 registers, all 36 loads of a 6x6
+// slot in one batch, measured the same)
+#ifndef CAMG_BIG_MINB
+#define CAMG_BIG_MINB 4
 #endif
 
 namespace camg {
-
-constexpr int kMaskedUnroll = CAMG_MASKED_UNROLL;
 
 Sell::~Sell() {
   dfree(slice_ptr);
@@ -50,6 +50,7 @@ Sell::~Sell() {
   dfree(mask);
   dfree(voff);
   dfree(desc);
+  dfree(zero);
   dfree(perm);
   dfree(dblk);
 }
@@ -252,6 +253,8 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   note_launch();
   k_slot_popc<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, slots, cnt.p);
   if (masked) {
+    S->zero = dalloc<double>(32);
+    CAMG_CUDA(cudaMemsetAsync(S->zero, 0, sizeof(double) * 32, s));
     S->desc = dalloc<unsigned long long>(slots + 1);
     note_launch();
     k_slot_desc<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, slots, BE, S->desc);
@@ -363,7 +366,7 @@ __device__ __forceinline__ void sell_epilogue(const SellEpi& e, int64_t p, const
 }
 
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED>
-__global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row(SellView S, const double* __restrict__ xu,
+__global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : (BR * BC >= 18 ? CAMG_BIG_MINB : 0)) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
   CAMG_PDL_ENTRY();
@@ -410,69 +413,28 @@ __global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row
         const uint64_t m1 = lane + 32 < width ? __ldg(S.desc + base + 32 + lane) : 0ull;
         // the slice's values start at group voff[base]; slots follow in order
         const double* v = S.bval + __ldg(S.voff + base) * 32 + lane;
-#if CAMG_MASKED_PIPE
-        // software pipeline: slot k+1's value and x loads are issued before
-        // slot k's FMAs, so two slots' bytes are in flight per warp
-        auto desc_at = [&](int k) -> uint64_t {
-          return k < 32 ? __shfl_sync(0xffffffffu, m0, k)
-                        : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
-        };
-        auto fetch = [&](int k, uint64_t m, const double* vp, double* val, double* xv) {
-          if (k < n) {
-            load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
-#pragma unroll
-            for (int q = 0; q < BE; ++q) {
-              const int g = (int)((m >> (4 * q)) & 15u);
-              const double t = __ldcs(vp + max(g - 1, 0) * 32);
-              val[q] = g ? t : 0.0;
-            }
-          }
-        };
-        double vc[BE], xc[BC];
-        uint64_t mc = width > 0 ? desc_at(0) : 0ull;
-        fetch(0, mc, v, vc, xc);
-        for (int k = 0; k < width; ++k) {
-          const double* vn = v + (int)(mc >> 60) * 32;
-          const uint64_t mn = k + 1 < width ? desc_at(k + 1) : 0ull;
-          double vv[BE], xx[BC];
-          fetch(k + 1, mn, vn, vv, xx);
-          if (k < n) {
-#pragma unroll
-            for (int q = 0; q < BE; ++q) acc[q / BC] = fma(vc[q], xc[q % BC], acc[q / BC]);
-          }
-#pragma unroll
-          for (int q = 0; q < BE; ++q) vc[q] = vv[q];
-#pragma unroll
-          for (int c = 0; c < BC; ++c) xc[c] = xx[c];
-          mc = mn;
-          v = vn;
-        }
-#else
-#pragma unroll kMaskedUnroll
         for (int k = 0; k < width; ++k) {
           const uint64_t m = k < 32 ? __shfl_sync(0xffffffffu, m0, k)
                                     : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
           if (k < n) {
             double xv[BC];
             load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
-            // absent positions enter as fma(0, x, acc): the same operations
-            // (and results) as the full-block kernel on its stored zeros
+            // absent positions load the zero group (L1/L2-resident): all BE
+            // loads are unconditional and independent, nothing but the loaded
+            // values stays live across them, and an absent position enters as
+            // fma(0, x, acc) -- the same operations (and results) as the
+            // full-block kernel on its stored zeros
             double val[BE];
 #pragma unroll
             for (int q = 0; q < BE; ++q) {
-              // absent positions load group 0 (a sector the slot streams
-              // anyway) and are zeroed after the load, so all BE loads are
-              // unconditional and independent
               const int g = (int)((m >> (4 * q)) & 15u);
-              const double t = __ldcs(v + max(g - 1, 0) * 32);
-              val[q] = g ? t : 0.0;
+              val[q] = __ldcs(g ? v + (g - 1) * 32 : S.zero + lane);
             }
 #pragma unroll
             for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
           }
           v += (int)(m >> 60) * 32;
         }
-#endif
       }
     }
     if (!active) continue;
@@ -485,7 +447,7 @@ __global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : 0) k_sell_row
 // a lane pair (even lane: first half of its slots, odd lane: second half,
 // deterministic pair reduction), i.e. two work units per slice.
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, int LPR>
-__global__ void __launch_bounds__(256) k_sell_row2(SellView S, const double* __restrict__ xu,
+__global__ void __launch_bounds__(256, BR * BC >= 18 ? CAMG_BIG_MINB : 0) k_sell_row2(SellView S, const double* __restrict__ xu,
                                                    const double* __restrict__ xl, int64_t split_blocks,
                                                    SellEpi e) {
   CAMG_PDL_ENTRY();
@@ -558,7 +520,7 @@ static int64_t quad_min_blocks() {
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
-  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->nbr, S->nslices};
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->zero, S->nbr, S->nslices};
   v.slist = slist;
   v.nwork = slist ? nlist : S->nslices;
   if (v.nwork <= 0) return;
@@ -685,7 +647,7 @@ __global__ void __launch_bounds__(256) k_sell_gs(SellView S, const int32_t* __re
 template <int BR>
 static void launch_gs(const Sell* S, int64_t s0, int64_t s1, bool fwd, bool zero, const double* xl, int64_t split,
                       const double* b, const double* dinv, double* y, cudaStream_t st) {
-  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->nbr, S->nslices};
+  SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->zero, S->nbr, S->nslices};
   const unsigned grid = grid_for((s1 - s0) * 32, 256, int64_t(kNumSMs) * 16);
   const int64_t sb = split / BR;
   note_launch();

@@ -19,6 +19,7 @@ struct Sell {
   int64_t* voff = nullptr;            // per slot: offset of its value groups (32 doubles each)
   unsigned long long* desc = nullptr; // per slot (BR*BC <= 15): nibble q = 1 + rank of position q (0: absent),
                                       // bits 36-59 = 1 + first column of a linear slot (0: load bcol), bits 60-63 = count
+  double* zero = nullptr;             // masked: one zero value group (absent positions load it)
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
   double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]
   ~Sell();
@@ -33,6 +34,7 @@ struct SellView {
   const unsigned long long* __restrict__ mask;
   const int64_t* __restrict__ voff;
   const unsigned long long* __restrict__ desc;
+  const double* __restrict__ zero;
   int64_t nbr, nslices;
   const int32_t* __restrict__ slist = nullptr;  // optional subset of slices to process
   int64_t nwork = 0;                            // slices to process (slist length, or nslices)
