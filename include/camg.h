@@ -41,6 +41,8 @@ extern "C" {
 #define CAMG_PT_CHEBYSHEV 4 /* GPU-only */
 #define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel: predictor on K (node-block
                                colouring, node_block), corrector on S~ (point colouring)      */
+#define CAMG_PT_MCILU0 6    /* GPU-only multicolour ILU(0) corrector on S~: the reference ILU(0)
+                               (smoothers.py:82-123) on the point-colour permuted S~          */
 /* A_hat modes: smoothers.py:26 A_HAT_MODES */
 #define CAMG_AHAT_PLAIN 0
 #define CAMG_AHAT_ABS_ROWSUM 1

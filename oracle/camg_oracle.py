@@ -228,11 +228,12 @@ class Point:
     def __init__(self, cfg: PointCfg, A):
         self.cfg, self.A = cfg, A
         n = A.shape[0]
-        if cfg.kind == "mcgs":
-            # reference SSOR ("sgs") on the colour-permuted matrix
+        if cfg.kind in ("mcgs", "mcilu0"):
+            # reference SSOR ("sgs") / ILU(0) on the colour-permuted matrix
             perm = np.argsort(greedy_colors(A, cfg.block), kind="stable")
             self.perm = perm
-            self.inner = Point(PointCfg("sgs", cfg.sweeps, cfg.damping), canon(A[perm][:, perm]))
+            inner = "sgs" if cfg.kind == "mcgs" else "ilu0"
+            self.inner = Point(PointCfg(inner, cfg.sweeps, cfg.damping), canon(A[perm][:, perm]))
             return
         if cfg.kind == "gpu_chebyshev":
             # GPU-only predictor (not in the reference): Chebyshev polynomial
@@ -273,7 +274,7 @@ class Point:
     def smooth(self, x, b):
         x = np.array(x, dtype=np.float64)
         k = self.cfg.kind
-        if k == "mcgs":
+        if k in ("mcgs", "mcilu0"):
             xp = self.inner.smooth(x[self.perm], np.asarray(b)[self.perm])
             out = np.empty_like(xp)
             out[self.perm] = xp

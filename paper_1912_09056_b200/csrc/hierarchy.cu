@@ -10,6 +10,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <memory>
+#include <string>
+#include <utility>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -963,6 +966,198 @@ struct McgsK {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Multicolour ILU(0) corrector on S~ (GPU-only variant of the reference's
+// "ilu0", smoothers.py:82-123, 167-171, 195-197): the reference ILU(0) -- no
+// fill, IKJ order, unit lower factor -- of S~ with its rows and columns
+// renumbered by the greedy point colouring of the MC-SGS corrector (colour
+// by colour, ascending within a colour).  Rows of one colour are uncoupled,
+// so on the renumbered matrix the strictly lower part of a row only reaches
+// earlier colours and both triangular solves run one colour per pass.  The
+// factors are kept in the original numbering (L and the strictly upper U as
+// CSR over the original rows, U's diagonal apart), so the passes need no
+// permuted vectors.  One sweep (smoothers.py:195-197):
+//   forward  colour c = 0..C-1:  y_i = (rc_i - (S~ x)_i) - sum_{k in L(i)} l_ik y_k
+//   backward colour c = C-1..0:  z_i = (y_i - sum_{j in U(i)} u_ij z_j) / u_ii,  x_i += z_i
+// (x = 0 on the first sweep: no S~ product).  The oracle emulates it as the
+// reference ILU(0) on the colour-permuted S~ (oracle/camg_oracle.py, Point).
+template <int G, bool FWD, bool RES>
+__global__ void __launch_bounds__(256) k_ilu_pass(CsrView T, CsrView A, const int32_t* __restrict__ nodes, int64_t nn,
+                                                  const double* __restrict__ rc, const double* __restrict__ udiag,
+                                                  double* y, double* z, double* x) {
+  CAMG_PDL_ENTRY();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
+  const double* v = FWD ? y : z;  // earlier colours' entries of the vector being solved for
+  for (int64_t k = tid / G; k < nn; k += stride) {
+    const int64_t i = nodes[k];
+    double acc = 0.0;
+    for (int64_t p = T.rowptr[i] + lane; p < T.rowptr[i + 1]; p += G) acc = fma(T.val[p], v[T.col[p]], acc);
+    acc = group_sum<G>(acc, mask);
+    double ax = 0.0;
+    if (FWD && RES) {
+      for (int64_t p = A.rowptr[i] + lane; p < A.rowptr[i + 1]; p += G) ax = fma(A.val[p], x[A.col[p]], ax);
+      ax = group_sum<G>(ax, mask);
+    }
+    if (lane == 0) {
+      if (FWD) {
+        y[i] = (RES ? rc[i] - ax : rc[i]) - acc;
+      } else {
+        const double zi = (y[i] - acc) / udiag[i];
+        z[i] = zi;
+        x[i] = RES ? x[i] + zi : zi;
+      }
+    }
+  }
+}
+
+template <int G>
+struct LaunchIluPass {
+  static void run(const Csr* T, const Csr* A, const int32_t* nodes, int64_t nn, bool fwd, bool res,
+                  const double* rc, const double* udiag, double* y, double* z, double* x, cudaStream_t s) {
+    if (nn <= 0) return;
+    const unsigned grid = grid_for(nn * G, 256, int64_t(kNumSMs) * 16);
+    note_launch();
+    const CsrView tv = view(T), av = view(A);
+#define CAMG_ILU_L(F, R) launch_k(k_ilu_pass<G, F, R>, grid, 256, 0, s, tv, av, nodes, nn, rc, udiag, y, z, x)
+    if (fwd) { if (res) CAMG_ILU_L(true, true); else CAMG_ILU_L(true, false); }
+    else { if (res) CAMG_ILU_L(false, true); else CAMG_ILU_L(false, false); }
+#undef CAMG_ILU_L
+  }
+};
+
+struct McIlu {
+  int64_t n = 0;
+  std::vector<int64_t> col_ptr;
+  DBuf<int32_t> nodes;
+  std::unique_ptr<Csr> L, U;  // strictly lower / upper factor rows, original numbering
+  DBuf<double> udiag, y, z;
+
+  int colors() const { return (int)col_ptr.size() - 1; }
+
+  void setup(const Csr* S, cudaStream_t s) {
+    n = S->n_rows;
+    CAMG_CHECK(S->n_cols == n, CAMG_ERR_DIMENSION, "ILU(0) needs a square operator");
+    std::vector<int32_t> color = node_colors(S, n, 1);
+    int ncol = 0;
+    for (int32_t c : color) ncol = std::max(ncol, c + 1);
+    col_ptr.assign(ncol + 1, 0);
+    for (int32_t c : color) col_ptr[c + 1]++;
+    for (int c = 0; c < ncol; ++c) col_ptr[c + 1] += col_ptr[c];
+    std::vector<int32_t> nd(n), pos(n);  // nd[new] = old, pos[old] = new
+    {
+      std::vector<int64_t> at(col_ptr.begin(), col_ptr.end() - 1);
+      for (int64_t i = 0; i < n; ++i) nd[at[color[i]]++] = (int32_t)i;
+    }
+    for (int64_t r = 0; r < n; ++r) pos[nd[r]] = (int32_t)r;
+    std::vector<int64_t> rp(n + 1);
+    std::vector<int32_t> ci(S->nnz);
+    std::vector<double> va(S->nnz);
+    CAMG_CUDA(cudaMemcpy(rp.data(), S->rowptr, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost));
+    if (S->nnz) {
+      CAMG_CUDA(cudaMemcpy(ci.data(), S->col, sizeof(int32_t) * S->nnz, cudaMemcpyDeviceToHost));
+      CAMG_CUDA(cudaMemcpy(va.data(), S->val, sizeof(double) * S->nnz, cudaMemcpyDeviceToHost));
+    }
+    // renumbered matrix: row r = old row nd[r], columns renumbered and sorted
+    std::vector<int64_t> prp(n + 1, 0);
+    std::vector<int32_t> pci(S->nnz);
+    std::vector<double> pva(S->nnz);
+    {
+      std::vector<std::pair<int32_t, double>> row;
+      for (int64_t r = 0; r < n; ++r) {
+        const int32_t o = nd[r];
+        row.clear();
+        for (int64_t q = rp[o]; q < rp[o + 1]; ++q) row.emplace_back(pos[ci[q]], va[q]);
+        std::sort(row.begin(), row.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+        prp[r + 1] = prp[r] + (int64_t)row.size();
+        for (size_t t = 0; t < row.size(); ++t) {
+          pci[prp[r] + t] = row[t].first;
+          pva[prp[r] + t] = row[t].second;
+        }
+      }
+    }
+    // reference ILU(0) (smoothers.py:80-123) on the renumbered matrix
+    std::vector<int64_t> dpos(n, -1), where(n, -1);
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t q = prp[r]; q < prp[r + 1]; ++q)
+        if (pci[q] == r) dpos[r] = q;
+    for (int64_t r = 0; r < n; ++r)
+      if (dpos[r] < 0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): missing diagonal entry in row " + std::to_string(nd[r]));
+    for (int64_t i = 0; i < n; ++i) {
+      for (int64_t q = prp[i]; q < prp[i + 1]; ++q) where[pci[q]] = q;
+      for (int64_t q = prp[i]; q < prp[i + 1]; ++q) {
+        const int64_t k = pci[q];
+        if (k >= i) break;
+        const double ukk = pva[dpos[k]];
+        if (ukk == 0.0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): zero pivot in row " + std::to_string(nd[k]));
+        const double lik = pva[q] / ukk;
+        pva[q] = lik;
+        for (int64_t t = dpos[k] + 1; t < prp[k + 1]; ++t) {
+          const int64_t w = where[pci[t]];
+          if (w >= 0) {
+            const double prod = lik * pva[t];  // separate product and difference (no contraction)
+            pva[w] = pva[w] - prod;
+          }
+        }
+      }
+      for (int64_t q = prp[i]; q < prp[i + 1]; ++q) where[pci[q]] = -1;
+      if (pva[dpos[i]] == 0.0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): zero pivot in row " + std::to_string(nd[i]));
+    }
+    // factors in the original numbering
+    std::vector<int64_t> lrp(n + 1, 0), urp(n + 1, 0);
+    for (int64_t r = 0; r < n; ++r) {
+      lrp[nd[r] + 1] = dpos[r] - prp[r];
+      urp[nd[r] + 1] = prp[r + 1] - dpos[r] - 1;
+    }
+    for (int64_t o = 0; o < n; ++o) {
+      lrp[o + 1] += lrp[o];
+      urp[o + 1] += urp[o];
+    }
+    std::vector<int32_t> lci(lrp[n]), uci(urp[n]);
+    std::vector<double> lva(lrp[n]), uva(urp[n]), ud(n);
+    for (int64_t r = 0; r < n; ++r) {
+      const int32_t o = nd[r];
+      int64_t a = lrp[o], b = urp[o];
+      for (int64_t q = prp[r]; q < dpos[r]; ++q, ++a) { lci[a] = nd[pci[q]]; lva[a] = pva[q]; }
+      for (int64_t q = dpos[r] + 1; q < prp[r + 1]; ++q, ++b) { uci[b] = nd[pci[q]]; uva[b] = pva[q]; }
+      ud[o] = pva[dpos[r]];
+    }
+    auto upload = [&](const std::vector<int64_t>& tr, const std::vector<int32_t>& tc, const std::vector<double>& tv) {
+      Csr* T = csr_alloc(n, n, tr[n]);
+      CAMG_CUDA(cudaMemcpy(T->rowptr, tr.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+      if (tr[n]) {
+        CAMG_CUDA(cudaMemcpy(T->col, tc.data(), sizeof(int32_t) * tr[n], cudaMemcpyHostToDevice));
+        CAMG_CUDA(cudaMemcpy(T->val, tv.data(), sizeof(double) * tr[n], cudaMemcpyHostToDevice));
+      }
+      return T;
+    };
+    L.reset(upload(lrp, lci, lva));
+    U.reset(upload(urp, uci, uva));
+    udiag = DBuf<double>(n + 1);
+    CAMG_CUDA(cudaMemcpy(udiag.p, ud.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    nodes = DBuf<int32_t>(n + 1);
+    CAMG_CUDA(cudaMemcpy(nodes.p, nd.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    y = DBuf<double>(n + 1);
+    z = DBuf<double>(n + 1);
+  }
+
+  // x = `sweeps` ILU(0) sweeps on S x = rc from zero
+  void run(const Csr* S, const double* rc, double* x, int sweeps, cudaStream_t s) {
+    const int nc = colors();
+    for (int k = 0; k < sweeps; ++k) {
+      const bool res = k > 0;
+      for (int c = 0; c < nc; ++c)
+        dispatch_g<LaunchIluPass>(std::max(L->avg_row, res ? S->avg_row : 0.0), L.get(), S, nodes.p + col_ptr[c],
+                                  col_ptr[c + 1] - col_ptr[c], true, res, rc, udiag.p, y.p, z.p, x, s);
+      for (int c = nc - 1; c >= 0; --c)
+        dispatch_g<LaunchIluPass>(U->avg_row, U.get(), S, nodes.p + col_ptr[c], col_ptr[c + 1] - col_ptr[c], false,
+                                  res, rc, udiag.p, y.p, z.p, x, s);
+    }
+  }
+};
+
 // pred_update: out = x + alpha du (and, when uh != null, uh = x + du)
 __global__ void k_pred_update(int64_t n, const double* __restrict__ x, const double* __restrict__ du, double alpha,
                               double* __restrict__ uh, double* __restrict__ out) {
@@ -994,6 +1189,8 @@ struct Level {
   DBuf<double> dinv_p, ainv, dinv_c;
   // multicolour Gauss-Seidel corrector on S~ (point colouring)
   McgsK cgs;
+  // multicolour ILU(0) corrector on S~
+  McIlu cilu;
   // multicolour Gauss-Seidel predictor on K
   McgsK gs;
   // external predictor solver (nested preconditioner: scalar AMG V-cycle on
@@ -1078,6 +1275,11 @@ struct Level {
       // permuted S~, from zero
       cgs.init(nullptr, rc, w_dl.p, s);
       cgs.run(true, S, nullptr, rc, dinv_c.p, w_dl.p, cfg.corr_sweeps, s);
+      return w_dl.p;
+    }
+    if (cfg.corr_kind == CAMG_PT_MCILU0) {
+      // reference ILU(0) sweeps (smoothers.py:195-197) on the colour-permuted S~, from zero
+      cilu.run(S, rc, w_dl.p, cfg.corr_sweeps, s);
       return w_dl.p;
     }
     double* cur = w_dl.p;
@@ -1354,8 +1556,9 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
                  cfg.pred_kind == CAMG_PT_CHEBYSHEV,
              CAMG_ERR_CONFIG, "GPU predictor supports jacobi, chebyshev and mcgs");
   CAMG_CHECK(cfg.pred_sweeps >= 1, CAMG_ERR_CONFIG, "predictor sweeps must be >= 1");
-  CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT || cfg.corr_kind == CAMG_PT_MCGS,
-             CAMG_ERR_CONFIG, "GPU corrector supports jacobi, mcgs and direct");
+  CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT || cfg.corr_kind == CAMG_PT_MCGS ||
+                 cfg.corr_kind == CAMG_PT_MCILU0,
+             CAMG_ERR_CONFIG, "GPU corrector supports jacobi, mcgs, mcilu0 and direct");
   cudaStream_t s = 0;
   std::unique_ptr<Level> L(new Level());
   L->cfg = cfg;
@@ -1418,6 +1621,7 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
   // point colouring of S~: the multiplier-node graph needs as many colours
   // (16 on C5) and the per-node kernels measured slower
   if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) L->cgs.setup(L->S, 1, s);
+  if (cfg.corr_kind == CAMG_PT_MCILU0 && nl > 0) L->cilu.setup(L->S, s);
   if ((cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_MCGS) && nl > 0) {
     DBuf<double> dS(nl + 1);
     csr_diagonal(L->S, 0, dS.p, s);
@@ -1985,7 +2189,10 @@ int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, dou
                               : spm(L->A, L->nu, top) + 8.0 * 2 * L->nu;
       // lambda side: B2/Cz rows, corrector sweeps over S~ (MCGS: forward +
       // backward), interface-row B1 correction, a few lambda vectors
-      const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps : std::max(0, c.corr_sweeps - 1);
+      // (MC-ILU(0): forward + backward factor passes, plus an S~ product from the second sweep)
+      const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps
+                              : c.corr_kind == CAMG_PT_MCILU0 ? c.corr_sweeps + std::max(0, c.corr_sweeps - 1)
+                                                              : std::max(0, c.corr_sweeps - 1);
       const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
                          (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
       // Chebyshev keeps d_k between its steps: + write / read of one vector

@@ -14,7 +14,10 @@ reference SGS by convergence, and elementwise with the oracle's emulation of
 the same colouring.  As corrector it colours the rows of S~; as predictor it
 colours the nodes of K (`node_block` consecutive DOFs per node, visited in
 order within a node), which is the block Gauss-Seidel the paper's Uzawa / BGS
-configurations use on the GPU.  `gpu_chebyshev` (predictor, GPU-only like
+configurations use on the GPU.  `mcilu0` (corrector) is the reference's
+ILU(0) (smoothers.py:82-123, 195-197) on S~ with rows and columns renumbered
+by the same greedy point colouring: both triangular solves then run one
+colour per pass.  `gpu_chebyshev` (predictor, GPU-only like
 `mcgs`; the reference rejects the name "chebyshev", and so does this
 package) is the Chebyshev polynomial of D^-1 K of degree `sweeps` on
 [lmax/30, 1.1 lmax] with lmax from the smoothed-aggregation power
@@ -43,15 +46,15 @@ from .sparse import (
     to_device,
 )
 
-POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct", "mcgs", "gpu_chebyshev")
+POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct", "mcgs", "mcilu0", "gpu_chebyshev")
 BLOCK_KINDS = ("uzawa", "braess_sarazin", "simple", "simplec")
 A_HAT_MODES = ("plain_diag", "abs_rowsum", "exact")
 GPU_POINT_KINDS = ("jacobi", "direct")
 GPU_PREDICTOR_KINDS = ("jacobi", "gpu_chebyshev", "mcgs")
-GPU_CORRECTOR_KINDS = ("jacobi", "direct", "mcgs")
+GPU_CORRECTOR_KINDS = ("jacobi", "direct", "mcgs", "mcilu0")
 
 _BLOCK_CODE = {"uzawa": 0, "braess_sarazin": 1, "simple": 2, "simplec": 3}
-_POINT_CODE = {"jacobi": 0, "direct": 3, "gpu_chebyshev": 4, "mcgs": 5}
+_POINT_CODE = {"jacobi": 0, "direct": 3, "gpu_chebyshev": 4, "mcgs": 5, "mcilu0": 6}
 
 
 @dataclass(frozen=True)

@@ -308,6 +308,41 @@ def test_masked_sell_bit_identical_to_full_blocks(cfg, scale, bs, monkeypatch):
     assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("cfg,scale,sweeps", [("C5", 10, 1), ("C4", 8, 2), ("C2", 4, 1)])
+def test_mcilu0_corrector_vs_oracle_emulation(cfg, scale, sweeps):
+    """GPU multicolour ILU(0) corrector == reference ILU(0) on the
+    colour-permuted S~ (oracle emulation): sweep within 1e-12, V-cycle within
+    1e-10, GMRES its within +-1; the reference's default corrector kind."""
+    skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 2, 0.6),
+               corrector=("mcilu0", sweeps, 1.0))
+    hkw = dict(max_levels=3, max_coarse_size=50)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), block_cfg(skw))
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), oracle_block_cfg(skw))
+    x0 = np.random.default_rng(0).standard_normal(op.total_rows)
+    out = H.levels[0].smoother.sweep_merged(x0, rhs).cpu().numpy()
+    u, lam = OH.levels[0].smoother.sweep(x0[:op.n_u], x0[op.n_u:], rhs[:op.n_u], rhs[op.n_u:])
+    ref = np.concatenate([u, lam])
+    assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+    v, ref = H.apply(rhs), OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, 200, 100)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
+    assert orep.converged and rep.converged
+    assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
+
+
+def test_mcilu0_rejected_as_predictor():
+    skw = dict(kind="simple", alpha=0.8, predictor=("mcilu0", 1, 1.0), corrector=("jacobi", 1, 0.8))
+    g = generate(config_spec("C2", 8))
+    op = saddle_operator(g)
+    with pytest.raises(ConfigError):
+        setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2, max_coarse_size=50), block_cfg(skw))
+
+
 @pytest.mark.parametrize("cfg,scale,levels", [("C5", 10, 3), ("C4", 8, 3), ("C2", 4, 3)])
 def test_mcgs_corrector_vs_oracle_emulation(cfg, scale, levels):
     """GPU multicolour SGS corrector == reference SSOR on the colour-permuted

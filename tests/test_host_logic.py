@@ -160,6 +160,34 @@ def test_oracle_mcgs_block_equals_permuted_ssor():
     np.testing.assert_array_equal(P.smooth(x, b), ref)
 
 
+def test_oracle_mcilu0_colour_structure():
+    """mcilu0 is the reference ILU(0) on S~ renumbered colour-major: rows of
+    one colour are uncoupled, so every strictly lower factor entry reaches an
+    earlier colour and every strictly upper one a later colour -- the property
+    that lets the GPU run both triangular solves one colour per pass."""
+    g = generate(config_spec("C4", 16))
+    oop, ometa, rhs = O.system_from_generated(g)
+    sm = O.Block(O.BlockCfg(kind="simple", alpha=0.8, predictor=O.PointCfg("jacobi", 1, 0.6),
+                             corrector=O.PointCfg("mcilu0", 2)), oop)
+    S = sm.S
+    P = sm.corr
+    col = O.greedy_colors(S)
+    perm = np.argsort(col, kind="stable")
+    Sp = O.canon(S[perm][:, perm])
+    rows = np.repeat(np.arange(Sp.shape[0]), np.diff(Sp.indptr))
+    cr, cc = col[perm][rows], col[perm][Sp.indices]
+    off = rows != Sp.indices
+    assert np.all(cr[off] != cc[off])
+    assert np.all((cc < cr)[off & (Sp.indices < rows)])
+    assert np.all((cc > cr)[off & (Sp.indices > rows)])
+    # two sweeps from zero: x1 = M^-1 b, x2 = x1 + M^-1 (b - S x1), M = LU on the permuted S~
+    b = np.random.default_rng(0).standard_normal(S.shape[0])
+    one = O.Point(O.PointCfg("mcilu0", 1), S)
+    x1 = one.apply(b)
+    x2 = x1 + one.apply(b - S @ x1)
+    np.testing.assert_allclose(P.apply(b), x2, rtol=0, atol=1e-12 * np.abs(x2).max())
+
+
 def test_parallel_pivoted_qr_bit_identical():
     """The process-parallel batched QR of the tentative prolongator equals
     scipy's batched (= per-aggregate) pivoted QR bit for bit."""
