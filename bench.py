@@ -33,8 +33,8 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # launch, from profiles/ (one `ncu --set full` capture; None until measured)
 TRAFFIC = {
     # profiles/r01_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1> (masked
-    # slots), C5, dram__bytes_read.sum 13.510467 GB + dram__bytes_write.sum 0.176302 GB
-    "C5": 13.686769e9,
+    # slots), C5, dram__bytes_read.sum 13.510589 GB + dram__bytes_write.sum 0.179949 GB
+    "C5": 13.690538e9,
 }
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 
@@ -55,11 +55,12 @@ def solver_for(config):
         "C4": (dict(max_levels=5, max_coarse_size=500),
                BlockSmootherConfig(kind="uzawa", alpha=0.6, predictor=P("jacobi", 2, 0.6),
                                    corrector=P("jacobi", 1, 0.6)), 100),
-        # chosen on C5 time to solution: Jacobi(1,0.6) predictor
-        # 0.96 s / 30 its; Jacobi(2,0.6) 1.39 s / 26 its; outer x2 1.30 s / 34 its
+        # chosen on C5 time to solution: multicolour ILU(0)
+        # corrector (the reference's default corrector kind) 20 its / 0.52 s;
+        # multicolour SGS corrector 30 its / 0.77 s
         "C5": (dict(max_levels=6, max_coarse_size=500),
                BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=3, predictor=P("jacobi", 1, 0.6),
-                                   corrector=P("mcgs", 1, 1.0)), 100),
+                                   corrector=P("mcilu0", 1, 1.0)), 100),
     }
     h, s, r = table[config]
     override = os.environ.get("CAMG_BENCH_SMOOTHER")

@@ -985,16 +985,26 @@ template <int G, bool FWD, bool RES>
 __global__ void __launch_bounds__(256) k_ilu_pass(CsrView T, CsrView A, const int32_t* __restrict__ nodes, int64_t nn,
                                                   const double* __restrict__ rc, const double* __restrict__ udiag,
                                                   double* y, double* z, double* x) {
-  CAMG_PDL_ENTRY();
+  // the factor rows are constant: each pass loads its first entries before
+  // waiting for the previous colour (PDL, as k_mcgs_node)
+  pdl_launch_dependents();
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & (G - 1);
   const unsigned mask = group_mask<G>();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x / G;
   const double* v = FWD ? y : z;  // earlier colours' entries of the vector being solved for
+  bool waited = false;
   for (int64_t k = tid / G; k < nn; k += stride) {
     const int64_t i = nodes[k];
-    double acc = 0.0;
-    for (int64_t p = T.rowptr[i] + lane; p < T.rowptr[i + 1]; p += G) acc = fma(T.val[p], v[T.col[p]], acc);
+    const int64_t p0 = T.rowptr[i] + lane, p1 = T.rowptr[i + 1];
+    const int32_t c0 = p0 < p1 ? T.col[p0] : 0;
+    const double v0 = p0 < p1 ? T.val[p0] : 0.0;
+    if (!waited) {
+      pdl_wait();
+      waited = true;
+    }
+    double acc = p0 < p1 ? v0 * v[c0] : 0.0;
+    for (int64_t p = p0 + G; p < p1; p += G) acc = fma(T.val[p], v[T.col[p]], acc);
     acc = group_sum<G>(acc, mask);
     double ax = 0.0;
     if (FWD && RES) {
@@ -1028,12 +1038,127 @@ struct LaunchIluPass {
   }
 };
 
+// One zero-start MC-ILU(0) sweep of a small S~ on one 16-CTA cluster (the
+// MC-SGS cluster layout, k_mcgs_cl): each CTA holds the L and U rows of the
+// p-th row of every colour (p mod 16) and a replica of the vector being
+// solved for; a solved entry is stored into all 16 replicas through
+// distributed shared memory, colours are separated by cluster barriers, and
+// y is overwritten by z in place (row i's y_i is last read by its own
+// backward update, later colours' entries are z by then).
+template <int G>
+__global__ void __launch_bounds__(1024, 1) k_ilu_cl(int n, int ncol, const int32_t* __restrict__ nd_all,
+                                                    const int32_t* __restrict__ lrp_all,
+                                                    const uint16_t* __restrict__ lcol_all,
+                                                    const double* __restrict__ lval_all,
+                                                    const int32_t* __restrict__ urp_all,
+                                                    const uint16_t* __restrict__ ucol_all,
+                                                    const double* __restrict__ uval_all,
+                                                    const int64_t* __restrict__ off_nd,
+                                                    const int64_t* __restrict__ off_lnz,
+                                                    const int64_t* __restrict__ off_unz,
+                                                    const int32_t* __restrict__ cp_all, const double* __restrict__ rc,
+                                                    const double* __restrict__ udiag, double* __restrict__ x) {
+  CAMG_PDL_ENTRY();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int64_t nloc = off_nd[r + 1] - off_nd[r];
+  const int64_t lnz = off_lnz[r + 1] - off_lnz[r], unz = off_unz[r + 1] - off_unz[r];
+  double* w = reinterpret_cast<double*>(smraw);
+  double* lval = w + n;
+  double* uval = lval + lnz;
+  int32_t* lrp = reinterpret_cast<int32_t*>(uval + unz);
+  int32_t* urp = lrp + nloc + 1;
+  int32_t* nd = urp + nloc + 1;
+  int32_t* cp = nd + nloc;
+  uint16_t* lcol = reinterpret_cast<uint16_t*>(cp + ncol + 1);
+  uint16_t* ucol = lcol + lnz;
+  for (int64_t i = threadIdx.x; i < lnz; i += blockDim.x) {
+    lval[i] = lval_all[off_lnz[r] + i];
+    lcol[i] = lcol_all[off_lnz[r] + i];
+  }
+  for (int64_t i = threadIdx.x; i < unz; i += blockDim.x) {
+    uval[i] = uval_all[off_unz[r] + i];
+    ucol[i] = ucol_all[off_unz[r] + i];
+  }
+  for (int64_t i = threadIdx.x; i <= nloc; i += blockDim.x) {
+    lrp[i] = lrp_all[off_nd[r] + r + i];
+    urp[i] = urp_all[off_nd[r] + r + i];
+  }
+  for (int64_t i = threadIdx.x; i < nloc; i += blockDim.x) nd[i] = nd_all[off_nd[r] + i];
+  for (int i = threadIdx.x; i <= ncol; i += blockDim.x) cp[i] = cp_all[(int64_t)r * (ncol + 1) + i];
+  cl.sync();
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int grp = threadIdx.x / G, ngrp = blockDim.x / G;
+  for (int dir = 0; dir < 2; ++dir) {
+    for (int cc = 0; cc < ncol; ++cc) {
+      const int c = dir == 0 ? cc : ncol - 1 - cc;
+      for (int k = cp[c] + grp; k < cp[c + 1]; k += ngrp) {
+        const int i = nd[k];
+        double acc = 0.0;
+        if (dir == 0) {
+          for (int p = lrp[k] + lane; p < lrp[k + 1]; p += G) acc = fma(lval[p], w[lcol[p]], acc);
+        } else {
+          for (int p = urp[k] + lane; p < urp[k + 1]; p += G) acc = fma(uval[p], w[ucol[p]], acc);
+        }
+        acc = group_sum<G>(acc, mask);
+        const double v = dir == 0 ? rc[i] - acc : (w[i] - acc) / udiag[i];
+        for (int t = lane; t < kMcgsCluster; t += G) *cl.map_shared_rank(w + i, t) = v;
+      }
+      cl.sync();
+    }
+  }
+  if (r == 0)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = w[i];
+}
+
+template <int G>
+struct LaunchIluCl {
+  static void run(int n, int ncol, const int32_t* nd, const int32_t* lrp, const uint16_t* lcol, const double* lval,
+                  const int32_t* urp, const uint16_t* ucol, const double* uval, const int64_t* off_nd,
+                  const int64_t* off_lnz, const int64_t* off_unz, const int32_t* cp, size_t smem, const double* rc,
+                  const double* udiag, double* x, cudaStream_t s) {
+    constexpr int GG = G < 4 ? 4 : G;
+    static bool attr = false;
+    if (!attr) {
+      CAMG_CUDA(cudaFuncSetAttribute(k_ilu_cl<GG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      CAMG_CUDA(cudaFuncSetAttribute(k_ilu_cl<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kMcgsCluster);
+    cfg.blockDim = dim3(1024);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kMcgsCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    note_launch();
+    CAMG_CUDA(cudaLaunchKernelEx(&cfg, k_ilu_cl<GG>, n, ncol, nd, lrp, lcol, lval, urp, ucol, uval, off_nd, off_lnz,
+                                 off_unz, cp, rc, udiag, x));
+  }
+};
+
 struct McIlu {
   int64_t n = 0;
   std::vector<int64_t> col_ptr;
   DBuf<int32_t> nodes;
   std::unique_ptr<Csr> L, U;  // strictly lower / upper factor rows, original numbering
   DBuf<double> udiag, y, z;
+  // small S~: zero-start sweeps on one 16-CTA cluster (k_ilu_cl)
+  bool cl = false;
+  size_t cl_smem = 0;
+  double cl_avg = 0.0;
+  DBuf<int32_t> cl_nd, cl_lrp, cl_urp, cl_cp;
+  DBuf<uint16_t> cl_lcol, cl_ucol;
+  DBuf<double> cl_lval, cl_uval;
+  DBuf<int64_t> cl_offnd, cl_offl, cl_offu;
 
   int colors() const { return (int)col_ptr.size() - 1; }
 
@@ -1141,11 +1266,96 @@ struct McIlu {
     CAMG_CUDA(cudaMemcpy(nodes.p, nd.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
     y = DBuf<double>(n + 1);
     z = DBuf<double>(n + 1);
+    const char* cl_env = getenv("CAMG_MCGS_CLUSTER");
+    if (n <= 65535 && !(cl_env && cl_env[0] == '0')) setup_cluster(nd, lrp, lci, lva, urp, uci, uva);
+  }
+
+  // the p-th row of every colour on CTA p mod 16 (k_mcgs_cl layout); enabled
+  // if the largest CTA's rows plus the vector replica fit in shared memory
+  void setup_cluster(const std::vector<int32_t>& nd, const std::vector<int64_t>& lrp, const std::vector<int32_t>& lci,
+                     const std::vector<double>& lva, const std::vector<int64_t>& urp,
+                     const std::vector<int32_t>& uci, const std::vector<double>& uva) {
+    const int64_t CS = kMcgsCluster;
+    const int ncol = colors();
+    std::vector<std::vector<int32_t>> lnd(CS), llrp(CS), lurp(CS), lcp(CS);
+    std::vector<std::vector<uint16_t>> llcol(CS), lucol(CS);
+    std::vector<std::vector<double>> llval(CS), luval(CS);
+    for (int64_t r = 0; r < CS; ++r) {
+      llrp[r].push_back(0);
+      lurp[r].push_back(0);
+    }
+    for (int c = 0; c < ncol; ++c) {
+      for (int64_t r = 0; r < CS; ++r) lcp[r].push_back((int32_t)lnd[r].size());
+      for (int64_t k = col_ptr[c]; k < col_ptr[c + 1]; ++k) {
+        const int64_t r = (k - col_ptr[c]) % CS;
+        const int32_t i = nd[k];
+        lnd[r].push_back(i);
+        for (int64_t p = lrp[i]; p < lrp[i + 1]; ++p) {
+          llcol[r].push_back((uint16_t)lci[p]);
+          llval[r].push_back(lva[p]);
+        }
+        for (int64_t p = urp[i]; p < urp[i + 1]; ++p) {
+          lucol[r].push_back((uint16_t)uci[p]);
+          luval[r].push_back(uva[p]);
+        }
+        llrp[r].push_back((int32_t)llcol[r].size());
+        lurp[r].push_back((int32_t)lucol[r].size());
+      }
+    }
+    for (int64_t r = 0; r < CS; ++r) lcp[r].push_back((int32_t)lnd[r].size());
+    size_t need = 0;
+    for (int64_t r = 0; r < CS; ++r) {
+      const size_t b = 8 * (size_t)n + 10 * (llval[r].size() + luval[r].size()) + 4 * (3 * lnd[r].size() + 2) +
+                       4 * (size_t)(ncol + 1) + 32;
+      need = std::max(need, b);
+    }
+    if (need > size_t(200) * 1024) return;
+    std::vector<int32_t> fnd, flrp, furp, fcp;
+    std::vector<uint16_t> flcol, fucol;
+    std::vector<double> flval, fuval;
+    std::vector<int64_t> ond(CS + 1, 0), ol(CS + 1, 0), ou(CS + 1, 0);
+    for (int64_t r = 0; r < CS; ++r) {
+      ond[r + 1] = ond[r] + (int64_t)lnd[r].size();
+      ol[r + 1] = ol[r] + (int64_t)llval[r].size();
+      ou[r + 1] = ou[r] + (int64_t)luval[r].size();
+      fnd.insert(fnd.end(), lnd[r].begin(), lnd[r].end());
+      flrp.insert(flrp.end(), llrp[r].begin(), llrp[r].end());  // nloc+1 entries per CTA: offset ond[r] + r
+      furp.insert(furp.end(), lurp[r].begin(), lurp[r].end());
+      fcp.insert(fcp.end(), lcp[r].begin(), lcp[r].end());
+      flcol.insert(flcol.end(), llcol[r].begin(), llcol[r].end());
+      fucol.insert(fucol.end(), lucol[r].begin(), lucol[r].end());
+      flval.insert(flval.end(), llval[r].begin(), llval[r].end());
+      fuval.insert(fuval.end(), luval[r].begin(), luval[r].end());
+    }
+    auto up = [](auto& dst, const auto& src) {
+      using T = typename std::decay_t<decltype(src)>::value_type;
+      dst = std::decay_t<decltype(dst)>(src.size() + 1);
+      if (!src.empty()) CAMG_CUDA(cudaMemcpy(dst.p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+    };
+    up(cl_nd, fnd);
+    up(cl_lrp, flrp);
+    up(cl_urp, furp);
+    up(cl_cp, fcp);
+    up(cl_lcol, flcol);
+    up(cl_ucol, fucol);
+    up(cl_lval, flval);
+    up(cl_uval, fuval);
+    up(cl_offnd, ond);
+    up(cl_offl, ol);
+    up(cl_offu, ou);
+    cl_smem = need;
+    cl_avg = n ? double(lrp[n] + urp[n]) / (2.0 * n) : 0.0;
+    cl = true;
   }
 
   // x = `sweeps` ILU(0) sweeps on S x = rc from zero
   void run(const Csr* S, const double* rc, double* x, int sweeps, cudaStream_t s) {
     const int nc = colors();
+    if (cl && sweeps == 1) {
+      dispatch_g<LaunchIluCl>(cl_avg, (int)n, nc, cl_nd.p, cl_lrp.p, cl_lcol.p, cl_lval.p, cl_urp.p, cl_ucol.p,
+                              cl_uval.p, cl_offnd.p, cl_offl.p, cl_offu.p, cl_cp.p, cl_smem, rc, udiag.p, x, s);
+      return;
+    }
     for (int k = 0; k < sweeps; ++k) {
       const bool res = k > 0;
       for (int c = 0; c < nc; ++c)

@@ -10,7 +10,7 @@ python bench.py > gpurun_out/${TAG}_bench_c5.log 2>&1 || { echo bench failed; ex
 CMD="python bench.py --steps 1 --warmup 3 --no-solve --no-cpu-baseline"
 $CMD > gpurun_out/plain_dom.log 2>&1 || { echo plain failed; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:'k_sell|k_resid|k_jacobi|k_spmv|k_lam|k_corr|k_lu_solve|k_b1_correct|k_mcgs|k_copy|k_add' -c 3000 --csv \
+    -k regex:'k_sell|k_resid|k_jacobi|k_spmv|k_lam|k_corr|k_lu_solve|k_b1_correct|k_mcgs|k_ilu|k_copy|k_add' -c 3000 --csv \
     --log-file gpurun_out/${TAG}_launches_vc_c5.csv $CMD > gpurun_out/ncu_vc.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_sell_row -s 23 -c 1 \
     -o gpurun_out/${TAG}_dominant_kernel_c5 $CMD > gpurun_out/ncu_dom.log 2>&1

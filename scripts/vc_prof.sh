@@ -8,7 +8,7 @@ print(d['ms_per_step'], d['solve']['gmres_iterations'], d['solve']['time_to_solu
 [ "$1" = "noprof" ] && exit 0
 $CMD > gpurun_out/plain_vc.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:'k_sell|k_resid|k_jacobi|k_spmv|k_lam|k_corr|k_lu_solve|k_b1|k_mcgs|k_copy|k_gs|k_pred' -c 3000 --csv \
+    -k regex:'k_sell|k_resid|k_jacobi|k_spmv|k_lam|k_corr|k_lu_solve|k_b1|k_mcgs|k_ilu|k_copy|k_gs|k_pred' -c 3000 --csv \
     --log-file gpurun_out/vc_launches.csv $CMD > gpurun_out/ncu_vc.log 2>&1
 python scripts/launch_breakdown.py gpurun_out/vc_launches.csv > gpurun_out/vc_breakdown.txt
 head -22 gpurun_out/vc_breakdown.txt

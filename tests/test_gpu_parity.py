@@ -308,11 +308,15 @@ def test_masked_sell_bit_identical_to_full_blocks(cfg, scale, bs, monkeypatch):
     assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("cfg,scale,sweeps", [("C5", 10, 1), ("C4", 8, 2), ("C2", 4, 1)])
-def test_mcilu0_corrector_vs_oracle_emulation(cfg, scale, sweeps):
+@pytest.mark.parametrize("cfg,scale,sweeps,cluster", [("C5", 10, 1, "1"), ("C5", 10, 1, "0"), ("C4", 8, 2, "1"),
+                                                     ("C2", 4, 1, "1")])
+def test_mcilu0_corrector_vs_oracle_emulation(cfg, scale, sweeps, cluster, monkeypatch):
     """GPU multicolour ILU(0) corrector == reference ILU(0) on the
     colour-permuted S~ (oracle emulation): sweep within 1e-12, V-cycle within
-    1e-10, GMRES its within +-1; the reference's default corrector kind."""
+    1e-10, GMRES its within +-1; the reference's default corrector kind.
+    Small S~ run whole sweeps on one 16-CTA cluster (cluster "1"), else one
+    launch per colour and direction (cluster "0", and every multi-sweep)."""
+    monkeypatch.setenv("CAMG_MCGS_CLUSTER", cluster)
     skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 2, 0.6),
                corrector=("mcilu0", sweeps, 1.0))
     hkw = dict(max_levels=3, max_coarse_size=50)
