@@ -254,6 +254,13 @@ int camg_gmres(const camg_csr* A, camg_hierarchy* H, const double* b, double* x,
 int camg_dot(int64_t n, const double* x, const double* y, double* result, void* stream);
 int camg_axpy(int64_t n, double alpha, const double* x, double* y, void* stream);
 
+/* reference ilu0_factor (smoothers.py:80-106): ILU(0) of the canonical host
+ * CSR (n x n, columns strictly increasing per row) in place: the combined
+ * factor values on A's pattern, unit lower diagonal implicit.  Host only (no
+ * device work); a missing diagonal or zero pivot -> CAMG_ERR_SINGULAR naming
+ * the row. */
+int camg_ilu0_factor(int64_t n, const int64_t* rowptr, const int32_t* col, double* val);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,7 @@ _SIGS = {
     "camg_spgemm": (C.c_int, [vp, vp, C.POINTER(vp)]),
     "camg_galerkin": (C.c_int, [vp, vp, vp, C.POINTER(vp)]),
     "camg_diagonal": (C.c_int, [vp, C.c_int, vp]),
+    "camg_ilu0_factor": (C.c_int, [i64, vp, vp, vp]),
     "camg_csr_axpby": (C.c_int, [f64, vp, f64, vp, C.POINTER(vp)]),
     "camg_csr_scale_rows": (C.c_int, [vp, vp, C.POINTER(vp)]),
     "camg_power_step": (C.c_int, [vp, vp, vp, vp, vp]),

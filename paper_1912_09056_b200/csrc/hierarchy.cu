@@ -1038,6 +1038,44 @@ struct LaunchIluPass {
   }
 };
 
+// The reference ILU(0) (smoothers.py:80-123): no fill, no pivoting, IKJ
+// order on A's pattern (columns ascending), unit lower factor implicit;
+// values factored in place with the product and the difference rounded
+// separately, as the reference's Python loop does.  Returns the diagonal
+// positions.  `name` maps a row to the number reported in errors (null:
+// itself).
+static std::vector<int64_t> ilu0_ikj(int64_t n, const int64_t* rp, const int32_t* ci, double* va,
+                                     const int32_t* name) {
+  auto nm = [&](int64_t r) { return std::to_string(name ? (int64_t)name[r] : r); };
+  std::vector<int64_t> dpos(n, -1), where(n, -1);
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t q = rp[r]; q < rp[r + 1]; ++q)
+      if (ci[q] == r) dpos[r] = q;
+  for (int64_t r = 0; r < n; ++r)
+    if (dpos[r] < 0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): missing diagonal entry in row " + nm(r));
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) where[ci[q]] = q;
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+      const int64_t k = ci[q];
+      if (k >= i) break;
+      const double ukk = va[dpos[k]];
+      if (ukk == 0.0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): zero pivot in row " + nm(k));
+      const double lik = va[q] / ukk;
+      va[q] = lik;
+      for (int64_t t = dpos[k] + 1; t < rp[k + 1]; ++t) {
+        const int64_t w = where[ci[t]];
+        if (w >= 0) {
+          volatile double prod = lik * va[t];  // no contraction into an FMA
+          va[w] = va[w] - prod;
+        }
+      }
+    }
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) where[ci[q]] = -1;
+    if (va[dpos[i]] == 0.0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): zero pivot in row " + nm(i));
+  }
+  return dpos;
+}
+
 // One zero-start MC-ILU(0) sweep of a small S~ on one 16-CTA cluster (the
 // MC-SGS cluster layout, k_mcgs_cl): each CTA holds the L and U rows of the
 // p-th row of every colour (p mod 16) and a replica of the vector being
@@ -1204,32 +1242,7 @@ struct McIlu {
       }
     }
     // reference ILU(0) (smoothers.py:80-123) on the renumbered matrix
-    std::vector<int64_t> dpos(n, -1), where(n, -1);
-    for (int64_t r = 0; r < n; ++r)
-      for (int64_t q = prp[r]; q < prp[r + 1]; ++q)
-        if (pci[q] == r) dpos[r] = q;
-    for (int64_t r = 0; r < n; ++r)
-      if (dpos[r] < 0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): missing diagonal entry in row " + std::to_string(nd[r]));
-    for (int64_t i = 0; i < n; ++i) {
-      for (int64_t q = prp[i]; q < prp[i + 1]; ++q) where[pci[q]] = q;
-      for (int64_t q = prp[i]; q < prp[i + 1]; ++q) {
-        const int64_t k = pci[q];
-        if (k >= i) break;
-        const double ukk = pva[dpos[k]];
-        if (ukk == 0.0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): zero pivot in row " + std::to_string(nd[k]));
-        const double lik = pva[q] / ukk;
-        pva[q] = lik;
-        for (int64_t t = dpos[k] + 1; t < prp[k + 1]; ++t) {
-          const int64_t w = where[pci[t]];
-          if (w >= 0) {
-            const double prod = lik * pva[t];  // separate product and difference (no contraction)
-            pva[w] = pva[w] - prod;
-          }
-        }
-      }
-      for (int64_t q = prp[i]; q < prp[i + 1]; ++q) where[pci[q]] = -1;
-      if (pva[dpos[i]] == 0.0) throw Error(CAMG_ERR_SINGULAR, "ILU(0): zero pivot in row " + std::to_string(nd[i]));
-    }
+    std::vector<int64_t> dpos = ilu0_ikj(n, prp.data(), pci.data(), pva.data(), nd.data());
     // factors in the original numbering
     std::vector<int64_t> lrp(n + 1, 0), urp(n + 1, 0);
     for (int64_t r = 0; r < n; ++r) {
@@ -2431,3 +2444,14 @@ int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, dou
 }
 
 }  // extern "C"
+
+// reference ilu0_factor (smoothers.py:80-106) on host CSR arrays, in place
+extern "C" int camg_ilu0_factor(int64_t n, const int64_t* rowptr, const int32_t* col, double* val) {
+  return guarded([&] {
+    CAMG_CHECK(n >= 0 && (n == 0 || (rowptr && col && val)), CAMG_ERR_ARG, "ilu0_factor: bad arguments");
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t q = rowptr[r] + 1; q < rowptr[r + 1]; ++q)
+        CAMG_CHECK(col[q - 1] < col[q], CAMG_ERR_ARG, "ilu0_factor: columns must be strictly increasing");
+    ilu0_ikj(n, rowptr, col, val, nullptr);
+  });
+}

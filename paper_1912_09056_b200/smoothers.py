@@ -32,12 +32,13 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .errors import ConfigError
+from .errors import ConfigError, SingularMatrixError
 from .saddle import SaddleOperator, SaddleSystem
 from .sparse import (
     BlockVector,
     SparseMatrix,
     diagonal_device,
+    extract_diagonal,
     empty,
     is_device,
     lu_factor_quiet,
@@ -301,3 +302,66 @@ def simple_sweep(sys, cfg: BlockSmootherConfig, x: BlockVector, b: BlockVector) 
 
 def point_smooth(cfg: PointSmootherConfig, A: SparseMatrix, x, b):
     return PointSmoother(cfg, A).smooth(x, b)
+
+
+# -- host helpers of the reference API (smoothers.py:80-123, 209-217, 347-384) --
+
+
+def ilu0_factor(A: SparseMatrix) -> np.ndarray:
+    """ILU(0) factor values on A's exact pattern, unit lower diagonal implicit
+    (smoothers.py:80-123): libcamg's host factorization (camg_ilu0_factor),
+    the one the multicolour ILU(0) corrector applies to the permuted S~.  A
+    missing diagonal or a zero pivot raises SingularMatrixError naming the
+    row."""
+    ro, ci, va = A._host_arrays()
+    ro = np.ascontiguousarray(ro, dtype=np.int64)
+    ci32 = np.ascontiguousarray(ci, dtype=np.int32)
+    out = np.array(va, dtype=np.float64)
+    N.call("camg_ilu0_factor", A.num_rows, ro.ctypes.data_as(C.c_void_p), ci32.ctypes.data_as(C.c_void_p),
+           out.ctypes.data_as(C.c_void_p))
+    return out
+
+
+def a_hat_diagonal(K: SparseMatrix, mode: str) -> np.ndarray:
+    """Diagonal approximation of K used in S~ (smoothers.py:209-217)."""
+    if mode == "plain_diag":
+        d = extract_diagonal(K, "plain")
+        if np.any(d == 0.0):
+            raise SingularMatrixError("a_hat: zero diagonal entry")
+        return d
+    if mode == "abs_rowsum":
+        return extract_diagonal(K, "abs_rowsum")
+    raise ValueError(f"a_hat_diagonal: unsupported mode {mode!r}")
+
+
+def preconditioning_matrix(sys, cfg: BlockSmootherConfig) -> np.ndarray:
+    """Dense block preconditioner M of one smoother step with exact inner
+    solves, x <- x + M^-1 (b - A x) (smoothers.py:347-378; paper Algs. 2-4):
+    Uzawa  M = [[K, 0], [B2, -S]] / alpha,            S = Cz + B2 A^-1 B1
+    BS     M = [[alpha A^, B1], [B2, -Cz]]
+    SIMPLE M = [[K, 0], [B2, -S]] [[I, A^-1 B1], [0, I / alpha]],  S = alpha (Cz + B2 A^-1 B1)
+    with A^ = K for a_hat_mode "exact", else diag(a_hat_diagonal).  Test-scale
+    (dense) helper."""
+    op = sys.op if isinstance(sys, SaddleSystem) else sys
+    K, B1, B2, Cz = (m.to_dense() for m in (op.K, op.B1, op.B2, op.Cz))
+    nu, nl = op.n_u, op.n_lam
+    a = cfg.alpha
+    mode = cfg.effective_a_hat_mode()
+    ahat = K if mode == "exact" else np.diag(a_hat_diagonal(op.K, mode))
+    ahat_inv = np.linalg.inv(ahat)
+    zero_ul = np.zeros((nu, nl))
+    if cfg.kind == "uzawa":
+        S = Cz + B2 @ ahat_inv @ B1
+        return np.block([[K, zero_ul], [B2, -S]]) / a
+    if cfg.kind == "braess_sarazin":
+        return np.block([[a * ahat, B1], [B2, -Cz]])
+    S = a * (Cz + B2 @ ahat_inv @ B1)
+    lower = np.block([[K, zero_ul], [B2, -S]])
+    upper = np.block([[np.eye(nu), ahat_inv @ B1], [np.zeros((nl, nu)), np.eye(nl) / a]])
+    return lower @ upper
+
+
+def error_matrix(sys, cfg: BlockSmootherConfig) -> np.ndarray:
+    """E = A - M of the configured smoother (smoothers.py:381-384)."""
+    op = sys.op if isinstance(sys, SaddleSystem) else sys
+    return op.merged_dense() - preconditioning_matrix(sys, cfg)

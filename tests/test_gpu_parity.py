@@ -339,6 +339,52 @@ def test_mcilu0_corrector_vs_oracle_emulation(cfg, scale, sweeps, cluster, monke
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
 
 
+@pytest.mark.parametrize("kind,alpha", [("uzawa", 0.7), ("braess_sarazin", 1.9), ("simple", 0.8), ("simplec", 1.0)])
+def test_sweep_is_richardson_with_preconditioning_matrix(kind, alpha):
+    """With exact inner solves a block-smoother step is x + M^-1 (b - A x), M
+    from the defining equations (smoothers.preconditioning_matrix; reference
+    tests/test_smoothers.py:201-213).  K diagonal makes the GPU's one-sweep
+    undamped Jacobi predictor exact; the corrector is the dense LU."""
+    from paper_1912_09056_b200.saddle import SaddleOperator
+    from paper_1912_09056_b200.smoothers import BlockSmoother, error_matrix, preconditioning_matrix
+    from paper_1912_09056_b200.sparse import BlockVector
+    rng = np.random.default_rng(11)
+    for _ in range(3):
+        nu, nl = int(rng.integers(6, 31)), int(rng.integers(2, 11))
+        K = np.diag(rng.uniform(1.0, 3.0, nu))
+        B1 = rng.standard_normal((nu, nl))
+        B2 = B1.T.copy()
+        Cz = np.diag(rng.uniform(0.5, 1.5, nl))
+        op = SaddleOperator(*(SparseMatrix.from_dense(m) for m in (K, B1, B2, Cz)))
+        cfg = BlockSmootherConfig(kind=kind, alpha=alpha, predictor=PointSmootherConfig("jacobi", 1, 1.0),
+                                  corrector=PointSmootherConfig("direct"))
+        x0 = BlockVector(rng.standard_normal(nu), rng.standard_normal(nl))
+        b = BlockVector(rng.standard_normal(nu), rng.standard_normal(nl))
+        out = BlockSmoother(cfg, op).sweep(x0, b).merged()
+        A = op.merged_dense()
+        M = preconditioning_matrix(op, cfg)
+        ref = x0.merged() + np.linalg.solve(M, b.merged() - A @ x0.merged())
+        assert np.abs(out - ref).max() <= 1e-11 * max(1.0, np.abs(ref).max())
+        np.testing.assert_allclose(error_matrix(op, cfg), A - M, rtol=0, atol=0)
+
+
+def test_uzawa_error_matrix_closed_form():
+    """E = A - M for Uzawa (reference tests/test_smoothers.py:231-247)."""
+    from paper_1912_09056_b200.saddle import SaddleOperator
+    from paper_1912_09056_b200.smoothers import error_matrix
+    rng = np.random.default_rng(13)
+    nu, nl = 12, 4
+    K = np.diag(rng.uniform(1.0, 3.0, nu)) + 0.1 * rng.standard_normal((nu, nu))
+    B1 = rng.standard_normal((nu, nl))
+    B2, Cz = B1.T.copy(), np.eye(nl)
+    op = SaddleOperator(*(SparseMatrix.from_dense(m) for m in (K, B1, B2, Cz)))
+    alpha = 0.7
+    E = error_matrix(op, BlockSmootherConfig(kind="uzawa", alpha=alpha))
+    S = Cz + B2 @ np.diag(1.0 / np.diag(K)) @ B1
+    E_ref = np.block([[(1 - 1 / alpha) * K, B1], [(1 - 1 / alpha) * B2, -Cz + S / alpha]])
+    assert np.abs(E - E_ref).max() <= 1e-12 * max(1.0, np.abs(E_ref).max())
+
+
 def test_mcilu0_rejected_as_predictor():
     skw = dict(kind="simple", alpha=0.8, predictor=("mcilu0", 1, 1.0), corrector=("jacobi", 1, 0.8))
     g = generate(config_spec("C2", 8))

@@ -188,6 +188,31 @@ def test_oracle_mcilu0_colour_structure():
     np.testing.assert_allclose(P.apply(b), x2, rtol=0, atol=1e-12 * np.abs(x2).max())
 
 
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_ilu0_factor_matches_oracle_bit_for_bit(seed):
+    """smoothers.ilu0_factor (libcamg host factorization, the one the MC-ILU(0)
+    corrector uses) == the reference ILU(0) restated in the oracle."""
+    from paper_1912_09056_b200.smoothers import ilu0_factor
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(20, 120))
+    A = scipy.sparse.random(n, n, density=0.08, random_state=seed, format="csr")
+    A = O.canon(A + A.T + scipy.sparse.diags(rng.uniform(2.0, 4.0, n)))
+    M = SparseMatrix(n, n, A.indptr, A.indices, A.data)
+    np.testing.assert_array_equal(ilu0_factor(M), O.ilu0_values(A))
+
+
+def test_ilu0_factor_errors():
+    from paper_1912_09056_b200.errors import SingularMatrixError
+    from paper_1912_09056_b200.smoothers import ilu0_factor
+    no_diag = SparseMatrix(2, 2, [0, 1, 2], [1, 0], [1.0, 1.0])
+    with pytest.raises(SingularMatrixError, match="missing diagonal entry in row 0"):
+        ilu0_factor(no_diag)
+    # [[1, 1], [1, 1]]: the second pivot cancels to zero
+    zero_piv = SparseMatrix(2, 2, [0, 2, 4], [0, 1, 0, 1], [1.0, 1.0, 1.0, 1.0])
+    with pytest.raises(SingularMatrixError, match="zero pivot in row 1"):
+        ilu0_factor(zero_piv)
+
+
 def test_parallel_pivoted_qr_bit_identical():
     """The process-parallel batched QR of the tentative prolongator equals
     scipy's batched (= per-aggregate) pivoted QR bit for bit."""
