@@ -201,6 +201,29 @@ __global__ void k_sell_fill(CsrView A, int64_t nbr, const int32_t* __restrict__ 
   }
 }
 
+// per block row: its stored value bytes + column bytes (acc[0]) and blocks (acc[1])
+__global__ void k_sell_row_bytes(const int64_t* __restrict__ slice_ptr, const uint8_t* __restrict__ len,
+                                 const unsigned long long* __restrict__ mask,
+                                 const unsigned long long* __restrict__ desc, int64_t nbr,
+                                 unsigned long long* __restrict__ acc) {
+  unsigned long long b = 0, u = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t base = slice_ptr[p >> 5];
+    const int n = len[p];
+    for (int k = 0; k < n; ++k)
+      b += 8ull * __popcll(mask[base + k]) + ((desc && ((desc[base + k] >> 36) & 0xFFFFFFull)) ? 0ull : 4ull);
+    u += n;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(acc, b);
+    atomicAdd(acc + 1, u);
+  }
+}
+
 template <int BR, int BC>
 Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cudaStream_t s,
             const std::vector<int32_t>* order = nullptr) {
@@ -270,31 +293,25 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->perm, S->slice_ptr, S->mask, S->voff,
                                                          S->bcol, S->bval, S->dblk);
   CAMG_LAUNCH_CHECK();
-  std::vector<unsigned long long> hd;
   if (masked) {
     note_launch();
     k_slot_linear<<<grid_for(nslices * 32, 256), 256, 0, s>>>(S->slice_ptr, S->len, S->bcol, nbr, nslices, S->desc);
     CAMG_LAUNCH_CHECK();
-    hd.resize(slots + 1);
-    CAMG_CUDA(cudaMemcpyAsync(hd.data(), S->desc, sizeof(unsigned long long) * (slots + 1), cudaMemcpyDeviceToHost, s));
   }
-  CAMG_CUDA(cudaStreamSynchronize(s));
   // compulsory bytes of one pass: for every row, its blocks' stored values and
-  // column (the padding of shorter rows is skipped; linear slots load no column)
-  std::vector<uint8_t> hl(nbr + 1);
-  std::vector<int64_t> hs(nslices + 1);
-  std::vector<unsigned long long> hm(slots + 1);
-  CAMG_CUDA(cudaMemcpy(hl.data(), S->len, nbr, cudaMemcpyDeviceToHost));
-  CAMG_CUDA(cudaMemcpy(hs.data(), S->slice_ptr, sizeof(int64_t) * (nslices + 1), cudaMemcpyDeviceToHost));
-  CAMG_CUDA(cudaMemcpy(hm.data(), S->mask, sizeof(unsigned long long) * (slots + 1), cudaMemcpyDeviceToHost));
-  double bytes = 0.0;
-  int64_t used = 0;
-  for (int64_t p = 0; p < nbr; ++p) {
-    const int64_t base = hs[p >> 5];
-    for (int k = 0; k < hl[p]; ++k)
-      bytes += 8.0 * __builtin_popcountll(hm[base + k]) + ((masked && (hd[base + k] >> 36) & 0xFFFFFFull) ? 0.0 : 4.0);
-    used += hl[p];
-  }
+  // column (the padding of shorter rows is skipped; linear slots load no
+  // column), summed on the device
+  DBuf<unsigned long long> acc(2);
+  CAMG_CUDA(cudaMemsetAsync(acc.p, 0, 2 * sizeof(unsigned long long), s));
+  note_launch();
+  k_sell_row_bytes<<<grid_for(nbr, 256), 256, 0, s>>>(S->slice_ptr, S->len, S->mask, masked ? S->desc : nullptr, nbr,
+                                                      acc.p);
+  CAMG_LAUNCH_CHECK();
+  unsigned long long h_acc[2] = {0, 0};
+  CAMG_CUDA(cudaMemcpyAsync(h_acc, acc.p, sizeof(h_acc), cudaMemcpyDeviceToHost, s));
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  const double bytes = (double)h_acc[0];
+  const int64_t used = (int64_t)h_acc[1];
   S->used_blocks = used;
   S->pass_bytes = bytes + (double)nbr + 16.0 * (double)(nslices + 1) + 16.0 * (double)slots / 32.0;
   return S.release();
