@@ -453,11 +453,34 @@ struct OutArgs {
   double* val;
   int32_t* overflow;      // per row flag (count pass)
   double tol;
+  // staging (count pass): a counted row is also stored, final order, at
+  // soff[row] in (scol, sval) while the buffer lasts, so the fill pass
+  // copies it instead of recomputing it; soff[row] = -1: recompute
+  int32_t* scol = nullptr;
+  double* sval = nullptr;
+  int64_t* soff = nullptr;
+  unsigned long long* stop = nullptr;
+  int64_t scap = 0;
 };
 
 template <bool FILL>
 __device__ void emit(Hash h, int64_t row, int lane, const OutArgs& o) {
-  if (!FILL) {
+  if (!FILL && o.scol) {
+    const int n = compact_sort(h, lane, o.tol);
+    long long off = -1;
+    if (lane == 0) {
+      const unsigned long long t = atomicAdd(o.stop, (unsigned long long)n);
+      off = (t + (unsigned long long)n <= (unsigned long long)o.scap) ? (long long)t : -1;
+      o.cnt[row] = n;
+      o.soff[row] = off;
+    }
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off >= 0)
+      for (int i = lane; i < n; i += 32) {
+        o.scol[off + i] = h.keys[i];
+        o.sval[off + i] = h.vals[i];
+      }
+  } else if (!FILL) {
     int n = count_kept(h, lane, o.tol);
     if (lane == 0) o.cnt[row] = n;
   } else {
@@ -484,6 +507,7 @@ __global__ void k_product(CsrView A, CsrView B, bool reverse_a, const double* __
   Hash h{reinterpret_cast<int32_t*>(base + (size_t)cap * 8), nullptr, reinterpret_cast<double*>(base), cap};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
+    if (FILL && o.soff && o.soff[row] >= 0) continue;  // copied from the staging buffer
     bool ok = row_product_flat(A, B, row, reverse_a, scale_a, h, lane, (cap * 3) / 4, sp_all[w]);
     if (!ok) {
       if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
@@ -511,12 +535,30 @@ __global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restr
   Hash h2{reinterpret_cast<int32_t*>(b2 + (size_t)cap2 * 8), nullptr, reinterpret_cast<double*>(b2), cap2};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
+    if (FILL && o.soff && o.soff[row] >= 0) continue;  // copied from the staging buffer
     bool ok = row_triple(R, A, P, row, h1, h2, lane, (cap1 * 3) / 4, (cap2 * 3) / 4, sp_all[w]);
     if (!ok) {
       if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
       continue;
     }
     emit<FILL>(h2, row, lane, o);
+  }
+}
+
+// fill the staged rows: warp per row, copy from the staging buffer
+__global__ void k_copy_staged(int64_t n_rows, const int64_t* __restrict__ soff, const int64_t* __restrict__ rowptr,
+                              const int32_t* __restrict__ scol, const double* __restrict__ sval,
+                              int32_t* __restrict__ col, double* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; row < n_rows; row += nw) {
+    const int64_t off = soff[row];
+    if (off < 0) continue;
+    const int64_t b = rowptr[row], n = rowptr[row + 1] - b;
+    for (int64_t i = lane; i < n; i += 32) {
+      col[b + i] = scol[off + i];
+      val[b + i] = sval[off + i];
+    }
   }
 }
 
@@ -559,6 +601,31 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   DBuf<int32_t> ovf(n_rows + 1);
   CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
   OutArgs o{cnt.p, nullptr, nullptr, nullptr, ovf.p, tol};
+  // staging buffer: up to 40% of the free memory (<= 16 GB); rows past it
+  // are recomputed by the fill pass (CAMG_SPGEMM_STAGE=0 disables)
+  DBuf<int32_t> scol;
+  DBuf<double> sval;
+  DBuf<int64_t> soff;
+  DBuf<unsigned long long> stop;
+  {
+    const char* e = getenv("CAMG_SPGEMM_STAGE");
+    size_t fr = 0, tot = 0;
+    CAMG_CUDA(cudaMemGetInfo(&fr, &tot));
+    const int64_t cap = std::min<int64_t>((int64_t)(0.4 * (double)fr) / 12, (int64_t(16) << 30) / 12);
+    if (!(e && e[0] == '0') && n_rows > 0 && cap > 0) {
+      scol = DBuf<int32_t>(cap);
+      sval = DBuf<double>(cap);
+      soff = DBuf<int64_t>(n_rows + 1);
+      stop = DBuf<unsigned long long>(1);
+      CAMG_CUDA(cudaMemsetAsync(soff.p, 0xFF, sizeof(int64_t) * (n_rows + 1), s));
+      CAMG_CUDA(cudaMemsetAsync(stop.p, 0, sizeof(unsigned long long), s));
+      o.scol = scol.p;
+      o.sval = sval.p;
+      o.soff = soff.p;
+      o.stop = stop.p;
+      o.scap = cap;
+    }
+  }
   std::vector<int64_t> big;
   if (start_global) {
     // every row starts in the global-memory hash tables (L2-resident, full
@@ -619,6 +686,23 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   C->val = dalloc<double>(nnz);
   C->avg_row = n_rows ? double(nnz) / n_rows : 0.0;
   OutArgs f{nullptr, C->rowptr, C->col, C->val, nullptr, tol};
+  f.soff = o.soff;
+  if (o.scol && n_rows) {
+    note_launch();
+    k_copy_staged<<<grid_for(n_rows * 32, 256, int64_t(kNumSMs) * 16), 256, 0, s>>>(n_rows, o.soff, C->rowptr, o.scol,
+                                                                                   o.sval, C->col, C->val);
+    CAMG_LAUNCH_CHECK();
+    unsigned long long used = 0;
+    CAMG_CUDA(cudaMemcpyAsync(&used, o.stop, sizeof(used), cudaMemcpyDeviceToHost, s));
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    if (getenv("CAMG_DEBUG"))
+      fprintf(stderr, "[camg] spgemm staged %llu of %lld entries (cap %lld)\n", used, (long long)nnz,
+              (long long)o.scap);
+    if (used <= (unsigned long long)o.scap) {  // every row staged: nothing to recompute
+      CAMG_CUDA(cudaStreamSynchronize(s));
+      return C;
+    }
+  }
   // fill: small rows from shared memory (overflow rows are skipped there)
   if (n_rows && !start_global) launch(true, false, nullptr, n_rows, 0, 0, nullptr, f);
   for (auto& b : batches) {
