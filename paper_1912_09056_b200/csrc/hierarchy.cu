@@ -1044,8 +1044,9 @@ struct LaunchIluPass {
 // separately, as the reference's Python loop does.  Returns the diagonal
 // positions.  `name` maps a row to the number reported in errors (null:
 // itself).
-static std::vector<int64_t> ilu0_ikj(int64_t n, const int64_t* rp, const int32_t* ci, double* va,
-                                     const int32_t* name) {
+__attribute__((optimize("fp-contract=off"))) static std::vector<int64_t> ilu0_ikj(int64_t n, const int64_t* rp,
+                                                                                  const int32_t* ci, double* va,
+                                                                                  const int32_t* name) {
   auto nm = [&](int64_t r) { return std::to_string(name ? (int64_t)name[r] : r); };
   std::vector<int64_t> dpos(n, -1), where(n, -1);
   for (int64_t r = 0; r < n; ++r)
@@ -1065,8 +1066,7 @@ static std::vector<int64_t> ilu0_ikj(int64_t n, const int64_t* rp, const int32_t
       for (int64_t t = dpos[k] + 1; t < rp[k + 1]; ++t) {
         const int64_t w = where[ci[t]];
         if (w >= 0) {
-          volatile double prod = lik * va[t];  // no contraction into an FMA
-          va[w] = va[w] - prod;
+          va[w] = va[w] - lik * va[t];  // product and difference rounded separately (fp-contract=off)
         }
       }
     }

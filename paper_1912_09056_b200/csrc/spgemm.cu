@@ -596,13 +596,14 @@ std::vector<int64_t> overflow_rows(const int32_t* dflag, int64_t n) {
 // filled with the table size its count pass succeeded with.
 template <class Launch>
 Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint32_t c2_0, double tol,
-              cudaStream_t s, bool start_global = false) {
+              cudaStream_t s, int64_t est_nnz, bool start_global = false) {
   DBuf<int64_t> cnt(n_rows + 1);
   DBuf<int32_t> ovf(n_rows + 1);
   CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
   OutArgs o{cnt.p, nullptr, nullptr, nullptr, ovf.p, tol};
-  // staging buffer: up to 40% of the free memory (<= 16 GB); rows past it
-  // are recomputed by the fill pass (CAMG_SPGEMM_STAGE=0 disables)
+  // staging buffer: the caller's output estimate, at most 40% of the free
+  // memory and 16 GB; rows past it are recomputed by the fill pass
+  // (CAMG_SPGEMM_STAGE=0 disables)
   DBuf<int32_t> scol;
   DBuf<double> sval;
   DBuf<int64_t> soff;
@@ -611,7 +612,8 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
     const char* e = getenv("CAMG_SPGEMM_STAGE");
     size_t fr = 0, tot = 0;
     CAMG_CUDA(cudaMemGetInfo(&fr, &tot));
-    const int64_t cap = std::min<int64_t>((int64_t)(0.4 * (double)fr) / 12, (int64_t(16) << 30) / 12);
+    const int64_t cap = std::min<int64_t>(std::min<int64_t>((int64_t)(0.4 * (double)fr) / 12, (int64_t(16) << 30) / 12),
+                                          std::max<int64_t>(est_nnz, int64_t(1) << 16));
     if (!(e && e[0] == '0') && n_rows > 0 && cap > 0) {
       scol = DBuf<int32_t>(cap);
       sval = DBuf<double>(cap);
@@ -754,7 +756,8 @@ Csr* spgemm_ex(const Csr* A, const Csr* B, bool reverse_a, double tol, cudaStrea
     }
     CAMG_LAUNCH_CHECK();
   };
-  return two_pass(A->n_rows, B->n_cols, launch, 2 * capp, 0, tol, s);
+  // output estimate: 2 (nnz(A) + nnz(B)) (D^-1 K P_tent: 0.4x; S~ products: small)
+  return two_pass(A->n_rows, B->n_cols, launch, 2 * capp, 0, tol, s, 2 * (A->nnz + B->nnz));
 }
 
 Csr* spgemm(const Csr* A, const Csr* B, cudaStream_t s) { return spgemm_ex(A, B, false, kDropTol, s, nullptr); }
@@ -794,6 +797,9 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
     }
     CAMG_LAUNCH_CHECK();
   };
+  // output estimate for the staging buffer: nnz(R) + nnz(A) + nnz(P) (C5
+  // level 0: 2.8e9 for a 0.28e9-entry coarse K)
+  const int64_t est = R->nnz + A->nnz + P->nnz;
   static int rap_global = -1;
   if (rap_global < 0) {
     const char* e = getenv("CAMG_RAP_GLOBAL");
@@ -803,8 +809,8 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
   // row) start in the global-memory tables: L2-resident, ~28 warps per SM
   // against 6 with shared-memory tables (C5: 7.0 s -> 4.7 s)
   if (rap_global && R->avg_row * A->avg_row > 4096.0)
-    return two_pass(R->n_rows, P->n_cols, launch, cap1, cap2, kDropTol, s, true);
-  return two_pass(R->n_rows, P->n_cols, launch, 2 * cap1, 2 * cap2, kDropTol, s);
+    return two_pass(R->n_rows, P->n_cols, launch, cap1, cap2, kDropTol, s, est, true);
+  return two_pass(R->n_rows, P->n_cols, launch, 2 * cap1, 2 * cap2, kDropTol, s, est);
 }
 
 }  // namespace camg
