@@ -1,5 +1,6 @@
 """C5 level-0 K-block Galerkin product: time and a digest of the result
-(run with CAMG_RAP_MULTI=0/1 to compare the multi-row and single-row paths)."""
+(compare digests across builds; the multi-row variant this was written for,
+CAMG_RAP_MULTI, measured slower and was removed -- DESIGN.md §5)."""
 import hashlib, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
