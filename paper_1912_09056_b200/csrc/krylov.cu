@@ -7,7 +7,13 @@
 // into one streaming multi-vector kernel.  Three passes over the Krylov basis
 // per iteration:  h1 = V^T w ;  w -= V h1 fused with h2 = V^T w ;
 // w -= V h2 fused with ||w||^2.  One host synchronisation per iteration.
+//
+// The preconditioned vectors z_j = M^-1 v_j each iteration computes anyway
+// are kept (Z, n x m, when the device has room), so a restart cycle ends
+// with x += Z y instead of x += M^-1 (V y): one V-cycle less per cycle.  The
+// V-cycle is linear, so the iterates are the reference's up to rounding.
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -141,10 +147,18 @@ __global__ void k_add(int64_t n, const double* __restrict__ a, double* __restric
 struct Gmres {
   int64_t n;
   int m;
-  DBuf<double> V, w, z, r, u, part, hdev;
+  DBuf<double> V, Z, w, z, r, u, part, hdev;
   double* hhost = nullptr;
   Gmres(int64_t n_, int m_) : n(n_), m(m_) {
     V = DBuf<double>((size_t)n * (m + 1));
+    {
+      // Z only with 4 GB to spare (CAMG_GMRES_STORE_Z=0 disables)
+      const char* e = getenv("CAMG_GMRES_STORE_Z");
+      size_t fr = 0, tot = 0;
+      CAMG_CUDA(cudaMemGetInfo(&fr, &tot));
+      const size_t need = sizeof(double) * (size_t)n * m;
+      if (!(e && e[0] == '0') && fr > need + (size_t(4) << 30)) Z = DBuf<double>((size_t)n * m);
+    }
     w = DBuf<double>(n);
     z = DBuf<double>(n);
     r = DBuf<double>(n);
@@ -223,10 +237,12 @@ void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rt
     note_launch();
     k_scale_into<<<grid_for(n, 256), 256, 0, s>>>(n, G.r.p, beta, G.V.p);
     int used = 0;
+    const bool keep_z = H && G.Z.p;
     for (int j = 0; j < m; ++j) {
       const double* vj = G.V.p + (int64_t)j * n;
-      G.precond(H, vj, G.z.p, s);
-      spmv(A, 1.0, G.z.p, 0.0, G.w.p, s);
+      double* zj = keep_z ? G.Z.p + (int64_t)j * n : G.z.p;
+      G.precond(H, vj, zj, s);
+      spmv(A, 1.0, zj, 0.0, G.w.p, s);
       const int k = j + 1;
       double* h1 = G.hdev.p;
       double* h2 = G.hdev.p + (m + 2);
@@ -269,8 +285,14 @@ void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rt
     }
     CAMG_CUDA(cudaMemcpyAsync(G.hdev.p, y.data(), sizeof(double) * used, cudaMemcpyHostToDevice, s));
     note_launch();
-    k_lincomb<<<grid_for(n, 256), 256, sizeof(double) * used, s>>>(G.V.p, n, used, n, G.hdev.p, G.u.p);
-    G.precond(H, G.u.p, G.z.p, s);
+    if (keep_z) {
+      // x += Z y
+      k_lincomb<<<grid_for(n, 256), 256, sizeof(double) * used, s>>>(G.Z.p, n, used, n, G.hdev.p, G.z.p);
+    } else {
+      // x += M^-1 (V y)
+      k_lincomb<<<grid_for(n, 256), 256, sizeof(double) * used, s>>>(G.V.p, n, used, n, G.hdev.p, G.u.p);
+      G.precond(H, G.u.p, G.z.p, s);
+    }
     note_launch();
     k_add<<<grid_for(n, 256), 256, 0, s>>>(n, G.z.p, x);
     G.residual(A, b, x, G.r.p, s);
