@@ -223,9 +223,17 @@ void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rt
   }
   const double target = rtol * norm_b;
   std::vector<double> Hm, cs, sn, g, y;
+  bool first = true;
   while (total < max_iters && !conv) {
-    G.residual(A, b, x, G.r.p, s);
-    const double beta = G.norm(G.r.p, s);
+    // x0 = 0: the first residual is b and its norm is known
+    double beta = norm_b;
+    if (first) {
+      CAMG_CUDA(cudaMemcpyAsync(G.r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    } else {
+      G.residual(A, b, x, G.r.p, s);
+      beta = G.norm(G.r.p, s);
+    }
+    first = false;
     if (beta <= target) { conv = true; break; }
     const int m = std::min(restart, max_iters - total);
     Hm.assign((size_t)(m + 1) * m, 0.0);
