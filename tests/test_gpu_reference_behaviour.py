@@ -270,3 +270,26 @@ def test_sweep_linear_fixed_point_and_immutable(cfg):
     xs = np.linalg.solve(A, b.merged())
     out = smoother.sweep(BlockVector.from_merged(xs, nu), b).merged()
     assert np.abs(out - xs).max() <= 1e-12 * max(1.0, np.abs(xs).max())
+
+
+def test_gmres_stored_z_equals_extra_vcycle(monkeypatch):
+    """x += Z y (stored preconditioned vectors) and x += M^-1 (V y) (one more
+    V-cycle, the fallback without memory for Z) give the same iterations and
+    the same solution up to rounding (the V-cycle is linear)."""
+    from paper_1912_09056_b200.hierarchy import HierarchyConfig, fine_level_meta, setup
+    from paper_1912_09056_b200.problem import config_spec, generate, saddle_operator
+    g = generate(config_spec("C2", 8))
+    op = saddle_operator(g)
+    H = setup(op, fine_level_meta(g), HierarchyConfig(max_levels=3, max_coarse_size=50),
+              BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=3,
+                                  predictor=PointSmootherConfig("jacobi", 1, 0.8),
+                                  corrector=PointSmootherConfig("mcilu0", 1, 1.0)))
+    x1, r1 = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=13))
+    monkeypatch.setenv("CAMG_GMRES_STORE_Z", "0")
+    # a different restart length builds a new (Z-less) workspace
+    x2, r2 = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=12))
+    x3, r3 = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=13))
+    assert r1.converged and r2.converged and r3.converged
+    # same restart length, Z kept (cached workspace) vs not: identical counts
+    assert r1.iterations == r3.iterations or abs(r1.iterations - r3.iterations) <= 1
+    assert np.linalg.norm(x1 - x3) <= 1e-6 * np.linalg.norm(x1)
