@@ -519,6 +519,20 @@ static int64_t quad_slices() {
   return v;
 }
 
+// grid cap of the one-lane-per-row kernels in CTAs per SM (CAMG_SELL_CTAS):
+// 64 (~3 slices per warp on the C5 fine level, short CTAs that rebalance
+// the per-SM load) beats 16 (~13 slices per warp): fine predictor pass
+// 2.154 -> 2.113 ms, V-cycle 20.0 -> 19.8 ms; 4 (persistent), 8, 32, 48, 96,
+// 128 measured in between or slower
+static int64_t sell_ctas_per_sm() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("CAMG_SELL_CTAS");
+    v = e ? atoll(e) : 64;
+  }
+  return v;
+}
+
 // read per call (build and capture time only): tests switch it per case
 static int64_t pair_slices() {
   const char* e = getenv("CAMG_SELL_PAIR");
@@ -545,7 +559,7 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   // rows with many blocks (R = P^T: ~117 6x3 blocks per coarse node) split
   // over four lanes, short ones over two
   const bool long_rows = S->nbr > 0 && S->used_blocks >= quad_min_blocks() * S->nbr;
-  const unsigned grid = grid_for(nw * 32, 256, int64_t(kNumSMs) * 16);
+  const unsigned grid = grid_for(nw * 32, 256, int64_t(kNumSMs) * sell_ctas_per_sm());
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
   note_launch();
