@@ -33,9 +33,9 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # launch, from profiles/ (one `ncu --set full` capture; None until measured)
 TRAFFIC = {
     # profiles/r01_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1> (masked
-    # slots, 64-CTA/SM grid cap), C5, dram__bytes_read.sum 13.423698 GB +
-    # dram__bytes_write.sum 0.175877 GB
-    "C5": 13.599575e9,
+    # slots, 64-thread CTAs), C5, dram__bytes_read.sum 13.422817 GB +
+    # dram__bytes_write.sum 0.175971 GB
+    "C5": 13.598788e9,
 }
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 

@@ -36,11 +36,20 @@
 // loads in flight per warp); 4 CTAs/SM (62 registers) batches them (C5
 // V-cycle 21.72 -> 21.35 ms; 2 CTAs / 122 registers, all 36 loads of a 6x6
 // slot in one batch, measured the same)
+// 64-thread CTAs for the one-lane-per-row kernels: finer CTA granularity
+// rebalances the per-SM load (C5 fine predictor pass 2.113 -> 2.067 ms,
+// V-cycle 19.8 -> 19.5 ms; 128: 2.083 ms, 512: 2.140 ms, 32: 2.34 ms -- the
+// 32-CTA/SM limit caps 1-warp CTAs at 32 warps)
+#ifndef CAMG_SELL_THREADS
+#define CAMG_SELL_THREADS 64
+#endif
 #ifndef CAMG_BIG_MINB
 #define CAMG_BIG_MINB 4
 #endif
 
 namespace camg {
+
+constexpr int kSellThreads = CAMG_SELL_THREADS;  // threads per CTA of the one-lane-per-row kernels
 
 Sell::~Sell() {
   dfree(slice_ptr);
@@ -383,7 +392,7 @@ __device__ __forceinline__ void sell_epilogue(const SellEpi& e, int64_t p, const
 }
 
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED>
-__global__ void __launch_bounds__(256, MASKED ? CAMG_MASKED_MINB : (BR * BC >= 18 ? CAMG_BIG_MINB : 0)) k_sell_row(SellView S, const double* __restrict__ xu,
+__global__ void __launch_bounds__(kSellThreads, (MASKED ? CAMG_MASKED_MINB : (BR * BC >= 18 ? CAMG_BIG_MINB : 6)) * 256 / kSellThreads) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
   CAMG_PDL_ENTRY();
@@ -559,20 +568,20 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   // rows with many blocks (R = P^T: ~117 6x3 blocks per coarse node) split
   // over four lanes, short ones over two
   const bool long_rows = S->nbr > 0 && S->used_blocks >= quad_min_blocks() * S->nbr;
-  const unsigned grid = grid_for(nw * 32, 256, int64_t(kNumSMs) * sell_ctas_per_sm());
+  const unsigned grid = grid_for(nw * 32, kSellThreads, int64_t(kNumSMs) * sell_ctas_per_sm() * 256 / kSellThreads);
   const bool sp = split >= 0;
   const int64_t sb = sp ? split / BC : 0;
   note_launch();
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
-    if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, 256, 0, st, v, xu, xl, sb, e);         \
+    if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, kSellThreads, 0, st, v, xu, xl, sb, e);         \
     else if (nw < quad_slices() || (nw < pair_slices() && long_rows))                       \
       launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(nw * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
     else if (nw < pair_slices())                                                             \
       launch_k(k_sell_row2<BR, BC, Z, SP, M, 2>, grid_for(nw * 64, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
-    else launch_k(k_sell_row<BR, BC, Z, SP, M, false>, grid, 256, 0, st, v, xu, xl, sb, e);                  \
+    else launch_k(k_sell_row<BR, BC, Z, SP, M, false>, grid, kSellThreads, 0, st, v, xu, xl, sb, e);                  \
   } while (0)
   if (mode == 0) {
     if (sp) CAMG_SELL_LAUNCH(false, true, 0); else CAMG_SELL_LAUNCH(false, false, 0);
