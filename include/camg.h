@@ -54,6 +54,8 @@ typedef struct camg_csr camg_csr;
 typedef struct camg_level camg_level;
 typedef struct camg_hierarchy camg_hierarchy;
 typedef struct camg_scalar_hierarchy camg_scalar_hierarchy;
+typedef struct camg_vcycle_workspace camg_vcycle_workspace;
+typedef struct camg_gmres_workspace camg_gmres_workspace;
 
 typedef struct {
   int kind;           /* CAMG_UZAWA .. CAMG_SIMPLEC                 (BlockSmootherConfig.kind)   */
@@ -69,6 +71,31 @@ typedef struct {
   int node_block;     /* DOFs per displacement node of the level (uniform contiguous blocks;
                          1 = none): the node colouring of a CAMG_PT_MCGS predictor on K          */
 } camg_smoother_cfg;
+
+/* execution paths reported by camg_level_get_info (which kernels a level's
+ * smoother runs; several engage only above size thresholds) */
+#define CAMG_PATH_NONE 0
+#define CAMG_PATH_FUSED 1         /* Jacobi / Chebyshev sweeps fused into the row passes */
+#define CAMG_PATH_DENSE_LU 2      /* dense LU solve (direct corrector)                    */
+#define CAMG_PATH_COLOUR_CSR 3    /* one launch per colour (and direction), CSR rows      */
+#define CAMG_PATH_COLOUR_SELL 4   /* one launch per colour over a colour-ordered block SELL */
+#define CAMG_PATH_CTA 5           /* whole sweeps in one CTA                              */
+#define CAMG_PATH_CLUSTER 6       /* whole sweeps on one 16-CTA thread-block cluster      */
+#define CAMG_PATH_INNER_AMG 7     /* nested preconditioner: scalar AMG V-cycle predictor  */
+
+typedef struct {
+  int64_t n_u, n_lam, nnz;     /* merged operator of the level                                   */
+  int sell_block;              /* node-block SELL-32 mirror of the [K | B1] rows: block size, 0 = CSR */
+  int sell_masked;             /* 1: masked slots (only the union pattern of a slot stored)     */
+  int sell_lanes;              /* lanes per block row of a pass: 1, 2 (pairs) or 4              */
+  int64_t sell_rows, sell_slices;
+  int overlap;                 /* lambda-side chain overlapped with the next [K | B1] pass      */
+  int64_t overlap_indep_slices, overlap_dep_slices;
+  int pred_path, pred_colors;  /* CAMG_PATH_* of the predictor on K                             */
+  int corr_path, corr_colors;  /* CAMG_PATH_* of the corrector on S~                            */
+  int transfer_block_rows;     /* P has a br x bc block SELL mirror: br (0 = CSR)               */
+  int restrict_block_rows;     /* R = P^T has one: its block rows (0 = CSR)                     */
+} camg_level_info;
 
 /* ---- library ------------------------------------------------------------ */
 const char* camg_last_error(void);
@@ -217,6 +244,20 @@ int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu_
 int camg_hierarchy_destroy(camg_hierarchy* H);
 /* one V-cycle from zero: z = M^-1 r  (Hierarchy.apply, hierarchy.py:115-120) */
 int camg_vcycle(camg_hierarchy* H, const double* r, double* z, void* stream);
+/* Re-entrant application (a built hierarchy may be applied
+ * concurrently to independent right-hand sides, each application owning its
+ * work vectors; hierarchy.py:115-120).  A workspace owns private copies of
+ * every vector a V-cycle writes plus its own CUDA graph and stream; cycles on
+ * different workspaces may run concurrently (different caller streams or
+ * threads).  camg_vcycle uses the hierarchy's own (default) workspace.       */
+int camg_vcycle_workspace_create(camg_hierarchy* H, camg_vcycle_workspace** out);
+int camg_vcycle_workspace_destroy(camg_vcycle_workspace* ws);
+/* z = M^-1 r on workspace ws (NULL = the default workspace) */
+int camg_vcycle_ws(camg_hierarchy* H, camg_vcycle_workspace* ws, const double* r, double* z, void* stream);
+/* kernels in one recorded V-cycle graph (-1 before the first camg_vcycle) */
+int camg_hierarchy_kernels_per_cycle(camg_hierarchy* H, int64_t* kernels);
+/* execution paths and formats a level's smoother uses (see camg_level_info) */
+int camg_level_get_info(const camg_level* L, camg_level_info* info);
 /* enable/disable CUDA-graph replay of the V-cycle (default on) */
 int camg_hierarchy_use_graph(camg_hierarchy* H, int enable);
 /* algorithmic bytes of one V-cycle (SURVEY.md §8(d) model) */
@@ -249,6 +290,31 @@ int camg_level_set_predictor_solver(camg_level* L, camg_scalar_hierarchy* inner)
 int camg_gmres(const camg_csr* A, camg_hierarchy* H, const double* b, double* x, double rel_tol,
                int max_iters, int restart, int* iterations, double* history, int* converged,
                void* stream);
+/* camg_gmres keeps its Krylov basis (n x (restart+1)) and the stored
+ * preconditioned vectors Z (n x restart, when 4 GB remain free) cached per
+ * thread for later solves of the same size; this frees that cache.          */
+int camg_gmres_release(void);
+/* caller-owned GMRES workspace for systems of n rows and restart length
+ * `restart` (re-entrant solves); store_z: 1 keep Z (x += Z y at
+ * the end of a restart cycle, no extra V-cycle), 0 recompute, -1 keep Z when
+ * 4 GB of device memory remain free at each solve                           */
+int camg_gmres_workspace_create(int64_t n, int restart, int store_z, camg_gmres_workspace** out);
+int camg_gmres_workspace_destroy(camg_gmres_workspace* ws);
+/* caller-supplied linear map y = f(x) on device vectors of the solve's
+ * length, enqueued on `stream`; returns 0 on success (the solve stops with
+ * CAMG_ERR_NATIVE otherwise).  krylov.py:45's `apply_A` / `apply_Minv`
+ * callables.                                                                 */
+typedef int (*camg_apply_fn)(void* user, const double* x, double* y, void* stream);
+/* general form of camg_gmres (krylov.py:45-129) for n unknowns: the operator
+ * is the device matrix A or the callback apply_A (exactly one); the
+ * preconditioner is a V-cycle of H on the V-cycle workspace vws (NULL = its
+ * default), or one block-smoother sweep from zero of level L (the nested
+ * preconditioner, hierarchy.py:366-376), or the callback apply_M, or none
+ * (at most one).  gws NULL = the per-thread cache.                           */
+int camg_gmres_ex(int64_t n, const camg_csr* A, camg_apply_fn apply_A, void* user_A, camg_hierarchy* H,
+                  camg_vcycle_workspace* vws, camg_level* L, camg_apply_fn apply_M, void* user_M,
+                  camg_gmres_workspace* gws, const double* b, double* x, double rel_tol, int max_iters,
+                  int restart, int* iterations, double* history, int* converged, void* stream);
 
 /* ---- dense vector helpers (device) ---------------------------------------- */
 int camg_dot(int64_t n, const double* x, const double* y, double* result, void* stream);

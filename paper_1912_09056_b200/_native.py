@@ -38,6 +38,32 @@ class SmootherCfg(C.Structure):
     ]
 
 
+# camg_apply_fn: int (*)(void* user, const double* x, double* y, void* stream)
+APPLY_FN = C.CFUNCTYPE(C.c_int, vp, vp, vp, vp)
+
+
+class LevelInfo(C.Structure):
+    """camg_level_info: formats and execution paths of one level's smoother."""
+    _fields_ = [
+        ("n_u", i64), ("n_lam", i64), ("nnz", i64),
+        ("sell_block", C.c_int), ("sell_masked", C.c_int), ("sell_lanes", C.c_int),
+        ("sell_rows", i64), ("sell_slices", i64),
+        ("overlap", C.c_int), ("overlap_indep_slices", i64), ("overlap_dep_slices", i64),
+        ("pred_path", C.c_int), ("pred_colors", C.c_int), ("corr_path", C.c_int), ("corr_colors", C.c_int),
+        ("transfer_block_rows", C.c_int), ("restrict_block_rows", C.c_int),
+    ]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["pred_path"] = PATHS[d["pred_path"]]
+        d["corr_path"] = PATHS[d["corr_path"]]
+        return d
+
+
+# CAMG_PATH_* (include/camg.h)
+PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg")
+
+
 _SIGS = {
     "camg_last_error": (C.c_char_p, []),
     "camg_version": (C.c_int, []),
@@ -97,6 +123,16 @@ _SIGS = {
     "camg_hierarchy_vcycle_bytes": (C.c_int, [vp, C.POINTER(f64), C.POINTER(f64)]),
     "camg_gmres": (C.c_int, [vp, vp, vp, vp, f64, C.c_int, C.c_int, C.POINTER(C.c_int), vp,
                              C.POINTER(C.c_int), vp]),
+    "camg_gmres_ex": (C.c_int, [i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, f64, C.c_int, C.c_int,
+                                C.POINTER(C.c_int), vp, C.POINTER(C.c_int), vp]),
+    "camg_gmres_release": (C.c_int, []),
+    "camg_gmres_workspace_create": (C.c_int, [i64, C.c_int, C.c_int, C.POINTER(vp)]),
+    "camg_gmres_workspace_destroy": (C.c_int, [vp]),
+    "camg_vcycle_workspace_create": (C.c_int, [vp, C.POINTER(vp)]),
+    "camg_vcycle_workspace_destroy": (C.c_int, [vp]),
+    "camg_vcycle_ws": (C.c_int, [vp, vp, vp, vp, vp]),
+    "camg_hierarchy_kernels_per_cycle": (C.c_int, [vp, P64]),
+    "camg_level_get_info": (C.c_int, [vp, C.POINTER(LevelInfo)]),
     "camg_dot": (C.c_int, [i64, vp, vp, C.POINTER(f64), vp]),
     "camg_axpy": (C.c_int, [i64, f64, vp, vp, vp]),
 }

@@ -141,8 +141,10 @@ constexpr int kNumSMs = 148;
 }  // namespace camg
 
 // opaque handle types exposed through the C ABI
-namespace camg { struct Level; struct Hierarchy; struct ScalarHier; }
+namespace camg { struct Level; struct Hierarchy; struct ScalarHier; struct VcycleWs; struct Gmres; }
 struct camg_csr { camg::Csr* m; };
 struct camg_level { camg::Level* L; };
 struct camg_hierarchy { camg::Hierarchy* H; };
 struct camg_scalar_hierarchy { camg::ScalarHier* H; };
+struct camg_vcycle_workspace { camg::VcycleWs* W; camg::Hierarchy* H; };
+struct camg_gmres_workspace { camg::Gmres* G; };

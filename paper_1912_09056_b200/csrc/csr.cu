@@ -17,6 +17,7 @@ namespace camg {
 
 static thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
+thread_local int64_t g_thread_launches = 0;
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 

@@ -13,6 +13,7 @@
 #include <memory>
 #include <string>
 #include <utility>
+#include <mutex>
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -1394,6 +1395,7 @@ __global__ void k_pred_update(int64_t n, const double* __restrict__ x, const dou
 
 struct ScalarHier;
 const double* scalar_run(ScalarHier* H, const double* b, cudaStream_t s);
+void scalar_work_slots(ScalarHier* H, std::vector<DBuf<double>*>& v);
 
 // ---------------------------------------------------------------------------
 // level
@@ -1911,6 +1913,35 @@ void shift_copy(const int64_t* rp, int64_t n, int64_t add, int64_t* out, const i
 // ---------------------------------------------------------------------------
 // hierarchy
 
+// A V-cycle workspace: the work vectors of one caller plus the CUDA graph
+// recorded over them.  A built hierarchy "may be applied concurrently to
+// independent right-hand sides, each application owning its work vectors"
+// (SPEC.md:526): every workspace owns a private copy of every vector the
+// cycle writes (per-level rhs / iterates / residuals, the smoother's step
+// vectors, the multicolour and ILU(0) solve vectors, an inner scalar
+// hierarchy's vectors) and its own graph, stream and events, so cycles on
+// different workspaces may run at the same time on different streams.  The
+// operators, factors and colourings are shared and read-only.  The graph is
+// recorded with the workspace's vectors bound in place of the hierarchy's
+// own (swapped in under a process-wide lock for the capture only).
+struct VcycleWs {
+  std::vector<DBuf<double>> bufs;  // one per Hierarchy::work_slots() entry (owned == true)
+  bool owned = false;              // false: the hierarchy's own vectors (default workspace)
+  DBuf<double> in, out;            // level-0 rhs / result bound into the graph
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int64_t kernels = 0;
+  ~VcycleWs() {
+    if (graph) cudaGraphExecDestroy(graph);
+    if (stream) cudaStreamDestroy(stream);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+};
+
+static std::mutex g_capture_mu;
+
 struct Hierarchy {
   std::vector<Level*> levels;
   int coarse_solver = CAMG_COARSE_MERGED_LU;
@@ -1919,17 +1950,21 @@ struct Hierarchy {
   int64_t n_coarse = 0;
   // per-level vectors: b (rhs), x[2]
   std::vector<DBuf<double>> vb, vx0, vx1, vr;
-  cudaStream_t stream = nullptr;
-  cudaGraphExec_t graph = nullptr;
-  int64_t kernels_in_graph = 0;
   bool use_graph = true;
-  DBuf<double> in, out;  // level-0 rhs / result buffers used by the graph
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  ~Hierarchy() {
-    if (graph) cudaGraphExecDestroy(graph);
-    if (stream) cudaStreamDestroy(stream);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
+  VcycleWs def;  // workspace of camg_vcycle (the hierarchy's own vectors)
+
+  // every device vector a V-cycle writes (the per-call state of a workspace)
+  std::vector<DBuf<double>*> work_slots() {
+    std::vector<DBuf<double>*> v;
+    for (size_t l = 0; l < levels.size(); ++l) {
+      Level* L = levels[l];
+      for (DBuf<double>* b : {&vb[l], &vx0[l], &vx1[l], &vr[l], &L->w_du, &L->w_du2, &L->w_ru, &L->w_rc, &L->w_dl,
+                              &L->w_dl2, &L->w_rl, &L->w_tmp, &L->w_cd[0], &L->w_cd[1], &L->gs.g, &L->cgs.g,
+                              &L->cilu.y, &L->cilu.z})
+        v.push_back(b);
+      if (L->inner) scalar_work_slots(L->inner, v);
+    }
+    return v;
   }
 
   void coarse_solve(const double* b, double* x, cudaStream_t s) {
@@ -1987,39 +2022,76 @@ struct Hierarchy {
     CAMG_CUDA(cudaMemcpyAsync(z, res, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
 
-  void apply(const double* r, double* z, cudaStream_t caller) {
+  // a fresh workspace with private copies of every work vector
+  VcycleWs* make_ws() {
+    std::unique_ptr<VcycleWs> w(new VcycleWs());
+    w->owned = true;
+    for (DBuf<double>* b : work_slots()) w->bufs.emplace_back(b->p ? DBuf<double>(b->n) : DBuf<double>());
+    return w.release();
+  }
+
+  // record the cycle over w's vectors into w's graph
+  void capture(VcycleWs& w) {
     const int64_t n = levels[0]->n;
-    if (!use_graph) {
+    if (!w.stream) {
+      CAMG_CUDA(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+      CAMG_CUDA(cudaEventCreateWithFlags(&w.ev0, cudaEventDisableTiming));
+      CAMG_CUDA(cudaEventCreateWithFlags(&w.ev1, cudaEventDisableTiming));
+      w.in = DBuf<double>(n);
+      w.out = DBuf<double>(n);
+    }
+    std::lock_guard<std::mutex> lk(g_capture_mu);
+    std::vector<DBuf<double>*> slots;
+    if (w.owned) {
+      slots = work_slots();
+      CAMG_CHECK(slots.size() == w.bufs.size(), CAMG_ERR_NATIVE, "workspace does not match the hierarchy");
+    }
+    struct Swap {  // bind w's vectors for the capture, restore on every exit
+      std::vector<DBuf<double>*>& s;
+      std::vector<DBuf<double>>& b;
+      Swap(std::vector<DBuf<double>*>& s_, std::vector<DBuf<double>>& b_) : s(s_), b(b_) { flip(); }
+      ~Swap() { flip(); }
+      void flip() { for (size_t i = 0; i < s.size(); ++i) std::swap(*s[i], b[i]); }
+    } bind(slots, w.bufs);
+    cudaGraph_t g;
+    CAMG_CUDA(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = g_thread_launches;
+    try {
+      run(w.in.p, w.out.p, w.stream);
+    } catch (...) {
+      cudaStreamEndCapture(w.stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    w.kernels = g_thread_launches - before;
+    g_launches.fetch_sub(w.kernels);
+    g_thread_launches -= w.kernels;
+    CAMG_CUDA(cudaStreamEndCapture(w.stream, &g));
+    CAMG_CUDA(cudaGraphInstantiate(&w.graph, g, 0));
+    cudaGraphDestroy(g);
+  }
+
+  void apply_ws(VcycleWs& w, const double* r, double* z, cudaStream_t caller) {
+    const int64_t n = levels[0]->n;
+    if (!w.graph) capture(w);
+    CAMG_CUDA(cudaMemcpyAsync(w.in.p, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
+    CAMG_CUDA(cudaEventRecord(w.ev0, caller));
+    CAMG_CUDA(cudaStreamWaitEvent(w.stream, w.ev0, 0));
+    note_launch((int)w.kernels);
+    CAMG_CUDA(cudaGraphLaunch(w.graph, w.stream));
+    CAMG_CUDA(cudaEventRecord(w.ev1, w.stream));
+    CAMG_CUDA(cudaStreamWaitEvent(caller, w.ev1, 0));
+    CAMG_CUDA(cudaMemcpyAsync(z, w.out.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
+  }
+
+  void apply(const double* r, double* z, cudaStream_t caller) {
+    if (!use_graph) {  // eager launches over the hierarchy's own vectors (not re-entrant)
+      std::lock_guard<std::mutex> lk(g_capture_mu);
       run(r, z, caller);
       CAMG_LAUNCH_CHECK();
       return;
     }
-    if (!stream) {
-      CAMG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-      CAMG_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
-      CAMG_CUDA(cudaEventCreateWithFlags(&ev1, cudaEventDisableTiming));
-      in = DBuf<double>(n);
-      out = DBuf<double>(n);
-    }
-    if (!graph) {
-      cudaGraph_t g;
-      CAMG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      const int64_t before = g_launches.load();
-      run(in.p, out.p, stream);
-      kernels_in_graph = g_launches.load() - before;
-      g_launches.fetch_sub(kernels_in_graph);
-      CAMG_CUDA(cudaStreamEndCapture(stream, &g));
-      CAMG_CUDA(cudaGraphInstantiate(&graph, g, 0));
-      cudaGraphDestroy(g);
-    }
-    CAMG_CUDA(cudaMemcpyAsync(in.p, r, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
-    CAMG_CUDA(cudaEventRecord(ev0, caller));
-    CAMG_CUDA(cudaStreamWaitEvent(stream, ev0, 0));
-    note_launch((int)kernels_in_graph);
-    CAMG_CUDA(cudaGraphLaunch(graph, stream));
-    CAMG_CUDA(cudaEventRecord(ev1, stream));
-    CAMG_CUDA(cudaStreamWaitEvent(caller, ev1, 0));
-    CAMG_CUDA(cudaMemcpyAsync(z, out.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, caller));
+    apply_ws(def, r, z, caller);
   }
 };
 
@@ -2043,6 +2115,18 @@ Hierarchy* hierarchy_create(Level** lv, int nlev, int coarse_solver) {
 }
 
 void hierarchy_apply(Hierarchy* H, const double* r, double* z, cudaStream_t s) { H->apply(r, z, s); }
+void hierarchy_apply_ws(Hierarchy* H, VcycleWs* w, const double* r, double* z, cudaStream_t s) {
+  if (w) H->apply_ws(*w, r, z, s);
+  else H->apply(r, z, s);
+}
+int64_t hierarchy_rows(const Hierarchy* H) { return H->levels[0]->n; }
+// one BlockSmoother sweep from zero (the nested preconditioner's apply,
+// hierarchy.py:366-376): out = sweep(0, b)
+void level_precond(Level* L, const double* b, double* out, cudaStream_t s) {
+  L->sweep(nullptr, b, out, s);
+  L->join(s);
+}
+int64_t level_rows(const Level* L) { return L->n; }
 
 // ---------------------------------------------------------------------------
 // scalar smoothed-aggregation hierarchy on K (ScalarHierarchy,
@@ -2115,6 +2199,11 @@ struct ScalarHier {
 };
 
 const double* scalar_run(ScalarHier* H, const double* b, cudaStream_t s) { return H->vcycle(0, b, s); }
+
+void scalar_work_slots(ScalarHier* H, std::vector<DBuf<double>*>& v) {
+  for (auto& L : H->levels)
+    for (DBuf<double>* b : {&L->b, &L->x0, &L->x1, &L->r, &L->t, &L->cd[0], &L->cd[1], &L->gs.g}) v.push_back(b);
+}
 
 static ScalarHier* scalar_hierarchy_create(int nlev, const Csr* const* A, const Csr* const* P, const int* node_block,
                                            int kind, int sweeps, double damping) {
@@ -2381,6 +2470,69 @@ int camg_level_set_predictor_solver(camg_level* L, camg_scalar_hierarchy* inner)
       CAMG_CHECK(lv->cfg.kind != CAMG_BRAESS_SARAZIN, CAMG_ERR_CONFIG, "braess_sarazin has no predictor");
     }
     lv->inner = inner ? inner->H : nullptr;
+  });
+}
+
+int camg_vcycle_workspace_create(camg_hierarchy* H, camg_vcycle_workspace** out) {
+  return guarded([&] { *out = new camg_vcycle_workspace{H->H->make_ws(), H->H}; });
+}
+
+int camg_vcycle_workspace_destroy(camg_vcycle_workspace* W) {
+  return guarded([&] {
+    if (W) { delete W->W; delete W; }
+  });
+}
+
+int camg_vcycle_ws(camg_hierarchy* H, camg_vcycle_workspace* W, const double* r, double* z, void* stream) {
+  return guarded([&] {
+    CAMG_CHECK(!W || W->H == H->H, CAMG_ERR_ARG, "workspace belongs to another hierarchy");
+    hierarchy_apply_ws(H->H, W ? W->W : nullptr, r, z, (cudaStream_t)stream);
+  });
+}
+
+int camg_hierarchy_kernels_per_cycle(camg_hierarchy* H, int64_t* kernels) {
+  return guarded([&] { *kernels = H->H->def.graph ? H->H->def.kernels : -1; });
+}
+
+int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
+  return guarded([&] {
+    const Level* L = Lh->L;
+    camg_level_info o{};
+    o.n_u = L->nu;
+    o.n_lam = L->nl;
+    o.nnz = L->A->nnz;
+    const Sell* S = L->A->sell;
+    if (S) {
+      o.sell_block = S->br;
+      o.sell_rows = S->rows();
+      o.sell_masked = S->masked ? 1 : 0;
+      o.sell_lanes = sell_lanes(S);
+      o.sell_slices = S->nslices;
+    }
+    o.overlap = L->overlap ? 1 : 0;
+    o.overlap_indep_slices = L->n_indep;
+    o.overlap_dep_slices = L->n_dep;
+    const camg_smoother_cfg& c = L->cfg;
+    auto mc_path = [](const McgsK& g) {
+      return g.cl ? CAMG_PATH_CLUSTER : g.cta ? CAMG_PATH_CTA : g.sell ? CAMG_PATH_COLOUR_SELL : CAMG_PATH_COLOUR_CSR;
+    };
+    if (L->nl == 0) o.corr_path = CAMG_PATH_NONE;
+    else if (c.corr_kind == CAMG_PT_DIRECT) o.corr_path = CAMG_PATH_DENSE_LU;
+    else if (c.corr_kind == CAMG_PT_MCGS) { o.corr_path = mc_path(L->cgs); o.corr_colors = L->cgs.colors(); }
+    else if (c.corr_kind == CAMG_PT_MCILU0) {
+      o.corr_path = (L->cilu.cl && c.corr_sweeps == 1) ? CAMG_PATH_CLUSTER : CAMG_PATH_COLOUR_CSR;
+      o.corr_colors = L->cilu.colors();
+    } else o.corr_path = CAMG_PATH_FUSED;
+    if (L->inner) o.pred_path = CAMG_PATH_INNER_AMG;
+    else if (c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_MCGS) {
+      o.pred_path = mc_path(L->gs);
+      o.pred_colors = L->gs.colors();
+    } else o.pred_path = CAMG_PATH_FUSED;
+    if (L->P) {
+      o.transfer_block_rows = L->P->sell ? L->P->sell->br : 0;
+      o.restrict_block_rows = L->R->sell ? L->R->sell->br : 0;
+    }
+    *info = o;
   });
 }
 

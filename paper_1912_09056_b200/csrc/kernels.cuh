@@ -7,7 +7,12 @@
 namespace camg {
 
 extern std::atomic<int64_t> g_launches;
-inline void note_launch(int n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+// per-thread count (kernels recorded into a graph by this thread's capture)
+extern thread_local int64_t g_thread_launches;
+inline void note_launch(int n = 1) {
+  g_launches.fetch_add(n, std::memory_order_relaxed);
+  g_thread_launches += n;
+}
 
 constexpr double kDropTol = 1e-300;  // sparse.py:21 DROP_TOL
 constexpr int kDotBlocks = 592;      // 4 x 148 SMs

@@ -23,7 +23,12 @@
 namespace camg {
 
 struct Hierarchy;
-void hierarchy_apply(Hierarchy* H, const double* r, double* z, cudaStream_t s);
+struct Level;
+struct VcycleWs;
+void hierarchy_apply_ws(Hierarchy* H, VcycleWs* w, const double* r, double* z, cudaStream_t s);
+int64_t hierarchy_rows(const Hierarchy* H);
+void level_precond(Level* L, const double* b, double* out, cudaStream_t s);
+int64_t level_rows(const Level* L);
 
 namespace {
 
@@ -137,6 +142,11 @@ __global__ void k_scale_into(int64_t n, const double* __restrict__ w, double inv
     v[e] = w[e] / inv;
 }
 
+__global__ void k_sub(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ c) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    c[e] = a[e] - b[e];
+}
+
 __global__ void k_add(int64_t n, const double* __restrict__ a, double* __restrict__ x) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
     x[e] += a[e];
@@ -144,30 +154,72 @@ __global__ void k_add(int64_t n, const double* __restrict__ a, double* __restric
 
 }  // namespace
 
+constexpr int kMaxOrthoK = 2048;  // basis vectors per k_ortho launch (shared memory: 72 B per vector)
+
+static void call_back(camg_apply_fn f, void* user, const double* x, double* y, cudaStream_t s) {
+  const int rc = f(user, x, y, (void*)s);
+  CAMG_CHECK(rc == 0, CAMG_ERR_NATIVE, "gmres: caller-supplied apply callback failed (status " + std::to_string(rc) + ")");
+}
+
+// the operator of a solve: a device matrix or a caller callback y = A x
+struct Operator {
+  const Csr* A = nullptr;
+  camg_apply_fn fn = nullptr;
+  void* user = nullptr;
+  // y = A x
+  void apply(const double* x, double* y, cudaStream_t s) const {
+    if (A) spmv(A, 1.0, x, 0.0, y, s);
+    else call_back(fn, user, x, y, s);
+  }
+};
+
+// the preconditioner of a solve: a V-cycle (on a workspace), one block
+// smoother sweep from zero (nested preconditioner), a caller callback, or none
+struct Precond {
+  Hierarchy* H = nullptr;
+  VcycleWs* ws = nullptr;
+  Level* L = nullptr;
+  camg_apply_fn fn = nullptr;
+  void* user = nullptr;
+  bool any() const { return H || L || fn; }
+  void apply(const double* v, double* out, int64_t n, cudaStream_t s) const {
+    if (H) hierarchy_apply_ws(H, ws, v, out, s);
+    else if (L) level_precond(L, v, out, s);
+    else if (fn) call_back(fn, user, v, out, s);
+    else CAMG_CUDA(cudaMemcpyAsync(out, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+};
+
 struct Gmres {
   int64_t n;
   int m;
+  int store_z;  // 1 keep Z, 0 never, -1 when 4 GB remain free (checked per solve)
   DBuf<double> V, Z, w, z, r, u, part, hdev;
   double* hhost = nullptr;
-  Gmres(int64_t n_, int m_) : n(n_), m(m_) {
+  Gmres(int64_t n_, int m_, int store_z_) : n(n_), m(m_), store_z(store_z_) {
     V = DBuf<double>((size_t)n * (m + 1));
-    {
-      // Z only with 4 GB to spare (CAMG_GMRES_STORE_Z=0 disables)
-      const char* e = getenv("CAMG_GMRES_STORE_Z");
-      size_t fr = 0, tot = 0;
-      CAMG_CUDA(cudaMemGetInfo(&fr, &tot));
-      const size_t need = sizeof(double) * (size_t)n * m;
-      if (!(e && e[0] == '0') && fr > need + (size_t(4) << 30)) Z = DBuf<double>((size_t)n * m);
-    }
     w = DBuf<double>(n);
     z = DBuf<double>(n);
     r = DBuf<double>(n);
     u = DBuf<double>(n);
-    part = DBuf<double>((size_t)kGrid * (m + 2));
+    part = DBuf<double>((size_t)kGrid * (std::min(m, kMaxOrthoK) + 2));
     hdev = DBuf<double>(3 * (m + 2) + 8);
     CAMG_CUDA(cudaMallocHost(&hhost, sizeof(double) * (3 * (m + 2) + 8)));
+    if (store_z == 1) Z = DBuf<double>((size_t)n * m);
   }
   ~Gmres() { if (hhost) cudaFreeHost(hhost); }
+
+  // Z (n x m, the preconditioned basis) when policy and free memory allow;
+  // CAMG_GMRES_STORE_Z=0 disables it for the per-thread cache
+  void ensure_z() {
+    if (store_z != -1 || Z.p) return;
+    const char* e = getenv("CAMG_GMRES_STORE_Z");
+    if (e && e[0] == '0') return;
+    size_t fr = 0, tot = 0;
+    CAMG_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t need = sizeof(double) * (size_t)n * m;
+    if (fr > need + (size_t(4) << 30)) Z = DBuf<double>((size_t)n * m);
+  }
 
   double norm(const double* v, cudaStream_t s) {
     dot_device(n, v, v, hdev.p, part.p, s);
@@ -176,41 +228,75 @@ struct Gmres {
     return std::sqrt(hhost[0]);
   }
 
-  void precond(Hierarchy* H, const double* v, double* out, cudaStream_t s) {
-    if (H) hierarchy_apply(H, v, out, s);
-    else CAMG_CUDA(cudaMemcpyAsync(out, v, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  void residual(const Operator& A, const double* b, const double* x, double* r_, cudaStream_t s) {
+    if (A.A) {
+      CAMG_CUDA(cudaMemcpyAsync(r_, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      spmv(A.A, -1.0, x, 1.0, r_, s);
+      return;
+    }
+    A.apply(x, u.p, s);  // r = b - A x
+    note_launch();
+    k_sub<<<grid_for(n, 256), 256, 0, s>>>(n, b, u.p, r_);
   }
 
-  void residual(const Csr* A, const double* b, const double* x, double* r_, cudaStream_t s) {
-    CAMG_CUDA(cudaMemcpyAsync(r_, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    spmv(A, -1.0, x, 1.0, r_, s);
+  // one k_ortho pass over basis vectors [i0, i0 + k) (k <= kMaxOrthoK)
+  template <int MODE>
+  void ortho_part(int i0, int k, const double* h, double* out, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+      CAMG_CUDA(cudaFuncSetAttribute(k_ortho<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * (kWarps + 1) * kMaxOrthoK)));
+      attr = true;
+    }
+    const int nacc = MODE == 2 ? 1 : k;
+    const size_t sh = sizeof(double) * (kWarps * nacc + k);
+    note_launch(2);
+    k_ortho<MODE><<<kGrid, kBlk, sh, s>>>(V.p + (int64_t)i0 * n, n, k, n, h ? h + i0 : nullptr, w.p, part.p);
+    CAMG_LAUNCH_CHECK();
+    k_reduce_cols<<<std::min(nacc, 1024), 256, 0, s>>>(part.p, kGrid, nacc, out + (MODE == 2 ? 0 : i0));
+    CAMG_LAUNCH_CHECK();
   }
 
+  // MODE 0: out = V^T w; 1: w -= V h, out = V^T w; 2: w -= V h, out[0] = w.w
+  // over the first k basis vectors.  Bases longer than kMaxOrthoK vectors
+  // (restart > 2048) go in chunks: all subtractions first, then the dots.
   template <int MODE>
   void ortho(int k, const double* h, double* out, cudaStream_t s) {
-    const int nacc = MODE == 2 ? 1 : k;
-    size_t sh = sizeof(double) * (kWarps * nacc + k);
-    note_launch(2);
-    k_ortho<MODE><<<kGrid, kBlk, sh, s>>>(V.p, n, k, n, h, w.p, part.p);
-    k_reduce_cols<<<std::min(nacc, 1024), 256, 0, s>>>(part.p, kGrid, nacc, out);
+    if (k <= kMaxOrthoK) return ortho_part<MODE>(0, k, h, out, s);
+    if (MODE != 0)
+      for (int i0 = 0; i0 < k; i0 += kMaxOrthoK) ortho_part<2>(i0, std::min(kMaxOrthoK, k - i0), h, out, s);
+    if (MODE != 2)
+      for (int i0 = 0; i0 < k; i0 += kMaxOrthoK) ortho_part<0>(i0, std::min(kMaxOrthoK, k - i0), nullptr, out, s);
   }
 };
 
-void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rtol, int max_iters, int restart,
-               int* iterations, double* hist, int* converged, cudaStream_t s) {
-  CAMG_CHECK(A->n_rows == A->n_cols, CAMG_ERR_DIMENSION, "gmres: operator must be square");
+static thread_local std::unique_ptr<Gmres> g_gmres_cache;
+
+void gmres_run(int64_t n, const Operator& A, const Precond& M, Gmres* ws, const double* b, double* x, double rtol,
+               int max_iters, int restart, int* iterations, double* hist, int* converged, cudaStream_t s) {
+  if (A.A) {
+    CAMG_CHECK(A.A->n_rows == A.A->n_cols, CAMG_ERR_DIMENSION, "gmres: operator must be square");
+    CAMG_CHECK(A.A->n_rows == n, CAMG_ERR_DIMENSION, "gmres: operator size does not match");
+  }
+  CAMG_CHECK(A.A || A.fn, CAMG_ERR_ARG, "gmres: no operator");
+  CAMG_CHECK(n >= 1, CAMG_ERR_DIMENSION, "gmres: empty system");
   CAMG_CHECK(rtol > 0.0 && rtol < 1.0, CAMG_ERR_CONFIG, "rel_tol must lie in (0, 1)");
   CAMG_CHECK(restart >= 1 && max_iters >= 1, CAMG_ERR_CONFIG, "restart and max_iters must be >= 1");
-  const int64_t n = A->n_rows;
+  if (M.H) CAMG_CHECK(hierarchy_rows(M.H) == n, CAMG_ERR_DIMENSION, "gmres: preconditioner size does not match");
+  if (M.L) CAMG_CHECK(level_rows(M.L) == n, CAMG_ERR_DIMENSION, "gmres: preconditioner size does not match");
   const int mmax = std::min(restart, max_iters);
-  // the Krylov basis (n x (m+1), 19 GB at C5) is allocated once and reused
-  // by later solves of the same size on this thread
-  static thread_local std::unique_ptr<Gmres> cache;
-  if (!cache || cache->n != n || cache->m != mmax) {
-    cache.reset();
-    cache.reset(new Gmres(n, mmax));
+  if (!ws) {
+    // the Krylov basis (n x (m+1), 19 GB at C5) is allocated once and reused
+    // by later solves of the same size on this thread (camg_gmres_release frees it)
+    if (!g_gmres_cache || g_gmres_cache->n != n || g_gmres_cache->m != mmax) {
+      g_gmres_cache.reset();
+      g_gmres_cache.reset(new Gmres(n, mmax, -1));
+    }
+    ws = g_gmres_cache.get();
   }
-  Gmres& G = *cache;
+  CAMG_CHECK(ws->n == n && ws->m >= mmax, CAMG_ERR_DIMENSION, "gmres: workspace is smaller than the solve");
+  if (M.any()) ws->ensure_z();
+  Gmres& G = *ws;
   CAMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
   const double norm_b = G.norm(b, s);
   hist[0] = norm_b;
@@ -245,23 +331,23 @@ void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rt
     note_launch();
     k_scale_into<<<grid_for(n, 256), 256, 0, s>>>(n, G.r.p, beta, G.V.p);
     int used = 0;
-    const bool keep_z = H && G.Z.p;
+    const bool keep_z = M.any() && G.Z.p;
     for (int j = 0; j < m; ++j) {
       const double* vj = G.V.p + (int64_t)j * n;
       double* zj = keep_z ? G.Z.p + (int64_t)j * n : G.z.p;
-      G.precond(H, vj, zj, s);
-      spmv(A, 1.0, zj, 0.0, G.w.p, s);
+      M.apply(vj, zj, n, s);
+      A.apply(zj, G.w.p, s);
       const int k = j + 1;
       double* h1 = G.hdev.p;
-      double* h2 = G.hdev.p + (m + 2);
-      double* nr = G.hdev.p + 2 * (m + 2);
+      double* h2 = G.hdev.p + (G.m + 2);
+      double* nr = G.hdev.p + 2 * (G.m + 2);
       G.ortho<0>(k, nullptr, h1, s);
       G.ortho<1>(k, h1, h2, s);
       G.ortho<2>(k, h2, nr, s);
-      CAMG_CUDA(cudaMemcpyAsync(G.hhost, G.hdev.p, sizeof(double) * (2 * (m + 2) + 1), cudaMemcpyDeviceToHost, s));
+      CAMG_CUDA(cudaMemcpyAsync(G.hhost, G.hdev.p, sizeof(double) * (2 * (G.m + 2) + 1), cudaMemcpyDeviceToHost, s));
       CAMG_CUDA(cudaStreamSynchronize(s));
-      for (int i = 0; i <= j; ++i) Hij(i, j) = G.hhost[i] + G.hhost[(m + 2) + i];
-      Hij(j + 1, j) = std::sqrt(G.hhost[2 * (m + 2)]);
+      for (int i = 0; i <= j; ++i) Hij(i, j) = G.hhost[i] + G.hhost[(G.m + 2) + i];
+      Hij(j + 1, j) = std::sqrt(G.hhost[2 * (G.m + 2)]);
       const bool happy = Hij(j + 1, j) <= 1e-14 * std::max(1.0, std::fabs(Hij(j, j)));
       if (!happy) {
         note_launch();
@@ -299,7 +385,7 @@ void gmres_run(const Csr* A, Hierarchy* H, const double* b, double* x, double rt
     } else {
       // x += M^-1 (V y)
       k_lincomb<<<grid_for(n, 256), 256, sizeof(double) * used, s>>>(G.V.p, n, used, n, G.hdev.p, G.u.p);
-      G.precond(H, G.u.p, G.z.p, s);
+      M.apply(G.u.p, G.z.p, n, s);
     }
     note_launch();
     k_add<<<grid_for(n, 256), 256, 0, s>>>(n, G.z.p, x);
@@ -320,7 +406,53 @@ extern "C" int camg_gmres(const camg_csr* A, camg_hierarchy* H, const double* b,
                           int max_iters, int restart, int* iterations, double* history, int* converged,
                           void* stream) {
   return guarded([&] {
-    gmres_run(A->m, H ? H->H : nullptr, b, x, rel_tol, max_iters, restart, iterations, history, converged,
+    Operator op;
+    op.A = A->m;
+    Precond M;
+    M.H = H ? H->H : nullptr;
+    gmres_run(A->m->n_rows, op, M, nullptr, b, x, rel_tol, max_iters, restart, iterations, history, converged,
               (cudaStream_t)stream);
+  });
+}
+
+extern "C" int camg_gmres_ex(int64_t n, const camg_csr* A, camg_apply_fn apply_A, void* user_A, camg_hierarchy* H,
+                             camg_vcycle_workspace* vws, camg_level* L, camg_apply_fn apply_M, void* user_M,
+                             camg_gmres_workspace* gws, const double* b, double* x, double rel_tol, int max_iters,
+                             int restart, int* iterations, double* history, int* converged, void* stream) {
+  return guarded([&] {
+    CAMG_CHECK((A != nullptr) != (apply_A != nullptr), CAMG_ERR_ARG, "gmres: give exactly one of A and apply_A");
+    CAMG_CHECK((H != nullptr) + (L != nullptr) + (apply_M != nullptr) <= 1, CAMG_ERR_ARG,
+               "gmres: give at most one preconditioner (hierarchy, level or callback)");
+    CAMG_CHECK(!vws || (H && vws->H == H->H), CAMG_ERR_ARG, "gmres: V-cycle workspace of another hierarchy");
+    Operator op;
+    op.A = A ? A->m : nullptr;
+    op.fn = apply_A;
+    op.user = user_A;
+    Precond M;
+    M.H = H ? H->H : nullptr;
+    M.ws = vws ? vws->W : nullptr;
+    M.L = L ? L->L : nullptr;
+    M.fn = apply_M;
+    M.user = user_M;
+    gmres_run(n, op, M, gws ? gws->G : nullptr, b, x, rel_tol, max_iters, restart, iterations, history, converged,
+              (cudaStream_t)stream);
+  });
+}
+
+extern "C" int camg_gmres_release(void) {
+  return guarded([&] { g_gmres_cache.reset(); });
+}
+
+extern "C" int camg_gmres_workspace_create(int64_t n, int restart, int store_z, camg_gmres_workspace** out) {
+  return guarded([&] {
+    CAMG_CHECK(n >= 1 && restart >= 1, CAMG_ERR_CONFIG, "gmres workspace: n and restart must be >= 1");
+    CAMG_CHECK(store_z >= -1 && store_z <= 1, CAMG_ERR_ARG, "gmres workspace: store_z must be -1, 0 or 1");
+    *out = new camg_gmres_workspace{new Gmres(n, restart, store_z)};
+  });
+}
+
+extern "C" int camg_gmres_workspace_destroy(camg_gmres_workspace* ws) {
+  return guarded([&] {
+    if (ws) { delete ws->G; delete ws; }
   });
 }

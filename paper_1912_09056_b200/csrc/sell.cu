@@ -614,6 +614,17 @@ void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const dou
 
 double sell_pass_bytes(const Sell* S) { return S->pass_bytes; }
 
+// lanes per block row of a full pass (the choice launch_blk makes for
+// nwork = nslices): 1 = one lane per block row, 2 = lane pairs, 4 = quads
+int sell_lanes(const Sell* S) {
+  const int64_t nw = S->nslices;
+  const bool long_rows = S->nbr > 0 && S->used_blocks >= quad_min_blocks() * S->nbr;
+  if (S->masked) return 1;
+  if (nw < quad_slices() || (nw < pair_slices() && long_rows)) return 4;
+  if (nw < pair_slices()) return 2;
+  return 1;
+}
+
 // ---------------------------------------------------------------------------
 // Multicolour Gauss-Seidel on a colour-ordered SELL (slices [s0, s1) hold the
 // block rows of one colour; rows of one colour share no entries, so each lane

@@ -68,6 +68,7 @@ Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_bloc
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                  const SellEpi& e, cudaStream_t st, const int32_t* slist = nullptr, int64_t nlist = -1);
 double sell_pass_bytes(const Sell* S);
+int sell_lanes(const Sell* S);
 // colour-ordered SELL (square bs x bs blocks, full): position t of the
 // mirror holds block row order[t] (-1 = padding), order.size() % 32 == 0
 Sell* sell_build_ordered(const Csr* A, int bs, int64_t nrows, int64_t ncols_blocked, const std::vector<int32_t>& order,

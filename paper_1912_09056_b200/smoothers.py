@@ -7,7 +7,12 @@ reference names, defaults and validation (smoothers.py:29-70).
 
 Inner solves on the GPU: `jacobi` (predictor and corrector) and `direct`
 (corrector, dense LU of S~).  The reference's lexicographic `sgs` / `ilu0`
-are sequential; they are rejected here with ConfigError.  The GPU variant
+are sequential; a block smoother configured with them (the reference default
+`BlockSmootherConfig()` is sgs predictor + ilu0 corrector) runs their
+multicolour GPU variants instead, `sgs -> mcgs`, `ilu0 -> mcilu0`, and says
+so in `BlockSmoother.substitutions` and the hierarchy report (compared with
+the lexicographic reference by convergence: profiles/r02_convergence_table.md).
+The GPU variant
 `mcgs` is the reference's residual-form SSOR applied with rows renumbered by
 a greedy colouring: multicolour symmetric Gauss-Seidel, compared with the
 reference SGS by convergence, and elementwise with the oracle's emulation of
@@ -53,6 +58,9 @@ A_HAT_MODES = ("plain_diag", "abs_rowsum", "exact")
 GPU_POINT_KINDS = ("jacobi", "direct")
 GPU_PREDICTOR_KINDS = ("jacobi", "gpu_chebyshev", "mcgs")
 GPU_CORRECTOR_KINDS = ("jacobi", "direct", "mcgs", "mcilu0")
+
+# multicolour GPU variants of the reference's sequential inner solves
+GPU_VARIANT = {"sgs": "mcgs", "ilu0": "mcilu0"}
 
 _BLOCK_CODE = {"uzawa": 0, "braess_sarazin": 1, "simple": 2, "simplec": 3}
 _POINT_CODE = {"jacobi": 0, "direct": 3, "gpu_chebyshev": 4, "mcgs": 5, "mcilu0": 6}
@@ -106,6 +114,25 @@ class BlockSmootherConfig:                       # smoothers.py:44-70
 class SchurOperator:
     S_tilde: SparseMatrix
     a_hat_inv_diag: np.ndarray | None
+
+
+def gpu_block_cfg(cfg: BlockSmootherConfig):
+    """The configuration the GPU runs: sequential `sgs` / `ilu0` inner solves
+    replaced by their multicolour variants (same damping; ILU(0) has none).
+    Returns (config, list of substitutions made)."""
+    from dataclasses import replace
+
+    subs = []
+    pred, corr = cfg.predictor, cfg.corrector
+    if cfg.kind != "braess_sarazin" and pred.kind in GPU_VARIANT:
+        subs.append(f"predictor {pred.kind} -> {GPU_VARIANT[pred.kind]}")
+        pred = replace(pred, kind=GPU_VARIANT[pred.kind])
+    if corr.kind in GPU_VARIANT:
+        subs.append(f"corrector {corr.kind} -> {GPU_VARIANT[corr.kind]}")
+        corr = replace(corr, kind=GPU_VARIANT[corr.kind])
+    if not subs:
+        return cfg, subs
+    return replace(cfg, predictor=pred, corrector=corr), subs
 
 
 def native_cfg(cfg: BlockSmootherConfig, node_block: int = 1) -> N.SmootherCfg:
@@ -210,6 +237,8 @@ class BlockSmoother:
                  post_sweeps: int = 1, node_block: int = 1):
         if isinstance(op, SaddleSystem):
             op = op.op
+        user_cfg = cfg
+        cfg, self.substitutions = gpu_block_cfg(cfg)
         inner = None
         if predictor_solver is not None:
             # smoothers.py:277-278: any object with apply(rhs); on the GPU path it
@@ -226,7 +255,8 @@ class BlockSmoother:
                 cfg_native = cfg
         else:
             cfg_native = cfg
-        self.cfg = cfg
+        self.cfg = user_cfg
+        self.gpu_cfg = cfg
         self.op = op
         ncfg = native_cfg(cfg_native, node_block)
         h = C.c_void_p()
