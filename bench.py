@@ -38,6 +38,35 @@ TRAFFIC = {
     "C5": 13.598788e9,
 }
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+# DRAM bytes of one whole V-cycle summed over its ncu launch list (dram__bytes_read.sum +
+# dram__bytes_write.sum per kernel, serialised, cold cache) and the cycle time of the
+# same build: the measured (not modelled) V-cycle bandwidth
+VCYCLE_DRAM = {
+    "C5": {"dram_bytes_per_cycle": 111.6e9, "source": "profiles/r01_vcycle_launches_c5.csv "
+           "(round-1 build; VERDICT r01 recomputed 5.68 TB/s = 0.87 of measured peak at 19.66 ms)"},
+}
+
+# BASELINE.json's literal smoother per config and why the bench runs another
+# (reference-side evidence: profiles/r02_convergence_table.md §2)
+BASELINE_SMOOTHER = {
+    "C1": "block Gauss-Seidel (Uzawa alpha=1), Jacobi(1, 0.8) per block",
+    "C2": "SIMPLEC, diagonal Schur approximation, 3 sweeps, damping 0.8",
+    "C3": "Braess-Sarazin, Jacobi approximation of K, 1 Schur Jacobi sweep, damping 0.7",
+    "C4": "Uzawa, 2 inner Jacobi sweeps on K, damping 0.6",
+    "C5": "SIMPLEC (parameters unstated)",
+}
+MAPPING_REASON = {
+    "C1": "literal BGS + Jacobi(1,0.8) does not converge in the reference (300 its, relres 1.8e-3); "
+          "Jacobi(2,0.6)/(1,0.6) converges",
+    "C2": "literal SIMPLEC x3 stalls in the reference (C2/2: relres 0.72 with Jacobi, C2 full: 1.0 with the "
+          "reference default sgs/ilu0 after 300 its); SIMPLE(0.8)x3 converges (15 its)",
+    "C3": "literal Braess-Sarazin + Jacobi stalls in the reference (C3/4: relres 0.90 / 0.68 after 300 its); "
+          "SIMPLE(0.8)x3 converges (16 its)",
+    "C4": "literal; corrector unstated -> the reference default kind ilu0, run as its multicolour variant mcilu0",
+    "C5": "SIMPLEC stalls in the reference (C5/10: relres 0.99 / 0.93 with Jacobi, 3.1e-2 with sgs/ilu0 after "
+          "300 its); SIMPLE(0.8)x3, Jacobi(1,0.6), ILU(0) corrector converges (reference lexicographic ilu0: 13 "
+          "its at C5/10; GPU multicolour mcilu0: 13)",
+}
 
 # BASELINE config -> reference-API mapping
 def solver_for(config):
@@ -152,36 +181,127 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference arm / cpu_baseline (oracle port, bounded sample)
+# CPU reference arm / cpu_baseline
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+# the reference has no multicolour inner solves: its CPU path runs their
+# lexicographic originals (profiles/r02_convergence_table.md compares them)
+_REF_KIND = {"mcilu0": "ilu0", "mcgs": "sgs"}
 
 
-def vcycle_cost_units(levels):
-    """Work units of one V-cycle: sum over levels of the sparse entries the
-    cycle streams (same structure on CPU and GPU, so the ratio scales a CPU
-    sample to the GPU workload)."""
-    return float(sum(lv["nnz_A"] * lv["streams"] + lv["nnz_P"] + lv["nnz_R"] for lv in levels))
+def cpu_info():
+    """CPU model, core count and BLAS threading of the host."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        import threadpoolctl
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads")}
+                for i in threadpoolctl.threadpool_info()]
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS"), "blas_pools": blas,
+            "sparse_kernels_threads": 1}
 
 
-def cpu_reference_sample(config, sample_scale, steps, warmup):
-    """Time the oracle V-cycle (scipy, single-threaded sparse kernels) on a
-    coarsened copy of the config.  Returns (seconds per V-cycle, cost units,
-    description)."""
+def reference_impl():
+    """(module namespace, kind): the unmodified reference package installed in
+    baseline/_ref (pip install --target), else the oracle port."""
+    if os.path.isdir(os.path.join(REF_DIR, "contactamg")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        from contactamg import hierarchy as R_h, krylov as R_k, smoothers as R_s  # noqa: F401
+        return "reference", (R_h, R_k, R_s)
+    return "port", None
+
+
+def _ref_system(g):
+    """(SaddleOperator, LevelMeta) of a generated system built from the
+    reference package's own classes (as tests/golden/make_golden.py does)."""
+    import scipy.sparse
+    from contactamg import hierarchy as R_h, sparse as R_sp, transfer as R_t
+    from contactamg.aggregation import LagrangeMap
+    from contactamg.saddle import SaddleOperator
+
+    def sm(m):
+        return R_sp.SparseMatrix.from_scipy(scipy.sparse.csr_matrix(m))
+
+    d, n_s = g.dim, len(g.slave_nodes)
+    op = SaddleOperator(sm(g.K), sm(g.B1), sm(g.B2), sm(g.Cz))
+    meta = R_h.LevelMeta(
+        u_dof_node=np.arange(g.n_u, dtype=np.int64) // d, num_u_nodes=g.n_u // d,
+        node_body=g.node_body.astype(np.int8), lam_dof_node=np.arange(g.n_lam, dtype=np.int64) // d,
+        num_lam_nodes=n_s, ns_u=R_t.NullSpace(g.rigid_body_modes(), "rigid-body"),
+        ns_lam=R_t.build_nullspace(n_s, R_t.NULLSPACE_CONSTANT_PER_COMPONENT, dofs_per_node=d),
+        mortar_block=sm(g.mortar_block),
+        lmap=LagrangeMap(slave_dofs=g.slave_dofs.astype(np.int64),
+                         row_node=np.repeat(g.slave_nodes, d).astype(np.int64),
+                         lm_node_of_lm_dof=np.arange(g.n_lam, dtype=np.int64) // d))
+    return op, meta
+
+
+def _ref_setup(mods, g, hcfg, scfg):
+    """Reference-package hierarchy of generated system g with the mapped
+    smoother (GPU-only kinds -> their lexicographic originals)."""
+    R_h, R_k, R_s = mods
+    op, meta = _ref_system(g)
+
+    def pc(p):
+        return R_s.PointSmootherConfig(kind=_REF_KIND.get(p.kind, p.kind), sweeps=p.sweeps, damping=p.damping)
+
+    sc = R_s.BlockSmootherConfig(kind=scfg.kind, alpha=scfg.alpha, outer_sweeps=scfg.outer_sweeps,
+                                 predictor=pc(scfg.predictor), corrector=pc(scfg.corrector), a_hat_mode=scfg.a_hat_mode)
+    hc = R_h.HierarchyConfig(max_levels=hcfg.max_levels, max_coarse_size=hcfg.max_coarse_size,
+                             coarse_solver=hcfg.coarse_solver, min_agg_size=hcfg.min_agg_size)
+    H = R_h.setup(op, meta, hc, sc)
+    A = op.merged().to_scipy()
+    return H, (lambda v: A @ v), R_k
+
+
+def _port_setup(g, hcfg, scfg):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import camg_oracle as O
+    op, meta, _ = O.system_from_generated(g)
 
-    from paper_1912_09056_b200.problem import config_spec, generate
+    def pc(p):
+        return O.PointCfg(_REF_KIND.get(p.kind, p.kind), p.sweeps, p.damping)
 
-    hcfg, scfg, _ = solver_for(config)
-    g = generate(config_spec(config, sample_scale))
-    op, meta, rhs = O.system_from_generated(g)
-    bc = O.BlockCfg(kind=scfg.kind, alpha=scfg.alpha, outer_sweeps=scfg.outer_sweeps,
-                    predictor=O.PointCfg(scfg.predictor.kind, scfg.predictor.sweeps, scfg.predictor.damping),
-                    corrector=O.PointCfg(scfg.corrector.kind, scfg.corrector.sweeps, scfg.corrector.damping),
-                    a_hat_mode=scfg.a_hat_mode)
-    t0 = time.perf_counter()
+    bc = O.BlockCfg(kind=scfg.kind, alpha=scfg.alpha, outer_sweeps=scfg.outer_sweeps, predictor=pc(scfg.predictor),
+                    corrector=pc(scfg.corrector), a_hat_mode=scfg.a_hat_mode)
     H = O.setup(op, meta, O.HierCfg(**{k: getattr(hcfg, k) for k in
                                        ("max_levels", "max_coarse_size", "coarse_solver", "min_agg_size")}), bc)
+    A = op.merged()
+    return H, (lambda v: A @ v), O
+
+
+def cpu_reference_run(config, scale, steps, warmup, solve=True, impl=None):
+    """Time the CPU reference path on `config/scale`: setup, `steps` V-cycles
+    (median), and (solve) GMRES(restart) to rtol 1e-8.  impl: "reference"
+    (unmodified package), "port" (oracle), None = the package when installed."""
+    from paper_1912_09056_b200.problem import config_spec, generate
+
+    kind, mods = reference_impl()
+    if impl == "port":
+        kind, mods = "port", None
+    hcfg, scfg, restart = solver_for(config)
+    g = generate(config_spec(config, scale))
+    t0 = time.perf_counter()
+    if kind == "reference":
+        H, applyA, R_k = _ref_setup(mods, g, hcfg, scfg)
+        levels = H.levels
+    else:
+        H, applyA, O = _port_setup(g, hcfg, scfg)
+        levels = H.levels
     setup_s = time.perf_counter() - t0
+    rhs = g.rhs
     for _ in range(warmup):
         H.apply(rhs)
     times = []
@@ -189,17 +309,42 @@ def cpu_reference_sample(config, sample_scale, steps, warmup):
         t0 = time.perf_counter()
         H.apply(rhs)
         times.append(time.perf_counter() - t0)
-    lv = []
+    out = {"kind": kind, "config": f"{config}/{scale}", "n": int(len(rhs)), "levels": len(levels),
+           "setup_s": round(setup_s, 3), "vcycle_s": float(np.median(times)), "vcycles_timed": steps,
+           "smoother": smoother_desc(scfg).replace("mcilu0", "ilu0").replace("mcgs", "sgs")}
+    if solve:
+        t0 = time.perf_counter()
+        if kind == "reference":
+            x, rep = R_k.gmres(applyA, H.apply, rhs, R_k.GmresConfig(rel_tol=1e-8, max_iters=300, restart=restart))
+        else:
+            x, rep = O.gmres(applyA, H.apply, rhs, 1e-8, 300, restart)
+        out.update(gmres_s=round(time.perf_counter() - t0, 3), gmres_iterations=int(rep.iterations),
+                   gmres_converged=bool(rep.converged),
+                   true_relres=float(np.linalg.norm(rhs - applyA(x)) / np.linalg.norm(rhs)))
+    units = []
     streams = steps_per_level(scfg)
-    for i, l in enumerate(H.levels):
-        A_nnz = l.op.nnz
-        lv.append(dict(nnz_A=A_nnz, streams=streams if i < len(H.levels) - 1 else 0,
-                       nnz_P=(l.P_u.nnz + l.P_lam.nnz) if l.P_u is not None else 0,
-                       nnz_R=(l.R_u.nnz + l.R_lam.nnz) if l.R_u is not None else 0))
-    desc = (f"oracle (numpy/scipy port of the reference) V-cycle on {config}/{sample_scale} "
-            f"(n={op.n}, nnz(K)={op.K.nnz}, {len(H.levels)} levels, setup {setup_s:.1f}s), "
-            f"{steps} timed cycles; scaled to the full config by V-cycle sparse-entry ratio")
-    return float(np.median(times)), vcycle_cost_units(lv), desc
+    for i, l in enumerate(levels):
+        last = i == len(levels) - 1
+        T = getattr(l, "transfer", None)
+        nP = (T.P_u.nnz + T.P_lam.nnz) if T is not None else ((l.P_u.nnz + l.P_lam.nnz) if getattr(l, "P_u", None)
+                                                              is not None else 0)
+        units.append(dict(nnz_A=l.op.nnz, streams=0 if last else streams, nnz_P=0 if last else nP,
+                          nnz_R=0 if last else nP))
+    out["units"] = vcycle_cost_units(units)
+    return out
+
+
+def cpu_baseline_line(run, full_units, extrapolated_from):
+    """cpu_baseline / reference-arm fields from a bounded CPU sample scaled to
+    the full workload by V-cycle sparse entries streamed."""
+    sec_full = run["vcycle_s"] * full_units / run["units"]
+    return {"value": 1.0 / sec_full, "unit": "V-cycles/s", "cores": 1, "kind": run["kind"],
+            "extrapolated": abs(full_units - run["units"]) > 1e-9 * full_units,
+            "sample": (f"{'unmodified reference package (baseline/_ref)' if run['kind'] == 'reference' else 'oracle port'}"
+                       f" V-cycle on {run['config']} (n={run['n']}, {run['levels']} levels, {run['smoother']}), "
+                       f"median of {run['vcycles_timed']} cycles = {run['vcycle_s']:.3f} s, scaled to {extrapolated_from} "
+                       f"by the ratio of sparse entries one V-cycle streams ({full_units:.4g} / {run['units']:.4g})"),
+            "sample_run": run, "host": cpu_info()}
 
 
 def steps_per_level(scfg):
@@ -208,6 +353,13 @@ def steps_per_level(scfg):
     per_step = sp  # first predictor sweep fused with the step residual
     s = scfg.outer_sweeps
     return max(0, s * per_step - 1) + 1 + s * per_step
+
+
+def vcycle_cost_units(levels):
+    """Work units of one V-cycle: sum over levels of the sparse entries the
+    cycle streams (same structure on CPU and GPU, so the ratio scales a CPU
+    sample to the GPU workload)."""
+    return float(sum(lv["nnz_A"] * lv["streams"] + lv["nnz_P"] + lv["nnz_R"] for lv in levels))
 
 
 def gpu_cost_units(H, scfg):
@@ -226,19 +378,28 @@ def run_reference(args):
     if rank != 0:
         return
     steps = max(1, args.steps)
-    sample_scale = args.cpu_sample_scale
-    per_cycle, units, desc = cpu_reference_sample(args.config, sample_scale, steps, min(args.warmup, 1))
-    # scale to the full workload by the same cost model the GPU arm reports
-    full_units = estimate_full_units(args.config, args.scale, sample_scale, units)
-    sec_full = per_cycle * full_units / units
-    value = 1.0 / sec_full
+    sample = cpu_reference_run(args.config, args.cpu_sample_scale, steps, min(args.warmup, 1), solve=True)
+    full_units = estimate_full_units(args.config, args.scale, args.cpu_sample_scale, sample["units"])
+    cb = cpu_baseline_line(sample, full_units, f"{args.config}{'' if args.scale == 1 else '/' + str(args.scale)}")
+    value = cb["value"]
+    full = {}
+    if not args.no_full_size:
+        # full-size CPU runs in the same process (C2 by the reference package,
+        # C3 by the oracle port: the package's C3 setup alone takes minutes)
+        for cfg, impl in (("C2", None), ("C3", "port")):
+            try:
+                full[cfg] = cpu_reference_run(cfg, 1, 3, 1, solve=True, impl=impl)
+            except Exception as e:  # noqa: BLE001
+                full[cfg] = {"error": repr(e)}
     line = {
         "impl": "reference",
         "metric": metric_name(args.config), "value": value, "unit": "V-cycles/s",
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": sec_full * 1e3,
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args),
-        "cpu_baseline": {"value": value, "unit": "V-cycles/s", "cores": 1, "kind": "port", "sample": desc},
+        "cpu_baseline": {k: v for k, v in cb.items() if k != "sample_run"},
+        "sample_run": sample,
+        "full_size_cpu": full,
         "e2e": {"value": value, "unit": "V-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -271,6 +432,9 @@ def workload_config(args):
         "hierarchy": {"max_levels": hcfg.max_levels, "max_coarse_size": hcfg.max_coarse_size,
                       "coarse_solver": hcfg.coarse_solver, "min_agg_size": hcfg.min_agg_size},
         "smoother": smoother_desc(scfg), "gmres_restart": restart,
+        "baseline_smoother": BASELINE_SMOOTHER[args.config],
+        "mapped_smoother": smoother_desc(scfg),
+        "mapping_reason": MAPPING_REASON[args.config],
         "l2": "inputs exceed L2 (fine-level operator >> 126 MB); no flush needed",
         "parallelism": f"replicas x{args.gpus}",
     }
@@ -399,9 +563,9 @@ def run_gpu(args):
     vc_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     total_cycles = args.steps * world
     value = total_cycles / (vc_ms * 1e-3 * args.steps)
-    kernels_per_cycle = N.kernels_per_apply(H.handle) if hasattr(N, "kernels_per_apply") else None
     bytes_csr, bytes_fmt = H.vcycle_bytes()
     vc_gbs = bytes_csr / (vc_ms * 1e-3) / 1e9
+    vc_fmt_gbs = bytes_fmt / (vc_ms * 1e-3) / 1e9
 
     # ---- e2e through the public API on pinned host vectors: every step's
     # host->device copy of its residual and device->host copy of its result
@@ -450,6 +614,18 @@ def run_gpu(args):
         solve = {"gmres_iterations": its, "converged": conv, "true_relres": relres,
                  "time_to_solution_s": t_solve, "setup_s": t_setup, "generate_s": t_gen,
                  "setup_breakdown_s": {k: round(v, 3) for k, v in H.timings.items()}}
+        # convergence margin of the mapping: the same solve for further
+        # uniform(-1,1) right-hand sides (seeds after the config's own)
+        seeds = {}
+        for sd in args.rhs_seeds:
+            rs_ = torch.from_numpy(np.random.default_rng(sd).uniform(-1.0, 1.0, n)).cuda()
+            t0 = time.perf_counter()
+            xs, its_s, conv_s, _ = gmres_device(Am, H, rs_, GmresConfig(rel_tol=1e-8, max_iters=args.max_iters,
+                                                                        restart=restart))
+            torch.cuda.synchronize()
+            seeds[str(sd)] = {"gmres_iterations": its_s, "converged": conv_s,
+                              "time_to_solution_s": round(time.perf_counter() - t0, 4)}
+        solve["other_rhs_seeds"] = seeds
 
     if rank != 0:
         if world > 1:
@@ -460,10 +636,8 @@ def run_gpu(args):
     peak, peak_kind = peaks()
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        per_cycle, units, desc = cpu_reference_sample(args.config, args.cpu_sample_scale, 2, 1)
-        full_units = gpu_cost_units(H, scfg)
-        cpu_value = 1.0 / (per_cycle * full_units / units)
-        cpu = {"value": cpu_value, "unit": "V-cycles/s", "cores": 1, "kind": "port", "sample": desc}
+        run = cpu_reference_run(args.config, args.cpu_sample_scale, 3, 1, solve=False)
+        cpu = cpu_baseline_line(run, gpu_cost_units(H, scfg), "the GPU's full hierarchy")
 
     levels = [{"n_u": l.op.n_u, "n_lam": l.op.n_lam, "nnz_K": l.op.K.nnz, "nnz_total": l.op.nnz}
               for l in H.levels]
@@ -475,22 +649,31 @@ def run_gpu(args):
         "dtype": "f64", "data": "synthetic (seeded generator, BASELINE config geometry/materials)",
         "config": dict(workload_config(args), levels=levels, operator_complexity=H.complexity,
                        device_memory_used_gb=round((total_b - free_b) / 1e9, 1)),
-        "roofline": {"bound": "hbm", "achieved": dom_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": dom_gbs / peak, "traffic": None if gs else TRAFFIC.get(args.config),
+        "roofline": {"bound": "hbm", "achieved": dom_fmt_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": dom_fmt_gbs / peak, "traffic": None if gs else TRAFFIC.get(args.config),
                      "kernel": ("k_sell_gs<3>: one fine-level multicolour block-SGS predictor sweep (forward + backward "
                                 "colour passes over a colour-ordered block SELL of K)") if gs else
                                ("k_sell_row<3,3,mode 1,masked>: fine-level Jacobi predictor sweep y += w D^-1 (b - [K B1][y; lam]) "
                                 "(block SELL-32 [K | B1] stream)"),
-                     "algorithmic_bytes_per_launch": dom_model,
-                     "bytes_model": ("SURVEY §8(d): 2 x (12 B/nnz(K) + offsets + 4 vector streams) + y/g init" if gs else
-                                     "SURVEY §8(d): 12 B/nnz (int32 CSR) + offsets + x read + 3 vector streams (b, D^-1, y out)"),
-                     "avg_launch_ms": dom_ms,
-                     "achieved_format_bytes": dom_fmt_gbs, "frac_format_bytes": dom_fmt_gbs / peak,
-                     "format_bytes_per_launch": dom_fmt,
+                     "bytes": "format bytes: what the stored format must stream per launch (block SELL values, one "
+                              "int32 per stored block, none for linear slots; x read once; b, D^-1 read, y written)",
+                     "bytes_per_launch": dom_fmt, "avg_launch_ms": dom_ms,
+                     "traffic_over_bytes": (TRAFFIC[args.config] / dom_fmt) if (not gs and args.config in TRAFFIC)
+                     else None,
+                     "model_bytes_per_launch": dom_model,
+                     "model_achieved": dom_gbs,
+                     "model": ("SURVEY §8(d): 2 x (12 B/nnz(K) + offsets + 4 vector streams) + y/g init" if gs else
+                               "SURVEY §8(d) int32-CSR model: 12 B/nnz + offsets + x read + 3 vector streams; the "
+                               "block format streams fewer bytes than this model, so model_achieved can exceed peak"),
                      "peak_kind": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"},
-        "vcycle_roofline": {"achieved": vc_gbs, "unit": "GB/s", "bytes_per_cycle": bytes_csr,
-                            "frac_of_measured_peak": vc_gbs / peak, "frac_of_8TBs": vc_gbs / 8000.0,
-                            "model": "SURVEY.md §8(d): 12 B/nnz + index/vector terms, zero products skipped"},
+        "vcycle_roofline": {"achieved": vc_fmt_gbs, "unit": "GB/s", "bytes_per_cycle": bytes_fmt,
+                            "frac_of_measured_peak": vc_fmt_gbs / peak, "frac_of_8TBs": vc_fmt_gbs / 8000.0,
+                            "bytes": "format bytes of every sparse application and vector stream of one cycle "
+                                     "(camg_hierarchy_vcycle_bytes), zero-vector products skipped",
+                            "dram_measured": VCYCLE_DRAM.get(args.config),
+                            "model_bytes_per_cycle": bytes_csr, "model_achieved": vc_gbs,
+                            "model": "SURVEY.md §8(d): 12 B/nnz + index/vector terms, zero products skipped",
+                            "kernels_per_cycle": H.kernels_per_cycle()},
         "spmv": {"GB/s": spmv_gbs, "GB/s_format_bytes": spmv_fmt_gbs, "ms": spmv_ms, "nnz": nnzA,
                  "kernel": "merged operator y = A x (SELL-32 [K|B1] rows + CSR [B2 -Cz] rows)"},
         "cpu_baseline": cpu,
@@ -522,6 +705,9 @@ def main():
     ap.add_argument("--max-iters", type=int, default=300)
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-size", action="store_true", help="reference arm: skip the full-size C2/C3 CPU runs")
+    ap.add_argument("--rhs-seeds", type=lambda t: [int(v) for v in t.split(",") if v], default=[5, 6, 7],
+                    help="extra right-hand-side seeds solved after the timed region (convergence margin)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -2323,7 +2323,11 @@ int camg_level_block_transfer(camg_level* L, int bs_fine, int bs_coarse, int64_t
     lv->R->sell = nullptr;
     // R has few, long rows: one lane per block row only pays when there are
     // enough block rows to fill the GPU; otherwise the warp-per-row CSR wins
-    if (ncoarse_u / bs_coarse >= kSellMinBlockRows)
+    // (CAMG_SELL_MIN_BLOCK_ROWS overrides the threshold: tests force the
+    // block SELL restriction on small hierarchies)
+    const char* e = getenv("CAMG_SELL_MIN_BLOCK_ROWS");
+    const int64_t min_rows = e ? atoll(e) : kSellMinBlockRows;
+    if (ncoarse_u / bs_coarse >= min_rows)
       lv->R->sell = sell_build(lv->R, bs_coarse, bs_fine, ncoarse_u, lv->nu, 0);
   });
 }
@@ -2543,55 +2547,74 @@ int camg_hierarchy_use_graph(camg_hierarchy* H, int enable) {
 int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, double* bytes_fmt) {
   return guarded([&] {
     // 12 B/nnz + 4(m+1) + 8 n + 8 m per sparse application,
-    // zero-vector products skipped, fused epilogue vectors counted.
+    // zero-vector products skipped, fused epilogue vectors counted.  The
+    // format count replaces the matrix term by what the stored format must
+    // stream: the block SELL mirror for the rows it covers (values + one
+    // int32 per block, none for linear slots, masked slots only their union
+    // pattern), int32-CSR with int64 offsets for the rest.
     const Hierarchy* H = Hh->H;
-    double total = 0.0;
-    auto spm = [](const Csr* A, int64_t rows, double nnz) {
-      return 12.0 * nnz + 4.0 * (rows + 1) + 8.0 * A->n_cols + 8.0 * rows;
-    };
-    const int nl = (int)H->levels.size();
-    for (int l = 0; l < nl; ++l) {
-      const Level* L = H->levels[l];
-      const double nnzA = (double)L->A->nnz;
-      const double top = (double)L->nnz_top;
-      const camg_smoother_cfg& c = L->cfg;
-      const int sp = (c.kind == CAMG_BRAESS_SARAZIN) ? 1 : c.pred_sweeps;
-      // one predictor sweep over [K | B1]: matrix + x read + (b, D^-1, y out);
-      // a multicolour SGS sweep is two such passes (forward, backward) plus
-      // the per-step init of y (and g) from x, b
-      const bool gs = c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_MCGS;
-      const double sweep = gs ? 2.0 * (spm(L->A, L->nu, top) + 8.0 * 2 * L->nu)
-                              : spm(L->A, L->nu, top) + 8.0 * 2 * L->nu;
-      // lambda side: B2/Cz rows, corrector sweeps over S~ (MCGS: forward +
-      // backward), interface-row B1 correction, a few lambda vectors
-      // (MC-ILU(0): forward + backward factor passes, plus an S~ product from the second sweep)
-      const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps
-                              : c.corr_kind == CAMG_PT_MCILU0 ? c.corr_sweeps + std::max(0, c.corr_sweeps - 1)
-                                                              : std::max(0, c.corr_sweeps - 1);
-      const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
-                         (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
-      // Chebyshev keeps d_k between its steps: + write / read of one vector
-      const double cheb = (!gs && c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_CHEBYSHEV)
-                              ? 16.0 * L->nu * std::max(0, sp - 1) : 0.0;
-      const double step = sp * sweep + lam + cheb +
-                          (gs ? 32.0 * L->nu + (c.kind == CAMG_UZAWA ? 24.0 * L->nu : 0.0) : 0.0);
-      // zero start: the first sweep reads no matrix / x (MC-SGS: only its
-      // first colour is skipped)
-      const double step0 = gs ? step - (12.0 * top + 8.0 * L->n) / std::max(1, L->pred_colors())
-                              : step - 12.0 * top - 8.0 * L->n;
-      int nsteps_pre = L->pre * c.outer_sweeps, nsteps_post = L->post * c.outer_sweeps;
-      if (l == nl - 1) {
-        if (H->coarse_solver == CAMG_COARSE_MERGED_LU) total += 8.0 * H->n_coarse * H->n_coarse + 16.0 * H->n_coarse;
-        else total += step0 + (c.outer_sweeps - 1) * step;
-        continue;
+    for (int pass = 0; pass < 2; ++pass) {
+      const bool F = pass == 1;
+      auto mat = [&](const Csr* A, int64_t rows, double nnz) {
+        if (!F) return 12.0 * nnz + 4.0 * (rows + 1);
+        double b = 0.0;
+        int64_t r0 = 0;
+        if (A->sell && A->sell->rows() <= rows) {
+          b += sell_pass_bytes(A->sell);
+          r0 = A->sell->rows();
+        }
+        const double tail = (double)(read_i64(A->rowptr + rows) - read_i64(A->rowptr + r0));
+        return b + 12.0 * tail + 8.0 * (rows - r0 + 1);
+      };
+      auto spm = [&](const Csr* A, int64_t rows, double nnz) {
+        return mat(A, rows, nnz) + 8.0 * A->n_cols + 8.0 * rows;
+      };
+      double total = 0.0;
+      const int nl = (int)H->levels.size();
+      for (int l = 0; l < nl; ++l) {
+        const Level* L = H->levels[l];
+        const double nnzA = (double)L->A->nnz;
+        const double top = (double)L->nnz_top;
+        const camg_smoother_cfg& c = L->cfg;
+        const int sp = (c.kind == CAMG_BRAESS_SARAZIN) ? 1 : c.pred_sweeps;
+        // one predictor sweep over [K | B1]: matrix + x read + (b, D^-1, y out);
+        // a multicolour SGS sweep is two such passes (forward, backward) plus
+        // the per-step init of y (and g) from x, b
+        const bool gs = c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_MCGS;
+        const double top_pass = (gs && F && L->gs.sell) ? sell_pass_bytes(L->gs.sell) + 8.0 * L->n + 8.0 * L->nu
+                                                        : spm(L->A, L->nu, top);
+        const double sweep = gs ? 2.0 * (top_pass + 8.0 * 2 * L->nu) : top_pass + 8.0 * 2 * L->nu;
+        // lambda side: B2/Cz rows, corrector sweeps over S~ (MCGS: forward +
+        // backward), interface-row B1 correction, a few lambda vectors
+        // (MC-ILU(0): forward + backward factor passes, plus an S~ product from the second sweep)
+        const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps
+                                : c.corr_kind == CAMG_PT_MCILU0 ? c.corr_sweeps + std::max(0, c.corr_sweeps - 1)
+                                                                : std::max(0, c.corr_sweeps - 1);
+        const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
+                           (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
+        // Chebyshev keeps d_k between its steps: + write / read of one vector
+        const double cheb = (!gs && c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_CHEBYSHEV)
+                                ? 16.0 * L->nu * std::max(0, sp - 1) : 0.0;
+        const double step = sp * sweep + lam + cheb +
+                            (gs ? 32.0 * L->nu + (c.kind == CAMG_UZAWA ? 24.0 * L->nu : 0.0) : 0.0);
+        // zero start: the first sweep reads no matrix / x (MC-SGS: only its
+        // first colour is skipped)
+        const double mat_top = top_pass - 8.0 * L->n - 8.0 * L->nu;
+        const double step0 = gs ? step - (mat_top + 8.0 * L->n) / std::max(1, L->pred_colors())
+                                : step - mat_top - 8.0 * L->n;
+        int nsteps_pre = L->pre * c.outer_sweeps, nsteps_post = L->post * c.outer_sweeps;
+        if (l == nl - 1) {
+          if (H->coarse_solver == CAMG_COARSE_MERGED_LU) total += 8.0 * H->n_coarse * H->n_coarse + 16.0 * H->n_coarse;
+          else total += step0 + (c.outer_sweeps - 1) * step;
+          continue;
+        }
+        total += (nsteps_pre > 0 ? step0 + (nsteps_pre - 1) * step : 0.0) + nsteps_post * step;
+        total += spm(L->A, L->n, nnzA) + 8.0 * L->n;          // residual (+ b read)
+        total += spm(L->R, L->R->n_rows, (double)L->R->nnz);    // restriction
+        total += spm(L->P, L->P->n_rows, (double)L->P->nnz) + 8.0 * L->n;  // prolong-add
       }
-      total += (nsteps_pre > 0 ? step0 + (nsteps_pre - 1) * step : 0.0) + nsteps_post * step;
-      total += spm(L->A, L->n, nnzA) + 8.0 * L->n;          // residual (+ b read)
-      total += spm(L->R, L->R->n_rows, (double)L->R->nnz);    // restriction
-      total += spm(L->P, L->P->n_rows, (double)L->P->nnz) + 8.0 * L->n;  // prolong-add
+      (F ? *bytes_fmt : *bytes_csr) = total;
     }
-    *bytes_csr = total;
-    *bytes_fmt = total;
   });
 }
 

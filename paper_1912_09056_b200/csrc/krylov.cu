@@ -196,7 +196,9 @@ struct Gmres {
   int store_z;  // 1 keep Z, 0 never, -1 when 4 GB remain free (checked per solve)
   DBuf<double> V, Z, w, z, r, u, part, hdev;
   double* hhost = nullptr;
+  int chunk = kMaxOrthoK;  // basis vectors per k_ortho launch (CAMG_ORTHO_CHUNK lowers it: tests)
   Gmres(int64_t n_, int m_, int store_z_) : n(n_), m(m_), store_z(store_z_) {
+    if (const char* e = getenv("CAMG_ORTHO_CHUNK")) chunk = std::max(1, std::min(kMaxOrthoK, atoi(e)));
     V = DBuf<double>((size_t)n * (m + 1));
     w = DBuf<double>(n);
     z = DBuf<double>(n);
@@ -262,11 +264,12 @@ struct Gmres {
   // (restart > 2048) go in chunks: all subtractions first, then the dots.
   template <int MODE>
   void ortho(int k, const double* h, double* out, cudaStream_t s) {
-    if (k <= kMaxOrthoK) return ortho_part<MODE>(0, k, h, out, s);
+    const int ck = chunk;
+    if (k <= ck) return ortho_part<MODE>(0, k, h, out, s);
     if (MODE != 0)
-      for (int i0 = 0; i0 < k; i0 += kMaxOrthoK) ortho_part<2>(i0, std::min(kMaxOrthoK, k - i0), h, out, s);
+      for (int i0 = 0; i0 < k; i0 += ck) ortho_part<2>(i0, std::min(ck, k - i0), h, out, s);
     if (MODE != 2)
-      for (int i0 = 0; i0 < k; i0 += kMaxOrthoK) ortho_part<0>(i0, std::min(kMaxOrthoK, k - i0), nullptr, out, s);
+      for (int i0 = 0; i0 < k; i0 += ck) ortho_part<0>(i0, std::min(ck, k - i0), nullptr, out, s);
   }
 };
 

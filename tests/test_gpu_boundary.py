@@ -1,0 +1,226 @@
+"""The drop-in boundary beyond single calls: re-entrant V-cycles on private
+workspaces, GMRES with caller-owned workspaces,
+GMRES over arbitrary callables and over the nested preconditioner through
+the native solver (krylov.py:45-129, hierarchy.py:366-385), the reference
+default smoother configuration (smoothers.py:44-50), and the reference's
+setup report (hierarchy.py:251-269)."""
+
+import sys
+import threading
+
+import numpy as np
+import pytest
+
+import camg_oracle as O
+from _golden import GOLDEN, load
+
+pytestmark = pytest.mark.gpu
+
+sys.path.insert(0, GOLDEN)
+from cases import BY_NAME  # noqa: E402
+
+from paper_1912_09056_b200 import _native  # noqa: E402
+from paper_1912_09056_b200.hierarchy import HierarchyConfig, fine_level_meta, nested_preconditioner, setup  # noqa: E402
+from paper_1912_09056_b200.krylov import GmresConfig, GmresWorkspace, gmres, release_workspace  # noqa: E402
+from paper_1912_09056_b200.problem import config_spec, generate, saddle_operator  # noqa: E402
+from paper_1912_09056_b200.smoothers import BlockSmootherConfig, PointSmootherConfig  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def device():
+    _native.require_device()
+
+
+_S = {}
+
+
+def system(cfg="C5", scale=10, skw=None, hkw=None):
+    key = (cfg, scale, repr(skw), repr(hkw))
+    if key not in _S:
+        g = generate(config_spec(cfg, scale))
+        op = saddle_operator(g)
+        skw = skw or dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=PointSmootherConfig("jacobi", 1, 0.6),
+                          corrector=PointSmootherConfig("mcilu0", 1, 1.0))
+        H = setup(op, fine_level_meta(g), HierarchyConfig(**(hkw or dict(max_levels=3, max_coarse_size=50))),
+                  BlockSmootherConfig(**skw))
+        _S[key] = (g, op, H)
+    return _S[key]
+
+
+def test_apply_returns_a_fresh_result_each_call():
+    """Every apply owns its result (the reference returns a new array)."""
+    import torch
+    g, op, H = system()
+    rng = np.random.default_rng(1)
+    r1 = torch.from_numpy(rng.standard_normal(H.n)).pin_memory()
+    r2 = torch.from_numpy(rng.standard_normal(H.n)).pin_memory()
+    z1 = H.apply(r1)
+    z1c = z1.clone()
+    z2 = H.apply(r2)
+    assert z1.data_ptr() != z2.data_ptr()
+    assert torch.equal(z1, z1c) and not torch.equal(z1, z2)
+    out = torch.empty(H.n, dtype=torch.float64).pin_memory()
+    assert H.apply(r1, out=out) is out and torch.equal(out, z1c)
+
+
+def test_workspaces_on_concurrent_streams_equal_default():
+    """Two workspaces applied concurrently on two streams give exactly the
+    default workspace's results."""
+    import torch
+    g, op, H = system()
+    rng = np.random.default_rng(2)
+    rs = [torch.from_numpy(rng.standard_normal(H.n)).cuda() for _ in range(4)]
+    ref = [H.apply_device(r).clone() for r in rs]
+    ws = [H.workspace(), H.workspace()]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty_like(r) for r in rs]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for i, r in enumerate(rs):
+            with torch.cuda.stream(streams[i % 2]):
+                H.apply_device(r, outs[i], ws[i % 2])
+    torch.cuda.synchronize()
+    for o, e in zip(outs, ref):
+        assert torch.equal(o, e)
+
+
+def test_workspaces_from_threads():
+    """One hierarchy applied from several host threads, each on its own
+    workspace and stream (captures serialise inside the library)."""
+    import torch
+    g, op, H = system()
+    rng = np.random.default_rng(3)
+    rs = [torch.from_numpy(rng.standard_normal(H.n)).cuda() for _ in range(4)]
+    ref = [H.apply_device(r).clone() for r in rs]
+    torch.cuda.synchronize()
+    res, errs = [None] * 4, []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            w = H.workspace()
+            with torch.cuda.stream(s):
+                o = torch.empty_like(rs[i])
+                for _ in range(3):
+                    H.apply_device(rs[i], o, w)
+                s.synchronize()
+            res[i] = o
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for o, e in zip(res, ref):
+        assert torch.equal(o, e)
+
+
+def test_workspace_of_another_hierarchy_is_rejected():
+    g, op, H = system()
+    g2, op2, H2 = system("C1", 1, hkw=dict(max_levels=2, max_coarse_size=1))
+    import torch
+    r = torch.zeros(H.n, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError):
+        H.apply_device(r, None, H2.workspace())
+
+
+def test_gmres_workspaces_and_release():
+    g, op, H = system()
+    cfg = GmresConfig(rel_tol=1e-8, max_iters=200, restart=100)
+    x0, r0 = gmres(op.apply_merged, H.apply, g.rhs, cfg)
+    release_workspace()
+    for store_z in (True, False, None):
+        ws = GmresWorkspace(H.n, 100, store_z)
+        x, rep = gmres(op.apply_merged, H.apply, g.rhs, cfg, workspace=ws, vcycle_workspace=H.workspace())
+        assert rep.iterations == r0.iterations
+        assert np.linalg.norm(x - x0) <= 1e-10 * np.linalg.norm(x0)
+    with pytest.raises(Exception):
+        gmres(op.apply_merged, H.apply, g.rhs, cfg, workspace=GmresWorkspace(H.n - 1, 100))
+
+
+def test_gmres_chunked_orthogonalisation(monkeypatch):
+    """Restarts longer than one k_ortho launch holds (> 2048 basis vectors)
+    run the CGS2 passes in chunks; forced to chunks of 7 here."""
+    g, op, H = system()
+    cfg = GmresConfig(rel_tol=1e-8, max_iters=200, restart=100)
+    x0, r0 = gmres(op.apply_merged, H.apply, g.rhs, cfg, workspace=GmresWorkspace(H.n, 100))
+    monkeypatch.setenv("CAMG_ORTHO_CHUNK", "7")
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, cfg, workspace=GmresWorkspace(H.n, 100))
+    assert abs(rep.iterations - r0.iterations) <= 1
+    assert np.linalg.norm(x - x0) <= 1e-7 * np.linalg.norm(x0)
+
+
+def test_gmres_over_python_callables_runs_native_loop():
+    """apply_A / apply_Minv as plain callables (numpy on host, torch on
+    device) are called back from the native solver; the result matches the
+    natively bound operator + hierarchy."""
+    import torch
+    g, op, H = system()
+    A = op.merged().to_scipy()
+    cfg = GmresConfig(rel_tol=1e-8, max_iters=200, restart=100)
+    x0, r0 = gmres(op.apply_merged, H.apply, g.rhs, cfg)
+    x1, r1 = gmres(lambda v: A @ v, lambda v: H.apply(v), g.rhs, cfg)            # host numpy callables
+    assert isinstance(x1, np.ndarray) and r1.iterations == r0.iterations
+    assert np.linalg.norm(x1 - x0) <= 1e-9 * np.linalg.norm(x0)
+    bd = torch.from_numpy(g.rhs).cuda()
+    x2, r2 = gmres(lambda v: op.apply_merged(v), lambda v: H.apply(v), bd, cfg)  # device callables
+    assert x2.is_cuda and r2.iterations == r0.iterations
+    # oracle: same problem, the oracle's V-cycle emulation
+    _, orep = O.gmres(lambda t: A @ t, lambda t: H.apply(t), g.rhs, 1e-8, 200, 100)
+    assert abs(orep.iterations - r0.iterations) <= 1
+    with pytest.raises(ZeroDivisionError):  # a callback's exception surfaces unchanged
+        gmres(lambda v: A @ v, lambda v: 1 / 0, g.rhs, cfg)
+
+
+def test_nested_preconditioner_gmres_is_native():
+    """GMRES over NestedPreconditioner.apply binds the level natively (no
+    Python in the Krylov loop); equals the callback form."""
+    g = generate(config_spec("C5", 25))
+    op = saddle_operator(g)
+    skw = BY_NAME["c5s_simple"][4]
+    NP = nested_preconditioner(op, fine_level_meta(g),
+                               BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=1,
+                                                   predictor=PointSmootherConfig("jacobi", 1, 0.8),
+                                                   corrector=PointSmootherConfig("jacobi", 1, 0.8)),
+                               HierarchyConfig(max_levels=3, max_coarse_size=50), PointSmootherConfig("jacobi", 2, 0.6))
+    assert skw  # the golden case family (nested_c5s) uses this system
+    cfg = GmresConfig(rel_tol=1e-8, max_iters=200, restart=100)
+    calls = []
+    x0, r0 = gmres(op.apply_merged, NP.apply, g.rhs, cfg)
+    x1, r1 = gmres(op.apply_merged, lambda v: (calls.append(1), NP.apply(v))[1], g.rhs, cfg)
+    assert calls and r1.iterations == r0.iterations
+    assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+    z = load("nested_c5s")
+    assert abs(r0.iterations - int(z["gmres_iterations"])) <= 1
+
+
+def test_reference_default_block_smoother_runs_multicolour_variants():
+    """BlockSmootherConfig() (reference default: sgs predictor, ilu0
+    corrector, smoothers.py:44-50) is accepted: the GPU runs mcgs / mcilu0,
+    says so in the report, and equals the explicit multicolour config."""
+    g = generate(config_spec("C5", 10))
+    op = saddle_operator(g)
+    meta = fine_level_meta(g)
+    hc = HierarchyConfig(max_levels=3, max_coarse_size=50)
+    Hd = setup(op, meta, hc, BlockSmootherConfig())
+    He = setup(op, meta, hc, BlockSmootherConfig(predictor=PointSmootherConfig("mcgs", 1, 1.0),
+                                                 corrector=PointSmootherConfig("mcilu0", 1, 1.0)))
+    assert "GPU variants: predictor sgs -> mcgs, corrector ilu0 -> mcilu0" in Hd.report
+    assert "GPU variants" not in He.report
+    assert Hd.levels[0].smoother.cfg == BlockSmootherConfig()
+    np.testing.assert_array_equal(Hd.apply(g.rhs), He.apply(g.rhs))
+    x, rep = gmres(op.apply_merged, Hd.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=200, restart=100))
+    assert rep.converged
+
+
+@pytest.mark.parametrize("name", ["c1_uzawa_jac2", "c2s_simplec", "c3s_bs", "c4s_uzawa", "c5s_simple",
+                                  "c3s_bs_blocksmoother", "c5s_simple_direct"])
+def test_setup_report_matches_reference(name):
+    """H.report is the reference's report string (hierarchy.py:251-269)."""
+    from test_gpu_parity import gpu_hier
+    z = load(name)
+    _, _, H = gpu_hier(name)
+    assert H.report == str(z["report"])

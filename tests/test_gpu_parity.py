@@ -207,11 +207,16 @@ def test_gmres_iterations_vs_reference(name):
         assert np.linalg.norm(g.rhs - A @ x) <= 2e-8 * np.linalg.norm(g.rhs)
 
 
-def test_unsupported_sequential_smoothers_are_rejected():
+def test_sequential_smoothers_map_to_multicolour_variants():
+    """Block smoothers run the multicolour variant of a sequential inner
+    solve (reported); a standalone sequential PointSmoother is rejected."""
+    from paper_1912_09056_b200.smoothers import PointSmoother
     g, op, _ = gpu_hier(GPU_CASES[0])
-    with pytest.raises(ConfigError):
-        setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2),
+    H = setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2),
               BlockSmootherConfig(kind="simple", predictor=PointSmootherConfig("sgs")))
+    assert H.levels[0].smoother.substitutions == ["predictor sgs -> mcgs", "corrector ilu0 -> mcilu0"]
+    with pytest.raises(ConfigError):
+        PointSmoother(PointSmootherConfig("sgs"), op.K)
 
 
 # ---------------------------------------------------------------------------
