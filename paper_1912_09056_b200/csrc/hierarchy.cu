@@ -601,6 +601,111 @@ __global__ void __launch_bounds__(1024) k_lu_solve_smem(int n, const double* __r
   for (int i = threadIdx.x; i < n; i += blockDim.x) xg[i] = y[i];
 }
 
+// Dense LU solve of a larger coarsest operator (n_c^2 doubles do not fit in
+// shared memory; C2: n_c = 2448, 48 MB of factors) on many SMs: one CTA per
+// block of kLuB rows.  Forward: CTA i accumulates L_ik y_k over the earlier
+// row blocks k as each one is published (release/acquire flags), then solves
+// its unit-lower diagonal block by substitution in one warp and publishes
+// y_i.  Backward, in reverse block order, the same with U and a non-unit
+// diagonal.  The factors are read once (each CTA streams its row panel);
+// the critical path is one diagonal-block solve + one flag hand-off per row
+// block and direction.  Same LAPACK factors and pivots as k_lu_solve; the
+// accumulation order within a row differs (parity bar 1e-10 on the V-cycle).
+// flags[0..nb) forward, [nb..2nb) backward, flags[2nb] = finished CTAs: the
+// last CTA to finish resets them for the next launch.
+constexpr int kLuB = 64;
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_lu_solve_blk(int n, const double* __restrict__ LU,
+                                                      const int32_t* __restrict__ perm, const double* __restrict__ b,
+                                                      double* y, double* x, unsigned* flags) {
+  CAMG_PDL_ENTRY();
+  __shared__ double acc[4][kLuB];
+  __shared__ double diag[kLuB][kLuB + 1];  // diagonal block, [row][col]
+  __shared__ double v[kLuB];
+  const int nb = (n + kLuB - 1) / kLuB;
+  const int i = blockIdx.x;
+  const int r0 = i * kLuB;
+  const int rows = min(kLuB, n - r0);
+  const int t = threadIdx.x, rr = t & (kLuB - 1), cq = t >> 6;  // row in block, column quarter
+  for (int dir = 0; dir < 2; ++dir) {
+    const bool fwd = dir == 0;
+    // diagonal block of L (fwd) / U (bwd) into shared memory
+    for (int e = t; e < kLuB * kLuB; e += blockDim.x) {
+      const int c = e / kLuB, r = e % kLuB;
+      diag[r][c] = (r < rows && c < rows) ? LU[(size_t)(r0 + c) * n + (r0 + r)] : 0.0;
+    }
+    double a = 0.0;
+    const double* src = fwd ? y : x;  // published blocks of the vector being solved for
+    for (int q = 0; q < nb - 1; ++q) {
+      const int k = fwd ? q : nb - 1 - q;  // blocks in publication order
+      if (fwd ? k >= i : k <= i) break;
+      const int c0 = k * kLuB, cols = min(kLuB, n - c0);
+      if (t == 0)
+        while (ld_acquire(flags + (fwd ? 0 : nb) + k) == 0) __nanosleep(64);
+      __syncthreads();
+      if (rr < rows)
+        for (int c = cq; c < cols; c += 4)
+          a = fma(LU[(size_t)(c0 + c) * n + (r0 + rr)], __ldcg(src + c0 + c), a);
+    }
+    acc[cq][rr] = a;
+    __syncthreads();
+    if (t < kLuB) {
+      const double base = fwd ? (t < rows ? b[perm[r0 + t]] : 0.0) : (t < rows ? y[r0 + t] : 0.0);
+      v[t] = base - (((acc[0][t] + acc[1][t]) + acc[2][t]) + acc[3][t]);
+    }
+    __syncthreads();
+    if (t < 32) {  // substitution on the diagonal block: lane owns rows t, t+32
+      double v0 = v[t], v1 = v[t + 32];
+      if (fwd) {
+        for (int j = 0; j < rows; ++j) {
+          const double xj = __shfl_sync(0xffffffffu, j < 32 ? v0 : v1, j & 31);
+          if (t > j) v0 = fma(-diag[t][j], xj, v0);
+          if (t + 32 > j) v1 = fma(-diag[t + 32][j], xj, v1);
+        }
+      } else {
+        for (int j = rows - 1; j >= 0; --j) {
+          double xj = __shfl_sync(0xffffffffu, j < 32 ? v0 : v1, j & 31);
+          xj = xj / diag[j][j];
+          if (t == (j & 31)) {
+            if (j < 32) v0 = xj; else v1 = xj;
+          }
+          if (t < j) v0 = fma(-diag[t][j], xj, v0);
+          if (t + 32 < j) v1 = fma(-diag[t + 32][j], xj, v1);
+        }
+      }
+      double* dst = fwd ? y : x;
+      if (t < rows) dst[r0 + t] = v0;
+      if (t + 32 < rows) dst[r0 + t + 32] = v1;
+      __threadfence();
+      __syncwarp();
+      if (t == 0) st_release(flags + (fwd ? 0 : nb) + i, 1u);
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    __threadfence();
+    if (atomicAdd(flags + 2 * nb, 1u) == (unsigned)(nb - 1)) {  // last CTA: reset for the next launch
+      for (int k = 0; k < 2 * nb; ++k) flags[k] = 0u;
+      __threadfence();
+      flags[2 * nb] = 0u;
+    }
+  }
+}
+
+// the blocked multi-CTA solve needs all nb CTAs resident (they wait on each
+// other): used from kLuBlkMin rows up to 148 row blocks
+constexpr int kLuBlkMin = 192;
+constexpr int kLuBlkMaxBlocks = 148;
+
 // dense LU solve on one CTA: factors in shared memory when they fit
 static void lu_solve(int n, const double* LU, const int32_t* piv, const double* b, double* x, cudaStream_t s) {
   const size_t need = sizeof(double) * ((size_t)n * n + 2 * (size_t)n);
@@ -1948,6 +2053,11 @@ struct Hierarchy {
   DBuf<double> lu;
   DBuf<int32_t> piv;
   int64_t n_coarse = 0;
+  // blocked multi-CTA coarse solve (k_lu_solve_blk): composed row
+  // permutation, forward-solve vector, hand-off flags (per workspace)
+  bool lu_blk = false;
+  DBuf<int32_t> lu_perm;
+  DBuf<double> lu_y, lu_flags;
   // per-level vectors: b (rhs), x[2]
   std::vector<DBuf<double>> vb, vx0, vx1, vr;
   bool use_graph = true;
@@ -1964,13 +2074,46 @@ struct Hierarchy {
         v.push_back(b);
       if (L->inner) scalar_work_slots(L->inner, v);
     }
+    v.push_back(&lu_y);
+    v.push_back(&lu_flags);
     return v;
+  }
+
+  void set_coarse_lu(int64_t n, const double* lu_h, const int32_t* piv_h) {
+    n_coarse = n;
+    lu = DBuf<double>(n * n + 1);
+    piv = DBuf<int32_t>(n + 1);
+    CAMG_CUDA(cudaMemcpy(lu.p, lu_h, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(piv.p, piv_h, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    const int64_t nb = (n + kLuB - 1) / kLuB;
+    const char* e = getenv("CAMG_LU_BLOCKED");  // 0: always the one-CTA solve
+    const size_t smem_need = sizeof(double) * ((size_t)n * n + 2 * (size_t)n);
+    lu_blk = !(e && e[0] == '0') && (n >= kLuBlkMin || (e && e[0] == '1')) && nb <= kLuBlkMaxBlocks &&
+             !(smem_need <= size_t(220) * 1024 && !(e && e[0] == '1'));
+    if (lu_blk) {
+      // x = P b with LAPACK's sequential row swaps composed into one gather
+      std::vector<int32_t> idx(n);
+      for (int64_t i = 0; i < n; ++i) idx[i] = (int32_t)i;
+      for (int64_t i = 0; i < n; ++i) std::swap(idx[i], idx[piv_h[i]]);
+      lu_perm = DBuf<int32_t>(n + 1);
+      CAMG_CUDA(cudaMemcpy(lu_perm.p, idx.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+      lu_y = DBuf<double>(n + 1);
+      lu_flags = DBuf<double>(nb + 2);  // 2 nb + 1 unsigned flags
+      CAMG_CUDA(cudaMemset(lu_flags.p, 0, sizeof(double) * (nb + 2)));
+    }
   }
 
   void coarse_solve(const double* b, double* x, cudaStream_t s) {
     Level* L = levels.back();
     if (coarse_solver == CAMG_COARSE_MERGED_LU) {
       CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "coarse LU factors were not set");
+      if (lu_blk) {
+        const int nb = (int)((n_coarse + kLuB - 1) / kLuB);
+        note_launch();
+        launch_k(k_lu_solve_blk, nb, 256, 0, s, (int)n_coarse, (const double*)lu.p, (const int32_t*)lu_perm.p, b,
+                 lu_y.p, x, reinterpret_cast<unsigned*>(lu_flags.p));
+        return;
+      }
       lu_solve((int)n_coarse, lu.p, piv.p, b, x, s);
     } else {
       L->sweep(nullptr, b, x, s);
@@ -2026,7 +2169,10 @@ struct Hierarchy {
   VcycleWs* make_ws() {
     std::unique_ptr<VcycleWs> w(new VcycleWs());
     w->owned = true;
-    for (DBuf<double>* b : work_slots()) w->bufs.emplace_back(b->p ? DBuf<double>(b->n) : DBuf<double>());
+    for (DBuf<double>* b : work_slots()) {
+      w->bufs.emplace_back(b->p ? DBuf<double>(b->n) : DBuf<double>());
+      if (b->p) CAMG_CUDA(cudaMemset(w->bufs.back().p, 0, sizeof(double) * b->n));  // (hand-off flags start at 0)
+    }
     return w.release();
   }
 
@@ -2407,11 +2553,8 @@ int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu,
   return guarded([&] {
     CAMG_CHECK(n == H->H->levels.back()->n, CAMG_ERR_DIMENSION, "coarse LU size mismatch");
     CAMG_CHECK(n < (1 << 30), CAMG_ERR_DIMENSION, "coarse LU too large");
-    H->H->n_coarse = n;
-    H->H->lu = DBuf<double>(n * n + 1);
-    H->H->piv = DBuf<int32_t>(n + 1);
-    CAMG_CUDA(cudaMemcpy(H->H->lu.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice));
-    CAMG_CUDA(cudaMemcpy(H->H->piv.p, piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    CAMG_CHECK(!H->H->def.graph, CAMG_ERR_SETUP, "coarse LU must be set before the first V-cycle");
+    H->H->set_coarse_lu(n, lu, piv);
   });
 }
 

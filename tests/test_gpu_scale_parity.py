@@ -188,3 +188,33 @@ def test_convergence_vs_reference_lexicographic(row):
     assert rep.converged
     assert abs(rep.iterations - emu) <= 1, (rep.iterations, emu)
     assert rep.iterations <= max(ref + 3, 1.25 * ref), (r["config"], r["variant"], rep.iterations, ref)
+
+
+@pytest.mark.parametrize("cfg,scale,levels", [("C5", 10, 2), ("C2", 4, 2), ("C3", 8, 2)])
+def test_blocked_coarse_lu_solve_vs_oracle(cfg, scale, levels, monkeypatch):
+    """The multi-CTA blocked coarse LU solve (k_lu_solve_blk: row-block CTAs
+    with release/acquire hand-offs) against the one-CTA solve and the oracle's
+    scipy lu_solve, forced on for coarse sizes below its threshold too."""
+    from paper_1912_09056_b200.hierarchy import HierarchyConfig
+    from paper_1912_09056_b200.smoothers import BlockSmootherConfig, PointSmootherConfig
+
+    hkw = dict(max_levels=levels, max_coarse_size=50)
+    skw = BlockSmootherConfig(kind="simple", alpha=0.8, outer_sweeps=3, predictor=PointSmootherConfig("jacobi", 1, 0.6),
+                              corrector=PointSmootherConfig("mcilu0", 1, 1.0))
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("CAMG_LU_BLOCKED", mode)
+        H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), skw)
+        out[mode] = [H.apply(g.rhs), H.apply(g.rhs)]  # second call: flags were reset by the first
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(**hkw), O.BlockCfg(kind="simple", alpha=0.8, outer_sweeps=3,
+                                                           predictor=O.PointCfg("jacobi", 1, 0.6),
+                                                           corrector=O.PointCfg("mcilu0", 1, 1.0)))
+    ref = OH.apply(rhs)
+    for mode in ("0", "1"):
+        for v in out[mode]:
+            assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref), mode
+    np.testing.assert_array_equal(out["1"][0], out["1"][1])
+    assert np.linalg.norm(out["1"][0] - out["0"][0]) <= 1e-12 * np.linalg.norm(out["0"][0])
