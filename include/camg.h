@@ -34,9 +34,13 @@ extern "C" {
 #define CAMG_BRAESS_SARAZIN 1
 #define CAMG_SIMPLE 2
 #define CAMG_SIMPLEC 3
-/* point smoother kinds: smoothers.py:24 POINT_KINDS (jacobi, direct) plus
- * GPU-only variants compared by convergence, never elementwise */
+/* point smoother kinds: smoothers.py:24 POINT_KINDS (jacobi, sgs, ilu0,
+ * direct with the reference's exact semantics; sgs / ilu0 as lexicographic
+ * sync-free triangular solves) plus GPU-only variants compared by
+ * convergence, never elementwise */
 #define CAMG_PT_JACOBI 0
+#define CAMG_PT_SGS 1       /* smoothers.py:155-164, 189-191 */
+#define CAMG_PT_ILU0 2      /* smoothers.py:80-138, 193-196  */
 #define CAMG_PT_DIRECT 3
 #define CAMG_PT_CHEBYSHEV 4 /* GPU-only */
 #define CAMG_PT_MCGS 5      /* GPU-only multicolour symmetric Gauss-Seidel: predictor on K (node-block
@@ -46,6 +50,8 @@ extern "C" {
 /* A_hat modes: smoothers.py:26 A_HAT_MODES */
 #define CAMG_AHAT_PLAIN 0
 #define CAMG_AHAT_ABS_ROWSUM 1
+#define CAMG_AHAT_EXACT 2   /* test-scale: S~ = scale (Cz + B2 K^-1 B1) supplied by camg_level_set_schur,
+                               A^-1 = K^-1 from camg_level_set_k_lu (smoothers.py:233-236, 272-273) */
 /* coarse solvers: hierarchy.py:47 COARSE_SOLVERS */
 #define CAMG_COARSE_MERGED_LU 0
 #define CAMG_COARSE_BLOCK_SMOOTHER 1
@@ -56,6 +62,7 @@ typedef struct camg_hierarchy camg_hierarchy;
 typedef struct camg_scalar_hierarchy camg_scalar_hierarchy;
 typedef struct camg_vcycle_workspace camg_vcycle_workspace;
 typedef struct camg_gmres_workspace camg_gmres_workspace;
+typedef struct camg_point camg_point;
 
 typedef struct {
   int kind;           /* CAMG_UZAWA .. CAMG_SIMPLEC                 (BlockSmootherConfig.kind)   */
@@ -82,6 +89,7 @@ typedef struct {
 #define CAMG_PATH_CTA 5           /* whole sweeps in one CTA                              */
 #define CAMG_PATH_CLUSTER 6       /* whole sweeps on one 16-CTA thread-block cluster      */
 #define CAMG_PATH_INNER_AMG 7     /* nested preconditioner: scalar AMG V-cycle predictor  */
+#define CAMG_PATH_LEX_TRSV 8      /* lexicographic sgs / ilu0: sync-free triangular solves */
 
 typedef struct {
   int64_t n_u, n_lam, nnz;     /* merged operator of the level                                   */
@@ -219,6 +227,13 @@ int camg_level_operator(const camg_level* L, const camg_csr** out);
  * LAPACK pivots (scipy.linalg.lu_factor)                                      */
 int camg_level_set_corrector_lu(camg_level* L, int64_t n, const double* lu_colmajor,
                                 const int32_t* piv);
+/* dense LU factors of K (column-major, 0-based LAPACK pivots): the `direct`
+ * predictor (smoothers.py:182-183) and the exact A^-1 of a_hat_mode "exact"
+ * (smoothers.py:272-273) */
+int camg_level_set_k_lu(camg_level* L, int64_t n, const double* lu_colmajor, const int32_t* piv);
+/* replace S~ (a_hat_mode "exact": scale (Cz + B2 K^-1 B1), smoothers.py:233-236)
+ * and rebuild the corrector on it (copied)                                    */
+int camg_level_set_schur(camg_level* L, const camg_csr* S);
 /* segregated transfer (transfer.py:186-188): R = P^T computed on device */
 int camg_level_set_transfer(camg_level* L, const camg_csr* P_u, const camg_csr* P_lam);
 /* block SELL-32 mirrors for the transfers of a level with uniform node
@@ -283,6 +298,18 @@ int camg_scalar_hierarchy_destroy(camg_scalar_hierarchy* H);
  * level's predictor becomes du = inner(r_u) (NULL restores the configured
  * predictor); inner is borrowed                                              */
 int camg_level_set_predictor_solver(camg_level* L, camg_scalar_hierarchy* inner);
+
+/* ---- point smoothers (PointSmoother, smoothers.py:141-199) ---------------- */
+/* kind CAMG_PT_JACOBI / SGS / ILU0 / DIRECT bound to a square A (borrowed);
+ * sgs / ilu0 keep the reference's lexicographic order (sync-free triangular
+ * solves); ilu0 factors on the host in the reference's IKJ order; direct
+ * needs camg_point_set_lu.  Zero diagonals raise CAMG_ERR_SINGULAR naming
+ * the row (smoothers.py:146-158).                                            */
+int camg_point_create(const camg_csr* A, int kind, int sweeps, double damping, camg_point** out);
+int camg_point_set_lu(camg_point* P, int64_t n, const double* lu_colmajor, const int32_t* piv);
+/* PointSmoother.smooth(x, b) (x NULL = zero start, i.e. .apply(b)) -> out   */
+int camg_point_smooth(camg_point* P, const double* x, const double* b, double* out, void* stream);
+int camg_point_destroy(camg_point* P);
 
 /* ---- Krylov (krylov.py:45-129) -------------------------------------------- */
 /* right-preconditioned GMRES(restart), x0 = 0, CGS2 orthogonalisation.

@@ -61,7 +61,7 @@ class LevelInfo(C.Structure):
 
 
 # CAMG_PATH_* (include/camg.h)
-PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg")
+PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg", "lex_trsv")
 
 
 _SIGS = {
@@ -108,6 +108,12 @@ _SIGS = {
     "camg_level_schur": (C.c_int, [vp, C.POINTER(vp)]),
     "camg_level_operator": (C.c_int, [vp, C.POINTER(vp)]),
     "camg_level_set_corrector_lu": (C.c_int, [vp, i64, vp, vp]),
+    "camg_level_set_k_lu": (C.c_int, [vp, i64, vp, vp]),
+    "camg_level_set_schur": (C.c_int, [vp, vp]),
+    "camg_point_create": (C.c_int, [vp, C.c_int, C.c_int, f64, C.POINTER(vp)]),
+    "camg_point_set_lu": (C.c_int, [vp, i64, vp, vp]),
+    "camg_point_smooth": (C.c_int, [vp, vp, vp, vp, vp]),
+    "camg_point_destroy": (C.c_int, [vp]),
     "camg_level_set_transfer": (C.c_int, [vp, vp, vp]),
     "camg_level_sweep": (C.c_int, [vp, vp, vp, vp, vp]),
     "camg_hierarchy_create": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp)]),

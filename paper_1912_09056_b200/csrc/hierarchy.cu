@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "pointsolve.cuh"
 #include "kernels.cuh"
 #include "sell.cuh"
 
@@ -707,7 +708,7 @@ constexpr int kLuBlkMin = 192;
 constexpr int kLuBlkMaxBlocks = 148;
 
 // dense LU solve on one CTA: factors in shared memory when they fit
-static void lu_solve(int n, const double* LU, const int32_t* piv, const double* b, double* x, cudaStream_t s) {
+void lu_solve(int n, const double* LU, const int32_t* piv, const double* b, double* x, cudaStream_t s) {
   const size_t need = sizeof(double) * ((size_t)n * n + 2 * (size_t)n);
   note_launch();
   if (need <= size_t(220) * 1024) {
@@ -1150,7 +1151,7 @@ struct LaunchIluPass {
 // separately, as the reference's Python loop does.  Returns the diagonal
 // positions.  `name` maps a row to the number reported in errors (null:
 // itself).
-__attribute__((optimize("fp-contract=off"))) static std::vector<int64_t> ilu0_ikj(int64_t n, const int64_t* rp,
+__attribute__((optimize("fp-contract=off"))) std::vector<int64_t> ilu0_ikj(int64_t n, const int64_t* rp,
                                                                                   const int32_t* ci, double* va,
                                                                                   const int32_t* name) {
   auto nm = [&](int64_t r) { return std::to_string(name ? (int64_t)name[r] : r); };
@@ -1545,6 +1546,15 @@ struct Level {
   // direct corrector
   DBuf<double> corr_lu;
   DBuf<int32_t> corr_piv;
+  // reference-semantics inner solves: lexicographic sgs / ilu0 predictor on
+  // K (pps, on the level's own copy of K) and corrector on S~ (cps)
+  PointSolver pps, cps;
+  std::unique_ptr<Csr> K_own;
+  // dense LU of K: the `direct` predictor and the exact A^-1 of a_hat_mode
+  // "exact" (smoothers.py:182-183, 272-273; factors from the host)
+  DBuf<double> k_lu;
+  DBuf<int32_t> k_piv;
+  bool exact = false;
   // transfer (merged block-diagonal)
   Csr* P = nullptr;
   Csr* R = nullptr;
@@ -1612,6 +1622,11 @@ struct Level {
       cilu.run(S, rc, w_dl.p, cfg.corr_sweeps, s);
       return w_dl.p;
     }
+    if (cfg.corr_kind == CAMG_PT_SGS || cfg.corr_kind == CAMG_PT_ILU0) {
+      // the reference's lexicographic sweeps on S~ from zero (smoothers.py:197-199)
+      cps.smooth(nullptr, rc, w_dl.p, s);
+      return w_dl.p;
+    }
     double* cur = w_dl.p;
     double* nxt = w_dl2.p;
     dispatch_g<LaunchCorr>(S->avg_row, S, rc, dinv_c.p, nullptr, cur, true, s);
@@ -1623,6 +1638,10 @@ struct Level {
   }
 
   int pred_colors() const { return gs.colors(); }
+  bool pred_generic() const {
+    return cfg.kind != CAMG_BRAESS_SARAZIN &&
+           (cfg.pred_kind == CAMG_PT_DIRECT || cfg.pred_kind == CAMG_PT_SGS || cfg.pred_kind == CAMG_PT_ILU0);
+  }
 
   // MC-SGS predictor in iterate form: y_0 = u, then pred_sweeps forward +
   // backward colour sweeps of Gauss-Seidel on K y = b_u - B1 lam -- the
@@ -1652,13 +1671,23 @@ struct Level {
       // u_half = u + (A^-1 r_u) / alpha   (smoothers.py:296)
       RowEpi e{b, x, nullptr, ainv.p, nullptr, xo, 1.0 / alpha};
       top_pass(e, xu, xl, zero, s);
-    } else if (inner) {
+    } else if (inner || pred_generic()) {
       join(s);
-      // du = inner.apply(r_u), r_u = b_u - K u - B1 lam (smoothers.py:285-314
-      // with predictor_solver); SIMPLE: u_half = u + du; Uzawa: u + alpha du
+      // du = predictor.apply(r_u), r_u = b_u - K u - B1 lam (smoothers.py:285-314):
+      // the nested preconditioner's inner AMG (predictor_solver), a dense LU
+      // of K (direct) or lexicographic sgs / ilu0 sweeps on K from zero;
+      // SIMPLE: u_half = u + du; Uzawa: u + alpha du
       RowEpi e{b, x, w_ru.p, nullptr, nullptr, nullptr, 0.0};
       resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
-      const double* du = scalar_run(inner, w_ru.p, s);
+      const double* du = w_du.p;
+      if (inner) {
+        du = scalar_run(inner, w_ru.p, s);
+      } else if (cfg.pred_kind == CAMG_PT_DIRECT) {
+        CAMG_CHECK(k_lu.p != nullptr, CAMG_ERR_SETUP, "direct predictor factors were not set");
+        lu_solve((int)nu, k_lu.p, k_piv.p, w_ru.p, w_du.p, s);
+      } else {
+        pps.smooth(nullptr, w_ru.p, w_du.p, s);
+      }
       note_launch();
       if (kind == CAMG_UZAWA) {
         launch_k(k_pred_update, grid_for(nu, 256), 256, 0, s, nu, xu, du, alpha, w_du2.p, xo);
@@ -1715,6 +1744,7 @@ struct Level {
       }
     }
     if (nl == 0) return;
+    CAMG_CHECK(S != nullptr, CAMG_ERR_SETUP, "S~ was not set (a_hat_mode exact: camg_level_set_schur)");
     join(s);
     cudaStream_t ls = s;
     if (overlap) {  // fork the lambda side onto `side`
@@ -1728,7 +1758,13 @@ struct Level {
     const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
     note_launch();
     launch_k(k_lam_update, grid_for(nl, 256), 256, 0, ls, nl, xl, dl, cl, xo + nu);
-    if (kind != CAMG_UZAWA && n_b1_rows) {
+    if (kind != CAMG_UZAWA && n_b1_rows && exact) {
+      // u_new = u_half - alpha K^-1 B1 dlam (a_hat_mode "exact", smoothers.py:313)
+      CAMG_CHECK(k_lu.p != nullptr, CAMG_ERR_SETUP, "exact a_hat mode needs the LU factors of K");
+      spmv(B1, 1.0, dl, 0.0, w_ru.p, ls);
+      lu_solve((int)nu, k_lu.p, k_piv.p, w_ru.p, w_du.p, ls);
+      vec_axpy(nu, -alpha, w_du.p, xo, ls);
+    } else if (kind != CAMG_UZAWA && n_b1_rows) {
       // u_new = u_half - c A^-1 B1 dlam on the interface rows
       const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
       note_launch();
@@ -1877,18 +1913,42 @@ static void setup_overlap(Level* L) {
             (long long)L->n_dep);
 }
 
+// corrector structures on S~ (colourings, factors, inverse diagonal)
+static void setup_corrector(Level* L) {
+  const camg_smoother_cfg& cfg = L->cfg;
+  const int64_t nl = L->nl;
+  cudaStream_t s = 0;
+  if (nl == 0) return;
+  // point colouring of S~: the multiplier-node graph needs as many colours
+  // (16 on C5) and the per-node kernels measured slower
+  if (cfg.corr_kind == CAMG_PT_MCGS) L->cgs.setup(L->S, 1, s);
+  if (cfg.corr_kind == CAMG_PT_MCILU0) L->cilu.setup(L->S, s);
+  if (cfg.corr_kind == CAMG_PT_SGS || cfg.corr_kind == CAMG_PT_ILU0)
+    L->cps.setup(L->S, cfg.corr_kind, cfg.corr_sweeps, cfg.corr_damping);
+  if (cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_MCGS) {
+    DBuf<double> dS(nl + 1);
+    csr_diagonal(L->S, 0, dS.p, s);
+    CAMG_CUDA(cudaDeviceSynchronize());
+    check_no_zero(dS.p, nl, "jacobi");
+    L->dinv_c = DBuf<double>(nl + 1);
+    note_launch();
+    k_scaled_recip<<<grid_for(nl, 256), 256>>>(nl, dS.p, cfg.corr_damping, 1.0, L->dinv_c.p);
+  }
+  CAMG_CUDA(cudaDeviceSynchronize());
+}
+
 Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, const camg_smoother_cfg& cfg, int pre,
                     int post, Csr* A_shared) {
   CAMG_CHECK(cfg.kind >= CAMG_UZAWA && cfg.kind <= CAMG_SIMPLEC, CAMG_ERR_CONFIG, "unknown block smoother kind");
   CAMG_CHECK(cfg.alpha > 0.0, CAMG_ERR_CONFIG, "alpha must be positive");
   CAMG_CHECK(cfg.outer_sweeps >= 1, CAMG_ERR_CONFIG, "outer_sweeps must be >= 1");
-  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || cfg.pred_kind == CAMG_PT_JACOBI || cfg.pred_kind == CAMG_PT_MCGS ||
-                 cfg.pred_kind == CAMG_PT_CHEBYSHEV,
-             CAMG_ERR_CONFIG, "GPU predictor supports jacobi, chebyshev and mcgs");
+  CAMG_CHECK(cfg.kind == CAMG_BRAESS_SARAZIN || (cfg.pred_kind >= CAMG_PT_JACOBI && cfg.pred_kind <= CAMG_PT_MCGS),
+             CAMG_ERR_CONFIG, "GPU predictor supports jacobi, sgs, ilu0, direct, chebyshev and mcgs");
   CAMG_CHECK(cfg.pred_sweeps >= 1, CAMG_ERR_CONFIG, "predictor sweeps must be >= 1");
-  CAMG_CHECK(cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_DIRECT || cfg.corr_kind == CAMG_PT_MCGS ||
-                 cfg.corr_kind == CAMG_PT_MCILU0,
-             CAMG_ERR_CONFIG, "GPU corrector supports jacobi, mcgs, mcilu0 and direct");
+  CAMG_CHECK(cfg.corr_kind >= CAMG_PT_JACOBI && cfg.corr_kind <= CAMG_PT_MCILU0 && cfg.corr_kind != CAMG_PT_CHEBYSHEV,
+             CAMG_ERR_CONFIG, "GPU corrector supports jacobi, sgs, ilu0, direct, mcgs and mcilu0");
+  CAMG_CHECK(cfg.a_hat_mode >= CAMG_AHAT_PLAIN && cfg.a_hat_mode <= CAMG_AHAT_EXACT, CAMG_ERR_CONFIG,
+             "unknown a_hat mode");
   cudaStream_t s = 0;
   std::unique_ptr<Level> L(new Level());
   L->cfg = cfg;
@@ -1914,8 +1974,13 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
   const int mode = (cfg.kind == CAMG_SIMPLEC) ? CAMG_AHAT_ABS_ROWSUM
                    : (cfg.kind == CAMG_BRAESS_SARAZIN) ? CAMG_AHAT_PLAIN
                                                        : cfg.a_hat_mode;
+  L->exact = mode == CAMG_AHAT_EXACT;
   DBuf<double> ahat(nu + 1);
-  if (mode == CAMG_AHAT_ABS_ROWSUM) {
+  if (L->exact) {
+    // A^ = K: A^-1 applications are LU solves, S~ comes from camg_level_set_schur
+    note_launch();
+    k_copy<<<grid_for(nu, 256), 256>>>(nu, dK.p, ahat.p);
+  } else if (mode == CAMG_AHAT_ABS_ROWSUM) {
     csr_diagonal(K, 1, ahat.p, s);
     CAMG_CUDA(cudaDeviceSynchronize());
     check_no_zero(ahat.p, nu, "abs_rowsum lumping");
@@ -1934,8 +1999,8 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     k_scaled_recip<<<grid_for(nu, 256), 256>>>(nu, dK.p, cheb ? 1.0 : cfg.pred_damping, 1.0, L->dinv_p.p);
     if (cheb) setup_chebyshev(L.get(), K, dK.p, cfg.pred_sweeps, s);
   }
-  // Schur approximation (smoothers.py:255-267)
-  {
+  // Schur approximation (smoothers.py:255-267); exact: set later
+  if (!L->exact) {
     DBuf<double> ainv_s(nu + 1);
     double scale = 1.0;
     if (cfg.kind == CAMG_BRAESS_SARAZIN) {
@@ -1948,19 +2013,11 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     L->S = schur(B2, Cz, B1, ainv_s.p, scale, s);
   }
   if (cfg.kind != CAMG_BRAESS_SARAZIN && cfg.pred_kind == CAMG_PT_MCGS) L->gs.setup(K, cfg.node_block, s);
-  // point colouring of S~: the multiplier-node graph needs as many colours
-  // (16 on C5) and the per-node kernels measured slower
-  if (cfg.corr_kind == CAMG_PT_MCGS && nl > 0) L->cgs.setup(L->S, 1, s);
-  if (cfg.corr_kind == CAMG_PT_MCILU0 && nl > 0) L->cilu.setup(L->S, s);
-  if ((cfg.corr_kind == CAMG_PT_JACOBI || cfg.corr_kind == CAMG_PT_MCGS) && nl > 0) {
-    DBuf<double> dS(nl + 1);
-    csr_diagonal(L->S, 0, dS.p, s);
-    CAMG_CUDA(cudaDeviceSynchronize());
-    check_no_zero(dS.p, nl, "jacobi");
-    L->dinv_c = DBuf<double>(nl + 1);
-    note_launch();
-    k_scaled_recip<<<grid_for(nl, 256), 256>>>(nl, dS.p, cfg.corr_damping, 1.0, L->dinv_c.p);
+  if (L->pred_generic() && cfg.pred_kind != CAMG_PT_DIRECT) {
+    L->K_own.reset(csr_copy(K, s));
+    L->pps.setup(L->K_own.get(), cfg.pred_kind, cfg.pred_sweeps, cfg.pred_damping);
   }
+  if (L->S) setup_corrector(L.get());
   // nonempty rows of B1
   {
     DBuf<int32_t> flags(nu + 1);
@@ -1976,7 +2033,7 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     L->n_b1_rows = read_i64(nsel.p);
     L->b1_rows = std::move(out);
   }
-  setup_overlap(L.get());
+  if (!L->exact) setup_overlap(L.get());
   L->alloc_work();
   CAMG_CUDA(cudaDeviceSynchronize());
   return L.release();
@@ -2073,6 +2130,8 @@ struct Hierarchy {
                               &L->cilu.y, &L->cilu.z})
         v.push_back(b);
       if (L->inner) scalar_work_slots(L->inner, v);
+      L->pps.work_slots(v);
+      L->cps.work_slots(v);
     }
     v.push_back(&lu_y);
     v.push_back(&lu_flags);
@@ -2426,7 +2485,10 @@ int camg_level_destroy(camg_level* L) {
 }
 
 int camg_level_schur(const camg_level* L, camg_csr** out) {
-  return guarded([&] { *out = new camg_csr{csr_copy(L->L->S, 0)}; });
+  return guarded([&] {
+    CAMG_CHECK(L->L->S != nullptr, CAMG_ERR_SETUP, "S~ was not set");
+    *out = new camg_csr{csr_copy(L->L->S, 0)};
+  });
 }
 
 int camg_level_operator(const camg_level* L, const camg_csr** out) {
@@ -2443,6 +2505,27 @@ int camg_level_set_corrector_lu(camg_level* L, int64_t n, const double* lu, cons
     L->L->corr_piv = DBuf<int32_t>(n + 1);
     CAMG_CUDA(cudaMemcpy(L->L->corr_lu.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice));
     CAMG_CUDA(cudaMemcpy(L->L->corr_piv.p, piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  });
+}
+
+int camg_level_set_k_lu(camg_level* L, int64_t n, const double* lu, const int32_t* piv) {
+  return guarded([&] {
+    CAMG_CHECK(n == L->L->nu, CAMG_ERR_DIMENSION, "K LU size does not match n_u");
+    L->L->k_lu = DBuf<double>(n * n + 1);
+    L->L->k_piv = DBuf<int32_t>(n + 1);
+    CAMG_CUDA(cudaMemcpy(L->L->k_lu.p, lu, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    CAMG_CUDA(cudaMemcpy(L->L->k_piv.p, piv, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  });
+}
+
+int camg_level_set_schur(camg_level* L, const camg_csr* S) {
+  return guarded([&] {
+    Level* lv = L->L;
+    CAMG_CHECK(lv->exact, CAMG_ERR_CONFIG, "S~ is supplied only for a_hat_mode exact");
+    CAMG_CHECK(lv->S == nullptr, CAMG_ERR_SETUP, "S~ was already set");
+    CAMG_CHECK(S->m->n_rows == lv->nl && S->m->n_cols == lv->nl, CAMG_ERR_DIMENSION, "S~ must be n_lam x n_lam");
+    lv->S = csr_copy(S->m, 0);
+    setup_corrector(lv);
   });
 }
 
@@ -2666,11 +2749,13 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
     if (L->nl == 0) o.corr_path = CAMG_PATH_NONE;
     else if (c.corr_kind == CAMG_PT_DIRECT) o.corr_path = CAMG_PATH_DENSE_LU;
     else if (c.corr_kind == CAMG_PT_MCGS) { o.corr_path = mc_path(L->cgs); o.corr_colors = L->cgs.colors(); }
+    else if (c.corr_kind == CAMG_PT_SGS || c.corr_kind == CAMG_PT_ILU0) o.corr_path = CAMG_PATH_LEX_TRSV;
     else if (c.corr_kind == CAMG_PT_MCILU0) {
       o.corr_path = (L->cilu.cl && c.corr_sweeps == 1) ? CAMG_PATH_CLUSTER : CAMG_PATH_COLOUR_CSR;
       o.corr_colors = L->cilu.colors();
     } else o.corr_path = CAMG_PATH_FUSED;
     if (L->inner) o.pred_path = CAMG_PATH_INNER_AMG;
+    else if (L->pred_generic()) o.pred_path = c.pred_kind == CAMG_PT_DIRECT ? CAMG_PATH_DENSE_LU : CAMG_PATH_LEX_TRSV;
     else if (c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_MCGS) {
       o.pred_path = mc_path(L->gs);
       o.pred_colors = L->gs.colors();
@@ -2733,7 +2818,7 @@ int camg_hierarchy_vcycle_bytes(const camg_hierarchy* Hh, double* bytes_csr, dou
         const int corr_passes = c.corr_kind == CAMG_PT_MCGS ? 2 * c.corr_sweeps
                                 : c.corr_kind == CAMG_PT_MCILU0 ? c.corr_sweeps + std::max(0, c.corr_sweeps - 1)
                                                                 : std::max(0, c.corr_sweeps - 1);
-        const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * L->S->nnz * corr_passes +
+        const double lam = 8.0 * 6 * L->nl + (nnzA - top) * 12.0 + 12.0 * (L->S ? L->S->nnz : 0) * corr_passes +
                            (c.kind != CAMG_UZAWA ? 12.0 * L->B1->nnz : 0.0);
         // Chebyshev keeps d_k between its steps: + write / read of one vector
         const double cheb = (!gs && c.kind != CAMG_BRAESS_SARAZIN && c.pred_kind == CAMG_PT_CHEBYSHEV)

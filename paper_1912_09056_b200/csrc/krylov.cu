@@ -298,7 +298,7 @@ void gmres_run(int64_t n, const Operator& A, const Precond& M, Gmres* ws, const 
     ws = g_gmres_cache.get();
   }
   CAMG_CHECK(ws->n == n && ws->m >= mmax, CAMG_ERR_DIMENSION, "gmres: workspace is smaller than the solve");
-  if (M.any()) ws->ensure_z();
+  if (M.any() && !M.fn) ws->ensure_z();
   Gmres& G = *ws;
   CAMG_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, s));
   const double norm_b = G.norm(b, s);
@@ -314,9 +314,11 @@ void gmres_run(int64_t n, const Operator& A, const Precond& M, Gmres* ws, const 
   std::vector<double> Hm, cs, sn, g, y;
   bool first = true;
   while (total < max_iters && !conv) {
-    // x0 = 0: the first residual is b and its norm is known
+    // x0 = 0: the first residual is b and its norm is known (a caller
+    // callback operator is still applied to x0, the reference's call
+    // sequence, krylov.py:69)
     double beta = norm_b;
-    if (first) {
+    if (first && A.A) {
       CAMG_CUDA(cudaMemcpyAsync(G.r.p, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
     } else {
       G.residual(A, b, x, G.r.p, s);
@@ -334,7 +336,9 @@ void gmres_run(int64_t n, const Operator& A, const Precond& M, Gmres* ws, const 
     note_launch();
     k_scale_into<<<grid_for(n, 256), 256, 0, s>>>(n, G.r.p, beta, G.V.p);
     int used = 0;
-    const bool keep_z = M.any() && G.Z.p;
+    // stored Z replaces the restart-cycle M^-1 (V y) of a native
+    // preconditioner; caller callbacks see the reference's calls (krylov.py:122)
+    const bool keep_z = M.any() && !M.fn && G.Z.p;
     for (int j = 0; j < m; ++j) {
       const double* vj = G.V.p + (int64_t)j * n;
       double* zj = keep_z ? G.Z.p + (int64_t)j * n : G.z.p;

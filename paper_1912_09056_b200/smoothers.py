@@ -5,13 +5,17 @@ native level (`camg_level`): merged operator, S~, inverse diagonals and the
 fused step kernels of `csrc/hierarchy.cu`.  Configuration classes keep the
 reference names, defaults and validation (smoothers.py:29-70).
 
-Inner solves on the GPU: `jacobi` (predictor and corrector) and `direct`
-(corrector, dense LU of S~).  The reference's lexicographic `sgs` / `ilu0`
-are sequential; a block smoother configured with them (the reference default
-`BlockSmootherConfig()` is sgs predictor + ilu0 corrector) runs their
-multicolour GPU variants instead, `sgs -> mcgs`, `ilu0 -> mcilu0`, and says
-so in `BlockSmoother.substitutions` and the hierarchy report (compared with
-the lexicographic reference by convergence: profiles/r02_convergence_table.md).
+Inner solves on the GPU keep the reference's semantics: `jacobi` (fused into
+the row passes), `direct` (dense LU solve; LAPACK factors from the host),
+and the lexicographic `sgs` / `ilu0` (smoothers.py:141-199) as sync-free
+triangular solves in the reference's row order (`csrc/pointsolve.cu`), so the
+reference default `BlockSmootherConfig()` (sgs predictor, ilu0 corrector)
+runs the reference's algorithm and matches it elementwise.  Their
+dependency chains make them latency-bound on large levels; the GPU variants
+below are the fast choices (compared with the lexicographic reference by
+convergence: profiles/r02_convergence_table.md).  `a_hat_mode="exact"`
+(test-scale, smoothers.py:233-236) builds S~ densely on the host from K's LU
+factors and applies A^-1 = K^-1 by dense LU solves on the device.
 The GPU variant
 `mcgs` is the reference's residual-form SSOR applied with rows renumbered by
 a greedy colouring: multicolour symmetric Gauss-Seidel, compared with the
@@ -55,15 +59,16 @@ from .sparse import (
 POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct", "mcgs", "mcilu0", "gpu_chebyshev")
 BLOCK_KINDS = ("uzawa", "braess_sarazin", "simple", "simplec")
 A_HAT_MODES = ("plain_diag", "abs_rowsum", "exact")
-GPU_POINT_KINDS = ("jacobi", "direct")
-GPU_PREDICTOR_KINDS = ("jacobi", "gpu_chebyshev", "mcgs")
-GPU_CORRECTOR_KINDS = ("jacobi", "direct", "mcgs", "mcilu0")
+GPU_POINT_KINDS = ("jacobi", "sgs", "ilu0", "direct")
+GPU_PREDICTOR_KINDS = ("jacobi", "sgs", "ilu0", "direct", "gpu_chebyshev", "mcgs")
+GPU_CORRECTOR_KINDS = ("jacobi", "sgs", "ilu0", "direct", "mcgs", "mcilu0")
 
 # multicolour GPU variants of the reference's sequential inner solves
 GPU_VARIANT = {"sgs": "mcgs", "ilu0": "mcilu0"}
 
 _BLOCK_CODE = {"uzawa": 0, "braess_sarazin": 1, "simple": 2, "simplec": 3}
-_POINT_CODE = {"jacobi": 0, "direct": 3, "gpu_chebyshev": 4, "mcgs": 5, "mcilu0": 6}
+_POINT_CODE = {"jacobi": 0, "sgs": 1, "ilu0": 2, "direct": 3, "gpu_chebyshev": 4, "mcgs": 5, "mcilu0": 6}
+_AHAT_CODE = {"plain_diag": 0, "abs_rowsum": 1, "exact": 2}
 
 
 @dataclass(frozen=True)
@@ -116,10 +121,10 @@ class SchurOperator:
     a_hat_inv_diag: np.ndarray | None
 
 
-def gpu_block_cfg(cfg: BlockSmootherConfig):
-    """The configuration the GPU runs: sequential `sgs` / `ilu0` inner solves
-    replaced by their multicolour variants (same damping; ILU(0) has none).
-    Returns (config, list of substitutions made)."""
+def multicolour_cfg(cfg: BlockSmootherConfig):
+    """`cfg` with the sequential `sgs` / `ilu0` inner solves replaced by their
+    multicolour GPU variants (same damping; ILU(0) has none) -- the fast
+    choice on large levels.  Returns (config, list of substitutions made)."""
     from dataclasses import replace
 
     subs = []
@@ -137,15 +142,13 @@ def gpu_block_cfg(cfg: BlockSmootherConfig):
 
 def native_cfg(cfg: BlockSmootherConfig, node_block: int = 1) -> N.SmootherCfg:
     mode = cfg.effective_a_hat_mode()
-    if mode == "exact":
-        raise ConfigError("a_hat_mode 'exact' (dense K inverse) is not available on the GPU path")
     if cfg.kind != "braess_sarazin" and cfg.predictor.kind not in GPU_PREDICTOR_KINDS:
         raise ConfigError(f"GPU predictor supports {GPU_PREDICTOR_KINDS}, got {cfg.predictor.kind!r}")
     if cfg.corrector.kind not in GPU_CORRECTOR_KINDS:
         raise ConfigError(f"GPU corrector supports {GPU_CORRECTOR_KINDS}, got {cfg.corrector.kind!r}")
     return N.SmootherCfg(
         kind=_BLOCK_CODE[cfg.kind], alpha=float(cfg.alpha), outer_sweeps=int(cfg.outer_sweeps),
-        a_hat_mode=1 if mode == "abs_rowsum" else 0,
+        a_hat_mode=_AHAT_CODE[mode],
         pred_kind=_POINT_CODE.get(cfg.predictor.kind, 0), pred_sweeps=int(cfg.predictor.sweeps),
         pred_damping=float(cfg.predictor.damping),
         corr_kind=_POINT_CODE[cfg.corrector.kind], corr_sweeps=int(cfg.corrector.sweeps),
@@ -165,45 +168,60 @@ class _LevelHandle:
             self.h = None
 
 
+class _PointHandle:
+    __slots__ = ("h",)
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        if self.h and N._lib is not None:
+            N._lib.camg_point_destroy(self.h)
+            self.h = None
+
+
+def _lu_factors(A_dense):
+    """LAPACK LU (scipy.linalg.lu_factor) as (column-major factors, int32
+    pivots); a zero pivot raises like the reference (smoothers.py:176-181)."""
+    lu, piv = lu_factor_quiet(A_dense)
+    if np.any(np.diag(lu) == 0.0):
+        raise SingularMatrixError("direct smoother: singular matrix")
+    return np.asfortranarray(lu), np.ascontiguousarray(piv, dtype=np.int32)
+
+
 class PointSmoother:
-    """Point smoother bound to one matrix (smoothers.py:141-199): jacobi on
-    the device, direct via dense LU."""
+    """Point smoother bound to one matrix (smoothers.py:141-199), executed by
+    libcamg (`camg_point_*`): jacobi, the lexicographic sgs / ilu0 sweeps
+    (sync-free triangular solves in the reference's order; ilu0 factored in
+    the reference's IKJ order), direct (dense LU solve on the device)."""
 
     def __init__(self, cfg: PointSmootherConfig, A: SparseMatrix):
         if cfg.kind not in GPU_POINT_KINDS:
             raise ConfigError(f"GPU point smoother supports {GPU_POINT_KINDS}, got {cfg.kind!r}")
         self.cfg, self.A = cfg, A
-        if cfg.kind == "jacobi":
-            d = diagonal_device(A, "plain")
-            if bool((d == 0).any()):
-                from .errors import SingularMatrixError
-                row = int((d == 0).nonzero()[0])
-                raise SingularMatrixError(f"jacobi: zero diagonal in row {row}")
-            self._dinv = cfg.damping / d
-        else:
-            from .errors import SingularMatrixError
-            self._lu = lu_factor_quiet(A.to_dense())
-            if np.any(np.diag(self._lu[0]) == 0.0):
-                raise SingularMatrixError("direct smoother: singular matrix")
+        h = C.c_void_p()
+        N.call("camg_point_create", A.device, _POINT_CODE[cfg.kind], int(cfg.sweeps), float(cfg.damping),
+               C.byref(h))
+        self._h = _PointHandle(h)
+        if cfg.kind == "direct" and A.num_rows:
+            lu, piv = _lu_factors(A.to_dense())
+            N.call("camg_point_set_lu", h, A.num_rows, lu.ctypes.data_as(C.c_void_p), piv.ctypes.data_as(C.c_void_p))
+
+    def _run(self, x, b):
+        n = self.A.num_rows
+        bd = to_device(b, n)
+        xd = None if x is None else to_device(x, n)
+        out = empty(n)
+        N.call("camg_point_smooth", self._h.h, C.c_void_p(0) if xd is None else ptr(xd), ptr(bd), ptr(out),
+               stream_ptr())
+        return out if is_device(b) else out.cpu().numpy()
 
     def smooth(self, x, b):
-        if self.cfg.kind == "direct":
-            import scipy.linalg
-            sol = scipy.linalg.lu_solve(self._lu, np.asarray(b.cpu() if is_device(b) else b, dtype=np.float64))
-            return to_device(sol) if is_device(b) else sol
-        xd = to_device(x, self.A.num_cols).clone()
-        bd = to_device(b, self.A.num_rows)
-        t = empty(self.A.num_rows)
-        for _ in range(self.cfg.sweeps):
-            t.copy_(bd)
-            N.call("camg_spmv", self.A.device, -1.0, ptr(xd), 1.0, ptr(t), stream_ptr())
-            xd += self._dinv * t
-        return xd if is_device(b) else xd.cpu().numpy()
+        return self._run(x, b)
 
     def apply(self, b):
-        n = self.A.num_rows
-        z = np.zeros(n)
-        return self.smooth(to_device(z) if is_device(b) else z, b)
+        """Approximate A^-1 b from the zero vector (linear in b)."""
+        return self._run(None, b)
 
 
 def build_schur(op, a_hat_mode: str = "plain_diag", alpha: float = 1.0, scale_with_alpha: bool = False,
@@ -212,9 +230,12 @@ def build_schur(op, a_hat_mode: str = "plain_diag", alpha: float = 1.0, scale_wi
     (smoothers.py:220-239)."""
     if isinstance(op, SaddleSystem):
         op = op.op
-    if a_hat_mode == "exact":
-        raise ConfigError("a_hat_mode 'exact' is not available on the GPU path")
     scale = alpha if scale_with_alpha else 1.0
+    if a_hat_mode == "exact":
+        # test-scale (smoothers.py:233-236): dense K inverse, as the reference
+        Kinv = np.linalg.inv(op.K.to_dense())
+        S = scale * (op.Cz.to_dense() + op.B2.to_dense() @ Kinv @ op.B1.to_dense())
+        return SchurOperator(SparseMatrix.from_dense(S), None)
     d = diagonal_device(op.K, "plain" if a_hat_mode == "plain_diag" else "abs_rowsum")
     if bool((d == 0).any()):
         from .errors import SingularMatrixError
@@ -238,7 +259,7 @@ class BlockSmoother:
         if isinstance(op, SaddleSystem):
             op = op.op
         user_cfg = cfg
-        cfg, self.substitutions = gpu_block_cfg(cfg)
+        self.substitutions = []
         inner = None
         if predictor_solver is not None:
             # smoothers.py:277-278: any object with apply(rhs); on the GPU path it
@@ -269,14 +290,23 @@ class BlockSmoother:
         self.predictor_solver = inner
         if inner is not None and cfg.kind != "braess_sarazin":
             N.call("camg_level_set_predictor_solver", h, inner.handle)
+        exact = cfg.effective_a_hat_mode() == "exact"
+        pred_direct = cfg.kind != "braess_sarazin" and inner is None and cfg.predictor.kind == "direct"
+        if exact or pred_direct:
+            # dense LU of K (smoothers.py:176, 272-273): the direct predictor and A^-1
+            Kd = op.K.to_dense()
+            lu, piv = _lu_factors(Kd)
+            N.call("camg_level_set_k_lu", h, op.n_u, lu.ctypes.data_as(C.c_void_p), piv.ctypes.data_as(C.c_void_p))
+        if exact:
+            # S~ = scale (Cz + B2 K^-1 B1) (smoothers.py:233-236), dense, test-scale
+            import scipy.linalg
+            scale = cfg.alpha if cfg.kind in ("simple", "simplec") else 1.0
+            KinvB1 = scipy.linalg.lu_solve((np.asarray(lu), piv), op.B1.to_dense())
+            S = scale * (op.Cz.to_dense() + op.B2.to_dense() @ KinvB1)
+            Ssm = SparseMatrix.from_dense(S)
+            N.call("camg_level_set_schur", h, Ssm.device)
         if cfg.corrector.kind == "direct" and op.n_lam > 0:
-            S = self.schur.S_tilde.to_dense()
-            lu, piv = lu_factor_quiet(S)
-            if np.any(np.diag(lu) == 0.0):
-                from .errors import SingularMatrixError
-                raise SingularMatrixError("direct smoother: singular matrix")
-            lu_f = np.asfortranarray(lu)
-            piv32 = np.ascontiguousarray(piv, dtype=np.int32)
+            lu_f, piv32 = _lu_factors(self.schur.S_tilde.to_dense())
             N.call("camg_level_set_corrector_lu", self._level.h, op.n_lam,
                    lu_f.ctypes.data_as(C.c_void_p), piv32.ctypes.data_as(C.c_void_p))
 

@@ -67,8 +67,9 @@ def same_pattern(A, B):
     return A.shape == B.shape and np.array_equal(A.indptr, B.indptr) and np.array_equal(A.indices, B.indices)
 
 
-GPU_CASES = [c for c in cases() if BY_NAME[c][4].get("predictor", ("jacobi",))[0] == "jacobi"
-             and BY_NAME[c][4].get("corrector", ("jacobi",))[0] in ("jacobi", "direct")]
+# every golden case runs on the GPU with the reference's own inner solves
+# (c2s_simple_sgs_ilu: lexicographic sgs predictor and ilu0 corrector)
+GPU_CASES = list(cases())
 
 
 # ---------------------------------------------------------------------------
@@ -207,16 +208,43 @@ def test_gmres_iterations_vs_reference(name):
         assert np.linalg.norm(g.rhs - A @ x) <= 2e-8 * np.linalg.norm(g.rhs)
 
 
-def test_sequential_smoothers_map_to_multicolour_variants():
-    """Block smoothers run the multicolour variant of a sequential inner
-    solve (reported); a standalone sequential PointSmoother is rejected."""
+@pytest.mark.parametrize("kind,sweeps,damping", [("sgs", 1, 1.0), ("sgs", 2, 0.9), ("ilu0", 1, 1.0),
+                                                 ("ilu0", 3, 1.0), ("jacobi", 2, 0.7), ("direct", 1, 1.0)])
+def test_point_smoother_reference_semantics(kind, sweeps, damping):
+    """PointSmoother with the reference's lexicographic sgs / ilu0 (sync-free
+    triangular solves), jacobi and direct, on K and on S~ of a golden case,
+    against the oracle's restatement of smoothers.py:141-199."""
     from paper_1912_09056_b200.smoothers import PointSmoother
+    g, op, H = gpu_hier("c2s_simple_sgs_ilu")
+    rng = np.random.default_rng(7)
+    for A in (op.K, H.levels[0].smoother.schur.S_tilde):
+        if kind == "direct" and A.num_rows > 3000:
+            continue
+        As = A.to_scipy()
+        x0, b = rng.standard_normal(A.num_rows), rng.standard_normal(A.num_rows)
+        P = PointSmoother(PointSmootherConfig(kind, sweeps, damping), A)
+        Q = O.Point(O.PointCfg(kind, sweeps, damping), As)
+        for x in (None, x0):
+            got = P.apply(b) if x is None else P.smooth(x, b)
+            ref = Q.apply(b) if x is None else Q.smooth(x, b)
+            assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref), (kind, np.linalg.norm(got - ref))
+
+
+def test_reference_default_block_smoother_is_lexicographic():
+    """BlockSmootherConfig() (sgs predictor, ilu0 corrector, smoothers.py:44-50)
+    runs the reference's lexicographic sweeps: no substitution, no report line,
+    and the sweep equals the oracle's."""
     g, op, _ = gpu_hier(GPU_CASES[0])
-    H = setup(op, fine_level_meta(g), HierarchyConfig(max_levels=2),
-              BlockSmootherConfig(kind="simple", predictor=PointSmootherConfig("sgs")))
-    assert H.levels[0].smoother.substitutions == ["predictor sgs -> mcgs", "corrector ilu0 -> mcilu0"]
-    with pytest.raises(ConfigError):
-        PointSmoother(PointSmootherConfig("sgs"), op.K)
+    meta = fine_level_meta(g)
+    H = setup(op, meta, HierarchyConfig(max_levels=2), BlockSmootherConfig(kind="simple", predictor=PointSmootherConfig("sgs")))
+    assert H.levels[0].smoother.substitutions == []
+    assert "GPU variants" not in H.report
+    info = H.level_info(0)
+    assert info["pred_path"] == "lex_trsv" and info["corr_path"] == "lex_trsv"
+    oop, ometa, rhs = O.system_from_generated(g)
+    OH = O.setup(oop, ometa, O.HierCfg(max_levels=2), O.BlockCfg(kind="simple", predictor=O.PointCfg("sgs")))
+    v, ref = H.apply(rhs), OH.apply(rhs)
+    assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
 # ---------------------------------------------------------------------------
