@@ -256,6 +256,13 @@ int camg_hierarchy_create(camg_level** levels, int num_levels, int coarse_solver
 /* merged dense LU of the coarsest operator (hierarchy.py:242-249) */
 int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu_colmajor,
                                  const int32_t* piv);
+/* explicit inverse of the coarsest merged operator (row-major n x n, n <=
+ * 4096; from the same LU factors): the coarse solve becomes two dense GEMVs
+ * with one refinement step, x0 = A^-1 b, x = x0 + A^-1 (b - A x0)
+ * (hierarchy.py:110-113 semantics, O(eps cond) like the LU solve)          */
+int camg_hierarchy_set_coarse_inverse(camg_hierarchy* H, int64_t n, const double* inv_rowmajor);
+/* Hierarchy.solve_coarsest on device vectors (hierarchy.py:108-113)        */
+int camg_hierarchy_coarse_solve(camg_hierarchy* H, const double* b, double* x, void* stream);
 int camg_hierarchy_destroy(camg_hierarchy* H);
 /* one V-cycle from zero: z = M^-1 r  (Hierarchy.apply, hierarchy.py:115-120) */
 int camg_vcycle(camg_hierarchy* H, const double* r, double* z, void* stream);

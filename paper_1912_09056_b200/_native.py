@@ -118,6 +118,8 @@ _SIGS = {
     "camg_level_sweep": (C.c_int, [vp, vp, vp, vp, vp]),
     "camg_hierarchy_create": (C.c_int, [C.POINTER(vp), C.c_int, C.c_int, C.POINTER(vp)]),
     "camg_hierarchy_set_coarse_lu": (C.c_int, [vp, i64, vp, vp]),
+    "camg_hierarchy_set_coarse_inverse": (C.c_int, [vp, i64, vp]),
+    "camg_hierarchy_coarse_solve": (C.c_int, [vp, vp, vp, vp]),
     "camg_hierarchy_destroy": (C.c_int, [vp]),
     "camg_vcycle": (C.c_int, [vp, vp, vp, vp]),
     "camg_hierarchy_use_graph": (C.c_int, [vp, C.c_int]),

@@ -702,6 +702,52 @@ __global__ void __launch_bounds__(256) k_lu_solve_blk(int n, const double* __res
   }
 }
 
+// Coarsest solve through the explicit inverse of the merged coarse operator
+// (computed once at setup from the same LAPACK LU factors): x0 = A^-1 b,
+// r = b - A x0 (sparse coarse operator), x = x0 + A^-1 r.  Two dense GEMVs
+// (every row of A^-1 one warp, b staged in shared memory) replace 2 n
+// dependent substitution steps; the refinement step brings the forward
+// error back to the LU solve's O(eps cond(A)).  out = add + M v.
+__global__ void __launch_bounds__(256) k_dense_gemv(int n, const double* __restrict__ M, const double* __restrict__ v,
+                                                    const double* __restrict__ add, double* __restrict__ out) {
+  CAMG_PDL_ENTRY();
+  extern __shared__ double vs[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const double* row = M + (size_t)r * n;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = lane;
+    for (; c + 96 < n; c += 128) {
+      a0 = fma(__ldg(row + c), vs[c], a0);
+      a1 = fma(__ldg(row + c + 32), vs[c + 32], a1);
+      a2 = fma(__ldg(row + c + 64), vs[c + 64], a2);
+      a3 = fma(__ldg(row + c + 96), vs[c + 96], a3);
+    }
+    for (; c < n; c += 32) a0 = fma(__ldg(row + c), vs[c], a0);
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[r] = add ? add[r] + acc : acc;
+  }
+}
+
+constexpr int kCoarseInvMax = 4096;  // n^2 doubles <= 128 MB (about the L2)
+
+static void dense_gemv(int n, const double* M, const double* v, const double* add, double* out, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    CAMG_CUDA(cudaFuncSetAttribute(k_dense_gemv, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(double) * kCoarseInvMax)));
+    attr = true;
+  }
+  note_launch();
+  launch_k(k_dense_gemv, grid_for((int64_t)n * 32, 256, int64_t(kNumSMs) * 4), 256, sizeof(double) * n, s, n, M, v,
+           add, out);
+}
+
 // the blocked multi-CTA solve needs all nb CTAs resident (they wait on each
 // other): used from kLuBlkMin rows up to 148 row blocks
 constexpr int kLuBlkMin = 192;
@@ -2115,6 +2161,9 @@ struct Hierarchy {
   bool lu_blk = false;
   DBuf<int32_t> lu_perm;
   DBuf<double> lu_y, lu_flags;
+  // explicit inverse of the coarsest operator (k_dense_gemv path) and its
+  // refinement vectors (per workspace)
+  DBuf<double> cinv, c_x0, c_r;
   // per-level vectors: b (rhs), x[2]
   std::vector<DBuf<double>> vb, vx0, vx1, vr;
   bool use_graph = true;
@@ -2135,6 +2184,8 @@ struct Hierarchy {
     }
     v.push_back(&lu_y);
     v.push_back(&lu_flags);
+    v.push_back(&c_x0);
+    v.push_back(&c_r);
     return v;
   }
 
@@ -2162,10 +2213,27 @@ struct Hierarchy {
     }
   }
 
+  void set_coarse_inverse(int64_t n, const double* inv_rowmajor) {
+    CAMG_CHECK(n == n_coarse, CAMG_ERR_DIMENSION, "coarse inverse does not match the LU factors");
+    CAMG_CHECK(n <= kCoarseInvMax, CAMG_ERR_DIMENSION, "coarse inverse larger than 4096 rows");
+    cinv = DBuf<double>(n * n + 1);
+    CAMG_CUDA(cudaMemcpy(cinv.p, inv_rowmajor, sizeof(double) * n * n, cudaMemcpyHostToDevice));
+    c_x0 = DBuf<double>(n + 1);
+    c_r = DBuf<double>(n + 1);
+  }
+
   void coarse_solve(const double* b, double* x, cudaStream_t s) {
     Level* L = levels.back();
     if (coarse_solver == CAMG_COARSE_MERGED_LU) {
       CAMG_CHECK(lu.p != nullptr, CAMG_ERR_SETUP, "coarse LU factors were not set");
+      if (cinv.p) {
+        const int n = (int)n_coarse;
+        dense_gemv(n, cinv.p, b, nullptr, c_x0.p, s);
+        RowEpi e{b, nullptr, c_r.p, nullptr, nullptr, nullptr, 0.0};
+        resid_rows(L->A, int64_t(0), n, c_x0.p, (const double*)nullptr, n, e, false, s);
+        dense_gemv(n, cinv.p, c_r.p, c_x0.p, x, s);
+        return;
+      }
       if (lu_blk) {
         const int nb = (int)((n_coarse + kLuB - 1) / kLuB);
         note_launch();
@@ -2638,6 +2706,22 @@ int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu,
     CAMG_CHECK(n < (1 << 30), CAMG_ERR_DIMENSION, "coarse LU too large");
     CAMG_CHECK(!H->H->def.graph, CAMG_ERR_SETUP, "coarse LU must be set before the first V-cycle");
     H->H->set_coarse_lu(n, lu, piv);
+  });
+}
+
+int camg_hierarchy_set_coarse_inverse(camg_hierarchy* H, int64_t n, const double* inv) {
+  return guarded([&] {
+    CAMG_CHECK(!H->H->def.graph, CAMG_ERR_SETUP, "coarse inverse must be set before the first V-cycle");
+    H->H->set_coarse_inverse(n, inv);
+  });
+}
+
+int camg_hierarchy_coarse_solve(camg_hierarchy* H, const double* b, double* x, void* stream) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_capture_mu);  // the hierarchy's own work vectors
+    H->H->coarse_solve(b, x, (cudaStream_t)stream);
+    H->H->levels.back()->join((cudaStream_t)stream);
+    CAMG_LAUNCH_CHECK();
   });
 }
 
