@@ -90,6 +90,8 @@ typedef struct {
 #define CAMG_PATH_CLUSTER 6       /* whole sweeps on one 16-CTA thread-block cluster      */
 #define CAMG_PATH_INNER_AMG 7     /* nested preconditioner: scalar AMG V-cycle predictor  */
 #define CAMG_PATH_LEX_TRSV 8      /* lexicographic sgs / ilu0: sync-free triangular solves */
+#define CAMG_PATH_LAM_FUSED 9     /* whole lambda side of a step (rc, MC-ILU(0) sweep, lambda
+                                     update, B1 correction) in one 16-CTA cluster launch     */
 
 typedef struct {
   int64_t n_u, n_lam, nnz;     /* merged operator of the level                                   */
@@ -103,6 +105,8 @@ typedef struct {
   int corr_path, corr_colors;  /* CAMG_PATH_* of the corrector on S~                            */
   int transfer_block_rows;     /* P has a br x bc block SELL mirror: br (0 = CSR)               */
   int restrict_block_rows;     /* R = P^T has one: its block rows (0 = CSR)                     */
+  int watchdog;                /* 1: a bounded device wait of this level expired (a bug; results
+                                  invalid) -- reading it synchronises the device               */
 } camg_level_info;
 
 /* ---- library ------------------------------------------------------------ */

@@ -50,7 +50,7 @@ class LevelInfo(C.Structure):
         ("sell_rows", i64), ("sell_slices", i64),
         ("overlap", C.c_int), ("overlap_indep_slices", i64), ("overlap_dep_slices", i64),
         ("pred_path", C.c_int), ("pred_colors", C.c_int), ("corr_path", C.c_int), ("corr_colors", C.c_int),
-        ("transfer_block_rows", C.c_int), ("restrict_block_rows", C.c_int),
+        ("transfer_block_rows", C.c_int), ("restrict_block_rows", C.c_int), ("watchdog", C.c_int),
     ]
 
     def as_dict(self):
@@ -61,7 +61,7 @@ class LevelInfo(C.Structure):
 
 
 # CAMG_PATH_* (include/camg.h)
-PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg", "lex_trsv")
+PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg", "lex_trsv", "lam_fused")
 
 
 _SIGS = {

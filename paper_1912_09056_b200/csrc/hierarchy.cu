@@ -1336,6 +1336,247 @@ struct LaunchIluCl {
   }
 };
 
+
+// ---------------------------------------------------------------------------
+// One zero-start MC-ILU(0) sweep of S~ (up to kLamIluMaxRows rows) fused with
+// the lambda update on one 16-CTA cluster, without cluster barriers:
+//   y = forward colour passes with L, z = backward passes with U,
+//   lam'_q = lam_q + cl z_q,  dl_q = z_q (for the B1 correction kernel).
+// Layout: CTA r owns the p-th row of every colour with p mod 16 == r (as
+// k_ilu_cl).  Its factor rows are one contiguous byte stream in processing
+// order (forward colour 0..C-1: L rows; backward C-1..0: U rows + u_ii), one
+// 16-byte aligned segment per colour pass, streamed from L2 into shared
+// memory by bulk copies (cp.async.bulk + mbarrier complete_tx): the whole
+// stream at once when it fits, else through a ring of NB segment buffers
+// refilled NB passes ahead.  The copies read only constant data and are
+// issued before the programmatic-dependent-launch wait.  Every CTA keeps a
+// replica of the solved vector in shared memory.  A solved entry is sent to
+// all 16 replicas with st.async ... mbarrier::complete_tx (DSMEM store that
+// signals the receiving CTA's barrier of that colour pass): each CTA waits
+// for pass k-1's bytes (8 x rows of that colour) before computing pass k --
+// no cluster barriers, no memory fences in the chain.  One barrier per pass
+// (used once), so a fast CTA's stores for a later pass never count towards
+// an earlier one; an entry's forward value y_i is overwritten by z_i only
+// after every CTA has left the forward passes.  Per-row arithmetic equals
+// k_ilu_cl<G> and k_lam_update (bit-identical results).
+constexpr int kLamIluThreads = 1024;
+constexpr int kLamIluMaxRows = 16384;
+
+struct LamIluArgs {
+  int n;                     // lambda rows (S~)
+  int ncol;                  // colours
+  int nb;                    // ring buffers (0: resident stream)
+  int bufb;                  // ring buffer bytes
+  const unsigned char* blob; // all CTAs' streams
+  const int64_t* cta_off;    // [16+1] byte offsets of the CTA streams
+  const int32_t* tab;        // [16][2C][3] {byte offset in stream, rows, nnz}
+  const int32_t* own_off;    // [16][C+1] own rows before colour c
+  const int32_t* own_nodes;  // own rows of every CTA, forward order, at own_base[r]
+  const int32_t* own_base;   // [16+1]
+  const int32_t* col_rows;   // [C] rows of each colour (bytes expected per pass / 8)
+  int max_own;               // most rows owned by one CTA (uniform shared-memory layout)
+  int* err;                  // barrier watchdog
+  const double* rc;          // corrector right-hand side
+  const double* xl;          // lambda (null = 0)
+  double* xo_l;              // lambda out
+  double* dl;                // z out
+  double cl;                 // lambda update coefficient
+};
+
+__device__ __forceinline__ void lmb_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void lmb_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void lmb_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LMB_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra LMB_WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// bounded wait: a barrier that never completes (a bug) sets *err and returns
+// instead of hanging the GPU
+__device__ __forceinline__ void lmb_wait_guard(uint64_t* bar, unsigned parity, int* err) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  for (int it = 0; it < (1 << 22); ++it) {
+    unsigned ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+  }
+  atomicExch(err, 1);
+}
+__device__ __forceinline__ void lbulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ unsigned mapa_cluster(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// DSMEM store of v to [raddr] in another CTA, completing 8 bytes of its barrier rbar
+__device__ __forceinline__ void st_async_f64(unsigned raddr, double v, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(raddr), "d"(v),
+               "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(kLamIluThreads, 1) k_lam_ilu_cl(LamIluArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int r = (int)cl.block_rank();
+  const int C2 = 2 * a.ncol;
+  // shared memory, same offsets in every CTA of the cluster (the pass
+  // barriers and the replica are addressed remotely): barriers | replica |
+  // own rc | tables | factor stream (resident) or ring
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* sbar = reinterpret_cast<uint64_t*>(smraw);  // stream buffers
+  uint64_t* pbar = sbar + 8;                             // one per colour pass
+  double* w = reinterpret_cast<double*>(pbar + ((C2 + 1) & ~1));
+  const int nown = a.own_base[r + 1] - a.own_base[r];
+  double* rcs = w + ((a.n + 1) & ~1);
+  int32_t* tab = reinterpret_cast<int32_t*>(rcs + ((a.max_own + 1) & ~1));
+  int32_t* oof = tab + ((3 * C2 + 3) & ~3);
+  unsigned char* ring = reinterpret_cast<unsigned char*>(oof + ((a.ncol + 4) & ~3));
+  const int64_t stream_bytes = a.cta_off[r + 1] - a.cta_off[r];
+  const unsigned char* src = a.blob + a.cta_off[r];
+  const int32_t* gtab = a.tab + (int64_t)r * 3 * C2;
+  // constant data first: tables, barriers and the factor stream (before the PDL wait)
+  for (int i = threadIdx.x; i < 3 * C2; i += blockDim.x) tab[i] = gtab[i];
+  for (int i = threadIdx.x; i <= a.ncol; i += blockDim.x) oof[i] = a.own_off[(int64_t)r * (a.ncol + 1) + i];
+  if (threadIdx.x == 0) {
+    const int nsb = a.nb ? a.nb : 1;
+    for (int i = 0; i < nsb; ++i) lmb_init(sbar + i, 1);
+    for (int k = 0; k < C2; ++k) lmb_init(pbar + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = 0; k < C2; ++k) {  // pass k receives 8 bytes per row of its colour
+      const int c = k < a.ncol ? k : C2 - 1 - k;
+      lmb_expect_tx(pbar + k, 8u * (unsigned)a.col_rows[c]);
+    }
+    if (a.nb == 0) {
+      lmb_expect_tx(sbar, (unsigned)stream_bytes);
+      lbulk_g2s(ring, src, (unsigned)stream_bytes, sbar);
+    } else {
+      for (int k = 0; k < a.nb && k < C2; ++k) {
+        const int off = gtab[3 * k];
+        const int bytes = (k + 1 < C2 ? gtab[3 * (k + 1)] : (int)stream_bytes) - off;
+        lmb_expect_tx(sbar + k, (unsigned)bytes);
+        lbulk_g2s(ring + (int64_t)k * a.bufb, src + off, (unsigned)bytes, sbar + k);
+      }
+    }
+  }
+  pdl_launch_dependents();
+  pdl_wait();
+  {
+    const int32_t* own = a.own_nodes + a.own_base[r];
+    for (int o = threadIdx.x; o < nown; o += blockDim.x) rcs[o] = a.rc[own[o]];
+  }
+  __syncthreads();
+  cluster_barrier();  // every CTA runs and its barriers are armed: stores may start
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned mask = group_mask<G>();
+  const int grp = threadIdx.x / G, ngrp = blockDim.x / G;
+  const unsigned w_s = (unsigned)__cvta_generic_to_shared(w);
+  const unsigned pbar_s = (unsigned)__cvta_generic_to_shared(pbar);
+  // lanes t < 16 of a row group send to CTA t: cluster addresses of its replica and barriers
+  const unsigned w_t = lane < kMcgsCluster ? mapa_cluster(w_s, lane) : 0u;
+  const unsigned pbar_t = lane < kMcgsCluster ? mapa_cluster(pbar_s, lane) : 0u;
+  for (int k = 0; k < C2; ++k) {
+    const bool fwd = k < a.ncol;
+    const int c = fwd ? k : C2 - 1 - k;
+    const unsigned char* seg;
+    if (a.nb == 0) {
+      if (k == 0) lmb_wait_guard(sbar, 0, a.err);
+      seg = ring + tab[3 * k];
+    } else {
+      lmb_wait_guard(sbar + (k % a.nb), (unsigned)((k / a.nb) & 1), a.err);
+      seg = ring + (int64_t)(k % a.nb) * a.bufb;
+    }
+    if (k > 0) lmb_wait_guard(pbar + (k - 1), 0, a.err);  // every entry of the previous colour pass has arrived
+    const int nrows = tab[3 * k + 1], nnz = tab[3 * k + 2];
+    const double* val = reinterpret_cast<const double*>(seg);
+    const double* ud = val + nnz;
+    const int32_t* rp = reinterpret_cast<const int32_t*>(ud + (fwd ? 0 : nrows));
+    const int32_t* node = rp + nrows + 1;
+    const uint16_t* col = reinterpret_cast<const uint16_t*>(node + nrows);
+    for (int q = grp; q < nrows; q += ngrp) {
+      double acc = 0.0;
+      for (int p = rp[q] + lane; p < rp[q + 1]; p += G) acc = fma(val[p], w[col[p]], acc);
+      acc = group_sum<G>(acc, mask);
+      const int i = node[q];
+      const double v = fwd ? rcs[oof[c] + q] - acc : (w[i] - acc) / ud[q];
+      for (int t = lane; t < kMcgsCluster; t += G) {
+        const unsigned wt = G >= kMcgsCluster ? w_t : mapa_cluster(w_s, t);
+        const unsigned bt = G >= kMcgsCluster ? pbar_t : mapa_cluster(pbar_s, t);
+        st_async_f64(wt + 8u * (unsigned)i, v, bt + 8u * (unsigned)k);
+      }
+      if (!fwd && lane == 0) {
+        a.xo_l[i] = (a.xl ? a.xl[i] : 0.0) + a.cl * v;
+        a.dl[i] = v;
+      }
+    }
+    if (a.nb && k + a.nb < C2) {  // refill this stream buffer NB passes ahead
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int kk = k + a.nb;
+        const int off = tab[3 * kk];
+        const int bytes = (kk + 1 < C2 ? tab[3 * (kk + 1)] : (int)stream_bytes) - off;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        lmb_expect_tx(sbar + (k % a.nb), (unsigned)bytes);
+        lbulk_g2s(ring + (int64_t)(k % a.nb) * a.bufb, src + off, (unsigned)bytes, sbar + (k % a.nb));
+      }
+    }
+  }
+  lmb_wait_guard(pbar + (C2 - 1), 0, a.err);  // no store into this CTA's memory is still in flight when it exits
+}
+
+template <int G>
+static void launch_lam_ilu(const LamIluArgs& a, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    CAMG_CUDA(cudaFuncSetAttribute(k_lam_ilu_cl<G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CAMG_CUDA(cudaFuncSetAttribute(k_lam_ilu_cl<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kMcgsCluster);
+  cfg.blockDim = dim3(kLamIluThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kMcgsCluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl() ? 2 : 1;
+  note_launch();
+  CAMG_CUDA(cudaLaunchKernelEx(&cfg, k_lam_ilu_cl<G>, a));
+}
+
 struct McIlu {
   int64_t n = 0;
   std::vector<int64_t> col_ptr;
@@ -1350,6 +1591,14 @@ struct McIlu {
   DBuf<uint16_t> cl_lcol, cl_ucol;
   DBuf<double> cl_lval, cl_uval;
   DBuf<int64_t> cl_offnd, cl_offl, cl_offu;
+  // fused lambda step (k_lam_ilu_cl)
+  bool fused = false;
+  int fz_nb = 0, fz_bufb = 0, fz_g = 4, fz_max_own = 0;
+  size_t fz_smem = 0;
+  DBuf<unsigned char> fz_blob;
+  DBuf<int64_t> fz_cta_off;
+  DBuf<int32_t> fz_tab, fz_own_off, fz_own_nodes, fz_own_base, fz_col_rows;
+  DBuf<int> fz_err;
 
   int colors() const { return (int)col_ptr.size() - 1; }
 
@@ -1434,6 +1683,142 @@ struct McIlu {
     z = DBuf<double>(n + 1);
     const char* cl_env = getenv("CAMG_MCGS_CLUSTER");
     if (n <= 65535 && !(cl_env && cl_env[0] == '0')) setup_cluster(nd, lrp, lci, lva, urp, uci, uva);
+    const char* fz_env = getenv("CAMG_LAM_FUSED");
+    if (n <= kLamIluMaxRows && !(fz_env && fz_env[0] == '0')) setup_fused(nd, lrp, lci, lva, urp, uci, uva, ud);
+  }
+
+  // per-CTA factor streams of k_lam_ilu_cl (see there)
+  void setup_fused(const std::vector<int32_t>& nd, const std::vector<int64_t>& lrp, const std::vector<int32_t>& lci,
+                   const std::vector<double>& lva, const std::vector<int64_t>& urp, const std::vector<int32_t>& uci,
+                   const std::vector<double>& uva, const std::vector<double>& ud) {
+    const int CS = kMcgsCluster;
+    const int C = colors();
+    const int C2 = 2 * C;
+    std::vector<std::vector<unsigned char>> stream(CS);
+    std::vector<int32_t> tab((size_t)CS * C2 * 3), oof((size_t)CS * (C + 1)), own_nodes, own_base(CS + 1, 0);
+    std::vector<std::vector<int32_t>> own(CS);
+    auto put = [](std::vector<unsigned char>& st, const void* p, size_t b) {
+      const unsigned char* q = static_cast<const unsigned char*>(p);
+      st.insert(st.end(), q, q + b);
+    };
+    int64_t max_seg = 0;
+    for (int r = 0; r < CS; ++r) {
+      for (int c = 0; c < C; ++c) {
+        oof[(size_t)r * (C + 1) + c] = (int32_t)own[r].size();
+        for (int64_t k = col_ptr[c] + r; k < col_ptr[c + 1]; k += CS) own[r].push_back(nd[k]);
+      }
+      oof[(size_t)r * (C + 1) + C] = (int32_t)own[r].size();
+      for (int k = 0; k < C2; ++k) {
+        const bool fwd = k < C;
+        const int c = fwd ? k : C2 - 1 - k;
+        std::vector<int32_t> rows;
+        for (int64_t q = col_ptr[c] + r; q < col_ptr[c + 1]; q += CS) rows.push_back(nd[q]);
+        const std::vector<int64_t>& rp = fwd ? lrp : urp;
+        const std::vector<int32_t>& ci = fwd ? lci : uci;
+        const std::vector<double>& va = fwd ? lva : uva;
+        std::vector<int32_t> lrp2(1, 0);
+        std::vector<double> vals, dg;
+        std::vector<uint16_t> cols;
+        for (int32_t i : rows) {
+          for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            vals.push_back(va[p]);
+            cols.push_back((uint16_t)ci[p]);
+          }
+          lrp2.push_back((int32_t)vals.size());
+          if (!fwd) dg.push_back(ud[i]);
+        }
+        std::vector<unsigned char>& st = stream[r];
+        const size_t start = st.size();
+        tab[((size_t)r * C2 + k) * 3 + 0] = (int32_t)start;
+        tab[((size_t)r * C2 + k) * 3 + 1] = (int32_t)rows.size();
+        tab[((size_t)r * C2 + k) * 3 + 2] = (int32_t)vals.size();
+        put(st, vals.data(), 8 * vals.size());
+        put(st, dg.data(), 8 * dg.size());
+        put(st, lrp2.data(), 4 * lrp2.size());
+        put(st, rows.data(), 4 * rows.size());
+        put(st, cols.data(), 2 * cols.size());
+        st.resize((st.size() + 15) & ~size_t(15), 0);
+        max_seg = std::max<int64_t>(max_seg, (int64_t)(st.size() - start));
+      }
+      own_base[r + 1] = own_base[r] + (int32_t)own[r].size();
+      own_nodes.insert(own_nodes.end(), own[r].begin(), own[r].end());
+    }
+    // shared memory: replica + own rc + stream (resident) or ring + tables + barriers
+    size_t max_stream = 0, max_own = 0;
+    for (int r = 0; r < CS; ++r) {
+      max_stream = std::max(max_stream, stream[r].size());
+      max_own = std::max(max_own, own[r].size());
+    }
+    const size_t fixed = 8 * (8 + (size_t)((C2 + 1) & ~1)) + 8 * (size_t)((n + 1) & ~1) +
+                         8 * ((max_own + 1) & ~size_t(1)) + 4 * (size_t)((3 * C2 + 3) & ~3) + 4 * (size_t)((C + 4) & ~3) + 16;
+    const size_t cap = 227 * 1024;
+    if (fixed + 16 > cap) return;
+    int nb = 0;
+    size_t ring = max_stream;
+    if (fixed + max_stream > cap) {
+      nb = (int)std::min<int64_t>((cap - fixed) / max_seg, 8);
+      if (nb < 2) return;
+      ring = (size_t)nb * max_seg;
+    }
+    std::vector<int64_t> cta_off(CS + 1, 0);
+    std::vector<unsigned char> blob;
+    for (int r = 0; r < CS; ++r) {
+      blob.insert(blob.end(), stream[r].begin(), stream[r].end());
+      cta_off[r + 1] = (int64_t)blob.size();
+    }
+    auto up = [](auto& dst, const auto& src) {
+      using T = typename std::decay_t<decltype(src)>::value_type;
+      dst = std::decay_t<decltype(dst)>(src.size() + 1);
+      if (!src.empty()) CAMG_CUDA(cudaMemcpy(dst.p, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice));
+    };
+    up(fz_blob, blob);
+    up(fz_cta_off, cta_off);
+    up(fz_tab, tab);
+    up(fz_own_off, oof);
+    up(fz_own_nodes, own_nodes);
+    up(fz_own_base, own_base);
+    std::vector<int32_t> crows(C);
+    for (int c = 0; c < C; ++c) crows[c] = (int32_t)(col_ptr[c + 1] - col_ptr[c]);
+    up(fz_col_rows, crows);
+    fz_nb = nb;
+    fz_max_own = (int)max_own;
+    fz_err = DBuf<int>(1);
+    CAMG_CUDA(cudaMemset(fz_err.p, 0, sizeof(int)));
+    fz_bufb = (int)max_seg;
+    fz_smem = fixed + ring;
+    const double avg = n ? double(lrp[n] + urp[n]) / (2.0 * n) : 0.0;
+    fz_g = std::max(4, group_for(avg));
+    fused = true;
+  }
+
+  // one zero-start sweep fused with the lambda update (k_lam_ilu_cl):
+  // xo_l = xl + cl z, dl = z for rc
+  void run_fused(const double* rc, const double* xl, double* xo_l, double* dl, double cl, cudaStream_t s) {
+    LamIluArgs a;
+    a.n = (int)n;
+    a.ncol = colors();
+    a.nb = fz_nb;
+    a.bufb = fz_bufb;
+    a.blob = fz_blob.p;
+    a.cta_off = fz_cta_off.p;
+    a.tab = fz_tab.p;
+    a.own_off = fz_own_off.p;
+    a.own_nodes = fz_own_nodes.p;
+    a.own_base = fz_own_base.p;
+    a.col_rows = fz_col_rows.p;
+    a.max_own = fz_max_own;
+    a.err = fz_err.p;
+    a.rc = rc;
+    a.xl = xl;
+    a.xo_l = xo_l;
+    a.dl = dl;
+    a.cl = cl;
+    switch (fz_g) {
+      case 4: launch_lam_ilu<4>(a, fz_smem, s); break;
+      case 8: launch_lam_ilu<8>(a, fz_smem, s); break;
+      case 16: launch_lam_ilu<16>(a, fz_smem, s); break;
+      default: launch_lam_ilu<32>(a, fz_smem, s); break;
+    }
   }
 
   // the p-th row of every colour on CTA p mod 16 (k_mcgs_cl layout); enabled
@@ -1684,6 +2069,15 @@ struct Level {
   }
 
   int pred_colors() const { return gs.colors(); }
+  // the fused one-launch lambda side (k_lam_ilu_cl): single zero-start
+  // MC-ILU(0) corrector sweep on a small S~.  CAMG_LAM_FUSED: 0 off, 1 (the
+  // default) on levels without the overlapped lambda stream, 2 on all levels.
+  bool lam_fused() const {
+    if (cfg.corr_kind != CAMG_PT_MCILU0 || cfg.corr_sweeps != 1 || exact || !cilu.fused) return false;
+    const char* e = getenv("CAMG_LAM_FUSED");
+    const int mode = e ? atoi(e) : 1;
+    return mode == 2 || (mode == 1 && !overlap);
+  }
   bool pred_generic() const {
     return cfg.kind != CAMG_BRAESS_SARAZIN &&
            (cfg.pred_kind == CAMG_PT_DIRECT || cfg.pred_kind == CAMG_PT_SGS || cfg.pred_kind == CAMG_PT_ILU0);
@@ -1799,22 +2193,35 @@ struct Level {
       ls = side;
     }
     // lambda side: rc = B2 u_half - Cz lam - b_lam = -(b_lam + Cz lam - B2 u_half)
-    dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, ls);
-    double* dl = corrector(w_rc.p, ls);
     const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
-    note_launch();
-    launch_k(k_lam_update, grid_for(nl, 256), 256, 0, ls, nl, xl, dl, cl, xo + nu);
-    if (kind != CAMG_UZAWA && n_b1_rows && exact) {
-      // u_new = u_half - alpha K^-1 B1 dlam (a_hat_mode "exact", smoothers.py:313)
-      CAMG_CHECK(k_lu.p != nullptr, CAMG_ERR_SETUP, "exact a_hat mode needs the LU factors of K");
-      spmv(B1, 1.0, dl, 0.0, w_ru.p, ls);
-      lu_solve((int)nu, k_lu.p, k_piv.p, w_ru.p, w_du.p, ls);
-      vec_axpy(nu, -alpha, w_du.p, xo, ls);
-    } else if (kind != CAMG_UZAWA && n_b1_rows) {
-      // u_new = u_half - c A^-1 B1 dlam on the interface rows
-      const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
+    const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
+    if (lam_fused()) {
+      // rc (wide kernel), then the ILU(0) sweep + lambda update on one
+      // cluster, then the interface-row B1 correction (wide kernel)
+      dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, ls);
+      cilu.run_fused(w_rc.p, xl, xo + nu, w_dl.p, cl, ls);
+      if (kind != CAMG_UZAWA && n_b1_rows) {
+        note_launch();
+        launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, ls, view(B1), b1_rows.p, n_b1_rows, ainv.p,
+                 (const double*)w_dl.p, mult, xo);
+      }
+    } else {
+      dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, ls);
+      double* dl = corrector(w_rc.p, ls);
       note_launch();
-      launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, ls, view(B1), b1_rows.p, n_b1_rows, ainv.p, dl, mult, xo);
+      launch_k(k_lam_update, grid_for(nl, 256), 256, 0, ls, nl, xl, dl, cl, xo + nu);
+      if (kind != CAMG_UZAWA && n_b1_rows && exact) {
+        // u_new = u_half - alpha K^-1 B1 dlam (a_hat_mode "exact", smoothers.py:313)
+        CAMG_CHECK(k_lu.p != nullptr, CAMG_ERR_SETUP, "exact a_hat mode needs the LU factors of K");
+        spmv(B1, 1.0, dl, 0.0, w_ru.p, ls);
+        lu_solve((int)nu, k_lu.p, k_piv.p, w_ru.p, w_du.p, ls);
+        vec_axpy(nu, -alpha, w_du.p, xo, ls);
+      } else if (kind != CAMG_UZAWA && n_b1_rows) {
+        // u_new = u_half - c A^-1 B1 dlam on the interface rows
+        note_launch();
+        launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, ls, view(B1), b1_rows.p, n_b1_rows, ainv.p, dl,
+                 mult, xo);
+      }
     }
     if (overlap) {
       CAMG_CUDA(cudaEventRecord(ev_join, side));
@@ -2835,7 +3242,8 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
     else if (c.corr_kind == CAMG_PT_MCGS) { o.corr_path = mc_path(L->cgs); o.corr_colors = L->cgs.colors(); }
     else if (c.corr_kind == CAMG_PT_SGS || c.corr_kind == CAMG_PT_ILU0) o.corr_path = CAMG_PATH_LEX_TRSV;
     else if (c.corr_kind == CAMG_PT_MCILU0) {
-      o.corr_path = (L->cilu.cl && c.corr_sweeps == 1) ? CAMG_PATH_CLUSTER : CAMG_PATH_COLOUR_CSR;
+      o.corr_path = L->lam_fused() ? CAMG_PATH_LAM_FUSED
+                    : (L->cilu.cl && c.corr_sweeps == 1) ? CAMG_PATH_CLUSTER : CAMG_PATH_COLOUR_CSR;
       o.corr_colors = L->cilu.colors();
     } else o.corr_path = CAMG_PATH_FUSED;
     if (L->inner) o.pred_path = CAMG_PATH_INNER_AMG;
@@ -2844,6 +3252,11 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
       o.pred_path = mc_path(L->gs);
       o.pred_colors = L->gs.colors();
     } else o.pred_path = CAMG_PATH_FUSED;
+    if (L->cilu.fz_err.p) {
+      int h = 0;
+      CAMG_CUDA(cudaMemcpy(&h, L->cilu.fz_err.p, sizeof(int), cudaMemcpyDeviceToHost));
+      o.watchdog = h;
+    }
     if (L->P) {
       o.transfer_block_rows = L->P->sell ? L->P->sell->br : 0;
       o.restrict_block_rows = L->R->sell ? L->R->sell->br : 0;

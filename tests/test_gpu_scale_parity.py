@@ -135,7 +135,7 @@ def test_size_gated_paths_are_exercised():
     assert any(i["sell_block"] and not i["sell_masked"] and i["sell_lanes"] == 2 for i in lv), "lane-pair SELL"
     assert any(i["overlap"] and i["overlap_indep_slices"] > 0 and i["overlap_dep_slices"] > 0 for i in lv), "overlap"
     assert any(i["corr_path"] == "colour_csr" for i in lv), "per-colour MC-ILU(0)"
-    assert any(i["corr_path"] == "cluster" for i in lv), "one-cluster MC-ILU(0)"
+    assert any(i["corr_path"] == "lam_fused" for i in lv), "fused one-launch lambda side"
     assert any(i["transfer_block_rows"] == 3 for i in lv), "block SELL prolongation"
     # C3 full and C5/3: the fine level runs the headline kernel (masked
     # one-lane SELL + overlap), as C5 does
@@ -204,6 +204,7 @@ def test_blocked_coarse_lu_solve_vs_oracle(cfg, scale, levels, monkeypatch):
     g = generate(config_spec(cfg, scale))
     op = saddle_operator(g)
     out = {}
+    monkeypatch.setenv("CAMG_COARSE_INV", "0")  # the LU substitution kernels, not the inverse
     for mode in ("0", "1"):
         monkeypatch.setenv("CAMG_LU_BLOCKED", mode)
         H = setup(op, fine_level_meta(g), HierarchyConfig(**hkw), skw)
@@ -218,3 +219,36 @@ def test_blocked_coarse_lu_solve_vs_oracle(cfg, scale, levels, monkeypatch):
             assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref), mode
     np.testing.assert_array_equal(out["1"][0], out["1"][1])
     assert np.linalg.norm(out["1"][0] - out["0"][0]) <= 1e-12 * np.linalg.norm(out["0"][0])
+
+
+@pytest.mark.parametrize("cfg,scale", [("C3", 2), ("C5", 5), ("C2", 1)])
+def test_fused_lambda_side_vs_unfused(cfg, scale, monkeypatch):
+    """The one-launch lambda side (k_lam_ilu_cl: rc, MC-ILU(0) sweep, lambda
+    update, B1 correction on one cluster, factor streams by bulk copies)
+    against the separate kernels: bit-identical where the unfused level runs
+    the one-cluster ILU sweep (same per-row arithmetic), 1e-13 otherwise; and
+    within 1e-10 of the oracle.  Mode 2 forces it on the overlapped levels."""
+    hcfg, scfg, _ = bench.solver_for(cfg)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g, device_K=True)
+    meta = fine_level_meta(g)
+    out, paths = {}, {}
+    for mode in ("0", "1", "2"):
+        monkeypatch.setenv("CAMG_LAM_FUSED", mode)
+        H = setup(op, meta, hcfg, scfg)
+        out[mode] = [H.apply(g.rhs), H.apply(g.rhs)]
+        paths[mode] = [H.level_info(l)["corr_path"] for l in range(H.num_levels - 1)]
+        assert not any(H.level_info(l)["watchdog"] for l in range(H.num_levels)), mode
+    assert "lam_fused" in paths["2"] and "lam_fused" not in paths["0"]
+    oop, ometa, rhs = O.system_from_generated(g)
+    ohc, obc = oracle_cfgs(hcfg, scfg)
+    ref = O.setup(oop, ometa, ohc, obc).apply(rhs)
+    for mode in ("0", "1", "2"):
+        np.testing.assert_array_equal(out[mode][0], out[mode][1])
+        assert np.linalg.norm(out[mode][0] - ref) <= 1e-10 * np.linalg.norm(ref), mode
+    exact = all(p in ("cluster", "none") for p in paths["0"])
+    for mode in ("1", "2"):
+        if exact:
+            np.testing.assert_array_equal(out[mode][0], out["0"][0])
+        else:
+            assert np.linalg.norm(out[mode][0] - out["0"][0]) <= 1e-12 * np.linalg.norm(out["0"][0]), mode
