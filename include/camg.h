@@ -92,6 +92,8 @@ typedef struct {
 #define CAMG_PATH_LEX_TRSV 8      /* lexicographic sgs / ilu0: sync-free triangular solves */
 #define CAMG_PATH_LAM_FUSED 9     /* whole lambda side of a step (rc, MC-ILU(0) sweep, lambda
                                      update, B1 correction) in one 16-CTA cluster launch     */
+#define CAMG_PATH_DENSE_INV 10    /* small S~: the zero-start MC-ILU(0) sweep as one dense GEMV
+                                     with the explicit inverse of its factors                */
 
 typedef struct {
   int64_t n_u, n_lam, nnz;     /* merged operator of the level                                   */

@@ -748,6 +748,61 @@ static void dense_gemv(int n, const double* M, const double* v, const double* ad
            add, out);
 }
 
+// Explicit inverse X = (L U)^-1 of the MC-ILU(0) factors of a small S~
+// (setup): thread j solves L U x = e_j over the rows in colour order
+// (forward: unit L, backward: U with diagonal udiag), x = column j of X,
+// stored row-major (X[i][j] at i*n + j: a warp's 32 columns are one
+// coalesced 256-byte row segment; every thread of the warp walks the same
+// factor row, so the factor loads are broadcasts).
+__global__ void __launch_bounds__(128) k_ilu_inverse(int n, const int32_t* __restrict__ nd, CsrView L, CsrView U,
+                                                     const double* __restrict__ udiag, double* __restrict__ X) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int r = 0; r < n; ++r) {
+    const int i = nd[r];
+    double acc = (i == j) ? 1.0 : 0.0;
+    for (int64_t p = L.rowptr[i]; p < L.rowptr[i + 1]; ++p) acc -= L.val[p] * X[(size_t)L.col[p] * n + j];
+    X[(size_t)i * n + j] = acc;
+  }
+  for (int r = n - 1; r >= 0; --r) {
+    const int i = nd[r];
+    double acc = X[(size_t)i * n + j];
+    for (int64_t p = U.rowptr[i]; p < U.rowptr[i + 1]; ++p) acc -= U.val[p] * X[(size_t)U.col[p] * n + j];
+    X[(size_t)i * n + j] = acc / udiag[i];
+  }
+}
+
+// dl = X rc and the lambda update xo_l = xl + cl dl in one GEMV (warp per row)
+__global__ void __launch_bounds__(256) k_dense_gemv_lam(int n, const double* __restrict__ M,
+                                                        const double* __restrict__ v, const double* __restrict__ xl,
+                                                        double cl, double* __restrict__ dl, double* __restrict__ xo_l) {
+  CAMG_PDL_ENTRY();
+  extern __shared__ double vs[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const double* row = M + (size_t)r * n;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int c = lane;
+    for (; c + 96 < n; c += 128) {
+      a0 = fma(__ldg(row + c), vs[c], a0);
+      a1 = fma(__ldg(row + c + 32), vs[c + 32], a1);
+      a2 = fma(__ldg(row + c + 64), vs[c + 64], a2);
+      a3 = fma(__ldg(row + c + 96), vs[c + 96], a3);
+    }
+    for (; c < n; c += 32) a0 = fma(__ldg(row + c), vs[c], a0);
+    double acc = (a0 + a1) + (a2 + a3);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      dl[r] = acc;
+      xo_l[r] = (xl ? xl[r] : 0.0) + cl * acc;
+    }
+  }
+}
+
 // the blocked multi-CTA solve needs all nb CTAs resident (they wait on each
 // other): used from kLuBlkMin rows up to 148 row blocks
 constexpr int kLuBlkMin = 192;
@@ -1360,6 +1415,7 @@ struct LaunchIluCl {
 // after every CTA has left the forward passes.  Per-row arithmetic equals
 // k_ilu_cl<G> and k_lam_update (bit-identical results).
 constexpr int kLamIluThreads = 1024;
+constexpr int64_t kIluDenseMax = 2048;  // S~ rows up to which MC-ILU(0) runs through (L U)^-1 (32 MB)
 constexpr int kLamIluMaxRows = 16384;
 
 struct LamIluArgs {
@@ -1441,8 +1497,8 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
-template <int G>
-__global__ void __launch_bounds__(kLamIluThreads, 1) k_lam_ilu_cl(LamIluArgs a) {
+template <int G, int NT>
+__global__ void __launch_bounds__(NT, 1) k_lam_ilu_cl(LamIluArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
@@ -1551,17 +1607,17 @@ __global__ void __launch_bounds__(kLamIluThreads, 1) k_lam_ilu_cl(LamIluArgs a) 
   lmb_wait_guard(pbar + (C2 - 1), 0, a.err);  // no store into this CTA's memory is still in flight when it exits
 }
 
-template <int G>
-static void launch_lam_ilu(const LamIluArgs& a, size_t smem, cudaStream_t s) {
+template <int G, int NT>
+static void launch_lam_ilu_nt(const LamIluArgs& a, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    CAMG_CUDA(cudaFuncSetAttribute(k_lam_ilu_cl<G>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    CAMG_CUDA(cudaFuncSetAttribute(k_lam_ilu_cl<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    CAMG_CUDA(cudaFuncSetAttribute(k_lam_ilu_cl<G, NT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CAMG_CUDA(cudaFuncSetAttribute(k_lam_ilu_cl<G, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kMcgsCluster);
-  cfg.blockDim = dim3(kLamIluThreads);
+  cfg.blockDim = dim3(NT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -1574,7 +1630,15 @@ static void launch_lam_ilu(const LamIluArgs& a, size_t smem, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = use_pdl() ? 2 : 1;
   note_launch();
-  CAMG_CUDA(cudaLaunchKernelEx(&cfg, k_lam_ilu_cl<G>, a));
+  CAMG_CUDA(cudaLaunchKernelEx(&cfg, k_lam_ilu_cl<G, NT>, a));
+}
+
+template <int G>
+static void launch_lam_ilu(const LamIluArgs& a, size_t smem, cudaStream_t s) {
+  static const int nt = getenv("CAMG_LAMILU_NT") ? atoi(getenv("CAMG_LAMILU_NT")) : kLamIluThreads;
+  if (nt == 256) launch_lam_ilu_nt<G, 256>(a, smem, s);
+  else if (nt == 512) launch_lam_ilu_nt<G, 512>(a, smem, s);
+  else launch_lam_ilu_nt<G, 1024>(a, smem, s);
 }
 
 struct McIlu {
@@ -1599,6 +1663,8 @@ struct McIlu {
   DBuf<int64_t> fz_cta_off;
   DBuf<int32_t> fz_tab, fz_own_off, fz_own_nodes, fz_own_base, fz_col_rows;
   DBuf<int> fz_err;
+  // explicit inverse of the factors (small S~): one GEMV per zero-start sweep
+  DBuf<double> dense_inv;
 
   int colors() const { return (int)col_ptr.size() - 1; }
 
@@ -1685,6 +1751,31 @@ struct McIlu {
     if (n <= 65535 && !(cl_env && cl_env[0] == '0')) setup_cluster(nd, lrp, lci, lva, urp, uci, uva);
     const char* fz_env = getenv("CAMG_LAM_FUSED");
     if (n <= kLamIluMaxRows && !(fz_env && fz_env[0] == '0')) setup_fused(nd, lrp, lci, lva, urp, uci, uva, ud);
+    const char* dn_env = getenv("CAMG_ILU_DENSE_MAX");
+    const int64_t dense_max = dn_env ? atoll(dn_env) : kIluDenseMax;
+    if (n >= 1 && n <= dense_max) {
+      // (L U)^-1 in the original numbering, on the device
+      dense_inv = DBuf<double>((size_t)n * n + 1);
+      note_launch();
+      k_ilu_inverse<<<(unsigned)((n + 127) / 128), 128>>>((int)n, nodes.p, view(L.get()), view(U.get()), udiag.p,
+                                                         dense_inv.p);
+      CAMG_LAUNCH_CHECK();
+      CAMG_CUDA(cudaDeviceSynchronize());
+    }
+  }
+
+  // one zero-start sweep through the explicit inverse fused with the lambda
+  // update: dl = (L U)^-1 rc, xo_l = xl + cl dl
+  void run_dense(const double* rc, const double* xl, double* xo_l, double* dl, double cl, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+      CAMG_CUDA(cudaFuncSetAttribute(k_dense_gemv_lam, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(sizeof(double) * kCoarseInvMax)));
+      attr = true;
+    }
+    note_launch();
+    launch_k(k_dense_gemv_lam, grid_for(n * 32, 256, int64_t(kNumSMs) * 4), 256, sizeof(double) * n, s, (int)n,
+             (const double*)dense_inv.p, rc, xl, cl, dl, xo_l);
   }
 
   // per-CTA factor streams of k_lam_ilu_cl (see there)
@@ -2072,6 +2163,11 @@ struct Level {
   // the fused one-launch lambda side (k_lam_ilu_cl): single zero-start
   // MC-ILU(0) corrector sweep on a small S~.  CAMG_LAM_FUSED: 0 off, 1 (the
   // default) on levels without the overlapped lambda stream, 2 on all levels.
+  // small S~: the zero-start MC-ILU(0) sweep as one GEMV with (L U)^-1
+  bool lam_dense() const {
+    return cfg.corr_kind == CAMG_PT_MCILU0 && cfg.corr_sweeps == 1 && !exact && cilu.dense_inv.p != nullptr &&
+           !overlap;
+  }
   bool lam_fused() const {
     if (cfg.corr_kind != CAMG_PT_MCILU0 || cfg.corr_sweeps != 1 || exact || !cilu.fused) return false;
     const char* e = getenv("CAMG_LAM_FUSED");
@@ -2195,11 +2291,13 @@ struct Level {
     // lambda side: rc = B2 u_half - Cz lam - b_lam = -(b_lam + Cz lam - B2 u_half)
     const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
     const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
-    if (lam_fused()) {
-      // rc (wide kernel), then the ILU(0) sweep + lambda update on one
-      // cluster, then the interface-row B1 correction (wide kernel)
+    if (lam_dense() || lam_fused()) {
+      // rc (wide kernel), then the ILU(0) sweep + lambda update (one GEMV
+      // with the explicit inverse, or one cluster), then the interface-row
+      // B1 correction (wide kernel)
       dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, ls);
-      cilu.run_fused(w_rc.p, xl, xo + nu, w_dl.p, cl, ls);
+      if (lam_dense()) cilu.run_dense(w_rc.p, xl, xo + nu, w_dl.p, cl, ls);
+      else cilu.run_fused(w_rc.p, xl, xo + nu, w_dl.p, cl, ls);
       if (kind != CAMG_UZAWA && n_b1_rows) {
         note_launch();
         launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, ls, view(B1), b1_rows.p, n_b1_rows, ainv.p,
@@ -3242,7 +3340,8 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
     else if (c.corr_kind == CAMG_PT_MCGS) { o.corr_path = mc_path(L->cgs); o.corr_colors = L->cgs.colors(); }
     else if (c.corr_kind == CAMG_PT_SGS || c.corr_kind == CAMG_PT_ILU0) o.corr_path = CAMG_PATH_LEX_TRSV;
     else if (c.corr_kind == CAMG_PT_MCILU0) {
-      o.corr_path = L->lam_fused() ? CAMG_PATH_LAM_FUSED
+      o.corr_path = L->lam_dense() ? CAMG_PATH_DENSE_INV
+                    : L->lam_fused() ? CAMG_PATH_LAM_FUSED
                     : (L->cilu.cl && c.corr_sweeps == 1) ? CAMG_PATH_CLUSTER : CAMG_PATH_COLOUR_CSR;
       o.corr_colors = L->cilu.colors();
     } else o.corr_path = CAMG_PATH_FUSED;

@@ -135,7 +135,7 @@ def test_size_gated_paths_are_exercised():
     assert any(i["sell_block"] and not i["sell_masked"] and i["sell_lanes"] == 2 for i in lv), "lane-pair SELL"
     assert any(i["overlap"] and i["overlap_indep_slices"] > 0 and i["overlap_dep_slices"] > 0 for i in lv), "overlap"
     assert any(i["corr_path"] == "colour_csr" for i in lv), "per-colour MC-ILU(0)"
-    assert any(i["corr_path"] == "lam_fused" for i in lv), "fused one-launch lambda side"
+    assert any(i["corr_path"] == "dense_inv" for i in lv), "MC-ILU(0) through the explicit factor inverse"
     assert any(i["transfer_block_rows"] == 3 for i in lv), "block SELL prolongation"
     # C3 full and C5/3: the fine level runs the headline kernel (masked
     # one-lane SELL + overlap), as C5 does
@@ -233,6 +233,7 @@ def test_fused_lambda_side_vs_unfused(cfg, scale, monkeypatch):
     op = saddle_operator(g, device_K=True)
     meta = fine_level_meta(g)
     out, paths = {}, {}
+    monkeypatch.setenv("CAMG_ILU_DENSE_MAX", "0")  # the cluster kernel, not the dense inverse
     for mode in ("0", "1", "2"):
         monkeypatch.setenv("CAMG_LAM_FUSED", mode)
         H = setup(op, meta, hcfg, scfg)
@@ -252,3 +253,28 @@ def test_fused_lambda_side_vs_unfused(cfg, scale, monkeypatch):
             np.testing.assert_array_equal(out[mode][0], out["0"][0])
         else:
             assert np.linalg.norm(out[mode][0] - out["0"][0]) <= 1e-12 * np.linalg.norm(out["0"][0]), mode
+
+
+@pytest.mark.parametrize("cfg,scale", [("C3", 1), ("C5", 5), ("C2", 1)])
+def test_dense_inverse_ilu_vs_sweeps(cfg, scale, monkeypatch):
+    """Small S~ (<= 2048 rows, levels without the overlapped lambda stream):
+    the zero-start MC-ILU(0) sweep applied as one GEMV with (L U)^-1 of the
+    same factors, against the colour-pass sweeps (1e-12) and the oracle's
+    emulation (V-cycle 1e-10)."""
+    hcfg, scfg, _ = bench.solver_for(cfg)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g, device_K=True)
+    meta = fine_level_meta(g)
+    out, paths = {}, {}
+    for dmax in ("0", "2048"):
+        monkeypatch.setenv("CAMG_ILU_DENSE_MAX", dmax)
+        monkeypatch.setenv("CAMG_LAM_FUSED", "0")
+        H = setup(op, meta, hcfg, scfg)
+        out[dmax] = H.apply(g.rhs)
+        paths[dmax] = [H.level_info(l)["corr_path"] for l in range(H.num_levels - 1)]
+    assert "dense_inv" in paths["2048"] and "dense_inv" not in paths["0"]
+    oop, ometa, rhs = O.system_from_generated(g)
+    ohc, obc = oracle_cfgs(hcfg, scfg)
+    ref = O.setup(oop, ometa, ohc, obc).apply(rhs)
+    assert np.linalg.norm(out["2048"] - ref) <= 1e-10 * np.linalg.norm(ref)
+    assert np.linalg.norm(out["2048"] - out["0"]) <= 1e-12 * np.linalg.norm(out["0"])
