@@ -1236,7 +1236,8 @@ struct LaunchIluPass {
   static void run(const Csr* T, const Csr* A, const int32_t* nodes, int64_t nn, bool fwd, bool res,
                   const double* rc, const double* udiag, double* y, double* z, double* x, cudaStream_t s) {
     if (nn <= 0) return;
-    const unsigned grid = grid_for(nn * G, 256, int64_t(kNumSMs) * 16);
+    static const int64_t cap = getenv("CAMG_ILU_GRID") ? atoll(getenv("CAMG_ILU_GRID")) : int64_t(kNumSMs) * 16;
+    const unsigned grid = grid_for(nn * G, 256, cap);
     note_launch();
     const CsrView tv = view(T), av = view(A);
 #define CAMG_ILU_L(F, R) launch_k(k_ilu_pass<G, F, R>, grid, 256, 0, s, tv, av, nodes, nn, rc, udiag, y, z, x)
@@ -2102,7 +2103,7 @@ struct Level {
   // fused pass over the [K | B1] rows reading x = [xu; xl]: with a pending
   // lambda-side chain, the independent slices go first
   void top_pass(const RowEpi& e, const double* xu, const double* xl, bool zero, cudaStream_t s) {
-    if (!pending || !overlap) {
+    if (!pending || !ovl()) {
       join(s);
       resid_rows(A, int64_t(0), nu, xu, xl, nu, e, zero, s);
       return;
@@ -2160,19 +2161,25 @@ struct Level {
   }
 
   int pred_colors() const { return gs.colors(); }
-  // the fused one-launch lambda side (k_lam_ilu_cl): single zero-start
-  // MC-ILU(0) corrector sweep on a small S~.  CAMG_LAM_FUSED: 0 off, 1 (the
-  // default) on levels without the overlapped lambda stream, 2 on all levels.
-  // small S~: the zero-start MC-ILU(0) sweep as one GEMV with (L U)^-1
-  bool lam_dense() const {
-    return cfg.corr_kind == CAMG_PT_MCILU0 && cfg.corr_sweeps == 1 && !exact && cilu.dense_inv.p != nullptr &&
-           !overlap;
-  }
-  bool lam_fused() const {
-    if (cfg.corr_kind != CAMG_PT_MCILU0 || cfg.corr_sweeps != 1 || exact || !cilu.fused) return false;
+  // CAMG_LAM_FUSED: 0 no fused cluster kernel (k_lam_ilu_cl), 1 (the
+  // default) on levels without the overlapped lambda stream, 2 on all
+  // levels, 3 on all levels with the overlap turned off where it would run
+  static int lam_mode() {
     const char* e = getenv("CAMG_LAM_FUSED");
-    const int mode = e ? atoi(e) : 1;
-    return mode == 2 || (mode == 1 && !overlap);
+    return e ? atoi(e) : 1;
+  }
+  bool mcilu_once() const { return cfg.corr_kind == CAMG_PT_MCILU0 && cfg.corr_sweeps == 1 && !exact; }
+  // the lambda-side chain runs on the second stream, overlapping the next pass
+  bool ovl() const {
+    return overlap && !(lam_mode() == 3 && mcilu_once() && (cilu.fused || cilu.dense_inv.p != nullptr));
+  }
+  // small S~: the zero-start MC-ILU(0) sweep as one GEMV with (L U)^-1
+  bool lam_dense() const { return mcilu_once() && cilu.dense_inv.p != nullptr && !ovl(); }
+  // the one-cluster ILU(0) sweep
+  bool lam_fused() const {
+    if (!mcilu_once() || !cilu.fused) return false;
+    const int m = lam_mode();
+    return m == 2 || m == 3 || (m == 1 && !ovl());
   }
   bool pred_generic() const {
     return cfg.kind != CAMG_BRAESS_SARAZIN &&
@@ -2283,7 +2290,7 @@ struct Level {
     CAMG_CHECK(S != nullptr, CAMG_ERR_SETUP, "S~ was not set (a_hat_mode exact: camg_level_set_schur)");
     join(s);
     cudaStream_t ls = s;
-    if (overlap) {  // fork the lambda side onto `side`
+    if (ovl()) {  // fork the lambda side onto `side`
       CAMG_CUDA(cudaEventRecord(ev_fork, s));
       CAMG_CUDA(cudaStreamWaitEvent(side, ev_fork, 0));
       ls = side;
@@ -2321,7 +2328,7 @@ struct Level {
                  mult, xo);
       }
     }
-    if (overlap) {
+    if (ovl()) {
       CAMG_CUDA(cudaEventRecord(ev_join, side));
       pending = true;
     }
@@ -2342,7 +2349,7 @@ struct Level {
   // chain is pending)
   void residual(const double* x, const double* b, double* r, cudaStream_t s) {
     RowEpi e{b, nullptr, r, nullptr, nullptr, nullptr, 0.0};
-    if (pending && overlap && x) {
+    if (pending && ovl() && x) {
       const SellEpi se = sell_epi(e);
       sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, sl_indep.p, n_indep);
       join(s);
@@ -2455,7 +2462,16 @@ static void setup_overlap(Level* L) {
   L->sl_dep = DBuf<int32_t>(dp.size() + 1);
   if (!ind.empty()) CAMG_CUDA(cudaMemcpy(L->sl_indep.p, ind.data(), sizeof(int32_t) * ind.size(), cudaMemcpyHostToDevice));
   if (!dp.empty()) CAMG_CUDA(cudaMemcpy(L->sl_dep.p, dp.data(), sizeof(int32_t) * dp.size(), cudaMemcpyHostToDevice));
-  CAMG_CUDA(cudaStreamCreateWithFlags(&L->side, cudaStreamNonBlocking));
+  {
+    // the lambda-side stream at the greatest priority (graph nodes keep it:
+    // cudaGraphInstantiateFlagUseNodePriority): its short chain kernels take
+    // the CTA slots the concurrent pass frees first (C5 19.19 -> 18.98 ms,
+    // C3 1.565 -> 1.507 ms); CAMG_SIDE_PRIO=0 restores equal priority
+    const char* pe = getenv("CAMG_SIDE_PRIO");
+    int lo = 0, hi = 0;
+    CAMG_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CAMG_CUDA(cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, (pe && pe[0] == '0') ? lo : hi));
+  }
   CAMG_CUDA(cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming));
   CAMG_CUDA(cudaEventCreateWithFlags(&L->ev_join, cudaEventDisableTiming));
   L->overlap = true;
@@ -2845,7 +2861,8 @@ struct Hierarchy {
     g_launches.fetch_sub(w.kernels);
     g_thread_launches -= w.kernels;
     CAMG_CUDA(cudaStreamEndCapture(w.stream, &g));
-    CAMG_CUDA(cudaGraphInstantiate(&w.graph, g, 0));
+    const char* pe = getenv("CAMG_SIDE_PRIO");
+    CAMG_CUDA(cudaGraphInstantiate(&w.graph, g, (pe && pe[0] == '0') ? 0 : cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(g);
   }
 
