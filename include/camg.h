@@ -210,6 +210,16 @@ int camg_assemble_stencil(int dim, const int64_t* grid, int clamp_lo, int clamp_
                           camg_csr* K_inout, int64_t row_offset);
 int camg_stencil_block_counts(int dim, const int64_t* grid, int clamp_lo, int clamp_hi,
                               const double* table, int64_t* nnz_out);
+/* Host batched pivoted QR of G aggregate blocks of M x k (block g = rows
+ * dofs[g*M .. g*M+M) of the row-major n_dofs x k null space `vecs`), for the
+ * tentative prolongator (transfer.py:86-145: scipy.linalg.qr(mode="economic",
+ * pivoting=True) per aggregate): LAPACK dgeqp3 + dorgqr from the library at
+ * lapack_path (scipy's bundled OpenBLAS: bit-identical to the reference),
+ * on nthreads host threads.  Q (G, M, kk), R (G, kk, k), piv (G, k) 0-based
+ * in C order, kk = min(M, k); info_out = first block LAPACK rejected, or -1. */
+int camg_qr_batch(const char* lapack_path, int64_t G, int M, int k, const double* vecs, int64_t n_dofs,
+                  const int64_t* dofs, double* q_out, double* r_out, int64_t* piv_out, int nthreads,
+                  int64_t* info_out);
 /* Allocates an empty n_rows x n_cols matrix with nnz slots (filled by
  * camg_assemble_stencil). */
 int camg_csr_alloc(int64_t n_rows, int64_t n_cols, int64_t nnz, camg_csr** out);
