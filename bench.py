@@ -32,18 +32,19 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 # ncu dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per
 # launch, from profiles/ (one `ncu --set full` capture; None until measured)
 TRAFFIC = {
-    # profiles/r01_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1> (masked
-    # slots, 64-thread CTAs), C5, dram__bytes_read.sum 13.422817 GB +
-    # dram__bytes_write.sum 0.175971 GB
-    "C5": 13.598788e9,
+    # profiles/r02_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1> (masked
+    # slots, 64-thread CTAs), C5, dram__bytes_read.sum 13.422556 GB +
+    # dram__bytes_write.sum 0.176220 GB, 2.062 ms
+    "C5": 13.598776e9,
 }
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 # DRAM bytes of one whole V-cycle summed over its ncu launch list (dram__bytes_read.sum +
 # dram__bytes_write.sum per kernel, serialised, cold cache) and the cycle time of the
 # same build: the measured (not modelled) V-cycle bandwidth
 VCYCLE_DRAM = {
-    "C5": {"dram_bytes_per_cycle": 111.6e9, "source": "profiles/r01_vcycle_launches_c5.csv "
-           "(round-1 build; VERDICT r01 recomputed 5.68 TB/s = 0.87 of measured peak at 19.66 ms)"},
+    "C5": {"dram_bytes_per_cycle": 111.70e9, "source": "profiles/r02_vcycle_launches_C5.csv (522 kernels, one cycle)"},
+    "C3": {"dram_bytes_per_cycle": 4.16e9, "source": "profiles/r02_vcycle_launches_C3.csv (283 kernels, one cycle)"},
+    "C2": {"dram_bytes_per_cycle": 0.35e9, "source": "profiles/r02_vcycle_launches_C2.csv (57 kernels, one cycle)"},
 }
 
 # BASELINE.json's literal smoother per config and why the bench runs another
@@ -670,7 +671,14 @@ def run_gpu(args):
                             "frac_of_measured_peak": vc_fmt_gbs / peak, "frac_of_8TBs": vc_fmt_gbs / 8000.0,
                             "bytes": "format bytes of every sparse application and vector stream of one cycle "
                                      "(camg_hierarchy_vcycle_bytes), zero-vector products skipped",
-                            "dram_measured": VCYCLE_DRAM.get(args.config),
+                            "dram_measured": (dict(VCYCLE_DRAM[args.config],
+                                                   achieved_gbs=VCYCLE_DRAM[args.config]["dram_bytes_per_cycle"]
+                                                   / (vc_ms * 1e-3) / 1e9,
+                                                   frac_of_measured_peak=VCYCLE_DRAM[args.config]["dram_bytes_per_cycle"]
+                                                   / (vc_ms * 1e-3) / 1e9 / peak,
+                                                   frac_of_8TBs=VCYCLE_DRAM[args.config]["dram_bytes_per_cycle"]
+                                                   / (vc_ms * 1e-3) / 1e9 / 8000.0)
+                                              if args.config in VCYCLE_DRAM and args.scale == 1 else None),
                             "model_bytes_per_cycle": bytes_csr, "model_achieved": vc_gbs,
                             "model": "SURVEY.md §8(d): 12 B/nnz + index/vector terms, zero products skipped",
                             "kernels_per_cycle": H.kernels_per_cycle()},
