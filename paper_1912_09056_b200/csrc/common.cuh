@@ -41,6 +41,24 @@ void set_last_error(const std::string& msg);
 
 #define CAMG_LAUNCH_CHECK() CAMG_CUDA(cudaGetLastError())
 
+// Device-side bounds / invariant checks of the checked build (`make checked`
+// -> libcamg_checked.so, -DCAMG_CHECKED; load it with CAMG_LIB): a failed
+// check prints its site and traps (the launch fails with an error).  The
+// substitute for compute-sanitizer, which this GPU pool does not allow.
+#ifdef CAMG_CHECKED
+#define CAMG_DCHECK(cond, what)                                                          \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("camg device check failed: %s (%s:%d)\n", what, __FILE__, __LINE__);        \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define CAMG_DCHECK(cond, what) \
+  do {                          \
+  } while (0)
+#endif
+
 // Run `body` and translate exceptions into status codes.
 template <class F>
 int guarded(F&& body) {

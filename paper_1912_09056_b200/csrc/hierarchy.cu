@@ -711,6 +711,7 @@ __global__ void __launch_bounds__(256) k_lu_solve_blk(int n, const double* __res
 __global__ void __launch_bounds__(256) k_dense_gemv(int n, const double* __restrict__ M, const double* __restrict__ v,
                                                     const double* __restrict__ add, double* __restrict__ out) {
   CAMG_PDL_ENTRY();
+  CAMG_DCHECK(n >= 0 && n <= 4096, "dense gemv size beyond its shared-memory staging");
   extern __shared__ double vs[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v[i];
   __syncthreads();
@@ -777,6 +778,7 @@ __global__ void __launch_bounds__(256) k_dense_gemv_lam(int n, const double* __r
                                                         const double* __restrict__ v, const double* __restrict__ xl,
                                                         double cl, double* __restrict__ dl, double* __restrict__ xo_l) {
   CAMG_PDL_ENTRY();
+  CAMG_DCHECK(n >= 0 && n <= 4096, "dense gemv size beyond its shared-memory staging");
   extern __shared__ double vs[];
   for (int i = threadIdx.x; i < n; i += blockDim.x) vs[i] = v[i];
   __syncthreads();
@@ -1204,8 +1206,10 @@ __global__ void __launch_bounds__(256) k_ilu_pass(CsrView T, CsrView A, const in
   bool waited = false;
   for (int64_t k = tid / G; k < nn; k += stride) {
     const int64_t i = nodes[k];
+    CAMG_DCHECK(i >= 0 && i < T.n_rows, "ilu pass row out of range");
     const int64_t p0 = T.rowptr[i] + lane, p1 = T.rowptr[i + 1];
     const int32_t c0 = p0 < p1 ? T.col[p0] : 0;
+    CAMG_DCHECK(c0 >= 0 && c0 < T.n_cols, "ilu factor column out of range");
     const double v0 = p0 < p1 ? T.val[p0] : 0.0;
     if (!waited) {
       pdl_wait();
@@ -1577,11 +1581,16 @@ __global__ void __launch_bounds__(NT, 1) k_lam_ilu_cl(LamIluArgs a) {
     const int32_t* rp = reinterpret_cast<const int32_t*>(ud + (fwd ? 0 : nrows));
     const int32_t* node = rp + nrows + 1;
     const uint16_t* col = reinterpret_cast<const uint16_t*>(node + nrows);
+    CAMG_DCHECK(tab[3 * k] + 8ll * nnz + 4ll * (nrows + 1) <= stream_bytes, "lam_ilu segment beyond its stream");
     for (int q = grp; q < nrows; q += ngrp) {
       double acc = 0.0;
-      for (int p = rp[q] + lane; p < rp[q + 1]; p += G) acc = fma(val[p], w[col[p]], acc);
+      for (int p = rp[q] + lane; p < rp[q + 1]; p += G) {
+        CAMG_DCHECK(p < nnz && col[p] < a.n, "lam_ilu entry out of range");
+        acc = fma(val[p], w[col[p]], acc);
+      }
       acc = group_sum<G>(acc, mask);
       const int i = node[q];
+      CAMG_DCHECK(i >= 0 && i < a.n, "lam_ilu row out of range");
       const double v = fwd ? rcs[oof[c] + q] - acc : (w[i] - acc) / ud[q];
       for (int t = lane; t < kMcgsCluster; t += G) {
         const unsigned wt = G >= kMcgsCluster ? w_t : mapa_cluster(w_s, t);

@@ -102,6 +102,7 @@ __device__ __forceinline__ double row_dot(const CsrView& A, int64_t row, const d
   double acc = 0.0;
   for (int64_t p = s + lane; p < e; p += G) {
     const int32_t c = __ldcs(A.col + p);
+    CAMG_DCHECK(c >= 0 && c < A.n_cols, "csr column index out of range");
     acc = fma(__ldcs(A.val + p), xload<SPLIT>(xu, xl, split, c), acc);
   }
   return acc;

@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(256) k_sptrsv(int64_t n, CsrView T, const doub
     double acc = 0.0;
     for (int64_t q = s0 + lane; q < e0; q += 32) {
       const int32_t j = T.col[q];
+      CAMG_DCHECK(j >= 0 && j < n && (LOWER ? j < i : j > i), "triangular solve column out of range / wrong side");
       const double a = T.val[q];
       unsigned f = ld_acquire_u32(flags + j);
       int spins = 0;

@@ -295,6 +295,8 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   exclusive_scan_i64(cnt.p, S->voff, slots, s);
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t groups = read_i64(S->voff + slots);
+  S->ngroups = groups;
+  S->ncb = (A->n_cols + BC - 1) / BC;
   S->bcol = dalloc<int32_t>((size_t)slots * 32);
   S->bval = dalloc<double>((size_t)groups * 32);
   CAMG_CUDA(cudaMemsetAsync(S->bval, 0, sizeof(double) * (size_t)groups * 32, s));
@@ -415,6 +417,7 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? CAMG_MASKED_MINB : (BR
       const int64_t base = S.slice_ptr[s];
       auto load_x = [&](int64_t slot, double* xv, uint32_t lin = 0) {
         const int32_t bc = lin ? (int32_t)(lin - 1) + lane : __ldcs(S.bcol + slot * 32 + lane);
+        CAMG_DCHECK(bc >= 0 && (S.ncb == 0 || bc < S.ncb), "sell block column out of range");
         const double* xs;
         if (!SPLIT || bc < split_blocks) xs = xu + (int64_t)bc * BC;
         else xs = xl ? xl + ((int64_t)bc - split_blocks) * BC : nullptr;
@@ -454,6 +457,8 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? CAMG_MASKED_MINB : (BR
 #pragma unroll
             for (int q = 0; q < BE; ++q) {
               const int g = (int)((m >> (4 * q)) & 15u);
+              CAMG_DCHECK(!g || S.ngroups == 0 || (v - S.bval - lane) / 32 + g - 1 < S.ngroups,
+                          "sell value group out of range");
               val[q] = __ldcs(g ? v + (g - 1) * 32 : S.zero + lane);
             }
 #pragma unroll
@@ -561,6 +566,8 @@ template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                        const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
   SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->zero, S->nbr, S->nslices};
+  v.ncb = S->ncb;
+  v.ngroups = S->masked ? S->ngroups : 0;
   v.slist = slist;
   v.nwork = slist ? nlist : S->nslices;
   if (v.nwork <= 0) return;

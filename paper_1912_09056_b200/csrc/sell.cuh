@@ -10,6 +10,8 @@ struct Sell {
   int br = 0, bc = 0;                 // block rows x block columns
   bool masked = false;                // per-slot union masks (else full blocks)
   int64_t nbr = 0, nslices = 0, slots = 0, used_blocks = 0;
+  int64_t ncb = 0;                    // block columns of the vector read (checked build)
+  int64_t ngroups = 0;                // 32-double value groups stored (checked build)
   double pass_bytes = 0.0;            // compulsory bytes of one pass over the blocks
   int64_t* slice_ptr = nullptr;       // slot offset of each slice (nslices+1)
   uint8_t* len = nullptr;             // blocks per block row
@@ -38,6 +40,7 @@ struct SellView {
   int64_t nbr, nslices;
   const int32_t* __restrict__ slist = nullptr;  // optional subset of slices to process
   int64_t nwork = 0;                            // slices to process (slist length, or nslices)
+  int64_t ncb = 0, ngroups = 0;                 // bounds for the checked build (0: unknown)
 };
 
 // epilogue arguments of the three SELL row kernels (modes 0/1/2)

@@ -288,8 +288,19 @@ def test_live_oracle_parity(cfg, scale, hkw, skw):
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
 
 
+# the benchmarked smoother (bench.solver_for C2-C5: SIMPLE(0.8)x3, Jacobi(1,0.6)
+# predictor, MC-ILU(0) corrector) on small systems with every size-gated
+# path forced on
+BENCH_SMOOTHER_CASES = [
+    ("C5", 10, dict(max_levels=4, max_coarse_size=50),
+     dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcilu0", 1, 1.0))),
+    ("C3", 4, dict(max_levels=3, max_coarse_size=50),
+     dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcilu0", 1, 1.0))),
+]
+
+
 @pytest.mark.parametrize("masked", ["1", "0"])
-@pytest.mark.parametrize("cfg,scale,hkw,skw", [LIVE[2], LIVE[3], LIVE[1]])
+@pytest.mark.parametrize("cfg,scale,hkw,skw", [LIVE[2], LIVE[3], LIVE[1]] + BENCH_SMOOTHER_CASES)
 def test_sell_block_path_parity(cfg, scale, hkw, skw, masked, monkeypatch):
     """Force the block SELL-32 mirror on every level that has uniform node
     blocks (masked slots, the default, and full blocks) and check the
@@ -297,6 +308,7 @@ def test_sell_block_path_parity(cfg, scale, hkw, skw, masked, monkeypatch):
     import paper_1912_09056_b200.hierarchy as hmod
     monkeypatch.setattr(hmod, "SELL_MIN_ROWS", 0)
     monkeypatch.setenv("CAMG_SELL_MASKED", masked)
+    monkeypatch.setenv("CAMG_SELL_MIN_BLOCK_ROWS", "0")  # block SELL restriction too
     if masked == "1":  # one lane per row everywhere, so small levels get masked slots too
         monkeypatch.setenv("CAMG_SELL_PAIR", "0")
     g = generate(config_spec(cfg, scale))
