@@ -166,6 +166,10 @@ int camg_csr_scale_rows(const camg_csr* A, const double* s, camg_csr** out);
 int camg_power_step(const camg_csr* A, const double* d, const double* v, double* w, void* stream);
 /* v = w / s */
 int camg_vec_scale_div(int64_t n, const double* w, double s, double* v, void* stream);
+/* lambda_max(D^-1 A) of estimate_lambda_max (transfer.py:148-161) with the
+ * norms taken on the device (the Python path takes them with numpy on the
+ * host, bit-identical to the reference); d = device diag(A) or NULL        */
+int camg_lambda_max(const camg_csr* A, const double* d, int iters, double* out);
 /* P = P_tent - (omega/lam_max) * (diag(1/d) A) P_tent  (transfer.py:164-183) */
 int camg_smooth_prolongator(const camg_csr* P_tent, const camg_csr* A, const double* d,
                             double omega_eff, camg_csr** out);
@@ -277,6 +281,11 @@ int camg_hierarchy_set_coarse_lu(camg_hierarchy* H, int64_t n, const double* lu_
  * with one refinement step, x0 = A^-1 b, x = x0 + A^-1 (b - A x0)
  * (hierarchy.py:110-113 semantics, O(eps cond) like the LU solve)          */
 int camg_hierarchy_set_coarse_inverse(camg_hierarchy* H, int64_t n, const double* inv_rowmajor);
+/* LU factors (LAPACK dgetrf semantics, partial pivoting) and, up to 4096
+ * rows and when `inverse`, the explicit inverse of the coarsest merged
+ * operator computed on the device: replaces set_coarse_lu / set_coarse_inverse
+ * for hosts without LAPACK (hierarchy.py:242-249)                          */
+int camg_hierarchy_coarse_factor(camg_hierarchy* H, int inverse);
 /* Hierarchy.solve_coarsest on device vectors (hierarchy.py:108-113)        */
 int camg_hierarchy_coarse_solve(camg_hierarchy* H, const double* b, double* x, void* stream);
 int camg_hierarchy_destroy(camg_hierarchy* H);

@@ -87,6 +87,7 @@ _SIGS = {
     "camg_power_step": (C.c_int, [vp, vp, vp, vp, vp]),
     "camg_vec_scale_div": (C.c_int, [i64, vp, f64, vp, vp]),
     "camg_smooth_prolongator": (C.c_int, [vp, vp, vp, f64, C.POINTER(vp)]),
+    "camg_lambda_max": (C.c_int, [vp, vp, C.c_int, C.POINTER(f64)]),
     "camg_schur": (C.c_int, [vp, vp, vp, vp, f64, C.POINTER(vp)]),
     "camg_node_graph": (C.c_int, [vp, vp, i64, vp, f64, C.POINTER(vp), P64]),
     "camg_pattern_to_host": (C.c_int, [vp, vp, vp]),
@@ -120,6 +121,7 @@ _SIGS = {
     "camg_hierarchy_set_coarse_lu": (C.c_int, [vp, i64, vp, vp]),
     "camg_hierarchy_set_coarse_inverse": (C.c_int, [vp, i64, vp]),
     "camg_hierarchy_coarse_solve": (C.c_int, [vp, vp, vp, vp]),
+    "camg_hierarchy_coarse_factor": (C.c_int, [vp, C.c_int]),
     "camg_hierarchy_destroy": (C.c_int, [vp]),
     "camg_vcycle": (C.c_int, [vp, vp, vp, vp]),
     "camg_hierarchy_use_graph": (C.c_int, [vp, C.c_int]),

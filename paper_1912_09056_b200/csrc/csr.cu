@@ -498,6 +498,23 @@ double lambda_max_dinv(const Csr* A, const double* d, int iters, cudaStream_t s)
 
 }  // namespace camg
 
+// lambda_max(D^-1 A) by `iters` power steps from ones/sqrt(n) with device
+// norms (transfer.py:148-161) for hosts that do not reproduce numpy's norm;
+// d = diag(A) on the device (null: extracted here)
+extern "C" int camg_lambda_max(const camg_csr* A, const double* d, int iters, double* out) {
+  return camg::guarded([&] {
+    const camg::Csr* M = A->m;
+    CAMG_CHECK(M->n_rows == M->n_cols, CAMG_ERR_DIMENSION, "lambda_max: square matrix required");
+    camg::DBuf<double> dd;
+    if (!d) {
+      dd = camg::DBuf<double>(M->n_rows + 1);
+      camg::csr_diagonal(M, 0, dd.p, 0);
+      d = dd.p;
+    }
+    *out = camg::lambda_max_dinv(M, d, iters, 0);
+  });
+}
+
 using namespace camg;
 
 // ---------------------------------------------------------------------------

@@ -737,6 +737,108 @@ __global__ void __launch_bounds__(256) k_dense_gemv(int n, const double* __restr
 
 constexpr int kCoarseInvMax = 4096;  // n^2 doubles <= 128 MB (about the L2)
 
+// ---------------------------------------------------------------------------
+// Device factorization of the coarsest merged operator (hierarchy.py:242-249:
+// scipy.linalg.lu_factor, i.e. LAPACK dgetrf semantics: P A = L U with
+// partial pivoting, the first maximal |a_ik| as pivot (idamax), whole rows
+// swapped, 0-based pivot rows in ipiv order), for hosts without LAPACK
+// (camg_hierarchy_coarse_factor).  Right-looking, one cooperative grid with
+// three grid-wide barriers per column: (1) every CTA finds the pivot
+// redundantly and the grid swaps rows k and p; (2) multipliers l_i =
+// a_ik / a_kk; (3) rank-1 update of the trailing block.  The factors differ
+// from dgetrf's blocked order only in rounding.
+
+__global__ void k_csr_to_dense_colmajor(CsrView A, double* __restrict__ D) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.n_rows; i += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t p = A.rowptr[i]; p < A.rowptr[i + 1]; ++p) D[(size_t)A.col[p] * A.n_rows + i] = A.val[p];
+}
+
+__global__ void __launch_bounds__(256) k_dense_lu(int n, double* __restrict__ A, int32_t* __restrict__ piv,
+                                                  double* __restrict__ lk) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sv[8];
+  __shared__ int si[8];
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = 0; k < n; ++k) {
+    // (1) pivot: first maximal |a_ik|, i >= k (every CTA, same result)
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+      const double a = fabs(A[(size_t)k * n + i]);
+      if (a > best) { best = a; bi = i; }  // i ascending per thread: first max kept
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    if (lane == 0) { sv[w] = best; si[w] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < (int)(blockDim.x >> 5); ++q)
+        if (sv[q] > sv[0] || (sv[q] == sv[0] && si[q] < si[0])) { sv[0] = sv[q]; si[0] = si[q]; }
+    }
+    __syncthreads();
+    const int p = si[0] < n ? si[0] : k;
+    if (tid == 0) piv[k] = p;
+    if (p != k)
+      for (int64_t j = tid; j < n; j += nthr) {
+        const double t = A[(size_t)j * n + k];
+        A[(size_t)j * n + k] = A[(size_t)j * n + p];
+        A[(size_t)j * n + p] = t;
+      }
+    grid.sync();
+    // (2) multipliers
+    const double akk = A[(size_t)k * n + k];
+    for (int64_t i = k + 1 + tid; i < n; i += nthr) {
+      const double l = akk != 0.0 ? A[(size_t)k * n + i] / akk : 0.0;
+      lk[i] = l;
+      A[(size_t)k * n + i] = l;
+    }
+    grid.sync();
+    // (3) trailing update A[i][j] -= l_i a_kj, i, j > k (column-major: i fastest)
+    const int64_t m = n - k - 1;
+    for (int64_t e = tid; e < m * m; e += nthr) {
+      const int64_t j = k + 1 + e / m, i = k + 1 + e % m;
+      A[(size_t)j * n + i] -= lk[i] * A[(size_t)j * n + k];
+    }
+    grid.sync();
+  }
+}
+
+// X = A^-1 (row-major) from LAPACK-style factors: thread j solves for column
+// j (permute e_j by the row swaps, unit-lower forward, upper backward); the
+// column lives in X[., j], so a warp's stores are coalesced and its factor
+// loads broadcast
+__global__ void __launch_bounds__(128) k_lu_inverse(int n, const double* __restrict__ LU, const int32_t* __restrict__ piv,
+                                                    double* __restrict__ X) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  for (int i = 0; i < n; ++i) X[(size_t)i * n + j] = (i == j) ? 1.0 : 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int p = piv[i];
+    if (p != i) {
+      const double t = X[(size_t)i * n + j];
+      X[(size_t)i * n + j] = X[(size_t)p * n + j];
+      X[(size_t)p * n + j] = t;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    double acc = X[(size_t)i * n + j];
+    for (int k = 0; k < i; ++k) acc -= LU[(size_t)k * n + i] * X[(size_t)k * n + j];
+    X[(size_t)i * n + j] = acc;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double acc = X[(size_t)i * n + j];
+    for (int k = i + 1; k < n; ++k) acc -= LU[(size_t)k * n + i] * X[(size_t)k * n + j];
+    X[(size_t)i * n + j] = acc / LU[(size_t)i * n + i];
+  }
+}
+
 static void dense_gemv(int n, const double* M, const double* v, const double* add, double* out, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
@@ -1241,10 +1343,12 @@ struct LaunchIluPass {
                   const double* rc, const double* udiag, double* y, double* z, double* x, cudaStream_t s) {
     if (nn <= 0) return;
     static const int64_t cap = getenv("CAMG_ILU_GRID") ? atoll(getenv("CAMG_ILU_GRID")) : int64_t(kNumSMs) * 16;
-    const unsigned grid = grid_for(nn * G, 256, cap);
+    // CTA size of the colour passes (CAMG_ILU_BLOCK, 64 / 128 / 256)
+    static const int blk = getenv("CAMG_ILU_BLOCK") ? atoi(getenv("CAMG_ILU_BLOCK")) : 256;
+    const unsigned grid = grid_for(nn * G, blk, cap * 256 / blk);
     note_launch();
     const CsrView tv = view(T), av = view(A);
-#define CAMG_ILU_L(F, R) launch_k(k_ilu_pass<G, F, R>, grid, 256, 0, s, tv, av, nodes, nn, rc, udiag, y, z, x)
+#define CAMG_ILU_L(F, R) launch_k(k_ilu_pass<G, F, R>, grid, blk, 0, s, tv, av, nodes, nn, rc, udiag, y, z, x)
     if (fwd) { if (res) CAMG_ILU_L(true, true); else CAMG_ILU_L(true, false); }
     else { if (res) CAMG_ILU_L(false, true); else CAMG_ILU_L(false, false); }
 #undef CAMG_ILU_L
@@ -2752,6 +2856,44 @@ struct Hierarchy {
     c_r = DBuf<double>(n + 1);
   }
 
+  // LU (and, up to kCoarseInvMax rows, the inverse) of the coarsest merged
+  // operator computed on the device (no host LAPACK)
+  void coarse_factor(bool inverse) {
+    const Csr* A = levels.back()->A;
+    const int n = (int)A->n_rows;
+    CAMG_CHECK(n >= 1 && n < 46341, CAMG_ERR_DIMENSION, "coarse operator too large for a dense factorization");
+    DBuf<double> D((size_t)n * n + 1), lk(n + 1);
+    DBuf<int32_t> pv(n + 1);
+    CAMG_CUDA(cudaMemset(D.p, 0, sizeof(double) * (size_t)n * n));
+    note_launch(2);
+    k_csr_to_dense_colmajor<<<grid_for(n, 256), 256>>>(view(A), D.p);
+    CAMG_LAUNCH_CHECK();
+    int per_sm = 0;
+    CAMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_lu, 256, 0));
+    const int64_t want = ((int64_t)n * n + 255) / 256;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)kNumSMs * std::max(1, per_sm)));
+    int nn = n;
+    double* dp = D.p;
+    int32_t* pp = pv.p;
+    double* lp = lk.p;
+    void* args[] = {&nn, &dp, &pp, &lp};
+    CAMG_CUDA(cudaLaunchCooperativeKernel((void*)k_dense_lu, blocks, 256, args, 0, 0));
+    CAMG_CUDA(cudaDeviceSynchronize());
+    std::vector<double> lu_h((size_t)n * n);
+    std::vector<int32_t> piv_h(n);
+    CAMG_CUDA(cudaMemcpy(lu_h.data(), D.p, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost));
+    CAMG_CUDA(cudaMemcpy(piv_h.data(), pv.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+    set_coarse_lu(n, lu_h.data(), piv_h.data());
+    if (inverse && n <= kCoarseInvMax) {
+      cinv = DBuf<double>((size_t)n * n + 1);
+      k_lu_inverse<<<(n + 127) / 128, 128>>>(n, lu.p, piv.p, cinv.p);
+      CAMG_LAUNCH_CHECK();
+      CAMG_CUDA(cudaDeviceSynchronize());
+      c_x0 = DBuf<double>(n + 1);
+      c_r = DBuf<double>(n + 1);
+    }
+  }
+
   void coarse_solve(const double* b, double* x, cudaStream_t s) {
     Level* L = levels.back();
     if (coarse_solver == CAMG_COARSE_MERGED_LU) {
@@ -3244,6 +3386,14 @@ int camg_hierarchy_set_coarse_inverse(camg_hierarchy* H, int64_t n, const double
   return guarded([&] {
     CAMG_CHECK(!H->H->def.graph, CAMG_ERR_SETUP, "coarse inverse must be set before the first V-cycle");
     H->H->set_coarse_inverse(n, inv);
+  });
+}
+
+int camg_hierarchy_coarse_factor(camg_hierarchy* H, int inverse) {
+  return guarded([&] {
+    CAMG_CHECK(!H->H->def.graph, CAMG_ERR_SETUP, "coarse factors must be set before the first V-cycle");
+    CAMG_CHECK(H->H->coarse_solver == CAMG_COARSE_MERGED_LU, CAMG_ERR_CONFIG, "coarse solver is not merged_lu");
+    H->H->coarse_factor(inverse != 0);
   });
 }
 

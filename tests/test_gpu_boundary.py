@@ -265,3 +265,47 @@ def test_setup_report_matches_reference(name):
     z = load(name)
     _, _, H = gpu_hier(name)
     assert H.report == str(z["report"])
+
+
+@pytest.mark.parametrize("cfg,scale,levels", [("C2", 4, 3), ("C5", 10, 2), ("C1", 1, 2)])
+def test_device_coarse_factorization_matches_lapack(cfg, scale, levels, monkeypatch):
+    """camg_hierarchy_coarse_factor (device LU with partial pivoting + inverse,
+    the default) against host LAPACK factors (CAMG_COARSE_HOST=1,
+    scipy.linalg.lu_factor as hierarchy.py:242-249): same pivots on these
+    systems, coarse solves within 1e-12, V-cycles within 1e-11."""
+    import scipy.linalg
+    from paper_1912_09056_b200.sparse import BlockVector
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    meta = fine_level_meta(g)
+    hc = HierarchyConfig(max_levels=levels, max_coarse_size=50)
+    sc = BlockSmootherConfig(kind="uzawa", alpha=0.6, predictor=PointSmootherConfig("jacobi", 2, 0.6),
+                             corrector=PointSmootherConfig("jacobi", 1, 0.6))
+    out = {}
+    for host in ("1", "0"):
+        monkeypatch.setenv("CAMG_COARSE_HOST", host)
+        H = setup(op, meta, hc, sc)
+        out[host] = (H, H.apply(g.rhs))
+    Hd = out["0"][0]
+    cop = Hd.levels[-1].op
+    dense = cop.merged_dense()
+    lu = scipy.linalg.lu_factor(dense)
+    b = np.random.default_rng(1).standard_normal(cop.total_rows)
+    xb = Hd.solve_coarsest(BlockVector.zeros(cop.n_u, cop.n_lam), BlockVector.from_merged(b, cop.n_u)).merged()
+    ref = scipy.linalg.lu_solve(lu, b)
+    assert np.linalg.norm(xb - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert np.linalg.norm(out["0"][1] - out["1"][1]) <= 1e-11 * np.linalg.norm(out["1"][1])
+
+
+def test_device_lambda_max_matches_host_norms():
+    """camg_lambda_max (device norms, for non-Python hosts) against the
+    package's estimate_lambda_max (host numpy norms, bit-identical to the
+    reference, transfer.py:148-161): equal to 1e-13."""
+    import ctypes as C
+    from paper_1912_09056_b200.transfer import estimate_lambda_max
+    g = generate(config_spec("C4", 8))
+    op = saddle_operator(g)
+    ref = estimate_lambda_max(op.K)
+    out = C.c_double()
+    _native.call("camg_lambda_max", op.K.device, None, 10, C.byref(out))
+    assert abs(out.value - ref) <= 1e-13 * ref
