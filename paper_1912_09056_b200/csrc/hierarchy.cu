@@ -810,33 +810,52 @@ __global__ void __launch_bounds__(256) k_dense_lu(int n, double* __restrict__ A,
   }
 }
 
-// X = A^-1 (row-major) from LAPACK-style factors: thread j solves for column
-// j (permute e_j by the row swaps, unit-lower forward, upper backward); the
-// column lives in X[., j], so a warp's stores are coalesced and its factor
-// loads broadcast
-__global__ void __launch_bounds__(128) k_lu_inverse(int n, const double* __restrict__ LU, const int32_t* __restrict__ piv,
-                                                    double* __restrict__ X) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  for (int i = 0; i < n; ++i) X[(size_t)i * n + j] = (i == j) ? 1.0 : 0.0;
-  for (int i = 0; i < n; ++i) {
-    const int p = piv[i];
-    if (p != i) {
-      const double t = X[(size_t)i * n + j];
-      X[(size_t)i * n + j] = X[(size_t)p * n + j];
-      X[(size_t)p * n + j] = t;
+// X = A^-1 (row-major) from LAPACK-style factors on one cooperative grid:
+// X = P I, then the unit-lower forward elimination row by row (X[i] -= l_ik
+// X[k], i > k) and the backward one (X[k] /= u_kk; X[i] -= u_ik X[k], i < k),
+// every step a rank-1 row update spread over the grid (coalesced rows).
+__global__ void __launch_bounds__(256) k_lu_inverse_coop(int n, const double* __restrict__ LU,
+                                                         const int32_t* __restrict__ piv, double* __restrict__ X,
+                                                         int32_t* __restrict__ perm) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) {  // row i of P A is row perm[i] of A (LAPACK's sequential swaps)
+    for (int i = 0; i < n; ++i) perm[i] = i;
+    for (int i = 0; i < n; ++i) {
+      const int p = piv[i];
+      const int32_t t = perm[i];
+      perm[i] = perm[p];
+      perm[p] = t;
     }
   }
-  for (int i = 0; i < n; ++i) {
-    double acc = X[(size_t)i * n + j];
-    for (int k = 0; k < i; ++k) acc -= LU[(size_t)k * n + i] * X[(size_t)k * n + j];
-    X[(size_t)i * n + j] = acc;
+  grid.sync();
+  for (int64_t e = tid; e < (int64_t)n * n; e += nthr) {  // X = P (rows of the identity)
+    const int64_t i = e / n, j = e % n;
+    X[e] = (perm[i] == j) ? 1.0 : 0.0;
   }
-  for (int i = n - 1; i >= 0; --i) {
-    double acc = X[(size_t)i * n + j];
-    for (int k = i + 1; k < n; ++k) acc -= LU[(size_t)k * n + i] * X[(size_t)k * n + j];
-    X[(size_t)i * n + j] = acc / LU[(size_t)i * n + i];
+  grid.sync();
+  for (int k = 0; k < n - 1; ++k) {
+    const int64_t m = n - k - 1;
+    for (int64_t e = tid; e < m * n; e += nthr) {
+      const int64_t i = k + 1 + e / n, j = e % n;
+      X[i * n + j] -= LU[(size_t)k * n + i] * X[(int64_t)k * n + j];
+    }
+    grid.sync();
   }
+  for (int k = n - 1; k >= 0; --k) {
+    const double ukk = LU[(size_t)k * n + k];
+    for (int64_t j = tid; j < n; j += nthr) X[(int64_t)k * n + j] /= ukk;
+    grid.sync();
+    for (int64_t e = tid; e < (int64_t)k * n; e += nthr) {
+      const int64_t i = e / n, j = e % n;
+      X[i * n + j] -= LU[(size_t)k * n + i] * X[(int64_t)k * n + j];
+    }
+    grid.sync();
+  }
+}
+
 }
 
 static void dense_gemv(int n, const double* M, const double* v, const double* add, double* out, cudaStream_t s) {
@@ -2886,8 +2905,17 @@ struct Hierarchy {
     set_coarse_lu(n, lu_h.data(), piv_h.data());
     if (inverse && n <= kCoarseInvMax) {
       cinv = DBuf<double>((size_t)n * n + 1);
-      k_lu_inverse<<<(n + 127) / 128, 128>>>(n, lu.p, piv.p, cinv.p);
-      CAMG_LAUNCH_CHECK();
+      DBuf<int32_t> perm(n + 1);
+      int pb = 0;
+      CAMG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pb, k_lu_inverse_coop, 256, 0));
+      const int ib = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)n * n + 255) / 256,
+                                                                 (int64_t)kNumSMs * std::max(1, pb)));
+      const double* lup = lu.p;
+      const int32_t* pvp = piv.p;
+      double* xp = cinv.p;
+      int32_t* prp = perm.p;
+      void* iargs[] = {&nn, &lup, &pvp, &xp, &prp};
+      CAMG_CUDA(cudaLaunchCooperativeKernel((void*)k_lu_inverse_coop, ib, 256, iargs, 0, 0));
       CAMG_CUDA(cudaDeviceSynchronize());
       c_x0 = DBuf<double>(n + 1);
       c_r = DBuf<double>(n + 1);
