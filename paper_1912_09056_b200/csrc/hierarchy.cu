@@ -856,8 +856,6 @@ __global__ void __launch_bounds__(256) k_lu_inverse_coop(int n, const double* __
   }
 }
 
-}
-
 static void dense_gemv(int n, const double* M, const double* v, const double* add, double* out, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
