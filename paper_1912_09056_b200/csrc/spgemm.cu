@@ -307,7 +307,8 @@ __device__ __forceinline__ int owner_of(int64_t incl, int64_t f, bool act) {
 
 // (R*A)*P for one row: hash1 holds RA with first-touch groups, hash2 the result
 __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P, int64_t row, Hash h1,
-                           Hash h2, int lane, uint32_t limit1, uint32_t limit2, double* sp) {
+                           Hash h2, int lane, uint32_t limit1, uint32_t limit2, double* sp, int32_t* bk,
+                           double* bv, bool sorted_ra) {
   hash_clear(h1, lane);
   hash_clear(h2, lane);
   const int64_t rs = R.rowptr[row], re = R.rowptr[row + 1];
@@ -363,8 +364,120 @@ __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P,
   }
   // ---- stage 2: RA in scipy's stored order = descending (first-touch group,
   // column) -- csr_matmat's reverse first-touch linked list, exact zeros
-  // dropped.  Compact the table, bitonic-sort it by that key, then stream
-  // the entries times their P rows as ordered 32-wide chunks.
+  // dropped -- times the P rows, as ordered 32-wide chunks into h2.
+  // expand(cnt): the first cnt (<= 32) RA entries (bk, bv) in order
+  auto expand = [&](int cnt) -> bool {
+    const int e = lane;
+    double rav = 0.0;
+    int64_t pb = 0, pl = 0;
+    if (e < cnt) {
+      const int32_t t = bk[e];
+      rav = bv[e];
+      pb = P.rowptr[t];
+      pl = P.rowptr[t + 1] - pb;
+    }
+    int64_t incl = pl;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
+    for (int64_t f0 = 0; f0 < T; f0 += 32) {
+      if (c2 + 32 > limit2) return false;
+      const int64_t f = f0 + lane;
+      const bool act = f < T;
+      const int o = owner_of(incl, f, act);
+      const int64_t before = __shfl_sync(0xffffffffu, incl - pl, o);
+      const int64_t ob = __shfl_sync(0xffffffffu, pb, o);
+      const double ov = __shfl_sync(0xffffffffu, rav, o);
+      int32_t key = -1;
+      double prod = 0.0;
+      if (act) {
+        const int64_t pp = ob + (f - before);
+        key = P.col[pp];
+        prod = __dmul_rn(ov, P.val[pp]);
+      }
+      c2 += chunk_accumulate(h2, act, key, prod, 0, lane, sp);
+    }
+    return true;
+  };
+  if (!sorted_ra) {
+    // Sort-free enumeration of that order: walk R's row backwards (groups
+    // of 32 entries, then A-row chunks from the last) and each 32-entry
+    // chunk of an A row from its end, lane 0 on the highest column; a
+    // column is emitted at the A row of its first touch (h1.ft == q), so
+    // every RA entry appears once, in descending (group, column) order.
+    // Emitted entries queue in (bk, bv) and expand 32 at a time.
+    int nb = 0;
+    const int64_t last0 = ((nR - 1) / 32) * 32;
+    for (int64_t w0 = last0; w0 >= 0; w0 -= 32) {
+      const int64_t qq = w0 + lane;
+      int64_t aq = 0, lq = 0;
+      if (qq < nR) {
+        const int32_t j = R.col[rs + qq];
+        aq = A.rowptr[j];
+        lq = A.rowptr[j + 1] - aq;
+      }
+      const int64_t nch = (lq + 31) >> 5;
+      int64_t incl = nch;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
+      // column of this lane at step st (-1: none) and the step's A row q;
+      // the next step's column load is issued before this step's lookups
+      auto col_at = [&](int64_t st, int& q) -> int32_t {
+        const int o = owner_of(incl, st, true);
+        const int64_t c = st - (__shfl_sync(0xffffffffu, incl - nch, o));
+        const int64_t a = __shfl_sync(0xffffffffu, aq, o);
+        const int64_t l = __shfl_sync(0xffffffffu, lq, o);
+        const int64_t off = 32 * c + 31 - lane;
+        q = (int)(w0 + o);
+        return (off >= 0 && off < l) ? A.col[a + off] : -1;
+      };
+      int qn = 0;
+      int32_t tn = T > 0 ? col_at(T - 1, qn) : -1;
+      for (int64_t st = T - 1; st >= 0; --st) {
+        const int32_t t = tn;
+        const int q = qn;
+        if (st > 0) tn = col_at(st - 1, qn);
+        bool emit = false;
+        double v = 0.0;
+        if (t >= 0) {
+          const int sl = hash_find(h1, t);
+          if (sl >= 0 && h1.ft[sl] == (int16_t)q) {
+            v = h1.vals[sl];
+            emit = v != 0.0;
+          }
+        }
+        const unsigned em = __ballot_sync(0xffffffffu, emit);
+        if (emit) {
+          const int pos = nb + __popc(em & ((1u << lane) - 1u));
+          bk[pos] = t;
+          bv[pos] = v;
+        }
+        nb += __popc(em);
+        __syncwarp();
+        if (nb >= 32) {
+          if (!expand(32)) return false;
+          __syncwarp();
+          if (lane < nb - 32) {
+            bk[lane] = bk[32 + lane];
+            bv[lane] = bv[32 + lane];
+          }
+          nb -= 32;
+          __syncwarp();
+        }
+      }
+    }
+    if (nb > 0 && !expand(nb)) return false;
+    return true;
+  }
+  // (CAMG_RAP_SORT=1) compact the table, bitonic-sort it by that key, then
+  // expand it in chunks of 32
   int n1 = 0;
   for (uint32_t base = 0; base < h1.cap; base += 32) {
     const uint32_t sl = base + lane;
@@ -406,39 +519,14 @@ __device__ bool row_triple(const CsrView& R, const CsrView& A, const CsrView& P,
     }
   }
   for (int e0 = 0; e0 < n1; e0 += 32) {
-    const int e = e0 + lane;
-    double rav = 0.0;
-    int64_t pb = 0, pl = 0;
-    if (e < n1) {
-      const int32_t t = h1.keys[e];
-      rav = h1.vals[e];
-      pb = P.rowptr[t];
-      pl = P.rowptr[t + 1] - pb;
+    const int cnt = min(32, n1 - e0);
+    __syncwarp();
+    if (lane < cnt) {
+      bk[lane] = h1.keys[e0 + lane];
+      bv[lane] = h1.vals[e0 + lane];
     }
-    int64_t incl = pl;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    const int64_t T = __shfl_sync(0xffffffffu, incl, 31);
-    for (int64_t f0 = 0; f0 < T; f0 += 32) {
-      if (c2 + 32 > limit2) return false;
-      const int64_t f = f0 + lane;
-      const bool act = f < T;
-      const int o = owner_of(incl, f, act);
-      const int64_t before = __shfl_sync(0xffffffffu, incl - pl, o);
-      const int64_t ob = __shfl_sync(0xffffffffu, pb, o);
-      const double ov = __shfl_sync(0xffffffffu, rav, o);
-      int32_t key = -1;
-      double prod = 0.0;
-      if (act) {
-        const int64_t pp = ob + (f - before);
-        key = P.col[pp];
-        prod = __dmul_rn(ov, P.val[pp]);
-      }
-      c2 += chunk_accumulate(h2, act, key, prod, 0, lane, sp);
-    }
+    __syncwarp();
+    if (!expand(cnt)) return false;
   }
   return true;
 }
@@ -461,6 +549,8 @@ struct OutArgs {
   int64_t* soff = nullptr;
   unsigned long long* stop = nullptr;
   int64_t scap = 0;
+  bool rap_sort = false;  // k_triple: RA order by compaction + bitonic sort (CAMG_RAP_SORT=1)
+  bool h2_smem = false;   // k_triple global tables: h2 in dynamic shared memory
 };
 
 template <bool FILL>
@@ -522,6 +612,8 @@ __global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restr
                          uint32_t cap1, uint32_t cap2, char* __restrict__ gscratch, OutArgs o) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double sp_all[kWarpsPerBlock][32];
+  __shared__ int32_t bk_all[kWarpsPerBlock][64];
+  __shared__ double bv_all[kWarpsPerBlock][64];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const int64_t gw = (int64_t)blockIdx.x * kWarpsPerBlock + w;
@@ -531,12 +623,15 @@ __global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restr
   char* base = GLOBAL ? gscratch + gw * per : smem + (size_t)w * per;
   Hash h1{reinterpret_cast<int32_t*>(base + (size_t)cap1 * 8), reinterpret_cast<int16_t*>(base + (size_t)cap1 * 12),
           reinterpret_cast<double*>(base), cap1};
-  char* b2 = base + (size_t)cap1 * 14;
+  // global tables: the output table h2 (hit by every product) in shared
+  // memory when the launch provides it (dynamic shared memory > 0)
+  char* b2 = (GLOBAL && o.h2_smem) ? smem + (size_t)w * cap2 * 12 : base + (size_t)cap1 * 14;
   Hash h2{reinterpret_cast<int32_t*>(b2 + (size_t)cap2 * 8), nullptr, reinterpret_cast<double*>(b2), cap2};
   for (int64_t r = gw; r < nrows; r += nw) {
     const int64_t row = rows ? rows[r] : r;
     if (FILL && o.soff && o.soff[row] >= 0) continue;  // copied from the staging buffer
-    bool ok = row_triple(R, A, P, row, h1, h2, lane, (cap1 * 3) / 4, (cap2 * 3) / 4, sp_all[w]);
+    bool ok = row_triple(R, A, P, row, h1, h2, lane, (cap1 * 3) / 4, (cap2 * 3) / 4, sp_all[w], bk_all[w], bv_all[w],
+                         o.rap_sort);
     if (!ok) {
       if (!FILL && lane == 0) { o.overflow[row] = 1; o.cnt[row] = 0; }
       continue;
@@ -601,6 +696,8 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   DBuf<int32_t> ovf(n_rows + 1);
   CAMG_CUDA(cudaMemsetAsync(ovf.p, 0, sizeof(int32_t) * (n_rows + 1), s));
   OutArgs o{cnt.p, nullptr, nullptr, nullptr, ovf.p, tol};
+  static const bool rap_sort = getenv("CAMG_RAP_SORT") && getenv("CAMG_RAP_SORT")[0] == '1';
+  o.rap_sort = rap_sort;
   // staging buffer: the caller's output estimate, at most 40% of the free
   // memory and 16 GB; rows past it are recomputed by the fill pass
   // (CAMG_SPGEMM_STAGE=0 disables)
@@ -688,6 +785,7 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
   C->val = dalloc<double>(nnz);
   C->avg_row = n_rows ? double(nnz) / n_rows : 0.0;
   OutArgs f{nullptr, C->rowptr, C->col, C->val, nullptr, tol};
+  f.rap_sort = rap_sort;
   f.soff = o.soff;
   if (o.scol && n_rows) {
     note_launch();
@@ -792,8 +890,19 @@ Csr* galerkin(const Csr* R, const Csr* A, const Csr* P, cudaStream_t s) {
       const size_t pw = (size_t)c1 * 14 + (size_t)c2 * 12;
       int64_t warps = std::min<int64_t>(nrows, std::max<int64_t>(kWarpsPerBlock, (int64_t)((size_t(2) << 30) / pw)));
       unsigned grid = (unsigned)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
-      if (fill) k_triple<true, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
-      else k_triple<false, true><<<grid, 32 * kWarpsPerBlock, 0, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
+      // h2 in shared memory up to 48 KB per block (CAMG_RAP_H2_SMEM=0: global)
+      static const bool h2_env = !(getenv("CAMG_RAP_H2_SMEM") && getenv("CAMG_RAP_H2_SMEM")[0] == '0');
+      const size_t sm2 = (size_t)kWarpsPerBlock * c2 * 12;
+      static bool gattr = false;
+      if (!gattr) {
+        CAMG_CUDA(cudaFuncSetAttribute(k_triple<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        CAMG_CUDA(cudaFuncSetAttribute(k_triple<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+        gattr = true;
+      }
+      o.h2_smem = h2_env && sm2 <= size_t(96) * 1024;
+      const size_t dyn = o.h2_smem ? sm2 : 0;
+      if (fill) k_triple<true, true><<<grid, 32 * kWarpsPerBlock, dyn, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
+      else k_triple<false, true><<<grid, 32 * kWarpsPerBlock, dyn, s>>>(view(R), view(A), view(P), rows, nrows, c1, c2, scratch, o);
     }
     CAMG_LAUNCH_CHECK();
   };
