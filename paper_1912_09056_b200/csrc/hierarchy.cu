@@ -1977,7 +1977,13 @@ struct McIlu {
     if (fixed + 16 > cap) return;
     int nb = 0;
     size_t ring = max_stream;
-    if (fixed + max_stream > cap) {
+    // CAMG_LAM_RING=1 streams through a 2-buffer ring even when the whole
+    // stream fits (tests exercise the refill path on small systems)
+    const char* re = getenv("CAMG_LAM_RING");
+    if (re && re[0] == '1' && C2 > 2 && fixed + 2 * (size_t)max_seg <= cap) {
+      nb = 2;
+      ring = 2 * (size_t)max_seg;
+    } else if (fixed + max_stream > cap) {
       nb = (int)std::min<int64_t>((cap - fixed) / max_seg, 8);
       if (nb < 2) return;
       ring = (size_t)nb * max_seg;

@@ -221,8 +221,9 @@ def test_blocked_coarse_lu_solve_vs_oracle(cfg, scale, levels, monkeypatch):
     assert np.linalg.norm(out["1"][0] - out["0"][0]) <= 1e-12 * np.linalg.norm(out["0"][0])
 
 
+@pytest.mark.parametrize("ring", ["0", "1"])
 @pytest.mark.parametrize("cfg,scale", [("C3", 2), ("C5", 5), ("C2", 1)])
-def test_fused_lambda_side_vs_unfused(cfg, scale, monkeypatch):
+def test_fused_lambda_side_vs_unfused(cfg, scale, ring, monkeypatch):
     """The one-launch lambda side (k_lam_ilu_cl: rc, MC-ILU(0) sweep, lambda
     update, B1 correction on one cluster, factor streams by bulk copies)
     against the separate kernels: bit-identical where the unfused level runs
@@ -234,6 +235,7 @@ def test_fused_lambda_side_vs_unfused(cfg, scale, monkeypatch):
     meta = fine_level_meta(g)
     out, paths = {}, {}
     monkeypatch.setenv("CAMG_ILU_DENSE_MAX", "0")  # the cluster kernel, not the dense inverse
+    monkeypatch.setenv("CAMG_LAM_RING", ring)       # 1: factor stream through the 2-buffer ring
     for mode in ("0", "1", "2"):
         monkeypatch.setenv("CAMG_LAM_FUSED", mode)
         H = setup(op, meta, hcfg, scfg)
