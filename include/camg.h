@@ -94,6 +94,9 @@ typedef struct {
                                      update, B1 correction) in one 16-CTA cluster launch     */
 #define CAMG_PATH_DENSE_INV 10    /* small S~: the zero-start MC-ILU(0) sweep as one dense GEMV
                                      with the explicit inverse of its factors                */
+#define CAMG_PATH_LAM_ENGINE 11   /* whole lambda side of a step (rc, MC-ILU(0) forward /
+                                     backward rows, lambda update, B1 correction) in one
+                                     sync-free launch with per-row completion flags          */
 
 typedef struct {
   int64_t n_u, n_lam, nnz;     /* merged operator of the level                                   */

@@ -61,7 +61,7 @@ class LevelInfo(C.Structure):
 
 
 # CAMG_PATH_* (include/camg.h)
-PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg", "lex_trsv", "lam_fused", "dense_inv")
+PATHS = ("none", "fused", "dense_lu", "colour_csr", "colour_sell", "cta", "cluster", "inner_amg", "lex_trsv", "lam_fused", "dense_inv", "lam_engine")
 
 
 _SIGS = {

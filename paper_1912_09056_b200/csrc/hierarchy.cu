@@ -1772,6 +1772,155 @@ static void launch_lam_ilu(const LamIluArgs& a, size_t smem, cudaStream_t s) {
   else launch_lam_ilu_nt<G, 1024>(a, smem, s);
 }
 
+// ---------------------------------------------------------------------------
+// The whole lambda side of one smoother step in ONE sync-free launch
+// (k_lam_engine): every warp takes tickets in dependency order --
+//   [0, n)            forward MC-ILU(0) rows in colour order, rc computed inline:
+//                     y_i = ((A_bot [u_half; lam])_i - b_lam,i) - sum_{L(i)} l_ik y_k
+//   [n, 2n)           backward rows in reverse colour order:
+//                     z_i = (y_i - sum_{U(i)} u_ij z_j) / u_ii,  lam'_i = lam_i + cl z_i
+//   [2n, 2n + n_b1)   interface rows: u'_r = u_half,r - mult ainv_r (B1 z)_r
+// -- and reads an entry only after its producer's completion flag (acquire /
+// release, as the sync-free triangular solve): a row waits for exactly the
+// rows it reads instead of for whole colour passes, so the critical path is
+// one flag hand-off per dependency level rather than one kernel boundary per
+// colour, and the 35 launches of a step (k_lam_rhs, 2 x 16-17 colour passes,
+// k_lam_update, k_b1_correct) become one.  Tickets are handed out in order,
+// so every row a warp waits on is held by a running warp: deadlock-free for
+// any grid.  Flags hold the launch epoch + 1 (zeroed buffers are "not done");
+// the last warp to finish resets the ticket and advances the epoch, so the
+// launch replays from a CUDA graph without memset nodes.  Bounded waits set
+// the watchdog flag instead of hanging.  Same operations per row as the
+// colour-pass path up to the summation order inside a row.
+struct LamEngineArgs {
+  CsrView A;                    // merged operator (lambda rows)
+  CsrView L, U;                 // MC-ILU(0) factors, original numbering
+  const double* udiag;
+  const int32_t* nd;            // rows in colour order
+  int64_t nu, n, n_b1;
+  const double* uh;             // u_half
+  const double* xl;             // lambda (null = 0)
+  const double* bl;             // b_lam
+  double* y;                    // forward values
+  double* z;                    // backward values (dl)
+  double* xo;                   // merged output
+  double cl, mult;
+  CsrView B1;
+  const int64_t* b1_rows;
+  const double* ainv;
+  unsigned long long* ticket;   // sync block: ticket, done, epoch, flags
+  unsigned* done;
+  unsigned* epoch;
+  unsigned* fy;
+  unsigned* fz;
+  int* err;
+};
+
+__device__ __forceinline__ unsigned eng_ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double eng_ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void eng_st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// wait until flag == want (bounded)
+__device__ __forceinline__ void eng_wait(const unsigned* f, unsigned want, int* err) {
+  if (eng_ld_acquire(f) == want) return;
+  for (int it = 0; it < (1 << 22); ++it) {
+    __nanosleep(32);
+    if (eng_ld_acquire(f) == want) return;
+  }
+  atomicExch(err, 1);
+}
+
+__global__ void __launch_bounds__(256) k_lam_engine(LamEngineArgs a) {
+  CAMG_PDL_ENTRY();
+  const int lane = threadIdx.x & 31;
+  const unsigned want = *a.epoch + 1u;  // read before any warp can finish
+  const int64_t total = 2 * a.n + a.n_b1;
+  for (;;) {
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(a.ticket, 1ull);
+    tk = __shfl_sync(0xffffffffu, tk, 0);
+    if ((int64_t)tk >= total) break;
+    const int64_t t = (int64_t)tk;
+    if (t < a.n) {  // forward
+      const int64_t i = a.nd[t];
+      double r = 0.0;
+      for (int64_t p = a.A.rowptr[a.nu + i] + lane; p < a.A.rowptr[a.nu + i + 1]; p += 32) {
+        const int32_t c = a.A.col[p];
+        CAMG_DCHECK(c >= 0 && c < a.A.n_cols, "engine: A column out of range");
+        const double xv = c < a.nu ? a.uh[c] : (a.xl ? a.xl[c - a.nu] : 0.0);
+        r = fma(a.A.val[p], xv, r);
+      }
+      double acc = 0.0;
+      for (int64_t p = a.L.rowptr[i] + lane; p < a.L.rowptr[i + 1]; p += 32) {
+        const int32_t k = a.L.col[p];
+        CAMG_DCHECK(k >= 0 && k < a.n, "engine: L column out of range");
+        eng_wait(a.fy + k, want, a.err);
+        acc = fma(a.L.val[p], eng_ld_relaxed(a.y + k), acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      }
+      if (lane == 0) {
+        a.y[i] = (r - a.bl[i]) - acc;
+        eng_st_release(a.fy + i, want);
+      }
+    } else if (t < 2 * a.n) {  // backward
+      const int64_t i = a.nd[2 * a.n - 1 - t];
+      double acc = 0.0;
+      for (int64_t p = a.U.rowptr[i] + lane; p < a.U.rowptr[i + 1]; p += 32) {
+        const int32_t j = a.U.col[p];
+        CAMG_DCHECK(j >= 0 && j < a.n, "engine: U column out of range");
+        eng_wait(a.fz + j, want, a.err);
+        acc = fma(a.U.val[p], eng_ld_relaxed(a.z + j), acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        eng_wait(a.fy + i, want, a.err);
+        const double zi = (eng_ld_relaxed(a.y + i) - acc) / a.udiag[i];
+        a.z[i] = zi;
+        a.xo[a.nu + i] = (a.xl ? a.xl[i] : 0.0) + a.cl * zi;
+        eng_st_release(a.fz + i, want);
+      }
+    } else {  // interface row of B1
+      const int64_t r = a.b1_rows[t - 2 * a.n];
+      double acc = 0.0;
+      for (int64_t p = a.B1.rowptr[r] + lane; p < a.B1.rowptr[r + 1]; p += 32) {
+        const int32_t j = a.B1.col[p];
+        CAMG_DCHECK(j >= 0 && j < a.n, "engine: B1 column out of range");
+        eng_wait(a.fz + j, want, a.err);
+        acc = fma(a.B1.val[p], eng_ld_relaxed(a.z + j), acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) a.xo[r] = a.xo[r] - a.mult * (a.ainv[r] * acc);
+    }
+    __syncwarp();
+  }
+  // the last warp out resets the ticket and advances the epoch
+  if (lane == 0) {
+    __threadfence();
+    const unsigned nw = gridDim.x * (blockDim.x >> 5);
+    if (atomicAdd(a.done, 1u) == nw - 1) {
+      *a.ticket = 0ull;
+      *a.done = 0u;
+      __threadfence();
+      *a.epoch = want;
+    }
+  }
+}
+
 struct McIlu {
   int64_t n = 0;
   std::vector<int64_t> col_ptr;
@@ -1796,6 +1945,10 @@ struct McIlu {
   DBuf<int> fz_err;
   // explicit inverse of the factors (small S~): one GEMV per zero-start sweep
   DBuf<double> dense_inv;
+  // sync block of the one-launch lambda engine (k_lam_engine): ticket, done,
+  // epoch, forward / backward flags (per workspace)
+  DBuf<double> eng_sync;
+  DBuf<int> eng_err;
 
   int colors() const { return (int)col_ptr.size() - 1; }
 
@@ -1882,6 +2035,10 @@ struct McIlu {
     if (n <= 65535 && !(cl_env && cl_env[0] == '0')) setup_cluster(nd, lrp, lci, lva, urp, uci, uva);
     const char* fz_env = getenv("CAMG_LAM_FUSED");
     if (n <= kLamIluMaxRows && !(fz_env && fz_env[0] == '0')) setup_fused(nd, lrp, lci, lva, urp, uci, uva, ud);
+    eng_sync = DBuf<double>(2 + (n + 1));  // 16 B header + 2 x 4 B flags per row
+    CAMG_CUDA(cudaMemset(eng_sync.p, 0, sizeof(double) * (2 + (n + 1))));
+    eng_err = DBuf<int>(1);
+    CAMG_CUDA(cudaMemset(eng_err.p, 0, sizeof(int)));
     const char* dn_env = getenv("CAMG_ILU_DENSE_MAX");
     const int64_t dense_max = dn_env ? atoll(dn_env) : kIluDenseMax;
     if (n >= 1 && n <= dense_max) {
@@ -1893,6 +2050,43 @@ struct McIlu {
       CAMG_LAUNCH_CHECK();
       CAMG_CUDA(cudaDeviceSynchronize());
     }
+  }
+
+  // the whole lambda side of a step in one sync-free launch (k_lam_engine)
+  void run_engine(const Csr* A, int64_t nu, const double* uh, const double* xl, const double* bl, double* xo,
+                  double* dl, double cl, const Csr* B1, const int64_t* b1_rows, int64_t n_b1, const double* ainv,
+                  double mult, cudaStream_t s) {
+    LamEngineArgs a;
+    a.A = view(A);
+    a.L = view(L.get());
+    a.U = view(U.get());
+    a.udiag = udiag.p;
+    a.nd = nodes.p;
+    a.nu = nu;
+    a.n = n;
+    a.n_b1 = n_b1;
+    a.uh = uh;
+    a.xl = xl;
+    a.bl = bl;
+    a.y = y.p;
+    a.z = dl;
+    a.xo = xo;
+    a.cl = cl;
+    a.mult = mult;
+    a.B1 = view(B1);
+    a.b1_rows = b1_rows;
+    a.ainv = ainv;
+    unsigned char* sb = reinterpret_cast<unsigned char*>(eng_sync.p);
+    a.ticket = reinterpret_cast<unsigned long long*>(sb);
+    a.done = reinterpret_cast<unsigned*>(sb + 8);
+    a.epoch = reinterpret_cast<unsigned*>(sb + 12);
+    a.fy = reinterpret_cast<unsigned*>(sb + 16);
+    a.fz = a.fy + n;
+    a.err = eng_err.p;
+    const int64_t total = 2 * n + n_b1;
+    static const int64_t cap = getenv("CAMG_ENGINE_CTAS") ? atoll(getenv("CAMG_ENGINE_CTAS")) : int64_t(kNumSMs) * 8;
+    note_launch();
+    launch_k(k_lam_engine, grid_for(total * 32, 256, cap), 256, 0, s, a);
   }
 
   // one zero-start sweep through the explicit inverse fused with the lambda
@@ -2311,6 +2505,19 @@ struct Level {
   }
   // small S~: the zero-start MC-ILU(0) sweep as one GEMV with (L U)^-1
   bool lam_dense() const { return mcilu_once() && cilu.dense_inv.p != nullptr && !ovl(); }
+  // the one-launch sync-free lambda engine (CAMG_LAM_ENGINE: 0 off -- the
+  // default: measured slower, C5 19.0 -> 21.8 ms, C3 1.51 -> 2.41 ms, the
+  // flag hand-offs per dependency level cost more than the PDL-chained
+  // colour passes --, 1 on the levels that would run colour passes, 2
+  // everywhere)
+  bool lam_engine() const {
+    if (!mcilu_once() || !cilu.eng_sync.p) return false;
+    const char* e = getenv("CAMG_LAM_ENGINE");
+    const int m = e ? atoi(e) : 0;
+    if (m == 0) return false;
+    if (m == 2) return true;
+    return !lam_dense() && !lam_fused();
+  }
   // the one-cluster ILU(0) sweep
   bool lam_fused() const {
     if (!mcilu_once() || !cilu.fused) return false;
@@ -2434,7 +2641,10 @@ struct Level {
     // lambda side: rc = B2 u_half - Cz lam - b_lam = -(b_lam + Cz lam - B2 u_half)
     const double cl = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 : alpha;
     const double mult = (kind == CAMG_BRAESS_SARAZIN) ? 1.0 / alpha : alpha;
-    if (lam_dense() || lam_fused()) {
+    if (lam_engine()) {
+      cilu.run_engine(A, nu, uh, xl, b + nu, xo, w_dl.p, cl, B1, b1_rows.p, kind != CAMG_UZAWA ? n_b1_rows : 0,
+                      ainv.p, mult, ls);
+    } else if (lam_dense() || lam_fused()) {
       // rc (wide kernel), then the ILU(0) sweep + lambda update (one GEMV
       // with the explicit inverse, or one cluster), then the interface-row
       // B1 correction (wide kernel)
@@ -2833,7 +3043,7 @@ struct Hierarchy {
       Level* L = levels[l];
       for (DBuf<double>* b : {&vb[l], &vx0[l], &vx1[l], &vr[l], &L->w_du, &L->w_du2, &L->w_ru, &L->w_rc, &L->w_dl,
                               &L->w_dl2, &L->w_rl, &L->w_tmp, &L->w_cd[0], &L->w_cd[1], &L->gs.g, &L->cgs.g,
-                              &L->cilu.y, &L->cilu.z})
+                              &L->cilu.y, &L->cilu.z, &L->cilu.eng_sync})
         v.push_back(b);
       if (L->inner) scalar_work_slots(L->inner, v);
       L->pps.work_slots(v);
@@ -3548,7 +3758,8 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
     else if (c.corr_kind == CAMG_PT_MCGS) { o.corr_path = mc_path(L->cgs); o.corr_colors = L->cgs.colors(); }
     else if (c.corr_kind == CAMG_PT_SGS || c.corr_kind == CAMG_PT_ILU0) o.corr_path = CAMG_PATH_LEX_TRSV;
     else if (c.corr_kind == CAMG_PT_MCILU0) {
-      o.corr_path = L->lam_dense() ? CAMG_PATH_DENSE_INV
+      o.corr_path = L->lam_engine() ? CAMG_PATH_LAM_ENGINE
+                    : L->lam_dense() ? CAMG_PATH_DENSE_INV
                     : L->lam_fused() ? CAMG_PATH_LAM_FUSED
                     : (L->cilu.cl && c.corr_sweeps == 1) ? CAMG_PATH_CLUSTER : CAMG_PATH_COLOUR_CSR;
       o.corr_colors = L->cilu.colors();
@@ -3559,10 +3770,11 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
       o.pred_path = mc_path(L->gs);
       o.pred_colors = L->gs.colors();
     } else o.pred_path = CAMG_PATH_FUSED;
-    if (L->cilu.fz_err.p) {
+    for (const DBuf<int>* e : {&L->cilu.fz_err, &L->cilu.eng_err}) {
+      if (!e->p) continue;
       int h = 0;
-      CAMG_CUDA(cudaMemcpy(&h, L->cilu.fz_err.p, sizeof(int), cudaMemcpyDeviceToHost));
-      o.watchdog = h;
+      CAMG_CUDA(cudaMemcpy(&h, e->p, sizeof(int), cudaMemcpyDeviceToHost));
+      o.watchdog |= h;
     }
     if (L->P) {
       o.transfer_block_rows = L->P->sell ? L->P->sell->br : 0;

@@ -280,3 +280,33 @@ def test_dense_inverse_ilu_vs_sweeps(cfg, scale, monkeypatch):
     ref = O.setup(oop, ometa, ohc, obc).apply(rhs)
     assert np.linalg.norm(out["2048"] - ref) <= 1e-10 * np.linalg.norm(ref)
     assert np.linalg.norm(out["2048"] - out["0"]) <= 1e-12 * np.linalg.norm(out["0"])
+
+
+@pytest.mark.parametrize("cfg,scale", [("C3", 2), ("C5", 5), ("C2", 1), ("C3", 1)])
+def test_lambda_engine_vs_colour_passes(cfg, scale, monkeypatch):
+    """The one-launch sync-free lambda engine (k_lam_engine: tickets in
+    dependency order, per-row completion flags, rc / lambda update / B1
+    correction fused) forced on every level, against the colour-pass path
+    (1e-12) and the oracle (V-cycle 1e-10); repeated applies replay the
+    graph bit-identically (epoch flags), no watchdog fired."""
+    hcfg, scfg, _ = bench.solver_for(cfg)
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g, device_K=True)
+    meta = fine_level_meta(g)
+    monkeypatch.setenv("CAMG_ILU_DENSE_MAX", "0")
+    monkeypatch.setenv("CAMG_LAM_FUSED", "0")
+    out, paths = {}, {}
+    for mode in ("0", "2"):
+        monkeypatch.setenv("CAMG_LAM_ENGINE", mode)
+        H = setup(op, meta, hcfg, scfg)
+        out[mode] = [H.apply(g.rhs) for _ in range(3)]
+        paths[mode] = [H.level_info(l)["corr_path"] for l in range(H.num_levels - 1)]
+        assert not any(H.level_info(l)["watchdog"] for l in range(H.num_levels)), mode
+    assert all(p == "lam_engine" for p in paths["2"]) and "lam_engine" not in paths["0"]
+    oop, ometa, rhs = O.system_from_generated(g)
+    ohc, obc = oracle_cfgs(hcfg, scfg)
+    ref = O.setup(oop, ometa, ohc, obc).apply(rhs)
+    for mode in ("0", "2"):
+        np.testing.assert_array_equal(out[mode][0], out[mode][2])
+        assert np.linalg.norm(out[mode][0] - ref) <= 1e-10 * np.linalg.norm(ref), mode
+    assert np.linalg.norm(out["2"][0] - out["0"][0]) <= 1e-12 * np.linalg.norm(out["0"][0])
