@@ -892,10 +892,14 @@ __global__ void __launch_bounds__(128) k_ilu_inverse(int n, const int32_t* __res
   }
 }
 
-// dl = X rc and the lambda update xo_l = xl + cl dl in one GEMV (warp per row)
+// dl = X rc and the lambda update xo_l = xl + cl dl in one GEMV (warp per
+// row); with M2 (n_b1 rows: mult diag(ainv) B1 X on the interface rows) the
+// B1 correction xo_u[r_k] -= (M2 rc)_k runs in the same launch
 __global__ void __launch_bounds__(256) k_dense_gemv_lam(int n, const double* __restrict__ M,
                                                         const double* __restrict__ v, const double* __restrict__ xl,
-                                                        double cl, double* __restrict__ dl, double* __restrict__ xo_l) {
+                                                        double cl, double* __restrict__ dl, double* __restrict__ xo_l,
+                                                        const double* __restrict__ M2, const int64_t* __restrict__ b1_rows,
+                                                        int n_b1, double* __restrict__ xo_u) {
   CAMG_PDL_ENTRY();
   CAMG_DCHECK(n >= 0 && n <= 4096, "dense gemv size beyond its shared-memory staging");
   extern __shared__ double vs[];
@@ -903,8 +907,8 @@ __global__ void __launch_bounds__(256) k_dense_gemv_lam(int n, const double* __r
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-    const double* row = M + (size_t)r * n;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n + n_b1; r += nw) {
+    const double* row = r < n ? M + (size_t)r * n : M2 + (size_t)(r - n) * n;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     int c = lane;
     for (; c + 96 < n; c += 128) {
@@ -918,9 +922,27 @@ __global__ void __launch_bounds__(256) k_dense_gemv_lam(int n, const double* __r
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) {
-      dl[r] = acc;
-      xo_l[r] = (xl ? xl[r] : 0.0) + cl * acc;
+      if (r < n) {
+        dl[r] = acc;
+        xo_l[r] = (xl ? xl[r] : 0.0) + cl * acc;
+      } else {
+        const int64_t u = b1_rows[r - n];
+        xo_u[u] = xo_u[u] - acc;
+      }
     }
+  }
+}
+
+// M2[k][j] = mult ainv[r_k] sum_i B1[r_k, i] X[i][j] (r_k = b1_rows[k])
+__global__ void k_b1_dense(int n, int64_t n_b1, const int64_t* __restrict__ b1_rows, CsrView B1,
+                           const double* __restrict__ ainv, double mult, const double* __restrict__ X,
+                           double* __restrict__ M2) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_b1 * n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / n, j = e % n;
+    const int64_t r = b1_rows[k];
+    double acc = 0.0;
+    for (int64_t p = B1.rowptr[r]; p < B1.rowptr[r + 1]; ++p) acc = fma(B1.val[p], X[(size_t)B1.col[p] * n + j], acc);
+    M2[e] = mult * (ainv[r] * acc);
   }
 }
 
@@ -2091,7 +2113,9 @@ struct McIlu {
 
   // one zero-start sweep through the explicit inverse fused with the lambda
   // update: dl = (L U)^-1 rc, xo_l = xl + cl dl
-  void run_dense(const double* rc, const double* xl, double* xo_l, double* dl, double cl, cudaStream_t s) {
+  void run_dense(const double* rc, const double* xl, double* xo_l, double* dl, double cl, cudaStream_t s,
+                 const double* M2 = nullptr, const int64_t* b1_rows = nullptr, int64_t n_b1 = 0,
+                 double* xo_u = nullptr) {
     static bool attr = false;
     if (!attr) {
       CAMG_CUDA(cudaFuncSetAttribute(k_dense_gemv_lam, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2099,8 +2123,9 @@ struct McIlu {
       attr = true;
     }
     note_launch();
-    launch_k(k_dense_gemv_lam, grid_for(n * 32, 256, int64_t(kNumSMs) * 4), 256, sizeof(double) * n, s, (int)n,
-             (const double*)dense_inv.p, rc, xl, cl, dl, xo_l);
+    launch_k(k_dense_gemv_lam, grid_for((n + (M2 ? n_b1 : 0)) * 32, 256, int64_t(kNumSMs) * 4), 256,
+             sizeof(double) * n, s, (int)n, (const double*)dense_inv.p, rc, xl, cl, dl, xo_l, M2, b1_rows,
+             (int)(M2 ? n_b1 : 0), xo_u);
   }
 
   // per-CTA factor streams of k_lam_ilu_cl (see there)
@@ -2408,6 +2433,9 @@ struct Level {
   DBuf<double> k_lu;
   DBuf<int32_t> k_piv;
   bool exact = false;
+  // dense path: mult diag(ainv) B1 (L U)^-1 on the interface rows (n_b1 x nl),
+  // so the B1 correction is part of the corrector GEMV
+  DBuf<double> dense_b1;
   // transfer (merged block-diagonal)
   Csr* P = nullptr;
   Csr* R = nullptr;
@@ -2649,9 +2677,11 @@ struct Level {
       // with the explicit inverse, or one cluster), then the interface-row
       // B1 correction (wide kernel)
       dispatch_g<LaunchLamRhs>(A->avg_row, A, nu, nl, uh, xl, b + nu, w_rc.p, ls);
-      if (lam_dense()) cilu.run_dense(w_rc.p, xl, xo + nu, w_dl.p, cl, ls);
+      const bool b1_fused = lam_dense() && kind != CAMG_UZAWA && n_b1_rows && dense_b1.p;
+      if (lam_dense())
+        cilu.run_dense(w_rc.p, xl, xo + nu, w_dl.p, cl, ls, b1_fused ? dense_b1.p : nullptr, b1_rows.p, n_b1_rows, xo);
       else cilu.run_fused(w_rc.p, xl, xo + nu, w_dl.p, cl, ls);
-      if (kind != CAMG_UZAWA && n_b1_rows) {
+      if (kind != CAMG_UZAWA && n_b1_rows && !b1_fused) {
         note_launch();
         launch_k(k_b1_correct, grid_for(n_b1_rows * 8, 256), 256, 0, ls, view(B1), b1_rows.p, n_b1_rows, ainv.p,
                  (const double*)w_dl.p, mult, xo);
@@ -2947,6 +2977,16 @@ Level* level_create(const Csr* K, const Csr* B1, const Csr* B2, const Csr* Cz, c
     L->b1_rows = std::move(out);
   }
   if (!L->exact) setup_overlap(L.get());
+  const char* db_env = getenv("CAMG_DENSE_B1");
+  if (L->cilu.dense_inv.p && cfg.kind != CAMG_UZAWA && L->n_b1_rows && !L->exact && !(db_env && db_env[0] == '0') &&
+      L->n_b1_rows * nl <= (int64_t(1) << 25)) {
+    const double mult = (cfg.kind == CAMG_BRAESS_SARAZIN) ? 1.0 / cfg.alpha : cfg.alpha;
+    L->dense_b1 = DBuf<double>((size_t)L->n_b1_rows * nl + 1);
+    note_launch();
+    k_b1_dense<<<grid_for(L->n_b1_rows * nl, 256), 256>>>((int)nl, L->n_b1_rows, L->b1_rows.p, view(L->B1),
+                                                          L->ainv.p, mult, L->cilu.dense_inv.p, L->dense_b1.p);
+    CAMG_LAUNCH_CHECK();
+  }
   L->alloc_work();
   CAMG_CUDA(cudaDeviceSynchronize());
   return L.release();
