@@ -227,6 +227,15 @@ int camg_stencil_block_counts(int dim, const int64_t* grid, int clamp_lo, int cl
 int camg_qr_batch(const char* lapack_path, int64_t G, int M, int k, const double* vecs, int64_t n_dofs,
                   const int64_t* dofs, double* q_out, double* r_out, int64_t* piv_out, int nthreads,
                   int64_t* info_out);
+/* The whole tentative prolongator natively (transfer.py:86-145): DOFs of
+ * each aggregate (node_to_agg[dof_node[i]]) in ascending order, one LAPACK
+ * pivoted QR per aggregate (as camg_qr_batch, bit-identical to the
+ * reference), rank |r_ii| > rank_tol |r_00|, coarse null space R P^T rows
+ * (coarse_ns: room for na*k rows of k), the CSR of P on the device.
+ * rank_out: kept columns per aggregate; errors name the aggregate.       */
+int camg_tentative(const char* lapack_path, int64_t n_dofs, int k, const double* vecs, const int64_t* dof_node,
+                   const int64_t* node_to_agg, int64_t num_nodes, int64_t na, double rank_tol, int nthreads,
+                   camg_csr** P_out, int64_t* rank_out, double* coarse_ns, int64_t* ncoarse);
 /* Allocates an empty n_rows x n_cols matrix with nnz slots (filled by
  * camg_assemble_stencil). */
 int camg_csr_alloc(int64_t n_rows, int64_t n_cols, int64_t nnz, camg_csr** out);

@@ -144,6 +144,8 @@ _SIGS = {
     "camg_hierarchy_kernels_per_cycle": (C.c_int, [vp, P64]),
     "camg_level_get_info": (C.c_int, [vp, C.POINTER(LevelInfo)]),
     "camg_qr_batch": (C.c_int, [C.c_char_p, i64, C.c_int, C.c_int, vp, i64, vp, vp, vp, vp, C.c_int, P64]),
+    "camg_tentative": (C.c_int, [C.c_char_p, i64, C.c_int, vp, vp, vp, i64, i64, f64, C.c_int, C.POINTER(vp), vp, vp,
+                                 P64]),
     "camg_dot": (C.c_int, [i64, vp, vp, C.POINTER(f64), vp]),
     "camg_axpy": (C.c_int, [i64, f64, vp, vp, vp]),
 }

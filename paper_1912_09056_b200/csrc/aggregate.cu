@@ -398,12 +398,11 @@ __global__ void k_ptent(PtGroup gp, const int64_t* __restrict__ dofs, const doub
   }
 }
 
-}  // namespace camg
-
-extern "C" int camg_tentative_csr(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta,
-                                  const int64_t* dofs, int64_t ndofs_total, const double* Q, int64_t nq,
-                                  const int64_t* rank, const int64_t* col0, int64_t naggs, camg_csr** out) {
-  return guarded([&] {
+// device CSR of P_tent from the per-group QR factors (see camg_tentative_csr)
+Csr* tentative_assemble(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta, const int64_t* dofs,
+                        int64_t ndofs_total, const double* Q, int64_t nq, const int64_t* rank, const int64_t* col0,
+                        int64_t naggs) {
+  {
     cudaStream_t s = 0;
     CAMG_CHECK(ndofs_total == n_dofs, CAMG_ERR_DIMENSION, "every DOF must belong to one aggregate");
     DBuf<int64_t> d_dofs(ndofs_total + 1), d_rank(naggs + 1), d_col0(naggs + 1);
@@ -440,6 +439,17 @@ extern "C" int camg_tentative_csr(int64_t n_dofs, int64_t ncoarse, int64_t ngrou
     }
     CAMG_LAUNCH_CHECK();
     CAMG_CUDA(cudaStreamSynchronize(s));
-    *out = new camg_csr{P};
+    return P;
+  }
+}
+
+}  // namespace camg
+
+extern "C" int camg_tentative_csr(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta,
+                                  const int64_t* dofs, int64_t ndofs_total, const double* Q, int64_t nq,
+                                  const int64_t* rank, const int64_t* col0, int64_t naggs, camg_csr** out) {
+  return guarded([&] {
+    *out = new camg_csr{tentative_assemble(n_dofs, ncoarse, ngroups, meta, dofs, ndofs_total, Q, nq, rank, col0,
+                                           naggs)};
   });
 }

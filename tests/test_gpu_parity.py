@@ -463,10 +463,13 @@ def test_mcgs_corrector_vs_oracle_emulation(cfg, scale, levels):
     assert abs(rep.iterations - orep.iterations) <= 1, (rep.iterations, orep.iterations)
 
 
+@pytest.mark.parametrize("py", ["0", "1"])
 @pytest.mark.parametrize("cfg,scale", [("C5", 4), ("C2", 2), ("C3", 8)])
-def test_tentative_prolongator_bit_identical(cfg, scale):
-    """Batched host LAPACK + device CSR assembly == the reference's
-    per-aggregate pivoted QR (oracle), bit for bit, for u and lambda."""
+def test_tentative_prolongator_bit_identical(cfg, scale, py, monkeypatch):
+    """Host LAPACK + device CSR assembly == the reference's per-aggregate
+    pivoted QR (oracle), bit for bit, for u and lambda: the native
+    camg_tentative (py=0, the default) and the numpy-grouped path (py=1)."""
+    monkeypatch.setenv("CAMG_TENTATIVE_PY", py)
     from paper_1912_09056_b200.aggregation import NodeGraph, aggregate_greedy, aggregate_lagrange
     from paper_1912_09056_b200.transfer import NullSpace, tentative_prolongator
     from paper_1912_09056_b200.aggregation import filtered_node_graph
