@@ -28,7 +28,10 @@ namespace camg {
 namespace {
 
 constexpr int32_t kEmpty = -1;
-constexpr int kWarpsPerBlock = 2;  // smem hash per warp: 2-warp blocks pack 3+ blocks per SM
+constexpr int kWarpsPerBlock = 2;
+#ifndef CAMG_TRIPLE_MINB
+#define CAMG_TRIPLE_MINB 12  // resident 64-thread CTAs per SM the Galerkin kernel is compiled for
+#endif  // smem hash per warp: 2-warp blocks pack 3+ blocks per SM
 
 __device__ __forceinline__ uint32_t hslot(int32_t k, uint32_t mask) {
   return ((uint32_t)k * 2654435761u) & mask;
@@ -608,7 +611,8 @@ __global__ void k_product(CsrView A, CsrView B, bool reverse_a, const double* __
 }
 
 template <bool FILL, bool GLOBAL>
-__global__ void k_triple(CsrView R, CsrView A, CsrView P, const int64_t* __restrict__ rows, int64_t nrows,
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, CAMG_TRIPLE_MINB) k_triple(CsrView R, CsrView A, CsrView P,
+                                                                           const int64_t* __restrict__ rows, int64_t nrows,
                          uint32_t cap1, uint32_t cap2, char* __restrict__ gscratch, OutArgs o) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double sp_all[kWarpsPerBlock][32];
@@ -756,6 +760,9 @@ Csr* two_pass(int64_t n_rows, int64_t n_cols, Launch launch, uint32_t c1_0, uint
     CAMG_CUDA(cudaStreamSynchronize(s));
     CAMG_LAUNCH_CHECK();
     std::vector<int64_t> still = overflow_rows(ovf.p, n_rows);
+    if (getenv("CAMG_DEBUG"))
+      fprintf(stderr, "[camg] spgemm global pass caps %u/%u: rows %zu, overflow %zu\n", c1, c2, big.size(),
+              still.size());
     std::vector<int64_t> done;
     size_t k = 0;
     for (int64_t r : big) {
