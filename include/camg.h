@@ -112,6 +112,10 @@ typedef struct {
   int restrict_block_rows;     /* R = P^T has one: its block rows (0 = CSR)                     */
   int watchdog;                /* 1: a bounded device wait of this level expired (a bug; results
                                   invalid) -- reading it synchronises the device               */
+  int sell_shared_values;      /* 1: bit-identical slots of the masked mirror share one stored copy
+                                  (CAMG_SELL_DEDUP=0 disables)                                  */
+  int64_t sell_value_groups;   /* 32-value groups the mirror stores ...                          */
+  int64_t sell_value_groups_full; /* ... and before sharing                                      */
 } camg_level_info;
 
 /* ---- library ------------------------------------------------------------ */
@@ -137,6 +141,9 @@ int camg_csr_to_host(const camg_csr* A, int64_t* rowptr, int64_t* col, double* v
 int camg_csr_attach_blocks(camg_csr* A, int bs, int64_t nrows);
 /* same with br x bc blocks over the first ncols_blocked columns */
 int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked);
+/* 32-value groups the block mirror stores (kept) and would store without sharing
+ * bit-identical slots (full); kept < full: shared value groups are in use (sell.cu) */
+int camg_csr_value_groups(const camg_csr* A, int64_t* kept, int64_t* full);
 /* compulsory bytes of one SpMV pass in the matrix's current format */
 int camg_csr_stream_bytes(const camg_csr* A, double* bytes);
 /* merged saddle operator [[K, B1], [B2, -Cz]] (saddle.py:58-67) */

@@ -51,6 +51,7 @@ class LevelInfo(C.Structure):
         ("overlap", C.c_int), ("overlap_indep_slices", i64), ("overlap_dep_slices", i64),
         ("pred_path", C.c_int), ("pred_colors", C.c_int), ("corr_path", C.c_int), ("corr_colors", C.c_int),
         ("transfer_block_rows", C.c_int), ("restrict_block_rows", C.c_int), ("watchdog", C.c_int),
+        ("sell_shared_values", C.c_int), ("sell_value_groups", i64), ("sell_value_groups_full", i64),
     ]
 
     def as_dict(self):
@@ -104,6 +105,7 @@ _SIGS = {
     "camg_csr_attach_blocks": (C.c_int, [vp, C.c_int, i64]),
     "camg_csr_attach_rect_blocks": (C.c_int, [vp, C.c_int, C.c_int, i64, i64]),
     "camg_csr_stream_bytes": (C.c_int, [vp, C.POINTER(f64)]),
+    "camg_csr_value_groups": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)]),
     "camg_level_block_transfer": (C.c_int, [vp, C.c_int, C.c_int, i64]),
     "camg_level_fine_pass": (C.c_int, [vp, C.c_int, vp, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "camg_level_schur": (C.c_int, [vp, C.POINTER(vp)]),

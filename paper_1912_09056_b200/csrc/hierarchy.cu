@@ -3785,6 +3785,9 @@ int camg_level_get_info(const camg_level* Lh, camg_level_info* info) {
       o.sell_masked = S->masked ? 1 : 0;
       o.sell_lanes = sell_lanes(S);
       o.sell_slices = S->nslices;
+      o.sell_shared_values = S->dedup ? 1 : 0;
+      o.sell_value_groups = S->ngroups;
+      o.sell_value_groups_full = S->dedup ? S->ngroups_full : S->ngroups;
     }
     o.overlap = L->overlap ? 1 : 0;
     o.overlap_indep_slices = L->n_indep;

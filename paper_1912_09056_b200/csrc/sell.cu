@@ -21,6 +21,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "sell.cuh"
@@ -46,6 +48,10 @@
 #ifndef CAMG_BIG_MINB
 #define CAMG_BIG_MINB 4
 #endif
+// shared-value-group passes are bound by L1 / issue, not by loads in flight
+#ifndef CAMG_DEDUP_MINB
+#define CAMG_DEDUP_MINB 4
+#endif
 
 namespace camg {
 
@@ -60,6 +66,7 @@ Sell::~Sell() {
   dfree(voff);
   dfree(desc);
   dfree(zero);
+  dfree(vo);
   dfree(perm);
   dfree(dblk);
 }
@@ -215,22 +222,198 @@ __global__ void k_sell_row_bytes(const int64_t* __restrict__ slice_ptr, const ui
                                  const unsigned long long* __restrict__ mask,
                                  const unsigned long long* __restrict__ desc, int64_t nbr,
                                  unsigned long long* __restrict__ acc) {
-  unsigned long long b = 0, u = 0;
+  unsigned long long b = 0, u = 0, cb = 0;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t base = slice_ptr[p >> 5];
     const int n = len[p];
-    for (int k = 0; k < n; ++k)
-      b += 8ull * __popcll(mask[base + k]) + ((desc && ((desc[base + k] >> 36) & 0xFFFFFFull)) ? 0ull : 4ull);
+    for (int k = 0; k < n; ++k) {
+      const unsigned long long c = (desc && ((desc[base + k] >> 36) & 0xFFFFFFull)) ? 0ull : 4ull;
+      b += 8ull * __popcll(mask[base + k]) + c;
+      cb += c;
+    }
     u += n;
   }
   for (int o = 16; o > 0; o >>= 1) {
     b += __shfl_xor_sync(0xffffffffu, b, o);
     u += __shfl_xor_sync(0xffffffffu, u, o);
+    cb += __shfl_xor_sync(0xffffffffu, cb, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(acc, b);
     atomicAdd(acc + 1, u);
+    atomicAdd(acc + 2, cb);
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Shared value groups of a masked mirror.  Two slots with the same mask and
+// bit-identical stored values (every lane, every position) need one copy:
+// on a structured mesh the interior stencil repeats from slice to slice, so
+// the value stream of the mirror collapses to a small dictionary that lives
+// in L1/L2, and a pass streams only descriptors, columns and the vectors.
+// The result of every product is unchanged (same values, same order).
+// Slots are grouped by a 64-bit hash of their content, sorted (stable radix
+// sort), and every slot is compared bit for bit with the first slot of its
+// hash run before it shares that slot's copy (a hash collision keeps its own).
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void k_slot_hash(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
+                            const double* __restrict__ bval, int64_t slots, unsigned long long* __restrict__ key,
+                            uint32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < slots; s += nwarps) {
+    const unsigned long long m = mask[s];
+    const int ng = __popcll(m);
+    const double* v = bval + voff[s] * 32 + lane;
+    unsigned long long h = 0;
+    for (int g = 0; g < ng; ++g)
+      h += mix64((unsigned long long)__double_as_longlong(v[g * 32]) ^ mix64((unsigned long long)(g * 32 + lane + 1)));
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0) {
+      key[s] = mix64(h ^ mix64(m));
+      idx[s] = (uint32_t)s;
+    }
+  }
+}
+
+__global__ void k_run_heads(const unsigned long long* __restrict__ key, int64_t n, int64_t* __restrict__ head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || key[i] != key[i - 1]) ? i : 0;
+}
+
+// rep[s] = the slot whose copy s shares (itself: s keeps its own values)
+__global__ void k_slot_verify(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
+                              const double* __restrict__ bval, const uint32_t* __restrict__ sidx,
+                              const int64_t* __restrict__ head, int64_t slots, uint32_t* __restrict__ rep) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < slots; i += nwarps) {
+    const uint32_t s = sidx[i], r = sidx[head[i]];
+    bool eq = true;
+    if (s != r) {
+      const unsigned long long m = mask[s];
+      eq = m == mask[r];
+      if (eq) {
+        const int ng = __popcll(m);
+        const double* a = bval + voff[s] * 32 + lane;
+        const double* b = bval + voff[r] * 32 + lane;
+        for (int g = 0; g < ng; ++g) eq &= __double_as_longlong(a[g * 32]) == __double_as_longlong(b[g * 32]);
+      }
+      eq = __all_sync(0xffffffffu, eq);
+    }
+    if (lane == 0) rep[s] = eq ? r : s;
+  }
+}
+
+__global__ void k_slot_own_groups(const unsigned long long* __restrict__ mask, const uint32_t* __restrict__ rep,
+                                  int64_t slots, int64_t* __restrict__ cnt) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x)
+    cnt[s] = rep[s] == (uint32_t)s ? __popcll(mask[s]) : 0;
+}
+
+// copy the kept slots' groups to the compact array; uni[s] = every group of s is lane-uniform
+__global__ void k_slot_compact(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
+                               const double* __restrict__ bval, const uint32_t* __restrict__ rep,
+                               const int64_t* __restrict__ noff, int64_t slots, double* __restrict__ nval,
+                               uint8_t* __restrict__ uni) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s = warp; s < slots; s += nwarps) {
+    if (rep[s] != (uint32_t)s) continue;
+    const int ng = __popcll(mask[s]);
+    const double* a = bval + voff[s] * 32 + lane;
+    double* o = nval + noff[s] * 32 + lane;
+    bool u = true;
+    for (int g = 0; g < ng; ++g) {
+      const double x = a[g * 32];
+      o[g * 32] = x;
+      const long long b = __double_as_longlong(x);
+      u &= b == __shfl_sync(0xffffffffu, b, 0);
+    }
+    u = __all_sync(0xffffffffu, u);
+    if (lane == 0) uni[s] = u ? 1 : 0;
+  }
+}
+
+__global__ void k_slot_share(const uint32_t* __restrict__ rep, const int64_t* __restrict__ noff,
+                             const uint8_t* __restrict__ uni, int64_t slots, uint32_t* __restrict__ vo,
+                             unsigned long long* __restrict__ desc) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = rep[s];
+    vo[s] = (uint32_t)noff[r];
+    desc[s] = (desc[s] & ~(0xFull << 60)) | ((unsigned long long)uni[r] << 60);
+  }
+}
+
+// Replace S's value array by the shared one when that at least halves it;
+// returns the value groups kept (S->ngroups) -- S->dedup says whether it applied.
+static void share_value_groups(Sell* S, cudaStream_t s) {
+  const int64_t slots = S->slots;
+  S->ngroups_full = S->ngroups;
+  if (slots < 2 || slots >= (int64_t)1 << 32) return;
+  DBuf<unsigned long long> key(slots), key2(slots);
+  DBuf<uint32_t> idx(slots), sidx(slots), rep(slots);
+  note_launch();
+  k_slot_hash<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, slots, key.p, idx.p);
+  size_t tmp = 0;
+  CAMG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, key2.p, idx.p, sidx.p, slots, 0, 64, s));
+  {
+    DBuf<char> t(tmp);
+    note_launch();
+    CAMG_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, key.p, key2.p, idx.p, sidx.p, slots, 0, 64, s));
+    CAMG_CUDA(cudaStreamSynchronize(s));
+  }
+  DBuf<int64_t> head(slots);
+  note_launch();
+  k_run_heads<<<grid_for(slots, 256), 256, 0, s>>>(key2.p, slots, head.p);
+  tmp = 0;
+  CAMG_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tmp, head.p, head.p, cub::Max(), slots, s));
+  {
+    DBuf<char> t(tmp);
+    note_launch();
+    CAMG_CUDA(cub::DeviceScan::InclusiveScan(t.p, tmp, head.p, head.p, cub::Max(), slots, s));
+    CAMG_CUDA(cudaStreamSynchronize(s));
+  }
+  note_launch();
+  k_slot_verify<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, sidx.p, head.p, slots, rep.p);
+  DBuf<int64_t> cnt(slots + 1), noff(slots + 1);
+  note_launch();
+  k_slot_own_groups<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, rep.p, slots, cnt.p);
+  exclusive_scan_i64(cnt.p, noff.p, slots, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  const int64_t kept = read_i64(noff.p + slots);
+  if (kept * 2 > S->ngroups || kept >= (int64_t)1 << 32) return;  // little to share: keep the streaming layout
+  DBuf<double> nval((size_t)std::max<int64_t>(kept, 1) * 32);
+  DBuf<uint8_t> uni(slots);
+  CAMG_CUDA(cudaMemsetAsync(uni.p, 0, slots, s));
+  note_launch();
+  k_slot_compact<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, rep.p, noff.p, slots, nval.p,
+                                                           uni.p);
+  S->vo = dalloc<uint32_t>(slots + 1);
+  note_launch();
+  k_slot_share<<<grid_for(slots, 256), 256, 0, s>>>(rep.p, noff.p, uni.p, slots, S->vo, S->desc);
+  CAMG_LAUNCH_CHECK();
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  dfree(S->bval);
+  S->bval = nval.release();
+  S->ngroups = kept;
+  S->dedup = true;
+}
+
+static bool dedup_enabled() {
+  const char* e = getenv("CAMG_SELL_DEDUP");
+  return !(e && e[0] == '0');
 }
 
 template <int BR, int BC>
@@ -309,22 +492,27 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
     k_slot_linear<<<grid_for(nslices * 32, 256), 256, 0, s>>>(S->slice_ptr, S->len, S->bcol, nbr, nslices, S->desc);
     CAMG_LAUNCH_CHECK();
   }
+  if (masked && dedup_enabled()) share_value_groups(S.get(), s);
   // compulsory bytes of one pass: for every row, its blocks' stored values and
   // column (the padding of shorter rows is skipped; linear slots load no
   // column), summed on the device
-  DBuf<unsigned long long> acc(2);
-  CAMG_CUDA(cudaMemsetAsync(acc.p, 0, 2 * sizeof(unsigned long long), s));
+  DBuf<unsigned long long> acc(3);
+  CAMG_CUDA(cudaMemsetAsync(acc.p, 0, 3 * sizeof(unsigned long long), s));
   note_launch();
   k_sell_row_bytes<<<grid_for(nbr, 256), 256, 0, s>>>(S->slice_ptr, S->len, S->mask, masked ? S->desc : nullptr, nbr,
                                                       acc.p);
   CAMG_LAUNCH_CHECK();
-  unsigned long long h_acc[2] = {0, 0};
+  unsigned long long h_acc[3] = {0, 0, 0};
   CAMG_CUDA(cudaMemcpyAsync(h_acc, acc.p, sizeof(h_acc), cudaMemcpyDeviceToHost, s));
   CAMG_CUDA(cudaStreamSynchronize(s));
   const double bytes = (double)h_acc[0];
   const int64_t used = (int64_t)h_acc[1];
   S->used_blocks = used;
   S->pass_bytes = bytes + (double)nbr + 16.0 * (double)(nslices + 1) + 16.0 * (double)slots / 32.0;
+  // shared value groups: the rows' column bytes, every kept group once, a descriptor and a group offset per slot
+  if (S->dedup)
+    S->pass_bytes = (double)h_acc[2] + 256.0 * (double)S->ngroups + (double)nbr + 16.0 * (double)(nslices + 1) +
+                    12.0 * (double)slots;
   return S.release();
 }
 
@@ -393,8 +581,8 @@ __device__ __forceinline__ void sell_epilogue(const SellEpi& e, int64_t p, const
   }
 }
 
-template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED>
-__global__ void __launch_bounds__(kSellThreads, (MASKED ? CAMG_MASKED_MINB : (BR * BC >= 18 ? CAMG_BIG_MINB : 6)) * 256 / kSellThreads) k_sell_row(SellView S, const double* __restrict__ xu,
+template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED, bool DEDUP = false>
+__global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MINB : CAMG_MASKED_MINB) : (BR * BC >= 18 ? CAMG_BIG_MINB : 6)) * 256 / kSellThreads) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
                                                   SellEpi e) {
   CAMG_PDL_ENTRY();
@@ -441,10 +629,27 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? CAMG_MASKED_MINB : (BR
         const uint64_t m0 = lane < width ? __ldg(S.desc + base + lane) : 0ull;
         const uint64_t m1 = lane + 32 < width ? __ldg(S.desc + base + 32 + lane) : 0ull;
         // the slice's values start at group voff[base]; slots follow in order
-        const double* v = S.bval + __ldg(S.voff + base) * 32 + lane;
+        // (shared value groups: every slot names the first group of its copy)
+        const double* v = nullptr;
+        [[maybe_unused]] const double* vz = S.zero + lane;
+        [[maybe_unused]] uint32_t o0 = 0, o1 = 0;
+        if constexpr (DEDUP) {
+          o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
+          o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
+        } else {
+          v = S.bval + __ldg(S.voff + base) * 32 + lane;
+        }
         for (int k = 0; k < width; ++k) {
           const uint64_t m = k < 32 ? __shfl_sync(0xffffffffu, m0, k)
                                     : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
+          if constexpr (DEDUP) {
+            const uint32_t o = k < 32 ? __shfl_sync(0xffffffffu, o0, k)
+                                      : (k < 64 ? __shfl_sync(0xffffffffu, o1, k - 32) : __ldg(S.vo + base + k));
+            // lane-uniform slots (bit 60) load every value as a broadcast
+            const int ls = (m >> 60) & 1u ? 0 : lane;
+            v = S.bval + (int64_t)o * 32 + ls;
+            vz = S.zero + ls;
+          }
           if (k < n) {
             double xv[BC];
             load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
@@ -457,14 +662,15 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? CAMG_MASKED_MINB : (BR
 #pragma unroll
             for (int q = 0; q < BE; ++q) {
               const int g = (int)((m >> (4 * q)) & 15u);
-              CAMG_DCHECK(!g || S.ngroups == 0 || (v - S.bval - lane) / 32 + g - 1 < S.ngroups,
+              CAMG_DCHECK(!g || S.ngroups == 0 || (v - S.bval) / 32 + g - 1 < S.ngroups,
                           "sell value group out of range");
-              val[q] = __ldcs(g ? v + (g - 1) * 32 : S.zero + lane);
+              if constexpr (DEDUP) val[q] = __ldg(g ? v + (g - 1) * 32 : vz);
+              else val[q] = __ldcs(g ? v + (g - 1) * 32 : S.zero + lane);
             }
 #pragma unroll
             for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
           }
-          v += (int)(m >> 60) * 32;
+          if constexpr (!DEDUP) v += (int)(m >> 60) * 32;
         }
       }
     }
@@ -568,6 +774,7 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->zero, S->nbr, S->nslices};
   v.ncb = S->ncb;
   v.ngroups = S->masked ? S->ngroups : 0;
+  v.vo = S->vo;
   v.slist = slist;
   v.nwork = slist ? nlist : S->nslices;
   if (v.nwork <= 0) return;
@@ -581,7 +788,8 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   note_launch();
 #define CAMG_SELL_LAUNCH(Z, SP, M)                                                           \
   do {                                                                                       \
-    if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, kSellThreads, 0, st, v, xu, xl, sb, e);         \
+    if (S->masked && S->dedup) launch_k(k_sell_row<BR, BC, Z, SP, M, true, true>, grid, kSellThreads, 0, st, v, xu, xl, sb, e); \
+    else if (S->masked) launch_k(k_sell_row<BR, BC, Z, SP, M, true>, grid, kSellThreads, 0, st, v, xu, xl, sb, e);         \
     else if (nw < quad_slices() || (nw < pair_slices() && long_rows))                       \
       launch_k(k_sell_row2<BR, BC, Z, SP, M, 4>, grid_for(nw * 128, 256, int64_t(kNumSMs) * 16), 256, 0, st, \
                v, xu, xl, sb, e);                                                            \
@@ -760,6 +968,14 @@ extern "C" int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t 
     M->sell = nullptr;
     if (br <= 0 || bc <= 0 || nrows <= 0) return;
     M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0, false);
+  });
+}
+
+extern "C" int camg_csr_value_groups(const camg_csr* A, int64_t* kept, int64_t* full) {
+  return guarded([&] {
+    const Sell* S = A->m->sell;
+    *kept = S ? S->ngroups : 0;
+    *full = S ? (S->dedup ? S->ngroups_full : S->ngroups) : 0;
   });
 }
 

@@ -22,6 +22,12 @@ struct Sell {
   unsigned long long* desc = nullptr; // per slot (BR*BC <= 15): nibble q = 1 + rank of position q (0: absent),
                                       // bits 36-59 = 1 + first column of a linear slot (0: load bcol), bits 60-63 = count
   double* zero = nullptr;             // masked: one zero value group (absent positions load it)
+  // shared value groups (masked mirrors): slots whose stored values are bit-identical (the interior stencil
+  // of a structured mesh repeats from slice to slice) keep ONE copy; vo[slot] = first value group of the
+  // slot's copy, desc bit 60 = every group of the slot is lane-uniform (loaded as a broadcast)
+  bool dedup = false;
+  uint32_t* vo = nullptr;
+  int64_t ngroups_full = 0;           // value groups before sharing
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
   double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]
   ~Sell();
@@ -41,6 +47,7 @@ struct SellView {
   const int32_t* __restrict__ slist = nullptr;  // optional subset of slices to process
   int64_t nwork = 0;                            // slices to process (slist length, or nslices)
   int64_t ncb = 0, ngroups = 0;                 // bounds for the checked build (0: unknown)
+  const uint32_t* __restrict__ vo = nullptr;    // shared value groups: first group of each slot
 };
 
 // epilogue arguments of the three SELL row kernels (modes 0/1/2)

@@ -353,6 +353,39 @@ def test_masked_sell_bit_identical_to_full_blocks(cfg, scale, bs, monkeypatch):
     assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("cfg,scale,bs", [("C3", 1, 3), ("C5", 3, 3)])
+def test_shared_value_groups_bit_identical(cfg, scale, bs, monkeypatch):
+    """Masked mirrors keep one copy of bit-identical slots (the interior
+    stencil of a structured mesh): the sharing engages on the configs' fine
+    operators, stores a small fraction of the value groups, and the merged
+    SpMV is bit-identical to the streaming layout (CAMG_SELL_DEDUP=0) and to
+    full blocks."""
+    import ctypes as C
+    import torch
+    from paper_1912_09056_b200.sparse import empty, ptr, stream_ptr
+    g = generate(config_spec(cfg, scale))
+    op = saddle_operator(g)
+    A = op.merged()
+    n = A.num_rows
+    x = torch.from_numpy(np.random.default_rng(11).standard_normal(n)).cuda()
+    out, groups = {}, {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("CAMG_SELL_DEDUP", m)
+        _native.call("camg_csr_attach_blocks", A.device, bs, op.n_u)
+        kept, full = C.c_int64(0), C.c_int64(0)
+        _native.call("camg_csr_value_groups", A.device, C.byref(kept), C.byref(full))
+        groups[m] = (kept.value, full.value)
+        y = empty(n)
+        _native.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
+        torch.cuda.synchronize()
+        out[m] = y.cpu().numpy()
+    assert groups["0"][0] == groups["0"][1] == groups["1"][1]
+    assert groups["1"][0] * 4 < groups["1"][1], groups
+    np.testing.assert_array_equal(out["0"], out["1"])
+    ref = A.to_scipy() @ x.cpu().numpy()
+    assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
 @pytest.mark.parametrize("cfg,scale,sweeps,cluster", [("C5", 10, 1, "1"), ("C5", 10, 1, "0"), ("C4", 8, 2, "1"),
                                                      ("C2", 4, 1, "1")])
 def test_mcilu0_corrector_vs_oracle_emulation(cfg, scale, sweeps, cluster, monkeypatch):
