@@ -52,6 +52,10 @@
 #ifndef CAMG_DEDUP_MINB
 #define CAMG_DEDUP_MINB 4
 #endif
+// lane-uniform slots keep one dense BR x BC block (broadcast loads)
+#ifndef CAMG_DEDUP_UDENSE
+#define CAMG_DEDUP_UDENSE 1
+#endif
 
 namespace camg {
 
@@ -266,7 +270,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 
 __global__ void k_slot_hash(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
                             const double* __restrict__ bval, int64_t slots, unsigned long long* __restrict__ key,
-                            uint32_t* __restrict__ idx) {
+                            uint32_t* __restrict__ idx, uint8_t* __restrict__ uni) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -281,6 +285,15 @@ __global__ void k_slot_hash(const unsigned long long* __restrict__ mask, const i
     if (lane == 0) {
       key[s] = mix64(h ^ mix64(m));
       idx[s] = (uint32_t)s;
+    }
+    if (uni) {
+      bool u = true;
+      for (int g = 0; g < ng; ++g) {
+        const long long b = __double_as_longlong(v[g * 32]);
+        u &= b == __shfl_sync(0xffffffffu, b, 0);
+      }
+      u = __all_sync(0xffffffffu, u);
+      if (lane == 0) uni[s] = u ? 1 : 0;
     }
   }
 }
@@ -316,33 +329,33 @@ __global__ void k_slot_verify(const unsigned long long* __restrict__ mask, const
 }
 
 __global__ void k_slot_own_groups(const unsigned long long* __restrict__ mask, const uint32_t* __restrict__ rep,
-                                  int64_t slots, int64_t* __restrict__ cnt) {
+                                  const uint8_t* __restrict__ uni, int64_t slots, int64_t* __restrict__ cnt) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x)
-    cnt[s] = rep[s] == (uint32_t)s ? __popcll(mask[s]) : 0;
+    cnt[s] = rep[s] == (uint32_t)s ? (uni[s] ? 1 : __popcll(mask[s])) : 0;  // a uniform slot keeps one group
 }
 
-// copy the kept slots' groups to the compact array; uni[s] = every group of s is lane-uniform
+// copy the kept slots' groups to the compact array; a lane-uniform slot (uni)
+// becomes one group holding its dense block: entry q = the value at position
+// q, or 0 where the slot's mask has no entry
 __global__ void k_slot_compact(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
                                const double* __restrict__ bval, const uint32_t* __restrict__ rep,
                                const int64_t* __restrict__ noff, int64_t slots, double* __restrict__ nval,
-                               uint8_t* __restrict__ uni) {
+                               const uint8_t* __restrict__ uni) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t s = warp; s < slots; s += nwarps) {
     if (rep[s] != (uint32_t)s) continue;
-    const int ng = __popcll(mask[s]);
-    const double* a = bval + voff[s] * 32 + lane;
+    const unsigned long long m = mask[s];
+    const int ng = __popcll(m);
+    const double* a = bval + voff[s] * 32;
     double* o = nval + noff[s] * 32 + lane;
-    bool u = true;
-    for (int g = 0; g < ng; ++g) {
-      const double x = a[g * 32];
-      o[g * 32] = x;
-      const long long b = __double_as_longlong(x);
-      u &= b == __shfl_sync(0xffffffffu, b, 0);
+    if (uni[s]) {
+      const bool have = (m >> lane) & 1ull;
+      *o = have ? a[__popcll(m & ((1ull << lane) - 1ull)) * 32] : 0.0;
+    } else {
+      for (int g = 0; g < ng; ++g) o[g * 32] = a[g * 32 + lane];
     }
-    u = __all_sync(0xffffffffu, u);
-    if (lane == 0) uni[s] = u ? 1 : 0;
   }
 }
 
@@ -364,8 +377,11 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   if (slots < 2 || slots >= (int64_t)1 << 32) return;
   DBuf<unsigned long long> key(slots), key2(slots);
   DBuf<uint32_t> idx(slots), sidx(slots), rep(slots);
+  DBuf<uint8_t> uni(slots);
+  CAMG_CUDA(cudaMemsetAsync(uni.p, 0, slots, s));
   note_launch();
-  k_slot_hash<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, slots, key.p, idx.p);
+  k_slot_hash<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, slots, key.p, idx.p,
+                                                        (CAMG_DEDUP_UDENSE && S->br * S->bc <= 32) ? uni.p : nullptr);
   size_t tmp = 0;
   CAMG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, key2.p, idx.p, sidx.p, slots, 0, 64, s));
   {
@@ -389,14 +405,12 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   k_slot_verify<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, sidx.p, head.p, slots, rep.p);
   DBuf<int64_t> cnt(slots + 1), noff(slots + 1);
   note_launch();
-  k_slot_own_groups<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, rep.p, slots, cnt.p);
+  k_slot_own_groups<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, rep.p, uni.p, slots, cnt.p);
   exclusive_scan_i64(cnt.p, noff.p, slots, s);
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t kept = read_i64(noff.p + slots);
   if (kept * 2 > S->ngroups || kept >= (int64_t)1 << 32) return;  // little to share: keep the streaming layout
   DBuf<double> nval((size_t)std::max<int64_t>(kept, 1) * 32);
-  DBuf<uint8_t> uni(slots);
-  CAMG_CUDA(cudaMemsetAsync(uni.p, 0, slots, s));
   note_launch();
   k_slot_compact<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, rep.p, noff.p, slots, nval.p,
                                                            uni.p);
@@ -649,6 +663,39 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
             const int ls = (m >> 60) & 1u ? 0 : lane;
             v = S.bval + (int64_t)o * 32 + ls;
             vz = S.zero + ls;
+          }
+          if constexpr (DEDUP && CAMG_DEDUP_UDENSE) {
+            // lane-uniform slot: its BE values (absent positions stored as
+            // zeros) are one dense block, loaded as broadcasts
+            if ((m >> 60) & 1u) {
+              const uint32_t lin = (uint32_t)(m >> 36) & 0xFFFFFFu;
+              // a linear slot has a block in every lane (k < n for all 32)
+              if (lin || k < n) {
+                double xv[BC];
+                if (lin && (!SPLIT || (int64_t)lin + 30 < split_blocks)) {
+                  const double* xs = xu + ((int64_t)(lin - 1) + lane) * BC;
+#pragma unroll
+                  for (int c = 0; c < BC; ++c) xv[c] = __ldg(xs + c);
+                } else {
+                  load_x(base + k, xv, lin);
+                }
+                const double* vu = v;  // = bval + o * 32 (ls = 0)
+                double val[BE];
+                if constexpr (BE == 9) {
+                  const double2* v2 = reinterpret_cast<const double2*>(vu);
+                  const double2 a = __ldg(v2), b = __ldg(v2 + 1), c = __ldg(v2 + 2), d = __ldg(v2 + 3);
+                  val[0] = a.x; val[1] = a.y; val[2] = b.x; val[3] = b.y;
+                  val[4] = c.x; val[5] = c.y; val[6] = d.x; val[7] = d.y;
+                  val[8] = __ldg(vu + 8);
+                } else {
+#pragma unroll
+                  for (int q = 0; q < BE; ++q) val[q] = __ldg(vu + q);
+                }
+#pragma unroll
+                for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
+              }
+              continue;
+            }
           }
           if (k < n) {
             double xv[BC];
