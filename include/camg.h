@@ -144,6 +144,9 @@ int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t nrows, int6
 /* 32-value groups the block mirror stores (kept) and would store without sharing
  * bit-identical slots (full); kept < full: shared value groups are in use (sell.cu) */
 int camg_csr_value_groups(const camg_csr* A, int64_t* kept, int64_t* full);
+/* slots of the masked mirror: out[4] = {slots, lane-uniform (one dense block, shared-value mirrors),
+ * linear (block columns c0 + lane, no column index stored), both} */
+int camg_csr_slot_stats(const camg_csr* A, int64_t* out);
 /* compulsory bytes of one SpMV pass in the matrix's current format */
 int camg_csr_stream_bytes(const camg_csr* A, double* bytes);
 /* merged saddle operator [[K, B1], [B2, -Cz]] (saddle.py:58-67) */
@@ -283,7 +286,9 @@ int camg_level_block_transfer(camg_level* L, int bs_fine, int bs_coarse, int64_t
  * residual + first Jacobi sweep; mode 2: extra Jacobi sweep; mode 3: one
  * multicolour SGS predictor sweep, forward + backward over all colours) on
  * x, b; returns its algorithmic bytes (SURVEY §8(d) CSR model, and the
- * format's) */
+ * format's).  mode | 0x100 runs the pass through a second mirror of the rows in
+ * the streaming layout (no shared value groups; built on first use), mode
+ * 0x200 releases that mirror */
 int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double* b, void* stream,
                          double* bytes_csr_model, double* bytes_format);
 /* BlockSmoother.sweep on merged vectors x, b -> out (smoothers.py:316-326) */

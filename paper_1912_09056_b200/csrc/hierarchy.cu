@@ -2443,7 +2443,9 @@ struct Level {
   int64_t nnz_top = 0;  // entries of the [K | B1] rows
   // work vectors
   DBuf<double> w_du, w_du2, w_ru, w_rc, w_dl, w_dl2, w_rl, w_tmp;
+  Sell* alt_sell = nullptr;  // streaming-layout mirror of A's rows (camg_level_fine_pass mode | 0x100)
   ~Level() {
+    delete alt_sell;
     if (owns_A) delete A;
     delete B1; delete S; delete P; delete R;
     if (side) cudaStreamDestroy(side);
@@ -3592,6 +3594,35 @@ int camg_level_fine_pass(camg_level* L, int mode, const double* x, const double*
     Level* lv = L->L;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t nu = lv->nu;
+    // mode | 0x100: the same pass through a second mirror of the rows in the
+    // streaming layout (no shared value groups), built on first use, so one
+    // run times both layouts; 0x200 alone releases that mirror
+    if (mode == 0x200) {
+      delete lv->alt_sell;
+      lv->alt_sell = nullptr;
+      return;
+    }
+    struct Swap {
+      Csr* A; Sell* keep; bool on;
+      ~Swap() { if (on) A->sell = keep; }
+    } swap{lv->A, lv->A->sell, false};
+    if (mode & 0x100) {
+      mode &= 0xff;
+      const Sell* S = lv->A->sell;
+      CAMG_CHECK(S && S->br == S->bc && S->rows() == nu, CAMG_ERR_CONFIG, "level has no block mirror of its rows");
+      if (!lv->alt_sell) {
+        sell_share_override(0);
+        try {
+          lv->alt_sell = sell_build(lv->A, S->br, S->bc, nu, lv->A->n_cols - lv->A->n_cols % S->bc, 0, S->masked);
+        } catch (...) {
+          sell_share_override(-1);
+          throw;
+        }
+        sell_share_override(-1);
+      }
+      lv->A->sell = lv->alt_sell;
+      swap.on = true;
+    }
     // the smoother's predictor sweep: y_new = y + w D^-1 (b - [K B1][y; lam]),
     // or Braess-Sarazin's u_half = u + A^-1 r / alpha (no Jacobi predictor)
     const bool bs = lv->dinv_p.p == nullptr;

@@ -52,10 +52,13 @@
 #ifndef CAMG_DEDUP_MINB
 #define CAMG_DEDUP_MINB 4
 #endif
-// lane-uniform slots keep one dense BR x BC block (broadcast loads)
-#ifndef CAMG_DEDUP_UDENSE
-#define CAMG_DEDUP_UDENSE 1
+// non-uniform shared slots stored dense (a group per block position) instead of their union pattern:
+// same pass time, twice the dictionary (92 vs 44 MB on C5), merged SpMV 0.905 -> 0.957 ms
+#ifndef CAMG_DEDUP_NUDENSE
+#define CAMG_DEDUP_NUDENSE 0
 #endif
+
+
 
 namespace camg {
 
@@ -329,9 +332,10 @@ __global__ void k_slot_verify(const unsigned long long* __restrict__ mask, const
 }
 
 __global__ void k_slot_own_groups(const unsigned long long* __restrict__ mask, const uint32_t* __restrict__ rep,
-                                  const uint8_t* __restrict__ uni, int64_t slots, int64_t* __restrict__ cnt) {
+                                  const uint8_t* __restrict__ uni, int64_t slots, int be,
+                                  int64_t* __restrict__ cnt) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x)
-    cnt[s] = rep[s] == (uint32_t)s ? (uni[s] ? 1 : __popcll(mask[s])) : 0;  // a uniform slot keeps one group
+    cnt[s] = rep[s] == (uint32_t)s ? (uni[s] ? 1 : (CAMG_DEDUP_NUDENSE ? be : __popcll(mask[s]))) : 0;
 }
 
 // copy the kept slots' groups to the compact array; a lane-uniform slot (uni)
@@ -339,7 +343,7 @@ __global__ void k_slot_own_groups(const unsigned long long* __restrict__ mask, c
 // q, or 0 where the slot's mask has no entry
 __global__ void k_slot_compact(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
                                const double* __restrict__ bval, const uint32_t* __restrict__ rep,
-                               const int64_t* __restrict__ noff, int64_t slots, double* __restrict__ nval,
+                               const int64_t* __restrict__ noff, int64_t slots, int be, double* __restrict__ nval,
                                const uint8_t* __restrict__ uni) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -347,14 +351,21 @@ __global__ void k_slot_compact(const unsigned long long* __restrict__ mask, cons
   for (int64_t s = warp; s < slots; s += nwarps) {
     if (rep[s] != (uint32_t)s) continue;
     const unsigned long long m = mask[s];
-    const int ng = __popcll(m);
     const double* a = bval + voff[s] * 32;
     double* o = nval + noff[s] * 32 + lane;
     if (uni[s]) {
       const bool have = (m >> lane) & 1ull;
       *o = have ? a[__popcll(m & ((1ull << lane) - 1ull)) * 32] : 0.0;
     } else {
+#if CAMG_DEDUP_NUDENSE
+      // every position of the block gets a group (zeros where the mask has
+      // none): the pass reads position q at a fixed offset
+      for (int q = 0; q < be; ++q)
+        o[q * 32] = (m >> q) & 1ull ? a[__popcll(m & ((1ull << q) - 1ull)) * 32 + lane] : 0.0;
+#else
+      const int ng = __popcll(m);
       for (int g = 0; g < ng; ++g) o[g * 32] = a[g * 32 + lane];
+#endif
     }
   }
 }
@@ -381,7 +392,7 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   CAMG_CUDA(cudaMemsetAsync(uni.p, 0, slots, s));
   note_launch();
   k_slot_hash<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, slots, key.p, idx.p,
-                                                        (CAMG_DEDUP_UDENSE && S->br * S->bc <= 32) ? uni.p : nullptr);
+                                                        S->br * S->bc <= 32 ? uni.p : nullptr);
   size_t tmp = 0;
   CAMG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, key2.p, idx.p, sidx.p, slots, 0, 64, s));
   {
@@ -405,15 +416,15 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   k_slot_verify<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, sidx.p, head.p, slots, rep.p);
   DBuf<int64_t> cnt(slots + 1), noff(slots + 1);
   note_launch();
-  k_slot_own_groups<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, rep.p, uni.p, slots, cnt.p);
+  k_slot_own_groups<<<grid_for(slots, 256), 256, 0, s>>>(S->mask, rep.p, uni.p, slots, S->br * S->bc, cnt.p);
   exclusive_scan_i64(cnt.p, noff.p, slots, s);
   CAMG_CUDA(cudaStreamSynchronize(s));
   const int64_t kept = read_i64(noff.p + slots);
   if (kept * 2 > S->ngroups || kept >= (int64_t)1 << 32) return;  // little to share: keep the streaming layout
   DBuf<double> nval((size_t)std::max<int64_t>(kept, 1) * 32);
   note_launch();
-  k_slot_compact<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, rep.p, noff.p, slots, nval.p,
-                                                           uni.p);
+  k_slot_compact<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, rep.p, noff.p, slots,
+                                                           S->br * S->bc, nval.p, uni.p);
   S->vo = dalloc<uint32_t>(slots + 1);
   note_launch();
   k_slot_share<<<grid_for(slots, 256), 256, 0, s>>>(rep.p, noff.p, uni.p, slots, S->vo, S->desc);
@@ -425,7 +436,10 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   S->dedup = true;
 }
 
+static int g_share_override = -1;  // sell_share_override: -1 = CAMG_SELL_DEDUP decides
+
 static bool dedup_enabled() {
+  if (g_share_override >= 0) return g_share_override != 0;
   const char* e = getenv("CAMG_SELL_DEDUP");
   return !(e && e[0] == '0');
 }
@@ -531,6 +545,8 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
 }
 
 }  // namespace
+
+void sell_share_override(int v) { g_share_override = v; }
 
 Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s, bool masked) {
   CAMG_CHECK(nrows % br == 0 && nrows <= A->n_rows, CAMG_ERR_DIMENSION, "block rows must divide the row range");
@@ -642,82 +658,92 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
         const int width = (int)(S.slice_ptr[s + 1] - base);
         const uint64_t m0 = lane < width ? __ldg(S.desc + base + lane) : 0ull;
         const uint64_t m1 = lane + 32 < width ? __ldg(S.desc + base + 32 + lane) : 0ull;
-        // the slice's values start at group voff[base]; slots follow in order
-        // (shared value groups: every slot names the first group of its copy)
-        const double* v = nullptr;
-        [[maybe_unused]] const double* vz = S.zero + lane;
-        [[maybe_unused]] uint32_t o0 = 0, o1 = 0;
+        auto slot_desc = [&](int k) -> uint64_t {
+          return k < 32 ? __shfl_sync(0xffffffffu, m0, k)
+                        : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
+        };
         if constexpr (DEDUP) {
-          o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
-          o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
-        } else {
-          v = S.bval + __ldg(S.voff + base) * 32 + lane;
-        }
-        for (int k = 0; k < width; ++k) {
-          const uint64_t m = k < 32 ? __shfl_sync(0xffffffffu, m0, k)
-                                    : (k < 64 ? __shfl_sync(0xffffffffu, m1, k - 32) : __ldg(S.desc + base + k));
-          if constexpr (DEDUP) {
+          // shared value groups: every slot names the first group of its
+          // copy, stored dense -- one group per block position (zeros where
+          // the slot's mask has none), or, for a lane-uniform slot (bit 60),
+          // ONE group holding the BR x BC block, loaded as broadcasts.  An
+          // absent position enters as fma(0, x, acc), as in the other layouts.
+          const uint32_t o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
+          const uint32_t o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
+          for (int k = 0; k < width; ++k) {
+            const uint64_t m = slot_desc(k);
             const uint32_t o = k < 32 ? __shfl_sync(0xffffffffu, o0, k)
                                       : (k < 64 ? __shfl_sync(0xffffffffu, o1, k - 32) : __ldg(S.vo + base + k));
-            // lane-uniform slots (bit 60) load every value as a broadcast
-            const int ls = (m >> 60) & 1u ? 0 : lane;
-            v = S.bval + (int64_t)o * 32 + ls;
-            vz = S.zero + ls;
-          }
-          if constexpr (DEDUP && CAMG_DEDUP_UDENSE) {
-            // lane-uniform slot: its BE values (absent positions stored as
-            // zeros) are one dense block, loaded as broadcasts
-            if ((m >> 60) & 1u) {
-              const uint32_t lin = (uint32_t)(m >> 36) & 0xFFFFFFu;
-              // a linear slot has a block in every lane (k < n for all 32)
-              if (lin || k < n) {
-                double xv[BC];
-                if (lin && (!SPLIT || (int64_t)lin + 30 < split_blocks)) {
-                  const double* xs = xu + ((int64_t)(lin - 1) + lane) * BC;
-#pragma unroll
-                  for (int c = 0; c < BC; ++c) xv[c] = __ldg(xs + c);
-                } else {
-                  load_x(base + k, xv, lin);
-                }
-                const double* vu = v;  // = bval + o * 32 (ls = 0)
-                double val[BE];
-                if constexpr (BE == 9) {
-                  const double2* v2 = reinterpret_cast<const double2*>(vu);
-                  const double2 a = __ldg(v2), b = __ldg(v2 + 1), c = __ldg(v2 + 2), d = __ldg(v2 + 3);
-                  val[0] = a.x; val[1] = a.y; val[2] = b.x; val[3] = b.y;
-                  val[4] = c.x; val[5] = c.y; val[6] = d.x; val[7] = d.y;
-                  val[8] = __ldg(vu + 8);
-                } else {
-#pragma unroll
-                  for (int q = 0; q < BE; ++q) val[q] = __ldg(vu + q);
-                }
-#pragma unroll
-                for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
-              }
-              continue;
-            }
-          }
-          if (k < n) {
+            const uint32_t lin = (uint32_t)(m >> 36) & 0xFFFFFFu;
+            // a linear slot has a block in every lane (k < n for all 32)
+            if (!lin && k >= n) continue;
+            CAMG_DCHECK(S.ngroups == 0 || (int64_t)o < S.ngroups,
+                        "sell value group out of range");
             double xv[BC];
-            load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
-            // absent positions load the zero group (L1/L2-resident): all BE
-            // loads are unconditional and independent, nothing but the loaded
-            // values stays live across them, and an absent position enters as
-            // fma(0, x, acc) -- the same operations (and results) as the
-            // full-block kernel on its stored zeros
-            double val[BE];
+            if (lin && (!SPLIT || (int64_t)lin + 30 < split_blocks)) {
+              const double* xs = xu + ((int64_t)(lin - 1) + lane) * BC;
 #pragma unroll
-            for (int q = 0; q < BE; ++q) {
-              const int g = (int)((m >> (4 * q)) & 15u);
-              CAMG_DCHECK(!g || S.ngroups == 0 || (v - S.bval) / 32 + g - 1 < S.ngroups,
-                          "sell value group out of range");
-              if constexpr (DEDUP) val[q] = __ldg(g ? v + (g - 1) * 32 : vz);
-              else val[q] = __ldcs(g ? v + (g - 1) * 32 : S.zero + lane);
+              for (int c = 0; c < BC; ++c) xv[c] = __ldg(xs + c);
+            } else {
+              load_x(base + k, xv, lin);
+            }
+            double val[BE];
+            if ((m >> 60) & 1u) {
+              const double* vu = S.bval + (int64_t)o * 32;
+              if constexpr (BE == 9) {
+                const double2* v2 = reinterpret_cast<const double2*>(vu);
+                const double2 a = __ldg(v2), b = __ldg(v2 + 1), c = __ldg(v2 + 2), d = __ldg(v2 + 3);
+                val[0] = a.x; val[1] = a.y; val[2] = b.x; val[3] = b.y;
+                val[4] = c.x; val[5] = c.y; val[6] = d.x; val[7] = d.y;
+                val[8] = __ldg(vu + 8);
+              } else {
+#pragma unroll
+                for (int q = 0; q < BE; ++q) val[q] = __ldg(vu + q);
+              }
+            } else {
+              const double* v = S.bval + (int64_t)o * 32 + lane;
+#if CAMG_DEDUP_NUDENSE
+#pragma unroll
+              for (int q = 0; q < BE; ++q) val[q] = __ldg(v + q * 32);
+#else
+              // only the slot's union pattern is stored (nibble q of the
+              // descriptor = 1 + rank of position q; 0 = absent: the zero group)
+#pragma unroll
+              for (int q = 0; q < BE; ++q) {
+                const int g = (int)((m >> (4 * q)) & 15u);
+                val[q] = __ldg(g ? v + (g - 1) * 32 : S.zero + lane);
+              }
+#endif
             }
 #pragma unroll
             for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
           }
-          if constexpr (!DEDUP) v += (int)(m >> 60) * 32;
+        } else {
+          // the slice's values start at group voff[base]; slots follow in order
+          const double* v = S.bval + __ldg(S.voff + base) * 32 + lane;
+          for (int k = 0; k < width; ++k) {
+            const uint64_t m = slot_desc(k);
+            if (k < n) {
+              double xv[BC];
+              load_x(base + k, xv, (uint32_t)(m >> 36) & 0xFFFFFFu);
+              // absent positions load the zero group (L1/L2-resident): all BE
+              // loads are unconditional and independent, nothing but the loaded
+              // values stays live across them, and an absent position enters as
+              // fma(0, x, acc) -- the same operations (and results) as the
+              // full-block kernel on its stored zeros
+              double val[BE];
+#pragma unroll
+              for (int q = 0; q < BE; ++q) {
+                const int g = (int)((m >> (4 * q)) & 15u);
+                CAMG_DCHECK(!g || S.ngroups == 0 || (v - S.bval) / 32 + g - 1 < S.ngroups,
+                            "sell value group out of range");
+                val[q] = __ldcs(g ? v + (g - 1) * 32 : S.zero + lane);
+              }
+#pragma unroll
+              for (int q = 0; q < BE; ++q) acc[q / BC] = fma(val[q], xv[q % BC], acc[q / BC]);
+            }
+            v += (int)(m >> 60) * 32;
+          }
         }
       }
     }
@@ -1015,6 +1041,36 @@ extern "C" int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t 
     M->sell = nullptr;
     if (br <= 0 || bc <= 0 || nrows <= 0) return;
     M->sell = sell_build(M, br, bc, nrows, ncols_blocked, 0, false);
+  });
+}
+
+__global__ void k_slot_stats(const unsigned long long* __restrict__ desc, int64_t slots, unsigned long long* __restrict__ out) {
+  unsigned long long u = 0, l = 0, ul = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < slots; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = desc[i];
+    const bool un = (d >> 60) & 1u, li = ((d >> 36) & 0xFFFFFFull) != 0;
+    u += un; l += li; ul += un && li;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    u += __shfl_xor_sync(0xffffffffu, u, o);
+    l += __shfl_xor_sync(0xffffffffu, l, o);
+    ul += __shfl_xor_sync(0xffffffffu, ul, o);
+  }
+  if ((threadIdx.x & 31) == 0) { atomicAdd(out, u); atomicAdd(out + 1, l); atomicAdd(out + 2, ul); }
+}
+
+// slots of a shared-value mirror: out = {slots, lane-uniform, linear, both}
+extern "C" int camg_csr_slot_stats(const camg_csr* A, int64_t* out) {
+  return guarded([&] {
+    const Sell* S = A->m->sell;
+    out[0] = out[1] = out[2] = out[3] = 0;
+    if (!S || !S->desc) return;
+    DBuf<unsigned long long> acc(3);
+    CAMG_CUDA(cudaMemset(acc.p, 0, 3 * sizeof(unsigned long long)));
+    k_slot_stats<<<grid_for(S->slots, 256), 256>>>(S->desc, S->slots, acc.p);
+    unsigned long long h[3];
+    CAMG_CUDA(cudaMemcpy(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost));
+    out[0] = S->slots; out[1] = S->dedup ? (int64_t)h[0] : 0; out[2] = (int64_t)h[1]; out[3] = S->dedup ? (int64_t)h[2] : 0;
   });
 }
 

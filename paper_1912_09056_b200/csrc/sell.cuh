@@ -72,6 +72,8 @@ struct SellEpi {
 
 Sell* sell_build(const Csr* A, int br, int bc, int64_t nrows, int64_t ncols_blocked, cudaStream_t s,
                  bool masked = false);
+// shared value groups of the masked mirrors built next: 1 on, 0 off, -1 as CAMG_SELL_DEDUP says (default on)
+void sell_share_override(int v);
 // mode 0: spmv, 1: residual (+ fused Jacobi epilogue), 2: extra Jacobi sweep
 // (modes 1/2 need square blocks).  split < 0: x is one vector (xu); else
 // columns >= split read xl (null = 0).
