@@ -246,6 +246,17 @@ int camg_qr_batch(const char* lapack_path, int64_t G, int M, int k, const double
 int camg_tentative(const char* lapack_path, int64_t n_dofs, int k, const double* vecs, const int64_t* dof_node,
                    const int64_t* node_to_agg, int64_t num_nodes, int64_t na, double rank_tol, int nthreads,
                    camg_csr** P_out, int64_t* rank_out, double* coarse_ns, int64_t* ncoarse);
+/* The same with the pivoted QR on the device (tentqr.cu):
+ * one warp per aggregate runs LAPACK's dlaqp2 + dorg2r algorithm in shared
+ * memory.  Factors equal scipy's to rounding where the pivot order is decided
+ * by more than rounding; mathematically tied columns (rotation modes of
+ * symmetric aggregates) may come out in another order / sign -- the same
+ * coarse space and projector P P^T in another basis.  A GPU variant compared
+ * by spanned space and convergence; the bit-identical camg_tentative stays
+ * the default (transfer.py: CAMG_TENTATIVE=gpu selects this one).           */
+int camg_tentative_device(int64_t n_dofs, int k, const double* vecs, const int64_t* dof_node,
+                          const int64_t* node_to_agg, int64_t num_nodes, int64_t na, double rank_tol,
+                          camg_csr** P_out, int64_t* rank_out, double* coarse_ns, int64_t* ncoarse);
 /* Allocates an empty n_rows x n_cols matrix with nnz slots (filled by
  * camg_assemble_stencil). */
 int camg_csr_alloc(int64_t n_rows, int64_t n_cols, int64_t nnz, camg_csr** out);

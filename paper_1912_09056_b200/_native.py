@@ -149,6 +149,8 @@ _SIGS = {
     "camg_qr_batch": (C.c_int, [C.c_char_p, i64, C.c_int, C.c_int, vp, i64, vp, vp, vp, vp, C.c_int, P64]),
     "camg_tentative": (C.c_int, [C.c_char_p, i64, C.c_int, vp, vp, vp, i64, i64, f64, C.c_int, C.POINTER(vp), vp, vp,
                                  P64]),
+    "camg_tentative_device": (C.c_int, [i64, C.c_int, vp, vp, vp, i64, i64, f64, C.POINTER(vp), vp, vp,
+                                        C.POINTER(i64)]),
     "camg_dot": (C.c_int, [i64, vp, vp, C.POINTER(f64), vp]),
     "camg_axpy": (C.c_int, [i64, f64, vp, vp, vp]),
 }

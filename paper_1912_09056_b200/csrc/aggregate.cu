@@ -398,49 +398,54 @@ __global__ void k_ptent(PtGroup gp, const int64_t* __restrict__ dofs, const doub
   }
 }
 
-// device CSR of P_tent from the per-group QR factors (see camg_tentative_csr)
+// device CSR of P_tent from the per-group QR factors already on the device
+// (d_rank, d_col0 in group order)
+Csr* tentative_assemble_dev(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta,
+                            const int64_t* d_dofs, const double* d_q, const int64_t* d_rank, const int64_t* d_col0) {
+  cudaStream_t s = 0;
+  DBuf<int64_t> cnt(n_dofs + 1);
+  CAMG_CUDA(cudaMemset(cnt.p, 0, sizeof(int64_t) * (n_dofs + 1)));
+  for (int64_t gi = 0; gi < ngroups; ++gi) {
+    const int64_t* m = meta + 6 * gi;
+    PtGroup gp{m[0], m[1], m[2], m[3], m[4], m[5]};
+    note_launch();
+    k_ptent<false><<<grid_for(gp.G * gp.M, 256), 256, 0, s>>>(gp, d_dofs, d_q, d_rank, d_col0, cnt.p, nullptr, nullptr,
+                                                               nullptr);
+  }
+  DBuf<int64_t> rp(n_dofs + 1);
+  exclusive_scan_i64(cnt.p, rp.p, n_dofs, s);
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  const int64_t nnz = read_i64(rp.p + n_dofs);
+  Csr* P = new Csr();
+  P->n_rows = n_dofs; P->n_cols = ncoarse; P->nnz = nnz;
+  P->rowptr = rp.release();
+  P->col = dalloc<int32_t>(nnz);
+  P->val = dalloc<double>(nnz);
+  P->avg_row = n_dofs ? double(nnz) / n_dofs : 0.0;
+  for (int64_t gi = 0; gi < ngroups; ++gi) {
+    const int64_t* m = meta + 6 * gi;
+    PtGroup gp{m[0], m[1], m[2], m[3], m[4], m[5]};
+    note_launch();
+    k_ptent<true><<<grid_for(gp.G * gp.M, 256), 256, 0, s>>>(gp, d_dofs, d_q, d_rank, d_col0, nullptr, P->rowptr, P->col,
+                                                              P->val);
+  }
+  CAMG_LAUNCH_CHECK();
+  CAMG_CUDA(cudaStreamSynchronize(s));
+  return P;
+}
+
+// device CSR of P_tent from host QR factors (see camg_tentative_csr)
 Csr* tentative_assemble(int64_t n_dofs, int64_t ncoarse, int64_t ngroups, const int64_t* meta, const int64_t* dofs,
                         int64_t ndofs_total, const double* Q, int64_t nq, const int64_t* rank, const int64_t* col0,
                         int64_t naggs) {
-  {
-    cudaStream_t s = 0;
-    CAMG_CHECK(ndofs_total == n_dofs, CAMG_ERR_DIMENSION, "every DOF must belong to one aggregate");
-    DBuf<int64_t> d_dofs(ndofs_total + 1), d_rank(naggs + 1), d_col0(naggs + 1);
-    DBuf<double> d_q(nq + 1);
-    CAMG_CUDA(cudaMemcpy(d_dofs.p, dofs, sizeof(int64_t) * ndofs_total, cudaMemcpyHostToDevice));
-    CAMG_CUDA(cudaMemcpy(d_q.p, Q, sizeof(double) * nq, cudaMemcpyHostToDevice));
-    CAMG_CUDA(cudaMemcpy(d_rank.p, rank, sizeof(int64_t) * naggs, cudaMemcpyHostToDevice));
-    CAMG_CUDA(cudaMemcpy(d_col0.p, col0, sizeof(int64_t) * naggs, cudaMemcpyHostToDevice));
-    DBuf<int64_t> cnt(n_dofs + 1);
-    CAMG_CUDA(cudaMemset(cnt.p, 0, sizeof(int64_t) * (n_dofs + 1)));
-    for (int64_t gi = 0; gi < ngroups; ++gi) {
-      const int64_t* m = meta + 6 * gi;
-      PtGroup gp{m[0], m[1], m[2], m[3], m[4], m[5]};
-      note_launch();
-      k_ptent<false><<<grid_for(gp.G * gp.M, 256), 256, 0, s>>>(gp, d_dofs.p, d_q.p, d_rank.p, d_col0.p, cnt.p,
-                                                                 nullptr, nullptr, nullptr);
-    }
-    DBuf<int64_t> rp(n_dofs + 1);
-    exclusive_scan_i64(cnt.p, rp.p, n_dofs, s);
-    CAMG_CUDA(cudaStreamSynchronize(s));
-    const int64_t nnz = read_i64(rp.p + n_dofs);
-    Csr* P = new Csr();
-    P->n_rows = n_dofs; P->n_cols = ncoarse; P->nnz = nnz;
-    P->rowptr = rp.release();
-    P->col = dalloc<int32_t>(nnz);
-    P->val = dalloc<double>(nnz);
-    P->avg_row = n_dofs ? double(nnz) / n_dofs : 0.0;
-    for (int64_t gi = 0; gi < ngroups; ++gi) {
-      const int64_t* m = meta + 6 * gi;
-      PtGroup gp{m[0], m[1], m[2], m[3], m[4], m[5]};
-      note_launch();
-      k_ptent<true><<<grid_for(gp.G * gp.M, 256), 256, 0, s>>>(gp, d_dofs.p, d_q.p, d_rank.p, d_col0.p, nullptr,
-                                                                P->rowptr, P->col, P->val);
-    }
-    CAMG_LAUNCH_CHECK();
-    CAMG_CUDA(cudaStreamSynchronize(s));
-    return P;
-  }
+  CAMG_CHECK(ndofs_total == n_dofs, CAMG_ERR_DIMENSION, "every DOF must belong to one aggregate");
+  DBuf<int64_t> d_dofs(ndofs_total + 1), d_rank(naggs + 1), d_col0(naggs + 1);
+  DBuf<double> d_q(nq + 1);
+  CAMG_CUDA(cudaMemcpy(d_dofs.p, dofs, sizeof(int64_t) * ndofs_total, cudaMemcpyHostToDevice));
+  CAMG_CUDA(cudaMemcpy(d_q.p, Q, sizeof(double) * nq, cudaMemcpyHostToDevice));
+  CAMG_CUDA(cudaMemcpy(d_rank.p, rank, sizeof(int64_t) * naggs, cudaMemcpyHostToDevice));
+  CAMG_CUDA(cudaMemcpy(d_col0.p, col0, sizeof(int64_t) * naggs, cudaMemcpyHostToDevice));
+  return tentative_assemble_dev(n_dofs, ncoarse, ngroups, meta, d_dofs.p, d_q.p, d_rank.p, d_col0.p);
 }
 
 }  // namespace camg

@@ -7,7 +7,7 @@ files=${@:-sell.cu}
 cd "$(dirname "$0")/../paper_1912_09056_b200/csrc"
 mkdir -p ../ab/build_$name
 objs=""
-for f in sell.cu csr.cu spgemm.cu hierarchy.cu krylov.cu aggregate.cu generator.cu pointsolve.cu hostqr.cu; do
+for f in sell.cu csr.cu spgemm.cu hierarchy.cu krylov.cu aggregate.cu generator.cu pointsolve.cu hostqr.cu tentqr.cu; do
   if [[ " $files " == *" $f "* ]]; then
     /usr/local/cuda/bin/nvcc -O3 -std=c++17 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC -Xcompiler -O3 \
       --expt-relaxed-constexpr -Xptxas -v $flags -c $f -o ../ab/build_$name/${f%.cu}.o 2> ../ab/build_$name/${f%.cu}.ptxas.log

@@ -533,6 +533,86 @@ def test_tentative_prolongator_bit_identical(cfg, scale, py, monkeypatch):
     np.testing.assert_array_equal(rl.coarse_ns.vectors, nsl)
 
 
+def _same_space(P, Po, ns, cns):
+    """P and Po span the same coarse space aggregate by aggregate (equal
+    projectors P P^T) and P reproduces the fine near-kernel: P B_c = B."""
+    D = (P @ P.T - Po @ Po.T).tocsr()
+    scale = scipy.sparse.linalg.norm(Po @ Po.T)
+    assert scipy.sparse.linalg.norm(D) <= 1e-12 * scale
+    assert np.linalg.norm(P @ cns - ns) <= 1e-12 * np.linalg.norm(ns)
+    G = (P.T @ P).tocsr()                      # orthonormal columns
+    assert abs(G - scipy.sparse.identity(G.shape[0])).max() <= 1e-13
+
+
+@pytest.mark.parametrize("cfg,scale", [("C5", 4), ("C2", 2), ("C3", 4), ("C1", 1)])
+def test_device_tentative_prolongator_vs_lapack(cfg, scale, monkeypatch):
+    """the per-aggregate pivoted QR on the device
+    (camg_tentative_device: LAPACK's dlaqp2 + dorg2r, one warp per aggregate)
+    against the reference's scipy.linalg.qr (oracle): ranks and coarse DOF
+    ownership identical, the same coarse space aggregate by aggregate (equal
+    projectors P P^T to 1e-12), orthonormal columns, P B_c = B.  Columns whose
+    pivot order LAPACK decides by rounding (mathematically tied rotation
+    modes) may come in another order, so the factors themselves are compared
+    elementwise only where no pivot is tied (the block-shapes test below)."""
+    import scipy.sparse.linalg  # noqa: F401
+    monkeypatch.setenv("CAMG_TENTATIVE", "gpu")
+    from paper_1912_09056_b200.aggregation import aggregate_greedy, aggregate_lagrange, filtered_node_graph
+    from paper_1912_09056_b200.transfer import tentative_prolongator
+    g = generate(config_spec(cfg, scale))
+    oop, ometa, _ = O.system_from_generated(g)
+    meta = fine_level_meta(g)
+    op = saddle_operator(g)
+    gr = filtered_node_graph(op.K, meta.u_dof_node, meta.num_u_nodes, meta.node_body)
+    ag = aggregate_greedy(gr, 6)
+    ip, ix = O.node_graph(oop.K, ometa.u_dof_node, ometa.num_u_nodes, ometa.node_body)
+    oag = O.greedy(ip, ix, ometa.num_u_nodes, 6)
+    launches = _native.launch_count()
+    res = tentative_prolongator(ag, meta.ns_u, dof_node=meta.u_dof_node)
+    assert _native.launch_count() > launches
+    Po, nso, cao, dro = O.tentative(oag, ometa.ns_u, ometa.u_dof_node)
+    np.testing.assert_array_equal(res.coarse_dof_agg, cao)
+    assert res.dropped_columns == dro
+    _same_space(res.P.to_scipy(), Po, np.asarray(ometa.ns_u), res.coarse_ns.vectors)
+    la = aggregate_lagrange(ag, meta.mortar_block, meta.lmap)
+    ola = O.lagrange(oag, ometa.mortar, ometa.slave_dofs, ometa.row_node, ometa.lm_node_of_lm_dof)
+    rl = tentative_prolongator(la, meta.ns_lam, dof_node=meta.lam_dof_node)
+    Pl, nsl, cal, _ = O.tentative(ola, ometa.ns_lam, ometa.lam_dof_node)
+    np.testing.assert_array_equal(rl.coarse_dof_agg, cal)
+    _same_space(rl.P.to_scipy(), Pl, np.asarray(ometa.ns_lam), rl.coarse_ns.vectors)
+
+
+def test_device_tentative_prolongator_block_shapes(monkeypatch):
+    """Device QR on hand-made aggregates: tall, square, wide (fewer rows than
+    vectors), single-row, rank-deficient (a repeated column: one coarse DOF
+    dropped) and mixed sizes in one call, against the oracle's scipy QR."""
+    monkeypatch.setenv("CAMG_TENTATIVE", "gpu")
+    from paper_1912_09056_b200.aggregation import Aggregation
+    from paper_1912_09056_b200.transfer import NullSpace, tentative_prolongator
+    rng = np.random.default_rng(3)
+    k = 6
+    sizes = [40, 6, 3, 1, 17, 40, 9, 100, 6, 2]
+    n = sum(sizes)
+    perm = rng.permutation(n)                       # DOFs of an aggregate are not contiguous
+    node_to_agg = np.empty(n, dtype=np.int64)
+    node_to_agg[perm] = np.repeat(np.arange(len(sizes)), sizes)
+    vecs = rng.standard_normal((n, k))
+    rows4 = np.flatnonzero(node_to_agg == 4)
+    vecs[rows4, 5] = vecs[rows4, 2]                 # rank-deficient block (exact repeat)
+    rows6 = np.flatnonzero(node_to_agg == 6)
+    vecs[rows6, 1] = 0.0                            # a zero column
+    roots = np.zeros(len(sizes), dtype=np.int64)
+    ag = Aggregation(node_to_agg, len(sizes), roots)
+    res = tentative_prolongator(ag, NullSpace(vecs, "rigid"), dofs_per_node=1)
+    oag = O.Aggregates(node_to_agg, len(sizes), roots)
+    Po, nso, cao, dro = O.tentative(oag, vecs, np.arange(n))
+    P = res.P.to_scipy()
+    assert res.dropped_columns == dro and dro >= 2 + (6 - 3) + (6 - 1) + (6 - 2)
+    np.testing.assert_array_equal(res.coarse_dof_agg, cao)
+    assert same_pattern(P, Po)
+    assert np.max(np.abs(P.data - Po.data)) <= 1e-12
+    assert np.linalg.norm(res.coarse_ns.vectors - nso) <= 1e-12 * np.linalg.norm(nso)
+
+
 # ---------------------------------------------------------------------------
 # edge cases (reference behaviour: krylov.py:56-61, hierarchy.py:194,
 # smoothers.py:151-153, saddle.py:22-27)

@@ -125,6 +125,28 @@ def test_forced_block_sell_restriction_vs_oracle(monkeypatch):
     assert np.linalg.norm(v - ref) <= 1e-10 * np.linalg.norm(ref)
 
 
+@pytest.mark.parametrize("cfg,scale", [("C2", 1), ("C5", 5), ("C3", 2)])
+def test_device_tentative_hierarchy_by_convergence(cfg, scale, monkeypatch):
+    """The benchmarked mapping with the tentative prolongators' pivoted QR on
+    the device (CAMG_TENTATIVE=gpu) on every level.  A
+    GPU variant (tied pivot columns may be ordered differently: the same
+    coarse spaces in another basis), so it is compared with the reference
+    algorithm by structure and convergence: the same level sizes and fine-level
+    aggregates, and GMRES to rtol 1e-8 within +-2 iterations of the oracle."""
+    monkeypatch.setenv("CAMG_TENTATIVE", "gpu")
+    g, op, H, oop, OH, rhs, restart = run_case(cfg, scale)
+    assert H.num_levels == len(OH.levels)
+    np.testing.assert_array_equal(H.levels[0].info["u_agg"], OH.levels[0].info["u_agg"])
+    np.testing.assert_array_equal(H.levels[0].info["lam_agg"], OH.levels[0].info["lam_agg"])
+    assert (H.levels[1].op.n_u, H.levels[1].op.n_lam) == (OH.levels[1].op.K.shape[0], OH.levels[1].op.B2.shape[0])
+    A = oop.merged()
+    _, orep = O.gmres(lambda t: A @ t, OH.apply, rhs, 1e-8, MAX_ITERS, restart)
+    x, rep = gmres(op.apply_merged, H.apply, g.rhs, GmresConfig(rel_tol=1e-8, max_iters=MAX_ITERS, restart=restart))
+    assert orep.converged and rep.converged
+    assert abs(rep.iterations - orep.iterations) <= 2, (rep.iterations, orep.iterations)
+    assert np.linalg.norm(g.rhs - A @ x) <= 2e-8 * np.linalg.norm(g.rhs)
+
+
 def test_size_gated_paths_are_exercised():
     """The cases above, with the default thresholds, run every size-gated
     path of the headline configuration at least once."""
@@ -142,6 +164,8 @@ def test_size_gated_paths_are_exercised():
     for key in (("C3", 1), ("C5", 3)):
         i0 = PATHS_SEEN[key][0]
         assert i0["sell_masked"] and i0["sell_lanes"] == 1 and i0["overlap"], key
+        # ... with shared value groups (bit-identical slots of the structured mesh stored once)
+        assert i0["sell_shared_values"] and i0["sell_value_groups"] * 4 < i0["sell_value_groups_full"], key
 
 
 # ---------------------------------------------------------------------------
