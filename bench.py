@@ -37,17 +37,20 @@ TRAFFIC = {
     # dram__bytes_write.sum 0.176220 GB, 2.062 ms
     "C5": 13.598776e9,
 }
-# the same pass with shared value groups (profiles/r02_dominant_kernel_shared_c5.ncu-rep)
-TRAFFIC_SHARED = {}
+# the same pass with shared value groups (profiles/r02_dominant_kernel_shared_c5.ncu-rep:
+# k_sell_row<3,3,0,1,1,1,1>, dram__bytes_read.sum 858.25 MB + dram__bytes_write.sum 175.10 MB, 1.03 ms)
+TRAFFIC_SHARED = {"C5": 1.033341e9}
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 # DRAM bytes of one whole V-cycle summed over its ncu launch list (dram__bytes_read.sum +
 # dram__bytes_write.sum per kernel, serialised, cold cache) and the cycle time of the
 # same build: the measured (not modelled) V-cycle bandwidth
 VCYCLE_DRAM = {
-    "C5": {"dram_bytes_per_cycle": 111.70e9, "source": "profiles/r02_vcycle_launches_C5.csv (522 kernels, one cycle)"},
-    "C3": {"dram_bytes_per_cycle": 4.16e9, "source": "profiles/r02_vcycle_launches_C3.csv (283 kernels, one cycle)"},
-    "C2": {"dram_bytes_per_cycle": 0.35e9, "source": "profiles/r02_vcycle_launches_C2.csv (57 kernels, one cycle)"},
+    "C5": {"dram_bytes_per_cycle": 36.76e9, "source": "profiles/r02b_vcycle_launches_C5.csv (510 kernels, one cycle)"},
+    "C3": {"dram_bytes_per_cycle": 2.11e9, "source": "profiles/r02b_vcycle_launches_C3.csv (271 kernels, one cycle)"},
+    "C2": {"dram_bytes_per_cycle": 0.39e9, "source": "profiles/r02b_vcycle_launches_C2.csv (45 kernels, one cycle)"},
 }
+# the same lists before shared value groups (streaming layout, CAMG_SELL_DEDUP=0): profiles/r02_vcycle_launches_*.csv
+VCYCLE_DRAM_STREAMING = {"C5": 111.70e9, "C3": 4.16e9, "C2": 0.35e9}
 
 # BASELINE.json's literal smoother per config and why the bench runs another
 # (reference-side evidence: profiles/r02_convergence_table.md §2)

@@ -670,23 +670,26 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
           // absent position enters as fma(0, x, acc), as in the other layouts.
           const uint32_t o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
           const uint32_t o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
-          for (int k = 0; k < width; ++k) {
-            const uint64_t m = slot_desc(k);
-            const uint32_t o = k < 32 ? __shfl_sync(0xffffffffu, o0, k)
-                                      : (k < 64 ? __shfl_sync(0xffffffffu, o1, k - 32) : __ldg(S.vo + base + k));
-            const uint32_t lin = (uint32_t)(m >> 36) & 0xFFFFFFu;
-            // a linear slot has a block in every lane (k < n for all 32)
-            if (!lin && k >= n) continue;
-            CAMG_DCHECK(S.ngroups == 0 || (int64_t)o < S.ngroups,
-                        "sell value group out of range");
-            double xv[BC];
+          // x of slot k (a linear slot has a block in every lane: k < n for all 32)
+          auto fetch_x = [&](int k, uint64_t mk, double* xo) {
+            const uint32_t lin = (uint32_t)(mk >> 36) & 0xFFFFFFu;
             if (lin && (!SPLIT || (int64_t)lin + 30 < split_blocks)) {
               const double* xs = xu + ((int64_t)(lin - 1) + lane) * BC;
 #pragma unroll
-              for (int c = 0; c < BC; ++c) xv[c] = __ldg(xs + c);
-            } else {
-              load_x(base + k, xv, lin);
+              for (int c = 0; c < BC; ++c) xo[c] = __ldg(xs + c);
+            } else if (lin || k < n) {
+              load_x(base + k, xo, lin);
             }
+          };
+          for (int k = 0; k < width; ++k) {
+            const uint32_t o = k < 32 ? __shfl_sync(0xffffffffu, o0, k)
+                                      : (k < 64 ? __shfl_sync(0xffffffffu, o1, k - 32) : __ldg(S.vo + base + k));
+            double xv[BC];
+            const uint64_t m = slot_desc(k);
+            if (!((uint32_t)(m >> 36) & 0xFFFFFFu) && k >= n) continue;
+            fetch_x(k, m, xv);
+            CAMG_DCHECK(S.ngroups == 0 || (int64_t)o < S.ngroups,
+                        "sell value group out of range");
             double val[BE];
             if ((m >> 60) & 1u) {
               const double* vu = S.bval + (int64_t)o * 32;
