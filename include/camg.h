@@ -144,8 +144,8 @@ int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t nrows, int6
 /* 32-value groups the block mirror stores (kept) and would store without sharing
  * bit-identical slots (full); kept < full: shared value groups are in use (sell.cu) */
 int camg_csr_value_groups(const camg_csr* A, int64_t* kept, int64_t* full);
-/* slots of the masked mirror: out[4] = {slots, lane-uniform (one dense block, shared-value mirrors),
- * linear (block columns c0 + lane, no column index stored), both} */
+/* slots of the masked mirror: out[5] = {slots, lane-uniform (one dense block, shared-value mirrors),
+ * linear (block columns c0 + lane, no column index stored), both, uniform but for one or two lanes} */
 int camg_csr_slot_stats(const camg_csr* A, int64_t* out);
 /* compulsory bytes of one SpMV pass in the matrix's current format */
 int camg_csr_stream_bytes(const camg_csr* A, double* bytes);

@@ -273,7 +273,7 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
 
 __global__ void k_slot_hash(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
                             const double* __restrict__ bval, int64_t slots, unsigned long long* __restrict__ key,
-                            uint32_t* __restrict__ idx, uint8_t* __restrict__ uni) {
+                            uint32_t* __restrict__ idx, uint8_t* __restrict__ uni, uint32_t* __restrict__ uinfo) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -290,13 +290,31 @@ __global__ void k_slot_hash(const unsigned long long* __restrict__ mask, const i
       idx[s] = (uint32_t)s;
     }
     if (uni) {
-      bool u = true;
-      for (int g = 0; g < ng; ++g) {
-        const long long b = __double_as_longlong(v[g * 32]);
-        u &= b == __shfl_sync(0xffffffffu, b, 0);
+      // kind 1: every lane holds the same block.  kind 2: all but one or two
+      // lanes do (a slice that straddles a mesh row: the two boundary nodes
+      // differ) -- info = majority lane | exception lanes << 8, << 16 (0xFF: none)
+      unsigned kind = 0, info = 0;
+      unsigned tried = 0;
+      for (int t = 0; t < 3 && !kind; ++t) {
+        // candidate majority lane: the lowest lane not yet known to be an exception
+        const int a = __ffs(~tried) - 1;
+        bool eq = true;
+        for (int g = 0; g < ng; ++g) {
+          const long long b = __double_as_longlong(v[g * 32]);
+          eq &= b == __shfl_sync(0xffffffffu, b, a);
+        }
+        const unsigned same = __ballot_sync(0xffffffffu, eq);
+        const unsigned exc = ~same;
+        if (exc == 0) kind = 1;
+        else if (__popc(exc) <= 2) {
+          kind = 2;
+          const int e0 = __ffs(exc) - 1;
+          const unsigned rest = exc & (exc - 1);
+          const int e1 = rest ? __ffs(rest) - 1 : 0xFF;
+          info = (unsigned)a | ((unsigned)e0 << 8) | ((unsigned)e1 << 16);
+        } else tried |= same;  // lane a and its equals are the exceptions, if anything
       }
-      u = __all_sync(0xffffffffu, u);
-      if (lane == 0) uni[s] = u ? 1 : 0;
+      if (lane == 0) { uni[s] = (uint8_t)kind; uinfo[s] = info; }
     }
   }
 }
@@ -344,7 +362,7 @@ __global__ void k_slot_own_groups(const unsigned long long* __restrict__ mask, c
 __global__ void k_slot_compact(const unsigned long long* __restrict__ mask, const int64_t* __restrict__ voff,
                                const double* __restrict__ bval, const uint32_t* __restrict__ rep,
                                const int64_t* __restrict__ noff, int64_t slots, int be, double* __restrict__ nval,
-                               const uint8_t* __restrict__ uni) {
+                               const uint8_t* __restrict__ uni, const uint32_t* __restrict__ uinfo) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -354,8 +372,16 @@ __global__ void k_slot_compact(const unsigned long long* __restrict__ mask, cons
     const double* a = bval + voff[s] * 32;
     double* o = nval + noff[s] * 32 + lane;
     if (uni[s]) {
-      const bool have = (m >> lane) & 1ull;
-      *o = have ? a[__popcll(m & ((1ull << lane) - 1ull)) * 32] : 0.0;
+      // one group: entries 0..be-1 the majority lane's dense block (zeros where
+      // the mask has no entry); kind 2 adds the dense blocks of its exception
+      // lanes at entries 10.. and 20.. (the lanes are named in the descriptor)
+      const unsigned info = uni[s] == 2 ? uinfo[s] : 0u;
+      const int src = lane < 10 ? (int)(info & 0xFF) : lane < 20 ? (int)((info >> 8) & 0xFF) : (int)((info >> 16) & 0xFF);
+      const int q = lane < 10 ? lane : lane < 20 ? lane - 10 : lane - 20;
+      double x = 0.0;
+      if (q < be && src != 0xFF && (uni[s] == 2 || lane < 10) && ((m >> q) & 1ull))
+        x = a[__popcll(m & ((1ull << q) - 1ull)) * 32 + src];
+      *o = x;
     } else {
 #if CAMG_DEDUP_NUDENSE
       // every position of the block gets a group (zeros where the mask has
@@ -371,12 +397,15 @@ __global__ void k_slot_compact(const unsigned long long* __restrict__ mask, cons
 }
 
 __global__ void k_slot_share(const uint32_t* __restrict__ rep, const int64_t* __restrict__ noff,
-                             const uint8_t* __restrict__ uni, int64_t slots, uint32_t* __restrict__ vo,
-                             unsigned long long* __restrict__ desc) {
+                             const uint8_t* __restrict__ uni, const uint32_t* __restrict__ uinfo, int64_t slots,
+                             uint32_t* __restrict__ vo, unsigned long long* __restrict__ desc) {
   for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < slots; s += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t r = rep[s];
     vo[s] = (uint32_t)noff[r];
-    desc[s] = (desc[s] & ~(0xFull << 60)) | ((unsigned long long)uni[r] << 60);
+    unsigned long long d = (desc[s] & ~(0xFull << 60)) | ((unsigned long long)uni[r] << 60);  // bits 60-61: slot kind
+    // dense slots need no pattern nibbles; kind 2 keeps its exception lanes there (bits 0-7, 8-15)
+    if (uni[r] == 2) d = (d & ~0xFFFFFFFFFull) | (unsigned long long)(uinfo[r] >> 8);
+    desc[s] = d;
   }
 }
 
@@ -389,10 +418,11 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   DBuf<unsigned long long> key(slots), key2(slots);
   DBuf<uint32_t> idx(slots), sidx(slots), rep(slots);
   DBuf<uint8_t> uni(slots);
+  DBuf<uint32_t> uinfo(slots);
   CAMG_CUDA(cudaMemsetAsync(uni.p, 0, slots, s));
   note_launch();
   k_slot_hash<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, slots, key.p, idx.p,
-                                                        S->br * S->bc <= 32 ? uni.p : nullptr);
+                                                        S->br * S->bc <= 9 ? uni.p : nullptr, uinfo.p);
   size_t tmp = 0;
   CAMG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key.p, key2.p, idx.p, sidx.p, slots, 0, 64, s));
   {
@@ -424,10 +454,10 @@ static void share_value_groups(Sell* S, cudaStream_t s) {
   DBuf<double> nval((size_t)std::max<int64_t>(kept, 1) * 32);
   note_launch();
   k_slot_compact<<<grid_for(slots * 32, 256), 256, 0, s>>>(S->mask, S->voff, S->bval, rep.p, noff.p, slots,
-                                                           S->br * S->bc, nval.p, uni.p);
+                                                           S->br * S->bc, nval.p, uni.p, uinfo.p);
   S->vo = dalloc<uint32_t>(slots + 1);
   note_launch();
-  k_slot_share<<<grid_for(slots, 256), 256, 0, s>>>(rep.p, noff.p, uni.p, slots, S->vo, S->desc);
+  k_slot_share<<<grid_for(slots, 256), 256, 0, s>>>(rep.p, noff.p, uni.p, uinfo.p, slots, S->vo, S->desc);
   CAMG_LAUNCH_CHECK();
   CAMG_CUDA(cudaStreamSynchronize(s));
   dfree(S->bval);
@@ -664,10 +694,11 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
         };
         if constexpr (DEDUP) {
           // shared value groups: every slot names the first group of its
-          // copy, stored dense -- one group per block position (zeros where
-          // the slot's mask has none), or, for a lane-uniform slot (bit 60),
-          // ONE group holding the BR x BC block, loaded as broadcasts.  An
-          // absent position enters as fma(0, x, acc), as in the other layouts.
+          // copy: its union-pattern groups, or, for a slot whose lanes all hold
+          // the same block (bits 60-61 = 1) or all but one or two of them
+          // (= 2: slices that straddle a mesh row), ONE group with the dense
+          // BR x BC block(s), loaded as broadcasts.  An absent position enters
+          // as fma(0, x, acc), as in the other layouts.
           const uint32_t o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
           const uint32_t o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
           // x of slot k (a linear slot has a block in every lane: k < n for all 32)
@@ -691,8 +722,14 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
             CAMG_DCHECK(S.ngroups == 0 || (int64_t)o < S.ngroups,
                         "sell value group out of range");
             double val[BE];
-            if ((m >> 60) & 1u) {
+            const unsigned kind = (unsigned)(m >> 60) & 3u;
+            if (kind) {
+              // kind 1: one dense block for all lanes (broadcast loads); kind 2:
+              // the same with one or two exception lanes, whose blocks follow
+              // in the group (entry 9 names the lanes)
               const double* vu = S.bval + (int64_t)o * 32;
+              if (kind == 2)  // exception lanes: descriptor bits 0-7 and 8-15 (0xFF: none)
+                vu += lane == (int)(m & 0xFF) ? 10 : (lane == (int)((m >> 8) & 0xFF) ? 20 : 0);
               if constexpr (BE == 9) {
                 const double2* v2 = reinterpret_cast<const double2*>(vu);
                 const double2 a = __ldg(v2), b = __ldg(v2 + 1), c = __ldg(v2 + 2), d = __ldg(v2 + 3);
@@ -1048,32 +1085,36 @@ extern "C" int camg_csr_attach_rect_blocks(camg_csr* A, int br, int bc, int64_t 
 }
 
 __global__ void k_slot_stats(const unsigned long long* __restrict__ desc, int64_t slots, unsigned long long* __restrict__ out) {
-  unsigned long long u = 0, l = 0, ul = 0;
+  unsigned long long u = 0, l = 0, ul = 0, x = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < slots; i += (int64_t)gridDim.x * blockDim.x) {
     const unsigned long long d = desc[i];
-    const bool un = (d >> 60) & 1u, li = ((d >> 36) & 0xFFFFFFull) != 0;
-    u += un; l += li; ul += un && li;
+    const unsigned kind = (unsigned)(d >> 60) & 3u;
+    const bool li = ((d >> 36) & 0xFFFFFFull) != 0;
+    u += kind == 1; l += li; ul += kind == 1 && li; x += kind == 2;
   }
   for (int o = 16; o > 0; o >>= 1) {
     u += __shfl_xor_sync(0xffffffffu, u, o);
     l += __shfl_xor_sync(0xffffffffu, l, o);
     ul += __shfl_xor_sync(0xffffffffu, ul, o);
+    x += __shfl_xor_sync(0xffffffffu, x, o);
   }
-  if ((threadIdx.x & 31) == 0) { atomicAdd(out, u); atomicAdd(out + 1, l); atomicAdd(out + 2, ul); }
+  if ((threadIdx.x & 31) == 0) { atomicAdd(out, u); atomicAdd(out + 1, l); atomicAdd(out + 2, ul); atomicAdd(out + 3, x); }
 }
 
-// slots of a shared-value mirror: out = {slots, lane-uniform, linear, both}
+// slots of a masked mirror: out[5] = {slots, lane-uniform, linear, both, uniform with one or two exception lanes}
 extern "C" int camg_csr_slot_stats(const camg_csr* A, int64_t* out) {
   return guarded([&] {
     const Sell* S = A->m->sell;
-    out[0] = out[1] = out[2] = out[3] = 0;
+    for (int i = 0; i < 5; ++i) out[i] = 0;
     if (!S || !S->desc) return;
-    DBuf<unsigned long long> acc(3);
-    CAMG_CUDA(cudaMemset(acc.p, 0, 3 * sizeof(unsigned long long)));
+    DBuf<unsigned long long> acc(4);
+    CAMG_CUDA(cudaMemset(acc.p, 0, 4 * sizeof(unsigned long long)));
     k_slot_stats<<<grid_for(S->slots, 256), 256>>>(S->desc, S->slots, acc.p);
-    unsigned long long h[3];
+    unsigned long long h[4];
     CAMG_CUDA(cudaMemcpy(h, acc.p, sizeof(h), cudaMemcpyDeviceToHost));
-    out[0] = S->slots; out[1] = S->dedup ? (int64_t)h[0] : 0; out[2] = (int64_t)h[1]; out[3] = S->dedup ? (int64_t)h[2] : 0;
+    out[0] = S->slots;
+    out[2] = (int64_t)h[1];
+    if (S->dedup) { out[1] = (int64_t)h[0]; out[3] = (int64_t)h[2]; out[4] = (int64_t)h[3]; }
   });
 }
 
