@@ -107,6 +107,7 @@ _SIGS = {
     "camg_csr_stream_bytes": (C.c_int, [vp, C.POINTER(f64)]),
     "camg_csr_value_groups": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)]),
     "camg_csr_slot_stats": (C.c_int, [vp, vp]),
+    "camg_csr_uniform_slices": (C.c_int, [vp, vp]),
     "camg_level_block_transfer": (C.c_int, [vp, C.c_int, C.c_int, i64]),
     "camg_level_fine_pass": (C.c_int, [vp, C.c_int, vp, vp, vp, C.POINTER(f64), C.POINTER(f64)]),
     "camg_level_schur": (C.c_int, [vp, C.POINTER(vp)]),

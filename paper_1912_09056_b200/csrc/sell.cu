@@ -74,6 +74,7 @@ Sell::~Sell() {
   dfree(desc);
   dfree(zero);
   dfree(vo);
+  dfree(uslice);
   dfree(perm);
   dfree(dblk);
 }
@@ -409,6 +410,26 @@ __global__ void k_slot_share(const uint32_t* __restrict__ rep, const int64_t* __
   }
 }
 
+// uniform slices: a full slice (32 block rows, at most 32 slots) whose slots are all linear and
+// lane-uniform (kind 1) and read block columns below `sq` (the square part: never the split vector)
+__global__ void k_uniform_slices(const int64_t* __restrict__ slice_ptr, const uint8_t* __restrict__ len,
+                                 const unsigned long long* __restrict__ desc, int64_t nbr, int64_t nslices,
+                                 int64_t sq, uint8_t* __restrict__ us, unsigned long long* __restrict__ count) {
+  for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nslices;
+       sl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t base = slice_ptr[sl], width = slice_ptr[sl + 1] - base;
+    bool ok = width > 0 && width <= 32 && sl * 32 + 31 < nbr;
+    for (int l = 0; ok && l < 32; ++l) ok = len[sl * 32 + l] == width;
+    for (int64_t k = 0; ok && k < width; ++k) {
+      const unsigned long long d = desc[base + k];
+      const int64_t lin = (int64_t)((d >> 36) & 0xFFFFFFull);
+      ok = ((d >> 60) & 3ull) == 1ull && lin > 0 && lin - 1 + 31 < sq;
+    }
+    us[sl] = ok ? 1 : 0;
+    if (ok) atomicAdd(count, 1ull);
+  }
+}
+
 // Replace S's value array by the shared one when that at least halves it;
 // returns the value groups kept (S->ngroups) -- S->dedup says whether it applied.
 static void share_value_groups(Sell* S, cudaStream_t s) {
@@ -471,6 +492,12 @@ static int g_share_override = -1;  // sell_share_override: -1 = CAMG_SELL_DEDUP 
 static bool dedup_enabled() {
   if (g_share_override >= 0) return g_share_override != 0;
   const char* e = getenv("CAMG_SELL_DEDUP");
+  return !(e && e[0] == '0');
+}
+
+// CAMG_SELL_USLICE=0: no uniform-slice loop (every slice decodes its slot descriptors)
+static bool uslices_enabled() {
+  const char* e = getenv("CAMG_SELL_USLICE");
   return !(e && e[0] == '0');
 }
 
@@ -551,6 +578,21 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
     CAMG_LAUNCH_CHECK();
   }
   if (masked && dedup_enabled()) share_value_groups(S.get(), s);
+  if (S->dedup && BR == 3 && BC == 3 && !order && uslices_enabled()) {
+    S->uslice = dalloc<uint8_t>(nslices + 1);
+    DBuf<unsigned long long> nu_(1);
+    CAMG_CUDA(cudaMemsetAsync(nu_.p, 0, sizeof(unsigned long long), s));
+    note_launch();
+    k_uniform_slices<<<grid_for(nslices, 256), 256, 0, s>>>(S->slice_ptr, S->len, S->desc, nbr, nslices,
+                                                            std::min<int64_t>(nbr, ncols_blocked / BC), S->uslice,
+                                                            nu_.p);
+    CAMG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    CAMG_CUDA(cudaMemcpyAsync(&h, nu_.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    S->n_uslices = (int64_t)h;
+    if (h == 0) { dfree(S->uslice); S->uslice = nullptr; }
+  }
   // compulsory bytes of one pass: for every row, its blocks' stored values and
   // column (the padding of shorter rows is skipped; linear slots load no
   // column), summed on the device
@@ -700,6 +742,27 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
           // BR x BC block(s), loaded as broadcasts.  An absent position enters
           // as fma(0, x, acc), as in the other layouts.
           const uint32_t o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
+          if constexpr (BE == 9) {
+            // uniform slice: all slots linear and lane-uniform, columns in xu: no decoding, no branches
+            if (S.uslice && S.uslice[s]) {
+              const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;  // slot `lane`: first column
+#pragma unroll 1
+              for (int k = 0; k < width; ++k) {
+                const int32_t c = __shfl_sync(0xffffffffu, c0, k);
+                const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
+                const double* xs = xu + (int64_t)(c + lane) * 3;
+                const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
+                const double x0 = __ldg(xs), x1 = __ldg(xs + 1), x2 = __ldg(xs + 2);
+                const double2 a = __ldg(v2), b = __ldg(v2 + 1), cc = __ldg(v2 + 2), d = __ldg(v2 + 3);
+                const double v8 = __ldg(reinterpret_cast<const double*>(v2) + 8);
+                acc[0] = fma(a.x, x0, acc[0]); acc[0] = fma(a.y, x1, acc[0]); acc[0] = fma(b.x, x2, acc[0]);
+                acc[1] = fma(b.y, x0, acc[1]); acc[1] = fma(cc.x, x1, acc[1]); acc[1] = fma(cc.y, x2, acc[1]);
+                acc[2] = fma(d.x, x0, acc[2]); acc[2] = fma(d.y, x1, acc[2]); acc[2] = fma(v8, x2, acc[2]);
+              }
+              sell_epilogue<BR, ZERO, MODE>(e, p, acc);
+              continue;
+            }
+          }
           const uint32_t o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
           // x of slot k (a linear slot has a block in every lane: k < n for all 32)
           auto fetch_x = [&](int k, uint64_t mk, double* xo) {
@@ -888,6 +951,8 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   v.ncb = S->ncb;
   v.ngroups = S->masked ? S->ngroups : 0;
   v.vo = S->vo;
+  // uniform slices read xu only: their columns lie below nbr, so any split at or above it is safe
+  v.uslice = (split < 0 || split / BC >= S->nbr) ? S->uslice : nullptr;
   v.slist = slist;
   v.nwork = slist ? nlist : S->nslices;
   if (v.nwork <= 0) return;
@@ -1115,6 +1180,15 @@ extern "C" int camg_csr_slot_stats(const camg_csr* A, int64_t* out) {
     out[0] = S->slots;
     out[2] = (int64_t)h[1];
     if (S->dedup) { out[1] = (int64_t)h[0]; out[3] = (int64_t)h[2]; out[4] = (int64_t)h[3]; }
+  });
+}
+
+// slices of the block mirror and how many of them run the uniform-slice loop
+extern "C" int camg_csr_uniform_slices(const camg_csr* A, int64_t* out) {
+  return guarded([&] {
+    const Sell* S = A->m->sell;
+    out[0] = S ? S->nslices : 0;
+    out[1] = S ? S->n_uslices : 0;
   });
 }
 

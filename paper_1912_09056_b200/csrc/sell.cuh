@@ -28,6 +28,11 @@ struct Sell {
   bool dedup = false;
   uint32_t* vo = nullptr;
   int64_t ngroups_full = 0;           // value groups before sharing
+  // uniform slices (shared value groups, 3x3): every slot of the slice is linear and lane-uniform (a slice
+  // inside one mesh row of the structured interior) and reads columns of the square part only: the pass runs
+  // them through a loop without descriptor decoding (uslice[slice] = 1)
+  uint8_t* uslice = nullptr;
+  int64_t n_uslices = 0;
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
   double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]
   ~Sell();
@@ -48,6 +53,7 @@ struct SellView {
   int64_t nwork = 0;                            // slices to process (slist length, or nslices)
   int64_t ncb = 0, ngroups = 0;                 // bounds for the checked build (0: unknown)
   const uint32_t* __restrict__ vo = nullptr;    // shared value groups: first group of each slot
+  const uint8_t* __restrict__ uslice = nullptr; // uniform slices (null: none / columns may cross the split)
 };
 
 // epilogue arguments of the three SELL row kernels (modes 0/1/2)
