@@ -430,6 +430,30 @@ __global__ void k_uniform_slices(const int64_t* __restrict__ slice_ptr, const ui
   }
 }
 
+// pairs of uniform slices: slices s (even) and s + 1 with the same shared value groups slot by slot and
+// columns 32 apart (neighbours inside one mesh row) run as one work item, each lane carrying two block
+// rows, so the lane-uniform values -- 72 of the 96 bytes a lane receives per slot, the L1 data pipe's
+// load -- are loaded once for both: us[s] = 3 (leader), us[s + 1] = 4 (follower)
+__global__ void k_uniform_pairs(const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ desc,
+                                const uint32_t* __restrict__ vo, int64_t nslices, uint8_t* __restrict__ us,
+                                unsigned long long* __restrict__ count) {
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * h + 1 < nslices;
+       h += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = 2 * h;
+    if (us[s] != 1 || us[s + 1] != 1) continue;
+    const int64_t b0 = slice_ptr[s], b1 = slice_ptr[s + 1], width = b1 - b0;
+    bool ok = slice_ptr[s + 2] - b1 == width;
+    for (int64_t k = 0; ok && k < width; ++k)
+      ok = vo[b0 + k] == vo[b1 + k] &&
+           ((desc[b1 + k] >> 36) & 0xFFFFFFull) == ((desc[b0 + k] >> 36) & 0xFFFFFFull) + 32ull;
+    if (ok) {
+      us[s] = 3;
+      us[s + 1] = 4;
+      atomicAdd(count, 1ull);
+    }
+  }
+}
+
 // Replace S's value array by the shared one when that at least halves it;
 // returns the value groups kept (S->ngroups) -- S->dedup says whether it applied.
 static void share_value_groups(Sell* S, cudaStream_t s) {
@@ -496,10 +520,13 @@ static bool dedup_enabled() {
 }
 
 // CAMG_SELL_USLICE=0: no uniform-slice loop (every slice decodes its slot descriptors)
-static bool uslices_enabled() {
+// 1: uniform-slice loop, one block row per lane; 2 (default): neighbouring uniform slices in pairs, two
+// block rows per lane
+static int uslice_mode() {
   const char* e = getenv("CAMG_SELL_USLICE");
-  return !(e && e[0] == '0');
+  return e ? atoi(e) : 2;
 }
+static bool uslices_enabled() { return uslice_mode() != 0; }
 
 template <int BR, int BC>
 Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cudaStream_t s,
@@ -592,6 +619,16 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
     CAMG_CUDA(cudaStreamSynchronize(s));
     S->n_uslices = (int64_t)h;
     if (h == 0) { dfree(S->uslice); S->uslice = nullptr; }
+    if (h > 0 && uslice_mode() >= 2) {
+      CAMG_CUDA(cudaMemsetAsync(nu_.p, 0, sizeof(unsigned long long), s));
+      note_launch();
+      k_uniform_pairs<<<grid_for(nslices / 2 + 1, 256), 256, 0, s>>>(S->slice_ptr, S->desc, S->vo, nslices, S->uslice,
+                                                                     nu_.p);
+      CAMG_LAUNCH_CHECK();
+      CAMG_CUDA(cudaMemcpyAsync(&h, nu_.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+      CAMG_CUDA(cudaStreamSynchronize(s));
+      S->n_upairs = (int64_t)h;
+    }
   }
   // compulsory bytes of one pass: for every row, its blocks' stored values and
   // column (the padding of shorter rows is skipped; linear slots load no
@@ -683,6 +720,37 @@ __device__ __forceinline__ void sell_epilogue(const SellEpi& e, int64_t p, const
   }
 }
 
+// uniform-slice loops: the epilogue's own-row vectors (b, D^-1, x: compulsory DRAM reads) are prefetched to
+// L2 before the slot loop, so the slice does not end on a serial DRAM round trip
+#ifndef CAMG_US_PREFETCH
+#define CAMG_US_PREFETCH 1
+#endif
+#ifndef CAMG_US_UNROLL
+#define CAMG_US_UNROLL 1
+#endif
+constexpr int kUsUnroll = CAMG_US_UNROLL;
+#if CAMG_PF_L1
+#define CAMG_BCOL_PF "prefetch.global.L1"
+#else
+#define CAMG_BCOL_PF "prefetch.global.L2"
+#endif
+template <int BR, int MODE>
+__device__ __forceinline__ void sell_epilogue_prefetch(const SellEpi& e, int64_t p) {
+#if CAMG_US_PREFETCH
+  const int64_t i = p * BR;
+  auto pf = [&](const double* a) {
+    if (a) asm volatile("prefetch.global.L2 [%0];" ::"l"(a + i));
+  };
+  if constexpr (MODE == 0) {
+    if (e.beta != 0.0) pf(e.y);
+  } else if constexpr (MODE == 1) {
+    pf(e.b); pf(e.dscale); pf(e.x); pf(e.dprev);
+  } else {
+    pf(e.d); pf(e.dscale); pf(e.r); pf(e.x);
+  }
+#endif
+}
+
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED, bool DEDUP = false>
 __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MINB : CAMG_MASKED_MINB) : (BR * BC >= 18 ? CAMG_BIG_MINB : 6)) * 256 / kSellThreads) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
@@ -744,9 +812,46 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
           const uint32_t o0 = lane < width ? __ldg(S.vo + base + lane) : 0u;
           if constexpr (BE == 9) {
             // uniform slice: all slots linear and lane-uniform, columns in xu: no decoding, no branches
-            if (S.uslice && S.uslice[s]) {
-              const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;  // slot `lane`: first column
+            const int us = S.uslice ? S.uslice[s] : 0;
+            if (us >= 3) {
+              // pair of uniform slices (s, s + 1), both in this launch's list: the leader's warp carries both
+              const bool leader = us == 3;
+              const bool both = !S.slist || (leader ? (w + 1 < S.nwork && S.slist[w + 1] == (int32_t)(s + 1))
+                                                    : (w > 0 && S.slist[w - 1] == (int32_t)(s - 1)));
+              if (both && !leader) continue;
+              if (both) {
+                double acb[BR];
+#pragma unroll
+                for (int r = 0; r < BR; ++r) acb[r] = 0.0;
+                const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;
+                sell_epilogue_prefetch<BR, MODE>(e, p);
+                sell_epilogue_prefetch<BR, MODE>(e, p + 32);
 #pragma unroll 1
+                for (int k = 0; k < width; ++k) {
+                  const int32_t c = __shfl_sync(0xffffffffu, c0, k);
+                  const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
+                  const double* xs = xu + (int64_t)(c + lane) * 3;
+                  const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
+                  const double x0 = __ldg(xs), x1 = __ldg(xs + 1), x2 = __ldg(xs + 2);
+                  const double z0 = __ldg(xs + 96), z1 = __ldg(xs + 97), z2 = __ldg(xs + 98);
+                  const double2 a = __ldg(v2), b = __ldg(v2 + 1), cc = __ldg(v2 + 2), d = __ldg(v2 + 3);
+                  const double v8 = __ldg(reinterpret_cast<const double*>(v2) + 8);
+                  acc[0] = fma(a.x, x0, acc[0]); acc[0] = fma(a.y, x1, acc[0]); acc[0] = fma(b.x, x2, acc[0]);
+                  acc[1] = fma(b.y, x0, acc[1]); acc[1] = fma(cc.x, x1, acc[1]); acc[1] = fma(cc.y, x2, acc[1]);
+                  acc[2] = fma(d.x, x0, acc[2]); acc[2] = fma(d.y, x1, acc[2]); acc[2] = fma(v8, x2, acc[2]);
+                  acb[0] = fma(a.x, z0, acb[0]); acb[0] = fma(a.y, z1, acb[0]); acb[0] = fma(b.x, z2, acb[0]);
+                  acb[1] = fma(b.y, z0, acb[1]); acb[1] = fma(cc.x, z1, acb[1]); acb[1] = fma(cc.y, z2, acb[1]);
+                  acb[2] = fma(d.x, z0, acb[2]); acb[2] = fma(d.y, z1, acb[2]); acb[2] = fma(v8, z2, acb[2]);
+                }
+                sell_epilogue<BR, ZERO, MODE>(e, p, acc);
+                sell_epilogue<BR, ZERO, MODE>(e, p + 32, acb);
+                continue;
+              }
+            }
+            if (us) {
+              const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;  // slot `lane`: first column
+              sell_epilogue_prefetch<BR, MODE>(e, p);
+#pragma unroll kUsUnroll
               for (int k = 0; k < width; ++k) {
                 const int32_t c = __shfl_sync(0xffffffffu, c0, k);
                 const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
@@ -764,6 +869,16 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
             }
           }
           const uint32_t o1 = lane + 32 < width ? __ldg(S.vo + base + 32 + lane) : 0u;
+#if CAMG_US_PREFETCH
+          // other slices (mesh-row ends, boundaries, interface rows): the column indices of the non-linear
+          // slots -- one 128-byte line per slot, a compulsory DRAM read ahead of every x gather -- and the
+          // epilogue's vectors are prefetched now, all at once, instead of one DRAM round trip per slot
+          if (lane < width && !((uint32_t)(m0 >> 36) & 0xFFFFFFu))
+            asm volatile(CAMG_BCOL_PF " [%0];" ::"l"(S.bcol + (base + lane) * 32));
+          if (lane + 32 < width && !((uint32_t)(m1 >> 36) & 0xFFFFFFu))
+            asm volatile(CAMG_BCOL_PF " [%0];" ::"l"(S.bcol + (base + 32 + lane) * 32));
+          if (active) sell_epilogue_prefetch<BR, MODE>(e, p);
+#endif
           // x of slot k (a linear slot has a block in every lane: k < n for all 32)
           auto fetch_x = [&](int k, uint64_t mk, double* xo) {
             const uint32_t lin = (uint32_t)(mk >> 36) & 0xFFFFFFu;
@@ -1189,6 +1304,7 @@ extern "C" int camg_csr_uniform_slices(const camg_csr* A, int64_t* out) {
     const Sell* S = A->m->sell;
     out[0] = S ? S->nslices : 0;
     out[1] = S ? S->n_uslices : 0;
+    out[2] = S ? S->n_upairs : 0;
   });
 }
 

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 python -m pytest tests/test_gpu_parity.py -q -x -k "uniform_slice or shared_value or masked_sell" > gpurun_out/uslice_tests.log 2>&1
 echo "tests rc=$?"; tail -3 gpurun_out/uslice_tests.log
-for m in 0 1; do
+for m in 1 2; do
   CAMG_SELL_USLICE=$m python bench.py --no-cpu-baseline --rhs-seeds "" > gpurun_out/uslice_bench_$m.log 2>&1
   echo "bench $m rc=$?"
   tail -1 gpurun_out/uslice_bench_$m.log | python -c "

@@ -392,7 +392,8 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
     inside one mesh row) run a loop without descriptor decoding: it engages on
     most slices of the configs' fine operators, and the merged SpMV and the
     fused Jacobi predictor pass are bit-identical with the loop off
-    (CAMG_SELL_USLICE=0)."""
+    (CAMG_SELL_USLICE=0), one block row per lane (=1) and neighbouring uniform
+    slices in pairs (=2, the default)."""
     import ctypes as C
     import torch
     from paper_1912_09056_b200.sparse import empty, ptr, stream_ptr
@@ -402,12 +403,12 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
     n = A.num_rows
     x = torch.from_numpy(np.random.default_rng(12).standard_normal(n)).cuda()
     out, counts = {}, {}
-    for m in ("0", "1"):
+    for m in ("0", "1", "2"):
         monkeypatch.setenv("CAMG_SELL_USLICE", m)
         _native.call("camg_csr_attach_blocks", A.device, 3, op.n_u)
-        c = (C.c_int64 * 2)()
+        c = (C.c_int64 * 3)()
         _native.call("camg_csr_uniform_slices", A.device, c)
-        counts[m] = (c[0], c[1])
+        counts[m] = (c[0], c[1], c[2])
         y = empty(n)
         _native.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
         torch.cuda.synchronize()
@@ -415,20 +416,24 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
     assert counts["0"][1] == 0 and counts["1"][0] == counts["0"][0]
     # mesh rows of 65 / 67 nodes hold one or two whole 32-node slices each (C5 at full size: 84% of the slices)
     assert cfg == "C4" or counts["1"][1] * 5 > counts["1"][0], counts
+    assert counts["1"][2] == 0 and counts["2"][1] == counts["1"][1]
+    assert cfg != "C5" or counts["2"][2] > 0, counts
     np.testing.assert_array_equal(out["0"], out["1"])
+    np.testing.assert_array_equal(out["0"], out["2"])
     ref = A.to_scipy() @ x.cpu().numpy()
     assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
     # the smoother passes ([K | B1] rows with the lambda split) through a whole sweep
     skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcilu0", 1, 1.0))
     x0 = np.random.default_rng(0).standard_normal(op.total_rows)
     sw = {}
-    for m in ("0", "1"):
+    for m in ("0", "1", "2"):
         monkeypatch.setenv("CAMG_SELL_USLICE", m)
         H = setup(saddle_operator(g), fine_level_meta(g), HierarchyConfig(max_levels=3, max_coarse_size=50),
                   block_cfg(skw))
         sw[m] = (H.levels[0].smoother.sweep_merged(x0, g.rhs).cpu().numpy(), np.asarray(H.apply(g.rhs)))
-    np.testing.assert_array_equal(sw["0"][0], sw["1"][0])
-    np.testing.assert_array_equal(sw["0"][1], sw["1"][1])
+    for m in ("1", "2"):
+        np.testing.assert_array_equal(sw["0"][0], sw[m][0])
+        np.testing.assert_array_equal(sw["0"][1], sw[m][1])
 
 
 @pytest.mark.parametrize("cfg,scale,sweeps,cluster", [("C5", 10, 1, "1"), ("C5", 10, 1, "0"), ("C4", 8, 2, "1"),
