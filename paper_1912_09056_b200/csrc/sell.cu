@@ -141,14 +141,96 @@ __global__ void k_slice_width(const uint8_t* __restrict__ len, int64_t nbr, int6
   }
 }
 
+// Offset-aligned slots (masked mirrors).  Slot k of a slice normally holds every lane's k-th block; where the
+// block rows of a slice share one set of block-column offsets (column - row: the stencil of a structured
+// mesh), slot j holds instead, in every lane, the block at the j-th offset of that set -- an explicit zero
+// block (same fma(0, x, acc) as an absent position of a masked block) where a lane has none (a boundary
+// node).  Slices that straddle a mesh row or touch a boundary then have the interior's linear, lane-uniform
+// slots (kind 1 / 2) instead of per-lane columns and values.  A slice is aligned when the union of its
+// lanes' offsets has at most kOffCap entries and pads its longest row by at most an eighth (an
+// unstructured matrix never qualifies and keeps the rank order).  The order of a lane's own blocks is
+// unchanged (ascending columns), so every result is.
+constexpr int kOffCap = 32;
+
+template <int BR, int BC>
+__global__ void k_slice_offsets(CsrView A, int64_t nbr, int64_t nslices, const uint8_t* __restrict__ len,
+                                int32_t* __restrict__ otab, uint8_t* __restrict__ wal) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t sl = warp; sl < nslices; sl += nwarps) {
+    const int64_t p = sl * 32 + lane;
+    const bool active = p < nbr;
+    int64_t pos[BR], end[BR];
+#pragma unroll
+    for (int r = 0; r < BR; ++r) {
+      pos[r] = active ? A.rowptr[p * BR + r] : 0;
+      end[r] = active ? A.rowptr[p * BR + r + 1] : 0;
+    }
+    int maxlen = active ? (int)len[p] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    int cnt = 0;
+    bool ok = true;
+    while (true) {
+      int32_t head = INT32_MAX;
+#pragma unroll
+      for (int r = 0; r < BR; ++r)
+        if (pos[r] < end[r]) head = min(head, A.col[pos[r]] / BC);
+      const int32_t off = head == INT32_MAX ? INT32_MAX : (int32_t)((int64_t)head - p);
+      int32_t m = off;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (m == INT32_MAX) break;
+      if (cnt == kOffCap) { ok = false; break; }
+      if (lane == 0) otab[sl * kOffCap + cnt] = m;
+      ++cnt;
+      if (off == m) {
+#pragma unroll
+        for (int r = 0; r < BR; ++r)
+          while (pos[r] < end[r] && A.col[pos[r]] / BC == head) ++pos[r];
+      }
+    }
+    if (lane == 0) wal[sl] = (ok && cnt > 0 && cnt <= maxlen + max(1, maxlen / 8)) ? (uint8_t)cnt : 0;
+  }
+}
+
+// widths and row lengths of the aligned slices: every lane holds a block (possibly zero) in every slot
+__global__ void k_apply_aligned(const uint8_t* __restrict__ wal, int64_t nbr, int64_t nslices, int64_t* __restrict__ w,
+                                uint8_t* __restrict__ len) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nslices * 32;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int a = wal[p >> 5];
+    if (!a) continue;
+    if ((p & 31) == 0) w[p >> 5] = a;
+    if (p < nbr) len[p] = (uint8_t)a;
+  }
+}
+
+// slot of block column bc in block row p: its rank k, or the position of its offset in an aligned slice
+__device__ __forceinline__ int slot_of(const int32_t* __restrict__ otab, const uint8_t* __restrict__ wal, int64_t p,
+                                       int k, int32_t bc) {
+  const int n = wal ? (int)wal[p >> 5] : 0;
+  if (!n) return k;
+  const int32_t* t = otab + (p >> 5) * kOffCap;
+  const int32_t off = (int32_t)((int64_t)bc - p);
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (t[mid] < off) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
 // union mask of every slot (masked mode) or all-ones (full blocks)
 template <int BR, int BC>
 __global__ void k_sell_masks(CsrView A, int64_t nbr, const int64_t* __restrict__ slice_ptr,
+                             const int32_t* __restrict__ otab, const uint8_t* __restrict__ wal,
                              unsigned long long* __restrict__ mask) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nbr; p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t base = slice_ptr[p >> 5];
-    for_blocks<BR, BC>(A, p, [&](int k, int32_t, int r, int, double m) {
-      if (r < 0) atomicOr(mask + base + k, (unsigned long long)m);
+    for_blocks<BR, BC>(A, p, [&](int k, int32_t bc, int r, int, double m) {
+      if (r < 0) atomicOr(mask + base + slot_of(otab, wal, p, k, bc), (unsigned long long)m);
     });
   }
 }
@@ -201,15 +283,23 @@ template <int BR, int BC>
 __global__ void k_sell_fill(CsrView A, int64_t nbr, const int32_t* __restrict__ perm,
                             const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ mask,
                             const int64_t* __restrict__ voff, int32_t* __restrict__ bcol, double* __restrict__ bval,
-                            double* __restrict__ dblk) {
+                            double* __restrict__ dblk, const int32_t* __restrict__ otab,
+                            const uint8_t* __restrict__ wal, int64_t ncb_sq) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nbr; t += (int64_t)gridDim.x * blockDim.x) {
     const int lane = (int)(t & 31);
     const int64_t base = slice_ptr[t >> 5];
     const int64_t width = slice_ptr[(t >> 5) + 1] - base;
     const int64_t p = perm ? perm[t] : t;
+    const int al = (wal && !perm) ? (int)wal[t >> 5] : 0;
+    // aligned slice: a slot this lane has no block in reads the column at its offset (its own where that
+    // falls outside the square part) against a zero block
+    for (int j = 0; j < al; ++j) {
+      const int64_t c = p + otab[(t >> 5) * kOffCap + j];
+      bcol[(base + j) * 32 + lane] = (int32_t)((c >= 0 && c < ncb_sq) ? c : (p < ncb_sq ? p : 0));
+    }
     int n = 0;
     if (p >= 0) n = for_blocks<BR, BC>(A, p, [&](int k, int32_t bc, int r, int c, double v) {
-      const int64_t slot = base + k;
+      const int64_t slot = base + (al ? slot_of(otab, wal, p, k, bc) : k);
       if (r < 0) {
         bcol[slot * 32 + lane] = bc;
         return;
@@ -221,7 +311,8 @@ __global__ void k_sell_fill(CsrView A, int64_t nbr, const int32_t* __restrict__ 
       const int64_t idx = voff[slot] + __popcll(m & ((1ull << e) - 1ull));
       bval[idx * 32 + lane] = v;
     });
-    for (int k = n; k < width; ++k) bcol[(base + k) * 32 + lane] = 0;  // padding (never read)
+    if (!al)
+      for (int k = n; k < width; ++k) bcol[(base + k) * 32 + lane] = 0;  // padding (never read)
   }
 }
 
@@ -411,21 +502,24 @@ __global__ void k_slot_share(const uint32_t* __restrict__ rep, const int64_t* __
 }
 
 // uniform slices: a full slice (32 block rows, at most 32 slots) whose slots are all linear and
-// lane-uniform (kind 1) and read block columns below `sq` (the square part: never the split vector)
+// lane-uniform (kind 1, or kind 2: but for one or two lanes) and read block columns below `sq` (the square
+// part: never the split vector)
 __global__ void k_uniform_slices(const int64_t* __restrict__ slice_ptr, const uint8_t* __restrict__ len,
                                  const unsigned long long* __restrict__ desc, int64_t nbr, int64_t nslices,
                                  int64_t sq, uint8_t* __restrict__ us, unsigned long long* __restrict__ count) {
   for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nslices;
        sl += (int64_t)gridDim.x * blockDim.x) {
     const int64_t base = slice_ptr[sl], width = slice_ptr[sl + 1] - base;
-    bool ok = width > 0 && width <= 32 && sl * 32 + 31 < nbr;
+    bool ok = width > 0 && width <= 32 && sl * 32 + 31 < nbr, exc = false;
     for (int l = 0; ok && l < 32; ++l) ok = len[sl * 32 + l] == width;
     for (int64_t k = 0; ok && k < width; ++k) {
       const unsigned long long d = desc[base + k];
       const int64_t lin = (int64_t)((d >> 36) & 0xFFFFFFull);
-      ok = ((d >> 60) & 3ull) == 1ull && lin > 0 && lin - 1 + 31 < sq;
+      const unsigned kind = (unsigned)(d >> 60) & 3u;
+      ok = (kind == 1u || kind == 2u) && lin > 0 && lin - 1 + 31 < sq;
+      exc |= kind == 2u;
     }
-    us[sl] = ok ? 1 : 0;
+    us[sl] = ok ? (exc ? 2 : 1) : 0;  // 2: some slots have one or two exception lanes (kind 2)
     if (ok) atomicAdd(count, 1ull);
   }
 }
@@ -519,6 +613,12 @@ static bool dedup_enabled() {
   return !(e && e[0] == '0');
 }
 
+// CAMG_SELL_ALIGN=0: slots in rank order everywhere (no offset-aligned slices)
+static bool align_enabled() {
+  const char* e = getenv("CAMG_SELL_ALIGN");
+  return !(e && e[0] == '0');
+}
+
 // CAMG_SELL_USLICE=0: no uniform-slice loop (every slice decodes its slot descriptors)
 // 1: uniform-slice loop, one block row per lane; 2 (default): neighbouring uniform slices in pairs, two
 // block rows per lane
@@ -559,6 +659,23 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   DBuf<int64_t> w(nslices + 1);
   note_launch();
   k_slice_width<<<grid_for(nslices, 256), 256, 0, s>>>(S->len, nbr, nslices, w.p);
+  // offset-aligned slots where a slice's rows share their block-column offsets (masked 3x3 mirrors)
+  DBuf<int32_t> otab;
+  DBuf<uint8_t> wal;
+  const bool align = masked && BR * BC <= 9 && BR == BC && !order && align_enabled();
+  if (align) {
+    otab = DBuf<int32_t>((size_t)nslices * kOffCap + 1);
+    wal = DBuf<uint8_t>(nslices + 1);
+    note_launch();
+    k_slice_offsets<BR, BC><<<grid_for(nslices * 32, 256), 256, 0, s>>>(view(A), nbr, nslices, S->len, otab.p, wal.p);
+    note_launch();
+    k_apply_aligned<<<grid_for(nslices * 32, 256), 256, 0, s>>>(wal.p, nbr, nslices, w.p, S->len);
+    CAMG_LAUNCH_CHECK();
+    std::vector<uint8_t> h_wal(nslices);
+    CAMG_CUDA(cudaMemcpyAsync(h_wal.data(), wal.p, nslices, cudaMemcpyDeviceToHost, s));
+    CAMG_CUDA(cudaStreamSynchronize(s));
+    for (uint8_t a : h_wal) S->n_aligned += a != 0;
+  }
   S->slice_ptr = dalloc<int64_t>(nslices + 1);
   exclusive_scan_i64(w.p, S->slice_ptr, nslices, s);
   CAMG_CUDA(cudaStreamSynchronize(s));
@@ -571,7 +688,8 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   if (masked) {
     CAMG_CUDA(cudaMemsetAsync(S->mask, 0, sizeof(unsigned long long) * (slots + 1), s));
     note_launch();
-    k_sell_masks<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, S->mask);
+    k_sell_masks<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->slice_ptr, align ? otab.p : nullptr,
+                                                            align ? wal.p : nullptr, S->mask);
   } else {
     std::vector<unsigned long long> full(slots + 1, (BE == 64) ? ~0ull : ((1ull << BE) - 1ull));
     CAMG_CUDA(cudaMemcpy(S->mask, full.data(), sizeof(unsigned long long) * (slots + 1), cudaMemcpyHostToDevice));
@@ -597,7 +715,9 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
   CAMG_CUDA(cudaMemsetAsync(S->bval, 0, sizeof(double) * (size_t)groups * 32, s));
   note_launch();
   k_sell_fill<BR, BC><<<grid_for(nbr, 256), 256, 0, s>>>(view(A), nbr, S->perm, S->slice_ptr, S->mask, S->voff,
-                                                         S->bcol, S->bval, S->dblk);
+                                                         S->bcol, S->bval, S->dblk, align ? otab.p : nullptr,
+                                                         align ? wal.p : nullptr,
+                                                         std::min<int64_t>(nbr, ncols_blocked / BC));
   CAMG_LAUNCH_CHECK();
   if (masked) {
     note_launch();
@@ -847,6 +967,31 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
                 sell_epilogue<BR, ZERO, MODE>(e, p + 32, acb);
                 continue;
               }
+            }
+            if (us == 2) {
+              // uniform but for one or two lanes in some slots (a slice across the end of a mesh row: its two
+              // boundary nodes): those lanes read their own dense block at entries 10.. / 20.. of the group
+              const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;
+              const uint32_t ex = ((unsigned)(m0 >> 60) & 3u) == 2u ? (uint32_t)(m0 & 0xFFFFull) : 0xFFFFu;
+              sell_epilogue_prefetch<BR, MODE>(e, p);
+#pragma unroll 1
+              for (int k = 0; k < width; ++k) {
+                const int32_t c = __shfl_sync(0xffffffffu, c0, k);
+                const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
+                const uint32_t x = __shfl_sync(0xffffffffu, ex, k);
+                const double* xs = xu + (int64_t)(c + lane) * 3;
+                const int sh = lane == (int)(x & 0xFFu) ? 10 : (lane == (int)(x >> 8) ? 20 : 0);
+                const double* vu = S.bval + (int64_t)o * 32 + sh;
+                const double2* v2 = reinterpret_cast<const double2*>(vu);
+                const double x0 = __ldg(xs), x1 = __ldg(xs + 1), x2 = __ldg(xs + 2);
+                const double2 a = __ldg(v2), b = __ldg(v2 + 1), cc = __ldg(v2 + 2), d = __ldg(v2 + 3);
+                const double v8 = __ldg(vu + 8);
+                acc[0] = fma(a.x, x0, acc[0]); acc[0] = fma(a.y, x1, acc[0]); acc[0] = fma(b.x, x2, acc[0]);
+                acc[1] = fma(b.y, x0, acc[1]); acc[1] = fma(cc.x, x1, acc[1]); acc[1] = fma(cc.y, x2, acc[1]);
+                acc[2] = fma(d.x, x0, acc[2]); acc[2] = fma(d.y, x1, acc[2]); acc[2] = fma(v8, x2, acc[2]);
+              }
+              sell_epilogue<BR, ZERO, MODE>(e, p, acc);
+              continue;
             }
             if (us) {
               const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;  // slot `lane`: first column
@@ -1305,6 +1450,7 @@ extern "C" int camg_csr_uniform_slices(const camg_csr* A, int64_t* out) {
     out[0] = S ? S->nslices : 0;
     out[1] = S ? S->n_uslices : 0;
     out[2] = S ? S->n_upairs : 0;
+    out[3] = S ? S->n_aligned : 0;
   });
 }
 

@@ -32,6 +32,7 @@ struct Sell {
   // inside one mesh row of the structured interior) and reads columns of the square part only: the pass runs
   // them through a loop without descriptor decoding (uslice[slice] = 1)
   uint8_t* uslice = nullptr;
+  int64_t n_aligned = 0;  // slices with offset-aligned slots (sell.cu)
   int64_t n_uslices = 0, n_upairs = 0;  // n_upairs: pairs of neighbouring uniform slices run as one work item (uslice 3 / 4)
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
   double* dblk = nullptr;             // ordered SELL: diagonal node block per position [slice][e][lane]

@@ -386,14 +386,15 @@ def test_shared_value_groups_bit_identical(cfg, scale, bs, monkeypatch):
     assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("cfg,scale", [("C3", 1), ("C5", 3), ("C4", 4)])
+@pytest.mark.parametrize("cfg,scale", [("C3", 1), ("C5", 3), ("C4", 4), ("C2", 1)])
 def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
-    """Slices whose slots are all linear and lane-uniform (32 consecutive nodes
-    inside one mesh row) run a loop without descriptor decoding: it engages on
-    most slices of the configs' fine operators, and the merged SpMV and the
-    fused Jacobi predictor pass are bit-identical with the loop off
-    (CAMG_SELL_USLICE=0), one block row per lane (=1) and neighbouring uniform
-    slices in pairs (=2, the default)."""
+    """Masked 3x3 mirror variants.  Offset-aligned slots (slot j of a slice =
+    the block at its j-th column offset, explicit zero blocks at boundary
+    nodes; CAMG_SELL_ALIGN) make the slices across mesh-row ends linear and
+    lane-uniform but for one or two lanes; uniform slices (CAMG_SELL_USLICE)
+    run a loop without descriptor decoding, neighbouring ones in pairs (=2).
+    They engage on the configs' fine operators, and the merged SpMV, a whole
+    block-smoother sweep and the V-cycle are bit-identical across all variants."""
     import ctypes as C
     import torch
     from paper_1912_09056_b200.sparse import empty, ptr, stream_ptr
@@ -401,39 +402,47 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
     op = saddle_operator(g)
     A = op.merged()
     n = A.num_rows
+    bs = 2 if cfg == "C2" else 3
     x = torch.from_numpy(np.random.default_rng(12).standard_normal(n)).cuda()
+    variants = [("0", "0"), ("0", "2"), ("1", "0"), ("1", "1"), ("1", "2")]
     out, counts = {}, {}
-    for m in ("0", "1", "2"):
-        monkeypatch.setenv("CAMG_SELL_USLICE", m)
-        _native.call("camg_csr_attach_blocks", A.device, 3, op.n_u)
-        c = (C.c_int64 * 3)()
+    for v in variants:
+        monkeypatch.setenv("CAMG_SELL_ALIGN", v[0])
+        monkeypatch.setenv("CAMG_SELL_USLICE", v[1])
+        _native.call("camg_csr_attach_blocks", A.device, bs, op.n_u)
+        c = (C.c_int64 * 4)()
         _native.call("camg_csr_uniform_slices", A.device, c)
-        counts[m] = (c[0], c[1], c[2])
+        counts[v] = tuple(c)
         y = empty(n)
         _native.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
         torch.cuda.synchronize()
-        out[m] = y.cpu().numpy()
-    assert counts["0"][1] == 0 and counts["1"][0] == counts["0"][0]
-    # mesh rows of 65 / 67 nodes hold one or two whole 32-node slices each (C5 at full size: 84% of the slices)
-    assert cfg == "C4" or counts["1"][1] * 5 > counts["1"][0], counts
-    assert counts["1"][2] == 0 and counts["2"][1] == counts["1"][1]
-    assert cfg != "C5" or counts["2"][2] > 0, counts
-    np.testing.assert_array_equal(out["0"], out["1"])
-    np.testing.assert_array_equal(out["0"], out["2"])
+        out[v] = y.cpu().numpy()
+    base = ("0", "0")
+    assert counts[base][1:] == (0, 0, 0) and counts[("1", "0")][1] == 0
+    if bs == 3 and cfg != "C4":  # C4/4 (995 slices) is below the masked-mirror threshold: plain full blocks
+        # mesh rows of 65 / 67 nodes hold one or two whole 32-node slices each (C5 at full size: 84% of the
+        # slices); with aligned slots the slices across the row ends are uniform too
+        assert counts[("0", "2")][1] * 5 > counts[base][0], counts
+        assert counts[("1", "2")][3] * 2 > counts[base][0], counts
+        assert counts[("1", "2")][1] > counts[("0", "2")][1], counts
+        assert counts[("1", "1")][2] == 0 and (cfg != "C5" or counts[("1", "2")][2] > 0), counts
+    for v in variants[1:]:
+        np.testing.assert_array_equal(out[base], out[v])
     ref = A.to_scipy() @ x.cpu().numpy()
-    assert np.linalg.norm(out["1"] - ref) <= 1e-13 * np.linalg.norm(ref)
-    # the smoother passes ([K | B1] rows with the lambda split) through a whole sweep
+    assert np.linalg.norm(out[base] - ref) <= 1e-13 * np.linalg.norm(ref)
+    # the smoother passes ([K | B1] rows with the lambda split) through a whole sweep and a V-cycle
     skw = dict(kind="simple", alpha=0.8, outer_sweeps=3, predictor=("jacobi", 1, 0.6), corrector=("mcilu0", 1, 1.0))
     x0 = np.random.default_rng(0).standard_normal(op.total_rows)
     sw = {}
-    for m in ("0", "1", "2"):
-        monkeypatch.setenv("CAMG_SELL_USLICE", m)
+    for v in variants:
+        monkeypatch.setenv("CAMG_SELL_ALIGN", v[0])
+        monkeypatch.setenv("CAMG_SELL_USLICE", v[1])
         H = setup(saddle_operator(g), fine_level_meta(g), HierarchyConfig(max_levels=3, max_coarse_size=50),
                   block_cfg(skw))
-        sw[m] = (H.levels[0].smoother.sweep_merged(x0, g.rhs).cpu().numpy(), np.asarray(H.apply(g.rhs)))
-    for m in ("1", "2"):
-        np.testing.assert_array_equal(sw["0"][0], sw[m][0])
-        np.testing.assert_array_equal(sw["0"][1], sw[m][1])
+        sw[v] = (H.levels[0].smoother.sweep_merged(x0, g.rhs).cpu().numpy(), np.asarray(H.apply(g.rhs)))
+    for v in variants[1:]:
+        np.testing.assert_array_equal(sw[base][0], sw[v][0])
+        np.testing.assert_array_equal(sw[base][1], sw[v][1])
 
 
 @pytest.mark.parametrize("cfg,scale,sweeps,cluster", [("C5", 10, 1, "1"), ("C5", 10, 1, "0"), ("C4", 8, 2, "1"),
