@@ -524,26 +524,41 @@ __global__ void k_uniform_slices(const int64_t* __restrict__ slice_ptr, const ui
   }
 }
 
-// pairs of uniform slices: slices s (even) and s + 1 with the same shared value groups slot by slot and
-// columns 32 apart (neighbours inside one mesh row) run as one work item, each lane carrying two block
-// rows, so the lane-uniform values -- 72 of the 96 bytes a lane receives per slot, the L1 data pipe's
-// load -- are loaded once for both: us[s] = 3 (leader), us[s + 1] = 4 (follower)
-__global__ void k_uniform_pairs(const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ desc,
-                                const uint32_t* __restrict__ vo, int64_t nslices, uint8_t* __restrict__ us,
-                                unsigned long long* __restrict__ count) {
-  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; 2 * h + 1 < nslices;
-       h += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = 2 * h;
-    if (us[s] != 1 || us[s + 1] != 1) continue;
-    const int64_t b0 = slice_ptr[s], b1 = slice_ptr[s + 1], width = b1 - b0;
-    bool ok = slice_ptr[s + 2] - b1 == width;
-    for (int64_t k = 0; ok && k < width; ++k)
-      ok = vo[b0 + k] == vo[b1 + k] &&
-           ((desc[b1 + k] >> 36) & 0xFFFFFFull) == ((desc[b0 + k] >> 36) & 0xFFFFFFull) + 32ull;
-    if (ok) {
-      us[s] = 3;
-      us[s + 1] = 4;
+// groups of uniform slices: neighbouring slices with the same shared value groups slot by slot and columns
+// 32 apart (one mesh row) run as one work item, each lane carrying two or three block rows, so the
+// lane-uniform values -- 72 of the 96 bytes a lane receives per slot, the L1 data pipe's load -- are loaded
+// once for the group.  A run of compatible slices (broken every 60) is cut into threes and twos (a lone
+// slice stays 1): us = 3 / 5 leader of two / three, 4 / 6 first / second follower
+__device__ bool uslice_compat(const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ desc,
+                              const uint32_t* __restrict__ vo, int64_t s) {  // slices s and s + 1
+  const int64_t b0 = slice_ptr[s], b1 = slice_ptr[s + 1], width = b1 - b0;
+  if (slice_ptr[s + 2] - b1 != width) return false;
+  for (int64_t k = 0; k < width; ++k)
+    if (vo[b0 + k] != vo[b1 + k] ||
+        ((desc[b1 + k] >> 36) & 0xFFFFFFull) != ((desc[b0 + k] >> 36) & 0xFFFFFFull) + 32ull)
+      return false;
+  return true;
+}
+
+__global__ void k_uniform_groups(const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ desc,
+                                 const uint32_t* __restrict__ vo, int64_t nslices, const uint8_t* __restrict__ us,
+                                 uint8_t* __restrict__ out, unsigned long long* __restrict__ count) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    if (us[s] != 1) continue;
+    // run start: the slice before is not a compatible uniform slice, or a forced break
+    if (s % 60 != 0 && s > 0 && us[s - 1] == 1 && uslice_compat(slice_ptr, desc, vo, s - 1)) continue;
+    int64_t L = 1;
+    while (s + L < nslices && (s + L) % 60 != 0 && us[s + L] == 1 && uslice_compat(slice_ptr, desc, vo, s + L - 1)) ++L;
+    int64_t t = s;
+    while (L > 1) {
+      const int g = (L == 2 || L == 4) ? 2 : 3;
+      out[t] = g == 2 ? 3 : 5;
+      out[t + 1] = 4;
+      if (g == 3) out[t + 2] = 6;
       atomicAdd(count, 1ull);
+      t += g;
+      L -= g;
     }
   }
 }
@@ -742,9 +757,15 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
     if (h > 0 && uslice_mode() >= 2) {
       CAMG_CUDA(cudaMemsetAsync(nu_.p, 0, sizeof(unsigned long long), s));
       note_launch();
-      k_uniform_pairs<<<grid_for(nslices / 2 + 1, 256), 256, 0, s>>>(S->slice_ptr, S->desc, S->vo, nslices, S->uslice,
-                                                                     nu_.p);
+      // groups are written to a copy: every thread reads the ungrouped flags
+      uint8_t* grouped = dalloc<uint8_t>(nslices + 1);
+      CAMG_CUDA(cudaMemcpyAsync(grouped, S->uslice, nslices, cudaMemcpyDeviceToDevice, s));
+      k_uniform_groups<<<grid_for(nslices, 256), 256, 0, s>>>(S->slice_ptr, S->desc, S->vo, nslices, S->uslice, grouped,
+                                                              nu_.p);
       CAMG_LAUNCH_CHECK();
+      CAMG_CUDA(cudaStreamSynchronize(s));
+      dfree(S->uslice);
+      S->uslice = grouped;
       CAMG_CUDA(cudaMemcpyAsync(&h, nu_.p, sizeof(h), cudaMemcpyDeviceToHost, s));
       CAMG_CUDA(cudaStreamSynchronize(s));
       S->n_upairs = (int64_t)h;
@@ -871,6 +892,44 @@ __device__ __forceinline__ void sell_epilogue_prefetch(const SellEpi& e, int64_t
 #endif
 }
 
+// NB neighbouring uniform 3x3 slices (same shared value groups, columns 32 apart) as one work item: each lane
+// carries NB block rows (p, p + 32, ...), the slot's lane-uniform values are loaded once for all of them
+template <int NB, bool ZERO, int MODE>
+__device__ __forceinline__ void uniform_group(const SellView& S, const double* __restrict__ xu, const SellEpi& e,
+                                              int64_t p, int32_t c0, uint32_t o0, int width, int lane) {
+  double acc[NB][3];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+    sell_epilogue_prefetch<3, MODE>(e, p + 32 * j);
+  }
+#pragma unroll 1
+  for (int k = 0; k < width; ++k) {
+    const int32_t c = __shfl_sync(0xffffffffu, c0, k);
+    const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
+    const double* xs = xu + (int64_t)(c + lane) * 3;
+    const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
+    double x[NB][3];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      x[j][0] = __ldg(xs + 96 * j); x[j][1] = __ldg(xs + 96 * j + 1); x[j][2] = __ldg(xs + 96 * j + 2);
+    }
+    const double2 a = __ldg(v2), b = __ldg(v2 + 1), cc = __ldg(v2 + 2), d = __ldg(v2 + 3);
+    const double v8 = __ldg(reinterpret_cast<const double*>(v2) + 8);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      acc[j][0] = fma(a.x, x[j][0], acc[j][0]); acc[j][0] = fma(a.y, x[j][1], acc[j][0]);
+      acc[j][0] = fma(b.x, x[j][2], acc[j][0]);
+      acc[j][1] = fma(b.y, x[j][0], acc[j][1]); acc[j][1] = fma(cc.x, x[j][1], acc[j][1]);
+      acc[j][1] = fma(cc.y, x[j][2], acc[j][1]);
+      acc[j][2] = fma(d.x, x[j][0], acc[j][2]); acc[j][2] = fma(d.y, x[j][1], acc[j][2]);
+      acc[j][2] = fma(v8, x[j][2], acc[j][2]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) sell_epilogue<3, ZERO, MODE>(e, p + 32 * j, acc[j]);
+}
+
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED, bool DEDUP = false>
 __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MINB : CAMG_MASKED_MINB) : (BR * BC >= 18 ? CAMG_BIG_MINB : 6)) * 256 / kSellThreads) k_sell_row(SellView S, const double* __restrict__ xu,
                                                   const double* __restrict__ xl, int64_t split_blocks,
@@ -934,37 +993,20 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
             // uniform slice: all slots linear and lane-uniform, columns in xu: no decoding, no branches
             const int us = S.uslice ? S.uslice[s] : 0;
             if (us >= 3) {
-              // pair of uniform slices (s, s + 1), both in this launch's list: the leader's warp carries both
-              const bool leader = us == 3;
-              const bool both = !S.slist || (leader ? (w + 1 < S.nwork && S.slist[w + 1] == (int32_t)(s + 1))
-                                                    : (w > 0 && S.slist[w - 1] == (int32_t)(s - 1)));
-              if (both && !leader) continue;
-              if (both) {
-                double acb[BR];
-#pragma unroll
-                for (int r = 0; r < BR; ++r) acb[r] = 0.0;
+              // group of two or three uniform slices (leader us = 3 / 5; followers 4 / 6 at distance 1 / 2),
+              // all in this launch's list: the leader's warp carries the group, NB block rows per lane
+              const int dist = us == 4 ? 1 : (us == 6 ? 2 : 0);
+              const int gsz = S.uslice[s - dist] == 5 ? 3 : 2;
+              bool whole = true;
+              if (S.slist) {
+                whole = w - dist >= 0 && w - dist + gsz <= S.nwork;
+                for (int j = 0; whole && j < gsz; ++j) whole = S.slist[w - dist + j] == (int32_t)(s - dist + j);
+              }
+              if (whole && dist) continue;
+              if (whole) {
                 const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;
-                sell_epilogue_prefetch<BR, MODE>(e, p);
-                sell_epilogue_prefetch<BR, MODE>(e, p + 32);
-#pragma unroll 1
-                for (int k = 0; k < width; ++k) {
-                  const int32_t c = __shfl_sync(0xffffffffu, c0, k);
-                  const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
-                  const double* xs = xu + (int64_t)(c + lane) * 3;
-                  const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
-                  const double x0 = __ldg(xs), x1 = __ldg(xs + 1), x2 = __ldg(xs + 2);
-                  const double z0 = __ldg(xs + 96), z1 = __ldg(xs + 97), z2 = __ldg(xs + 98);
-                  const double2 a = __ldg(v2), b = __ldg(v2 + 1), cc = __ldg(v2 + 2), d = __ldg(v2 + 3);
-                  const double v8 = __ldg(reinterpret_cast<const double*>(v2) + 8);
-                  acc[0] = fma(a.x, x0, acc[0]); acc[0] = fma(a.y, x1, acc[0]); acc[0] = fma(b.x, x2, acc[0]);
-                  acc[1] = fma(b.y, x0, acc[1]); acc[1] = fma(cc.x, x1, acc[1]); acc[1] = fma(cc.y, x2, acc[1]);
-                  acc[2] = fma(d.x, x0, acc[2]); acc[2] = fma(d.y, x1, acc[2]); acc[2] = fma(v8, x2, acc[2]);
-                  acb[0] = fma(a.x, z0, acb[0]); acb[0] = fma(a.y, z1, acb[0]); acb[0] = fma(b.x, z2, acb[0]);
-                  acb[1] = fma(b.y, z0, acb[1]); acb[1] = fma(cc.x, z1, acb[1]); acb[1] = fma(cc.y, z2, acb[1]);
-                  acb[2] = fma(d.x, z0, acb[2]); acb[2] = fma(d.y, z1, acb[2]); acb[2] = fma(v8, z2, acb[2]);
-                }
-                sell_epilogue<BR, ZERO, MODE>(e, p, acc);
-                sell_epilogue<BR, ZERO, MODE>(e, p + 32, acb);
+                if (gsz == 2) uniform_group<2, ZERO, MODE>(S, xu, e, p, c0, o0, width, lane);
+                else uniform_group<3, ZERO, MODE>(S, xu, e, p, c0, o0, width, lane);
                 continue;
               }
             }
