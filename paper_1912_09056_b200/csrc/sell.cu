@@ -907,6 +907,9 @@ __device__ __forceinline__ void uniform_group(const SellView& S, const double* _
   for (int k = 0; k < width; ++k) {
     const int32_t c = __shfl_sync(0xffffffffu, c0, k);
     const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
+    CAMG_DCHECK(c >= 0 && (S.ncb == 0 || (int64_t)c + lane + 32 * (NB - 1) < S.ncb),
+                "uniform group: block column out of range");
+    CAMG_DCHECK(S.ngroups == 0 || (int64_t)o < S.ngroups, "uniform group: value group out of range");
     const double* xs = xu + (int64_t)(c + lane) * 3;
     const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
     double x[NB][3];
@@ -1021,6 +1024,9 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
                 const int32_t c = __shfl_sync(0xffffffffu, c0, k);
                 const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
                 const uint32_t x = __shfl_sync(0xffffffffu, ex, k);
+                CAMG_DCHECK(c >= 0 && (S.ncb == 0 || (int64_t)c + lane < S.ncb) &&
+                                (S.ngroups == 0 || (int64_t)o < S.ngroups),
+                            "uniform slice (exception lanes): column or value group out of range");
                 const double* xs = xu + (int64_t)(c + lane) * 3;
                 const int sh = lane == (int)(x & 0xFFu) ? 10 : (lane == (int)(x >> 8) ? 20 : 0);
                 const double* vu = S.bval + (int64_t)o * 32 + sh;
@@ -1042,6 +1048,9 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
               for (int k = 0; k < width; ++k) {
                 const int32_t c = __shfl_sync(0xffffffffu, c0, k);
                 const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
+                CAMG_DCHECK(c >= 0 && (S.ncb == 0 || (int64_t)c + lane < S.ncb) &&
+                                (S.ngroups == 0 || (int64_t)o < S.ngroups),
+                            "uniform slice: column or value group out of range");
                 const double* xs = xu + (int64_t)(c + lane) * 3;
                 const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
                 const double x0 = __ldg(xs), x1 = __ldg(xs + 1), x2 = __ldg(xs + 2);
