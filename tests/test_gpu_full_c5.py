@@ -22,6 +22,46 @@ from paper_1912_09056_b200.krylov import GmresConfig, gmres_device, release_work
 from paper_1912_09056_b200.problem import config_spec, generate, saddle_operator  # noqa: E402
 
 
+def test_full_c5_mirror_variants_bit_identical(monkeypatch):
+    """The fine operator's block mirror at full size: offset-aligned slots,
+    uniform-slice loops and groups (DESIGN 5b) engage on nearly every slice,
+    and the merged SpMV is bit-identical to the mirror without them and to
+    the streaming layout without shared value groups."""
+    import ctypes as C
+    import torch
+    from paper_1912_09056_b200.sparse import empty, ptr, stream_ptr
+    _native.require_device()
+    g = generate(config_spec("C5", 1), assemble_K=False)
+    op = saddle_operator(g, device_K=True)
+    A = op.merged()
+    n = A.num_rows
+    x = torch.from_numpy(np.random.default_rng(21).standard_normal(n)).cuda()
+    out, counts = {}, {}
+    for name, env in (("plain", {"CAMG_SELL_ALIGN": "0", "CAMG_SELL_USLICE": "0"}),
+                      ("streaming", {"CAMG_SELL_DEDUP": "0"}),
+                      ("default", {})):
+        for k in ("CAMG_SELL_ALIGN", "CAMG_SELL_USLICE", "CAMG_SELL_DEDUP"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        _native.call("camg_csr_attach_blocks", A.device, 3, op.n_u)
+        c = (C.c_int64 * 4)()
+        _native.call("camg_csr_uniform_slices", A.device, c)
+        counts[name] = tuple(c)
+        y = empty(n)
+        _native.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
+        torch.cuda.synchronize()
+        out[name] = y
+    slices, uniform, groups, aligned = counts["default"]
+    assert counts["plain"][1:] == (0, 0, 0) and counts["streaming"][1:3] == (0, 0)
+    assert aligned > 0.98 * slices and uniform > 0.97 * slices and groups > 0.25 * slices, counts
+    assert torch.equal(out["plain"], out["default"])
+    assert torch.equal(out["streaming"], out["default"])
+    assert torch.isfinite(out["default"]).all()
+    del out, y, x, A, op
+    torch.cuda.empty_cache()
+
+
 @pytest.fixture(scope="module")
 def c5():
     import torch
