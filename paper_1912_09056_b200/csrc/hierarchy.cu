@@ -2415,6 +2415,16 @@ struct Level {
   bool pending = false;  // a lambda-side chain runs on `side`
   DBuf<int32_t> sl_indep, sl_dep;
   int64_t n_indep = 0, n_dep = 0;
+  // the same lists as work items of the passes with x != 0 (sell_compact_list: group followers dropped)
+  DBuf<int32_t> wi_indep, wi_dep;
+  DBuf<uint8_t> wm_indep, wm_dep;
+  int64_t nw_indep = 0, nw_dep = 0;
+  void pass_lists(bool zero, bool dep, const int32_t*& list, int64_t& n, const uint8_t*& lmode) const {
+    const bool wi = !zero && (dep ? wi_dep.p : wi_indep.p) != nullptr;
+    list = wi ? (dep ? wi_dep.p : wi_indep.p) : (dep ? sl_dep.p : sl_indep.p);
+    n = wi ? (dep ? nw_dep : nw_indep) : (dep ? n_dep : n_indep);
+    lmode = wi ? (dep ? wm_dep.p : wm_indep.p) : nullptr;
+  }
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // Chebyshev predictor: d_k = c1[k] d_{k-1} + c2[k] D^-1 r_k, y_{k+1} = y_k + d_k
@@ -2469,9 +2479,14 @@ struct Level {
       return;
     }
     const SellEpi se = sell_epi(e);
-    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, sl_indep.p, n_indep);
+    const int32_t* li;
+    const uint8_t* lm;
+    int64_t ln;
+    pass_lists(zero, false, li, ln, lm);
+    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, li, ln, lm);
     join(s);
-    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, sl_dep.p, n_dep);
+    pass_lists(zero, true, li, ln, lm);
+    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, li, ln, lm);
   }
 
   void alloc_work() {
@@ -2729,9 +2744,14 @@ struct Level {
     RowEpi e{b, nullptr, r, nullptr, nullptr, nullptr, 0.0};
     if (pending && ovl() && x) {
       const SellEpi se = sell_epi(e);
-      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, sl_indep.p, n_indep);
+      const int32_t* li;
+      const uint8_t* lm;
+      int64_t ln;
+      pass_lists(false, false, li, ln, lm);
+      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, li, ln, lm);
       join(s);
-      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, sl_dep.p, n_dep);
+      pass_lists(false, true, li, ln, lm);
+      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, li, ln, lm);
       const int64_t done = A->sell->rows();
       if (n > done) dispatch_g<LaunchResid>(A->avg_row, A, done, n - done, x, (const double*)nullptr, n, e, false, s);
       return;
@@ -2840,6 +2860,22 @@ static void setup_overlap(Level* L) {
   L->sl_dep = DBuf<int32_t>(dp.size() + 1);
   if (!ind.empty()) CAMG_CUDA(cudaMemcpy(L->sl_indep.p, ind.data(), sizeof(int32_t) * ind.size(), cudaMemcpyHostToDevice));
   if (!dp.empty()) CAMG_CUDA(cudaMemcpy(L->sl_dep.p, dp.data(), sizeof(int32_t) * dp.size(), cudaMemcpyHostToDevice));
+  if (S->witems) {
+    // work items of the passes with x != 0: the followers of the uniform-slice groups leave the lists
+    auto items = [&](std::vector<int32_t>& list, DBuf<int32_t>& wi, DBuf<uint8_t>& wm, int64_t& nw) {
+      std::vector<uint8_t> mode;
+      sell_compact_list(S, list, mode);
+      nw = (int64_t)list.size();
+      wi = DBuf<int32_t>(list.size() + 1);
+      wm = DBuf<uint8_t>(list.size() + 1);
+      if (!list.empty()) {
+        CAMG_CUDA(cudaMemcpy(wi.p, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice));
+        CAMG_CUDA(cudaMemcpy(wm.p, mode.data(), list.size(), cudaMemcpyHostToDevice));
+      }
+    };
+    items(ind, L->wi_indep, L->wm_indep, L->nw_indep);
+    items(dp, L->wi_dep, L->wm_dep, L->nw_dep);
+  }
   {
     // the lambda-side stream at the greatest priority (graph nodes keep it:
     // cudaGraphInstantiateFlagUseNodePriority): its short chain kernels take

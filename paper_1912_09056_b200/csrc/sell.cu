@@ -75,6 +75,8 @@ Sell::~Sell() {
   dfree(zero);
   dfree(vo);
   dfree(uslice);
+  dfree(witems);
+  dfree(wmode);
   dfree(perm);
   dfree(dblk);
 }
@@ -642,6 +644,11 @@ static int uslice_mode() {
   return e ? atoi(e) : 2;
 }
 static bool uslices_enabled() { return uslice_mode() != 0; }
+// CAMG_SELL_WITEMS=0: the passes walk every slice and the followers' warps skip (no host-made work items)
+static bool witems_enabled() {
+  const char* e = getenv("CAMG_SELL_WITEMS");
+  return !(e && e[0] == '0');
+}
 
 template <int BR, int BC>
 Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cudaStream_t s,
@@ -769,6 +776,17 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
       CAMG_CUDA(cudaMemcpyAsync(&h, nu_.p, sizeof(h), cudaMemcpyDeviceToHost, s));
       CAMG_CUDA(cudaStreamSynchronize(s));
       S->n_upairs = (int64_t)h;
+      if (S->n_upairs > 0 && witems_enabled()) {
+        std::vector<int32_t> all(nslices);
+        for (int64_t i = 0; i < nslices; ++i) all[i] = (int32_t)i;
+        std::vector<uint8_t> wm;
+        sell_compact_list(S.get(), all, wm);
+        S->n_witems = (int64_t)all.size();
+        S->witems = dalloc<int32_t>(all.size() + 1);
+        S->wmode = dalloc<uint8_t>(all.size() + 1);
+        CAMG_CUDA(cudaMemcpy(S->witems, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
+        CAMG_CUDA(cudaMemcpy(S->wmode, wm.data(), all.size(), cudaMemcpyHostToDevice));
+      }
     }
   }
   // compulsory bytes of one pass: for every row, its blocks' stored values and
@@ -998,12 +1016,20 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
             if (us >= 3) {
               // group of two or three uniform slices (leader us = 3 / 5; followers 4 / 6 at distance 1 / 2),
               // all in this launch's list: the leader's warp carries the group, NB block rows per lane
-              const int dist = us == 4 ? 1 : (us == 6 ? 2 : 0);
-              const int gsz = S.uslice[s - dist] == 5 ? 3 : 2;
+              int dist = us == 4 ? 1 : (us == 6 ? 2 : 0);
+              int gsz;
               bool whole = true;
-              if (S.slist) {
-                whole = w - dist >= 0 && w - dist + gsz <= S.nwork;
-                for (int j = 0; whole && j < gsz; ++j) whole = S.slist[w - dist + j] == (int32_t)(s - dist + j);
+              if (S.wmode) {
+                // work items: the host dropped the followers and decided which leaders run their group
+                gsz = S.wmode[w];
+                whole = gsz >= 2;
+                dist = 0;
+              } else {
+                gsz = S.uslice[s - dist] == 5 ? 3 : 2;
+                if (S.slist) {
+                  whole = w - dist >= 0 && w - dist + gsz <= S.nwork;
+                  for (int j = 0; whole && j < gsz; ++j) whole = S.slist[w - dist + j] == (int32_t)(s - dist + j);
+                }
               }
               if (whole && dist) continue;
               if (whole) {
@@ -1257,7 +1283,7 @@ static int64_t quad_min_blocks() {
 
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                       const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
+                       const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist, const uint8_t* lmode) {
   SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->zero, S->nbr, S->nslices};
   v.ncb = S->ncb;
   v.ngroups = S->masked ? S->ngroups : 0;
@@ -1266,6 +1292,17 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   v.uslice = (split < 0 || split / BC >= S->nbr) ? S->uslice : nullptr;
   v.slist = slist;
   v.nwork = slist ? nlist : S->nslices;
+  if (v.uslice && !zero) {
+    if (!slist && S->witems) {
+      v.slist = S->witems;
+      v.nwork = S->n_witems;
+      v.wmode = S->wmode;
+    } else if (slist) {
+      v.wmode = lmode;
+    }
+  }
+  CAMG_CHECK(!(slist && lmode && !v.wmode), CAMG_ERR_NATIVE,
+             "work-item list passed to a pass that cannot run uniform-slice groups");
   if (v.nwork <= 0) return;
   const int64_t nw = v.nwork;
   // rows with many blocks (R = P^T: ~117 6x3 blocks per coarse node) split
@@ -1306,10 +1343,38 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   CAMG_LAUNCH_CHECK();
 }
 
+void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<uint8_t>& mode) {
+  mode.assign(list.size(), 0);
+  if (!S->uslice || S->n_upairs == 0) return;
+  if (S->h_uslice.empty()) {
+    Sell* M = const_cast<Sell*>(S);
+    M->h_uslice.resize(S->nslices);
+    CAMG_CUDA(cudaMemcpy(M->h_uslice.data(), S->uslice, S->nslices, cudaMemcpyDeviceToHost));
+  }
+  const std::vector<uint8_t>& us = S->h_uslice;
+  std::vector<int32_t> out;
+  std::vector<uint8_t> om;
+  out.reserve(list.size());
+  om.reserve(list.size());
+  const size_t n = list.size();
+  for (size_t w = 0; w < n;) {
+    const int32_t s = list[w];
+    const int u = us[s];
+    const int g = u == 3 ? 2 : (u == 5 ? 3 : 0);
+    bool whole = g && w + g <= n;
+    for (int j = 1; whole && j < g; ++j) whole = list[w + j] == s + j;
+    out.push_back(s);
+    om.push_back(whole ? (uint8_t)g : 0);
+    w += whole ? g : 1;  // a follower without its leader in front stays an entry of its own
+  }
+  list.swap(out);
+  mode.swap(om);
+}
+
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                 const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist) {
+                 const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist, const uint8_t* lmode) {
 #define CAMG_SELL_CASE(R_, C_) \
-  if (S->br == R_ && S->bc == C_) return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st, slist, nlist);
+  if (S->br == R_ && S->bc == C_) return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st, slist, nlist, lmode);
   CAMG_SELL_CASE(2, 2) CAMG_SELL_CASE(3, 3) CAMG_SELL_CASE(6, 6)
   CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
 #undef CAMG_SELL_CASE

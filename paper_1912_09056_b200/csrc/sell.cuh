@@ -32,6 +32,12 @@ struct Sell {
   // inside one mesh row of the structured interior) and reads columns of the square part only: the pass runs
   // them through a loop without descriptor decoding (uslice[slice] = 1)
   uint8_t* uslice = nullptr;
+  // work items of a full pass: the slices without the followers of the groups (a follower's warp would only
+  // skip), wmode[w] = block rows per lane of item w's group (2 / 3) or 0 (run the slice by itself)
+  int32_t* witems = nullptr;
+  uint8_t* wmode = nullptr;
+  int64_t n_witems = 0;
+  std::vector<uint8_t> h_uslice;      // host copy of uslice (sell_compact_list)
   int64_t n_aligned = 0;  // slices with offset-aligned slots (sell.cu)
   int64_t n_uslices = 0, n_upairs = 0;  // n_upairs: pairs of neighbouring uniform slices run as one work item (uslice 3 / 4)
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
@@ -55,6 +61,8 @@ struct SellView {
   int64_t ncb = 0, ngroups = 0;                 // bounds for the checked build (0: unknown)
   const uint32_t* __restrict__ vo = nullptr;    // shared value groups: first group of each slot
   const uint8_t* __restrict__ uslice = nullptr; // uniform slices (null: none / columns may cross the split)
+  const uint8_t* __restrict__ wmode = nullptr;  // per work item: group size decided on the host (null: the kernel
+                                                // checks the group's members in the list itself)
 };
 
 // epilogue arguments of the three SELL row kernels (modes 0/1/2)
@@ -85,7 +93,12 @@ void sell_share_override(int v);
 // (modes 1/2 need square blocks).  split < 0: x is one vector (xu); else
 // columns >= split read xl (null = 0).
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                 const SellEpi& e, cudaStream_t st, const int32_t* slist = nullptr, int64_t nlist = -1);
+                 const SellEpi& e, cudaStream_t st, const int32_t* slist = nullptr, int64_t nlist = -1,
+                 const uint8_t* lmode = nullptr);
+// Turn an ascending slice list into work items for passes with x != 0: followers of uniform-slice groups
+// whose whole group is in the list are dropped, mode[w] = 2 / 3 for an entry that leads such a group, 0 for an
+// entry that runs by itself.  Pass the result as (slist, nlist, lmode); zero-start passes keep the slice list.
+void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<uint8_t>& mode);
 double sell_pass_bytes(const Sell* S);
 int sell_lanes(const Sell* S);
 // colour-ordered SELL (square bs x bs blocks, full): position t of the

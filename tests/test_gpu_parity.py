@@ -404,11 +404,13 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
     n = A.num_rows
     bs = 2 if cfg == "C2" else 3
     x = torch.from_numpy(np.random.default_rng(12).standard_normal(n)).cuda()
-    variants = [("0", "0"), ("0", "2"), ("1", "0"), ("1", "1"), ("1", "2")]
+    # (CAMG_SELL_ALIGN, CAMG_SELL_USLICE, CAMG_SELL_WITEMS: host-made work items without the groups' followers)
+    variants = [("0", "0", "1"), ("0", "2", "1"), ("1", "0", "1"), ("1", "1", "1"), ("1", "2", "0"), ("1", "2", "1")]
     out, counts = {}, {}
     for v in variants:
         monkeypatch.setenv("CAMG_SELL_ALIGN", v[0])
         monkeypatch.setenv("CAMG_SELL_USLICE", v[1])
+        monkeypatch.setenv("CAMG_SELL_WITEMS", v[2])
         _native.call("camg_csr_attach_blocks", A.device, bs, op.n_u)
         c = (C.c_int64 * 4)()
         _native.call("camg_csr_uniform_slices", A.device, c)
@@ -417,15 +419,15 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
         _native.call("camg_spmv", A.device, 1.0, ptr(x), 0.0, ptr(y), stream_ptr())
         torch.cuda.synchronize()
         out[v] = y.cpu().numpy()
-    base = ("0", "0")
-    assert counts[base][1:] == (0, 0, 0) and counts[("1", "0")][1] == 0
+    base = ("0", "0", "1")
+    assert counts[base][1:] == (0, 0, 0) and counts[("1", "0", "1")][1] == 0
     if bs == 3 and cfg != "C4":  # C4/4 (995 slices) is below the masked-mirror threshold: plain full blocks
         # mesh rows of 65 / 67 nodes hold one or two whole 32-node slices each (C5 at full size: 84% of the
         # slices); with aligned slots the slices across the row ends are uniform too
-        assert counts[("0", "2")][1] * 5 > counts[base][0], counts
-        assert counts[("1", "2")][3] * 2 > counts[base][0], counts
-        assert counts[("1", "2")][1] > counts[("0", "2")][1], counts
-        assert counts[("1", "1")][2] == 0 and (cfg != "C5" or counts[("1", "2")][2] > 0), counts
+        assert counts[("0", "2", "1")][1] * 5 > counts[base][0], counts
+        assert counts[("1", "2", "1")][3] * 2 > counts[base][0], counts
+        assert counts[("1", "2", "1")][1] > counts[("0", "2", "1")][1], counts
+        assert counts[("1", "1", "1")][2] == 0 and (cfg != "C5" or counts[("1", "2", "1")][2] > 0), counts
     for v in variants[1:]:
         np.testing.assert_array_equal(out[base], out[v])
     ref = A.to_scipy() @ x.cpu().numpy()
@@ -437,6 +439,7 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
     for v in variants:
         monkeypatch.setenv("CAMG_SELL_ALIGN", v[0])
         monkeypatch.setenv("CAMG_SELL_USLICE", v[1])
+        monkeypatch.setenv("CAMG_SELL_WITEMS", v[2])
         H = setup(saddle_operator(g), fine_level_meta(g), HierarchyConfig(max_levels=3, max_coarse_size=50),
                   block_cfg(skw))
         sw[v] = (H.levels[0].smoother.sweep_merged(x0, g.rhs).cpu().numpy(), np.asarray(H.apply(g.rhs)))
