@@ -37,20 +37,20 @@ TRAFFIC = {
     # dram__bytes_write.sum 0.176220 GB, 2.062 ms
     "C5": 13.598776e9,
 }
-# the same pass with shared value groups, offset-aligned slots and uniform-slice groups
-# (profiles/r02d_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1,1>, dram__bytes_read.sum 709.11 MB +
-# dram__bytes_write.sum 175.21 MB, 0.562 ms, L1/TEX data pipe 88.9 % of its peak)
-TRAFFIC_SHARED = {"C5": 0.884322e9}
-L1_PIPE_SHARED = {"C5": {"l1tex_data_pipe_pct_of_peak": 88.9, "dram_pct_of_peak": 19.2, "registers": 63,
-                         "source": "profiles/r02d_dominant_kernel_ncu_full.txt"}}
+# the same pass with shared value groups, offset-aligned slots and uniform-slice groups as work items
+# (profiles/r02f_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1,1>, dram__bytes_read.sum 686.54 MB +
+# dram__bytes_write.sum 172.92 MB, 0.526 ms, L1/TEX data pipe 91.8 % of its peak)
+TRAFFIC_SHARED = {"C5": 0.859468e9}
+L1_PIPE_SHARED = {"C5": {"l1tex_data_pipe_pct_of_peak": 91.8, "dram_pct_of_peak": 20.0, "warps_active_pct": 45.8,
+                         "registers": 63, "source": "profiles/r02f_dominant_kernel_ncu_full.txt"}}
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 # DRAM bytes of one whole V-cycle summed over its ncu launch list (dram__bytes_read.sum +
 # dram__bytes_write.sum per kernel, serialised, cold cache) and the cycle time of the
 # same build: the measured (not modelled) V-cycle bandwidth
 VCYCLE_DRAM = {
-    "C5": {"dram_bytes_per_cycle": 35.82e9, "source": "profiles/r02d_vcycle_launches_C5.csv (510 kernels, one cycle)"},
-    "C3": {"dram_bytes_per_cycle": 1.95e9, "source": "profiles/r02d_vcycle_launches_C3.csv (271 kernels, one cycle)"},
-    "C2": {"dram_bytes_per_cycle": 0.37e9, "source": "profiles/r02d_vcycle_launches_C2.csv (45 kernels, one cycle)"},
+    "C5": {"dram_bytes_per_cycle": 35.68e9, "source": "profiles/r02f_vcycle_launches_C5.csv (510 kernels, one cycle)"},
+    "C3": {"dram_bytes_per_cycle": 1.95e9, "source": "profiles/r02f_vcycle_launches_C3.csv (271 kernels, one cycle)"},
+    "C2": {"dram_bytes_per_cycle": 0.37e9, "source": "profiles/r02f_vcycle_launches_C2.csv (45 kernels, one cycle)"},
 }
 # the same lists before shared value groups (streaming layout, CAMG_SELL_DEDUP=0): profiles/r02_vcycle_launches_*.csv
 VCYCLE_DRAM_STREAMING = {"C5": 111.70e9, "C3": 4.16e9, "C2": 0.35e9}
@@ -559,6 +559,9 @@ def run_gpu(args):
     # the same pass through a second mirror in the streaming layout (no shared
     # value groups: what a matrix without repeated slots runs), same run
     info0 = H.level_info(0)
+    _us = (C.c_int64 * 4)()
+    N.call("camg_csr_uniform_slices", Am.device, _us)
+    uslices = {"slices": _us[0], "uniform": _us[1], "groups": _us[2], "offset_aligned": _us[3]}
     streaming = None
     if not gs and info0.get("sell_shared_values"):
         for _ in range(3):
@@ -695,11 +698,15 @@ def run_gpu(args):
             "kept": info0["sell_value_groups"], "full": info0["sell_value_groups_full"],
             "note": "bit-identical slots of the mirror (the interior stencil of the structured mesh) keep one copy, "
                     "found by content hash + bitwise verification at setup: the value stream becomes an L1/L2-resident "
-                    "dictionary and the pass is no longer HBM-bound but bound by the L1 data pipe (ncu: 89% of its "
+                    "dictionary and the pass is no longer HBM-bound but bound by the L1 data pipe (ncu: 92% of its "
                     "peak, DRAM 19%: every lane receives the slot's 72 bytes of block values and 24 bytes of x), so "
                     "frac -- its compulsory HBM bytes over the measured peak -- is the headroom left, not wasted "
                     "traffic; results are bit-identical to the streaming layout",
-            "l1_data_pipe": L1_PIPE_SHARED.get(args.config) if args.scale == 1 else None}
+            "l1_data_pipe": L1_PIPE_SHARED.get(args.config) if args.scale == 1 else None,
+            "uniform_slices": dict(uslices, note="slices of 32 block rows whose slots are all linear and lane-uniform "
+                                   "(offset-aligned slots make the slices across mesh-row ends qualify) run a loop "
+                                   "without descriptor decoding, neighbouring ones in groups of 2-3 block rows per "
+                                   "lane so that a slot's block is loaded once for the group (DESIGN 5b)")}
         if streaming:
             st_traffic = TRAFFIC.get(args.config) if args.scale == 1 else None
             roofline["streaming_layout"] = dict(
