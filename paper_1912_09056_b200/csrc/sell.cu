@@ -881,13 +881,17 @@ __device__ __forceinline__ void sell_epilogue(const SellEpi& e, int64_t p, const
 
 // uniform-slice loops: the epilogue's own-row vectors (b, D^-1, x: compulsory DRAM reads) are prefetched to
 // L2 before the slot loop, so the slice does not end on a serial DRAM round trip
+// (C5 K pass 0.836 -> 0.814 ms; with the column prefetch of the other slices 0.765 ms)
 #ifndef CAMG_US_PREFETCH
 #define CAMG_US_PREFETCH 1
 #endif
+// unroll of the one-row uniform loop: at 2 ptxas serialises the two slots under the 64-register cap
+// (0.807 vs 0.814 ms), kept at 1
 #ifndef CAMG_US_UNROLL
 #define CAMG_US_UNROLL 1
 #endif
 constexpr int kUsUnroll = CAMG_US_UNROLL;
+// column-index prefetch of the non-uniform slices to L1 instead of L2: measured the same
 #if CAMG_PF_L1
 #define CAMG_BCOL_PF "prefetch.global.L1"
 #else
