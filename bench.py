@@ -559,9 +559,10 @@ def run_gpu(args):
     # the same pass through a second mirror in the streaming layout (no shared
     # value groups: what a matrix without repeated slots runs), same run
     info0 = H.level_info(0)
-    _us = (C.c_int64 * 4)()
+    _us = (C.c_int64 * 5)()
     N.call("camg_csr_uniform_slices", Am.device, _us)
-    uslices = {"slices": _us[0], "uniform": _us[1], "groups": _us[2], "offset_aligned": _us[3]}
+    uslices = {"slices": _us[0], "uniform": _us[1], "groups": _us[2], "offset_aligned": _us[3],
+               "exception_lane_pairs": _us[4]}
     streaming = None
     if not gs and info0.get("sell_shared_values"):
         for _ in range(3):

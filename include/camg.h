@@ -147,12 +147,14 @@ int camg_csr_value_groups(const camg_csr* A, int64_t* kept, int64_t* full);
 /* slots of the masked mirror: out[5] = {slots, lane-uniform (one dense block, shared-value mirrors),
  * linear (block columns c0 + lane, no column index stored), both, uniform but for one or two lanes} */
 int camg_csr_slot_stats(const camg_csr* A, int64_t* out);
-/* out[4] = {slices of the block mirror, uniform slices: 32 consecutive block rows whose slots are all linear
+/* out[5] = {slices of the block mirror, uniform slices: 32 consecutive block rows whose slots are all linear
  * and lane-uniform but for one or two lanes (a structured mesh row and its ends), which the pass runs without
- * descriptor decoding, pairs of neighbouring uniform slices run as one work item (two block rows per lane,
- * values loaded once), slices with offset-aligned slots (slot j = the block at the slice's j-th column
- * offset, zero blocks where a row has none)}; CAMG_SELL_USLICE=0 turns the loop off, =1 the pairing,
- * CAMG_SELL_ALIGN=0 the offset alignment */
+ * descriptor decoding, groups of neighbouring uniform slices run as one work item (two or three block rows
+ * per lane, values loaded once), slices with offset-aligned slots (slot j = the block at the slice's j-th
+ * column offset, zero blocks where a row has none), pairs of slices with the same exception lanes a mesh-row
+ * period apart run as one work item}; CAMG_SELL_USLICE=0 turns the loops off, =1 the grouping,
+ * CAMG_SELL_ALIGN=0 the offset alignment, CAMG_SELL_WITEMS=0 / CAMG_SELL_XGROUPS=0 the host-made work items /
+ * the exception-lane pairs */
 int camg_csr_uniform_slices(const camg_csr* A, int64_t* out);
 /* compulsory bytes of one SpMV pass in the matrix's current format */
 int camg_csr_stream_bytes(const camg_csr* A, double* bytes);

@@ -2418,12 +2418,15 @@ struct Level {
   // the same lists as work items of the passes with x != 0 (sell_compact_list: group followers dropped)
   DBuf<int32_t> wi_indep, wi_dep;
   DBuf<uint8_t> wm_indep, wm_dep;
+  DBuf<int32_t> wd_indep, wd_dep;
   int64_t nw_indep = 0, nw_dep = 0;
-  void pass_lists(bool zero, bool dep, const int32_t*& list, int64_t& n, const uint8_t*& lmode) const {
+  void pass_lists(bool zero, bool dep, const int32_t*& list, int64_t& n, const uint8_t*& lmode,
+                  const int32_t*& ldist) const {
     const bool wi = !zero && (dep ? wi_dep.p : wi_indep.p) != nullptr;
     list = wi ? (dep ? wi_dep.p : wi_indep.p) : (dep ? sl_dep.p : sl_indep.p);
     n = wi ? (dep ? nw_dep : nw_indep) : (dep ? n_dep : n_indep);
     lmode = wi ? (dep ? wm_dep.p : wm_indep.p) : nullptr;
+    ldist = wi ? (dep ? wd_dep.p : wd_indep.p) : nullptr;
   }
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -2479,14 +2482,14 @@ struct Level {
       return;
     }
     const SellEpi se = sell_epi(e);
-    const int32_t* li;
+    const int32_t *li, *ld;
     const uint8_t* lm;
     int64_t ln;
-    pass_lists(zero, false, li, ln, lm);
-    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, li, ln, lm);
+    pass_lists(zero, false, li, ln, lm, ld);
+    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, li, ln, lm, ld);
     join(s);
-    pass_lists(zero, true, li, ln, lm);
-    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, li, ln, lm);
+    pass_lists(zero, true, li, ln, lm, ld);
+    sell_launch(A->sell, 1, zero, xu, xl, nu, se, s, li, ln, lm, ld);
   }
 
   void alloc_work() {
@@ -2744,14 +2747,14 @@ struct Level {
     RowEpi e{b, nullptr, r, nullptr, nullptr, nullptr, 0.0};
     if (pending && ovl() && x) {
       const SellEpi se = sell_epi(e);
-      const int32_t* li;
+      const int32_t *li, *ld;
       const uint8_t* lm;
       int64_t ln;
-      pass_lists(false, false, li, ln, lm);
-      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, li, ln, lm);
+      pass_lists(false, false, li, ln, lm, ld);
+      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, li, ln, lm, ld);
       join(s);
-      pass_lists(false, true, li, ln, lm);
-      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, li, ln, lm);
+      pass_lists(false, true, li, ln, lm, ld);
+      sell_launch(A->sell, 1, false, x, nullptr, -1, se, s, li, ln, lm, ld);
       const int64_t done = A->sell->rows();
       if (n > done) dispatch_g<LaunchResid>(A->avg_row, A, done, n - done, x, (const double*)nullptr, n, e, false, s);
       return;
@@ -2862,19 +2865,23 @@ static void setup_overlap(Level* L) {
   if (!dp.empty()) CAMG_CUDA(cudaMemcpy(L->sl_dep.p, dp.data(), sizeof(int32_t) * dp.size(), cudaMemcpyHostToDevice));
   if (S->witems) {
     // work items of the passes with x != 0: the followers of the uniform-slice groups leave the lists
-    auto items = [&](std::vector<int32_t>& list, DBuf<int32_t>& wi, DBuf<uint8_t>& wm, int64_t& nw) {
+    auto items = [&](std::vector<int32_t>& list, DBuf<int32_t>& wi, DBuf<uint8_t>& wm, DBuf<int32_t>& wd,
+                     int64_t& nw) {
       std::vector<uint8_t> mode;
-      sell_compact_list(S, list, mode);
+      std::vector<int32_t> dist;
+      sell_compact_list(S, list, mode, dist);
       nw = (int64_t)list.size();
       wi = DBuf<int32_t>(list.size() + 1);
       wm = DBuf<uint8_t>(list.size() + 1);
+      wd = DBuf<int32_t>(list.size() + 1);
       if (!list.empty()) {
         CAMG_CUDA(cudaMemcpy(wi.p, list.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice));
         CAMG_CUDA(cudaMemcpy(wm.p, mode.data(), list.size(), cudaMemcpyHostToDevice));
+        CAMG_CUDA(cudaMemcpy(wd.p, dist.data(), sizeof(int32_t) * list.size(), cudaMemcpyHostToDevice));
       }
     };
-    items(ind, L->wi_indep, L->wm_indep, L->nw_indep);
-    items(dp, L->wi_dep, L->wm_dep, L->nw_dep);
+    items(ind, L->wi_indep, L->wm_indep, L->wd_indep, L->nw_indep);
+    items(dp, L->wi_dep, L->wm_dep, L->wd_dep, L->nw_dep);
   }
   {
     // the lambda-side stream at the greatest priority (graph nodes keep it:

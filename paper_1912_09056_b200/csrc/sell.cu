@@ -77,6 +77,8 @@ Sell::~Sell() {
   dfree(uslice);
   dfree(witems);
   dfree(wmode);
+  dfree(wdist);
+  dfree(xpart);
   dfree(perm);
   dfree(dblk);
 }
@@ -565,6 +567,37 @@ __global__ void k_uniform_groups(const int64_t* __restrict__ slice_ptr, const un
   }
 }
 
+// period of a slice with exception lanes: the distance d (in slices) to a slice with the same width, value
+// groups and exception lanes, slot by slot, and first columns 32 d further on.  Candidates are the
+// differences of the slice's own slot columns (on a structured mesh the mesh-row length is one of them: 32
+// mesh rows of nx nodes are nx slices); 0 = none
+__global__ void k_exc_partner(const int64_t* __restrict__ slice_ptr, const unsigned long long* __restrict__ desc,
+                              const uint32_t* __restrict__ vo, const uint8_t* __restrict__ us, int64_t nslices,
+                              int32_t* __restrict__ xpart) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nslices;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    int32_t found = 0;
+    if (us[s] == 2) {
+      const int64_t b0 = slice_ptr[s], width = slice_ptr[s + 1] - b0;
+      const int64_t c0 = (int64_t)((desc[b0] >> 36) & 0xFFFFFFull);
+      for (int64_t q = 1; q < width && !found; ++q) {
+        const int64_t d = (int64_t)((desc[b0 + q] >> 36) & 0xFFFFFFull) - c0;
+        if (d < 2 || s + d >= nslices || us[s + d] != 2) continue;
+        const int64_t b1 = slice_ptr[s + d];
+        bool ok = slice_ptr[s + d + 1] - b1 == width;
+        for (int64_t k = 0; ok && k < width; ++k) {
+          const unsigned long long da = desc[b0 + k], db = desc[b1 + k];
+          ok = vo[b0 + k] == vo[b1 + k] && (da >> 60) == (db >> 60) &&
+               ((db >> 36) & 0xFFFFFFull) == ((da >> 36) & 0xFFFFFFull) + 32ull * (unsigned long long)d &&
+               (((da >> 60) & 3ull) != 2ull || (da & 0xFFFFull) == (db & 0xFFFFull));
+        }
+        if (ok) found = (int32_t)d;
+      }
+    }
+    xpart[s] = found;
+  }
+}
+
 // Replace S's value array by the shared one when that at least halves it;
 // returns the value groups kept (S->ngroups) -- S->dedup says whether it applied.
 static void share_value_groups(Sell* S, cudaStream_t s) {
@@ -644,6 +677,11 @@ static int uslice_mode() {
   return e ? atoi(e) : 2;
 }
 static bool uslices_enabled() { return uslice_mode() != 0; }
+// CAMG_SELL_XGROUPS=0: slices with exception lanes always run by themselves
+static bool xgroups_enabled() {
+  const char* e = getenv("CAMG_SELL_XGROUPS");
+  return !(e && e[0] == '0');
+}
 // CAMG_SELL_WITEMS=0: the passes walk every slice and the followers' warps skip (no host-made work items)
 static bool witems_enabled() {
   const char* e = getenv("CAMG_SELL_WITEMS");
@@ -777,15 +815,28 @@ Sell* build(const Csr* A, int64_t nrows, int64_t ncols_blocked, bool masked, cud
       CAMG_CUDA(cudaStreamSynchronize(s));
       S->n_upairs = (int64_t)h;
       if (S->n_upairs > 0 && witems_enabled()) {
-        std::vector<int32_t> all(nslices);
+        if (xgroups_enabled()) {
+          S->xpart = dalloc<int32_t>(nslices + 1);
+          note_launch();
+          k_exc_partner<<<grid_for(nslices, 256), 256, 0, s>>>(S->slice_ptr, S->desc, S->vo, S->uslice, nslices,
+                                                               S->xpart);
+          CAMG_LAUNCH_CHECK();
+          S->h_xpart.resize(nslices);
+          CAMG_CUDA(cudaMemcpyAsync(S->h_xpart.data(), S->xpart, sizeof(int32_t) * nslices, cudaMemcpyDeviceToHost, s));
+          CAMG_CUDA(cudaStreamSynchronize(s));
+        }
+        std::vector<int32_t> all(nslices), wd;
         for (int64_t i = 0; i < nslices; ++i) all[i] = (int32_t)i;
         std::vector<uint8_t> wm;
-        sell_compact_list(S.get(), all, wm);
+        sell_compact_list(S.get(), all, wm, wd);
+        for (uint8_t m : wm) S->n_xgroups += (m & 4) != 0;
         S->n_witems = (int64_t)all.size();
         S->witems = dalloc<int32_t>(all.size() + 1);
         S->wmode = dalloc<uint8_t>(all.size() + 1);
+        S->wdist = dalloc<int32_t>(all.size() + 1);
         CAMG_CUDA(cudaMemcpy(S->witems, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
         CAMG_CUDA(cudaMemcpy(S->wmode, wm.data(), all.size(), cudaMemcpyHostToDevice));
+        CAMG_CUDA(cudaMemcpy(S->wdist, wd.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice));
       }
     }
   }
@@ -916,31 +967,41 @@ __device__ __forceinline__ void sell_epilogue_prefetch(const SellEpi& e, int64_t
 
 // NB neighbouring uniform 3x3 slices (same shared value groups, columns 32 apart) as one work item: each lane
 // carries NB block rows (p, p + 32, ...), the slot's lane-uniform values are loaded once for all of them
-template <int NB, bool ZERO, int MODE>
+template <int NB, bool EXC, bool ZERO, int MODE>
 __device__ __forceinline__ void uniform_group(const SellView& S, const double* __restrict__ xu, const SellEpi& e,
-                                              int64_t p, int32_t c0, uint32_t o0, int width, int lane) {
+                                              int64_t p, int32_t c0, uint32_t o0, uint32_t ex, int dn, int width,
+                                              int lane) {
+  // dn: block rows between the members (32 for neighbouring slices).  EXC: the members are slices with the
+  // same exception lanes (a mesh-row period apart); such a lane reads its own dense block (entries 10.. /
+  // 20.. of the group) for all its rows
   double acc[NB][3];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
-    sell_epilogue_prefetch<3, MODE>(e, p + 32 * j);
+    sell_epilogue_prefetch<3, MODE>(e, p + (int64_t)dn * j);
   }
 #pragma unroll 1
   for (int k = 0; k < width; ++k) {
     const int32_t c = __shfl_sync(0xffffffffu, c0, k);
     const uint32_t o = __shfl_sync(0xffffffffu, o0, k);
-    CAMG_DCHECK(c >= 0 && (S.ncb == 0 || (int64_t)c + lane + 32 * (NB - 1) < S.ncb),
+    CAMG_DCHECK(c >= 0 && (S.ncb == 0 || (int64_t)c + lane + (int64_t)dn * (NB - 1) < S.ncb),
                 "uniform group: block column out of range");
     CAMG_DCHECK(S.ngroups == 0 || (int64_t)o < S.ngroups, "uniform group: value group out of range");
     const double* xs = xu + (int64_t)(c + lane) * 3;
-    const double2* v2 = reinterpret_cast<const double2*>(S.bval + (int64_t)o * 32);
+    const double* vu = S.bval + (int64_t)o * 32;
+    if constexpr (EXC) {
+      const uint32_t xk = __shfl_sync(0xffffffffu, ex, k);
+      vu += lane == (int)(xk & 0xFFu) ? 10 : (lane == (int)(xk >> 8) ? 20 : 0);
+    }
+    const double2* v2 = reinterpret_cast<const double2*>(vu);
     double x[NB][3];
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      x[j][0] = __ldg(xs + 96 * j); x[j][1] = __ldg(xs + 96 * j + 1); x[j][2] = __ldg(xs + 96 * j + 2);
+      const double* xj = xs + (int64_t)(3 * dn) * j;
+      x[j][0] = __ldg(xj); x[j][1] = __ldg(xj + 1); x[j][2] = __ldg(xj + 2);
     }
     const double2 a = __ldg(v2), b = __ldg(v2 + 1), cc = __ldg(v2 + 2), d = __ldg(v2 + 3);
-    const double v8 = __ldg(reinterpret_cast<const double*>(v2) + 8);
+    const double v8 = __ldg(vu + 8);
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       acc[j][0] = fma(a.x, x[j][0], acc[j][0]); acc[j][0] = fma(a.y, x[j][1], acc[j][0]);
@@ -952,7 +1013,7 @@ __device__ __forceinline__ void uniform_group(const SellView& S, const double* _
     }
   }
 #pragma unroll
-  for (int j = 0; j < NB; ++j) sell_epilogue<3, ZERO, MODE>(e, p + 32 * j, acc[j]);
+  for (int j = 0; j < NB; ++j) sell_epilogue<3, ZERO, MODE>(e, p + (int64_t)dn * j, acc[j]);
 }
 
 template <int BR, int BC, bool ZERO, bool SPLIT, int MODE, bool MASKED, bool DEDUP = false>
@@ -1038,8 +1099,8 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
               if (whole && dist) continue;
               if (whole) {
                 const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;
-                if (gsz == 2) uniform_group<2, ZERO, MODE>(S, xu, e, p, c0, o0, width, lane);
-                else uniform_group<3, ZERO, MODE>(S, xu, e, p, c0, o0, width, lane);
+                if (gsz == 2) uniform_group<2, false, ZERO, MODE>(S, xu, e, p, c0, o0, 0u, 32, width, lane);
+                else uniform_group<3, false, ZERO, MODE>(S, xu, e, p, c0, o0, 0u, 32, width, lane);
                 continue;
               }
             }
@@ -1048,6 +1109,12 @@ __global__ void __launch_bounds__(kSellThreads, (MASKED ? (DEDUP ? CAMG_DEDUP_MI
               // boundary nodes): those lanes read their own dense block at entries 10.. / 20.. of the group
               const int32_t c0 = (int32_t)((uint32_t)(m0 >> 36) & 0xFFFFFFu) - 1;
               const uint32_t ex = ((unsigned)(m0 >> 60) & 3u) == 2u ? (uint32_t)(m0 & 0xFFFFull) : 0xFFFFu;
+              if (S.wmode && (S.wmode[w] & 3) >= 2) {
+                // work item: a group of such slices a period apart (same lanes, same groups)
+                const int dn = 32 * S.wdist[w];
+                uniform_group<2, true, ZERO, MODE>(S, xu, e, p, c0, o0, ex, dn, width, lane);  // pairs only: registers
+                continue;
+              }
               sell_epilogue_prefetch<BR, MODE>(e, p);
 #pragma unroll 1
               for (int k = 0; k < width; ++k) {
@@ -1287,7 +1354,8 @@ static int64_t quad_min_blocks() {
 
 template <int BR, int BC>
 static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                       const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist, const uint8_t* lmode) {
+                       const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist, const uint8_t* lmode,
+                       const int32_t* ldist) {
   SellView v{S->slice_ptr, S->len, S->bcol, S->bval, S->mask, S->voff, S->desc, S->zero, S->nbr, S->nslices};
   v.ncb = S->ncb;
   v.ngroups = S->masked ? S->ngroups : 0;
@@ -1301,11 +1369,13 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
       v.slist = S->witems;
       v.nwork = S->n_witems;
       v.wmode = S->wmode;
+      v.wdist = S->wdist;
     } else if (slist) {
       v.wmode = lmode;
+      v.wdist = ldist;
     }
   }
-  CAMG_CHECK(!(slist && lmode && !v.wmode), CAMG_ERR_NATIVE,
+  CAMG_CHECK(!(slist && lmode && !v.wmode) && !(v.wmode && !v.wdist), CAMG_ERR_NATIVE,
              "work-item list passed to a pass that cannot run uniform-slice groups");
   if (v.nwork <= 0) return;
   const int64_t nw = v.nwork;
@@ -1347,8 +1417,10 @@ static void launch_blk(const Sell* S, int mode, bool zero, const double* xu, con
   CAMG_LAUNCH_CHECK();
 }
 
-void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<uint8_t>& mode) {
+void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<uint8_t>& mode,
+                       std::vector<int32_t>& dist) {
   mode.assign(list.size(), 0);
+  dist.assign(list.size(), 1);
   if (!S->uslice || S->n_upairs == 0) return;
   if (S->h_uslice.empty()) {
     Sell* M = const_cast<Sell*>(S);
@@ -1356,29 +1428,69 @@ void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<ui
     CAMG_CUDA(cudaMemcpy(M->h_uslice.data(), S->uslice, S->nslices, cudaMemcpyDeviceToHost));
   }
   const std::vector<uint8_t>& us = S->h_uslice;
-  std::vector<int32_t> out;
+  const std::vector<int32_t>& xp = S->h_xpart;
+  // slices with exception lanes: chains s, s + d, s + 2d, ... (d = xp[s]) cut into threes and twos, a group
+  // formed only of members that are all in the list; taken[s] = 1: s runs inside an earlier entry's group
+  std::vector<uint8_t> in_list, taken;
+  if (!xp.empty()) {
+    in_list.assign(S->nslices, 0);
+    taken.assign(S->nslices, 0);
+    for (int32_t s : list) in_list[s] = 1;
+  }
+  std::vector<int32_t> out, od;
   std::vector<uint8_t> om;
   out.reserve(list.size());
   om.reserve(list.size());
+  od.reserve(list.size());
   const size_t n = list.size();
   for (size_t w = 0; w < n;) {
     const int32_t s = list[w];
     const int u = us[s];
+    if (u == 2 && !xp.empty()) {
+      if (taken[s]) { ++w; continue; }
+      const int64_t d = xp[s];
+      int g = 1;
+      if (d > 0) {
+        // members available after s: in the list, not yet taken, and linked by the same period
+        int64_t t = s;
+        // (pairs: three rows per lane with the per-lane value pointer do not fit the pass's 64 registers)
+        while (g < 2 && xp[t] == d && t + d < S->nslices && in_list[t + d] && !taken[t + d] && us[t + d] == 2) {
+          t += d;
+          ++g;
+        }
+      }
+      if (g >= 2) {
+        for (int j = 1; j < g; ++j) taken[s + j * d] = 1;
+        out.push_back(s);
+        om.push_back((uint8_t)(g | 4));
+        od.push_back((int32_t)d);
+      } else {
+        out.push_back(s);
+        om.push_back(0);
+        od.push_back(1);
+      }
+      ++w;
+      continue;
+    }
     const int g = u == 3 ? 2 : (u == 5 ? 3 : 0);
     bool whole = g && w + g <= n;
     for (int j = 1; whole && j < g; ++j) whole = list[w + j] == s + j;
     out.push_back(s);
     om.push_back(whole ? (uint8_t)g : 0);
+    od.push_back(1);
     w += whole ? g : 1;  // a follower without its leader in front stays an entry of its own
   }
   list.swap(out);
   mode.swap(om);
+  dist.swap(od);
 }
 
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
-                 const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist, const uint8_t* lmode) {
+                 const SellEpi& e, cudaStream_t st, const int32_t* slist, int64_t nlist, const uint8_t* lmode,
+                 const int32_t* ldist) {
 #define CAMG_SELL_CASE(R_, C_) \
-  if (S->br == R_ && S->bc == C_) return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st, slist, nlist, lmode);
+  if (S->br == R_ && S->bc == C_) \
+    return launch_blk<R_, C_>(S, mode, zero, xu, xl, split, e, st, slist, nlist, lmode, ldist);
   CAMG_SELL_CASE(2, 2) CAMG_SELL_CASE(3, 3) CAMG_SELL_CASE(6, 6)
   CAMG_SELL_CASE(3, 6) CAMG_SELL_CASE(6, 3) CAMG_SELL_CASE(2, 3) CAMG_SELL_CASE(3, 2)
 #undef CAMG_SELL_CASE
@@ -1571,6 +1683,7 @@ extern "C" int camg_csr_uniform_slices(const camg_csr* A, int64_t* out) {
     out[1] = S ? S->n_uslices : 0;
     out[2] = S ? S->n_upairs : 0;
     out[3] = S ? S->n_aligned : 0;
+    out[4] = S ? S->n_xgroups : 0;
   });
 }
 

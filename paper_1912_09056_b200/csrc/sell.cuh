@@ -36,8 +36,16 @@ struct Sell {
   // skip), wmode[w] = block rows per lane of item w's group (2 / 3) or 0 (run the slice by itself)
   int32_t* witems = nullptr;
   uint8_t* wmode = nullptr;
+  int32_t* wdist = nullptr;           // slices between the members of item w's group (1: neighbours)
   int64_t n_witems = 0;
   std::vector<uint8_t> h_uslice;      // host copy of uslice (sell_compact_list)
+  // slices with exception lanes (uslice 2) repeat with a period: the slice `xpart[s]` slices further on has
+  // the same value groups, the same exception lanes and columns 32 * xpart[s] apart (0: none) -- on a
+  // structured mesh the slice across the end of mesh row j and the one across row j + 32.  Such slices run
+  // in groups too (work items only)
+  int32_t* xpart = nullptr;
+  std::vector<int32_t> h_xpart;
+  int64_t n_xgroups = 0;
   int64_t n_aligned = 0;  // slices with offset-aligned slots (sell.cu)
   int64_t n_uslices = 0, n_upairs = 0;  // n_upairs: pairs of neighbouring uniform slices run as one work item (uslice 3 / 4)
   int32_t* perm = nullptr;            // ordered SELL: block row at each position (-1 = padding)
@@ -62,7 +70,9 @@ struct SellView {
   const uint32_t* __restrict__ vo = nullptr;    // shared value groups: first group of each slot
   const uint8_t* __restrict__ uslice = nullptr; // uniform slices (null: none / columns may cross the split)
   const uint8_t* __restrict__ wmode = nullptr;  // per work item: group size decided on the host (null: the kernel
-                                                // checks the group's members in the list itself)
+                                                // checks the group's members in the list itself); bit 2: a
+                                                // group of slices with exception lanes
+  const int32_t* __restrict__ wdist = nullptr;  // per work item: slices between the group's members
 };
 
 // epilogue arguments of the three SELL row kernels (modes 0/1/2)
@@ -94,11 +104,14 @@ void sell_share_override(int v);
 // columns >= split read xl (null = 0).
 void sell_launch(const Sell* S, int mode, bool zero, const double* xu, const double* xl, int64_t split,
                  const SellEpi& e, cudaStream_t st, const int32_t* slist = nullptr, int64_t nlist = -1,
-                 const uint8_t* lmode = nullptr);
+                 const uint8_t* lmode = nullptr, const int32_t* ldist = nullptr);
 // Turn an ascending slice list into work items for passes with x != 0: followers of uniform-slice groups
 // whose whole group is in the list are dropped, mode[w] = 2 / 3 for an entry that leads such a group, 0 for an
 // entry that runs by itself.  Pass the result as (slist, nlist, lmode); zero-start passes keep the slice list.
-void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<uint8_t>& mode);
+// dist[w] = slices between the members of entry w's group (1 for neighbours; mode bit 2 marks a group of slices
+// with exception lanes, whose members lie a mesh-row period apart).  Pass (slist, nlist, lmode, ldist).
+void sell_compact_list(const Sell* S, std::vector<int32_t>& list, std::vector<uint8_t>& mode,
+                       std::vector<int32_t>& dist);
 double sell_pass_bytes(const Sell* S);
 int sell_lanes(const Sell* S);
 // colour-ordered SELL (square bs x bs blocks, full): position t of the

@@ -412,7 +412,7 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
         monkeypatch.setenv("CAMG_SELL_USLICE", v[1])
         monkeypatch.setenv("CAMG_SELL_WITEMS", v[2])
         _native.call("camg_csr_attach_blocks", A.device, bs, op.n_u)
-        c = (C.c_int64 * 4)()
+        c = (C.c_int64 * 5)()
         _native.call("camg_csr_uniform_slices", A.device, c)
         counts[v] = tuple(c)
         y = empty(n)
@@ -420,7 +420,7 @@ def test_uniform_slice_loop_bit_identical(cfg, scale, monkeypatch):
         torch.cuda.synchronize()
         out[v] = y.cpu().numpy()
     base = ("0", "0", "1")
-    assert counts[base][1:] == (0, 0, 0) and counts[("1", "0", "1")][1] == 0
+    assert counts[base][1:] == (0, 0, 0, 0) and counts[("1", "0", "1")][1] == 0
     if bs == 3 and cfg != "C4":  # C4/4 (995 slices) is below the masked-mirror threshold: plain full blocks
         # mesh rows of 65 / 67 nodes hold one or two whole 32-node slices each (C5 at full size: 84% of the
         # slices); with aligned slots the slices across the row ends are uniform too
