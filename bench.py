@@ -37,20 +37,20 @@ TRAFFIC = {
     # dram__bytes_write.sum 0.176220 GB, 2.062 ms
     "C5": 13.598776e9,
 }
-# the same pass with shared value groups, offset-aligned slots and uniform-slice groups as work items
-# (profiles/r02f_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1,1>, dram__bytes_read.sum 686.54 MB +
-# dram__bytes_write.sum 172.92 MB, 0.526 ms, L1/TEX data pipe 91.8 % of its peak)
-TRAFFIC_SHARED = {"C5": 0.859468e9}
-L1_PIPE_SHARED = {"C5": {"l1tex_data_pipe_pct_of_peak": 91.8, "dram_pct_of_peak": 20.0, "warps_active_pct": 45.8,
-                         "registers": 63, "source": "profiles/r02f_dominant_kernel_ncu_full.txt"}}
+# the same pass with shared value groups, offset-aligned slots, uniform-slice groups and exception-lane pairs
+# as work items (profiles/r02g_dominant_kernel_c5.ncu-rep: k_sell_row<3,3,0,1,1,1,1>, dram__bytes_read.sum
+# 681.46 MB + dram__bytes_write.sum 175.12 MB, 0.485 ms, L1/TEX data pipe 91.3 % of its peak)
+TRAFFIC_SHARED = {"C5": 0.856580e9}
+L1_PIPE_SHARED = {"C5": {"l1tex_data_pipe_pct_of_peak": 91.3, "dram_pct_of_peak": 21.6, "warps_active_pct": 46.8,
+                         "registers": 64, "source": "profiles/r02g_dominant_kernel_ncu_full.txt"}}
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
 # DRAM bytes of one whole V-cycle summed over its ncu launch list (dram__bytes_read.sum +
 # dram__bytes_write.sum per kernel, serialised, cold cache) and the cycle time of the
 # same build: the measured (not modelled) V-cycle bandwidth
 VCYCLE_DRAM = {
-    "C5": {"dram_bytes_per_cycle": 35.68e9, "source": "profiles/r02f_vcycle_launches_C5.csv (510 kernels, one cycle)"},
-    "C3": {"dram_bytes_per_cycle": 1.95e9, "source": "profiles/r02f_vcycle_launches_C3.csv (271 kernels, one cycle)"},
-    "C2": {"dram_bytes_per_cycle": 0.37e9, "source": "profiles/r02f_vcycle_launches_C2.csv (45 kernels, one cycle)"},
+    "C5": {"dram_bytes_per_cycle": 35.64e9, "source": "profiles/r02g_vcycle_launches_C5.csv (510 kernels, one cycle)"},
+    "C3": {"dram_bytes_per_cycle": 1.95e9, "source": "profiles/r02g_vcycle_launches_C3.csv (271 kernels, one cycle)"},
+    "C2": {"dram_bytes_per_cycle": 0.37e9, "source": "profiles/r02g_vcycle_launches_C2.csv (45 kernels, one cycle)"},
 }
 # the same lists before shared value groups (streaming layout, CAMG_SELL_DEDUP=0): profiles/r02_vcycle_launches_*.csv
 VCYCLE_DRAM_STREAMING = {"C5": 111.70e9, "C3": 4.16e9, "C2": 0.35e9}
@@ -699,7 +699,7 @@ def run_gpu(args):
             "kept": info0["sell_value_groups"], "full": info0["sell_value_groups_full"],
             "note": "bit-identical slots of the mirror (the interior stencil of the structured mesh) keep one copy, "
                     "found by content hash + bitwise verification at setup: the value stream becomes an L1/L2-resident "
-                    "dictionary and the pass is no longer HBM-bound but bound by the L1 data pipe (ncu: 92% of its "
+                    "dictionary and the pass is no longer HBM-bound but bound by the L1 data pipe (ncu: 91% of its "
                     "peak, DRAM 19%: every lane receives the slot's 72 bytes of block values and 24 bytes of x), so "
                     "frac -- its compulsory HBM bytes over the measured peak -- is the headroom left, not wasted "
                     "traffic; results are bit-identical to the streaming layout",
